@@ -1,0 +1,138 @@
+/*
+ * sbnet.h — C ABI of the B200-native (sm_100a) SBNet sparse-block hot path.
+ *
+ * The reference (`blockconv`, /root/reference/pkg/src/blockconv) is a pure-Python
+ * package; its "plugin surface" is the Python function API exported from
+ * `__init__.py:9-26`.  This header is the native boundary that sits UNDER the Python
+ * mirror of that API (paper_1801_02108_b200/*.py).  Each entry point below names the
+ * reference function it replaces.  Conventions:
+ *
+ *  - plain device pointers and sizes; no torch types.  All tensors are contiguous,
+ *    activations NHWC (logical (n, h, w, c), reference `tensor.py:43-49`), masks uint8
+ *    (n, h, w), block index lists int32 (cap, 3) rows (frame, block_y, block_x) in
+ *    ascending order plus a device-resident int32 count.
+ *  - the caller owns every buffer, including workspaces; the library never allocates
+ *    device memory.  `dst` / `out` arguments are mutated in place (the Python layer
+ *    clones first to keep the reference's functional semantics, `blocks.py:134`).
+ *  - every call is asynchronous and stream-ordered on `stream` (a cudaStream_t).  The
+ *    only data-dependent quantity, the active block count, stays on the device: kernels
+ *    read `*count` and run a persistent grid sized for `cap` rows, so no host sync is
+ *    needed between reduce_mask and the consumers.
+ *  - return 0 on success, a negative SBN_ERR_* code otherwise; sbn_last_error() returns
+ *    a message (thread-local).  The Python layer maps codes onto the reference's
+ *    exception classes (`errors.py:4-35`).
+ */
+#ifndef SBNET_H_
+#define SBNET_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* sbn_stream_t; /* cudaStream_t */
+
+enum sbn_status {
+  SBN_OK = 0,
+  SBN_ERR_INVALID = -1,     /* bad argument (-> ValueError / GeometryError) */
+  SBN_ERR_SHAPE = -2,       /* inconsistent dims (-> ShapeMismatchError) */
+  SBN_ERR_UNSUPPORTED = -3, /* dtype/config not implemented (-> UnsupportedConfigError) */
+  SBN_ERR_WORKSPACE = -4,   /* workspace too small */
+  SBN_ERR_CUDA = -5         /* launch / runtime error */
+};
+
+enum sbn_dtype { SBN_F32 = 0, SBN_F64 = 1, SBN_BF16 = 2 };
+enum sbn_pool { SBN_POOL_MAX = 0, SBN_POOL_AVG = 1 };
+enum sbn_algo { SBN_ALGO_AUTO = 0, SBN_ALGO_SIMT = 1, SBN_ALGO_TCGEN05 = 2 };
+
+/* Overlap-save tiling of one layer; the fields of the reference BlockSpec
+ * (`tiling.py:47-61`) as computed by `compute_block_spec` (`tiling.py:64-99`). */
+typedef struct sbn_geometry {
+  int32_t n, h, w;     /* input frames and spatial extent */
+  int32_t bh, bw;      /* block_size (input window incl. halo) */
+  int32_t sy, sx;      /* in_stride = block - overlap */
+  int32_t oy, ox;      /* grid_origin (<= 0) */
+  int32_t gy, gx;      /* grid_count */
+  int32_t obh, obw;    /* out_block_size (= output stride) */
+  int32_t oh, ow;      /* out_size of the dense conv */
+} sbn_geometry;
+
+/* Inference-mode bottleneck unit (reference ResidualUnitParams, `layers.py:85-114`).
+ * Filters HWIO (kh, kw, cin, cout) in the activation dtype; biases (cout) in the
+ * activation dtype; BN folded to per-channel scale/shift (`ops.py:213-216`) in the
+ * compute dtype (float for F32/BF16, double for F64). */
+typedef struct sbn_unit_params {
+  const void* w1; const void* b1;   /* 1x1, c -> m */
+  const void* w2; const void* b2;   /* 3x3, m -> m */
+  const void* w3; const void* b3;   /* 1x1, m -> c */
+  const void* bn1_scale; const void* bn1_shift;
+  const void* bn2_scale; const void* bn2_shift;
+  const void* bn3_scale; const void* bn3_shift;
+} sbn_unit_params;
+
+const char* sbn_version(void);
+const char* sbn_last_error(void);
+int sbn_device_sm_count(int device);
+
+/* reduce_mask (`tiling.py:138-160`): pool each block's input window of `mask`
+ * (zero outside the image) and emit active blocks in ascending (n, by, bx) order.
+ * MAX: any pixel set.  AVG: count/(bh*bw) >= threshold - 1e-12 in float64.
+ * idx: int32 (n*gy*gx, 3) capacity; count: one int32.  ws: sbn_reduce_mask_workspace
+ * bytes, ZEROED ONCE by the caller at allocation (the kernel leaves it zeroed). */
+size_t sbn_reduce_mask_workspace(const sbn_geometry* g);
+int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* g, int pool, double threshold,
+                    int32_t* idx, int32_t* count, void* ws, size_t ws_bytes, sbn_stream_t stream);
+
+/* downsample_mask (`tiling.py:163-174`): max-pool window = stride = factor, ceil dims. */
+int sbn_downsample_mask(const uint8_t* in, int n, int h, int w, int factor, uint8_t* out,
+                        sbn_stream_t stream);
+
+/* gather / gather_transpose (`blocks.py:57-94`): out is (cap, bh, bw, c) NHWC or
+ * (cap, c, bh, bw) when transpose != 0; rows >= *count are left untouched. */
+int sbn_gather(const void* x, int dtype, int c, const sbn_geometry* g, const int32_t* idx,
+               const int32_t* count, int cap, int transpose, void* out, sbn_stream_t stream);
+
+/* in_bounds_map (`blocks.py:97-112`): uint8 (cap, bh, bw). */
+int sbn_in_bounds(const sbn_geometry* g, const int32_t* idx, const int32_t* count, int cap,
+                  uint8_t* out, sbn_stream_t stream);
+
+/* scatter / scatter_add / scatter_transpose (`blocks.py:115-159`): write (add != 0:
+ * accumulate) each (obh, obw, c) block — (c, obh, obw) when transpose != 0 — into
+ * dst (n, oh, ow, c) at (by*obh, bx*obw), clipped to (oh, ow). */
+int sbn_scatter(const void* blocks, int dtype, int c, const sbn_geometry* g, const int32_t* idx,
+                const int32_t* count, int cap, int add, int transpose, void* dst,
+                sbn_stream_t stream);
+
+/* Fused sparse_conv2d body (`layers.py:27-47` after reduce_mask): gather -> valid
+ * conv (kh, kw, stride sh, sw) -> (+bias) -> scatter into dst (n, oh, ow, cout), all in
+ * one kernel; the block stack never touches HBM.  w: HWIO; bias nullable. */
+int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
+                    const sbn_geometry* g, const void* w, const void* bias, const int32_t* idx,
+                    const int32_t* count, int cap, void* dst, int algo, sbn_stream_t stream);
+
+/* Fused sparse_residual_unit body (`layers.py:203-229` after reduce_mask): gather ->
+ * bottleneck branch (`_unit_branch`, `layers.py:137-179`) -> scatter_add onto out.
+ * out must hold x's values on entry (out == x is allowed: in-place, as the paper's
+ * fused scatter-add).  halo >= 0 as in the reference; pre_act selects the chain. */
+size_t sbn_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* g, int halo,
+                                   int algo);
+int sbn_residual_unit(const void* x, int dtype, int c, int m, const sbn_geometry* g, int halo,
+                      int pre_act, const sbn_unit_params* p, const int32_t* idx,
+                      const int32_t* count, int cap, void* out, void* ws, size_t ws_bytes,
+                      int algo, sbn_stream_t stream);
+
+/* Which algorithm `algo=AUTO` would pick (SBN_ALGO_SIMT / SBN_ALGO_TCGEN05). */
+int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometry* g, int halo, int pre_act);
+int sbn_sparse_conv_algo(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
+                         const sbn_geometry* g);
+
+/* Number of kernels the library has launched since load (for the bench's
+ * gpu_launches claim). */
+uint64_t sbn_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBNET_H_ */

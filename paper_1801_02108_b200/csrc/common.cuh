@@ -1,0 +1,100 @@
+// Shared helpers for the sbnet sm_100a kernels: dtype traits, status plumbing,
+// device properties, geometry helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+
+#include "../../include/sbnet.h"
+
+namespace sbn {
+
+// ----------------------------------------------------------------- status / errors
+void set_error(const char* fmt, ...);
+void note_launch(int k = 1);
+
+#define SBN_CHECK_ARG(cond, code, ...)            \
+  do {                                            \
+    if (!(cond)) {                                \
+      ::sbn::set_error(__VA_ARGS__);              \
+      return (code);                              \
+    }                                             \
+  } while (0)
+
+inline int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return SBN_ERR_CUDA;
+  }
+  note_launch();
+  return SBN_OK;
+}
+
+int sm_count();           // SMs of the current device (cached)
+int max_smem_optin();     // max dynamic smem per block (cached)
+
+// ----------------------------------------------------------------- dtypes
+template <typename T> struct Acc { using type = float; };
+template <> struct Acc<double> { using type = double; };
+
+__device__ __forceinline__ float to_acc(float v) { return v; }
+__device__ __forceinline__ double to_acc(double v) { return v; }
+__device__ __forceinline__ float to_acc(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_acc(float v);
+template <> __device__ __forceinline__ float from_acc<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <typename T> __device__ __forceinline__ T from_acc(double v);
+template <> __device__ __forceinline__ double from_acc<double>(double v) { return v; }
+
+inline int dtype_size(int dtype) {
+  switch (dtype) {
+    case SBN_F32: return 4;
+    case SBN_F64: return 8;
+    case SBN_BF16: return 2;
+    default: return 0;
+  }
+}
+
+// ----------------------------------------------------------------- geometry
+struct Geo {
+  int n, h, w, bh, bw, sy, sx, oy, ox, gy, gx, obh, obw, oh, ow;
+};
+
+inline Geo to_geo(const sbn_geometry* g) {
+  return Geo{g->n, g->h, g->w, g->bh, g->bw, g->sy, g->sx, g->oy, g->ox,
+             g->gy, g->gx, g->obh, g->obw, g->oh, g->ow};
+}
+
+inline int check_geo(const sbn_geometry* g) {
+  SBN_CHECK_ARG(g != nullptr, SBN_ERR_INVALID, "geometry is null");
+  SBN_CHECK_ARG(g->n >= 0 && g->h > 0 && g->w > 0, SBN_ERR_SHAPE, "bad input dims n=%d h=%d w=%d",
+                g->n, g->h, g->w);
+  SBN_CHECK_ARG(g->bh > 0 && g->bw > 0 && g->sy > 0 && g->sx > 0, SBN_ERR_INVALID,
+                "bad block/in_stride");
+  SBN_CHECK_ARG(g->gy > 0 && g->gx > 0 && g->obh > 0 && g->obw > 0 && g->oh > 0 && g->ow > 0,
+                SBN_ERR_INVALID, "bad grid/out geometry");
+  SBN_CHECK_ARG(g->oy <= 0 && g->ox <= 0, SBN_ERR_INVALID, "grid origin must be <= 0");
+  return SBN_OK;
+}
+
+// Persistent grid size for a per-block kernel: enough CTAs to fill the device
+// `per_sm` deep, never more than the index-list capacity.
+inline int persistent_grid(int cap, int per_sm) {
+  long g = (long)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  return g < 1 ? 1 : (int)g;
+}
+
+__device__ __forceinline__ int ld_count(const int32_t* count, int cap) {
+  int c = __ldg(count);
+  return c < cap ? c : cap;
+}
+
+}  // namespace sbn

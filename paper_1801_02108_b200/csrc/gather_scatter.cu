@@ -1,0 +1,279 @@
+// gather / gather_transpose / scatter / scatter_add / scatter_transpose.
+//
+// Restates reference `blocks.py:57-159`.  NHWC rows are contiguous on both sides of
+// every copy (a window row of bw pixels x C channels in the source, one stack row in
+// the destination), so each warp streams whole rows with the widest vector (16 B when
+// C*elem_size and the base pointers allow it), zero-filling the out-of-image halo.
+// Scatter writes only each block's disjoint, clipped output window: no atomics, and
+// the result is bit-exact (add mode does exactly one add in the tensor dtype per
+// element, as numpy's `+=`).
+#include "common.cuh"
+
+namespace sbn {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int VS> struct VecT;
+template <> struct VecT<16> { using type = uint4; };
+template <> struct VecT<8> { using type = uint2; };
+template <> struct VecT<4> { using type = uint32_t; };
+template <> struct VecT<2> { using type = uint16_t; };
+template <> struct VecT<1> { using type = uint8_t; };
+
+template <int VS>
+__global__ void __launch_bounds__(kThreads)
+gather_rows_kernel(const uint8_t* __restrict__ x, Geo g, int pix_bytes,
+                   const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int cap,
+                   uint8_t* __restrict__ out) {
+  using V = typename VecT<VS>::type;
+  const int B = ld_count(count, cap);
+  const int lane = threadIdx.x & 31;
+  const long nwarps = (long)gridDim.x * (kThreads / 32);
+  const int vpp = pix_bytes / VS;  // vectors per pixel
+  const int nvec = g.bw * vpp;
+  for (long r = blockIdx.x * (long)(kThreads / 32) + (threadIdx.x >> 5); r < (long)B * g.bh;
+       r += nwarps) {
+    const int b = (int)(r / g.bh), wy = (int)(r - (long)b * g.bh);
+    const int n = __ldg(idx + 3 * b), by = __ldg(idx + 3 * b + 1), bx = __ldg(idx + 3 * b + 2);
+    const int y = g.oy + by * g.sy + wy;
+    const int xs = g.ox + bx * g.sx;
+    const bool row_ok = (y >= 0 && y < g.h);
+    V* dst = reinterpret_cast<V*>(out + (size_t)r * g.bw * pix_bytes);
+    const V* src = reinterpret_cast<const V*>(x + ((size_t)n * g.h + (row_ok ? y : 0)) * g.w *
+                                                      (size_t)pix_bytes);
+    for (int k = lane; k < nvec; k += 32) {
+      const int wx = k / vpp;
+      const int xx = xs + wx;
+      V v;
+      if (row_ok && xx >= 0 && xx < g.w) {
+        v = __ldg(src + (size_t)xx * vpp + (k - wx * vpp));
+      } else {
+        memset(&v, 0, sizeof(V));
+      }
+      dst[k] = v;
+    }
+  }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(kThreads)
+gather_transpose_kernel(const E* __restrict__ x, Geo g, int c, const int32_t* __restrict__ idx,
+                        const int32_t* __restrict__ count, int cap, E* __restrict__ out) {
+  const int B = ld_count(count, cap);
+  const long per = (long)c * g.bh * g.bw;
+  const long total = (long)B * per;
+  for (long i = blockIdx.x * (long)kThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kThreads) {
+    const int wx = (int)(i % g.bw);
+    long r = i / g.bw;
+    const int wy = (int)(r % g.bh);
+    r /= g.bh;
+    const int ch = (int)(r % c);
+    const int b = (int)(r / c);
+    const int n = __ldg(idx + 3 * b);
+    const int y = g.oy + __ldg(idx + 3 * b + 1) * g.sy + wy;
+    const int xx = g.ox + __ldg(idx + 3 * b + 2) * g.sx + wx;
+    E v = E(0);
+    if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+      v = __ldg(x + (((size_t)n * g.h + y) * g.w + xx) * c + ch);
+    out[i] = v;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T add_elem(T a, T b) {
+  return a + b;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 add_elem<__nv_bfloat16>(__nv_bfloat16 a,
+                                                                   __nv_bfloat16 b) {
+  return __float2bfloat16_rn(__bfloat162float(a) + __bfloat162float(b));
+}
+
+// ADD=false: plain vector copy of each clipped output row; ADD=true: typed add with
+// 16-byte vectors of T when VS == 16, else element-wise.
+template <int VS, typename T, bool ADD>
+__global__ void __launch_bounds__(kThreads)
+scatter_rows_kernel(const uint8_t* __restrict__ blk, Geo g, int pix_bytes,
+                    const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int cap,
+                    uint8_t* __restrict__ dst) {
+  using V = typename VecT<VS>::type;
+  const int B = ld_count(count, cap);
+  const int lane = threadIdx.x & 31;
+  const long nwarps = (long)gridDim.x * (kThreads / 32);
+  for (long r = blockIdx.x * (long)(kThreads / 32) + (threadIdx.x >> 5); r < (long)B * g.obh;
+       r += nwarps) {
+    const int b = (int)(r / g.obh), oy = (int)(r - (long)b * g.obh);
+    const int n = __ldg(idx + 3 * b), by = __ldg(idx + 3 * b + 1), bx = __ldg(idx + 3 * b + 2);
+    const int Y = by * g.obh + oy;
+    if (Y >= g.oh) continue;
+    const int X0 = bx * g.obw;
+    const int npix = min(g.obw, g.ow - X0);
+    if (npix <= 0) continue;
+    const int nvec = npix * pix_bytes / VS;
+    const V* src = reinterpret_cast<const V*>(blk + (size_t)r * g.obw * pix_bytes);
+    V* out = reinterpret_cast<V*>(dst + (((size_t)n * g.oh + Y) * g.ow + X0) * pix_bytes);
+    for (int k = lane; k < nvec; k += 32) {
+      V v = __ldg(src + k);
+      if constexpr (ADD) {
+        V d = out[k];
+        constexpr int ne = VS / sizeof(T);
+        T* dv = reinterpret_cast<T*>(&d);
+        const T* sv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+        for (int e = 0; e < ne; ++e) dv[e] = add_elem<T>(dv[e], sv[e]);
+        out[k] = d;
+      } else {
+        out[k] = v;
+      }
+    }
+  }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(kThreads)
+scatter_transpose_kernel(const E* __restrict__ blk, Geo g, int c, const int32_t* __restrict__ idx,
+                         const int32_t* __restrict__ count, int cap, E* __restrict__ dst) {
+  const int B = ld_count(count, cap);
+  const long per = (long)g.obh * g.obw * c;
+  const long total = (long)B * per;
+  for (long i = blockIdx.x * (long)kThreads + threadIdx.x; i < total;
+       i += (long)gridDim.x * kThreads) {
+    const int ch = (int)(i % c);
+    long r = i / c;
+    const int ox = (int)(r % g.obw);
+    r /= g.obw;
+    const int oy = (int)(r % g.obh);
+    const int b = (int)(r / g.obh);
+    const int Y = __ldg(idx + 3 * b + 1) * g.obh + oy;
+    const int X = __ldg(idx + 3 * b + 2) * g.obw + ox;
+    if (Y >= g.oh || X >= g.ow) continue;
+    const int n = __ldg(idx + 3 * b);
+    dst[(((size_t)n * g.oh + Y) * g.ow + X) * c + ch] =
+        blk[(((size_t)b * c + ch) * g.obh + oy) * g.obw + ox];
+  }
+}
+
+int pick_vec(size_t pix_bytes, const void* a, const void* b) {
+  const uintptr_t al = (uintptr_t)a | (uintptr_t)b;
+  for (int vs = 16; vs > 1; vs >>= 1)
+    if (pix_bytes % vs == 0 && al % vs == 0) return vs;
+  return 1;
+}
+
+long grid_for(long work_items, int per_cta) {
+  long b = (work_items + per_cta - 1) / per_cta;
+  long cap = (long)sm_count() * 16;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : b;
+}
+
+template <int VS>
+void launch_gather(const void* x, Geo g, int pix, const int32_t* idx, const int32_t* count,
+                   int cap, void* out, cudaStream_t s) {
+  gather_rows_kernel<VS><<<(unsigned)grid_for((long)cap * g.bh, kThreads / 32), kThreads, 0, s>>>(
+      (const uint8_t*)x, g, pix, idx, count, cap, (uint8_t*)out);
+}
+
+template <int VS, typename T, bool ADD>
+void launch_scatter(const void* blk, Geo g, int pix, const int32_t* idx, const int32_t* count,
+                    int cap, void* dst, cudaStream_t s) {
+  scatter_rows_kernel<VS, T, ADD>
+      <<<(unsigned)grid_for((long)cap * g.obh, kThreads / 32), kThreads, 0, s>>>(
+          (const uint8_t*)blk, g, pix, idx, count, cap, (uint8_t*)dst);
+}
+
+template <typename T>
+int scatter_add_typed(const void* blk, Geo g, int c, const int32_t* idx, const int32_t* count,
+                      int cap, void* dst, cudaStream_t s) {
+  const int pix = c * (int)sizeof(T);
+  if (pick_vec(pix, blk, dst) == 16)
+    launch_scatter<16, T, true>(blk, g, pix, idx, count, cap, dst, s);
+  else
+    launch_scatter<sizeof(T), T, true>(blk, g, pix, idx, count, cap, dst, s);
+  return launch_status("scatter_add");
+}
+
+}  // namespace
+}  // namespace sbn
+
+using namespace sbn;
+
+extern "C" int sbn_gather(const void* x, int dtype, int c, const sbn_geometry* gp,
+                          const int32_t* idx, const int32_t* count, int cap, int transpose,
+                          void* out, sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  const int es = dtype_size(dtype);
+  SBN_CHECK_ARG(es > 0, SBN_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
+  SBN_CHECK_ARG(c > 0, SBN_ERR_SHAPE, "channels must be > 0");
+  if (cap <= 0) return SBN_OK;
+  SBN_CHECK_ARG(x && idx && count && out, SBN_ERR_INVALID, "null pointer argument");
+  Geo g = to_geo(gp);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (transpose) {
+    const unsigned grid = (unsigned)grid_for((long)cap * c * g.bh * g.bw, kThreads);
+    if (es == 2)
+      gather_transpose_kernel<uint16_t><<<grid, kThreads, 0, s>>>((const uint16_t*)x, g, c, idx,
+                                                                  count, cap, (uint16_t*)out);
+    else if (es == 4)
+      gather_transpose_kernel<uint32_t><<<grid, kThreads, 0, s>>>((const uint32_t*)x, g, c, idx,
+                                                                  count, cap, (uint32_t*)out);
+    else
+      gather_transpose_kernel<uint64_t><<<grid, kThreads, 0, s>>>((const uint64_t*)x, g, c, idx,
+                                                                  count, cap, (uint64_t*)out);
+    return launch_status("gather_transpose");
+  }
+  const int pix = c * es;
+  switch (pick_vec(pix, x, out)) {
+    case 16: launch_gather<16>(x, g, pix, idx, count, cap, out, s); break;
+    case 8: launch_gather<8>(x, g, pix, idx, count, cap, out, s); break;
+    case 4: launch_gather<4>(x, g, pix, idx, count, cap, out, s); break;
+    default: launch_gather<2>(x, g, pix, idx, count, cap, out, s); break;
+  }
+  return launch_status("gather");
+}
+
+extern "C" int sbn_scatter(const void* blk, int dtype, int c, const sbn_geometry* gp,
+                           const int32_t* idx, const int32_t* count, int cap, int add,
+                           int transpose, void* dst, sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  const int es = dtype_size(dtype);
+  SBN_CHECK_ARG(es > 0, SBN_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
+  SBN_CHECK_ARG(c > 0, SBN_ERR_SHAPE, "channels must be > 0");
+  SBN_CHECK_ARG(!(add && transpose), SBN_ERR_UNSUPPORTED, "scatter_transpose has no add mode");
+  if (cap <= 0) return SBN_OK;
+  SBN_CHECK_ARG(blk && idx && count && dst, SBN_ERR_INVALID, "null pointer argument");
+  Geo g = to_geo(gp);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (transpose) {
+    const unsigned grid = (unsigned)grid_for((long)cap * c * g.obh * g.obw, kThreads);
+    if (es == 2)
+      scatter_transpose_kernel<uint16_t><<<grid, kThreads, 0, s>>>((const uint16_t*)blk, g, c, idx,
+                                                                   count, cap, (uint16_t*)dst);
+    else if (es == 4)
+      scatter_transpose_kernel<uint32_t><<<grid, kThreads, 0, s>>>((const uint32_t*)blk, g, c, idx,
+                                                                   count, cap, (uint32_t*)dst);
+    else
+      scatter_transpose_kernel<uint64_t><<<grid, kThreads, 0, s>>>((const uint64_t*)blk, g, c, idx,
+                                                                   count, cap, (uint64_t*)dst);
+    return launch_status("scatter_transpose");
+  }
+  if (add) {
+    switch (dtype) {
+      case SBN_F32: return scatter_add_typed<float>(blk, g, c, idx, count, cap, dst, s);
+      case SBN_F64: return scatter_add_typed<double>(blk, g, c, idx, count, cap, dst, s);
+      default: return scatter_add_typed<__nv_bfloat16>(blk, g, c, idx, count, cap, dst, s);
+    }
+  }
+  const int pix = c * es;
+  switch (pick_vec(pix, blk, dst)) {
+    case 16: launch_scatter<16, uint8_t, false>(blk, g, pix, idx, count, cap, dst, s); break;
+    case 8: launch_scatter<8, uint8_t, false>(blk, g, pix, idx, count, cap, dst, s); break;
+    case 4: launch_scatter<4, uint8_t, false>(blk, g, pix, idx, count, cap, dst, s); break;
+    default: launch_scatter<2, uint8_t, false>(blk, g, pix, idx, count, cap, dst, s); break;
+  }
+  return launch_status("scatter");
+}

@@ -1,0 +1,264 @@
+// Mask kernels: reduce_mask (ordered active-block list), downsample_mask, in_bounds_map.
+//
+// reduce_mask restates reference `tiling.py:120-160` (window sums + argwhere) as ONE
+// kernel launch:
+//   * one CTA per tile = one block row (frame n, block-row by); tiles are taken in
+//     ascending order through an atomic ticket so every earlier tile is resident or done;
+//   * the CTA column-reduces the bh mask rows its window row spans (coalesced byte
+//     loads, one pass over the mask), then window-reduces columns per block;
+//   * MAX: count > 0, AVG: count/(bh*bw) >= thr - 1e-12 in float64 (as the reference);
+//   * warp-ballot + popc compaction gives each active block its rank inside the tile;
+//     the tile's global offset comes from a decoupled look-back over earlier tiles, so
+//     the output is exactly argwhere's ascending (n, by, bx) order without a sort;
+//   * the last CTA to finish zeroes the workspace, so it can be reused (and captured
+//     in a CUDA graph) without a memset.
+#include "common.cuh"
+
+namespace sbn {
+namespace {
+
+constexpr int kMaskThreads = 256;
+constexpr int kColBuf = 4096;  // column-sum buffer (ints) per chunk
+
+struct MaskWs {
+  unsigned int ticket;
+  unsigned int done;
+  unsigned long long status[1];  // [tiles] : (flag << 32) | value
+};
+
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ int block_sum(int v, int* red) {
+  // 256-thread block reduction; result broadcast to all threads
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < kMaskThreads / 32; ++i) t += red[i];
+  return t;
+}
+
+__global__ void __launch_bounds__(kMaskThreads)
+reduce_mask_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int chunk,
+                   int32_t* __restrict__ idx, int32_t* __restrict__ count, MaskWs* ws, int tiles) {
+  __shared__ int colsum[kColBuf];
+  __shared__ int red[kMaskThreads / 32];
+  __shared__ int woff[kMaskThreads / 32];
+  __shared__ unsigned int s_tile;
+  __shared__ int s_prefix;
+  __shared__ int s_last;
+  extern __shared__ uint8_t flags[];  // [gx]
+
+  if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
+  __syncthreads();
+  const int tile = (int)s_tile;
+  const int n = tile / g.gy;
+  const int by = tile - n * g.gy;
+
+  const int wy0 = g.oy + by * g.sy;
+  const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
+  const uint8_t* mrow = mask + (size_t)n * g.h * g.w;
+  const double area = (double)g.bh * (double)g.bw;
+
+  int tile_count = 0;
+  for (int bx0 = 0; bx0 < g.gx; bx0 += chunk) {
+    const int bx1 = min(bx0 + chunk, g.gx);
+    const int cx0 = max(g.ox + bx0 * g.sx, 0);
+    const int cx1 = min(g.ox + (bx1 - 1) * g.sx + g.bw, g.w);
+    __syncthreads();
+    for (int x = cx0 + (int)threadIdx.x; x < cx1; x += kMaskThreads) {
+      int s = 0;
+      for (int y = y0; y < y1; ++y) s += __ldg(mrow + (size_t)y * g.w + x);
+      colsum[x - cx0] = s;
+    }
+    __syncthreads();
+    int local = 0;
+    for (int bx = bx0 + (int)threadIdx.x; bx < bx1; bx += kMaskThreads) {
+      const int wx0 = g.ox + bx * g.sx;
+      const int xa = max(wx0, 0), xb = min(wx0 + g.bw, g.w);
+      int cnt = 0;
+      if (y1 > y0)
+        for (int x = xa; x < xb; ++x) cnt += colsum[x - cx0];
+      bool on;
+      if (pool == SBN_POOL_MAX) on = cnt > 0;
+      else on = ((double)cnt / area) >= thr - 1e-12;
+      flags[bx] = on ? 1 : 0;
+      local += on ? 1 : 0;
+    }
+    tile_count += block_sum(local, red);
+  }
+
+  // ---- decoupled look-back: exclusive prefix of active blocks over earlier tiles
+  if (threadIdx.x == 0) {
+    int prefix = 0;
+    if (tile == 0) {
+      __threadfence();
+      atomicExch(&ws->status[0], (2ull << 32) | (unsigned)tile_count);
+    } else {
+      atomicExch(&ws->status[tile], (1ull << 32) | (unsigned)tile_count);
+      for (int j = tile - 1; j >= 0;) {
+        unsigned long long s = ld_volatile(&ws->status[j]);
+        unsigned flag = (unsigned)(s >> 32);
+        if (flag == 0) continue;  // predecessor not published yet: spin
+        prefix += (int)(unsigned)(s & 0xffffffffull);
+        if (flag == 2) break;
+        --j;
+      }
+      __threadfence();
+      atomicExch(&ws->status[tile], (2ull << 32) | (unsigned)(prefix + tile_count));
+    }
+    s_prefix = prefix;
+    if (tile == tiles - 1) *count = prefix + tile_count;
+  }
+  __syncthreads();
+
+  // ---- ordered compaction: ballot/popc ranks inside the tile
+  int base = s_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int bx0 = 0; bx0 < g.gx; bx0 += kMaskThreads) {
+    const int bx = bx0 + (int)threadIdx.x;
+    const bool on = bx < g.gx && flags[bx];
+    const unsigned bal = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) woff[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int i = 0; i < kMaskThreads / 32; ++i) {
+      before += (i < warp) ? woff[i] : 0;
+      total += woff[i];
+    }
+    if (on) {
+      const int pos = base + before + __popc(bal & ((1u << lane) - 1u));
+      idx[3 * pos + 0] = n;
+      idx[3 * pos + 1] = by;
+      idx[3 * pos + 2] = bx;
+    }
+    base += total;
+    __syncthreads();
+  }
+
+  // ---- self-cleaning workspace: the last CTA out resets ticket/done/status
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = (atomicAdd(&ws->done, 1u) == (unsigned)(tiles - 1));
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int t = threadIdx.x; t < tiles; t += kMaskThreads) ws->status[t] = 0ull;
+    if (threadIdx.x == 0) {
+      ws->ticket = 0u;
+      ws->done = 0u;
+    }
+    __threadfence();
+  }
+}
+
+__global__ void downsample_kernel(const uint8_t* __restrict__ in, int n, int h, int w, int f,
+                                  int oh, int ow, uint8_t* __restrict__ out) {
+  const long total = (long)n * oh * ow;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int ox = (int)(i % ow);
+    const long r = i / ow;
+    const int oy = (int)(r % oh);
+    const int fr = (int)(r / oh);
+    const int ya = oy * f, yb = min(ya + f, h), xa = ox * f, xb = min(xa + f, w);
+    uint8_t v = 0;
+    const uint8_t* p = in + (size_t)fr * h * w;
+    for (int y = ya; y < yb && !v; ++y)
+      for (int x = xa; x < xb; ++x) v = max(v, __ldg(p + (size_t)y * w + x));
+    out[i] = v;
+  }
+}
+
+__global__ void in_bounds_kernel(Geo g, const int32_t* __restrict__ idx,
+                                 const int32_t* __restrict__ count, int cap,
+                                 uint8_t* __restrict__ out) {
+  const int B = ld_count(count, cap);
+  const long per = (long)g.bh * g.bw;
+  const long total = (long)B * per;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / per);
+    const int r = (int)(i - (long)b * per);
+    const int wy = r / g.bw, wx = r - wy * g.bw;
+    const int y = g.oy + idx[3 * b + 1] * g.sy + wy;
+    const int x = g.ox + idx[3 * b + 2] * g.sx + wx;
+    out[i] = (y >= 0 && y < g.h && x >= 0 && x < g.w) ? 1 : 0;
+  }
+}
+
+}  // namespace
+}  // namespace sbn
+
+using namespace sbn;
+
+extern "C" size_t sbn_reduce_mask_workspace(const sbn_geometry* g) {
+  if (!g) return 0;
+  const size_t tiles = (size_t)g->n * (size_t)g->gy;
+  return 16 + 8 * (tiles > 0 ? tiles : 1);
+}
+
+extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int pool,
+                               double threshold, int32_t* idx, int32_t* count, void* ws,
+                               size_t ws_bytes, sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  SBN_CHECK_ARG(pool == SBN_POOL_MAX || pool == SBN_POOL_AVG, SBN_ERR_INVALID, "bad pool mode %d",
+                pool);
+  SBN_CHECK_ARG(mask && idx && count, SBN_ERR_INVALID, "null pointer argument");
+  SBN_CHECK_ARG(ws_bytes >= sbn_reduce_mask_workspace(gp) && ws, SBN_ERR_WORKSPACE,
+                "reduce_mask workspace too small (%zu < %zu)", ws_bytes,
+                sbn_reduce_mask_workspace(gp));
+  cudaStream_t s = (cudaStream_t)stream;
+  Geo g = to_geo(gp);
+  const long tiles = (long)g.n * g.gy;
+  if (tiles == 0) {
+    cudaMemsetAsync(count, 0, sizeof(int32_t), s);
+    return launch_status("reduce_mask(empty)");
+  }
+  SBN_CHECK_ARG(tiles < (1l << 31), SBN_ERR_INVALID, "too many block rows");
+  // chunk of block columns whose column range fits the column-sum buffer
+  int chunk = g.gx;
+  if ((long)(chunk - 1) * g.sx + g.bw > kColBuf) chunk = (kColBuf - g.bw) / g.sx + 1;
+  SBN_CHECK_ARG(chunk >= 1, SBN_ERR_UNSUPPORTED, "block width %d too large for reduce_mask", g.bw);
+  const size_t dyn = (size_t)g.gx;
+  SBN_CHECK_ARG(dyn <= 48 * 1024 - 20 * 1024, SBN_ERR_UNSUPPORTED, "grid width %d too large", g.gx);
+  reduce_mask_kernel<<<(unsigned)tiles, kMaskThreads, dyn, s>>>(
+      mask, g, pool, threshold, chunk, idx, count, reinterpret_cast<MaskWs*>(ws), (int)tiles);
+  return launch_status("reduce_mask");
+}
+
+extern "C" int sbn_downsample_mask(const uint8_t* in, int n, int h, int w, int factor,
+                                   uint8_t* out, sbn_stream_t stream) {
+  SBN_CHECK_ARG(factor >= 1, SBN_ERR_INVALID, "factor must be >= 1, got %d", factor);
+  SBN_CHECK_ARG(n >= 0 && h > 0 && w > 0, SBN_ERR_SHAPE, "bad mask dims");
+  const int oh = (h + factor - 1) / factor, ow = (w + factor - 1) / factor;
+  const long total = (long)n * oh * ow;
+  if (total == 0) return SBN_OK;
+  const int threads = 256;
+  long blocks = (total + threads - 1) / threads;
+  if (blocks > (long)sm_count() * 32) blocks = (long)sm_count() * 32;
+  downsample_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(in, n, h, w, factor,
+                                                                           oh, ow, out);
+  return launch_status("downsample_mask");
+}
+
+extern "C" int sbn_in_bounds(const sbn_geometry* gp, const int32_t* idx, const int32_t* count,
+                             int cap, uint8_t* out, sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  if (cap <= 0) return SBN_OK;
+  Geo g = to_geo(gp);
+  long total = (long)cap * g.bh * g.bw;
+  long blocks = (total + 255) / 256;
+  if (blocks > (long)sm_count() * 16) blocks = (long)sm_count() * 16;
+  in_bounds_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(g, idx, count, cap, out);
+  return launch_status("in_bounds");
+}

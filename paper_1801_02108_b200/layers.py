@@ -1,0 +1,398 @@
+"""Composite sparse layers (reference `layers.py`): sparse_conv2d, the sparse residual
+unit, stages and the backbone.
+
+Hot path per layer = two libsbnet launches on the current stream, no host sync:
+``sbn_reduce_mask`` (mask -> ordered device index list) and one fused kernel
+(``sbn_sparse_conv`` / ``sbn_residual_unit``) that gathers, computes and scatters
+without materialising the block stack.  Dense comparators (`conv2d_direct`,
+`dense_residual_unit`) and stage projections use cuDNN.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from .blocks import GatheredBlocks
+from .errors import EmptyBlockListError, GeometryError, ShapeMismatchError, UnsupportedConfigError
+from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, bn_inference,
+                  dense_conv_nhwc, exact_fp32)
+from .tensor import Tensor4D, cuda, dtype_code
+from .tiling import (BinaryMask, BlockIndexList, BlockSpec, compute_block_spec, downsample_mask,
+                     reduce_mask)
+
+_ALGOS = {"auto": _lib.SBN_ALGO_AUTO, "simt": _lib.SBN_ALGO_SIMT, "tcgen05": _lib.SBN_ALGO_TCGEN05}
+
+
+def _algo(a) -> int:
+    if isinstance(a, int):
+        return a
+    try:
+        return _ALGOS[a]
+    except KeyError:
+        raise ValueError(f"unknown algo {a!r}; expected one of {sorted(_ALGOS)}") from None
+
+
+def _check_mask(x: Tensor4D, mask: BinaryMask) -> None:
+    n, h, w, _ = x.dims
+    if mask.dims != (n, h, w):
+        raise ShapeMismatchError(f"mask dims {mask.dims} != tensor (n, h, w) {(n, h, w)}")
+
+
+class _Scratch(threading.local):
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+        b = self.bufs.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+            self.bufs[key] = b
+        return b
+
+
+_SCRATCH = _Scratch()
+
+
+# ----------------------------------------------------------------------------- sparse conv
+
+def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
+                  block_size: tuple[int, int], pool: PoolMode = PoolMode.MAX,
+                  threshold: float | None = None, dst: Tensor4D | None = None,
+                  algo="auto") -> Tensor4D:
+    """Mask-guided convolution (reference `layers.py:27-47`): reduce_mask, then one fused
+    gather -> valid conv -> scatter kernel.  Output pixels in active write regions equal
+    the dense convolution; others keep `dst` (zeros by default)."""
+    _check_mask(x, mask)
+    if f.kernel != tuple(p.kernel) or f.c_in != x.dims[3] or f.c_out != p.filter_count:
+        raise ShapeMismatchError("filter bank does not match the conv params / input channels")
+    spec = compute_block_spec(x.dims, p, block_size)
+    idx = reduce_mask(mask, spec, pool, threshold)
+    xt = cuda(x.nhwc())
+    n = x.dims[0]
+    if dst is None:
+        out = torch.zeros((n, spec.out_size[0], spec.out_size[1], f.c_out), dtype=xt.dtype,
+                          device=xt.device)
+    else:
+        if dst.dims != (n, spec.out_size[0], spec.out_size[1], f.c_out):
+            raise ShapeMismatchError(f"destination dims {dst.dims} != conv output")
+        out = cuda(dst.nhwc()).clone()
+    sparse_conv_into(xt, out, f, p, spec, idx, algo)
+    return Tensor4D.from_nhwc(out, x.layout)
+
+
+def sparse_conv_into(xt: torch.Tensor, out: torch.Tensor, f: FilterBank, p: ConvParams,
+                     spec: BlockSpec, idx: BlockIndexList, algo="auto") -> None:
+    """Fused gather -> conv -> scatter of the active blocks of `xt` into `out` (NHWC CUDA
+    tensors), stream-ordered, no sync."""
+    lib = _lib.load()
+    w, b = f.device_tensors(xt.dtype, xt.device)
+    idx.to_device(xt.device)
+    g = spec.c_geometry(xt.shape[0])
+    kh, kw = p.kernel
+    sh, sw = p.stride
+    st = lib.sbn_sparse_conv(xt.data_ptr(), dtype_code(xt.dtype), f.c_in, f.c_out, kh, kw, sh, sw,
+                             C.byref(g), w.data_ptr(), None if b is None else b.data_ptr(),
+                             idx.rows.data_ptr(), idx.count_dev.data_ptr(), idx.capacity,
+                             out.data_ptr(), _algo(algo), _lib.stream_handle(xt.device))
+    _lib.check(st, "sparse_conv2d")
+
+
+def sparse_conv_algo(dtype: torch.dtype, f: FilterBank, p: ConvParams, spec: BlockSpec) -> str:
+    g = spec.c_geometry(1)
+    a = _lib.load(False).sbn_sparse_conv_algo(dtype_code(dtype), f.c_in, f.c_out, *p.kernel,
+                                              *p.stride, C.byref(g))
+    return "tcgen05" if a == _lib.SBN_ALGO_TCGEN05 else "simt"
+
+
+def sparse_batch_norm(blocks: GatheredBlocks, bn: BnParams, mode: BnMode = BnMode.INFERENCE):
+    """Batch norm over gathered blocks only (reference `layers.py:68-82`)."""
+    t = cuda(blocks.tensor.nhwc())
+    if bn.channels != t.shape[3]:
+        raise ShapeMismatchError(f"bn channels {bn.channels} != block channels {t.shape[3]}")
+    if mode is BnMode.INFERENCE:
+        return blocks.with_tensor(Tensor4D.from_nhwc(bn_inference(t, bn), blocks.tensor.layout))
+    if blocks.count == 0:
+        raise EmptyBlockListError("train-mode statistics are undefined for an empty block list")
+    mean = t.mean(dim=(0, 1, 2))
+    var = t.var(dim=(0, 1, 2), unbiased=False)
+    g = torch.as_tensor(np.asarray(bn.gamma), device=t.device, dtype=t.dtype)
+    be = torch.as_tensor(np.asarray(bn.beta), device=t.device, dtype=t.dtype)
+    out = (t - mean) * (g / torch.sqrt(var + bn.epsilon)) + be
+    return blocks.with_tensor(Tensor4D.from_nhwc(out, blocks.tensor.layout)), (mean, var)
+
+
+# ----------------------------------------------------------------------------- residual unit
+
+@dataclass(frozen=True, eq=False)
+class ResidualUnitParams:
+    """Bottleneck 1x1 (c->m), 3x3 (m->m), 1x1 (m->c) with per-conv BN
+    (reference `layers.py:85-114`)."""
+
+    conv1: FilterBank
+    conv2: FilterBank
+    conv3: FilterBank
+    bn1: BnParams
+    bn2: BnParams
+    bn3: BnParams
+    pre_activation: bool = True
+    _cache: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.conv1.kernel != (1, 1) or self.conv3.kernel != (1, 1):
+            raise ShapeMismatchError("conv1/conv3 must be 1x1")
+        if self.conv2.kernel != (3, 3):
+            raise ShapeMismatchError("conv2 must be 3x3")
+        if self.conv1.c_out != self.conv2.c_in or self.conv2.c_out != self.conv3.c_in:
+            raise ShapeMismatchError("unit channel chain is inconsistent")
+        if self.conv3.c_out != self.conv1.c_in:
+            raise ShapeMismatchError(
+                f"identity shortcut needs c_out {self.conv3.c_out} == c_in {self.conv1.c_in}")
+
+    @property
+    def channels(self) -> int:
+        return self.conv1.c_in
+
+    @property
+    def mid_channels(self) -> int:
+        return self.conv1.c_out
+
+    def c_params(self, dtype: torch.dtype, device):
+        """(UnitParams struct, keep-alive tensors) for the C-ABI, cached per dtype/device."""
+        key = (dtype, str(device))
+        if key not in self._cache:
+            keep = []
+            up = _lib.UnitParams()
+            for i, fb in enumerate((self.conv1, self.conv2, self.conv3), 1):
+                w, b = fb.device_tensors(dtype, device)
+                if b is None:
+                    b = torch.zeros(fb.c_out, dtype=dtype, device=device)
+                keep += [w, b]
+                setattr(up, f"w{i}", w.data_ptr())
+                setattr(up, f"b{i}", b.data_ptr())
+            for i, bn in enumerate((self.bn1, self.bn2, self.bn3), 1):
+                s, t = bn.folded(dtype, device)
+                keep += [s, t]
+                setattr(up, f"bn{i}_scale", s.data_ptr())
+                setattr(up, f"bn{i}_shift", t.data_ptr())
+            self._cache[key] = (up, keep)
+        return self._cache[key][0]
+
+
+def random_unit_params(rng: np.random.Generator, c: int, m: int, dtype=np.float32,
+                       scale: float = 0.2, pre_activation: bool = True) -> ResidualUnitParams:
+    """Seeded random unit; consumes the generator in the same order as the reference
+    (`layers.py:117-134`) so equal seeds give equal weights on both sides."""
+    def filt(kh, kw, ci, co):
+        wts = rng.standard_normal((kh, kw, ci, co)).astype(dtype) * scale
+        return FilterBank(wts, rng.standard_normal(co).astype(dtype) * scale)
+
+    def norm(ch):
+        gamma = (0.5 + rng.random(ch)).astype(dtype)
+        beta = (rng.standard_normal(ch) * scale).astype(dtype)
+        mean = (rng.standard_normal(ch) * scale).astype(dtype)
+        var = (0.5 + rng.random(ch)).astype(dtype)
+        return BnParams(gamma, beta, mean, var)
+
+    first = norm(c if pre_activation else m)
+    last = norm(m if pre_activation else c)
+    f1, f2, f3 = filt(1, 1, c, m), filt(3, 3, m, m), filt(1, 1, m, c)
+    mid = norm(m)
+    return ResidualUnitParams(f1, f2, f3, first, mid, last, pre_activation)
+
+
+def unit_spec(x_dims, block_size, halo: int = 1) -> BlockSpec:
+    """Geometry of the shared gather/scatter pair around the unit's receptive growth:
+    an effective (2*halo+1)^2 SAME conv (reference `layers.py:182-191`)."""
+    if halo < 0:
+        raise GeometryError(f"halo must be >= 0, got {halo}")
+    k = 2 * halo + 1
+    if block_size[0] < k or block_size[1] < k:
+        raise GeometryError(f"block size {tuple(block_size)} too small for halo {halo}")
+    eff = ConvParams(kernel=(k, k), stride=(1, 1), padding=Padding.SAME, filter_count=x_dims[3])
+    return compute_block_spec(x_dims, eff, block_size)
+
+
+def _dense_branch(t: torch.Tensor, u: ResidualUnitParams) -> torch.Tensor:
+    dt, dev = t.dtype, t.device
+    w1, b1 = u.conv1.device_tensors(dt, dev)
+    w2, b2 = u.conv2.device_tensors(dt, dev)
+    w3, b3 = u.conv3.device_tensors(dt, dev)
+    if u.pre_activation:
+        r = torch.relu(bn_inference(t, u.bn1))
+        r = torch.relu(bn_inference(dense_conv_nhwc(r, w1, b1, (1, 1), (0, 0)), u.bn2))
+        r = torch.relu(bn_inference(dense_conv_nhwc(r, w2, b2, (1, 1), (1, 1)), u.bn3))
+        return dense_conv_nhwc(r, w3, b3, (1, 1), (0, 0))
+    r = torch.relu(bn_inference(dense_conv_nhwc(t, w1, b1, (1, 1), (0, 0)), u.bn1))
+    r = torch.relu(bn_inference(dense_conv_nhwc(r, w2, b2, (1, 1), (1, 1)), u.bn2))
+    return bn_inference(dense_conv_nhwc(r, w3, b3, (1, 1), (0, 0)), u.bn3)
+
+
+def dense_residual_unit(x: Tensor4D, u: ResidualUnitParams,
+                        bn_mode: BnMode = BnMode.INFERENCE) -> Tensor4D:
+    """Dense unit with SAME 3x3 (reference `layers.py:194-200`) on cuDNN: the dense
+    comparator of the sparse unit."""
+    if u.channels != x.dims[3]:
+        raise ShapeMismatchError(f"unit channels {u.channels} != input channels {x.dims[3]}")
+    if bn_mode is not BnMode.INFERENCE:
+        raise UnsupportedConfigError("dense_residual_unit: inference-mode BN only")
+    t = cuda(x.nhwc())
+    return Tensor4D.from_nhwc(t + _dense_branch(t, u), x.layout)
+
+
+def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
+                         block_size: tuple[int, int], halo: int = 1,
+                         bn_mode: BnMode = BnMode.INFERENCE,
+                         _shared: tuple[BlockSpec, BlockIndexList] | None = None,
+                         inplace: bool = False, algo="auto") -> Tensor4D:
+    """Residual unit inside one gather/scatter pair (reference `layers.py:203-229`);
+    inactive pixels stay bit-identical to x.
+
+    Default: functional like the reference (x is cloned, then the fused kernel
+    scatter-adds into the clone).  ``inplace=True`` updates x's storage directly — the
+    paper's fused scatter-add; the kernel snapshots the halo rims first, so neighbours'
+    writes never leak into a window.
+    """
+    if u.channels != x.dims[3]:
+        raise ShapeMismatchError(f"unit channels {u.channels} != input channels {x.dims[3]}")
+    if bn_mode is not BnMode.INFERENCE:
+        raise UnsupportedConfigError("sparse_residual_unit: inference-mode BN only (training is out of scope)")
+    if _shared is None:
+        _check_mask(x, mask)
+        spec = unit_spec(x.dims, block_size, halo)
+        idx = reduce_mask(mask, spec, PoolMode.MAX)
+    else:
+        spec, idx = _shared
+    xt = cuda(x.nhwc())
+    if inplace and x.nhwc().is_cuda and xt.data_ptr() == x.nhwc().data_ptr():
+        out = xt
+    else:
+        out = xt.clone()
+    residual_unit_into(out, out if (out is xt) else xt, u, spec, idx, halo, algo)
+    return Tensor4D.from_nhwc(out, x.layout)
+
+
+def residual_unit_into(out: torch.Tensor, src: torch.Tensor, u: ResidualUnitParams,
+                       spec: BlockSpec, idx: BlockIndexList, halo: int = 1, algo="auto") -> None:
+    """Fused unit: out[active] += branch(src windows).  `out` must hold src's values
+    (either a clone, or `out is src` for the in-place form)."""
+    lib = _lib.load()
+    dt, dev = src.dtype, src.device
+    n, _, _, c = src.shape
+    m = u.mid_channels
+    g = spec.c_geometry(n)
+    a = _algo(algo)
+    idx.to_device(dev)
+    nbytes = lib.sbn_residual_unit_workspace(dtype_code(dt), c, m, C.byref(g), halo, a)
+    ws = _SCRATCH.get(nbytes, dev)
+    up = u.c_params(dt, dev)
+    st = lib.sbn_residual_unit(src.data_ptr(), dtype_code(dt), c, m, C.byref(g), halo,
+                               int(u.pre_activation), C.byref(up), idx.rows.data_ptr(),
+                               idx.count_dev.data_ptr(), idx.capacity, out.data_ptr(),
+                               ws.data_ptr(), ws.numel(), a, _lib.stream_handle(dev))
+    _lib.check(st, "sparse_residual_unit")
+
+
+def residual_unit_algo(dtype: torch.dtype, u: ResidualUnitParams, spec: BlockSpec, halo=1) -> str:
+    g = spec.c_geometry(1)
+    a = _lib.load(False).sbn_residual_unit_algo(dtype_code(dtype), u.channels, u.mid_channels,
+                                                C.byref(g), halo, int(u.pre_activation))
+    return "tcgen05" if a == _lib.SBN_ALGO_TCGEN05 else "simt"
+
+
+# ----------------------------------------------------------------------------- stages
+
+@dataclass(frozen=True)
+class StageConfig:
+    unit_count: int
+    channels: tuple[int, int, int]   # (c_in, c_mid, c_out)
+    block_size: tuple[int, int]
+    mask_scale: int = 1              # downsample factor from the base mask
+    stride: int = 1                  # dense projection stride (stage transition)
+
+
+@dataclass(frozen=True)
+class Stage:
+    config: StageConfig
+    projection: FilterBank | None
+    units: tuple[ResidualUnitParams, ...]
+
+
+@dataclass(frozen=True)
+class StageResult:
+    output: Tensor4D
+    mask: BinaryMask | None
+    spec: BlockSpec | None
+    indices: BlockIndexList | None
+
+
+def build_stage(cfg: StageConfig, rng: np.random.Generator, dtype=np.float32,
+                scale: float = 0.2) -> Stage:
+    """Random stage weights, generator order as the reference (`layers.py:287-298`)."""
+    c_in, c_mid, c_out = cfg.channels
+    proj = None
+    if cfg.stride != 1 or c_in != c_out:
+        proj = FilterBank(rng.standard_normal((3, 3, c_in, c_out)).astype(dtype) * scale,
+                          rng.standard_normal(c_out).astype(dtype) * scale)
+    units = tuple(random_unit_params(rng, c_out, c_mid, dtype, scale) for _ in range(cfg.unit_count))
+    return Stage(cfg, proj, units)
+
+
+def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
+              bn_mode: BnMode = BnMode.INFERENCE, algo="auto") -> StageResult:
+    """Dense stride-s projection (cuDNN), then residual units sharing ONE index list
+    computed from the downsampled mask (reference `layers.py:311-329`).  The units run
+    in place on the stage's private activation buffer (one clone at most)."""
+    cfg = stage.config
+    t = cuda(x.nhwc())
+    owned = False
+    if stage.projection is not None:
+        p = ConvParams((3, 3), (cfg.stride, cfg.stride), Padding.SAME, cfg.channels[2])
+        w, b = stage.projection.device_tensors(t.dtype, t.device)
+        t = dense_conv_nhwc(t, w, b, p.stride, p.pad)
+        owned = True
+    if not sparse:
+        for u in stage.units:
+            t = t + _dense_branch(t, u)
+        return StageResult(Tensor4D.from_nhwc(t, x.layout), None, None, None)
+    mask = downsample_mask(base_mask, cfg.mask_scale)
+    if mask.dims != tuple(t.shape[:3]):
+        raise ShapeMismatchError(f"mask dims {mask.dims} != tensor (n, h, w) {tuple(t.shape[:3])}")
+    spec = unit_spec(tuple(t.shape), cfg.block_size, halo=1)
+    idx = reduce_mask(mask, spec, PoolMode.MAX)
+    if not owned:
+        t = t.clone()
+    for u in stage.units:
+        if u.channels != t.shape[3]:
+            raise ShapeMismatchError(f"unit channels {u.channels} != input channels {t.shape[3]}")
+        residual_unit_into(t, t, u, spec, idx, 1, algo)
+    return StageResult(Tensor4D.from_nhwc(t, x.layout), mask, spec, idx)
+
+
+@dataclass(frozen=True)
+class Backbone:
+    stages: tuple[Stage, ...]
+
+
+def build_backbone(stage_cfgs, rng: np.random.Generator, dtype=np.float32,
+                   scale: float = 0.2) -> Backbone:
+    for prev, nxt in zip(stage_cfgs, stage_cfgs[1:]):
+        if prev.channels[2] != nxt.channels[0]:
+            raise ShapeMismatchError(f"stage channel chain broken: {prev.channels[2]} -> {nxt.channels[0]}")
+    return Backbone(tuple(build_stage(cfg, rng, dtype, scale) for cfg in stage_cfgs))
+
+
+def run_backbone(bb: Backbone, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
+                 bn_mode: BnMode = BnMode.INFERENCE, algo="auto") -> list[StageResult]:
+    results = []
+    for stage in bb.stages:
+        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo)
+        results.append(res)
+        x = res.output
+    return results

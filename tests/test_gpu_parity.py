@@ -1,0 +1,368 @@
+"""GPU parity: every CUDA path vs the reference's golden vectors and the CPU oracle.
+
+Bit-exact for indices and copies; rel_err <= 1e-5 (conv) / 1e-4 (unit) for fp32 as the
+reference's own tests; <= 2e-2 for bf16 against the fp32 oracle on bf16-rounded
+inputs (north star).  All calls go through the drop-in Python API -> C-ABI -> CUDA.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_1801_02108_b200 as P
+from paper_1801_02108_b200 import _lib
+from golden_cases import cases, conv_cfg, load, unit_dict
+from oracle import sbnet_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _conv(k, s, same, co=1):
+    return P.ConvParams(tuple(k), tuple(s), P.Padding.SAME if same else P.Padding.VALID, co)
+
+
+def _spec(h, w, k, s, same, b, c=1):
+    return P.compute_block_spec((1, h, w, c), _conv(k, s, same, c), b)
+
+
+def _np(t):
+    t = t.data if isinstance(t, P.Tensor4D) else t
+    if t.dtype == torch.bfloat16:
+        t = t.float()
+    return t.detach().cpu().numpy()
+
+
+def _unit_params(case):
+    def fb(i):
+        return P.FilterBank(case[f"conv{i}_w"], case[f"conv{i}_b"])
+
+    def bn(i):
+        return P.BnParams(case[f"bn{i}_gamma"], case[f"bn{i}_beta"], case[f"bn{i}_mean"],
+                          case[f"bn{i}_var"])
+    return P.ResidualUnitParams(fb(1), fb(2), fb(3), bn(1), bn(2), bn(3), bool(case["pre"][0]))
+
+
+# ----------------------------------------------------------------------------- masks
+
+def test_reduce_mask_golden_bit_exact(cuda_device):
+    for case in cases(load("reduce_mask"), "c"):
+        h, w, k, s, same, b = conv_cfg(case["cfg"])
+        avg, thr = int(case["cfg"][9]), int(case["cfg"][10])
+        spec = _spec(h, w, k, s, same, b)
+        idx = P.reduce_mask(P.BinaryMask(case["mask"]), spec, P.PoolMode.AVG if avg else P.PoolMode.MAX,
+                            None if thr < 0 else thr / 1e6)
+        assert idx.entries.tolist() == case["idx"].tolist()
+
+
+def test_downsample_golden_bit_exact(cuda_device):
+    for case in cases(load("reduce_mask"), "d"):
+        out = P.downsample_mask(P.BinaryMask(case["mask"]), int(case["f"][0]))
+        assert np.array_equal(out.numpy(), case["out"])
+
+
+@pytest.mark.parametrize("block", [8, 16, 32])
+@pytest.mark.parametrize("density", [0.05, 0.3, 1.0])
+def test_reduce_mask_config3_sizes_vs_oracle(cuda_device, block, density):
+    m = P.synth_mask_topleft((2, 800, 700), 1.0 - density)
+    spec = _spec(800, 700, (3, 3), (1, 1), True, (block, block), 128)
+    idx = P.reduce_mask(m, spec)
+    ref = O.reduce_mask(m.numpy(), O.geometry(800, 700, (3, 3), (1, 1), True, (block, block)))
+    assert np.array_equal(idx.entries, ref)
+
+
+def test_reduce_mask_many_frames_ordered_and_repeatable(cuda_device):
+    """N=64 blob masks: many tiles exercise the look-back; the self-resetting workspace
+    must give identical results call after call (also under CUDA graph replay)."""
+    rng = np.random.default_rng(0)
+    m = (rng.random((64, 200, 175)) < 0.01).astype(np.uint8)
+    spec = _spec(200, 175, (3, 3), (1, 1), True, (10, 10), 8)
+    ref = O.reduce_mask(m, O.geometry(200, 175, (3, 3), (1, 1), True, (10, 10)))
+    bm = P.BinaryMask(m).cuda()
+    for _ in range(3):
+        assert np.array_equal(P.reduce_mask(bm, spec).entries, ref)
+    # graph capture of the reduce_mask launch (static buffers)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        idx0 = P.reduce_mask(bm, spec)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            idx = P.reduce_mask(bm, spec)
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(idx.rows[: len(ref)].cpu().numpy(), ref.astype(np.int32))
+        assert int(idx.count_dev.item()) == len(ref)
+    assert np.array_equal(idx0.entries, ref)
+
+
+def test_reduce_mask_avg_thresholds_vs_oracle(cuda_device):
+    rng = np.random.default_rng(1)
+    m = (rng.random((3, 57, 91)) < 0.4).astype(np.uint8)
+    for thr in (None, 0.1, 0.4, 0.5, 1.0):
+        for blk, same in (((6, 6), True), ((9, 5), False)):
+            spec = _spec(57, 91, (3, 3), (1, 1), same, blk)
+            got = P.reduce_mask(P.BinaryMask(m), spec, P.PoolMode.AVG, thr).entries
+            ref = O.reduce_mask(m, O.geometry(57, 91, (3, 3), (1, 1), same, blk), "avg", thr)
+            assert np.array_equal(got, ref)
+
+
+# ----------------------------------------------------------------------------- gather/scatter
+
+def test_gather_scatter_golden_bit_exact(cuda_device):
+    for case in cases(load("gather_scatter")):
+        h, w, k, s, same, b = conv_cfg(case["cfg"])
+        x = case["x"]
+        n, c = x.shape[0], x.shape[3]
+        spec = P.compute_block_spec((n, h, w, c), _conv(k, s, same, 1), b)
+        idx = P.BlockIndexList(case["idx"])
+        g = P.gather(P.Tensor4D(x), idx, spec)
+        assert np.array_equal(_np(g.tensor), case["gather"])
+        gt = P.gather_transpose(P.Tensor4D(x), idx, spec)
+        assert gt.tensor.layout is P.Layout.CHANNELS_FIRST
+        assert np.array_equal(_np(gt.tensor), case["gather_t"])
+        assert np.array_equal(P.in_bounds_map(idx, spec).cpu().numpy(), case["inb"])
+        blk = g.with_tensor(P.Tensor4D(case["blk"]))
+        dst = P.Tensor4D(case["dst"])
+        assert np.array_equal(_np(P.scatter(blk, spec, dst)), case["scatter"])
+        assert np.array_equal(_np(P.scatter_add(blk, spec, dst)), case["scatter_add"])
+        blk_t = g.with_tensor(P.transpose_layout(P.Tensor4D(case["blk"])))
+        assert np.array_equal(_np(P.scatter_transpose(blk_t, spec, dst)), case["scatter_t"])
+        assert np.array_equal(_np(dst), case["dst"])  # functional: dst untouched
+
+
+def test_gather_scatter_with_device_index_list(cuda_device):
+    """reduce_mask's device list feeds gather/scatter directly (count read on device)."""
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2, 40, 50, 24)).astype(np.float32)
+    m = (rng.random((2, 40, 50)) < 0.03).astype(np.uint8)
+    spec = P.compute_block_spec(x.shape, _conv((3, 3), (1, 1), True, 24), (10, 10))
+    geo = O.geometry(40, 50, (3, 3), (1, 1), True, (10, 10))
+    idx = P.reduce_mask(P.BinaryMask(m), spec)
+    ref_idx = O.reduce_mask(m, geo)
+    g = P.gather(P.Tensor4D(x), idx, spec)
+    assert np.array_equal(_np(g.tensor), O.gather(x, ref_idx, geo))
+    blk = rng.standard_normal((len(ref_idx), 8, 8, 24)).astype(np.float32)
+    out = P.scatter_add(g.with_tensor(P.Tensor4D(blk)), spec, P.Tensor4D(x))
+    assert np.array_equal(_np(out), O.scatter(blk, ref_idx, geo, x, add=True))
+
+
+def test_bf16_gather_scatter_bit_exact(cuda_device):
+    rng = np.random.default_rng(3)
+    x = torch.from_numpy(rng.standard_normal((1, 64, 48, 64)).astype(np.float32)).bfloat16()
+    xf = x.float().numpy()
+    m = (rng.random((1, 64, 48)) < 0.05).astype(np.uint8)
+    spec = P.compute_block_spec(tuple(x.shape), _conv((3, 3), (1, 1), True, 64), (16, 16))
+    geo = O.geometry(64, 48, (3, 3), (1, 1), True, (16, 16))
+    idx = P.reduce_mask(P.BinaryMask(m), spec)
+    ri = O.reduce_mask(m, geo)
+    g = P.gather(P.Tensor4D(x), idx, spec)
+    assert np.array_equal(_np(g.tensor), O.gather(xf, ri, geo))
+    blk = torch.from_numpy(rng.standard_normal((len(ri), 14, 14, 64)).astype(np.float32)).bfloat16()
+    out = P.scatter(g.with_tensor(P.Tensor4D(blk)), spec, P.Tensor4D(x))
+    assert np.array_equal(_np(out), O.scatter(blk.float().numpy(), ri, geo, xf))
+
+
+def test_gather_rejects_out_of_grid_index(cuda_device):
+    x = P.Tensor4D(np.ones((1, 8, 8, 1), np.float32))
+    spec = _spec(8, 8, (1, 1), (1, 1), False, (4, 4))
+    with pytest.raises(P.GeometryError):
+        P.gather(x, P.BlockIndexList(np.array([[0, 9, 0]])), spec)
+    g = P.gather(x, P.BlockIndexList(np.zeros((0, 3))), spec)
+    assert g.count == 0 and g.tensor.dims[0] == 0
+
+
+# ----------------------------------------------------------------------------- sparse conv
+
+def test_sparse_conv_golden_fp32(cuda_device):
+    for case in cases(load("sparse_conv")):
+        h, w, k, s, same, b = conv_cfg(case["cfg"])
+        co = case["w"].shape[3]
+        y = P.sparse_conv2d(P.Tensor4D(case["x"]), P.BinaryMask(case["mask"]),
+                            P.FilterBank(case["w"], case["b"]), _conv(k, s, same, co), b)
+        ref = case["y"]
+        assert y.dims == ref.shape
+        region = np.abs(ref).sum(-1) != 0
+        assert O.rel_err(_np(y), ref) <= 1e-5
+        assert np.all(_np(y)[~region] == 0)
+
+
+def test_config1_golden(cuda_device):
+    z = load("config1")
+    p = _conv((3, 3), (1, 1), True, 16)
+    spec = P.compute_block_spec((1, 64, 64, 16), p, (16, 16))
+    idx = P.reduce_mask(P.BinaryMask(z["mask"]), spec)
+    assert idx.entries.tolist() == z["idx"].tolist() and idx.count == 12
+    y = P.sparse_conv2d(P.Tensor4D(z["x"]), P.BinaryMask(z["mask"]), P.FilterBank(z["w"], z["b"]), p,
+                        (16, 16))
+    assert O.rel_err(_np(y), z["y"]) <= 1e-5
+
+
+def test_sparse_conv_random_sweep_vs_oracle(cuda_device):
+    """The reference's own sweep space (verify.py:60-76), dense-equivalence on active regions."""
+    rng = np.random.default_rng(21)
+    kinds = ["full", "empty", "0.25", "0.5", "0.9"]
+    for r in range(40):
+        n, c, co = int(rng.integers(1, 3)), int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        kh, kw = int(rng.choice([1, 3, 5])), int(rng.choice([1, 3, 5]))
+        sh = int(rng.choice([1, 2])) if kh > 1 else 1
+        sw = int(rng.choice([1, 2])) if kw > 1 else 1
+        h, w = int(rng.integers(max(kh, 6), 49)), int(rng.integers(max(kw, 6), 49))
+        same = bool(rng.random() < 0.5)
+        b = (kh + sh * int(rng.integers(1, 14)), kw + sw * int(rng.integers(1, 14)))
+        kind = kinds[r % len(kinds)]
+        m = {"full": np.ones((n, h, w), np.uint8), "empty": np.zeros((n, h, w), np.uint8)}.get(
+            kind, (rng.random((n, h, w)) < float(kind if kind[0] == "0" else 0)).astype(np.uint8))
+        x = rng.standard_normal((n, h, w, c)).astype(np.float32)
+        wt = rng.standard_normal((kh, kw, c, co)).astype(np.float32)
+        bias = rng.standard_normal(co).astype(np.float32)
+        p = _conv((kh, kw), (sh, sw), same, co)
+        y = _np(P.sparse_conv2d(P.Tensor4D(x), P.BinaryMask(m), P.FilterBank(wt, bias), p, b))
+        geo = O.geometry(h, w, (kh, kw), (sh, sw), same, b)
+        idx = O.reduce_mask(m, geo)
+        dense = O.dense_conv2d(x, wt, bias, (sh, sw), same)
+        reg = O.active_region(geo, idx, n)
+        assert O.rel_err(y[reg], dense[reg]) <= 1e-5
+        assert np.all(y[~reg] == 0)
+
+
+def test_sparse_conv_f64_and_dst(cuda_device):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((1, 30, 30, 3))
+    wt = rng.standard_normal((3, 3, 3, 5))
+    m = (rng.random((1, 30, 30)) < 0.05).astype(np.uint8)
+    dst = rng.standard_normal((1, 30, 30, 5))
+    p = _conv((3, 3), (1, 1), True, 5)
+    y = _np(P.sparse_conv2d(P.Tensor4D(x), P.BinaryMask(m), P.FilterBank(wt), p, (8, 8), dst=P.Tensor4D(dst)))
+    ref = O.sparse_conv2d(x, m, wt, None, (1, 1), True, (8, 8), dst=dst)
+    assert O.rel_err(y, ref) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- residual unit
+
+@pytest.mark.parametrize("inplace", [False, True])
+def test_residual_unit_golden_fp32(cuda_device, inplace):
+    for case in cases(load("residual")):
+        n, h, w, c, m, bs, halo, pre = (int(v) for v in case["cfg"])
+        u = _unit_params(case)
+        x = P.Tensor4D(torch.from_numpy(case["x"]).cuda())
+        x_before = x.data.clone()
+        y = P.sparse_residual_unit(x, P.BinaryMask(case["mask"]), u, (bs, bs), halo=halo, inplace=inplace)
+        assert O.rel_err(_np(y), case["y"]) <= 1e-4
+        if inplace:
+            assert y.data.data_ptr() == x.data.data_ptr()
+        else:
+            assert torch.equal(x.data, x_before)
+
+
+def test_residual_unit_inactive_pixels_bit_identical(cuda_device):
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((2, 37, 45, 6)).astype(np.float32)
+    mk = (rng.random((2, 37, 45)) < 0.02).astype(np.uint8)
+    u = P.random_unit_params(rng, 6, 4)
+    y = _np(P.sparse_residual_unit(P.Tensor4D(x), P.BinaryMask(mk), u, (9, 9)))
+    geo = O.unit_geometry(37, 45, (9, 9))
+    reg = O.active_region(geo, O.reduce_mask(mk, geo), 2)
+    assert np.array_equal(y[~reg], x[~reg])
+    y0 = _np(P.sparse_residual_unit(P.Tensor4D(x), P.BinaryMask.empty(2, 37, 45), u, (9, 9)))
+    assert np.array_equal(y0, x)
+
+
+def test_residual_unit_halo_accounting(cuda_device):
+    """halo 1/2 reproduce the dense unit on active regions; halo 0 does not
+    (reference test_layers.py:153-157)."""
+    rng = np.random.default_rng(31)
+    worst = {0: 0.0, 1: 0.0, 2: 0.0}
+    for r in range(8):
+        n, c, m = 1, int(rng.integers(2, 9)), int(rng.integers(2, 9))
+        h, w = int(rng.integers(8, 41)), int(rng.integers(8, 41))
+        x = rng.standard_normal((n, h, w, c)).astype(np.float32)
+        mk = (rng.random((n, h, w)) < 0.3).astype(np.uint8)
+        u = P.random_unit_params(rng, c, m)
+        ud = {"pre": True}
+        for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
+            ud[f"w{i}"], ud[f"b{i}"] = fb.weights, fb.bias
+            ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
+        dense = O.dense_residual_unit(x, ud)
+        for halo in (0, 1, 2):
+            bs = int(rng.integers(max(4, 2 * halo + 1), 17))
+            y = _np(P.sparse_residual_unit(P.Tensor4D(x), P.BinaryMask(mk), u, (bs, bs), halo=halo))
+            geo = O.unit_geometry(h, w, (bs, bs), halo)
+            reg = O.active_region(geo, O.reduce_mask(mk, geo), n)
+            if reg.any():
+                worst[halo] = max(worst[halo], O.rel_err(y[reg], dense[reg]))
+    assert worst[1] <= 1e-4 and worst[2] <= 1e-4
+    assert worst[0] > 1e-3
+
+
+def _bf16_unit_case(seed, h, w, c, m, density, block):
+    rng = np.random.default_rng(seed)
+    x = torch.from_numpy(rng.standard_normal((1, h, w, c)).astype(np.float32)).bfloat16()
+    u = P.random_unit_params(rng, c, m)
+    mk = P.synth_mask_blobs((1, h, w), 1.0 - density, seed)
+    return x, u, mk
+
+
+def _oracle_unit_bf16(x_bf16, u, mk, block):
+    """fp32 oracle on bf16-rounded inputs and weights (SURVEY §8(c) bf16 policy)."""
+    def r(a):
+        return torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()
+    ud = {"pre": u.pre_activation}
+    for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
+        ud[f"w{i}"], ud[f"b{i}"] = r(fb.weights), r(fb.bias)
+        ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
+    return O.sparse_residual_unit(x_bf16.float().numpy(), mk.numpy(), ud, block)
+
+
+@pytest.mark.parametrize("algo", ["auto", "simt"])
+def test_residual_unit_bf16_config2_vs_fp32_oracle(cuda_device, algo):
+    x, u, mk = _bf16_unit_case(0, 400, 400, 64, 32, 0.1, (16, 16))
+    ref = _oracle_unit_bf16(x, u, mk, (16, 16))
+    for inplace in (False, True):
+        xt = P.Tensor4D(x.clone().cuda())
+        y = _np(P.sparse_residual_unit(xt, mk, u, (16, 16), inplace=inplace, algo=algo))
+        err = O.rel_err(y, ref)
+        assert err <= 2e-2, (algo, inplace, err)
+
+
+def test_residual_unit_tc_matches_simt_bf16(cuda_device):
+    """When the tcgen05 path is built for this config it must agree with the SIMT path."""
+    x, u, mk = _bf16_unit_case(1, 160, 144, 64, 32, 0.3, (16, 16))
+    spec = P.unit_spec(tuple(x.shape), (16, 16))
+    from paper_1801_02108_b200.layers import residual_unit_algo
+    if residual_unit_algo(torch.bfloat16, u, spec) != "tcgen05":
+        pytest.skip("tcgen05 unit not available for this config")
+    a = _np(P.sparse_residual_unit(P.Tensor4D(x.cuda()), mk, u, (16, 16), algo="tcgen05"))
+    b = _np(P.sparse_residual_unit(P.Tensor4D(x.cuda()), mk, u, (16, 16), algo="simt"))
+    assert O.rel_err(a, b) <= 1e-2
+
+
+def test_stage_and_backbone_full_mask_match_dense(cuda_device):
+    rng = np.random.default_rng(10)
+    cfg = P.StageConfig(unit_count=2, channels=(4, 3, 8), block_size=(8, 8), stride=2)
+    stage = P.build_stage(cfg, rng)
+    x = P.Tensor4D(rng.standard_normal((1, 24, 24, 4)).astype(np.float32))
+    mask = P.BinaryMask.full(1, 12, 12)
+    sp = P.run_stage(stage, x, mask, sparse=True)
+    de = P.run_stage(stage, x, mask, sparse=False)
+    assert O.rel_err(_np(sp.output), _np(de.output)) <= 1e-4
+    cfgs = [P.StageConfig(1, (2, 2, 4), (6, 6), 1, 1), P.StageConfig(1, (4, 2, 6), (5, 5), 2, 2),
+            P.StageConfig(1, (6, 2, 8), (4, 4), 4, 2)]
+    bb = P.build_backbone(cfgs, rng)
+    xb = P.Tensor4D(rng.standard_normal((1, 32, 48, 2)).astype(np.float32))
+    res = P.run_backbone(bb, xb, P.BinaryMask.full(1, 32, 48))
+    assert [r.output.dims[1:3] for r in res] == [(32, 48), (16, 24), (8, 12)]
+    assert [r.mask.dims[1:] for r in res] == [(32, 48), (16, 24), (8, 12)]
+
+
+def test_stage_of_one_unit_equals_single_sparse_unit(cuda_device):
+    rng = np.random.default_rng(9)
+    stage = P.build_stage(P.StageConfig(1, (4, 3, 4), (8, 8)), rng)
+    x = P.Tensor4D(rng.standard_normal((1, 16, 16, 4)).astype(np.float32))
+    mask = P.BinaryMask((rng.random((1, 16, 16)) < 0.2).astype(np.uint8))
+    res = P.run_stage(stage, x, mask)
+    direct = P.sparse_residual_unit(x, mask, stage.units[0], (8, 8))
+    assert torch.equal(res.output.data, direct.data)
+
+
+def test_library_kernels_were_launched(cuda_device):
+    assert _lib.launch_count() > 0
