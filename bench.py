@@ -1,0 +1,416 @@
+"""Benchmark: sparse ResNet-block frames/s and speed-up vs the dense bf16 unit.
+
+Workload (BASELINE.json configs[1]): one sparse ResNet bottleneck unit (1x1 c->m,
+3x3 m->m, 1x1 m->c; c=64, m=32 = c//2 as reference cli.py:164), N=1 frame of
+400x400x64 NHWC bf16 per step, 10% road-map-like mask (reference synth_mask_blobs
+at 90% sparsity, seeded per frame), 16x16 blocks.  A step = reduce_mask + fused unit
+(in place: the paper's fused scatter-add) on one frame whose activations and mask are
+already resident in HBM.  Frames cycle through a ring whose total size exceeds L2
+(126 MB), so every step reads cold data.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun): frames are batch-sharded, one process per GPU, no collective on the
+hot path; timed region bracketed by barrier + synchronize, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse ResNet-block frames/s & speedup vs dense conv at 10–90% mask density"
+UNIT = "frames/s"
+H, W, C, M = 400, 400, 64, 32
+BLOCK = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--density", type=float, default=0.10)
+    ap.add_argument("--block", type=int, default=BLOCK)
+    ap.add_argument("--frames", type=int, default=32,
+                    help="ring of distinct frames; the blocks touched across the ring exceed L2")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons in a thread during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # NVML unavailable: record nothing
+            self.max = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max, "reasons": rs, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+
+def make_frames(P, torch, nframes, first_seed, density, device):
+    import numpy as np
+    xs, masks, dens = [], [], []
+    for f in range(nframes):
+        rng = np.random.default_rng(1000 + first_seed + f)
+        x = torch.from_numpy(rng.standard_normal((1, H, W, C), dtype=np.float32)).to(device).bfloat16()
+        mk = P.synth_mask_blobs((1, H, W), 1.0 - density, first_seed + f)
+        dens.append(float(mk.data.float().mean()))
+        xs.append(x)
+        masks.append(mk.cuda())
+    return xs, masks, dens
+
+
+def unit_bytes(P, spec, idx_entries, c=C, es=2):
+    """Algorithmic HBM bytes of one fused-unit launch: each active block's in-image window
+    read once + its clipped output window written once."""
+    h, w = spec.input_size
+    bh, bw = spec.block_size
+    (oy, ox), (sy, sx) = spec.grid_origin, spec.in_stride
+    obh, obw = spec.out_block_size
+    oh, ow = spec.out_size
+    tot = 0
+    for _, by, bx in idx_entries:
+        ys, xs = oy + by * sy, ox + bx * sx
+        win = (min(ys + bh, h) - max(ys, 0)) * (min(xs + bw, w) - max(xs, 0))
+        outp = (min(by * obh + obh, oh) - by * obh) * (min(bx * obw + obw, ow) - bx * obw)
+        tot += (win + outp) * c * es
+    return tot
+
+
+def time_graph(torch, fn_steps, steps, warmup, soak_s=0.3):
+    """Capture `steps` steps in one CUDA graph; warm up, soak, then time one replay."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn_steps(warmup)  # eager warm-up (also allocates every cached buffer)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn_steps(steps)
+        torch.cuda.synchronize()
+        t_end = time.time() + soak_s
+        while time.time() < t_end:  # clock ramp (untimed)
+            g.replay()
+            torch.cuda.synchronize()
+    return g, s
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1801_02108_b200 as P
+    from paper_1801_02108_b200 import _lib
+    from paper_1801_02108_b200.layers import residual_unit_into, residual_unit_algo
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    nf = args.frames
+    xs, masks, dens = make_frames(P, torch, nf, rank * nf, args.density, dev)
+    u = P.random_unit_params(np.random.default_rng(0), C, M)
+    blk = (args.block, args.block)
+    spec = P.unit_spec((1, H, W, C), blk)
+    algo = residual_unit_algo(torch.bfloat16, u, spec)
+
+    def step(f):
+        idx = P.reduce_mask(masks[f], spec)
+        residual_unit_into(xs[f], xs[f], u, spec, idx)
+
+    def steps(k):
+        for i in range(k):
+            step(i % nf)
+
+    launches0 = _lib.launch_count()
+    g, s = time_graph(torch, steps, args.steps, args.warmup)
+    per_step_launches = None
+    with torch.cuda.stream(s):
+        l0 = _lib.launch_count()
+        step(0)
+        per_step_launches = _lib.launch_count() - l0
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+            e1.synchronize()
+        ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    frames_per_s = world * args.steps / (ms / 1e3)
+
+    # ---- dominant kernel: fused unit alone, CUDA events on its stream, cold frames
+    idx_list = [P.reduce_mask(masks[f], spec) for f in range(nf)]
+    torch.cuda.synchronize()
+    alg_bytes = [unit_bytes(P, spec, idx_list[f].entries) for f in range(nf)]
+    kreps = max(nf, min(args.steps, 400))
+    with torch.cuda.stream(s):
+        for f in range(nf):
+            residual_unit_into(xs[f], xs[f], u, spec, idx_list[f])
+        torch.cuda.synchronize()
+        evs = []
+        for i in range(kreps):
+            f = i % nf
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(s)
+            residual_unit_into(xs[f], xs[f], u, spec, idx_list[f])
+            b_.record(s)
+            evs.append((f, a_, b_))
+        torch.cuda.synchronize()
+    k_ms = sum(a_.elapsed_time(b_) for _, a_, b_ in evs) / kreps
+    k_bytes = sum(alg_bytes[f] for f, _, _ in evs) / kreps
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = k_bytes / (k_ms * 1e-3) / 1e9
+
+    # ---- dense comparator (cuDNN bf16, same frames, CUDA graph)
+    def dense_steps(k):
+        for i in range(k):
+            P.dense_residual_unit(P.Tensor4D(xs[i % nf]), u)
+
+    gd, sd = time_graph(torch, dense_steps, max(nf, args.steps // 10), 3, soak_s=0.2)
+    with torch.cuda.stream(sd):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(sd)
+        gd.replay()
+        e1.record(sd)
+        e1.synchronize()
+    dense_ms = e0.elapsed_time(e1) / max(nf, args.steps // 10)
+
+    # ---- e2e: host (pinned) frame + mask -> public API -> host result, every step
+    ne = min(nf, 4)
+    hx = [xs[f].cpu().pin_memory() for f in range(ne)]
+    hm = [masks[f].data.cpu().pin_memory() for f in range(ne)]
+    hout = torch.empty_like(hx[0]).pin_memory()
+    e2e_steps = max(ne, min(args.steps // 10, 200))
+
+    def e2e_step(f):
+        x = P.Tensor4D(hx[f].to(dev, non_blocking=True))
+        mk = P.BinaryMask(hm[f].to(dev, non_blocking=True), validate=False)
+        y = P.sparse_residual_unit(x, mk, u, blk, inplace=True)
+        hout.copy_(y.data, non_blocking=True)
+
+    for i in range(3):
+        e2e_step(i % ne)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(e2e_steps):
+        e2e_step(i % ne)
+    e1.record()
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- density sweep (sparse vs dense, same protocol, fewer steps)
+    sweep = None
+    if not args.no_sweep and rank == 0:
+        sweep = {}
+        for d in (0.1, 0.3, 0.5, 0.7, 0.9):
+            mk = P.synth_mask_blobs((1, H, W), 1.0 - d, 7).cuda()
+
+            def sp(k, mk=mk):
+                for i in range(k):
+                    idx = P.reduce_mask(mk, spec)
+                    residual_unit_into(xs[i % nf], xs[i % nf], u, spec, idx)
+            gs, ss = time_graph(torch, sp, 200, 5, soak_s=0.05)
+            with torch.cuda.stream(ss):
+                a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(ss)
+                gs.replay()
+                b_.record(ss)
+                b_.synchronize()
+            t_sp = a_.elapsed_time(b_) / 200
+            sweep[f"{d:.1f}"] = {"density_achieved": round(float(mk.data.float().mean()), 4),
+                                 "sparse_ms": round(t_sp, 5), "speedup_vs_dense": round(dense_ms / t_sp, 3)}
+
+    # ---- CPU baseline: the oracle port of the reference's sparse_residual_unit
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_seconds, xs[0], masks[0], u, blk)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(frames_per_s, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 6),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded normal activations, seeded blob masks; random-init unit)",
+            "config": {"workload": "config2: sparse ResNet bottleneck unit (1x1/3x3/1x1), "
+                                   f"N=1 {H}x{W}x{C} BEV frame per step per GPU, c={C} m={M}, "
+                                   f"{args.density:.0%} blob (road-map stand-in) mask, {blk[0]}x{blk[1]} blocks, in-place",
+                       "frames_ring": nf, "ring_bytes": nf * H * W * C * 2,
+                       "l2": "inputs larger than L2 (ring of distinct frames cycled per step)",
+                       "mask_density_achieved": round(sum(dens) / len(dens), 4),
+                       "algo": algo, "parallelism": f"batch-shard x{world}", "cuda_graph": True},
+            "ms_per_step_dense": round(dense_ms, 5),
+            "speedup_vs_dense": round(dense_ms / ms_step, 3),
+            "e2e": {"value": round(world * 1e3 / e2e_ms, 2), "unit": UNIT,
+                    "h2d_bytes_per_step": int(hx[0].numel() * 2 + hm[0].numel()),
+                    "d2h_bytes_per_step": int(hout.numel() * 2)},
+            "gpu_launches": int(per_step_launches * args.steps),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "kernel": f"unit_tc_kernel<{C},{M},{blk[0]}>" if algo == "tcgen05" else "unit_simt_kernel",
+                         "kernel_ms": round(k_ms, 5), "alg_bytes_per_launch": int(k_bytes),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(seconds, x_dev, mask, u, blk):
+    """Oracle port of the reference sparse_residual_unit (numpy, all host threads) on a
+    bounded sample: the same frame repeated until `seconds` elapse."""
+    import numpy as np
+    from oracle import sbnet_oracle as O
+    x = x_dev.float().cpu().numpy()
+    mk = mask.numpy()
+    ud = _oracle_unit(u)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        O.sparse_residual_unit(x, mk, ud, blk)
+        n += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    return {"value": round(n / el, 3), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n} x sparse_residual_unit on one {H}x{W}x{C} frame (fp32, bf16-rounded inputs), {el:.1f}s"}
+
+
+def _oracle_unit(u):
+    ud = {"pre": u.pre_activation}
+    for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
+        ud[f"w{i}"], ud[f"b{i}"] = fb.weights, fb.bias
+        ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
+    return ud
+
+
+def run_reference(args):
+    """Reference arm: the reference's CPU algorithm (oracle port; the reference itself is
+    pure Python and cannot travel to the box) on the host cores, same workload/metric."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    ncores = len(os.sched_getaffinity(0))
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = str(ncores)
+    import numpy as np
+    from oracle import sbnet_oracle as O
+    import paper_1801_02108_b200.perf as perf
+    from paper_1801_02108_b200.layers import random_unit_params
+    u = random_unit_params(np.random.default_rng(0), C, M)
+    ud = _oracle_unit(u)
+    rng = np.random.default_rng(1000)
+    x = rng.standard_normal((1, H, W, C), dtype=np.float32)
+    mk = perf.synth_mask_blobs((1, H, W), 1.0 - args.density, 0).numpy()
+    blk = (args.block, args.block)
+    steps = max(1, min(args.steps, 60))
+    warm = max(1, min(args.warmup, 3))
+    for _ in range(warm):
+        O.sparse_residual_unit(x, mk, ud, blk)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.sparse_residual_unit(x, mk, ud, blk)
+    el = time.perf_counter() - t0
+    v = steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+            "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": steps, "warmup": warm,
+            "ms_per_step": round(el / steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config2: sparse ResNet bottleneck unit, N=1 {H}x{W}x{C}, "
+                                   f"{args.density:.0%} blob mask, {blk[0]}x{blk[1]} blocks (CPU, numpy)"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": ncores, "kind": "port",
+                             "sample": f"{steps} steps (requested {args.steps}, capped at 60 for runtime)"},
+            "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -128,6 +128,12 @@ int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometry* g, int h
 int sbn_sparse_conv_algo(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                          const sbn_geometry* g);
 
+/* Diagnostics: tensor-core descriptor self test.  d[128 x 32] (fp32) =
+ * a[shift:shift+128, 0:32] @ b[0:32, 0:32]^T with a (rows x 32) and b (32 x 32) bf16
+ * row-major, staged in the plane layout with plane stride rows*16 + plane_pad bytes. */
+int sbn_selftest_umma(const void* a, const void* b, int rows, int shift, int plane_pad, float* d,
+                      sbn_stream_t stream);
+
 /* Number of kernels the library has launched since load (for the bench's
  * gpu_launches claim). */
 uint64_t sbn_launch_count(void);

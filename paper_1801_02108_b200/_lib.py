@@ -59,6 +59,7 @@ _PROTOS = {
     "sbn_residual_unit": (_I, [_P, _I, _I, _I, _G, _I, _I, C.POINTER(UnitParams), _P, _P, _I,
                                _P, _P, C.c_size_t, _I, _P]),
     "sbn_residual_unit_algo": (_I, [_I, _I, _I, _G, _I, _I]),
+    "sbn_selftest_umma": (_I, [_P, _P, _I, _I, _I, _P, _P]),
 }
 
 _lib = None

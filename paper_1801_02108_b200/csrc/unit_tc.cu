@@ -1,10 +1,382 @@
-// tcgen05 / TMEM fused residual unit (bf16) — placeholder until the kernel lands.
+// tcgen05 / TMEM fused sparse residual unit (bf16 activations, fp32 accumulate).
+//
+// One persistent CTA (256 threads) walks the active blocks (device-side count).  Per
+// block the bottleneck of reference `_unit_branch` (`layers.py:155-169`, pre-activation)
+// runs as three tensor-core GEMMs whose operands never leave shared memory / TMEM:
+//
+//   stage   : window (BS x BS pixels x C) gathered from x (rim from the snapshot when
+//             in place), BN1 + ReLU applied in registers -> A1 [pixels x C] bf16
+//   GEMM1   : C1[pixels x MC]  = A1 . W1            (UMMA M=128 tiles, N=MC, K=C)
+//   epi 1   : +b1, BN2, ReLU, x in-bounds  -> A2 [pixels x MC] bf16
+//   GEMM2   : C2[q x MC] = sum_taps A2[q + ky*BS + kx] . W2[ky,kx]
+//             (3x3 valid conv as 9 row-shifted views of A2 — "full-width" implicit GEMM:
+//              output row q = oy*BS + ox, columns ox >= BS-2 are computed and dropped)
+//   epi 2   : +b2, BN3, ReLU -> A3 [q x MC] bf16 (aliases A1)
+//   GEMM3   : C3[q x C] = A3 . W3
+//   epi 3   : +b3, + x (residual, this block's own interior) -> out, clipped
+//
+// Operands use the K-major SWIZZLE_NONE plane layout of tc_util.cuh; plane strides are
+// padded by 16 B so the 16-byte staging stores of 8 consecutive threads hit 8 distinct
+// bank groups.  Accumulators live in TMEM (tcgen05.ld in the epilogues); MMAs are
+// issued by one thread and completion is signalled through an mbarrier
+// (tcgen05.commit).  Two CTAs per SM overlap one block's global traffic with the other's
+// tensor-core work.
 #include "unit.cuh"
+#include "tc_util.cuh"
+
 namespace sbn {
-bool unit_tc_supported(int, int, int, const Geo&, int, int) { return false; }
-int unit_tc_launch(const void*, void*, const void*, int, int, const Geo&, const sbn_unit_params*,
-                   const int32_t*, const int32_t*, int, cudaStream_t) {
-  set_error("tcgen05 residual unit not built");
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int C, int MC, int BS>
+struct Cfg {
+  static_assert(C % 16 == 0 && MC % 16 == 0 && C <= 256 && MC <= 256, "channel constraints");
+  static constexpr int NPIX = BS * BS;
+  static constexpr int NT1 = (NPIX + 127) / 128;
+  static constexpr int NQ = (BS - 2) * BS;
+  static constexpr int NT2 = (NQ + 127) / 128;
+  static constexpr int R1 = NT1 * 128;
+  static constexpr int R2a = NT2 * 128 + 2 * BS + 2;
+  static constexpr int R2 = (((R2a > R1 ? R2a : R1) + 7) / 8) * 8;
+  static constexpr int R3 = NT2 * 128;
+  static constexpr int PAD = 16;
+  static constexpr int P1 = R1 * 16 + PAD;   // A1 plane stride
+  static constexpr int P2 = R2 * 16 + PAD;   // A2 plane stride
+  static constexpr int P3 = R3 * 16 + PAD;   // A3 plane stride (aliases A1)
+  static constexpr int PB1 = MC * 16;        // W1^T: MC rows, K = C
+  static constexpr int PB2 = MC * 16;        // W2^T per tap: MC rows, K = MC
+  static constexpr int TAPB = (MC / 8) * PB2;
+  static constexpr int PB3 = C * 16;         // W3^T: C rows, K = MC
+  static constexpr int al(int v) { return (v + 127) / 128 * 128; }
+  static constexpr int SZ_A1 = al((C / 8) * P1 > (MC / 8) * P3 ? (C / 8) * P1 : (MC / 8) * P3);
+  static constexpr int SZ_A2 = al((MC / 8) * P2);
+  static constexpr int SZ_B1 = al((C / 8) * PB1);
+  static constexpr int SZ_B2 = al(9 * TAPB);
+  static constexpr int SZ_B3 = al((MC / 8) * PB3);
+  static constexpr int NPAR = 4 * C + 6 * MC;  // s1 t1 b3 + b1 s2 t2 b2 s3 t3 (floats)
+  static constexpr int OFF_A2 = SZ_A1;
+  static constexpr int OFF_B1 = OFF_A2 + SZ_A2;
+  static constexpr int OFF_B2 = OFF_B1 + SZ_B1;
+  static constexpr int OFF_B3 = OFF_B2 + SZ_B2;
+  static constexpr int OFF_PAR = OFF_B3 + SZ_B3;
+  static constexpr int SMEM = OFF_PAR + al(NPAR * 4);
+  static constexpr int COL1 = 0;
+  static constexpr int COL2 = NT1 * MC;
+  static constexpr int COL3 = COL2 + NT2 * MC;
+  static constexpr int TCOLS = COL3 + NT2 * C;
+  static_assert(TCOLS <= 512, "TMEM budget");
+  static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+  static constexpr int OCC = (SMEM <= 110 * 1024 && TALLOC <= 256) ? 2 : 1;
+};
+
+struct TcArgs {
+  const __nv_bfloat16* x;
+  __nv_bfloat16* out;
+  const __nv_bfloat16* rim;
+  Geo g;
+  const __nv_bfloat16 *w1, *b1, *w2, *b2, *w3, *b3;
+  const float *s1, *t1, *s2, *t2, *s3, *t3;
+  const int32_t* idx;
+  const int32_t* count;
+  int cap;
+};
+
+__device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+template <int C, int MC, int BS>
+__global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(TcArgs a) {
+  using K = Cfg<C, MC, BS>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* A1 = smem;
+  uint8_t* A2 = smem + K::OFF_A2;
+  uint8_t* A3 = smem;  // alias: A1 is dead once GEMM1 has completed
+  uint8_t* B1 = smem + K::OFF_B1;
+  uint8_t* B2 = smem + K::OFF_B2;
+  uint8_t* B3 = smem + K::OFF_B3;
+  float* par = reinterpret_cast<float*>(smem + K::OFF_PAR);
+  float* s1 = par;
+  float* t1 = s1 + C;
+  float* b3 = t1 + C;
+  float* b1 = b3 + C;
+  float* s2 = b1 + MC;
+  float* t2 = s2 + MC;
+  float* b2 = t2 + MC;
+  float* s3 = b2 + MC;
+  float* t3 = s3 + MC;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Geo& g = a.g;
+
+  // ---- prologue: weights -> smem (transposed into the K-major plane layout), params
+  for (int i = tid; i < C * MC; i += kThreads) {  // W1 [ci][j] -> B1[ci/8][j][ci%8]
+    const int ci = i / MC, j = i % MC;
+    *reinterpret_cast<__nv_bfloat16*>(B1 + (ci / 8) * K::PB1 + j * 16 + (ci % 8) * 2) = a.w1[i];
+  }
+  for (int i = tid; i < 9 * MC * MC; i += kThreads) {  // W2 [tap][ci][j] -> B2[tap][ci/8][j][ci%8]
+    const int tap = i / (MC * MC), r = i % (MC * MC), ci = r / MC, j = r % MC;
+    *reinterpret_cast<__nv_bfloat16*>(B2 + tap * K::TAPB + (ci / 8) * K::PB2 + j * 16 + (ci % 8) * 2) =
+        a.w2[i];
+  }
+  for (int i = tid; i < MC * C; i += kThreads) {  // W3 [j][co] -> B3[j/8][co][j%8]
+    const int j = i / C, co = i % C;
+    *reinterpret_cast<__nv_bfloat16*>(B3 + (j / 8) * K::PB3 + co * 16 + (j % 8) * 2) = a.w3[i];
+  }
+  for (int i = tid; i < C; i += kThreads) {
+    s1[i] = a.s1[i];
+    t1[i] = a.t1[i];
+    b3[i] = bf(a.b3 + i);
+  }
+  for (int i = tid; i < MC; i += kThreads) {
+    b1[i] = bf(a.b1 + i);
+    s2[i] = a.s2[i];
+    t2[i] = a.t2[i];
+    b2[i] = bf(a.b2 + i);
+    s3[i] = a.s3[i];
+    t3[i] = a.t3[i];
+  }
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<K::TALLOC>(&tslot);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  uint32_t phase = 0;
+
+  const Rim rim{BS, BS, 1};
+  const int P = rim.pixels();
+  const int B = ld_count(a.count, a.cap);
+  const int q = warp & 3;           // TMEM lane quarter of this warp
+  const int tpar = warp >> 2;       // tile parity handled by this warp
+
+  for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
+    const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+    const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+
+    // ---- 1. stage the window: BN1 + ReLU, bf16, plane layout
+    for (int i = tid; i < K::NPIX * (C / 8); i += kThreads) {
+      const int p = i / (C / 8), k = i % (C / 8);
+      const int wy = p / BS, wx = p % BS;
+      const int y = ys + wy, xx = xs + wx;
+      uint4 raw = make_uint4(0, 0, 0, 0);
+      if (a.rim && !rim.interior(wy, wx)) {
+        raw = __ldg(reinterpret_cast<const uint4*>(a.rim) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
+      } else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w) {
+        raw = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
+      }
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        const int ch = k * 8 + 2 * e;
+        const float v0 = fmaxf(__fadd_rn(__fmul_rn(f.x, s1[ch]), t1[ch]), 0.f);
+        const float v1 = fmaxf(__fadd_rn(__fmul_rn(f.y, s1[ch + 1]), t1[ch + 1]), 0.f);
+        o[e] = tc::pack_bf16(v0, v1);
+      }
+      *reinterpret_cast<uint4*>(A1 + k * K::P1 + p * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+
+    // ---- 2. GEMM1: C1 = A1 . W1
+    if (tid == 0) {
+      tc::fence_after();
+      constexpr uint32_t id1 = tc::idesc_bf16_f32(128, MC);
+#pragma unroll
+      for (int t = 0; t < K::NT1; ++t)
+#pragma unroll
+        for (int k = 0; k < C / 16; ++k)
+          tc::mma_bf16(tmem + K::COL1 + t * MC,
+                       tc::desc_kmajor_noswz(tc::smem_u32(A1 + 2 * k * K::P1 + t * 128 * 16), K::P1, 128),
+                       tc::desc_kmajor_noswz(tc::smem_u32(B1 + 2 * k * K::PB1), K::PB1, 128), id1, k > 0);
+      tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+
+    // ---- 3. epilogue 1: +b1, BN2, ReLU, x in-bounds -> A2
+    for (int t = tpar; t < K::NT1; t += 2) {
+      const int r = t * 128 + q * 32 + lane;
+      const int wy = r / BS, wx = r % BS;
+      const int y = ys + wy, xx = xs + wx;
+      const bool valid = r < K::NPIX && y >= 0 && y < g.h && xx >= 0 && xx < g.w;
+#pragma unroll
+      for (int c0 = 0; c0 < MC; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + K::COL1 + t * MC + c0, v);
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b1[c0 + 2 * e]));
+          float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b1[c0 + 2 * e + 1]));
+          u0 = fmaxf(__fadd_rn(__fmul_rn(u0, s2[c0 + 2 * e]), t2[c0 + 2 * e]), 0.f);
+          u1 = fmaxf(__fadd_rn(__fmul_rn(u1, s2[c0 + 2 * e + 1]), t2[c0 + 2 * e + 1]), 0.f);
+          o[e] = valid ? tc::pack_bf16(u0, u1) : 0u;
+        }
+        *reinterpret_cast<uint4*>(A2 + (c0 / 8) * K::P2 + r * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(A2 + (c0 / 8 + 1) * K::P2 + r * 16) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+    tc::fence_before();
+    tc::fence_async_smem();
+    __syncthreads();
+
+    // ---- 4. GEMM2: 3x3 valid conv as 9 row-shifted views of A2
+    if (tid == 0) {
+      tc::fence_after();
+      constexpr uint32_t id2 = tc::idesc_bf16_f32(128, MC);
+#pragma unroll
+      for (int t = 0; t < K::NT2; ++t)
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) {
+          const int shift = (tap / 3) * BS + (tap % 3);
+#pragma unroll
+          for (int k = 0; k < MC / 16; ++k)
+            tc::mma_bf16(tmem + K::COL2 + t * MC,
+                         tc::desc_kmajor_noswz(tc::smem_u32(A2 + 2 * k * K::P2 + (t * 128 + shift) * 16), K::P2, 128),
+                         tc::desc_kmajor_noswz(tc::smem_u32(B2 + tap * K::TAPB + 2 * k * K::PB2), K::PB2, 128),
+                         id2, (tap | k) > 0);
+        }
+      tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+
+    // ---- 5. epilogue 2: +b2, BN3, ReLU -> A3
+    for (int t = tpar; t < K::NT2; t += 2) {
+      const int r = t * 128 + q * 32 + lane;
+#pragma unroll
+      for (int c0 = 0; c0 < MC; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + K::COL2 + t * MC + c0, v);
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b2[c0 + 2 * e]));
+          float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b2[c0 + 2 * e + 1]));
+          u0 = fmaxf(__fadd_rn(__fmul_rn(u0, s3[c0 + 2 * e]), t3[c0 + 2 * e]), 0.f);
+          u1 = fmaxf(__fadd_rn(__fmul_rn(u1, s3[c0 + 2 * e + 1]), t3[c0 + 2 * e + 1]), 0.f);
+          o[e] = tc::pack_bf16(u0, u1);
+        }
+        *reinterpret_cast<uint4*>(A3 + (c0 / 8) * K::P3 + r * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(A3 + (c0 / 8 + 1) * K::P3 + r * 16) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+    tc::fence_before();
+    tc::fence_async_smem();
+    __syncthreads();
+
+    // ---- 6. GEMM3: C3 = A3 . W3
+    if (tid == 0) {
+      tc::fence_after();
+      constexpr uint32_t id3 = tc::idesc_bf16_f32(128, C);
+#pragma unroll
+      for (int t = 0; t < K::NT2; ++t)
+#pragma unroll
+        for (int k = 0; k < MC / 16; ++k)
+          tc::mma_bf16(tmem + K::COL3 + t * C,
+                       tc::desc_kmajor_noswz(tc::smem_u32(A3 + 2 * k * K::P3 + t * 128 * 16), K::P3, 128),
+                       tc::desc_kmajor_noswz(tc::smem_u32(B3 + 2 * k * K::PB3), K::PB3, 128), id3, k > 0);
+      tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+
+    // ---- 7. epilogue 3: +b3, + residual, store the block's clipped output window
+    for (int t = tpar; t < K::NT2; t += 2) {
+      const int r = t * 128 + q * 32 + lane;
+      const int oy = r / BS, ox = r % BS;
+      const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+      const bool store = oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow;
+      uint4* op = reinterpret_cast<uint4*>(a.out) + (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (C / 8);
+#pragma unroll 1
+      for (int c0 = 0; c0 < C; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + K::COL3 + t * C + c0, v);
+        if (store) {
+          uint4 xr[2] = {op[c0 / 8], op[c0 / 8 + 1]};
+          const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(xr);
+          uint32_t o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float2 xf = __bfloat1622float2(xh[e]);
+            const float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b3[c0 + 2 * e]));
+            const float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b3[c0 + 2 * e + 1]));
+            o[e] = tc::pack_bf16(__fadd_rn(xf.x, u0), __fadd_rn(xf.y, u1));
+          }
+          op[c0 / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+          op[c0 / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+  }
+
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
+}
+
+template <int C, int MC, int BS>
+int launch(const TcArgs& a, int cap, cudaStream_t s) {
+  using K = Cfg<C, MC, BS>;
+  auto kern = unit_tc_kernel<C, MC, BS>;
+  static bool attr = false;  // per-instantiation; attribute is per-function, idempotent
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    attr = true;
+  }
+  kern<<<persistent_grid(cap, K::OCC), kThreads, K::SMEM, s>>>(a);
+  return launch_status("residual_unit_tcgen05");
+}
+
+#define SBN_UNIT_TC_CONFIGS(X) \
+  X(64, 32, 16)                \
+  X(64, 32, 8)                 \
+  X(64, 64, 16)                \
+  X(128, 64, 16)               \
+  X(32, 16, 16)
+
+}  // namespace
+
+bool unit_tc_supported(int dtype, int c, int m, const Geo& g, int halo, int pre_act) {
+  if (dtype != SBN_BF16 || halo != 1 || !pre_act || g.bh != g.bw) return false;
+#define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_ && Cfg<C_, M_, B_>::SMEM <= max_smem_optin()) return true;
+  SBN_UNIT_TC_CONFIGS(X)
+#undef X
+  return false;
+}
+
+int unit_tc_launch(const void* x, void* out, const void* rim, int c, int m, const Geo& g,
+                   const sbn_unit_params* p, const int32_t* idx, const int32_t* count, int cap,
+                   cudaStream_t s) {
+  TcArgs a;
+  a.x = (const __nv_bfloat16*)x;
+  a.out = (__nv_bfloat16*)out;
+  a.rim = (const __nv_bfloat16*)rim;
+  a.g = g;
+  a.w1 = (const __nv_bfloat16*)p->w1; a.b1 = (const __nv_bfloat16*)p->b1;
+  a.w2 = (const __nv_bfloat16*)p->w2; a.b2 = (const __nv_bfloat16*)p->b2;
+  a.w3 = (const __nv_bfloat16*)p->w3; a.b3 = (const __nv_bfloat16*)p->b3;
+  a.s1 = (const float*)p->bn1_scale; a.t1 = (const float*)p->bn1_shift;
+  a.s2 = (const float*)p->bn2_scale; a.t2 = (const float*)p->bn2_shift;
+  a.s3 = (const float*)p->bn3_scale; a.t3 = (const float*)p->bn3_shift;
+  a.idx = idx; a.count = count; a.cap = cap;
+#define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_) return launch<C_, M_, B_>(a, cap, s);
+  SBN_UNIT_TC_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 residual-unit instantiation for c=%d m=%d block=%d", c, m, g.bh);
   return SBN_ERR_UNSUPPORTED;
 }
+
 }  // namespace sbn

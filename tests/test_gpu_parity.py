@@ -366,3 +366,22 @@ def test_stage_of_one_unit_equals_single_sparse_unit(cuda_device):
 
 def test_library_kernels_were_launched(cuda_device):
     assert _lib.launch_count() > 0
+
+
+@pytest.mark.parametrize("shift,pad", [(0, 0), (1, 0), (5, 0), (34, 0), (0, 16), (3, 16), (17, 48)])
+def test_umma_plane_descriptor_selftest(cuda_device, shift, pad):
+    """tcgen05 descriptors over the plane layout: row-shifted A views and padded plane
+    strides (what the fused kernels use for 3x3 taps and bank-conflict-free staging)."""
+    import ctypes
+    rows = ((128 + shift + 7) // 8) * 8
+    g = torch.Generator().manual_seed(shift * 7 + pad)
+    a = torch.randn(rows, 32, generator=g).bfloat16().cuda()
+    b = torch.randn(32, 32, generator=g).bfloat16().cuda()
+    d = torch.empty(128, 32, device="cuda")
+    lib = _lib.load()
+    st = lib.sbn_selftest_umma(a.data_ptr(), b.data_ptr(), rows, shift, pad, d.data_ptr(),
+                               _lib.stream_handle())
+    _lib.check(st, "selftest")
+    ref = a[shift:shift + 128].float() @ b.float().t()
+    torch.cuda.synchronize()
+    assert torch.allclose(d, ref, rtol=1e-3, atol=1e-3), (d - ref).abs().max()
