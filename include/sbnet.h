@@ -70,6 +70,9 @@ typedef struct sbn_unit_params {
   const void* bn1_scale; const void* bn1_shift;
   const void* bn2_scale; const void* bn2_shift;
   const void* bn3_scale; const void* bn3_shift;
+  /* optional: pre-packed tensor-core image from sbn_residual_unit_pack (NULL: the call
+   * packs into its workspace first, one extra launch) */
+  const void* tc_packed;
 } sbn_unit_params;
 
 const char* sbn_version(void);
@@ -122,6 +125,15 @@ int sbn_residual_unit(const void* x, int dtype, int c, int m, const sbn_geometry
                       int pre_act, const sbn_unit_params* p, const int32_t* idx,
                       const int32_t* count, int cap, void* out, void* ws, size_t ws_bytes,
                       int algo, sbn_stream_t stream);
+
+/* Tensor-core weight image: W1/W2/W3 transposed into the kernel's shared-memory operand
+ * layout plus the folded BN/bias vectors, built once per parameter set and block size
+ * and bulk-copied by every CTA.  bytes == 0: the tcgen05 path does not apply. */
+size_t sbn_residual_unit_packed_bytes(int dtype, int c, int m, const sbn_geometry* g, int halo,
+                                      int pre_act);
+int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
+                           const sbn_geometry* g, int halo, int pre_act, void* packed,
+                           sbn_stream_t stream);
 
 /* Which algorithm `algo=AUTO` would pick (SBN_ALGO_SIMT / SBN_ALGO_TCGEN05). */
 int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometry* g, int halo, int pre_act);

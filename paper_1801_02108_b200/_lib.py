@@ -34,7 +34,7 @@ class Geometry(C.Structure):
 class UnitParams(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in (
         "w1", "b1", "w2", "b2", "w3", "b3", "bn1_scale", "bn1_shift", "bn2_scale",
-        "bn2_shift", "bn3_scale", "bn3_shift")]
+        "bn2_shift", "bn3_scale", "bn3_shift", "tc_packed")]
 
 
 _P = C.c_void_p
@@ -60,6 +60,8 @@ _PROTOS = {
                                _P, _P, C.c_size_t, _I, _P]),
     "sbn_residual_unit_algo": (_I, [_I, _I, _I, _G, _I, _I]),
     "sbn_selftest_umma": (_I, [_P, _P, _I, _I, _I, _P, _P]),
+    "sbn_residual_unit_packed_bytes": (C.c_size_t, [_I, _I, _I, _G, _I, _I]),
+    "sbn_residual_unit_pack": (_I, [C.POINTER(UnitParams), _I, _I, _I, _G, _I, _I, _P, _P]),
 }
 
 _lib = None

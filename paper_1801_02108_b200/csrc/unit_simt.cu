@@ -249,6 +249,7 @@ size_t unit_workspace(int dtype, int c, int m, const Geo& g, int halo, int algo,
   const int es = dtype_size(dtype);
   const int cap = g.n * g.gy * g.gx;
   size_t ws = rim_bytes(es, c, g, halo, cap);  // rim snapshot for in-place calls
+  if (tc) ws += align_up(unit_tc_packed_bytes(c, m, g), 256);  // packing when no image given
   if (!tc) {
     const size_t ae = dtype == SBN_F64 ? 8 : 4;
     const size_t per = simt_scratch_elems<float>(c, m, g) * ae;
@@ -267,6 +268,25 @@ extern "C" int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometr
   if (!gp) return SBN_ALGO_SIMT;
   return unit_tc_supported(dtype, c, m, to_geo(gp), halo, pre_act) ? SBN_ALGO_TCGEN05
                                                                    : SBN_ALGO_SIMT;
+}
+
+extern "C" size_t sbn_residual_unit_packed_bytes(int dtype, int c, int m, const sbn_geometry* gp,
+                                                 int halo, int pre_act) {
+  if (!gp) return 0;
+  Geo g = to_geo(gp);
+  return unit_tc_supported(dtype, c, m, g, halo, pre_act) ? unit_tc_packed_bytes(c, m, g) : 0;
+}
+
+extern "C" int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
+                                      const sbn_geometry* gp, int halo, int pre_act, void* packed,
+                                      sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  Geo g = to_geo(gp);
+  SBN_CHECK_ARG(unit_tc_supported(dtype, c, m, g, halo, pre_act), SBN_ERR_UNSUPPORTED,
+                "tcgen05 residual unit does not support this config");
+  SBN_CHECK_ARG(p && packed, SBN_ERR_INVALID, "null argument");
+  return unit_tc_pack(p, c, m, g, packed, (cudaStream_t)stream);
 }
 
 extern "C" size_t sbn_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* gp,
@@ -313,7 +333,17 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
     if (st) return st;
     rim = wsb;
   }
-  if (use_tc) return unit_tc_launch(x, out, rim, c, m, g, p, idx, count, cap, s);
+  if (use_tc) {
+    const void* packed = p->tc_packed;
+    if (!packed) {
+      SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
+                    "residual unit needs a %zu-byte workspace", need);
+      st = unit_tc_pack(p, c, m, g, wsb + rb, s);
+      if (st) return st;
+      packed = wsb + rb;
+    }
+    return unit_tc_launch(x, out, rim, c, m, g, p, packed, idx, count, cap, s);
+  }
   void* scratch = nullptr;
   if (need > rb) {
     SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,

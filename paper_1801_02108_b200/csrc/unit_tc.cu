@@ -77,6 +77,7 @@ struct TcArgs {
   Geo g;
   const __nv_bfloat16 *w1, *b1, *w2, *b2, *w3, *b3;
   const float *s1, *t1, *s2, *t2, *s3, *t3;
+  const uint8_t* packed;  // smem image of [B1 | B2 | B3 | params] (unit_tc_pack)
   const int32_t* idx;
   const int32_t* count;
   int cap;
@@ -110,48 +111,33 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Geo& g = a.g;
 
-  // ---- prologue: weights -> smem (transposed into the K-major plane layout), params
-  for (int i = tid; i < C * MC; i += kThreads) {  // W1 [ci][j] -> B1[ci/8][j][ci%8]
-    const int ci = i / MC, j = i % MC;
-    *reinterpret_cast<__nv_bfloat16*>(B1 + (ci / 8) * K::PB1 + j * 16 + (ci % 8) * 2) = a.w1[i];
-  }
-  for (int i = tid; i < 9 * MC * MC; i += kThreads) {  // W2 [tap][ci][j] -> B2[tap][ci/8][j][ci%8]
-    const int tap = i / (MC * MC), r = i % (MC * MC), ci = r / MC, j = r % MC;
-    *reinterpret_cast<__nv_bfloat16*>(B2 + tap * K::TAPB + (ci / 8) * K::PB2 + j * 16 + (ci % 8) * 2) =
-        a.w2[i];
-  }
-  for (int i = tid; i < MC * C; i += kThreads) {  // W3 [j][co] -> B3[j/8][co][j%8]
-    const int j = i / C, co = i % C;
-    *reinterpret_cast<__nv_bfloat16*>(B3 + (j / 8) * K::PB3 + co * 16 + (j % 8) * 2) = a.w3[i];
-  }
-  for (int i = tid; i < C; i += kThreads) {
-    s1[i] = a.s1[i];
-    t1[i] = a.t1[i];
-    b3[i] = bf(a.b3 + i);
-  }
-  for (int i = tid; i < MC; i += kThreads) {
-    b1[i] = bf(a.b1 + i);
-    s2[i] = a.s2[i];
-    t2[i] = a.t2[i];
-    b2[i] = bf(a.b2 + i);
-    s3[i] = a.s3[i];
-    t3[i] = a.t3[i];
-  }
+  const int B = ld_count(a.count, a.cap);
+  if ((int)blockIdx.x >= B) return;  // no block for this CTA: skip weights and TMEM
+
+  // ---- prologue: one bulk (TMA) copy of the pre-packed weight/param image; it lands
+  //      while the first window is being loaded
+  __shared__ uint64_t wbar;
   if (tid == 0) {
     tc::mbar_init(&bar, 1);
+    tc::mbar_init(&wbar, 1);
     tc::mbar_fence_init();
   }
+  __syncthreads();
+  if (tid == 0) {
+    constexpr uint32_t bytes = K::SMEM - K::OFF_B1;
+    tc::mbar_expect_tx(&wbar, bytes);
+    tc::bulk_g2s(B1, a.packed, bytes, &wbar);
+  }
   if (warp == 0) tc::tmem_alloc<K::TALLOC>(&tslot);
-  tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tslot;
   uint32_t phase = 0;
+  bool weights_ready = false;
 
   const Rim rim{BS, BS, 1};
   const int P = rim.pixels();
-  const int B = ld_count(a.count, a.cap);
   const int q = warp & 3;           // TMEM lane quarter of this warp
   const int tpar = warp >> 2;       // tile parity handled by this warp
 
@@ -159,18 +145,34 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
 
-    // ---- 1. stage the window: BN1 + ReLU, bf16, plane layout
-    for (int i = tid; i < K::NPIX * (C / 8); i += kThreads) {
+    // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
+    constexpr int TOT = K::NPIX * (C / 8);
+    constexpr int ITEMS = (TOT + kThreads - 1) / kThreads;
+    uint4 raw[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int i = tid + it * kThreads;
       const int p = i / (C / 8), k = i % (C / 8);
       const int wy = p / BS, wx = p % BS;
       const int y = ys + wy, xx = xs + wx;
-      uint4 raw = make_uint4(0, 0, 0, 0);
-      if (a.rim && !rim.interior(wy, wx)) {
-        raw = __ldg(reinterpret_cast<const uint4*>(a.rim) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
-      } else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w) {
-        raw = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
+      raw[it] = make_uint4(0, 0, 0, 0);
+      if (i < TOT) {
+        if (a.rim && !rim.interior(wy, wx))
+          raw[it] = __ldg(reinterpret_cast<const uint4*>(a.rim) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
+        else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+          raw[it] = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
       }
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+    }
+    if (!weights_ready) {
+      tc::mbar_wait(&wbar, 0);
+      weights_ready = true;
+    }
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int i = tid + it * kThreads;
+      if (i >= TOT) break;
+      const int p = i / (C / 8), k = i % (C / 8);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[it]);
       uint32_t o[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -251,7 +253,20 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     phase ^= 1;
     tc::fence_after();
 
-    // ---- 5. epilogue 2: +b2, BN3, ReLU -> A3
+    // ---- 5. epilogue 2: +b2, BN3, ReLU -> A3; prefetch this row's residual (x at the
+    //      output pixel) so its latency hides under GEMM3
+    constexpr bool kPrefetch = K::NT2 <= 2;
+    uint4 res[kPrefetch ? C / 8 : 1];
+    if (kPrefetch && tpar < K::NT2) {
+      const int r = tpar * 128 + q * 32 + lane;
+      const int oy = r / BS, ox = r % BS;
+      const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+      if (oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow) {
+        const uint4* op = reinterpret_cast<const uint4*>(a.out) + (((size_t)n * g.oh + Y) * g.ow + X) * (C / 8);
+#pragma unroll
+        for (int k = 0; k < (kPrefetch ? C / 8 : 1); ++k) res[k] = op[k];
+      }
+    }
     for (int t = tpar; t < K::NT2; t += 2) {
       const int r = t * 128 + q * 32 + lane;
 #pragma unroll
@@ -299,12 +314,19 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
       const int Y = by * g.obh + oy, X = bx * g.obw + ox;
       const bool store = oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow;
       uint4* op = reinterpret_cast<uint4*>(a.out) + (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (C / 8);
-#pragma unroll 1
+#pragma unroll
       for (int c0 = 0; c0 < C; c0 += 16) {
         float v[16];
         tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + K::COL3 + t * C + c0, v);
         if (store) {
-          uint4 xr[2] = {op[c0 / 8], op[c0 / 8 + 1]};
+          uint4 xr[2];
+          if constexpr (kPrefetch) {
+            xr[0] = res[c0 / 8];
+            xr[1] = res[c0 / 8 + 1];
+          } else {
+            xr[0] = op[c0 / 8];
+            xr[1] = op[c0 / 8 + 1];
+          }
           const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(xr);
           uint32_t o[8];
 #pragma unroll
@@ -325,6 +347,66 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
   tc::fence_after();
   if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
+}
+
+// Pre-pack W1/W2/W3 (transposed into the K-major plane layout) and the float params into
+// the exact shared-memory image the kernel bulk-copies in its prologue.
+template <int C, int MC, int BS>
+__global__ void unit_tc_pack_kernel(TcArgs a, uint8_t* __restrict__ img) {
+  using K = Cfg<C, MC, BS>;
+  uint8_t* B1 = img;
+  uint8_t* B2 = img + (K::OFF_B2 - K::OFF_B1);
+  uint8_t* B3 = img + (K::OFF_B3 - K::OFF_B1);
+  float* par = reinterpret_cast<float*>(img + (K::OFF_PAR - K::OFF_B1));
+  const int stride = gridDim.x * blockDim.x;
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = t0; i < (K::SMEM - K::OFF_B1) / 4; i += stride) reinterpret_cast<uint32_t*>(img)[i] = 0u;
+  __syncthreads();  // single-CTA launch: zero fill before the scatter below
+  for (int i = t0; i < C * MC; i += stride) {
+    const int ci = i / MC, j = i % MC;
+    *reinterpret_cast<__nv_bfloat16*>(B1 + (ci / 8) * K::PB1 + j * 16 + (ci % 8) * 2) = a.w1[i];
+  }
+  for (int i = t0; i < 9 * MC * MC; i += stride) {
+    const int tap = i / (MC * MC), r = i % (MC * MC), ci = r / MC, j = r % MC;
+    *reinterpret_cast<__nv_bfloat16*>(B2 + tap * K::TAPB + (ci / 8) * K::PB2 + j * 16 + (ci % 8) * 2) = a.w2[i];
+  }
+  for (int i = t0; i < MC * C; i += stride) {
+    const int j = i / C, co = i % C;
+    *reinterpret_cast<__nv_bfloat16*>(B3 + (j / 8) * K::PB3 + co * 16 + (j % 8) * 2) = a.w3[i];
+  }
+  float* s1 = par;
+  float* t1 = s1 + C;
+  float* b3 = t1 + C;
+  float* b1 = b3 + C;
+  float* s2 = b1 + MC;
+  float* t2 = s2 + MC;
+  float* b2 = t2 + MC;
+  float* s3 = b2 + MC;
+  float* t3 = s3 + MC;
+  for (int i = t0; i < C; i += stride) {
+    s1[i] = a.s1[i];
+    t1[i] = a.t1[i];
+    b3[i] = bf(a.b3 + i);
+  }
+  for (int i = t0; i < MC; i += stride) {
+    b1[i] = bf(a.b1 + i);
+    s2[i] = a.s2[i];
+    t2[i] = a.t2[i];
+    b2[i] = bf(a.b2 + i);
+    s3[i] = a.s3[i];
+    t3[i] = a.t3[i];
+  }
+}
+
+template <int C, int MC, int BS>
+int pack(const TcArgs& a, void* img, cudaStream_t s) {
+  unit_tc_pack_kernel<C, MC, BS><<<1, 1024, 0, s>>>(a, (uint8_t*)img);
+  return launch_status("residual_unit_tc_pack");
+}
+
+template <int C, int MC, int BS>
+size_t packed_bytes() {
+  return (size_t)(Cfg<C, MC, BS>::SMEM - Cfg<C, MC, BS>::OFF_B1);
 }
 
 template <int C, int MC, int BS>
@@ -357,9 +439,15 @@ bool unit_tc_supported(int dtype, int c, int m, const Geo& g, int halo, int pre_
   return false;
 }
 
-int unit_tc_launch(const void* x, void* out, const void* rim, int c, int m, const Geo& g,
-                   const sbn_unit_params* p, const int32_t* idx, const int32_t* count, int cap,
-                   cudaStream_t s) {
+size_t unit_tc_packed_bytes(int c, int m, const Geo& g) {
+#define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_) return packed_bytes<C_, M_, B_>();
+  SBN_UNIT_TC_CONFIGS(X)
+#undef X
+  return 0;
+}
+
+static TcArgs make_args(const void* x, void* out, const void* rim, const Geo& g,
+                        const sbn_unit_params* p, const int32_t* idx, const int32_t* count, int cap) {
   TcArgs a;
   a.x = (const __nv_bfloat16*)x;
   a.out = (__nv_bfloat16*)out;
@@ -371,7 +459,25 @@ int unit_tc_launch(const void* x, void* out, const void* rim, int c, int m, cons
   a.s1 = (const float*)p->bn1_scale; a.t1 = (const float*)p->bn1_shift;
   a.s2 = (const float*)p->bn2_scale; a.t2 = (const float*)p->bn2_shift;
   a.s3 = (const float*)p->bn3_scale; a.t3 = (const float*)p->bn3_shift;
+  a.packed = (const uint8_t*)p->tc_packed;
   a.idx = idx; a.count = count; a.cap = cap;
+  return a;
+}
+
+int unit_tc_pack(const sbn_unit_params* p, int c, int m, const Geo& g, void* img, cudaStream_t s) {
+  TcArgs a = make_args(nullptr, nullptr, nullptr, g, p, nullptr, nullptr, 0);
+#define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_) return pack<C_, M_, B_>(a, img, s);
+  SBN_UNIT_TC_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 residual-unit instantiation for c=%d m=%d block=%d", c, m, g.bh);
+  return SBN_ERR_UNSUPPORTED;
+}
+
+int unit_tc_launch(const void* x, void* out, const void* rim, int c, int m, const Geo& g,
+                   const sbn_unit_params* p, const void* packed, const int32_t* idx,
+                   const int32_t* count, int cap, cudaStream_t s) {
+  TcArgs a = make_args(x, out, rim, g, p, idx, count, cap);
+  a.packed = (const uint8_t*)packed;
 #define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_) return launch<C_, M_, B_>(a, cap, s);
   SBN_UNIT_TC_CONFIGS(X)
 #undef X

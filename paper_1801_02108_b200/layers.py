@@ -163,8 +163,10 @@ class ResidualUnitParams:
     def mid_channels(self) -> int:
         return self.conv1.c_out
 
-    def c_params(self, dtype: torch.dtype, device):
-        """(UnitParams struct, keep-alive tensors) for the C-ABI, cached per dtype/device."""
+    def c_params(self, dtype: torch.dtype, device, geometry=None, halo: int = 1):
+        """UnitParams struct for the C-ABI (device tensors kept alive in the cache).  With
+        a geometry on the tcgen05 path, the packed tensor-core weight image is built once
+        (sbn_residual_unit_pack) and attached."""
         key = (dtype, str(device))
         if key not in self._cache:
             keep = []
@@ -181,8 +183,30 @@ class ResidualUnitParams:
                 keep += [s, t]
                 setattr(up, f"bn{i}_scale", s.data_ptr())
                 setattr(up, f"bn{i}_shift", t.data_ptr())
+            up.tc_packed = None
             self._cache[key] = (up, keep)
-        return self._cache[key][0]
+        base = self._cache[key][0]
+        if geometry is None:
+            return base
+        lib = _lib.load()
+        gkey = key + (geometry.bh, geometry.bw, halo)
+        if gkey not in self._cache:
+            nb = lib.sbn_residual_unit_packed_bytes(dtype_code(dtype), self.channels, self.mid_channels,
+                                                    C.byref(geometry), halo, int(self.pre_activation))
+            if nb == 0:
+                self._cache[gkey] = (base, None)
+            else:
+                img = torch.empty(nb, dtype=torch.uint8, device=device)
+                st = lib.sbn_residual_unit_pack(C.byref(base), dtype_code(dtype), self.channels,
+                                                self.mid_channels, C.byref(geometry), halo,
+                                                int(self.pre_activation), img.data_ptr(),
+                                                _lib.stream_handle(device))
+                _lib.check(st, "residual_unit_pack")
+                up = _lib.UnitParams()
+                C.memmove(C.byref(up), C.byref(base), C.sizeof(base))
+                up.tc_packed = img.data_ptr()
+                self._cache[gkey] = (up, img)
+        return self._cache[gkey][0]
 
 
 def random_unit_params(rng: np.random.Generator, c: int, m: int, dtype=np.float32,
@@ -291,7 +315,7 @@ def residual_unit_into(out: torch.Tensor, src: torch.Tensor, u: ResidualUnitPara
     idx.to_device(dev)
     nbytes = lib.sbn_residual_unit_workspace(dtype_code(dt), c, m, C.byref(g), halo, a)
     ws = _SCRATCH.get(nbytes, dev)
-    up = u.c_params(dt, dev)
+    up = u.c_params(dt, dev, g if a != _lib.SBN_ALGO_SIMT else None, halo)
     st = lib.sbn_residual_unit(src.data_ptr(), dtype_code(dt), c, m, C.byref(g), halo,
                                int(u.pre_activation), C.byref(up), idx.rows.data_ptr(),
                                idx.count_dev.data_ptr(), idx.capacity, out.data_ptr(),
