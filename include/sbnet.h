@@ -146,6 +146,10 @@ int sbn_sparse_conv_algo(int dtype, int cin, int cout, int kh, int kw, int sh, i
 int sbn_selftest_umma(const void* a, const void* b, int rows, int shift, int plane_pad, float* d,
                       sbn_stream_t stream);
 
+/* Diagnostics: when buf != NULL the fused kernels record %globaltimer at phase
+ * boundaries into buf[cta * 16 + phase] (buf: device memory, grid * 16 slots). */
+int sbn_debug_set_trace(unsigned long long* buf);
+
 /* Number of kernels the library has launched since load (for the bench's
  * gpu_launches claim). */
 uint64_t sbn_launch_count(void);

@@ -60,6 +60,7 @@ _PROTOS = {
                                _P, _P, C.c_size_t, _I, _P]),
     "sbn_residual_unit_algo": (_I, [_I, _I, _I, _G, _I, _I]),
     "sbn_selftest_umma": (_I, [_P, _P, _I, _I, _I, _P, _P]),
+    "sbn_debug_set_trace": (_I, [_P]),
     "sbn_residual_unit_packed_bytes": (C.c_size_t, [_I, _I, _I, _G, _I, _I]),
     "sbn_residual_unit_pack": (_I, [C.POINTER(UnitParams), _I, _I, _I, _G, _I, _I, _P, _P]),
 }

@@ -97,4 +97,37 @@ __device__ __forceinline__ int ld_count(const int32_t* count, int cap) {
   return c < cap ? c : cap;
 }
 
+// ---- optional phase tracing (diagnostics): kernels record %globaltimer at phase
+// boundaries into trace[cta * kTraceSlots + phase] when a buffer has been set with
+// sbn_debug_set_trace() (passed to kernels as an argument; null check otherwise).
+constexpr int kTraceSlots = 16;
+unsigned long long* trace_buffer();  // host side: current buffer or nullptr
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace(unsigned long long* tb, int phase) {
+  if (tb && threadIdx.x == 0) tb[blockIdx.x * kTraceSlots + phase] = gtimer();
+}
+
+// Grid-wide barrier among `expected` co-resident CTAs (caller guarantees residency).
+// `bar` = two zero-initialised words in global memory; the last CTA to leave resets
+// them, so the same words serve the next launch in the stream.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int expected) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (*reinterpret_cast<volatile unsigned int*>(bar) < expected) __nanosleep(64);
+    __threadfence();
+    if (atomicAdd(bar + 1, 1u) == expected - 1) {
+      bar[0] = 0u;
+      bar[1] = 0u;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace sbn

@@ -67,15 +67,41 @@ reduce_mask_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr
   const double area = (double)g.bh * (double)g.bw;
 
   int tile_count = 0;
+  const bool vec = ((g.w & 3) == 0) && ((reinterpret_cast<uintptr_t>(mask) & 3) == 0) && (y1 - y0) < 256;
   for (int bx0 = 0; bx0 < g.gx; bx0 += chunk) {
     const int bx1 = min(bx0 + chunk, g.gx);
-    const int cx0 = max(g.ox + bx0 * g.sx, 0);
+    int cx0 = max(g.ox + bx0 * g.sx, 0);
     const int cx1 = min(g.ox + (bx1 - 1) * g.sx + g.bw, g.w);
     __syncthreads();
-    for (int x = cx0 + (int)threadIdx.x; x < cx1; x += kMaskThreads) {
-      int s = 0;
-      for (int y = y0; y < y1; ++y) s += __ldg(mrow + (size_t)y * g.w + x);
-      colsum[x - cx0] = s;
+    if (vec) {
+      // 4 columns per thread: a 32-bit word of 0/1 bytes is four packed column counters
+      // (no carry between bytes for < 256 rows); every row load is issued before use.
+      cx0 &= ~3;
+      const int nw = (cx1 - cx0 + 3) >> 2;
+      const uint32_t* base = reinterpret_cast<const uint32_t*>(mrow) + (cx0 >> 2);
+      const int wpr = g.w >> 2;
+      for (int wi = threadIdx.x; wi < nw; wi += kMaskThreads) {
+        uint32_t acc = 0;
+        int y = y0;
+        for (; y + 8 <= y1; y += 8) {
+          uint32_t v[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) v[r] = __ldg(base + (size_t)(y + r) * wpr + wi);
+#pragma unroll
+          for (int r = 0; r < 8; ++r) acc += v[r];
+        }
+        for (; y < y1; ++y) acc += __ldg(base + (size_t)y * wpr + wi);
+        const int x = cx0 + 4 * wi;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (x + e < cx1) colsum[x + e - cx0] = (acc >> (8 * e)) & 0xffu;
+      }
+    } else {
+      for (int x = cx0 + (int)threadIdx.x; x < cx1; x += kMaskThreads) {
+        int sum = 0;
+        for (int y = y0; y < y1; ++y) sum += __ldg(mrow + (size_t)y * g.w + x);
+        colsum[x - cx0] = sum;
+      }
     }
     __syncthreads();
     int local = 0;
@@ -94,27 +120,43 @@ reduce_mask_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr
     tile_count += block_sum(local, red);
   }
 
-  // ---- decoupled look-back: exclusive prefix of active blocks over earlier tiles
-  if (threadIdx.x == 0) {
+  // ---- decoupled look-back: exclusive prefix of active blocks over earlier tiles.
+  //      Warp 0 inspects 32 predecessors per round (lane i -> tile - 1 - i): it sums the
+  //      published aggregates up to the nearest inclusive prefix, retrying the window
+  //      while any needed predecessor has not published yet.
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    if (lane == 0)
+      atomicExch(&ws->status[tile], ((tile == 0 ? 2ull : 1ull) << 32) | (unsigned)tile_count);
     int prefix = 0;
-    if (tile == 0) {
-      __threadfence();
-      atomicExch(&ws->status[0], (2ull << 32) | (unsigned)tile_count);
-    } else {
-      atomicExch(&ws->status[tile], (1ull << 32) | (unsigned)tile_count);
-      for (int j = tile - 1; j >= 0;) {
-        unsigned long long s = ld_volatile(&ws->status[j]);
-        unsigned flag = (unsigned)(s >> 32);
-        if (flag == 0) continue;  // predecessor not published yet: spin
-        prefix += (int)(unsigned)(s & 0xffffffffull);
-        if (flag == 2) break;
-        --j;
+    int j = tile - 1;
+    while (j >= 0) {
+      const int k = j - lane;
+      unsigned long long st = k >= 0 ? ld_volatile(&ws->status[k]) : (2ull << 32);
+      const unsigned flag = (unsigned)(st >> 32);
+      const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+      const unsigned none = __ballot_sync(0xffffffffu, flag == 0);
+      const int first = incl ? __ffs(incl) - 1 : 31;
+      const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+      if (none & need) {
+        __nanosleep(32);
+        continue;
       }
-      __threadfence();
-      atomicExch(&ws->status[tile], (2ull << 32) | (unsigned)(prefix + tile_count));
+      int v = lane <= first ? (int)(unsigned)(st & 0xffffffffull) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      prefix += v;
+      if (incl) break;
+      j -= 32;
     }
-    s_prefix = prefix;
-    if (tile == tiles - 1) *count = prefix + tile_count;
+    if (lane == 0) {
+      if (tile > 0) {
+        __threadfence();
+        atomicExch(&ws->status[tile], (2ull << 32) | (unsigned)(prefix + tile_count));
+      }
+      s_prefix = prefix;
+      if (tile == tiles - 1) *count = prefix + tile_count;
+    }
   }
   __syncthreads();
 
@@ -226,7 +268,7 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
   SBN_CHECK_ARG(tiles < (1l << 31), SBN_ERR_INVALID, "too many block rows");
   // chunk of block columns whose column range fits the column-sum buffer
   int chunk = g.gx;
-  if ((long)(chunk - 1) * g.sx + g.bw > kColBuf) chunk = (kColBuf - g.bw) / g.sx + 1;
+  if ((long)(chunk - 1) * g.sx + g.bw + 3 > kColBuf) chunk = (kColBuf - 3 - g.bw) / g.sx + 1;
   SBN_CHECK_ARG(chunk >= 1, SBN_ERR_UNSUPPORTED, "block width %d too large for reduce_mask", g.bw);
   const size_t dyn = (size_t)g.gx;
   SBN_CHECK_ARG(dyn <= 48 * 1024 - 20 * 1024, SBN_ERR_UNSUPPORTED, "grid width %d too large", g.gx);

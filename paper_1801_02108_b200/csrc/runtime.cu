@@ -6,6 +6,7 @@
 
 namespace sbn {
 namespace {
+unsigned long long* g_trace = nullptr;
 thread_local char g_err[512] = "";
 std::atomic<uint64_t> g_launches{0};
 constexpr int kMaxDev = 64;
@@ -51,7 +52,14 @@ int max_smem_optin() {
   return g_smem[d];
 }
 
+unsigned long long* trace_buffer() { return g_trace; }
+
 }  // namespace sbn
+
+extern "C" int sbn_debug_set_trace(unsigned long long* buf) {
+  sbn::g_trace = buf;
+  return SBN_OK;
+}
 
 extern "C" const char* sbn_version(void) { return "sbnet-b200 0.1.0 (sm_100a)"; }
 extern "C" const char* sbn_last_error(void) { return sbn::g_err; }

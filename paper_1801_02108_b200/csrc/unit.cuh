@@ -48,8 +48,8 @@ struct UnitFold {
 bool unit_tc_supported(int dtype, int c, int m, const Geo& g, int halo, int pre_act);
 size_t unit_tc_packed_bytes(int c, int m, const Geo& g);
 int unit_tc_pack(const sbn_unit_params* p, int c, int m, const Geo& g, void* img, cudaStream_t s);
-int unit_tc_launch(const void* x, void* out, const void* rim, int c, int m, const Geo& g,
-                   const sbn_unit_params* p, const void* packed, const int32_t* idx,
+int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, int c, int m,
+                   const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
                    const int32_t* count, int cap, cudaStream_t s);
 
 }  // namespace sbn

@@ -245,10 +245,14 @@ int unit_rim_snapshot(const void* x, int es, int c, const Geo& g, int halo, cons
   return launch_status("unit_rim_snapshot");
 }
 
+// Workspace layout: [256 B grid-barrier words (zeroed once by the caller, self-resetting)
+//                    | rim snapshot (in-place calls) | packed tc image or SIMT scratch]
+constexpr size_t kBarBytes = 256;
+
 size_t unit_workspace(int dtype, int c, int m, const Geo& g, int halo, int algo, bool tc) {
   const int es = dtype_size(dtype);
   const int cap = g.n * g.gy * g.gx;
-  size_t ws = rim_bytes(es, c, g, halo, cap);  // rim snapshot for in-place calls
+  size_t ws = kBarBytes + rim_bytes(es, c, g, halo, cap);
   if (tc) ws += align_up(unit_tc_packed_bytes(c, m, g), 256);  // packing when no image given
   if (!tc) {
     const size_t ae = dtype == SBN_F64 ? 8 : 4;
@@ -325,13 +329,15 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
   const bool inplace = (x == out);
   const void* rim = nullptr;
   uint8_t* wsb = (uint8_t*)ws;
-  size_t rb = rim_bytes(dtype_size(dtype), c, g, halo, cap);
+  const size_t rb = kBarBytes + rim_bytes(dtype_size(dtype), c, g, halo, cap);
   if (inplace && halo > 0) {
     SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
                   "in-place residual unit needs a %zu-byte workspace", need);
-    st = unit_rim_snapshot(x, dtype_size(dtype), c, g, halo, idx, count, cap, wsb, s);
-    if (st) return st;
-    rim = wsb;
+    if (!use_tc) {  // the tcgen05 kernel handles the rim itself (grid barrier)
+      st = unit_rim_snapshot(x, dtype_size(dtype), c, g, halo, idx, count, cap, wsb + kBarBytes, s);
+      if (st) return st;
+      rim = wsb + kBarBytes;
+    }
   }
   if (use_tc) {
     const void* packed = p->tc_packed;
@@ -342,7 +348,9 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
       if (st) return st;
       packed = wsb + rb;
     }
-    return unit_tc_launch(x, out, rim, c, m, g, p, packed, idx, count, cap, s);
+    return unit_tc_launch(x, out, inplace ? wsb + kBarBytes : nullptr,
+                          inplace ? reinterpret_cast<unsigned int*>(wsb) : nullptr, c, m, g, p,
+                          packed, idx, count, cap, s);
   }
   void* scratch = nullptr;
   if (need > rb) {

@@ -78,6 +78,9 @@ struct TcArgs {
   const __nv_bfloat16 *w1, *b1, *w2, *b2, *w3, *b3;
   const float *s1, *t1, *s2, *t2, *s3, *t3;
   const uint8_t* packed;  // smem image of [B1 | B2 | B3 | params] (unit_tc_pack)
+  __nv_bfloat16* rim_buf;  // in place, more blocks than CTAs: halo rims snapshotted here
+  unsigned int* gbar;      // grid-barrier words (in place only)
+  unsigned long long* trace;
   const int32_t* idx;
   const int32_t* count;
   int cap;
@@ -111,9 +114,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Geo& g = a.g;
 
-  const int B = ld_count(a.count, a.cap);
-  if ((int)blockIdx.x >= B) return;  // no block for this CTA: skip weights and TMEM
-
+  trace(a.trace, 0);
   // ---- prologue: one bulk (TMA) copy of the pre-packed weight/param image; it lands
   //      while the first window is being loaded
   __shared__ uint64_t wbar;
@@ -136,6 +137,48 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   uint32_t phase = 0;
   bool weights_ready = false;
 
+  trace(a.trace, 1);
+  // everything above overlaps the previous kernel (reduce_mask) under PDL
+  tc::pdl_wait();
+  const int B = ld_count(a.count, a.cap);
+  trace(a.trace, 2);
+  const bool inplace = a.x == a.out;
+  // In place, a block's halo rim is its neighbours' interior, which they overwrite.
+  //  resident (B <= grid): every block has its own CTA; all windows are staged before
+  //                        any CTA writes (one grid barrier after staging).
+  //  streamed (B > grid):  rims of all blocks are snapshotted first (grid barrier),
+  //                        then windows read interiors from x and rims from the snapshot.
+  const bool resident = B <= (int)gridDim.x;
+  const __nv_bfloat16* rimsrc = a.rim;
+  if (inplace && !resident) {
+    const Rim r{BS, BS, 1};
+    const int Pr = r.pixels();
+    for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
+      const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+      const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+      for (int i = tid; i < Pr * (C / 8); i += kThreads) {
+        const int rp = i / (C / 8), k = i % (C / 8);
+        int wy, wx;
+        r.coord(rp, wy, wx);
+        const int y = ys + wy, xx = xs + wx;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+          v = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
+        reinterpret_cast<uint4*>(a.rim_buf)[((size_t)blk * Pr + rp) * (C / 8) + k] = v;
+      }
+    }
+    grid_barrier(a.gbar, gridDim.x);
+    rimsrc = a.rim_buf;
+  }
+  if (resident && (int)blockIdx.x >= B) {  // idle CTA: drain the weight copy, release TMEM
+    tc::mbar_wait(&wbar, 0);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
+    return;
+  }
+
   const Rim rim{BS, BS, 1};
   const int P = rim.pixels();
   const int q = warp & 3;           // TMEM lane quarter of this warp
@@ -157,12 +200,15 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
       const int y = ys + wy, xx = xs + wx;
       raw[it] = make_uint4(0, 0, 0, 0);
       if (i < TOT) {
-        if (a.rim && !rim.interior(wy, wx))
-          raw[it] = __ldg(reinterpret_cast<const uint4*>(a.rim) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
+        if (rimsrc && !rim.interior(wy, wx))
+          raw[it] = *(reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
         else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
           raw[it] = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
       }
     }
+    trace(a.trace, 3);
+    if (inplace && resident) grid_barrier(a.gbar, (unsigned)B);  // all windows read
+    trace(a.trace, 4);
     if (!weights_ready) {
       tc::mbar_wait(&wbar, 0);
       weights_ready = true;
@@ -186,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     }
     tc::fence_async_smem();
     __syncthreads();
+    trace(a.trace, 5);
 
     // ---- 2. GEMM1: C1 = A1 . W1
     if (tid == 0) {
@@ -204,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     phase ^= 1;
     tc::fence_after();
 
+    trace(a.trace, 6);
     // ---- 3. epilogue 1: +b1, BN2, ReLU, x in-bounds -> A2
     for (int t = tpar; t < K::NT1; t += 2) {
       const int r = t * 128 + q * 32 + lane;
@@ -231,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     tc::fence_async_smem();
     __syncthreads();
 
+    trace(a.trace, 7);
     // ---- 4. GEMM2: 3x3 valid conv as 9 row-shifted views of A2
     if (tid == 0) {
       tc::fence_after();
@@ -253,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     phase ^= 1;
     tc::fence_after();
 
+    trace(a.trace, 8);
     // ---- 5. epilogue 2: +b2, BN3, ReLU -> A3; prefetch this row's residual (x at the
     //      output pixel) so its latency hides under GEMM3
     constexpr bool kPrefetch = K::NT2 <= 2;
@@ -290,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     tc::fence_async_smem();
     __syncthreads();
 
+    trace(a.trace, 9);
     // ---- 6. GEMM3: C3 = A3 . W3
     if (tid == 0) {
       tc::fence_after();
@@ -307,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     phase ^= 1;
     tc::fence_after();
 
+    trace(a.trace, 10);
     // ---- 7. epilogue 3: +b3, + residual, store the block's clipped output window
     for (int t = tpar; t < K::NT2; t += 2) {
       const int r = t * 128 + q * 32 + lane;
@@ -343,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     }
     tc::fence_before();
     __syncthreads();
+    trace(a.trace, 11);
   }
 
   tc::fence_after();
@@ -418,7 +471,21 @@ int launch(const TcArgs& a, int cap, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     attr = true;
   }
-  kern<<<persistent_grid(cap, K::OCC), kThreads, K::SMEM, s>>>(a);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, K::SMEM);
+  if (occ < 1) occ = 1;
+  if (occ > K::OCC) occ = K::OCC;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(persistent_grid(cap, occ));  // <= co-resident capacity (grid barrier)
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = K::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
   return launch_status("residual_unit_tcgen05");
 }
 
@@ -460,6 +527,9 @@ static TcArgs make_args(const void* x, void* out, const void* rim, const Geo& g,
   a.s2 = (const float*)p->bn2_scale; a.t2 = (const float*)p->bn2_shift;
   a.s3 = (const float*)p->bn3_scale; a.t3 = (const float*)p->bn3_shift;
   a.packed = (const uint8_t*)p->tc_packed;
+  a.rim_buf = nullptr;
+  a.gbar = nullptr;
+  a.trace = trace_buffer();
   a.idx = idx; a.count = count; a.cap = cap;
   return a;
 }
@@ -473,11 +543,13 @@ int unit_tc_pack(const sbn_unit_params* p, int c, int m, const Geo& g, void* img
   return SBN_ERR_UNSUPPORTED;
 }
 
-int unit_tc_launch(const void* x, void* out, const void* rim, int c, int m, const Geo& g,
-                   const sbn_unit_params* p, const void* packed, const int32_t* idx,
+int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, int c, int m,
+                   const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
                    const int32_t* count, int cap, cudaStream_t s) {
-  TcArgs a = make_args(x, out, rim, g, p, idx, count, cap);
+  TcArgs a = make_args(x, out, nullptr, g, p, idx, count, cap);
   a.packed = (const uint8_t*)packed;
+  a.rim_buf = (__nv_bfloat16*)rim_buf;
+  a.gbar = gbar;
 #define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_) return launch<C_, M_, B_>(a, cap, s);
   SBN_UNIT_TC_CONFIGS(X)
 #undef X

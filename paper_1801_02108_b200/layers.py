@@ -52,7 +52,7 @@ class _Scratch(threading.local):
         key = (str(device), torch.cuda.current_stream(device).cuda_stream)
         b = self.bufs.get(key)
         if b is None or b.numel() < nbytes:
-            b = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+            b = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)  # barrier words must start at 0
             self.bufs[key] = b
         return b
 
