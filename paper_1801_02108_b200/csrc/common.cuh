@@ -130,4 +130,27 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int exp
   __syncthreads();
 }
 
+// Split-phase grid barrier: arrive right after a CTA's last read of shared global data,
+// wait right before its first conflicting write, so the wait overlaps the work between.
+__device__ __forceinline__ void grid_arrive(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+  }
+}
+__device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int expected) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    while (*reinterpret_cast<volatile unsigned int*>(bar) < expected) __nanosleep(32);
+    __threadfence();
+    if (atomicAdd(bar + 1, 1u) == expected - 1) {
+      bar[0] = 0u;
+      bar[1] = 0u;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace sbn

@@ -140,6 +140,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   trace(a.trace, 1);
   // everything above overlaps the previous kernel (reduce_mask) under PDL
   tc::pdl_wait();
+  int n0 = 0, by0 = 0, bx0 = 0;
+  if ((int)blockIdx.x < a.cap) {  // speculative: the first block's row, loaded alongside the count
+    n0 = __ldg(a.idx + 3 * blockIdx.x);
+    by0 = __ldg(a.idx + 3 * blockIdx.x + 1);
+    bx0 = __ldg(a.idx + 3 * blockIdx.x + 2);
+  }
   const int B = ld_count(a.count, a.cap);
   trace(a.trace, 2);
   const bool inplace = a.x == a.out;
@@ -185,7 +191,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   const int tpar = warp >> 2;       // tile parity handled by this warp
 
   for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-    const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+    const bool first = blk == (int)blockIdx.x;
+    const int n = first ? n0 : __ldg(a.idx + 3 * blk);
+    const int by = first ? by0 : __ldg(a.idx + 3 * blk + 1);
+    const int bx = first ? bx0 : __ldg(a.idx + 3 * blk + 2);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
 
     // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
@@ -207,7 +216,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
       }
     }
     trace(a.trace, 3);
-    if (inplace && resident) grid_barrier(a.gbar, (unsigned)B);  // all windows read
+    // in place + resident: announce "my window is read"; the matching wait sits right
+    // before the first store of epilogue 3, so it overlaps the three GEMMs
+    if (inplace && resident) grid_arrive(a.gbar);
     trace(a.trace, 4);
     if (!weights_ready) {
       tc::mbar_wait(&wbar, 0);
@@ -358,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     phase ^= 1;
     tc::fence_after();
 
+    if (inplace && resident) grid_wait(a.gbar, (unsigned)B);  // neighbours have read my rim
     trace(a.trace, 10);
     // ---- 7. epilogue 3: +b3, + residual, store the block's clipped output window
     for (int t = tpar; t < K::NT2; t += 2) {
