@@ -110,10 +110,17 @@ int sbn_scatter(const void* blocks, int dtype, int c, const sbn_geometry* g, con
 
 /* Fused sparse_conv2d body (`layers.py:27-47` after reduce_mask): gather -> valid
  * conv (kh, kw, stride sh, sw) -> (+bias) -> scatter into dst (n, oh, ow, cout), all in
- * one kernel; the block stack never touches HBM.  w: HWIO; bias nullable. */
+ * one kernel; the block stack never touches HBM.  w: HWIO; bias nullable.
+ * w_packed: optional tensor-core weight image (sbn_sparse_conv_pack); when NULL on the
+ * tcgen05 path the call packs into ws (sbn_sparse_conv_packed_bytes bytes) first. */
 int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
-                    const sbn_geometry* g, const void* w, const void* bias, const int32_t* idx,
-                    const int32_t* count, int cap, void* dst, int algo, sbn_stream_t stream);
+                    const sbn_geometry* g, const void* w, const void* bias, const void* w_packed,
+                    const int32_t* idx, const int32_t* count, int cap, void* dst, void* ws,
+                    size_t ws_bytes, int algo, sbn_stream_t stream);
+size_t sbn_sparse_conv_packed_bytes(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
+                                    const sbn_geometry* g);
+int sbn_sparse_conv_pack(const void* w, int dtype, int cin, int cout, int kh, int kw, int sh,
+                         int sw, const sbn_geometry* g, void* packed, sbn_stream_t stream);
 
 /* Fused sparse_residual_unit body (`layers.py:203-229` after reduce_mask): gather ->
  * bottleneck branch (`_unit_branch`, `layers.py:137-179`) -> scatter_add onto out.

@@ -100,8 +100,10 @@ int launch_conv_simt(const void* x, int cin, int cout, int kh, int kw, int sh, i
 
 }  // namespace
 
-int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* w, const void* bias,
+int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, const void* bias,
                    const int32_t* idx, const int32_t* count, int cap, void* dst, cudaStream_t s);
+size_t sparse_conv_tc_packed_bytes(int cin, int cout);
+int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_t s);
 bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                               const Geo& g);
 
@@ -116,10 +118,30 @@ extern "C" int sbn_sparse_conv_algo(int dtype, int cin, int cout, int kh, int kw
                                                                               : SBN_ALGO_SIMT;
 }
 
+extern "C" size_t sbn_sparse_conv_packed_bytes(int dtype, int cin, int cout, int kh, int kw,
+                                               int sh, int sw, const sbn_geometry* gp) {
+  if (!gp) return 0;
+  return sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp))
+             ? sparse_conv_tc_packed_bytes(cin, cout)
+             : 0;
+}
+
+extern "C" int sbn_sparse_conv_pack(const void* w, int dtype, int cin, int cout, int kh, int kw,
+                                    int sh, int sw, const sbn_geometry* gp, void* packed,
+                                    sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  SBN_CHECK_ARG(sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp)),
+                SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
+  SBN_CHECK_ARG(w && packed, SBN_ERR_INVALID, "null argument");
+  return sparse_conv_tc_pack(w, cin, cout, packed, (cudaStream_t)stream);
+}
+
 extern "C" int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int kh, int kw, int sh,
                                int sw, const sbn_geometry* gp, const void* w, const void* bias,
-                               const int32_t* idx, const int32_t* count, int cap, void* dst,
-                               int algo, sbn_stream_t stream) {
+                               const void* w_packed, const int32_t* idx, const int32_t* count,
+                               int cap, void* dst, void* ws, size_t ws_bytes, int algo,
+                               sbn_stream_t stream) {
   int st = check_geo(gp);
   if (st) return st;
   SBN_CHECK_ARG(cin > 0 && cout > 0, SBN_ERR_SHAPE, "channels must be > 0");
@@ -136,8 +158,18 @@ extern "C" int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int 
   if (algo == SBN_ALGO_TCGEN05) {
     SBN_CHECK_ARG(tc_ok, SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
   }
-  if (tc_ok && algo != SBN_ALGO_SIMT)
-    return sparse_conv_tc(x, cin, cout, g, w, bias, idx, count, cap, dst, s);
+  if (tc_ok && algo != SBN_ALGO_SIMT) {
+    const void* wpk = w_packed;
+    if (!wpk) {
+      const size_t nb = sparse_conv_tc_packed_bytes(cin, cout);
+      SBN_CHECK_ARG(ws && ws_bytes >= nb, SBN_ERR_WORKSPACE,
+                    "tcgen05 sparse conv without a packed weight image needs a %zu-byte workspace", nb);
+      int st2 = sparse_conv_tc_pack(w, cin, cout, ws, s);
+      if (st2) return st2;
+      wpk = ws;
+    }
+    return sparse_conv_tc(x, cin, cout, g, wpk, bias, idx, count, cap, dst, s);
+  }
   switch (dtype) {
     case SBN_F32:
       return launch_conv_simt<float>(x, cin, cout, kh, kw, sh, sw, g, w, bias, idx, count, cap, dst, s);

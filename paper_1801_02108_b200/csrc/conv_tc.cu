@@ -1,10 +1,272 @@
-// tcgen05 / TMEM fused sparse conv (bf16) — placeholder until the kernel lands.
+// tcgen05 / TMEM fused sparse convolution (bf16 in/out, fp32 accumulate), 3x3 stride 1.
+//
+// Restates reference `sparse_conv2d` (`layers.py:27-47`): per active block, the
+// gathered window (`blocks.py:57-74`) is convolved with a valid 3x3 conv
+// (`ops.py:130-164`, pad (0, 0) on the block) and the (BS-2)^2 output window is written
+// straight into the destination (`blocks.py:125-142`).  The block stack never exists
+// in HBM.
+//
+// Implicit GEMM over the staged window (plane layout, tc_util.cuh): output row
+// q = oy*BS + ox ("full width": ox >= BS-2 columns are computed and dropped), and tap
+// (ky, kx) is the window viewed from row ky*BS + kx, so D[q, :] += A[q + shift, :] . W_tap.
+//
+// Warp roles (persistent CTA, 288 threads):
+//   warp 8, lane 0   producer: streams the 9 per-tap weight images (COUT x CIN bf16,
+//                    pre-packed) through a kStages-deep smem ring with cp.async.bulk,
+//                    running ahead into the next block while the current one drains;
+//   thread 0         MMA issuer: per tap, NT M-tiles x CIN/16 UMMAs (M=128, N=COUT);
+//   warps 0-7        stage the window (zero-filled halo) and run the TMEM epilogue
+//                    (+bias, bf16, clipped store).
 #include "common.cuh"
+#include "tc_util.cuh"
+
 namespace sbn {
-bool sparse_conv_tc_supported(int, int, int, int, int, int, int, const Geo&) { return false; }
-int sparse_conv_tc(const void*, int, int, Geo, const void*, const void*, const int32_t*,
-                   const int32_t*, int, void*, cudaStream_t) {
-  set_error("tcgen05 sparse conv not built");
+namespace {
+
+constexpr int kWorkers = 256;
+constexpr int kThreads = kWorkers + 32;
+
+template <int CIN, int COUT, int BS>
+struct ConvCfg {
+  static_assert(CIN % 16 == 0 && COUT % 16 == 0 && COUT <= 256, "channel constraints");
+  static constexpr int NQ = (BS - 2) * BS;
+  static constexpr int NT = (NQ + 127) / 128;
+  static_assert(NT * COUT <= 512, "TMEM budget");
+  static constexpr int R = (((NT * 128 + 2 * BS + 2) > BS * BS ? (NT * 128 + 2 * BS + 2) : BS * BS) + 7) / 8 * 8;
+  static constexpr int PA = R * 16 + 16;          // window plane stride (padded)
+  static constexpr int PW = COUT * 16;            // weight plane stride
+  static constexpr int TAP = (CIN / 8) * PW;      // bytes per tap image
+  static constexpr int al(int v) { return (v + 1023) / 1024 * 1024; }
+  static constexpr int SZ_A = al((CIN / 8) * PA);
+  static constexpr int STAGES = (SZ_A + 3 * TAP + COUT * 4 <= 220 * 1024) ? 3 : 2;
+  static constexpr int OFF_W = SZ_A;
+  static constexpr int OFF_BIAS = OFF_W + STAGES * TAP;
+  static constexpr int SMEM = OFF_BIAS + COUT * 4;
+  static constexpr int TCOLS = NT * COUT;
+  static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+};
+
+struct ConvArgs {
+  const __nv_bfloat16* x;
+  __nv_bfloat16* out;
+  Geo g;
+  const uint8_t* wpk;   // 9 tap images
+  const __nv_bfloat16* bias;  // nullable
+  const int32_t* idx;
+  const int32_t* count;
+  int cap;
+};
+
+template <int CIN, int COUT, int BS>
+__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs a) {
+  using K = ConvCfg<CIN, COUT, BS>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[K::STAGES], empty[K::STAGES], accb;
+  __shared__ uint32_t tslot;
+  uint8_t* A = smem;
+  uint8_t* Wst = smem + K::OFF_W;
+  float* bias = reinterpret_cast<float*>(smem + K::OFF_BIAS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Geo& g = a.g;
+
+  if (tid == 0) {
+    for (int s = 0; s < K::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(&accb, 1);
+    tc::mbar_fence_init();
+  }
+  for (int i = tid; i < COUT; i += kThreads) bias[i] = a.bias ? __bfloat162float(a.bias[i]) : 0.f;
+  if (warp == 0) tc::tmem_alloc<K::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_wait();
+  const int B = ld_count(a.count, a.cap);
+
+  if (warp == 8) {
+    // ---------------- producer: weight taps through the ring
+    if (lane == 0) {
+      int it = 0;
+      for (int blk = blockIdx.x; blk < B; blk += gridDim.x)
+        for (int tap = 0; tap < 9; ++tap, ++it) {
+          const int s = it % K::STAGES;
+          tc::mbar_wait(&empty[s], ((it / K::STAGES) & 1) ^ 1);
+          tc::mbar_expect_tx(&full[s], K::TAP);
+          tc::bulk_g2s(Wst + s * K::TAP, a.wpk + (size_t)tap * K::TAP, K::TAP, &full[s]);
+        }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- workers (warps 0-7) + MMA issuer (thread 0)
+    const int q = warp & 3, tpar = warp >> 2;
+    int it = 0;
+    uint32_t accphase = 0;
+    for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
+      const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+      const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+      // stage the window (zero-filled halo): all loads in flight, then plane stores
+      constexpr int TOT = BS * BS * (CIN / 8);
+      constexpr int ITEMS = (TOT + kWorkers - 1) / kWorkers;
+      constexpr int CH = ITEMS > 16 ? 16 : ITEMS;
+#pragma unroll 1
+      for (int base = 0; base < ITEMS; base += CH) {
+        uint4 raw[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int i = tid + (base + j) * kWorkers;
+          const int p = i / (CIN / 8), k = i % (CIN / 8);
+          const int y = ys + p / BS, xx = xs + p % BS;
+          raw[j] = make_uint4(0, 0, 0, 0);
+          if (i < TOT && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+            raw[j] = __ldg(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (CIN / 8) + k);
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int i = tid + (base + j) * kWorkers;
+          if (i < TOT) {
+            const int p = i / (CIN / 8), k = i % (CIN / 8);
+            *reinterpret_cast<uint4*>(A + k * K::PA + p * 16) = raw[j];
+          }
+        }
+      }
+      tc::fence_async_smem();
+      asm volatile("bar.sync 1, %0;" ::"n"(kWorkers));
+
+      if (tid == 0) {
+        tc::fence_after();
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(128, COUT);
+        for (int tap = 0; tap < 9; ++tap, ++it) {
+          const int s = it % K::STAGES;
+          tc::mbar_wait(&full[s], (it / K::STAGES) & 1);
+          tc::fence_after();
+          const int shift = (tap / 3) * BS + (tap % 3);
+          const uint32_t wbase = tc::smem_u32(Wst + s * K::TAP);
+#pragma unroll
+          for (int t = 0; t < K::NT; ++t)
+#pragma unroll
+            for (int k = 0; k < CIN / 16; ++k)
+              tc::mma_bf16(tmem + t * COUT,
+                           tc::desc_kmajor_noswz(tc::smem_u32(A + 2 * k * K::PA + (t * 128 + shift) * 16), K::PA, 128),
+                           tc::desc_kmajor_noswz(wbase + 2 * k * K::PW, K::PW, 128), idesc,
+                           (tap | k) > 0);
+          tc::mma_commit(&empty[s]);  // frees the weight stage once these MMAs are done
+        }
+        tc::mma_commit(&accb);
+      } else {
+        it += 9;
+      }
+      tc::mbar_wait(&accb, accphase);
+      accphase ^= 1;
+      tc::fence_after();
+
+      // epilogue: TMEM -> +bias -> bf16 -> clipped output window
+      for (int t = tpar; t < K::NT; t += 2) {
+        const int r = t * 128 + q * 32 + lane;
+        const int oy = r / BS, ox = r % BS;
+        const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+        const bool store = oy < g.obh && ox < g.obw && Y < g.oh && X < g.ow;
+        uint4* op = reinterpret_cast<uint4*>(a.out) +
+                    (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (COUT / 8);
+#pragma unroll 4
+        for (int c0 = 0; c0 < COUT; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + t * COUT + c0, v);
+          if (store) {
+            uint32_t o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = tc::pack_bf16(v[2 * e] + bias[c0 + 2 * e], v[2 * e + 1] + bias[c0 + 2 * e + 1]);
+            op[c0 / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+            op[c0 / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+      tc::fence_before();
+      asm volatile("bar.sync 1, %0;" ::"n"(kWorkers));
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
+}
+
+// HWIO (3, 3, CIN, COUT) -> 9 tap images, each CIN/8 planes x COUT rows x 16 B.
+template <int CIN, int COUT>
+__global__ void conv_tc_pack_kernel(const __nv_bfloat16* __restrict__ w, uint8_t* __restrict__ img) {
+  const int total = 9 * CIN * COUT;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int tap = i / (CIN * COUT), r = i % (CIN * COUT), ci = r / COUT, co = r % COUT;
+    *reinterpret_cast<__nv_bfloat16*>(img + (size_t)tap * (CIN / 8) * COUT * 16 + (ci / 8) * COUT * 16 +
+                                      co * 16 + (ci % 8) * 2) = w[i];
+  }
+}
+
+template <int CIN, int COUT, int BS>
+int launch_conv(const ConvArgs& a, int cap, cudaStream_t s) {
+  using K = ConvCfg<CIN, COUT, BS>;
+  auto kern = conv_tc_kernel<CIN, COUT, BS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(persistent_grid(cap, 1));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = K::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+  return launch_status("sparse_conv_tcgen05");
+}
+
+#define SBN_CONV_TC_CONFIGS(X) \
+  X(128, 128, 16)              \
+  X(128, 128, 8)               \
+  X(64, 64, 16)                \
+  X(64, 64, 8)                 \
+  X(32, 32, 16)
+
+}  // namespace
+
+bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
+                              const Geo& g) {
+  if (dtype != SBN_BF16 || kh != 3 || kw != 3 || sh != 1 || sw != 1 || g.bh != g.bw) return false;
+#define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_ && ConvCfg<CI, CO, BS_>::SMEM <= max_smem_optin()) return true;
+  SBN_CONV_TC_CONFIGS(X)
+#undef X
+  return false;
+}
+
+size_t sparse_conv_tc_packed_bytes(int cin, int cout) { return (size_t)9 * cin * cout * 2; }
+
+int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_t s) {
+#define X(CI, CO, BS_) if (cin == CI && cout == CO) { conv_tc_pack_kernel<CI, CO><<<64, 256, 0, s>>>((const __nv_bfloat16*)w, (uint8_t*)img); return launch_status("sparse_conv_tc_pack"); }
+  SBN_CONV_TC_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 conv instantiation for cin=%d cout=%d", cin, cout);
   return SBN_ERR_UNSUPPORTED;
 }
+
+int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, const void* bias,
+                   const int32_t* idx, const int32_t* count, int cap, void* dst, cudaStream_t s) {
+  ConvArgs a;
+  a.x = (const __nv_bfloat16*)x;
+  a.out = (__nv_bfloat16*)dst;
+  a.g = g;
+  a.wpk = (const uint8_t*)wpk;
+  a.bias = (const __nv_bfloat16*)bias;
+  a.idx = idx;
+  a.count = count;
+  a.cap = cap;
+#define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_) return launch_conv<CI, CO, BS_>(a, cap, s);
+  SBN_CONV_TC_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 conv instantiation for cin=%d cout=%d block=%d", cin, cout, g.bh);
+  return SBN_ERR_UNSUPPORTED;
+}
+
 }  // namespace sbn

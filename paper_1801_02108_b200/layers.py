@@ -97,10 +97,25 @@ def sparse_conv_into(xt: torch.Tensor, out: torch.Tensor, f: FilterBank, p: Conv
     g = spec.c_geometry(xt.shape[0])
     kh, kw = p.kernel
     sh, sw = p.stride
-    st = lib.sbn_sparse_conv(xt.data_ptr(), dtype_code(xt.dtype), f.c_in, f.c_out, kh, kw, sh, sw,
+    a = _algo(algo)
+    dc = dtype_code(xt.dtype)
+    packed = None
+    if a != _lib.SBN_ALGO_SIMT:
+        nb = lib.sbn_sparse_conv_packed_bytes(dc, f.c_in, f.c_out, kh, kw, sh, sw, C.byref(g))
+        if nb:
+            key = ("tc_pack", xt.dtype, str(xt.device))
+            packed = f._cache.get(key)
+            if packed is None:
+                packed = torch.empty(nb, dtype=torch.uint8, device=xt.device)
+                _lib.check(lib.sbn_sparse_conv_pack(w.data_ptr(), dc, f.c_in, f.c_out, kh, kw, sh, sw,
+                                                    C.byref(g), packed.data_ptr(),
+                                                    _lib.stream_handle(xt.device)), "sparse_conv_pack")
+                f._cache[key] = packed
+    st = lib.sbn_sparse_conv(xt.data_ptr(), dc, f.c_in, f.c_out, kh, kw, sh, sw,
                              C.byref(g), w.data_ptr(), None if b is None else b.data_ptr(),
+                             None if packed is None else packed.data_ptr(),
                              idx.rows.data_ptr(), idx.count_dev.data_ptr(), idx.capacity,
-                             out.data_ptr(), _algo(algo), _lib.stream_handle(xt.device))
+                             out.data_ptr(), None, 0, a, _lib.stream_handle(xt.device))
     _lib.check(st, "sparse_conv2d")
 
 

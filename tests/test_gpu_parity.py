@@ -385,3 +385,29 @@ def test_umma_plane_descriptor_selftest(cuda_device, shift, pad):
     ref = a[shift:shift + 128].float() @ b.float().t()
     torch.cuda.synchronize()
     assert torch.allclose(d, ref, rtol=1e-3, atol=1e-3), (d - ref).abs().max()
+
+
+@pytest.mark.parametrize("cin,block", [(128, 16), (128, 8), (64, 16), (32, 16)])
+def test_sparse_conv_tc_bf16_vs_fp32_oracle(cuda_device, cin, block):
+    """tcgen05 implicit-GEMM sparse conv (bf16 in, fp32 accumulate) vs the fp32 oracle on
+    bf16-rounded inputs: 2e-2 relative (north star); inactive pixels exactly zero."""
+    from paper_1801_02108_b200.layers import sparse_conv_algo
+    rng = np.random.default_rng(cin + block)
+    h, w = 120, 104
+    x = torch.from_numpy(rng.standard_normal((2, h, w, cin)).astype(np.float32)).bfloat16()
+    wt = torch.from_numpy((rng.standard_normal((3, 3, cin, cin)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16()
+    bias = torch.from_numpy(rng.standard_normal(cin).astype(np.float32)).bfloat16()
+    m = P.synth_mask_blobs((2, h, w), 0.7, 3)
+    p = _conv((3, 3), (1, 1), True, cin)
+    spec = P.compute_block_spec((2, h, w, cin), p, (block, block))
+    fb = P.FilterBank(wt, bias)
+    assert sparse_conv_algo(torch.bfloat16, fb, p, spec) == "tcgen05"
+    y = _np(P.sparse_conv2d(P.Tensor4D(x), m, fb, p, (block, block)))
+    ref = O.sparse_conv2d(x.float().numpy(), m.numpy(), wt.float().numpy(), bias.float().numpy(),
+                          (1, 1), True, (block, block))
+    assert O.rel_err(y, ref) <= 2e-2
+    geo = O.geometry(h, w, (3, 3), (1, 1), True, (block, block))
+    reg = O.active_region(geo, O.reduce_mask(m.numpy(), geo), 2)
+    assert np.all(y[~reg] == 0)
+    y2 = _np(P.sparse_conv2d(P.Tensor4D(x), m, fb, p, (block, block), algo="simt"))
+    assert O.rel_err(y, y2) <= 1e-2

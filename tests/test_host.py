@@ -184,8 +184,8 @@ def test_c_abi_argument_validation_without_gpu():
     cg = spec.c_geometry(1)
     assert lib.sbn_gather(None, 7, 16, ctypes.byref(cg), None, None, 4, 0, None, None) == _lib.SBN_ERR_UNSUPPORTED
     assert lib.sbn_scatter(None, 0, 16, ctypes.byref(cg), None, None, 4, 1, 1, None, None) == _lib.SBN_ERR_UNSUPPORTED
-    assert lib.sbn_sparse_conv(None, 0, 16, 16, 3, 3, 4, 1, ctypes.byref(cg), None, None, None, None, 4,
-                               None, 0, None) == _lib.SBN_ERR_INVALID
+    assert lib.sbn_sparse_conv(None, 0, 16, 16, 3, 3, 4, 1, ctypes.byref(cg), None, None, None, None,
+                               None, 4, None, None, 0, 0, None) == _lib.SBN_ERR_INVALID
     with pytest.raises(P.GeometryError):
         _lib.check(_lib.SBN_ERR_INVALID, "x")
     with pytest.raises(P.UnsupportedConfigError):
