@@ -142,6 +142,18 @@ int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
                            const sbn_geometry* g, int halo, int pre_act, void* packed,
                            sbn_stream_t stream);
 
+/* The whole sparse_residual_unit (`layers.py:203-229`): mask -> active blocks (MAX pool
+ * over each block's input window) -> fused unit -> scatter-add into out.  On the
+ * tcgen05 path this is ONE kernel: the mask reduction is fused in front of the unit and
+ * produces an unordered active list (blocks write disjoint windows, so the result does
+ * not depend on the order).  ws: sbn_sparse_residual_unit_workspace bytes, zeroed once. */
+size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* g, int halo,
+                                          int algo);
+int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
+                             const sbn_geometry* g, int halo, int pre_act,
+                             const sbn_unit_params* p, void* out, void* ws, size_t ws_bytes,
+                             int algo, sbn_stream_t stream);
+
 /* Which algorithm `algo=AUTO` would pick (SBN_ALGO_SIMT / SBN_ALGO_TCGEN05). */
 int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometry* g, int halo, int pre_act);
 int sbn_sparse_conv_algo(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,

@@ -50,6 +50,8 @@ size_t unit_tc_packed_bytes(int c, int m, const Geo& g);
 int unit_tc_pack(const sbn_unit_params* p, int c, int m, const Geo& g, void* img, cudaStream_t s);
 int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, int c, int m,
                    const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
-                   const int32_t* count, int cap, cudaStream_t s);
+                   const int32_t* count, int cap, cudaStream_t s,
+                   const uint8_t* mask = nullptr, int32_t* idx_out = nullptr,
+                   int32_t* count_out = nullptr);
 
 }  // namespace sbn

@@ -368,3 +368,63 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
                                              scratch, s);
   }
 }
+
+// ---- whole sparse_residual_unit (`layers.py:203-229`): mask -> active blocks -> fused unit.
+// tcgen05 path: ONE kernel (reduce_mask fused into the unit, unordered active list).
+// Otherwise: ordered sbn_reduce_mask + sbn_residual_unit.
+// Workspace: [idx (cap*12) | count | reduce_mask ws | residual-unit ws]
+static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
+
+extern "C" size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* gp,
+                                                     int halo, int algo) {
+  if (!gp || dtype_size(dtype) == 0) return 0;
+  const size_t cap = (size_t)gp->n * gp->gy * gp->gx;
+  return al256(cap * 12) + 256 + al256(sbn_reduce_mask_workspace(gp)) +
+         sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
+}
+
+extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
+                                        const sbn_geometry* gp, int halo, int pre_act,
+                                        const sbn_unit_params* p, void* out, void* ws,
+                                        size_t ws_bytes, int algo, sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  SBN_CHECK_ARG(x && mask && out && p, SBN_ERR_INVALID, "null pointer argument");
+  const size_t need = sbn_sparse_residual_unit_workspace(dtype, c, m, gp, halo, algo);
+  SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
+                "sparse_residual_unit needs a %zu-byte zero-initialised workspace", need);
+  const int cap = gp->n * gp->gy * gp->gx;
+  if (cap <= 0) return SBN_OK;
+  uint8_t* w8 = (uint8_t*)ws;
+  int32_t* idx = (int32_t*)w8;
+  int32_t* count = (int32_t*)(w8 + al256((size_t)cap * 12));
+  uint8_t* rmws = w8 + al256((size_t)cap * 12) + 256;
+  uint8_t* uws = rmws + al256(sbn_reduce_mask_workspace(gp));
+  const size_t uws_bytes = ws_bytes - (size_t)(uws - w8);
+  Geo g = to_geo(gp);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tc = algo != SBN_ALGO_SIMT && unit_tc_supported(dtype, c, m, g, halo, pre_act);
+  if (algo == SBN_ALGO_TCGEN05)
+    SBN_CHECK_ARG(tc, SBN_ERR_UNSUPPORTED, "tcgen05 residual unit does not support this config");
+  if (tc) {
+    SBN_CHECK_ARG(gp->sy == gp->obh && gp->sx == gp->obw && gp->bh - 2 * halo == gp->obh &&
+                      gp->oh == gp->h && gp->ow == gp->w,
+                  SBN_ERR_INVALID, "geometry is not a residual-unit spec");
+    const size_t rb = kBarBytes + rim_bytes(dtype_size(dtype), c, g, halo, cap);
+    const void* packed = p->tc_packed;
+    if (!packed) {
+      st = unit_tc_pack(p, c, m, g, uws + rb, s);
+      if (st) return st;
+      packed = uws + rb;
+    }
+    const bool inplace = x == out;
+    return unit_tc_launch(x, out, inplace ? uws + kBarBytes : nullptr,
+                          reinterpret_cast<unsigned int*>(uws), c, m, g, p, packed, idx, count, cap,
+                          s, mask, idx, count);
+  }
+  st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws,
+                       al256(sbn_reduce_mask_workspace(gp)), stream);
+  if (st) return st;
+  return sbn_residual_unit(x, dtype, c, m, gp, halo, pre_act, p, idx, count, cap, out, uws,
+                           uws_bytes, algo, stream);
+}

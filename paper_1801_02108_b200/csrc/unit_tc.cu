@@ -81,6 +81,9 @@ struct TcArgs {
   __nv_bfloat16* rim_buf;  // in place, more blocks than CTAs: halo rims snapshotted here
   unsigned int* gbar;      // grid-barrier words (in place only)
   unsigned long long* trace;
+  const uint8_t* mask;     // non-null: fused reduce_mask (MAX) + unordered compaction into idx/count
+  int32_t* idx_out;
+  int32_t* count_out;
   const int32_t* idx;
   const int32_t* count;
   int cap;
@@ -141,12 +144,79 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   // everything above overlaps the previous kernel (reduce_mask) under PDL
   tc::pdl_wait();
   int n0 = 0, by0 = 0, bx0 = 0;
-  if ((int)blockIdx.x < a.cap) {  // speculative: the first block's row, loaded alongside the count
-    n0 = __ldg(a.idx + 3 * blockIdx.x);
-    by0 = __ldg(a.idx + 3 * blockIdx.x + 1);
-    bx0 = __ldg(a.idx + 3 * blockIdx.x + 2);
+  int B;
+  const int32_t* idx = a.idx;
+  if (a.mask) {
+    // ---- fused reduce_mask (MAX pooling, `tiling.py:138-160`): every CTA tests the block
+    //      windows of candidates blockIdx.x + j*grid against the mask and appends the
+    //      active ones to one list (one atomic slot per CTA and round; order is irrelevant
+    //      to the unit: blocks write disjoint windows).  A grid barrier publishes the count.
+    __shared__ int s_flag[32];
+    __shared__ int s_base;
+    const int T = g.n * g.gy * g.gx;
+    const int area = g.bh * g.bw;
+    unsigned int* fb = a.gbar + 2;  // [arrive, depart, slot]
+    for (int r0 = blockIdx.x; r0 < T; r0 += 32 * gridDim.x) {
+      const int nj = min(32, (T - r0 + (int)gridDim.x - 1) / (int)gridDim.x);
+      if (tid < 32) s_flag[tid] = 0;
+      __syncthreads();
+      for (int e = tid; e < nj * area; e += kThreads) {
+        const int j = e / area, p = e - j * area;
+        const int cand = r0 + j * gridDim.x;
+        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+        const int cy = rr / g.gx, cx = rr - cy * g.gx;
+        const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
+        if (y >= 0 && y < g.h && xx >= 0 && xx < g.w && __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx))
+          s_flag[j] = 1;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const bool on = lane < nj && s_flag[lane];
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) s_base = bal ? (int)atomicAdd(fb + 2, (unsigned)__popc(bal)) : 0;
+        __syncwarp();
+        if (on) {
+          const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
+          const int cand = r0 + lane * gridDim.x;
+          const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+          a.idx_out[3 * pos] = fr;
+          a.idx_out[3 * pos + 1] = rr / g.gx;
+          a.idx_out[3 * pos + 2] = rr % g.gx;
+        }
+      }
+    }
+    __shared__ int s_B;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(fb, 1u);
+      while (*reinterpret_cast<volatile unsigned int*>(fb) < gridDim.x) __nanosleep(32);
+      __threadfence();
+      s_B = (int)*reinterpret_cast<volatile unsigned int*>(fb + 2);
+      if (blockIdx.x == 0) *a.count_out = s_B;
+      if (atomicAdd(fb + 1, 1u) == gridDim.x - 1) {  // last out: reset for the next launch
+        fb[0] = 0u;
+        fb[1] = 0u;
+        fb[2] = 0u;
+        __threadfence();
+      }
+    }
+    __syncthreads();
+    B = s_B;
+    idx = a.idx_out;
+    if ((int)blockIdx.x < B) {
+      n0 = __ldcg(idx + 3 * blockIdx.x);
+      by0 = __ldcg(idx + 3 * blockIdx.x + 1);
+      bx0 = __ldcg(idx + 3 * blockIdx.x + 2);
+    }
+  } else {
+    if ((int)blockIdx.x < a.cap) {  // speculative: the first block's row, loaded alongside the count
+      n0 = __ldg(idx + 3 * blockIdx.x);
+      by0 = __ldg(idx + 3 * blockIdx.x + 1);
+      bx0 = __ldg(idx + 3 * blockIdx.x + 2);
+    }
+    B = ld_count(a.count, a.cap);
   }
-  const int B = ld_count(a.count, a.cap);
   trace(a.trace, 2);
   const bool inplace = a.x == a.out;
   // In place, a block's halo rim is its neighbours' interior, which they overwrite.
@@ -160,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
     for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-      const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+      const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
       const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
       for (int i = tid; i < Pr * (C / 8); i += kThreads) {
         const int rp = i / (C / 8), k = i % (C / 8);
@@ -192,9 +262,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
   for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
     const bool first = blk == (int)blockIdx.x;
-    const int n = first ? n0 : __ldg(a.idx + 3 * blk);
-    const int by = first ? by0 : __ldg(a.idx + 3 * blk + 1);
-    const int bx = first ? bx0 : __ldg(a.idx + 3 * blk + 2);
+    const int n = first ? n0 : __ldcg(idx + 3 * blk);
+    const int by = first ? by0 : __ldcg(idx + 3 * blk + 1);
+    const int bx = first ? bx0 : __ldcg(idx + 3 * blk + 2);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
 
     // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
@@ -542,6 +612,9 @@ static TcArgs make_args(const void* x, void* out, const void* rim, const Geo& g,
   a.rim_buf = nullptr;
   a.gbar = nullptr;
   a.trace = trace_buffer();
+  a.mask = nullptr;
+  a.idx_out = nullptr;
+  a.count_out = nullptr;
   a.idx = idx; a.count = count; a.cap = cap;
   return a;
 }
@@ -557,8 +630,12 @@ int unit_tc_pack(const sbn_unit_params* p, int c, int m, const Geo& g, void* img
 
 int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, int c, int m,
                    const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
-                   const int32_t* count, int cap, cudaStream_t s) {
+                   const int32_t* count, int cap, cudaStream_t s, const uint8_t* mask,
+                   int32_t* idx_out, int32_t* count_out) {
   TcArgs a = make_args(x, out, nullptr, g, p, idx, count, cap);
+  a.mask = mask;
+  a.idx_out = idx_out;
+  a.count_out = count_out;
   a.packed = (const uint8_t*)packed;
   a.rim_buf = (__nv_bfloat16*)rim_buf;
   a.gbar = gbar;

@@ -48,8 +48,10 @@ class _Scratch(threading.local):
     def __init__(self):
         self.bufs = {}
 
-    def get(self, nbytes: int, device) -> torch.Tensor:
-        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    def get(self, nbytes: int, device, kind: str = "unit") -> torch.Tensor:
+        """Zero-initialised, cached per (device, stream, kind): each kind has its own
+        layout of self-resetting barrier words, so kinds must never share a buffer."""
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream, kind)
         b = self.bufs.get(key)
         if b is None or b.numel() < nbytes:
             b = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)  # barrier words must start at 0
@@ -302,19 +304,40 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
         raise ShapeMismatchError(f"unit channels {u.channels} != input channels {x.dims[3]}")
     if bn_mode is not BnMode.INFERENCE:
         raise UnsupportedConfigError("sparse_residual_unit: inference-mode BN only (training is out of scope)")
-    if _shared is None:
-        _check_mask(x, mask)
-        spec = unit_spec(x.dims, block_size, halo)
-        idx = reduce_mask(mask, spec, PoolMode.MAX)
-    else:
-        spec, idx = _shared
     xt = cuda(x.nhwc())
     if inplace and x.nhwc().is_cuda and xt.data_ptr() == x.nhwc().data_ptr():
         out = xt
     else:
         out = xt.clone()
-    residual_unit_into(out, out if (out is xt) else xt, u, spec, idx, halo, algo)
+    if _shared is None:
+        _check_mask(x, mask)
+        spec = unit_spec(x.dims, block_size, halo)
+        sparse_residual_unit_into(out, out if (out is xt) else xt, cuda(mask.data), u, spec, halo, algo)
+    else:
+        spec, idx = _shared
+        residual_unit_into(out, out if (out is xt) else xt, u, spec, idx, halo, algo)
     return Tensor4D.from_nhwc(out, x.layout)
+
+
+def sparse_residual_unit_into(out: torch.Tensor, src: torch.Tensor, mask: torch.Tensor,
+                              u: ResidualUnitParams, spec: BlockSpec, halo: int = 1,
+                              algo="auto") -> None:
+    """mask -> active blocks -> fused unit (sbn_sparse_residual_unit): one kernel on the
+    tcgen05 path.  `out` holds src's values (clone) or is src (in place)."""
+    lib = _lib.load()
+    dt, dev = src.dtype, src.device
+    n, _, _, c = src.shape
+    g = spec.c_geometry(n)
+    a = _algo(algo)
+    nbytes = lib.sbn_sparse_residual_unit_workspace(dtype_code(dt), c, u.mid_channels, C.byref(g),
+                                                    halo, a)
+    ws = _SCRATCH.get(nbytes, dev, "fused_unit")
+    up = u.c_params(dt, dev, g if a != _lib.SBN_ALGO_SIMT else None, halo)
+    st = lib.sbn_sparse_residual_unit(src.data_ptr(), mask.data_ptr(), dtype_code(dt), c,
+                                      u.mid_channels, C.byref(g), halo, int(u.pre_activation),
+                                      C.byref(up), out.data_ptr(), ws.data_ptr(), ws.numel(), a,
+                                      _lib.stream_handle(dev))
+    _lib.check(st, "sparse_residual_unit")
 
 
 def residual_unit_into(out: torch.Tensor, src: torch.Tensor, u: ResidualUnitParams,

@@ -411,3 +411,24 @@ def test_sparse_conv_tc_bf16_vs_fp32_oracle(cuda_device, cin, block):
     assert np.all(y[~reg] == 0)
     y2 = _np(P.sparse_conv2d(P.Tensor4D(x), m, fb, p, (block, block), algo="simt"))
     assert O.rel_err(y, y2) <= 1e-2
+
+
+@pytest.mark.parametrize("density,nframes", [(0.1, 1), (0.3, 3), (0.9, 2)])
+def test_fused_mask_unit_bit_identical_to_two_launch_path(cuda_device, density, nframes):
+    """The single-kernel sparse_residual_unit (mask reduction fused, unordered block list)
+    must equal the ordered reduce_mask + unit path bit for bit (blocks write disjoint
+    windows), in place and functional, call after call (self-resetting barriers)."""
+    from paper_1801_02108_b200.layers import residual_unit_into
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.standard_normal((nframes, 208, 176, 64)).astype(np.float32)).bfloat16().cuda()
+    u = P.random_unit_params(rng, 64, 32)
+    mk = P.synth_mask_blobs((nframes, 208, 176), 1.0 - density, 5).cuda()
+    spec = P.unit_spec(tuple(x.shape), (16, 16))
+    ref = x.clone()
+    residual_unit_into(ref, x, u, spec, P.reduce_mask(mk, spec))
+    for _ in range(3):
+        y = P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16))
+        assert torch.equal(y.data, ref)
+        xi = x.clone()
+        P.sparse_residual_unit(P.Tensor4D(xi), mk, u, (16, 16), inplace=True)
+        assert torch.equal(xi, ref)

@@ -9,7 +9,7 @@ import torch
 
 import paper_1801_02108_b200 as P
 from paper_1801_02108_b200 import _lib
-from paper_1801_02108_b200.layers import residual_unit_into
+from paper_1801_02108_b200.layers import residual_unit_into, sparse_residual_unit_into
 
 H, W, C, M = 400, 400, 64, 32
 block = int(os.environ.get("BLOCK", 16))
@@ -21,20 +21,36 @@ ms = [P.synth_mask_blobs((1, H, W), 1 - density, f).cuda() for f in range(nf)]
 u = P.random_unit_params(np.random.default_rng(0), C, M)
 spec = P.unit_spec((1, H, W, C), (block, block))
 lib = _lib.load()
+FUSED = os.environ.get("FUSED", "1") == "1"
+
+
+def run(f):
+    if FUSED:
+        sparse_residual_unit_into(xs[f], xs[f], ms[f].data, u, spec)
+        idx = P.reduce_mask(ms[f], spec)  # only for the block count
+        return idx
+    idx = P.reduce_mask(ms[f], spec)
+    residual_unit_into(xs[f], xs[f], u, spec, idx)
+    return idx
+
+
 for f in range(nf):
-    residual_unit_into(xs[f], xs[f], u, spec, P.reduce_mask(ms[f], spec))
+    run(f)
 torch.cuda.synchronize()
 buf = torch.zeros(4096 * 16, dtype=torch.int64, device=dev)
 names = ["entry", "prologue", "pdl+count", "loads", "barrier", "staged", "gemm1", "epi1", "gemm2",
          "epi2", "gemm3", "epi3"]
 for f in range(4):
-    idx = P.reduce_mask(ms[f], spec)
     torch.cuda.synchronize()
     buf.zero_()
     lib.sbn_debug_set_trace(buf.data_ptr())
-    residual_unit_into(xs[f], xs[f], u, spec, idx)
+    if FUSED:
+        sparse_residual_unit_into(xs[f], xs[f], ms[f].data, u, spec)
+    else:
+        residual_unit_into(xs[f], xs[f], u, spec, P.reduce_mask(ms[f], spec))
     torch.cuda.synchronize()
     lib.sbn_debug_set_trace(None)
+    idx = P.reduce_mask(ms[f], spec)
     t = buf.view(-1, 16).cpu().numpy().astype(np.int64)
     B = idx.count
     act = t[:B]
