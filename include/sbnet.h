@@ -146,13 +146,16 @@ int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
  * over each block's input window) -> fused unit -> scatter-add into out.  On the
  * tcgen05 path this is ONE kernel: the mask reduction is fused in front of the unit and
  * produces an unordered active list (blocks write disjoint windows, so the result does
- * not depend on the order).  ws: sbn_sparse_residual_unit_workspace bytes, zeroed once. */
+ * not depend on the order).  sync_ws: sbn_sparse_residual_unit_sync_bytes, zeroed ONCE by
+ * the caller and left zeroed by every call (barrier / look-back words at fixed offsets);
+ * ws: sbn_sparse_residual_unit_workspace bytes of scratch. */
+size_t sbn_sparse_residual_unit_sync_bytes(const sbn_geometry* g);
 size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* g, int halo,
                                           int algo);
 int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
                              const sbn_geometry* g, int halo, int pre_act,
-                             const sbn_unit_params* p, void* out, void* ws, size_t ws_bytes,
-                             int algo, sbn_stream_t stream);
+                             const sbn_unit_params* p, void* out, void* sync_ws, size_t sync_bytes,
+                             void* ws, size_t ws_bytes, int algo, sbn_stream_t stream);
 
 /* Which algorithm `algo=AUTO` would pick (SBN_ALGO_SIMT / SBN_ALGO_TCGEN05). */
 int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometry* g, int halo, int pre_act);

@@ -372,35 +372,45 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
 // ---- whole sparse_residual_unit (`layers.py:203-229`): mask -> active blocks -> fused unit.
 // tcgen05 path: ONE kernel (reduce_mask fused into the unit, unordered active list).
 // Otherwise: ordered sbn_reduce_mask + sbn_residual_unit.
-// Workspace: [idx (cap*12) | count | reduce_mask ws | residual-unit ws]
+// sync_ws (zeroed once, left zeroed): [unit barrier words (256 B) | reduce_mask ws]
+// ws (scratch):                      [idx (cap*12) | count | rim | packed image / SIMT scratch]
 static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
+
+extern "C" size_t sbn_sparse_residual_unit_sync_bytes(const sbn_geometry* gp) {
+  if (!gp) return 0;
+  return kBarBytes + al256(sbn_reduce_mask_workspace(gp));
+}
 
 extern "C" size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* gp,
                                                      int halo, int algo) {
   if (!gp || dtype_size(dtype) == 0) return 0;
   const size_t cap = (size_t)gp->n * gp->gy * gp->gx;
-  return al256(cap * 12) + 256 + al256(sbn_reduce_mask_workspace(gp)) +
-         sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
+  return al256(cap * 12) + 256 + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
 }
 
 extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
                                         const sbn_geometry* gp, int halo, int pre_act,
-                                        const sbn_unit_params* p, void* out, void* ws,
-                                        size_t ws_bytes, int algo, sbn_stream_t stream) {
+                                        const sbn_unit_params* p, void* out, void* sync_ws,
+                                        size_t sync_bytes, void* ws, size_t ws_bytes, int algo,
+                                        sbn_stream_t stream) {
   int st = check_geo(gp);
   if (st) return st;
   SBN_CHECK_ARG(x && mask && out && p, SBN_ERR_INVALID, "null pointer argument");
+  SBN_CHECK_ARG(sync_ws && sync_bytes >= sbn_sparse_residual_unit_sync_bytes(gp), SBN_ERR_WORKSPACE,
+                "sparse_residual_unit needs a %zu-byte zeroed sync workspace",
+                sbn_sparse_residual_unit_sync_bytes(gp));
   const size_t need = sbn_sparse_residual_unit_workspace(dtype, c, m, gp, halo, algo);
   SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
-                "sparse_residual_unit needs a %zu-byte zero-initialised workspace", need);
+                "sparse_residual_unit needs a %zu-byte workspace", need);
   const int cap = gp->n * gp->gy * gp->gx;
   if (cap <= 0) return SBN_OK;
   uint8_t* w8 = (uint8_t*)ws;
   int32_t* idx = (int32_t*)w8;
   int32_t* count = (int32_t*)(w8 + al256((size_t)cap * 12));
-  uint8_t* rmws = w8 + al256((size_t)cap * 12) + 256;
-  uint8_t* uws = rmws + al256(sbn_reduce_mask_workspace(gp));
-  const size_t uws_bytes = ws_bytes - (size_t)(uws - w8);
+  uint8_t* uws = w8 + al256((size_t)cap * 12) + 256;  // [barrier words unused here | rim | pack]
+  uint8_t* sync8 = (uint8_t*)sync_ws;
+  unsigned int* gbar = reinterpret_cast<unsigned int*>(sync8);
+  uint8_t* rmws = sync8 + kBarBytes;
   Geo g = to_geo(gp);
   cudaStream_t s = (cudaStream_t)stream;
   const bool tc = algo != SBN_ALGO_SIMT && unit_tc_supported(dtype, c, m, g, halo, pre_act);
@@ -418,13 +428,16 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
       packed = uws + rb;
     }
     const bool inplace = x == out;
-    return unit_tc_launch(x, out, inplace ? uws + kBarBytes : nullptr,
-                          reinterpret_cast<unsigned int*>(uws), c, m, g, p, packed, idx, count, cap,
-                          s, mask, idx, count);
+    return unit_tc_launch(x, out, inplace ? uws + kBarBytes : nullptr, gbar, c, m, g, p, packed,
+                          idx, count, cap, s, mask, idx, count);
   }
   st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws,
-                       al256(sbn_reduce_mask_workspace(gp)), stream);
+                       sync_bytes - kBarBytes, stream);
   if (st) return st;
+  // the two-launch path needs zeroed barrier words at the start of its workspace: the
+  // 256 barrier bytes of sync_ws are followed by the (zeroed) reduce_mask words, so point
+  // the unit at a scratch region whose first 256 bytes we clear here
+  cudaMemsetAsync(uws, 0, kBarBytes, s);
   return sbn_residual_unit(x, dtype, c, m, gp, halo, pre_act, p, idx, count, cap, out, uws,
-                           uws_bytes, algo, stream);
+                           ws_bytes - (size_t)(uws - w8), algo, stream);
 }

@@ -49,8 +49,10 @@ class _Scratch(threading.local):
         self.bufs = {}
 
     def get(self, nbytes: int, device, kind: str = "unit") -> torch.Tensor:
-        """Zero-initialised, cached per (device, stream, kind): each kind has its own
-        layout of self-resetting barrier words, so kinds must never share a buffer."""
+        """Zero-initialised, cached per (device, stream, kind); grows by reallocating (zeroed).
+        Kinds never share a buffer.  "*sync" kinds hold only self-resetting words (always
+        zero between calls), so reuse across geometries is safe; other kinds keep their
+        barrier words at offset 0 and free-form data after them."""
         key = (str(device), torch.cuda.current_stream(device).cuda_stream, kind)
         b = self.bufs.get(key)
         if b is None or b.numel() < nbytes:
@@ -331,12 +333,13 @@ def sparse_residual_unit_into(out: torch.Tensor, src: torch.Tensor, mask: torch.
     a = _algo(algo)
     nbytes = lib.sbn_sparse_residual_unit_workspace(dtype_code(dt), c, u.mid_channels, C.byref(g),
                                                     halo, a)
-    ws = _SCRATCH.get(nbytes, dev, "fused_unit")
+    ws = _SCRATCH.get(nbytes, dev, "fused_scratch")
+    sync = _SCRATCH.get(lib.sbn_sparse_residual_unit_sync_bytes(C.byref(g)), dev, "fused_sync")
     up = u.c_params(dt, dev, g if a != _lib.SBN_ALGO_SIMT else None, halo)
     st = lib.sbn_sparse_residual_unit(src.data_ptr(), mask.data_ptr(), dtype_code(dt), c,
                                       u.mid_channels, C.byref(g), halo, int(u.pre_activation),
-                                      C.byref(up), out.data_ptr(), ws.data_ptr(), ws.numel(), a,
-                                      _lib.stream_handle(dev))
+                                      C.byref(up), out.data_ptr(), sync.data_ptr(), sync.numel(),
+                                      ws.data_ptr(), ws.numel(), a, _lib.stream_handle(dev))
     _lib.check(st, "sparse_residual_unit")
 
 
