@@ -201,6 +201,109 @@ reduce_mask_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr
   }
 }
 
+// Small problems (the whole column-sum table fits in shared memory): ONE CTA of 1024
+// threads does everything — column sums for every block row straight from global
+// memory (all row loads of an item in flight), window sums per candidate, then an
+// in-CTA ordered scan — no ticket, no look-back, no workspace.
+constexpr int kSmallThreads = 1024;
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+reduce_mask_small_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr,
+                         int32_t* __restrict__ idx, int32_t* __restrict__ count, int vec) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int tiles = g.n * g.gy;
+  const int T = tiles * g.gx;
+  int* colsum = reinterpret_cast<int*>(sm);                 // [tiles][w]
+  uint8_t* flag = sm + (size_t)tiles * g.w * 4;              // [T]
+  __shared__ int wsum[kSmallThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double area = (double)g.bh * (double)g.bw;
+
+  // ---- 1. column sums of each block row's window rows
+  if (vec) {
+    const int wpr = g.w >> 2;
+    for (int i = tid; i < tiles * wpr; i += kSmallThreads) {
+      const int t = i / wpr, wi = i - t * wpr;
+      const int n = t / g.gy, by = t - n * g.gy;
+      const int wy0 = g.oy + by * g.sy;
+      const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
+      const uint32_t* base = reinterpret_cast<const uint32_t*>(mask + (size_t)n * g.h * g.w) + wi;
+      uint32_t v[16];
+      uint32_t acc = 0;
+      for (int y = y0; y < y1; y += 16) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = (y + r < y1) ? __ldg(base + (size_t)(y + r) * wpr) : 0u;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) acc += v[r];
+      }
+      int* cs = colsum + (size_t)t * g.w + 4 * wi;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cs[e] = (acc >> (8 * e)) & 0xffu;
+    }
+  } else {
+    for (int i = tid; i < tiles * g.w; i += kSmallThreads) {
+      const int t = i / g.w, x = i - t * g.w;
+      const int n = t / g.gy, by = t - n * g.gy;
+      const int wy0 = g.oy + by * g.sy;
+      const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
+      int acc = 0;
+      for (int y = y0; y < y1; ++y) acc += __ldg(mask + ((size_t)n * g.h + y) * g.w + x);
+      colsum[i] = acc;
+    }
+  }
+  __syncthreads();
+  // ---- 2. window sums -> flags
+  for (int c = tid; c < T; c += kSmallThreads) {
+    const int t = c / g.gx, bx = c - t * g.gx;
+    const int n = t / g.gy, by = t - n * g.gy;
+    const int wy0 = g.oy + by * g.sy;
+    const bool rows = max(wy0, 0) < min(wy0 + g.bh, g.h);
+    const int wx0 = g.ox + bx * g.sx;
+    const int xa = max(wx0, 0), xb = min(wx0 + g.bw, g.w);
+    int cnt = 0;
+    if (rows)
+      for (int x = xa; x < xb; ++x) cnt += colsum[(size_t)t * g.w + x];
+    flag[c] = pool == SBN_POOL_MAX ? (cnt > 0) : (((double)cnt / area) >= thr - 1e-12);
+  }
+  __syncthreads();
+  // ---- 3. ordered compaction: each thread owns a contiguous run of candidates
+  const int per = (T + kSmallThreads - 1) / kSmallThreads;
+  const int c0 = tid * per, c1 = min(c0 + per, T);
+  int mine = 0;
+  for (int c = c0; c < c1; ++c) mine += flag[c];
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int ws = wsum[lane];
+    int wi = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    wsum[lane] = wi - ws;  // exclusive warp offsets
+    if (lane == 31) *count = wi;
+  }
+  __syncthreads();
+  int pos = wsum[warp] + incl - mine;
+  for (int c = c0; c < c1; ++c) {
+    if (flag[c]) {
+      const int t = c / g.gx, bx = c - t * g.gx;
+      const int n = t / g.gy, by = t - n * g.gy;
+      idx[3 * pos] = n;
+      idx[3 * pos + 1] = by;
+      idx[3 * pos + 2] = bx;
+      ++pos;
+    }
+  }
+}
+
 __global__ void downsample_kernel(const uint8_t* __restrict__ in, int n, int h, int w, int f,
                                   int oh, int ow, uint8_t* __restrict__ out) {
   const long total = (long)n * oh * ow;
@@ -266,6 +369,20 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
     return launch_status("reduce_mask(empty)");
   }
   SBN_CHECK_ARG(tiles < (1l << 31), SBN_ERR_INVALID, "too many block rows");
+  {
+    const size_t small = (size_t)tiles * g.w * 4 + (size_t)tiles * g.gx;
+    if (small <= 200 * 1024 && (size_t)tiles * g.gx <= (size_t)kSmallThreads * 64) {
+      const int vec = ((g.w & 3) == 0) && (((uintptr_t)mask & 3) == 0) && g.bh < 256;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(reduce_mask_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024 + 16);
+        attr = true;
+      }
+      reduce_mask_small_kernel<<<1, kSmallThreads, small, s>>>(mask, g, pool, threshold, idx, count, vec);
+      return launch_status("reduce_mask(small)");
+    }
+  }
   // chunk of block columns whose column range fits the column-sum buffer
   int chunk = g.gx;
   if ((long)(chunk - 1) * g.sx + g.bw + 3 > kColBuf) chunk = (kColBuf - 3 - g.bw) / g.sx + 1;

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
                        tc::desc_kmajor_noswz(tc::smem_u32(A1 + 2 * k * K::P1 + t * 128 * 16), K::P1, 128),
                        tc::desc_kmajor_noswz(tc::smem_u32(B1 + 2 * k * K::PB1), K::PB1, 128), id1, k > 0);
       tc::mma_commit(&bar);
+      trace(a.trace, 12);
     }
     tc::mbar_wait(&bar, phase);
     phase ^= 1;
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
                          id2, (tap | k) > 0);
         }
       tc::mma_commit(&bar);
+      trace(a.trace, 13);
     }
     tc::mbar_wait(&bar, phase);
     phase ^= 1;
@@ -434,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
                        tc::desc_kmajor_noswz(tc::smem_u32(A3 + 2 * k * K::P3 + t * 128 * 16), K::P3, 128),
                        tc::desc_kmajor_noswz(tc::smem_u32(B3 + 2 * k * K::PB3), K::PB3, 128), id3, k > 0);
       tc::mma_commit(&bar);
+      trace(a.trace, 14);
     }
     tc::mbar_wait(&bar, phase);
     phase ^= 1;

@@ -61,3 +61,6 @@ for f in range(4):
     for i in range(11):
         print(f"   {names[i]:>10} -> {names[i + 1]:<10} median {np.median(d[:, i]) / 1e3:6.2f} us  max {d[:, i].max() / 1e3:6.2f}")
     print(f"   entry spread {(act[:, 0].max() - t0) / 1e3:.2f} us")
+    for nm, a_, b_ in (("gemm1 issue", 5, 12), ("gemm2 issue", 7, 13), ("gemm3 issue", 9, 14)):
+        dd = (act[:, b_] - act[:, a_]) / 1e3
+        print(f"   {nm:>12}: median {np.median(dd):.2f} us (issue of all MMAs + commit, thread 0)")
