@@ -331,7 +331,9 @@ def run_ours(args):
     # ---- CPU baseline: the oracle port of the reference's sparse_residual_unit
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(args.cpu_seconds, xs[0], masks[0], u, blk)
+        # pristine frame 0 (the ring frames have been updated in place by the timed steps)
+        x0 = torch.from_numpy(np.random.default_rng(1000).standard_normal((1, H, W, C), dtype=np.float32)).bfloat16()
+        cpu = cpu_baseline(args.cpu_seconds, x0, masks[0], u, blk)
 
     if rank == 0:
         line = {

@@ -14,6 +14,10 @@
 //     in a CUDA graph) without a memset.
 #include "common.cuh"
 
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
 namespace sbn {
 namespace {
 
@@ -201,48 +205,57 @@ reduce_mask_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr
   }
 }
 
-// Small problems (the whole column-sum table fits in shared memory): ONE CTA of 1024
-// threads does everything — column sums for every block row straight from global
-// memory (all row loads of an item in flight), window sums per candidate, then an
-// in-CTA ordered scan — no ticket, no look-back, no workspace.
-constexpr int kSmallThreads = 1024;
+// Moderate problems: ONE thread-block cluster (kClusterMax CTAs).  CTA r owns a contiguous
+// range of block rows; the per-CTA active counts are exchanged through distributed shared
+// memory (CTA 0's smem) with two cluster barriers — no global atomics, no look-back, no
+// workspace.  Each thread column-reduces one (block row, 4-column word) item with all of
+// its row loads in flight.
+constexpr int kClusterMax = 16;
+constexpr int kClusterThreads = 256;
 
-__global__ void __launch_bounds__(kSmallThreads, 1)
-reduce_mask_small_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr,
-                         int32_t* __restrict__ idx, int32_t* __restrict__ count, int vec) {
+__global__ void __launch_bounds__(kClusterThreads, 1)
+reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int per,
+                           int32_t* __restrict__ idx, int32_t* __restrict__ count, int vec) {
   extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ int s_cnt[kClusterMax];
+  __shared__ int wsum[kClusterThreads / 32];
+  __shared__ int s_base;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int ncl = (int)cl.num_blocks();
   const int tiles = g.n * g.gy;
-  const int T = tiles * g.gx;
-  int* colsum = reinterpret_cast<int*>(sm);                 // [tiles][w]
-  uint8_t* flag = sm + (size_t)tiles * g.w * 4;              // [T]
-  __shared__ int wsum[kSmallThreads / 32];
+  const int t0 = rank * per, t1 = min(t0 + per, tiles);
+  const int mt = max(t1 - t0, 0);
+  int* colsum = reinterpret_cast<int*>(sm);                 // [per][w]
+  uint8_t* flag = sm + (size_t)per * g.w * 4;                // [per * gx]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double area = (double)g.bh * (double)g.bw;
 
-  // ---- 1. column sums of each block row's window rows
   if (vec) {
     const int wpr = g.w >> 2;
-    for (int i = tid; i < tiles * wpr; i += kSmallThreads) {
-      const int t = i / wpr, wi = i - t * wpr;
+    for (int i = tid; i < mt * wpr; i += kClusterThreads) {
+      const int tl = i / wpr, wi = i - tl * wpr;
+      const int t = t0 + tl;
       const int n = t / g.gy, by = t - n * g.gy;
       const int wy0 = g.oy + by * g.sy;
       const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
       const uint32_t* base = reinterpret_cast<const uint32_t*>(mask + (size_t)n * g.h * g.w) + wi;
-      uint32_t v[16];
       uint32_t acc = 0;
       for (int y = y0; y < y1; y += 16) {
+        uint32_t v[16];
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = (y + r < y1) ? __ldg(base + (size_t)(y + r) * wpr) : 0u;
 #pragma unroll
         for (int r = 0; r < 16; ++r) acc += v[r];
       }
-      int* cs = colsum + (size_t)t * g.w + 4 * wi;
+      int* cs = colsum + (size_t)tl * g.w + 4 * wi;
 #pragma unroll
       for (int e = 0; e < 4; ++e) cs[e] = (acc >> (8 * e)) & 0xffu;
     }
   } else {
-    for (int i = tid; i < tiles * g.w; i += kSmallThreads) {
-      const int t = i / g.w, x = i - t * g.w;
+    for (int i = tid; i < mt * g.w; i += kClusterThreads) {
+      const int tl = i / g.w, x = i - tl * g.w;
+      const int t = t0 + tl;
       const int n = t / g.gy, by = t - n * g.gy;
       const int wy0 = g.oy + by * g.sy;
       const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
@@ -252,23 +265,24 @@ reduce_mask_small_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, doub
     }
   }
   __syncthreads();
-  // ---- 2. window sums -> flags
-  for (int c = tid; c < T; c += kSmallThreads) {
-    const int t = c / g.gx, bx = c - t * g.gx;
-    const int n = t / g.gy, by = t - n * g.gy;
+  const int T = mt * g.gx;
+  for (int c = tid; c < T; c += kClusterThreads) {
+    const int tl = c / g.gx, bx = c - tl * g.gx;
+    const int t = t0 + tl;
+    const int by = t % g.gy;
     const int wy0 = g.oy + by * g.sy;
     const bool rows = max(wy0, 0) < min(wy0 + g.bh, g.h);
     const int wx0 = g.ox + bx * g.sx;
     const int xa = max(wx0, 0), xb = min(wx0 + g.bw, g.w);
     int cnt = 0;
     if (rows)
-      for (int x = xa; x < xb; ++x) cnt += colsum[(size_t)t * g.w + x];
+      for (int x = xa; x < xb; ++x) cnt += colsum[(size_t)tl * g.w + x];
     flag[c] = pool == SBN_POOL_MAX ? (cnt > 0) : (((double)cnt / area) >= thr - 1e-12);
   }
   __syncthreads();
-  // ---- 3. ordered compaction: each thread owns a contiguous run of candidates
-  const int per = (T + kSmallThreads - 1) / kSmallThreads;
-  const int c0 = tid * per, c1 = min(c0 + per, T);
+  // per-thread contiguous run of candidates -> in-CTA exclusive scan
+  const int pc = (T + kClusterThreads - 1) / kClusterThreads;
+  const int c0 = min(tid * pc, T), c1 = min(c0 + pc, T);
   int mine = 0;
   for (int c = c0; c < c1; ++c) mine += flag[c];
   int incl = mine;
@@ -280,21 +294,37 @@ reduce_mask_small_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, doub
   if (lane == 31) wsum[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    int ws = wsum[lane];
+    const int ws = lane < kClusterThreads / 32 ? wsum[lane] : 0;
     int wi = ws;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= o) wi += v;
     }
-    wsum[lane] = wi - ws;  // exclusive warp offsets
-    if (lane == 31) *count = wi;
+    if (lane < kClusterThreads / 32) wsum[lane] = wi - ws;
+    if (lane == 31) {  // CTA total -> CTA 0's table (distributed shared memory)
+      int* remote = cl.map_shared_rank(s_cnt, 0);
+      remote[rank] = wi;
+    }
   }
-  __syncthreads();
-  int pos = wsum[warp] + incl - mine;
+  cl.sync();
+  if (tid == 0) {
+    const int* table = cl.map_shared_rank(s_cnt, 0);
+    int base = 0, total = 0;
+    for (int r = 0; r < ncl; ++r) {
+      const int v = table[r];
+      if (r < rank) base += v;
+      total += v;
+    }
+    s_base = base;
+    if (rank == 0) *count = total;
+  }
+  cl.sync();  // CTA 0's table stays alive until everyone has read it
+  int pos = s_base + wsum[warp] + incl - mine;
   for (int c = c0; c < c1; ++c) {
     if (flag[c]) {
-      const int t = c / g.gx, bx = c - t * g.gx;
+      const int tl = c / g.gx, bx = c - tl * g.gx;
+      const int t = t0 + tl;
       const int n = t / g.gy, by = t - n * g.gy;
       idx[3 * pos] = n;
       idx[3 * pos + 1] = by;
@@ -370,17 +400,36 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
   }
   SBN_CHECK_ARG(tiles < (1l << 31), SBN_ERR_INVALID, "too many block rows");
   {
-    const size_t small = (size_t)tiles * g.w * 4 + (size_t)tiles * g.gx;
-    if (small <= 200 * 1024 && (size_t)tiles * g.gx <= (size_t)kSmallThreads * 64) {
+    // one cluster of up to 16 CTAs when each CTA's block rows fit its shared memory
+    int cl = (int)(tiles < kClusterMax ? tiles : kClusterMax);
+    const int per = (int)((tiles + cl - 1) / cl);
+    cl = (int)((tiles + per - 1) / per);
+    const size_t smem = (size_t)per * g.w * 4 + (size_t)per * g.gx;
+    if (smem <= 160 * 1024) {
       const int vec = ((g.w & 3) == 0) && (((uintptr_t)mask & 3) == 0) && g.bh < 256;
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(reduce_mask_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024 + 16);
+        cudaFuncSetAttribute(reduce_mask_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024 + 16);
+        cudaFuncSetAttribute(reduce_mask_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr = true;
       }
-      reduce_mask_small_kernel<<<1, kSmallThreads, small, s>>>(mask, g, pool, threshold, idx, count, vec);
-      return launch_status("reduce_mask(small)");
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cl);
+      cfg.blockDim = dim3(kClusterThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cl;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, reduce_mask_cluster_kernel, mask, g, pool, threshold, per, idx,
+                             count, vec) == cudaSuccess)
+        return launch_status("reduce_mask(cluster)");
+      cudaGetLastError();  // cluster launch refused: fall through to the look-back kernel
     }
   }
   // chunk of block columns whose column range fits the column-sum buffer
