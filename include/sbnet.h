@@ -172,6 +172,11 @@ int sbn_selftest_umma(const void* a, const void* b, int rows, int shift, int pla
  * boundaries into buf[cta * 16 + phase] (buf: device memory, grid * 16 slots). */
 int sbn_debug_set_trace(unsigned long long* buf);
 
+/* Diagnostics: kernel-variant switches (returns the previous value).
+ * SBN_DEBUG_NO_PAIR: run the single-CTA tcgen05 unit instead of the CTA-pair variant. */
+enum { SBN_DEBUG_NO_PAIR = 1 };
+int sbn_debug_set_flags(int flags);
+
 /* Number of kernels the library has launched since load (for the bench's
  * gpu_launches claim). */
 uint64_t sbn_launch_count(void);

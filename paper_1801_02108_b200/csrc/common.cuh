@@ -102,6 +102,7 @@ __device__ __forceinline__ int ld_count(const int32_t* count, int cap) {
 // sbn_debug_set_trace() (passed to kernels as an argument; null check otherwise).
 constexpr int kTraceSlots = 16;
 unsigned long long* trace_buffer();  // host side: current buffer or nullptr
+int debug_flags();                   // host side: sbn_debug_set_flags()
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

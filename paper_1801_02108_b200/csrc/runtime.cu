@@ -53,8 +53,16 @@ int max_smem_optin() {
 }
 
 unsigned long long* trace_buffer() { return g_trace; }
+static int g_flags = 0;
+int debug_flags() { return g_flags; }
 
 }  // namespace sbn
+
+extern "C" int sbn_debug_set_flags(int flags) {
+  const int old = sbn::g_flags;
+  sbn::g_flags = flags;
+  return old;
+}
 
 extern "C" int sbn_debug_set_trace(unsigned long long* buf) {
   sbn::g_trace = buf;

@@ -24,6 +24,11 @@
 #include "unit.cuh"
 #include "tc_util.cuh"
 
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+namespace cg = cooperative_groups;
+
 namespace sbn {
 namespace {
 
@@ -91,6 +96,68 @@ struct TcArgs {
 
 __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
+// Fused reduce_mask (MAX pooling, `tiling.py:138-160`) used by the single-kernel
+// sparse_residual_unit: every CTA tests the windows of candidates blockIdx.x + j*grid
+// against the mask and appends the active ones to one list (one atomic slot per CTA and
+// round; order is irrelevant to the unit: blocks write disjoint windows).  A grid barrier
+// over all CTAs publishes the count; the last CTA out resets the words.  Returns B.
+__device__ __forceinline__ int fused_compact(const TcArgs& a) {
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ int s_flag[32];
+  __shared__ int s_base;
+  __shared__ int s_B;
+  const int T = g.n * g.gy * g.gx;
+  const int area = g.bh * g.bw;
+  unsigned int* fb = a.gbar + 2;  // [arrive, depart, slot]
+  for (int r0 = blockIdx.x; r0 < T; r0 += 32 * gridDim.x) {
+    const int nj = min(32, (T - r0 + (int)gridDim.x - 1) / (int)gridDim.x);
+    if (tid < 32) s_flag[tid] = 0;
+    __syncthreads();
+    for (int e = tid; e < nj * area; e += blockDim.x) {
+      const int j = e / area, p = e - j * area;
+      const int cand = r0 + j * gridDim.x;
+      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+      const int cy = rr / g.gx, cx = rr - cy * g.gx;
+      const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
+      if (y >= 0 && y < g.h && xx >= 0 && xx < g.w && __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx))
+        s_flag[j] = 1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const bool on = lane < nj && s_flag[lane];
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (lane == 0) s_base = bal ? (int)atomicAdd(fb + 2, (unsigned)__popc(bal)) : 0;
+      __syncwarp();
+      if (on) {
+        const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
+        const int cand = r0 + lane * gridDim.x;
+        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+        a.idx_out[3 * pos] = fr;
+        a.idx_out[3 * pos + 1] = rr / g.gx;
+        a.idx_out[3 * pos + 2] = rr % g.gx;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    atomicAdd(fb, 1u);
+    while (*reinterpret_cast<volatile unsigned int*>(fb) < gridDim.x) __nanosleep(32);
+    __threadfence();
+    s_B = (int)*reinterpret_cast<volatile unsigned int*>(fb + 2);
+    if (blockIdx.x == 0) *a.count_out = s_B;
+    if (atomicAdd(fb + 1, 1u) == gridDim.x - 1) {  // last out: reset for the next launch
+      fb[0] = 0u;
+      fb[1] = 0u;
+      fb[2] = 0u;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return s_B;
+}
+
 template <int C, int MC, int BS>
 __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(TcArgs a) {
   using K = Cfg<C, MC, BS>;
@@ -147,62 +214,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   int B;
   const int32_t* idx = a.idx;
   if (a.mask) {
-    // ---- fused reduce_mask (MAX pooling, `tiling.py:138-160`): every CTA tests the block
-    //      windows of candidates blockIdx.x + j*grid against the mask and appends the
-    //      active ones to one list (one atomic slot per CTA and round; order is irrelevant
-    //      to the unit: blocks write disjoint windows).  A grid barrier publishes the count.
-    __shared__ int s_flag[32];
-    __shared__ int s_base;
-    const int T = g.n * g.gy * g.gx;
-    const int area = g.bh * g.bw;
-    unsigned int* fb = a.gbar + 2;  // [arrive, depart, slot]
-    for (int r0 = blockIdx.x; r0 < T; r0 += 32 * gridDim.x) {
-      const int nj = min(32, (T - r0 + (int)gridDim.x - 1) / (int)gridDim.x);
-      if (tid < 32) s_flag[tid] = 0;
-      __syncthreads();
-      for (int e = tid; e < nj * area; e += kThreads) {
-        const int j = e / area, p = e - j * area;
-        const int cand = r0 + j * gridDim.x;
-        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-        const int cy = rr / g.gx, cx = rr - cy * g.gx;
-        const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
-        if (y >= 0 && y < g.h && xx >= 0 && xx < g.w && __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx))
-          s_flag[j] = 1;
-      }
-      __syncthreads();
-      if (warp == 0) {
-        const bool on = lane < nj && s_flag[lane];
-        const unsigned bal = __ballot_sync(0xffffffffu, on);
-        if (lane == 0) s_base = bal ? (int)atomicAdd(fb + 2, (unsigned)__popc(bal)) : 0;
-        __syncwarp();
-        if (on) {
-          const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
-          const int cand = r0 + lane * gridDim.x;
-          const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-          a.idx_out[3 * pos] = fr;
-          a.idx_out[3 * pos + 1] = rr / g.gx;
-          a.idx_out[3 * pos + 2] = rr % g.gx;
-        }
-      }
-    }
-    __shared__ int s_B;
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(fb, 1u);
-      while (*reinterpret_cast<volatile unsigned int*>(fb) < gridDim.x) __nanosleep(32);
-      __threadfence();
-      s_B = (int)*reinterpret_cast<volatile unsigned int*>(fb + 2);
-      if (blockIdx.x == 0) *a.count_out = s_B;
-      if (atomicAdd(fb + 1, 1u) == gridDim.x - 1) {  // last out: reset for the next launch
-        fb[0] = 0u;
-        fb[1] = 0u;
-        fb[2] = 0u;
-        __threadfence();
-      }
-    }
-    __syncthreads();
-    B = s_B;
+    B = fused_compact(a);
     idx = a.idx_out;
     if ((int)blockIdx.x < B) {
       n0 = __ldcg(idx + 3 * blockIdx.x);
@@ -574,6 +586,358 @@ int launch(const TcArgs& a, int cap, cudaStream_t s) {
   return launch_status("residual_unit_tcgen05");
 }
 
+
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (thread-block cluster of 2, block size with exactly two 128-row M-tiles,
+// e.g. 16x16): CTA rank r owns M-tile r of the block end to end — it stages only window
+// pixels [128r, 128r+128), runs 1-tile GEMMs, and its epilogues cover 128 rows with two
+// warps per TMEM lane quarter (column halves).  The 3x3 taps of tile 0 read A2 rows up to
+// 128 + 2*BS + 1, which belong to tile 1: rank 1 pushes those rows into rank 0's A2 with
+// DSMEM stores during epilogue 1, followed by one cluster barrier.  Per CTA this halves the
+// window traffic, the smem-bandwidth-bound GEMM2 MMA stream and the epilogue rows.
+template <int C, int MC, int BS>
+struct PairCfg {
+  using K = Cfg<C, MC, BS>;
+  static_assert(K::NT1 == 2 && K::NT2 == 2, "pair variant needs two M-tiles");
+  static constexpr int HALO_ROWS = 2 * BS + 2;
+  static constexpr int R2 = (128 + HALO_ROWS + 7) / 8 * 8;
+  static constexpr int P1 = 128 * 16 + 16;
+  static constexpr int P2 = R2 * 16 + 16;
+  static constexpr int P3 = 128 * 16 + 16;
+  static constexpr int al(int v) { return (v + 127) / 128 * 128; }
+  static constexpr int SZ_A1 = al((C / 8) * P1 > (MC / 8) * P3 ? (C / 8) * P1 : (MC / 8) * P3);
+  static constexpr int OFF_A2 = SZ_A1;
+  static constexpr int OFF_B1 = OFF_A2 + al((MC / 8) * P2);
+  static constexpr int IMG = K::SMEM - K::OFF_B1;  // same packed image as the single-CTA kernel
+  static constexpr int OFF_B2 = OFF_B1 + (K::OFF_B2 - K::OFF_B1);
+  static constexpr int OFF_B3 = OFF_B1 + (K::OFF_B3 - K::OFF_B1);
+  static constexpr int OFF_PAR = OFF_B1 + (K::OFF_PAR - K::OFF_B1);
+  static constexpr int SMEM = OFF_B1 + IMG;
+  static constexpr int COL1 = 0, COL2 = MC, COL3 = 2 * MC;
+  static constexpr int TCOLS = 2 * MC + C;
+  static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+  static_assert(MC % 32 == 0 && C % 32 == 0, "column halves of 16-column chunks");
+};
+
+template <int C, int MC, int BS>
+__global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
+  using K = Cfg<C, MC, BS>;
+  using PK = PairCfg<C, MC, BS>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, wbar;
+  __shared__ uint32_t tslot;
+  uint8_t* A1 = smem;
+  uint8_t* A2 = smem + PK::OFF_A2;
+  uint8_t* A3 = smem;
+  uint8_t* B1 = smem + PK::OFF_B1;
+  uint8_t* B2 = smem + PK::OFF_B2;
+  uint8_t* B3 = smem + PK::OFF_B3;
+  float* par = reinterpret_cast<float*>(smem + PK::OFF_PAR);
+  float* s1 = par;
+  float* t1 = s1 + C;
+  float* b3 = t1 + C;
+  float* b1 = b3 + C;
+  float* s2 = b1 + MC;
+  float* t2 = s2 + MC;
+  float* b2 = t2 + MC;
+  float* s3 = b2 + MC;
+  float* t3 = s3 + MC;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, hf = warp >> 2;  // TMEM lane quarter, column half
+  const Geo& g = a.g;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  trace(a.trace, 0);
+  if (tid == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_init(&wbar, 1);
+    tc::mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    tc::mbar_expect_tx(&wbar, PK::IMG);
+    tc::bulk_g2s(B1, a.packed, PK::IMG, &wbar);
+  }
+  if (warp == 0) tc::tmem_alloc<PK::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  uint32_t phase = 0;
+  bool weights_ready = false;
+  trace(a.trace, 1);
+  tc::pdl_wait();
+  int B;
+  const int32_t* idx = a.idx;
+  if (a.mask) {
+    B = fused_compact(a);
+    idx = a.idx_out;
+  } else {
+    B = ld_count(a.count, a.cap);
+  }
+  trace(a.trace, 2);
+  const bool inplace = a.x == a.out;
+  const bool resident = B <= npairs;
+  const __nv_bfloat16* rimsrc = nullptr;
+  if (inplace && !resident) {  // streamed in place: snapshot every block's rim first
+    const Rim r{BS, BS, 1};
+    const int Pr = r.pixels();
+    for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
+      const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
+      const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+      for (int i = tid; i < Pr * (C / 8); i += kThreads) {
+        const int rp = i / (C / 8), k = i % (C / 8);
+        int wy, wx;
+        r.coord(rp, wy, wx);
+        const int y = ys + wy, xx = xs + wx;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+          v = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
+        reinterpret_cast<uint4*>(a.rim_buf)[((size_t)blk * Pr + rp) * (C / 8) + k] = v;
+      }
+    }
+    grid_barrier(a.gbar, gridDim.x);
+    rimsrc = a.rim_buf;
+  }
+  if (resident && pair >= B) {  // idle pair
+    tc::mbar_wait(&wbar, 0);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
+    return;
+  }
+  const Rim rim{BS, BS, 1};
+  const int P = rim.pixels();
+  uint8_t* A2peer = rank > 0 ? cl.map_shared_rank(A2, rank - 1) : nullptr;
+
+  for (int blk = pair; blk < B; blk += npairs) {
+    const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
+    const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+    // ---- 1. stage my half of the window (pixels [128*rank, 128*rank + 128))
+    constexpr int TOT = 128 * (C / 8);
+    constexpr int ITEMS = TOT / kThreads;
+    uint4 raw[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int i = tid + it * kThreads;
+      const int pl = i / (C / 8), k = i % (C / 8);
+      const int p = rank * 128 + pl;
+      const int wy = p / BS, wx = p % BS;
+      const int y = ys + wy, xx = xs + wx;
+      raw[it] = make_uint4(0, 0, 0, 0);
+      if (p < K::NPIX) {
+        if (rimsrc && !rim.interior(wy, wx))
+          raw[it] = *(reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
+        else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+          raw[it] = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
+      }
+    }
+    trace(a.trace, 3);
+    if (inplace && resident) grid_arrive(a.gbar);
+    trace(a.trace, 4);
+    if (!weights_ready) {
+      tc::mbar_wait(&wbar, 0);
+      weights_ready = true;
+    }
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int i = tid + it * kThreads;
+      const int pl = i / (C / 8), k = i % (C / 8);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[it]);
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        const int ch = k * 8 + 2 * e;
+        const float v0 = fmaxf(__fadd_rn(__fmul_rn(f.x, s1[ch]), t1[ch]), 0.f);
+        const float v1 = fmaxf(__fadd_rn(__fmul_rn(f.y, s1[ch + 1]), t1[ch + 1]), 0.f);
+        o[e] = tc::pack_bf16(v0, v1);
+      }
+      *reinterpret_cast<uint4*>(A1 + k * PK::P1 + pl * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    tc::fence_async_smem();
+    __syncthreads();
+    trace(a.trace, 5);
+    // ---- 2. GEMM1 (one tile)
+    if (tid == 0) {
+      tc::fence_after();
+      constexpr uint32_t id1 = tc::idesc_bf16_f32(128, MC);
+#pragma unroll
+      for (int k = 0; k < C / 16; ++k)
+        tc::mma_bf16(tmem + PK::COL1,
+                     tc::desc_kmajor_noswz(tc::smem_u32(A1 + 2 * k * PK::P1), PK::P1, 128),
+                     tc::desc_kmajor_noswz(tc::smem_u32(B1 + 2 * k * K::PB1), K::PB1, 128), id1, k > 0);
+      tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+    trace(a.trace, 6);
+    // ---- 3. epilogue 1 -> A2 (local rows; rank>0 also feeds the previous tile's halo rows)
+    {
+      const int j = q * 32 + lane;
+      const int r = rank * 128 + j;
+      const int wy = r / BS, wx = r % BS;
+      const int y = ys + wy, xx = xs + wx;
+      const bool valid = r < K::NPIX && y >= 0 && y < g.h && xx >= 0 && xx < g.w;
+#pragma unroll
+      for (int c0 = hf * (MC / 2); c0 < (hf + 1) * (MC / 2); c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + PK::COL1 + c0, v);
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b1[c0 + 2 * e]));
+          float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b1[c0 + 2 * e + 1]));
+          u0 = fmaxf(__fadd_rn(__fmul_rn(u0, s2[c0 + 2 * e]), t2[c0 + 2 * e]), 0.f);
+          u1 = fmaxf(__fadd_rn(__fmul_rn(u1, s2[c0 + 2 * e + 1]), t2[c0 + 2 * e + 1]), 0.f);
+          o[e] = valid ? tc::pack_bf16(u0, u1) : 0u;
+        }
+        const uint4 lo = make_uint4(o[0], o[1], o[2], o[3]), hi = make_uint4(o[4], o[5], o[6], o[7]);
+        *reinterpret_cast<uint4*>(A2 + (c0 / 8) * PK::P2 + j * 16) = lo;
+        *reinterpret_cast<uint4*>(A2 + (c0 / 8 + 1) * PK::P2 + j * 16) = hi;
+        if (rank > 0 && j < PK::HALO_ROWS) {
+          *reinterpret_cast<uint4*>(A2peer + (c0 / 8) * PK::P2 + (128 + j) * 16) = lo;
+          *reinterpret_cast<uint4*>(A2peer + (c0 / 8 + 1) * PK::P2 + (128 + j) * 16) = hi;
+        }
+      }
+    }
+    tc::fence_before();
+    asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+    cl.sync();  // A2 halo rows from the partner have landed
+    tc::fence_async_smem();
+    trace(a.trace, 7);
+    // ---- 4. GEMM2: 9 row-shifted views of A2 (local rows 0 .. 127 + shift)
+    if (tid == 0) {
+      tc::fence_after();
+      constexpr uint32_t id2 = tc::idesc_bf16_f32(128, MC);
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const int shift = (tap / 3) * BS + (tap % 3);
+#pragma unroll
+        for (int k = 0; k < MC / 16; ++k)
+          tc::mma_bf16(tmem + PK::COL2,
+                       tc::desc_kmajor_noswz(tc::smem_u32(A2 + 2 * k * PK::P2 + shift * 16), PK::P2, 128),
+                       tc::desc_kmajor_noswz(tc::smem_u32(B2 + tap * K::TAPB + 2 * k * K::PB2), K::PB2, 128),
+                       id2, (tap | k) > 0);
+      }
+      tc::mma_commit(&bar);
+      trace(a.trace, 13);
+    }
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+    trace(a.trace, 8);
+    // ---- 5. epilogue 2 -> A3; prefetch this row's residual half
+    const int j = q * 32 + lane;
+    const int o_row = rank * 128 + j;
+    const int oy = o_row / BS, ox = o_row % BS;
+    const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+    const bool store = oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow;
+    uint4* op = reinterpret_cast<uint4*>(a.out) +
+                (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (C / 8) + hf * (C / 16);
+    uint4 res[C / 16];
+    if (store) {
+#pragma unroll
+      for (int k = 0; k < C / 16; ++k) res[k] = op[k];
+    }
+#pragma unroll
+    for (int c0 = hf * (MC / 2); c0 < (hf + 1) * (MC / 2); c0 += 16) {
+      float v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + PK::COL2 + c0, v);
+      uint32_t o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b2[c0 + 2 * e]));
+        float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b2[c0 + 2 * e + 1]));
+        u0 = fmaxf(__fadd_rn(__fmul_rn(u0, s3[c0 + 2 * e]), t3[c0 + 2 * e]), 0.f);
+        u1 = fmaxf(__fadd_rn(__fmul_rn(u1, s3[c0 + 2 * e + 1]), t3[c0 + 2 * e + 1]), 0.f);
+        o[e] = tc::pack_bf16(u0, u1);
+      }
+      *reinterpret_cast<uint4*>(A3 + (c0 / 8) * PK::P3 + j * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(A3 + (c0 / 8 + 1) * PK::P3 + j * 16) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+    tc::fence_before();
+    tc::fence_async_smem();
+    __syncthreads();
+    trace(a.trace, 9);
+    // ---- 6. GEMM3
+    if (tid == 0) {
+      tc::fence_after();
+      constexpr uint32_t id3 = tc::idesc_bf16_f32(128, C);
+#pragma unroll
+      for (int k = 0; k < MC / 16; ++k)
+        tc::mma_bf16(tmem + PK::COL3,
+                     tc::desc_kmajor_noswz(tc::smem_u32(A3 + 2 * k * PK::P3), PK::P3, 128),
+                     tc::desc_kmajor_noswz(tc::smem_u32(B3 + 2 * k * K::PB3), K::PB3, 128), id3, k > 0);
+      tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc::fence_after();
+    if (inplace && resident) grid_wait(a.gbar, 2u * (unsigned)B);
+    trace(a.trace, 10);
+    // ---- 7. epilogue 3: +b3 + residual, my column half of my rows
+#pragma unroll
+    for (int cc = 0; cc < C / 2; cc += 16) {
+      const int c0 = hf * (C / 2) + cc;
+      float v[16];
+      tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + PK::COL3 + c0, v);
+      if (store) {
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&res[cc / 8]);
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float2 xf = __bfloat1622float2(xh[e]);
+          const float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b3[c0 + 2 * e]));
+          const float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b3[c0 + 2 * e + 1]));
+          o[e] = tc::pack_bf16(__fadd_rn(xf.x, u0), __fadd_rn(xf.y, u1));
+        }
+        op[cc / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+        op[cc / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+    trace(a.trace, 11);
+    if (blk + npairs < B) cl.sync();  // partner done with my A2 before it writes the next halo
+  }
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
+}
+
+template <int C, int MC, int BS>
+int launch_pair(const TcArgs& a, int cap, cudaStream_t s) {
+  using PK = PairCfg<C, MC, BS>;
+  auto kern = unit_tc_pair_kernel<C, MC, BS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PK::SMEM);
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = PK::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  int maxcl = 0;
+  cfg.gridDim = dim3(2);
+  cudaOccupancyMaxActiveClusters(&maxcl, kern, &cfg);
+  if (maxcl < 1) maxcl = sm_count() / 2;
+  long pairs = cap < maxcl ? cap : maxcl;  // all pairs co-resident (grid barriers)
+  if (pairs < 1) pairs = 1;
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cudaLaunchKernelEx(&cfg, kern, a);
+  return launch_status("residual_unit_tcgen05_pair");
+}
+
 #define SBN_UNIT_TC_CONFIGS(X) \
   X(64, 32, 16)                \
   X(64, 32, 8)                 \
@@ -642,6 +1006,11 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
   a.packed = (const uint8_t*)packed;
   a.rim_buf = (__nv_bfloat16*)rim_buf;
   a.gbar = gbar;
+  if (!(debug_flags() & SBN_DEBUG_NO_PAIR)) {
+    if (c == 64 && m == 32 && g.bh == 16) return launch_pair<64, 32, 16>(a, cap, s);
+    if (c == 64 && m == 64 && g.bh == 16) return launch_pair<64, 64, 16>(a, cap, s);
+    if (c == 128 && m == 64 && g.bh == 16) return launch_pair<128, 64, 16>(a, cap, s);
+  }
 #define X(C_, M_, B_) if (c == C_ && m == M_ && g.bh == B_) return launch<C_, M_, B_>(a, cap, s);
   SBN_UNIT_TC_CONFIGS(X)
 #undef X

@@ -432,3 +432,33 @@ def test_fused_mask_unit_bit_identical_to_two_launch_path(cuda_device, density, 
         xi = x.clone()
         P.sparse_residual_unit(P.Tensor4D(xi), mk, u, (16, 16), inplace=True)
         assert torch.equal(xi, ref)
+
+
+@pytest.mark.parametrize("density,nframes", [(0.1, 1), (0.5, 2), (1.0, 3)])
+def test_unit_cta_pair_variant_bit_identical_to_single_cta(cuda_device, density, nframes):
+    """The CTA-pair tcgen05 unit (two CTAs per block, DSMEM halo rows) computes exactly what
+    the single-CTA kernel computes: fused and two-launch entry points, in place (resident
+    and streamed: 3 full frames exceed the co-resident pairs) and functional."""
+    from paper_1801_02108_b200.layers import residual_unit_into
+    lib = _lib.load()
+    rng = np.random.default_rng(12)
+    x = torch.from_numpy(rng.standard_normal((nframes, 240, 224, 64)).astype(np.float32)).bfloat16().cuda()
+    u = P.random_unit_params(rng, 64, 32)
+    mk = (P.synth_mask_blobs((nframes, 240, 224), 1.0 - density, 9) if density < 1 else
+          P.BinaryMask.full(nframes, 240, 224)).cuda()
+    spec = P.unit_spec(tuple(x.shape), (16, 16))
+    outs = []
+    for flags in (1, 0):
+        old = lib.sbn_debug_set_flags(flags)
+        try:
+            a = P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16)).data
+            b = x.clone()
+            P.sparse_residual_unit(P.Tensor4D(b), mk, u, (16, 16), inplace=True)
+            c = x.clone()
+            residual_unit_into(c, c, u, spec, P.reduce_mask(mk, spec))
+            torch.cuda.synchronize()
+        finally:
+            lib.sbn_debug_set_flags(old)
+        assert torch.equal(a, b) and torch.equal(a, c)
+        outs.append(a)
+    assert torch.equal(outs[0], outs[1])
