@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--frames", type=int, default=32,
                     help="ring of distinct frames; the blocks touched across the ring exceed L2")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-conv-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -328,6 +329,13 @@ def run_ours(args):
             sweep[f"{d:.1f}"] = {"density_achieved": round(float(mk.data.float().mean()), 4),
                                  "sparse_ms": round(t_sp, 5), "speedup_vs_dense": round(dense_ms / t_sp, 3)}
 
+    # ---- config 3: single 3x3 conv, 800x700x128 bf16, top-left masks (paper protocol,
+    #      PAPER.md:397-398), blocks 8/16, sparse (reduce_mask + tcgen05 fused conv into a
+    #      reused output buffer) vs dense cuDNN conv
+    conv_sweep = None
+    if not args.no_conv_sweep and rank == 0:
+        conv_sweep = run_conv_sweep(P, torch, dev, time_graph)
+
     # ---- CPU baseline: the oracle port of the reference's sparse_residual_unit
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -364,10 +372,61 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "sweep": sweep,
+            "conv_sweep": conv_sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_conv_sweep(P, torch, dev, time_graph):
+    import numpy as np
+    from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_into
+    from paper_1801_02108_b200.ops import dense_conv_nhwc
+    Hc, Wc, Cc = 800, 700, 128
+    nfr = 8  # 8 x 143 MB frames: inputs larger than L2
+    rng = np.random.default_rng(3)
+    xs = [torch.randn(1, Hc, Wc, Cc, device=dev).bfloat16() for _ in range(nfr)]
+    w = torch.from_numpy((rng.standard_normal((3, 3, Cc, Cc)) / np.sqrt(9 * Cc)).astype(np.float32)).bfloat16()
+    b = torch.from_numpy(rng.standard_normal(Cc).astype(np.float32)).bfloat16()
+    fb = P.FilterBank(w, b)
+    p = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, Cc)
+    out = torch.zeros(1, Hc, Wc, Cc, device=dev).bfloat16()
+    wd, bd = fb.device_tensors(torch.bfloat16, dev)
+    reps = 40
+
+    def timed(fn):
+        g, st = time_graph(torch, fn, reps, 2, soak_s=0.05)
+        with torch.cuda.stream(st):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(st)
+            g.replay()
+            b_.record(st)
+            b_.synchronize()
+        return a_.elapsed_time(b_) / reps
+
+    def dense(k):
+        for i in range(k):
+            dense_conv_nhwc(xs[i % nfr], wd, bd, (1, 1), (1, 1))
+    dense_ms = timed(dense)
+    res = {"workload": "config3: 3x3 SAME conv, N=1 800x700x128 bf16, top-left mask", "dense_ms": round(dense_ms, 5),
+           "flops_dense": 2 * Hc * Wc * 9 * Cc * Cc, "rows": []}
+    for d in (0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 0.9, 1.0):
+        mk = P.synth_mask_topleft((1, Hc, Wc), 1.0 - d).cuda()
+        for blk in (8, 16):
+            spec = P.compute_block_spec((1, Hc, Wc, Cc), p, (blk, blk))
+            algo = sparse_conv_algo(torch.bfloat16, fb, p, spec)
+
+            def sp(k, mk=mk, spec=spec):
+                for i in range(k):
+                    sparse_conv_into(xs[i % nfr], out, fb, p, spec, P.reduce_mask(mk, spec))
+            t = timed(sp)
+            nb = P.reduce_mask(mk, spec).count
+            flops = nb * 2 * spec.out_block_size[0] * spec.out_block_size[1] * 9 * Cc * Cc
+            res["rows"].append({"density": d, "block": blk, "blocks": nb, "algo": algo,
+                                "sparse_ms": round(t, 5), "speedup_vs_dense": round(dense_ms / t, 3),
+                                "tflops_alg": round(flops / (t * 1e-3) / 1e12, 1)})
+    return res
 
 
 def cpu_baseline(seconds, x_dev, mask, u, blk):

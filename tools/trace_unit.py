@@ -53,9 +53,9 @@ for f in range(4):
     idx = P.reduce_mask(ms[f], spec)
     t = buf.view(-1, 16).cpu().numpy().astype(np.int64)
     B = idx.count
-    act = t[:B]
+    act = t[t[:, 11] > 0]  # CTAs that processed a block (2 per block in the CTA-pair variant)
     t0 = act[:, 0].min()
-    print(f"frame {f}: B={B}, span {(act[:, 11].max() - t0) / 1e3:.2f} us "
+    print(f"frame {f}: B={B}, grid {int((t[:, 0] > 0).sum())} CTAs, active {len(act)}, span {(act[:, 11].max() - t0) / 1e3:.2f} us "
           f"(first entry -> last epi3 end); idle CTAs: {int((t[B:, 0] > 0).sum())}")
     d = np.diff(act[:, :12], axis=1)
     for i in range(11):
