@@ -176,6 +176,9 @@ int sbn_debug_set_trace(unsigned long long* buf);
  * SBN_DEBUG_NO_PAIR: run the single-CTA tcgen05 unit instead of the CTA-pair variant. */
 enum { SBN_DEBUG_NO_PAIR = 1 };
 int sbn_debug_set_flags(int flags);
+/* Diagnostics: occupancy the last tcgen05 unit launch computed (0: CTAs/SM of the
+ * single-CTA kernel, 1: co-resident clusters of the CTA-pair kernel). */
+int sbn_debug_last_occupancy(int which);
 
 /* Number of kernels the library has launched since load (for the bench's
  * gpu_launches claim). */

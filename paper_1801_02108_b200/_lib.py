@@ -65,6 +65,7 @@ _PROTOS = {
     "sbn_selftest_umma": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "sbn_debug_set_trace": (_I, [_P]),
     "sbn_debug_set_flags": (_I, [_I]),
+    "sbn_debug_last_occupancy": (_I, [_I]),
     "sbn_sparse_residual_unit_sync_bytes": (C.c_size_t, [_G]),
     "sbn_sparse_residual_unit_workspace": (C.c_size_t, [_I, _I, _I, _G, _I, _I]),
     "sbn_sparse_residual_unit": (_I, [_P, _P, _I, _I, _I, _G, _I, _I, C.POINTER(UnitParams), _P, _P,

@@ -33,6 +33,7 @@ namespace sbn {
 namespace {
 
 constexpr int kThreads = 256;
+int g_last_occ[2] = {0, 0};  // diagnostics: last occupancy (CTAs/SM single, clusters pair)
 
 template <int C, int MC, int BS>
 struct Cfg {
@@ -566,10 +567,13 @@ int launch(const TcArgs& a, int cap, cudaStream_t s) {
   static bool attr = false;  // per-instantiation; attribute is per-function, idempotent
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     attr = true;
   }
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, K::SMEM);
+  g_last_occ[0] = occ;
   if (occ < 1) occ = 1;
   if (occ > K::OCC) occ = K::OCC;
   cudaLaunchConfig_t cfg = {};
@@ -914,6 +918,8 @@ int launch_pair(const TcArgs& a, int cap, cudaStream_t s) {
   using PK = PairCfg<C, MC, BS>;
   auto kern = unit_tc_pair_kernel<C, MC, BS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PK::SMEM);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = PK::SMEM;
@@ -931,6 +937,7 @@ int launch_pair(const TcArgs& a, int cap, cudaStream_t s) {
   cfg.gridDim = dim3(2);
   cudaOccupancyMaxActiveClusters(&maxcl, kern, &cfg);
   if (maxcl < 1) maxcl = sm_count() / 2;
+  g_last_occ[1] = maxcl;
   long pairs = cap < maxcl ? cap : maxcl;  // all pairs co-resident (grid barriers)
   if (pairs < 1) pairs = 1;
   cfg.gridDim = dim3((unsigned)(2 * pairs));
@@ -1019,3 +1026,5 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
 }
 
 }  // namespace sbn
+
+extern "C" int sbn_debug_last_occupancy(int which) { return sbn::g_last_occ[which & 1]; }

@@ -22,4 +22,5 @@ for flags in (1, 0):
     lib.sbn_debug_set_trace(None)
     t = buf.view(-1, 16).cpu().numpy()
     print("pair" if flags == 0 else "single", "grid", int((t[:, 0] > 0).sum()), "active", int((t[:, 11] > 0).sum()),
-          "span_us", (t[t[:, 11] > 0, 11].max() - t[t[:, 0] > 0, 0].min()) / 1e3)
+          "span_us", (t[t[:, 11] > 0, 11].max() - t[t[:, 0] > 0, 0].min()) / 1e3,
+          "occ", lib.sbn_debug_last_occupancy(0), "clusters", lib.sbn_debug_last_occupancy(1))
