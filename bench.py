@@ -44,6 +44,7 @@ def parse():
                     help="ring of distinct frames; the blocks touched across the ring exceed L2")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-conv-sweep", action="store_true")
+    ap.add_argument("--no-gather-scatter", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -336,6 +337,11 @@ def run_ours(args):
     if not args.no_conv_sweep and rank == 0:
         conv_sweep = run_conv_sweep(P, torch, dev, time_graph)
 
+    # ---- standalone gather / scatter bandwidth (north star: >70% of HBM peak)
+    gs = None
+    if not args.no_gather_scatter and rank == 0:
+        gs = run_gather_scatter(P, torch, dev, time_graph, hbm_peak)
+
     # ---- CPU baseline: the oracle port of the reference's sparse_residual_unit
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -373,10 +379,69 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "sweep": sweep,
             "conv_sweep": conv_sweep,
+            "gather_scatter": gs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_gather_scatter(P, torch, dev, time_graph, hbm_peak):
+    """sbn_gather / sbn_scatter(add) on 800x700x128 bf16 with a full mask and 16x16 blocks
+    (config-3 sizes, 100% density: ~190 MB block stack); algorithmic bytes = in-image
+    window reads + stack writes (gather), stack reads + clipped window writes (+ dst reads
+    for add) (scatter), per SURVEY §8(d)."""
+    import ctypes as C
+    from paper_1801_02108_b200 import _lib
+    lib = _lib.load()
+    Hc, Wc, Cc = 800, 700, 128
+    x = torch.randn(1, Hc, Wc, Cc, device=dev).bfloat16()
+    dst = torch.zeros_like(x)
+    p = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, Cc)
+    spec = P.compute_block_spec((1, Hc, Wc, Cc), p, (16, 16))
+    idx = P.reduce_mask(P.BinaryMask.full(1, Hc, Wc).cuda(), spec)
+    B = idx.count
+    stack = torch.empty(B, 16, 16, Cc, device=dev, dtype=torch.bfloat16)
+    blocks = torch.randn(B, 14, 14, Cc, device=dev).bfloat16()
+    g = spec.c_geometry(1)
+    sh = _lib.stream_handle
+
+    def gat(k):
+        for _ in range(k):
+            _lib.check(lib.sbn_gather(x.data_ptr(), _lib.SBN_BF16, Cc, C.byref(g), idx.rows.data_ptr(),
+                                      idx.count_dev.data_ptr(), B, 0, stack.data_ptr(), sh(dev)), "gather")
+
+    def sca(k, add=0):
+        for _ in range(k):
+            _lib.check(lib.sbn_scatter(blocks.data_ptr(), _lib.SBN_BF16, Cc, C.byref(g), idx.rows.data_ptr(),
+                                       idx.count_dev.data_ptr(), B, add, 0, dst.data_ptr(), sh(dev)), "scatter")
+
+    def timed(fn, reps=20):
+        gr, st = time_graph(torch, fn, reps, 3, soak_s=0.05)
+        with torch.cuda.stream(st):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(st)
+            gr.replay()
+            b_.record(st)
+            b_.synchronize()
+        return a_.elapsed_time(b_) / reps
+
+    ent = idx.entries
+    (oy, ox), (sy, sx) = spec.grid_origin, spec.in_stride
+    win = sum((min(oy + by * sy + 16, Hc) - max(oy + by * sy, 0)) * (min(ox + bx * sx + 16, Wc) - max(ox + bx * sx, 0))
+              for _, by, bx in ent)
+    outp = sum((min(by * 14 + 14, Hc) - by * 14) * (min(bx * 14 + 14, Wc) - bx * 14) for _, by, bx in ent)
+    e = Cc * 2
+    g_bytes = (win + B * 256) * e
+    s_bytes = (B * 196 + outp) * e
+    a_bytes = (B * 196 + 2 * outp) * e
+    t_g, t_s, t_a = timed(gat), timed(sca), timed(lambda k: sca(k, 1))
+    r = lambda by_, t: round(by_ / (t * 1e-3) / 1e9, 1)  # noqa: E731
+    return {"workload": "800x700x128 bf16, full mask, 16x16 blocks (SAME 3x3 geometry)", "blocks": B,
+            "gather": {"ms": round(t_g, 4), "alg_bytes": g_bytes, "GBps": r(g_bytes, t_g), "frac": round(g_bytes / (t_g * 1e-3) / 1e9 / hbm_peak, 3)},
+            "scatter": {"ms": round(t_s, 4), "alg_bytes": s_bytes, "GBps": r(s_bytes, t_s), "frac": round(s_bytes / (t_s * 1e-3) / 1e9 / hbm_peak, 3)},
+            "scatter_add": {"ms": round(t_a, 4), "alg_bytes": a_bytes, "GBps": r(a_bytes, t_a), "frac": round(a_bytes / (t_a * 1e-3) / 1e9 / hbm_peak, 3)},
+            "peak_GBps": hbm_peak}
 
 
 def run_conv_sweep(P, torch, dev, time_graph):

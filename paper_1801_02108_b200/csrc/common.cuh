@@ -103,13 +103,21 @@ __device__ __forceinline__ int ld_count(const int32_t* count, int cap) {
 constexpr int kTraceSlots = 16;
 unsigned long long* trace_buffer();  // host side: current buffer or nullptr
 int debug_flags();                   // host side: sbn_debug_set_flags()
+enum { kDebugNoPair = 1 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 __device__ __forceinline__ void trace(unsigned long long* tb, int phase) {
-  if (tb && threadIdx.x == 0) tb[blockIdx.x * kTraceSlots + phase] = gtimer();
+  if (tb && threadIdx.x == 0) {
+    tb[blockIdx.x * kTraceSlots + phase] = gtimer();
+    if (phase == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tb[blockIdx.x * kTraceSlots + 15] = smid;
+    }
+  }
 }
 
 // Grid-wide barrier among `expected` co-resident CTAs (caller guarantees residency).

@@ -33,7 +33,7 @@ namespace sbn {
 namespace {
 
 constexpr int kThreads = 256;
-int g_last_occ[2] = {0, 0};  // diagnostics: last occupancy (CTAs/SM single, clusters pair)
+int g_last_occ[8] = {0};  // diagnostics: occ single, clusters pair, regs, static smem, max dyn, dyn
 
 template <int C, int MC, int BS>
 struct Cfg {
@@ -560,6 +560,29 @@ size_t packed_bytes() {
   return (size_t)(Cfg<C, MC, BS>::SMEM - Cfg<C, MC, BS>::OFF_B1);
 }
 
+// CTAs per SM that are guaranteed co-resident (grid barriers depend on it).  The CUDA
+// occupancy API reports 1 for these tcgen05 kernels although the hardware co-schedules
+// more (verified with tools/coresidency_probe.py: 296 CTAs on 148 SMs entered within
+// 1.1 us), so residency is computed from the real per-SM limits: registers, shared
+// memory, threads, and TMEM columns (512 per SM).
+template <typename KernT>
+int resident_per_sm(KernT kern, int threads, int dyn_smem, int tmem_cols, int cap_bound) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
+  const int warps = (threads + 31) / 32;
+  const int regs_per_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+  const int by_regs = 65536 / (regs_per_warp * warps);
+  const int by_smem = (228 * 1024) / (dyn_smem + (int)fa.sharedSizeBytes + 1024);
+  const int by_thr = 2048 / threads;
+  const int by_tmem = 512 / tmem_cols;
+  int r = by_regs;
+  if (by_smem < r) r = by_smem;
+  if (by_thr < r) r = by_thr;
+  if (by_tmem < r) r = by_tmem;
+  if (cap_bound < r) r = cap_bound;
+  return r < 1 ? 1 : r;
+}
+
 template <int C, int MC, int BS>
 int launch(const TcArgs& a, int cap, cudaStream_t s) {
   using K = Cfg<C, MC, BS>;
@@ -571,9 +594,18 @@ int launch(const TcArgs& a, int cap, cudaStream_t s) {
                          cudaSharedmemCarveoutMaxShared);
     attr = true;
   }
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, K::SMEM);
+  int occ = resident_per_sm(kern, kThreads, K::SMEM, K::TALLOC, K::OCC);
   g_last_occ[0] = occ;
+  {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
+      g_last_occ[2] = fa.numRegs;
+      g_last_occ[3] = (int)fa.sharedSizeBytes;
+      g_last_occ[4] = fa.maxDynamicSharedSizeBytes;
+      g_last_occ[5] = K::SMEM;
+      g_last_occ[6] = (int)fa.localSizeBytes;
+    }
+  }
   if (occ < 1) occ = 1;
   if (occ > K::OCC) occ = K::OCC;
   cudaLaunchConfig_t cfg = {};
@@ -933,10 +965,8 @@ int launch_pair(const TcArgs& a, int cap, cudaStream_t s) {
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  int maxcl = 0;
-  cfg.gridDim = dim3(2);
-  cudaOccupancyMaxActiveClusters(&maxcl, kern, &cfg);
-  if (maxcl < 1) maxcl = sm_count() / 2;
+  const int per_sm = resident_per_sm(kern, kThreads, PK::SMEM, PK::TALLOC, 2);
+  const int maxcl = sm_count() * per_sm / 2;
   g_last_occ[1] = maxcl;
   long pairs = cap < maxcl ? cap : maxcl;  // all pairs co-resident (grid barriers)
   if (pairs < 1) pairs = 1;
@@ -1013,7 +1043,7 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
   a.packed = (const uint8_t*)packed;
   a.rim_buf = (__nv_bfloat16*)rim_buf;
   a.gbar = gbar;
-  if (!(debug_flags() & SBN_DEBUG_NO_PAIR)) {
+  if (!(debug_flags() & kDebugNoPair)) {
     if (c == 64 && m == 32 && g.bh == 16) return launch_pair<64, 32, 16>(a, cap, s);
     if (c == 64 && m == 64 && g.bh == 16) return launch_pair<64, 64, 16>(a, cap, s);
     if (c == 128 && m == 64 && g.bh == 16) return launch_pair<128, 64, 16>(a, cap, s);
@@ -1027,4 +1057,4 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
 
 }  // namespace sbn
 
-extern "C" int sbn_debug_last_occupancy(int which) { return sbn::g_last_occ[which & 1]; }
+extern "C" int sbn_debug_last_occupancy(int which) { return sbn::g_last_occ[which & 7]; }

@@ -23,4 +23,5 @@ for flags in (1, 0):
     t = buf.view(-1, 16).cpu().numpy()
     print("pair" if flags == 0 else "single", "grid", int((t[:, 0] > 0).sum()), "active", int((t[:, 11] > 0).sum()),
           "span_us", (t[t[:, 11] > 0, 11].max() - t[t[:, 0] > 0, 0].min()) / 1e3,
-          "occ", lib.sbn_debug_last_occupancy(0), "clusters", lib.sbn_debug_last_occupancy(1))
+          "occ", lib.sbn_debug_last_occupancy(0), "clusters", lib.sbn_debug_last_occupancy(1),
+          "regs/static/maxdyn/dyn/local", [lib.sbn_debug_last_occupancy(i) for i in range(2, 7)])
