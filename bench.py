@@ -432,9 +432,9 @@ def run_gather_scatter(P, torch, dev, time_graph, hbm_peak):
               for _, by, bx in ent)
     outp = sum((min(by * 14 + 14, Hc) - by * 14) * (min(bx * 14 + 14, Wc) - bx * 14) for _, by, bx in ent)
     e = Cc * 2
-    g_bytes = (win + B * 256) * e
-    s_bytes = (B * 196 + outp) * e
-    a_bytes = (B * 196 + 2 * outp) * e
+    g_bytes = int((win + B * 256) * e)
+    s_bytes = int((B * 196 + outp) * e)
+    a_bytes = int((B * 196 + 2 * outp) * e)
     t_g, t_s, t_a = timed(gat), timed(sca), timed(lambda k: sca(k, 1))
     r = lambda by_, t: round(by_ / (t * 1e-3) / 1e9, 1)  # noqa: E731
     return {"workload": "800x700x128 bf16, full mask, 16x16 blocks (SAME 3x3 geometry)", "blocks": B,
@@ -488,7 +488,7 @@ def run_conv_sweep(P, torch, dev, time_graph):
             t = timed(sp)
             nb = P.reduce_mask(mk, spec).count
             flops = nb * 2 * spec.out_block_size[0] * spec.out_block_size[1] * 9 * Cc * Cc
-            res["rows"].append({"density": d, "block": blk, "blocks": nb, "algo": algo,
+            res["rows"].append({"density": d, "block": blk, "blocks": int(nb), "algo": algo,
                                 "sparse_ms": round(t, 5), "speedup_vs_dense": round(dense_ms / t, 3),
                                 "tflops_alg": round(flops / (t * 1e-3) / 1e12, 1)})
     return res
