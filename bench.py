@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-conv-sweep", action="store_true")
     ap.add_argument("--no-gather-scatter", action="store_true")
+    ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="process-group backend (nccl; gloo only to smoke-test the multi-rank "
+                         "plumbing with several ranks sharing one GPU)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -166,10 +170,15 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collective tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     nf = args.frames
     xs, masks, dens = make_frames(P, torch, nf, rank * nf, args.density, dev)
@@ -206,7 +215,7 @@ def run_ours(args):
             e1.synchronize()
         ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
@@ -305,7 +314,7 @@ def run_ours(args):
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([e2e_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
@@ -336,6 +345,11 @@ def run_ours(args):
     conv_sweep = None
     if not args.no_conv_sweep and rank == 0:
         conv_sweep = run_conv_sweep(P, torch, dev, time_graph)
+
+    # ---- batched throughput (config-5 style per-GPU shard: many frames per launch)
+    batched = None
+    if not args.no_batched and rank == 0:
+        batched = run_batched(P, torch, dev, time_graph, u, hbm_peak, sparse_residual_unit_into)
 
     # ---- standalone gather / scatter bandwidth (north star: >70% of HBM peak)
     gs = None
@@ -380,10 +394,41 @@ def run_ours(args):
             "sweep": sweep,
             "conv_sweep": conv_sweep,
             "gather_scatter": gs,
+            "batched": batched,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_batched(P, torch, dev, time_graph, u, hbm_peak, unit_fn):
+    """Same unit, N frames per launch (e.g. the 8-frame per-GPU shard of config 5's N=64 on
+    8 GPUs, and all 64 on one GPU): frames/s and the fused kernel's HBM fraction."""
+    out = []
+    for nb, dens in ((8, 0.1), (8, 0.2), (64, 0.2)):
+        x = torch.randn(nb, H, W, C, device=dev).bfloat16()
+        mk = P.synth_mask_blobs((nb, H, W), 1.0 - dens, 100 + nb).cuda()
+        spec = P.unit_spec((nb, H, W, C), (16, 16))
+
+        def st(k, x=x, mk=mk, spec=spec):
+            for _ in range(k):
+                unit_fn(x, x, mk.data, u, spec)
+        reps = 20
+        g, s_ = time_graph(torch, st, reps, 2, soak_s=0.05)
+        with torch.cuda.stream(s_):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(s_)
+            g.replay()
+            b_.record(s_)
+            b_.synchronize()
+        ms = a_.elapsed_time(b_) / reps
+        ent = P.reduce_mask(mk, spec).entries
+        byts = unit_bytes(P, spec, ent) + nb * H * W
+        out.append({"frames": nb, "density_target": dens, "blocks": int(len(ent)), "ms": round(ms, 4),
+                    "frames_per_s": round(nb / (ms * 1e-3), 1), "GBps": round(byts / (ms * 1e-3) / 1e9, 1),
+                    "hbm_frac": round(byts / (ms * 1e-3) / 1e9 / hbm_peak, 3)})
+        del x
+    return out
 
 
 def run_gather_scatter(P, torch, dev, time_graph, hbm_peak):
