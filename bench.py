@@ -258,6 +258,12 @@ def run_ours(args):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tj.get(f"unit_tc_pair_kernel<{C},{M},{args.block}>")
+    except Exception:
+        pass
 
     # ---- dense comparator (cuDNN bf16, same frames, CUDA graph)
     def dense_steps(k):
@@ -384,7 +390,8 @@ def run_ours(args):
                     "pipeline": "2 streams: H2D(i+1) overlaps compute+D2H(i)"},
             "gpu_launches": int(per_step_launches * args.steps),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                         "traffic_source": "profiles/traffic.json (ncu, same kernel/config)" if traffic else None,
                          "kernel": f"unit_tc_kernel<{C},{M},{blk[0]}> (mask reduction fused)" if algo == "tcgen05" else "unit_simt_kernel",
                          "kernel_ms": round(k_ms, 5), "alg_bytes_per_launch": int(k_bytes),
                          "two_launch_step_ms": round(two_launch_ms, 5),
