@@ -392,7 +392,9 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                          "traffic_source": "profiles/traffic.json (ncu, same kernel/config)" if traffic else None,
-                         "kernel": f"unit_tc_kernel<{C},{M},{blk[0]}> (mask reduction fused)" if algo == "tcgen05" else "unit_simt_kernel",
+                         "kernel": (f"unit_tc_pair_kernel<{C},{M},{blk[0]}> (mask reduction fused)" if blk[0] == 16
+                                    else f"unit_tc_kernel<{C},{M},{blk[0]}> (mask reduction fused)")
+                                   if algo == "tcgen05" else "unit_simt_kernel",
                          "kernel_ms": round(k_ms, 5), "alg_bytes_per_launch": int(k_bytes),
                          "two_launch_step_ms": round(two_launch_ms, 5),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
