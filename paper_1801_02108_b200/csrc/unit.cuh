@@ -52,6 +52,10 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
                    const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
                    const int32_t* count, int cap, cudaStream_t s,
                    const uint8_t* mask = nullptr, int32_t* idx_out = nullptr,
-                   int32_t* count_out = nullptr);
+                   int32_t* count_out = nullptr, unsigned long long* cst = nullptr,
+                   unsigned int* etag = nullptr);
+// epoch compaction handles up to this many mask candidates per CTA (else fused_compact)
+constexpr int kEpochMaxPerHost = 1024;
+constexpr int kEpochMaxCtas = 4096;
 
 }  // namespace sbn

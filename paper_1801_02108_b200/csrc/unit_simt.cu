@@ -376,16 +376,19 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
 // ws (scratch):                      [idx (cap*12) | count | rim | packed image / SIMT scratch]
 static size_t al256(size_t v) { return (v + 255) / 256 * 256; }
 
+// sync ws: [barrier/epoch words (256 B) | epoch look-back status (8 B x 4096 CTAs) | reduce_mask ws]
+constexpr size_t kCstBytes = 8 * (size_t)kEpochMaxCtas;
+
 extern "C" size_t sbn_sparse_residual_unit_sync_bytes(const sbn_geometry* gp) {
   if (!gp) return 0;
-  return kBarBytes + al256(sbn_reduce_mask_workspace(gp));
+  return kBarBytes + kCstBytes + al256(sbn_reduce_mask_workspace(gp));
 }
 
 extern "C" size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* gp,
                                                      int halo, int algo) {
   if (!gp || dtype_size(dtype) == 0) return 0;
   const size_t cap = (size_t)gp->n * gp->gy * gp->gx;
-  return al256(cap * 12) + 256 + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
+  return al256(cap * 12) + 256 + al256(cap * 4) + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
 }
 
 extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
@@ -407,10 +410,12 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
   uint8_t* w8 = (uint8_t*)ws;
   int32_t* idx = (int32_t*)w8;
   int32_t* count = (int32_t*)(w8 + al256((size_t)cap * 12));
-  uint8_t* uws = w8 + al256((size_t)cap * 12) + 256;  // [barrier words unused here | rim | pack]
+  unsigned int* etag = (unsigned int*)(w8 + al256((size_t)cap * 12) + 256);
+  uint8_t* uws = w8 + al256((size_t)cap * 12) + 256 + al256((size_t)cap * 4);  // [bar | rim | pack]
   uint8_t* sync8 = (uint8_t*)sync_ws;
   unsigned int* gbar = reinterpret_cast<unsigned int*>(sync8);
-  uint8_t* rmws = sync8 + kBarBytes;
+  unsigned long long* cst = reinterpret_cast<unsigned long long*>(sync8 + kBarBytes);
+  uint8_t* rmws = sync8 + kBarBytes + kCstBytes;
   Geo g = to_geo(gp);
   cudaStream_t s = (cudaStream_t)stream;
   const bool tc = algo != SBN_ALGO_SIMT && unit_tc_supported(dtype, c, m, g, halo, pre_act);
@@ -429,10 +434,10 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
     }
     const bool inplace = x == out;
     return unit_tc_launch(x, out, inplace ? uws + kBarBytes : nullptr, gbar, c, m, g, p, packed,
-                          idx, count, cap, s, mask, idx, count);
+                          idx, count, cap, s, mask, idx, count, cst, etag);
   }
   st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws,
-                       sync_bytes - kBarBytes, stream);
+                       sync_bytes - kBarBytes - kCstBytes, stream);
   if (st) return st;
   // the two-launch path needs zeroed barrier words at the start of its workspace: the
   // 256 barrier bytes of sync_ws are followed by the (zeroed) reduce_mask words, so point

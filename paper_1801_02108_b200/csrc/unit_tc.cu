@@ -87,7 +87,9 @@ struct TcArgs {
   __nv_bfloat16* rim_buf;  // in place, more blocks than CTAs: halo rims snapshotted here
   unsigned int* gbar;      // grid-barrier words (in place only)
   unsigned long long* trace;
-  const uint8_t* mask;     // non-null: fused reduce_mask (MAX) + unordered compaction into idx/count
+  const uint8_t* mask;     // non-null: fused reduce_mask (MAX) + compaction into idx/count
+  unsigned long long* cst; // epoch compaction: per-CTA look-back status (sync ws); null -> fused_compact
+  unsigned int* etag;      // epoch compaction: per-entry publication tag (scratch ws)
   int32_t* idx_out;
   int32_t* count_out;
   const int32_t* idx;
@@ -159,6 +161,175 @@ __device__ __forceinline__ int fused_compact(const TcArgs& a) {
   return s_B;
 }
 
+
+// ---- epoch-tagged ordered compaction (replaces the global slot atomic + grid barrier of
+// fused_compact).  CTA c flags the candidates of a contiguous range, publishes its count,
+// resolves its offset with a warp-parallel decoupled look-back and writes its active blocks
+// in ascending (frame, by, bx) order — the same list reduce_mask produces.  Every status
+// word and entry carries the launch's tag (epoch + 1), so nothing needs resetting: the last
+// CTA out bumps the epoch (epoch_finish).  Consumers only wait for the entry they need.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long cst_pack(unsigned tag, unsigned flag, unsigned v) {
+  return ((unsigned long long)tag << 32) | ((unsigned long long)flag << 30) | (v & 0x3fffffffu);
+}
+
+constexpr int kEpochMaxPer = 1024;  // candidates per CTA handled by epoch_compact
+
+__device__ __forceinline__ int epoch_compact(const TcArgs& a, unsigned tag) {
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ uint8_t s_fl[kEpochMaxPer];
+  __shared__ int s_ws[kThreads / 32];
+  __shared__ int s_P, s_B;
+  const int T = g.n * g.gy * g.gx;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int per = (T + G - 1) / G;
+  const int c0 = min(c * per, T), c1 = min(c0 + per, T), nc = c1 - c0;
+  const int area = g.bh * g.bw;
+  for (int j = tid; j < nc; j += kThreads) s_fl[j] = 0;
+  __syncthreads();
+  for (int e = tid; e < nc * area; e += kThreads) {
+    const int j = e / area, p = e - j * area;
+    const int cand = c0 + j;
+    const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+    const int cy = rr / g.gx, cx = rr - cy * g.gx;
+    const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
+    if (y >= 0 && y < g.h && xx >= 0 && xx < g.w && __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx))
+      s_fl[j] = 1;
+  }
+  __syncthreads();
+  // in-CTA exclusive scan over contiguous per-thread runs
+  const int pc = (nc + kThreads - 1) / kThreads;
+  const int j0 = min(tid * pc, nc), j1 = min(j0 + pc, nc);
+  int mine = 0;
+  for (int j = j0; j < j1; ++j) mine += s_fl[j];
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_ws[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = lane < kThreads / 32 ? s_ws[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    if (lane < kThreads / 32) s_ws[lane] = wi - w;
+    const int k = __shfl_sync(0xffffffffu, wi, 31);  // CTA total
+    if (lane == 0) st_release_u64(&a.cst[c], cst_pack(tag, c == 0 ? 2u : 1u, (unsigned)k));
+    int P = 0;
+    for (int j = c - 1; j >= 0;) {
+      const int q = j - lane;
+      unsigned long long st = q >= 0 ? ld_acquire_u64(&a.cst[q]) : cst_pack(tag, 2u, 0u);
+      const bool cur = (unsigned)(st >> 32) == tag;
+      const unsigned flag = cur ? (unsigned)(st >> 30) & 3u : 0u;
+      const unsigned incl_m = __ballot_sync(0xffffffffu, flag == 2);
+      const unsigned none = __ballot_sync(0xffffffffu, flag == 0);
+      const int first = incl_m ? __ffs(incl_m) - 1 : 31;
+      const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
+      if (none & need) {
+        __nanosleep(20);
+        continue;
+      }
+      int v = lane <= first ? (int)(st & 0x3fffffffu) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      P += v;
+      if (incl_m) break;
+      j -= 32;
+    }
+    if (lane == 0) {
+      if (c > 0) st_release_u64(&a.cst[c], cst_pack(tag, 2u, (unsigned)(P + k)));
+      s_P = P;
+      if (c == G - 1) *a.count_out = P + k;
+    }
+  }
+  __syncthreads();
+  // ordered entry writes (rows first, then the release of each entry's tag)
+  int pos = s_P + s_ws[warp] + incl - mine;
+  for (int j = j0; j < j1; ++j) {
+    if (s_fl[j]) {
+      const int cand = c0 + j;
+      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+      a.idx_out[3 * pos] = fr;
+      a.idx_out[3 * pos + 1] = rr / g.gx;
+      a.idx_out[3 * pos + 2] = rr % g.gx;
+      st_release_u32(&a.etag[pos], tag);
+      ++pos;
+    }
+  }
+  // the total: the last CTA's inclusive prefix
+  if (tid == 0) {
+    unsigned long long st;
+    while (true) {
+      st = ld_acquire_u64(&a.cst[G - 1]);
+      if ((unsigned)(st >> 32) == tag && ((unsigned)(st >> 30) & 3u) == 2u) break;
+      __nanosleep(32);
+    }
+    s_B = (int)(st & 0x3fffffffu);
+  }
+  __syncthreads();
+  return s_B;
+}
+
+// Wait until list entry `blk` of this launch is published (epoch mode), then read it.
+__device__ __forceinline__ void entry_rows(const TcArgs& a, const int32_t* idx, unsigned tag, int blk,
+                                           int& n, int& by, int& bx) {
+  if (tag) {
+    __shared__ int s_e[3];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      while (ld_acquire_u32(&a.etag[blk]) != tag) __nanosleep(20);
+      s_e[0] = __ldcg(idx + 3 * blk);
+      s_e[1] = __ldcg(idx + 3 * blk + 1);
+      s_e[2] = __ldcg(idx + 3 * blk + 2);
+    }
+    __syncthreads();
+    n = s_e[0];
+    by = s_e[1];
+    bx = s_e[2];
+  } else {
+    n = __ldcg(idx + 3 * blk);
+    by = __ldcg(idx + 3 * blk + 1);
+    bx = __ldcg(idx + 3 * blk + 2);
+  }
+}
+
+// Last CTA out bumps the epoch (all CTAs have read it at their start).
+__device__ __forceinline__ void epoch_finish(const TcArgs& a, unsigned tag) {
+  if (!tag) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned* w = a.gbar + 8;  // [epoch, seen]
+    if (atomicAdd(w + 1, 1u) == gridDim.x - 1) {
+      w[1] = 0u;
+      w[0] = tag;  // next launch uses tag + 1
+      __threadfence();
+    }
+  }
+}
+
 template <int C, int MC, int BS>
 __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(TcArgs a) {
   using K = Cfg<C, MC, BS>;
@@ -214,14 +385,17 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   int n0 = 0, by0 = 0, bx0 = 0;
   int B;
   const int32_t* idx = a.idx;
+  unsigned tag = 0;
   if (a.mask) {
-    B = fused_compact(a);
-    idx = a.idx_out;
-    if ((int)blockIdx.x < B) {
-      n0 = __ldcg(idx + 3 * blockIdx.x);
-      by0 = __ldcg(idx + 3 * blockIdx.x + 1);
-      bx0 = __ldcg(idx + 3 * blockIdx.x + 2);
+    const int Tc = g.n * g.gy * g.gx;
+    if (a.cst && (Tc + (int)gridDim.x - 1) / (int)gridDim.x <= kEpochMaxPer && gridDim.x <= 4096) {
+      tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
+      B = epoch_compact(a, tag);
+    } else {
+      B = fused_compact(a);
     }
+    idx = a.idx_out;
+    if ((int)blockIdx.x < B) entry_rows(a, idx, tag, blockIdx.x, n0, by0, bx0);
   } else {
     if ((int)blockIdx.x < a.cap) {  // speculative: the first block's row, loaded alongside the count
       n0 = __ldg(idx + 3 * blockIdx.x);
@@ -243,7 +417,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
     for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-      const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
+      int n, by, bx;
+      entry_rows(a, idx, tag, blk, n, by, bx);
       const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
       for (int i = tid; i < Pr * (C / 8); i += kThreads) {
         const int rp = i / (C / 8), k = i % (C / 8);
@@ -265,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     __syncthreads();
     tc::fence_after();
     if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
+    epoch_finish(a, tag);
     return;
   }
 
@@ -275,9 +451,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
   for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
     const bool first = blk == (int)blockIdx.x;
-    const int n = first ? n0 : __ldcg(idx + 3 * blk);
-    const int by = first ? by0 : __ldcg(idx + 3 * blk + 1);
-    const int bx = first ? bx0 : __ldcg(idx + 3 * blk + 2);
+    int n = n0, by = by0, bx = bx0;
+    if (!first) entry_rows(a, idx, tag, blk, n, by, bx);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
 
     // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
@@ -498,6 +673,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
   tc::fence_after();
   if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
+  epoch_finish(a, tag);
 }
 
 // Pre-pack W1/W2/W3 (transposed into the K-major plane layout) and the float params into
@@ -707,8 +883,15 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   tc::pdl_wait();
   int B;
   const int32_t* idx = a.idx;
+  unsigned tag = 0;
   if (a.mask) {
-    B = fused_compact(a);
+    const int Tc = g.n * g.gy * g.gx;
+    if (a.cst && (Tc + (int)gridDim.x - 1) / (int)gridDim.x <= kEpochMaxPer && gridDim.x <= 4096) {
+      tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
+      B = epoch_compact(a, tag);
+    } else {
+      B = fused_compact(a);
+    }
     idx = a.idx_out;
   } else {
     B = ld_count(a.count, a.cap);
@@ -721,7 +904,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
     for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-      const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
+      int n, by, bx;
+      entry_rows(a, idx, tag, blk, n, by, bx);
       const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
       for (int i = tid; i < Pr * (C / 8); i += kThreads) {
         const int rp = i / (C / 8), k = i % (C / 8);
@@ -743,6 +927,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     __syncthreads();
     tc::fence_after();
     if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
+    epoch_finish(a, tag);
     return;
   }
   const Rim rim{BS, BS, 1};
@@ -750,7 +935,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   uint8_t* A2peer = rank > 0 ? cl.map_shared_rank(A2, rank - 1) : nullptr;
 
   for (int blk = pair; blk < B; blk += npairs) {
-    const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
+    int n, by, bx;
+    entry_rows(a, idx, tag, blk, n, by, bx);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
     // ---- 1. stage my half of the window (pixels [128*rank, 128*rank + 128))
     constexpr int TOT = 128 * (C / 8);
@@ -943,6 +1129,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   }
   tc::fence_after();
   if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
+  epoch_finish(a, tag);
 }
 
 template <int C, int MC, int BS>
@@ -1019,6 +1206,8 @@ static TcArgs make_args(const void* x, void* out, const void* rim, const Geo& g,
   a.mask = nullptr;
   a.idx_out = nullptr;
   a.count_out = nullptr;
+  a.cst = nullptr;
+  a.etag = nullptr;
   a.idx = idx; a.count = count; a.cap = cap;
   return a;
 }
@@ -1035,11 +1224,14 @@ int unit_tc_pack(const sbn_unit_params* p, int c, int m, const Geo& g, void* img
 int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, int c, int m,
                    const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
                    const int32_t* count, int cap, cudaStream_t s, const uint8_t* mask,
-                   int32_t* idx_out, int32_t* count_out) {
+                   int32_t* idx_out, int32_t* count_out, unsigned long long* cst,
+                   unsigned int* etag) {
   TcArgs a = make_args(x, out, nullptr, g, p, idx, count, cap);
   a.mask = mask;
   a.idx_out = idx_out;
   a.count_out = count_out;
+  a.cst = cst;
+  a.etag = etag;
   a.packed = (const uint8_t*)packed;
   a.rim_buf = (__nv_bfloat16*)rim_buf;
   a.gbar = gbar;
