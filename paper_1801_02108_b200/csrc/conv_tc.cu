@@ -223,6 +223,211 @@ int launch_conv(const ConvArgs& a, int cap, cudaStream_t s) {
   return launch_status("sparse_conv_tcgen05");
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Double-buffered variant: two window buffers and two TMEM accumulators so that, per CTA,
+// the window load of block k+1 and the epilogue of block k-1 overlap the MMAs of block k.
+// Roles (320 threads): warps 0-7 workers (stage windows, drain TMEM), warp 8 weight
+// producer, warp 9 MMA issuer.  Handshakes are mbarriers:
+//   win_full[b]  workers -> MMA   (256 arrivals: window b staged)
+//   win_empty[b] MMA -> workers   (tcgen05.commit: MMAs reading window b done)
+//   acc_full[b]  MMA -> workers   (tcgen05.commit: accumulator b complete)
+//   acc_empty[b] workers -> MMA   (256 arrivals: accumulator b drained)
+constexpr int kDbThreads = kWorkers + 64;
+
+template <int CIN, int COUT, int BS>
+struct DbCfg {
+  using K = ConvCfg<CIN, COUT, BS>;
+  static constexpr int al(int v) { return (v + 1023) / 1024 * 1024; }
+  static constexpr int SZ_A = K::SZ_A;
+  static constexpr int STAGES = (2 * SZ_A + 3 * K::TAP + COUT * 4 <= 222 * 1024) ? 3 : 2;
+  static constexpr int OFF_W = 2 * SZ_A;
+  static constexpr int OFF_BIAS = OFF_W + STAGES * K::TAP;
+  static constexpr int SMEM = OFF_BIAS + COUT * 4;
+  static constexpr int ACC = K::NT * COUT;  // TMEM columns per accumulator
+  static constexpr int TALLOC = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
+  static_assert(2 * ACC <= 512, "two accumulators must fit TMEM");
+};
+
+template <int CIN, int COUT, int BS>
+__global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
+  using K = ConvCfg<CIN, COUT, BS>;
+  using D = DbCfg<CIN, COUT, BS>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[D::STAGES], empty[D::STAGES];
+  __shared__ uint64_t win_full[2], win_empty[2], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tslot;
+  uint8_t* Wst = smem + D::OFF_W;
+  float* bias = reinterpret_cast<float*>(smem + D::OFF_BIAS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Geo& g = a.g;
+
+  if (tid == 0) {
+    for (int s = 0; s < D::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&win_full[b], kWorkers);
+      tc::mbar_init(&win_empty[b], 1);
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], kWorkers);
+    }
+    tc::mbar_fence_init();
+  }
+  for (int i = tid; i < COUT; i += kDbThreads) bias[i] = a.bias ? __bfloat162float(a.bias[i]) : 0.f;
+  if (warp == 0) tc::tmem_alloc<D::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_wait();
+  const int B = ld_count(a.count, a.cap);
+
+  if (warp == 8) {
+    // ---------------- producer: weight taps through the ring
+    if (lane == 0) {
+      int it = 0;
+      for (int blk = blockIdx.x; blk < B; blk += gridDim.x)
+        for (int tap = 0; tap < 9; ++tap, ++it) {
+          const int s = it % D::STAGES;
+          tc::mbar_wait(&empty[s], ((it / D::STAGES) & 1) ^ 1);
+          tc::mbar_expect_tx(&full[s], K::TAP);
+          tc::bulk_g2s(Wst + s * K::TAP, a.wpk + (size_t)tap * K::TAP, K::TAP, &full[s]);
+        }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      int it = 0, k = 0;
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, COUT);
+      for (int blk = blockIdx.x; blk < B; blk += gridDim.x, ++k) {
+        const int b = k & 1;
+        const uint32_t use = (uint32_t)(k >> 1);
+        tc::mbar_wait(&win_full[b], use & 1);
+        tc::mbar_wait(&acc_empty[b], (use & 1) ^ 1);
+        tc::fence_after();
+        const uint8_t* A = smem + b * D::SZ_A;
+        const uint32_t acc = tmem + b * D::ACC;
+        for (int tap = 0; tap < 9; ++tap, ++it) {
+          const int s = it % D::STAGES;
+          tc::mbar_wait(&full[s], (it / D::STAGES) & 1);
+          tc::fence_after();
+          const int shift = (tap / 3) * BS + (tap % 3);
+          const uint32_t wbase = tc::smem_u32(Wst + s * K::TAP);
+#pragma unroll
+          for (int t = 0; t < K::NT; ++t)
+#pragma unroll
+            for (int kk = 0; kk < CIN / 16; ++kk)
+              tc::mma_bf16(acc + t * COUT,
+                           tc::desc_kmajor_noswz(tc::smem_u32(A + 2 * kk * K::PA + (t * 128 + shift) * 16), K::PA, 128),
+                           tc::desc_kmajor_noswz(wbase + 2 * kk * K::PW, K::PW, 128), idesc, (tap | kk) > 0);
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&win_empty[b]);
+        tc::mma_commit(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- workers: stage window k, drain accumulator k-1
+    const int q = warp & 3, tpar = warp >> 2;
+    int pn = 0, pby = 0, pbx = 0;  // previous block (for its epilogue)
+    int k = 0;
+    auto epilogue = [&](int kk, int n, int by, int bx) {
+      const int b = kk & 1;
+      tc::mbar_wait(&acc_full[b], (kk >> 1) & 1);
+      tc::fence_after();
+      const uint32_t acc = tmem + b * D::ACC;
+      for (int t = tpar; t < K::NT; t += 2) {
+        const int r = t * 128 + q * 32 + lane;
+        const int oy = r / BS, ox = r % BS;
+        const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+        const bool store = oy < g.obh && ox < g.obw && Y < g.oh && X < g.ow;
+        uint4* op = reinterpret_cast<uint4*>(a.out) +
+                    (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (COUT / 8);
+#pragma unroll 4
+        for (int c0 = 0; c0 < COUT; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(acc + ((uint32_t)(q * 32) << 16) + t * COUT + c0, v);
+          if (store) {
+            uint32_t o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              o[e] = tc::pack_bf16(v[2 * e] + bias[c0 + 2 * e], v[2 * e + 1] + bias[c0 + 2 * e + 1]);
+            op[c0 / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+            op[c0 / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&acc_empty[b]);
+    };
+    for (int blk = blockIdx.x; blk < B; blk += gridDim.x, ++k) {
+      const int b = k & 1;
+      const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+      const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+      tc::mbar_wait(&win_empty[b], ((k >> 1) & 1) ^ 1);
+      uint8_t* A = smem + b * D::SZ_A;
+      constexpr int TOT = BS * BS * (CIN / 8);
+      constexpr int ITEMS = (TOT + kWorkers - 1) / kWorkers;
+      constexpr int CH = ITEMS > 16 ? 16 : ITEMS;
+#pragma unroll 1
+      for (int base = 0; base < ITEMS; base += CH) {
+        uint4 raw[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int i = tid + (base + j) * kWorkers;
+          const int p = i / (CIN / 8), kc = i % (CIN / 8);
+          const int y = ys + p / BS, xx = xs + p % BS;
+          raw[j] = make_uint4(0, 0, 0, 0);
+          if (i < TOT && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+            raw[j] = __ldg(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (CIN / 8) + kc);
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int i = tid + (base + j) * kWorkers;
+          if (i < TOT) {
+            const int p = i / (CIN / 8), kc = i % (CIN / 8);
+            *reinterpret_cast<uint4*>(A + kc * K::PA + p * 16) = raw[j];
+          }
+        }
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&win_full[b]);
+      if (k > 0) epilogue(k - 1, pn, pby, pbx);
+      pn = n;
+      pby = by;
+      pbx = bx;
+    }
+    if (k > 0) epilogue(k - 1, pn, pby, pbx);
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free<D::TALLOC>(tmem);
+}
+
+template <int CIN, int COUT, int BS>
+int launch_conv_db(const ConvArgs& a, int cap, cudaStream_t s) {
+  using D = DbCfg<CIN, COUT, BS>;
+  auto kern = conv_tc_db_kernel<CIN, COUT, BS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(persistent_grid(cap, 1));
+  cfg.blockDim = dim3(kDbThreads);
+  cfg.dynamicSmemBytes = D::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+  return launch_status("sparse_conv_tcgen05_db");
+}
+
 #define SBN_CONV_TC_CONFIGS(X) \
   X(128, 128, 16)              \
   X(128, 128, 8)               \
@@ -262,6 +467,11 @@ int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, con
   a.idx = idx;
   a.count = count;
   a.cap = cap;
+  if (!(debug_flags() & kDebugConvSingleBuffer)) {
+#define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_ && DbCfg<CI, CO, BS_>::SMEM <= max_smem_optin()) return launch_conv_db<CI, CO, BS_>(a, cap, s);
+    SBN_CONV_TC_CONFIGS(X)
+#undef X
+  }
 #define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_) return launch_conv<CI, CO, BS_>(a, cap, s);
   SBN_CONV_TC_CONFIGS(X)
 #undef X

@@ -88,8 +88,8 @@ struct TcArgs {
   unsigned int* gbar;      // grid-barrier words (in place only)
   unsigned long long* trace;
   const uint8_t* mask;     // non-null: fused reduce_mask (MAX) + compaction into idx/count
-  unsigned long long* cst; // epoch compaction: per-CTA look-back status (sync ws); null -> fused_compact
-  unsigned int* etag;      // epoch compaction: per-entry publication tag (scratch ws)
+  unsigned long long* cst; // (unused; reserved)
+  unsigned int* etag;      // slot compaction: per-entry publication tag (scratch ws)
   int32_t* idx_out;
   int32_t* count_out;
   const int32_t* idx;
@@ -99,27 +99,45 @@ struct TcArgs {
 
 __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
-// Fused reduce_mask (MAX pooling, `tiling.py:138-160`) used by the single-kernel
-// sparse_residual_unit: every CTA tests the windows of candidates blockIdx.x + j*grid
-// against the mask and appends the active ones to one list (one atomic slot per CTA and
-// round; order is irrelevant to the unit: blocks write disjoint windows).  A grid barrier
-// over all CTAs publishes the count; the last CTA out resets the words.  Returns B.
-__device__ __forceinline__ int fused_compact(const TcArgs& a) {
+// ---- slot compaction (fused mask reduction of the single-kernel sparse_residual_unit).
+// Producers: CTA c tests candidates c, c+G, ... against the mask, claims list slots for its
+// active ones with ONE atomic per round, writes each entry, publishes it with the launch's
+// tag (release), and — in place — snapshots that block's halo rim into rim_buf[slot].
+// Then it increments `done`.  Consumers only wait for the entry they process (or for
+// done == G to learn that no more entries are coming); the in-place hazard needs all rims
+// snapshotted before any interior store, i.e. done == G just before epilogue 3.  Nothing is
+// reset on the critical path: the last CTA out clears the words and bumps the epoch, and
+// tags make stale entries from earlier launches invisible.
+//   words (sync ws, u32): [8] epoch, [9] seen, [10] slot counter, [11] done
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int C, int BS>
+__device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag, bool inplace) {
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int s_flag[32];
+  __shared__ int s_slot[32];
   __shared__ int s_base;
-  __shared__ int s_B;
+  unsigned* w = a.gbar + 8;
   const int T = g.n * g.gy * g.gx;
   const int area = g.bh * g.bw;
-  unsigned int* fb = a.gbar + 2;  // [arrive, depart, slot]
-  for (int r0 = blockIdx.x; r0 < T; r0 += 32 * gridDim.x) {
-    const int nj = min(32, (T - r0 + (int)gridDim.x - 1) / (int)gridDim.x);
+  const int G = gridDim.x;
+  const Rim rim{BS, BS, 1};
+  const int P = rim.pixels();
+  for (int r0 = blockIdx.x; r0 < T; r0 += 32 * G) {
+    const int nj = min(32, (T - r0 + G - 1) / G);
     if (tid < 32) s_flag[tid] = 0;
     __syncthreads();
-    for (int e = tid; e < nj * area; e += blockDim.x) {
+    for (int e = tid; e < nj * area; e += kThreads) {
       const int j = e / area, p = e - j * area;
-      const int cand = r0 + j * gridDim.x;
+      const int cand = r0 + j * G;
       const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
       const int cy = rr / g.gx, cx = rr - cy * g.gx;
       const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
@@ -130,200 +148,106 @@ __device__ __forceinline__ int fused_compact(const TcArgs& a) {
     if (warp == 0) {
       const bool on = lane < nj && s_flag[lane];
       const unsigned bal = __ballot_sync(0xffffffffu, on);
-      if (lane == 0) s_base = bal ? (int)atomicAdd(fb + 2, (unsigned)__popc(bal)) : 0;
+      if (lane == 0) s_base = bal ? (int)atomicAdd(w + 2, (unsigned)__popc(bal)) : 0;
       __syncwarp();
+      s_slot[lane] = on ? s_base + __popc(bal & ((1u << lane) - 1u)) : -1;
       if (on) {
-        const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
-        const int cand = r0 + lane * gridDim.x;
+        const int pos = s_slot[lane];
+        const int cand = r0 + lane * G;
         const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
         a.idx_out[3 * pos] = fr;
         a.idx_out[3 * pos + 1] = rr / g.gx;
         a.idx_out[3 * pos + 2] = rr % g.gx;
+        st_release_u32(&a.etag[pos], tag);
+      }
+    }
+    __syncthreads();
+    if (inplace) {  // snapshot the rims of this round's active blocks
+      for (int j = 0; j < nj; ++j) {
+        const int pos = s_slot[j];
+        if (pos < 0) continue;
+        const int cand = r0 + j * G;
+        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+        const int ys = g.oy + (rr / g.gx) * g.sy, xs = g.ox + (rr % g.gx) * g.sx;
+        for (int i = tid; i < P * (C / 8); i += kThreads) {
+          const int rp = i / (C / 8), k = i % (C / 8);
+          int wy, wx;
+          rim.coord(rp, wy, wx);
+          const int y = ys + wy, xx = xs + wx;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+            v = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)fr * g.h + y) * g.w + xx) * (C / 8) + k);
+          reinterpret_cast<uint4*>(a.rim_buf)[((size_t)pos * P + rp) * (C / 8) + k] = v;
+        }
       }
     }
   }
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    atomicAdd(fb, 1u);
-    while (*reinterpret_cast<volatile unsigned int*>(fb) < gridDim.x) __nanosleep(32);
-    __threadfence();
-    s_B = (int)*reinterpret_cast<volatile unsigned int*>(fb + 2);
-    if (blockIdx.x == 0) *a.count_out = s_B;
-    if (atomicAdd(fb + 1, 1u) == gridDim.x - 1) {  // last out: reset for the next launch
-      fb[0] = 0u;
-      fb[1] = 0u;
-      fb[2] = 0u;
-      __threadfence();
-    }
+    atomicAdd(w + 3, 1u);  // this producer is done (entries + rims published)
   }
-  __syncthreads();
-  return s_B;
 }
 
-
-// ---- epoch-tagged ordered compaction (replaces the global slot atomic + grid barrier of
-// fused_compact).  CTA c flags the candidates of a contiguous range, publishes its count,
-// resolves its offset with a warp-parallel decoupled look-back and writes its active blocks
-// in ascending (frame, by, bx) order — the same list reduce_mask produces.  Every status
-// word and entry carries the launch's tag (epoch + 1), so nothing needs resetting: the last
-// CTA out bumps the epoch (epoch_finish).  Consumers only wait for the entry they need.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long cst_pack(unsigned tag, unsigned flag, unsigned v) {
-  return ((unsigned long long)tag << 32) | ((unsigned long long)flag << 30) | (v & 0x3fffffffu);
-}
-
-constexpr int kEpochMaxPer = 1024;  // candidates per CTA handled by epoch_compact
-
-__device__ __forceinline__ int epoch_compact(const TcArgs& a, unsigned tag) {
-  const Geo& g = a.g;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ uint8_t s_fl[kEpochMaxPer];
-  __shared__ int s_ws[kThreads / 32];
-  __shared__ int s_P, s_B;
-  const int T = g.n * g.gy * g.gx;
-  const int G = gridDim.x, c = blockIdx.x;
-  const int per = (T + G - 1) / G;
-  const int c0 = min(c * per, T), c1 = min(c0 + per, T), nc = c1 - c0;
-  const int area = g.bh * g.bw;
-  for (int j = tid; j < nc; j += kThreads) s_fl[j] = 0;
+// Entry `blk` of this launch: returns false when the list is complete and shorter.
+__device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int blk, int& n, int& by,
+                                           int& bx) {
+  __shared__ int s_e[4];
+  if (blk >= a.g.n * a.g.gy * a.g.gx) return false;  // more consumers than candidates
   __syncthreads();
-  for (int e = tid; e < nc * area; e += kThreads) {
-    const int j = e / area, p = e - j * area;
-    const int cand = c0 + j;
-    const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-    const int cy = rr / g.gx, cx = rr - cy * g.gx;
-    const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
-    if (y >= 0 && y < g.h && xx >= 0 && xx < g.w && __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx))
-      s_fl[j] = 1;
-  }
-  __syncthreads();
-  // in-CTA exclusive scan over contiguous per-thread runs
-  const int pc = (nc + kThreads - 1) / kThreads;
-  const int j0 = min(tid * pc, nc), j1 = min(j0 + pc, nc);
-  int mine = 0;
-  for (int j = j0; j < j1; ++j) mine += s_fl[j];
-  int incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_ws[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const int w = lane < kThreads / 32 ? s_ws[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += v;
-    }
-    if (lane < kThreads / 32) s_ws[lane] = wi - w;
-    const int k = __shfl_sync(0xffffffffu, wi, 31);  // CTA total
-    if (lane == 0) st_release_u64(&a.cst[c], cst_pack(tag, c == 0 ? 2u : 1u, (unsigned)k));
-    int P = 0;
-    for (int j = c - 1; j >= 0;) {
-      const int q = j - lane;
-      unsigned long long st = q >= 0 ? ld_acquire_u64(&a.cst[q]) : cst_pack(tag, 2u, 0u);
-      const bool cur = (unsigned)(st >> 32) == tag;
-      const unsigned flag = cur ? (unsigned)(st >> 30) & 3u : 0u;
-      const unsigned incl_m = __ballot_sync(0xffffffffu, flag == 2);
-      const unsigned none = __ballot_sync(0xffffffffu, flag == 0);
-      const int first = incl_m ? __ffs(incl_m) - 1 : 31;
-      const unsigned need = first >= 31 ? 0xffffffffu : ((2u << first) - 1u);
-      if (none & need) {
-        __nanosleep(20);
-        continue;
-      }
-      int v = lane <= first ? (int)(st & 0x3fffffffu) : 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      P += v;
-      if (incl_m) break;
-      j -= 32;
-    }
-    if (lane == 0) {
-      if (c > 0) st_release_u64(&a.cst[c], cst_pack(tag, 2u, (unsigned)(P + k)));
-      s_P = P;
-      if (c == G - 1) *a.count_out = P + k;
-    }
-  }
-  __syncthreads();
-  // ordered entry writes (rows first, then the release of each entry's tag)
-  int pos = s_P + s_ws[warp] + incl - mine;
-  for (int j = j0; j < j1; ++j) {
-    if (s_fl[j]) {
-      const int cand = c0 + j;
-      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-      a.idx_out[3 * pos] = fr;
-      a.idx_out[3 * pos + 1] = rr / g.gx;
-      a.idx_out[3 * pos + 2] = rr % g.gx;
-      st_release_u32(&a.etag[pos], tag);
-      ++pos;
-    }
-  }
-  // the total: the last CTA's inclusive prefix
-  if (tid == 0) {
-    unsigned long long st;
+  if (threadIdx.x == 0) {
+    unsigned* w = a.gbar + 8;
+    int ok = 0;
     while (true) {
-      st = ld_acquire_u64(&a.cst[G - 1]);
-      if ((unsigned)(st >> 32) == tag && ((unsigned)(st >> 30) & 3u) == 2u) break;
-      __nanosleep(32);
+      if (ld_acquire_u32(&a.etag[blk]) == tag) {
+        ok = 1;
+        break;
+      }
+      if (ld_acquire_u32(w + 3) == gridDim.x) {  // all producers done
+        ok = ld_acquire_u32(&a.etag[blk]) == tag ? 1 : 0;
+        break;
+      }
+      __nanosleep(20);
     }
-    s_B = (int)(st & 0x3fffffffu);
+    s_e[3] = ok;
+    if (ok) {
+      s_e[0] = __ldcg(a.idx_out + 3 * blk);
+      s_e[1] = __ldcg(a.idx_out + 3 * blk + 1);
+      s_e[2] = __ldcg(a.idx_out + 3 * blk + 2);
+    }
+  }
+  __syncthreads();
+  n = s_e[0];
+  by = s_e[1];
+  bx = s_e[2];
+  return s_e[3] != 0;
+}
+
+// All producers done (rims snapshotted); returns the final block count.
+__device__ __forceinline__ int slot_all_done(const TcArgs& a) {
+  __shared__ int s_B;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* w = a.gbar + 8;
+    while (ld_acquire_u32(w + 3) != gridDim.x) __nanosleep(32);
+    s_B = (int)ld_acquire_u32(w + 2);
+    if (blockIdx.x == 0) *a.count_out = s_B;
   }
   __syncthreads();
   return s_B;
 }
 
-// Wait until list entry `blk` of this launch is published (epoch mode), then read it.
-__device__ __forceinline__ void entry_rows(const TcArgs& a, const int32_t* idx, unsigned tag, int blk,
-                                           int& n, int& by, int& bx) {
-  if (tag) {
-    __shared__ int s_e[3];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      while (ld_acquire_u32(&a.etag[blk]) != tag) __nanosleep(20);
-      s_e[0] = __ldcg(idx + 3 * blk);
-      s_e[1] = __ldcg(idx + 3 * blk + 1);
-      s_e[2] = __ldcg(idx + 3 * blk + 2);
-    }
-    __syncthreads();
-    n = s_e[0];
-    by = s_e[1];
-    bx = s_e[2];
-  } else {
-    n = __ldcg(idx + 3 * blk);
-    by = __ldcg(idx + 3 * blk + 1);
-    bx = __ldcg(idx + 3 * blk + 2);
-  }
-}
-
-// Last CTA out bumps the epoch (all CTAs have read it at their start).
-__device__ __forceinline__ void epoch_finish(const TcArgs& a, unsigned tag) {
+// Last CTA out clears the words and bumps the epoch (all CTAs have read them).
+__device__ __forceinline__ void slot_finish(const TcArgs& a, unsigned tag) {
   if (!tag) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned* w = a.gbar + 8;  // [epoch, seen]
+    unsigned* w = a.gbar + 8;
     if (atomicAdd(w + 1, 1u) == gridDim.x - 1) {
       w[1] = 0u;
+      w[2] = 0u;
+      w[3] = 0u;
       w[0] = tag;  // next launch uses tag + 1
       __threadfence();
     }
@@ -383,19 +307,17 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   // everything above overlaps the previous kernel (reduce_mask) under PDL
   tc::pdl_wait();
   int n0 = 0, by0 = 0, bx0 = 0;
-  int B;
+  int B = 0;
   const int32_t* idx = a.idx;
   unsigned tag = 0;
-  if (a.mask) {
-    const int Tc = g.n * g.gy * g.gx;
-    if (a.cst && (Tc + (int)gridDim.x - 1) / (int)gridDim.x <= kEpochMaxPer && gridDim.x <= 4096) {
-      tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
-      B = epoch_compact(a, tag);
-    } else {
-      B = fused_compact(a);
-    }
+  const bool inplace = a.x == a.out;
+  const bool fused = a.mask != nullptr;
+  bool have;
+  if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
+    tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
+    slot_produce<C, BS>(a, tag, inplace);
     idx = a.idx_out;
-    if ((int)blockIdx.x < B) entry_rows(a, idx, tag, blockIdx.x, n0, by0, bx0);
+    have = slot_entry(a, tag, blockIdx.x, n0, by0, bx0);
   } else {
     if ((int)blockIdx.x < a.cap) {  // speculative: the first block's row, loaded alongside the count
       n0 = __ldg(idx + 3 * blockIdx.x);
@@ -403,22 +325,25 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
       bx0 = __ldg(idx + 3 * blockIdx.x + 2);
     }
     B = ld_count(a.count, a.cap);
+    have = (int)blockIdx.x < B;
   }
   trace(a.trace, 2);
-  const bool inplace = a.x == a.out;
   // In place, a block's halo rim is its neighbours' interior, which they overwrite.
+  //  fused:     rims were snapshotted by the producers; wait for all of them before the
+  //             first store (slot_all_done).
   //  resident (B <= grid): every block has its own CTA; all windows are staged before
-  //                        any CTA writes (one grid barrier after staging).
+  //                        any CTA writes (split grid barrier: arrive after staging, wait
+  //                        before epilogue 3).
   //  streamed (B > grid):  rims of all blocks are snapshotted first (grid barrier),
   //                        then windows read interiors from x and rims from the snapshot.
-  const bool resident = B <= (int)gridDim.x;
-  const __nv_bfloat16* rimsrc = a.rim;
-  if (inplace && !resident) {
+  const bool resident = !fused && B <= (int)gridDim.x;
+  const __nv_bfloat16* rimsrc = (fused && inplace) ? a.rim_buf : a.rim;
+  bool rims_done = !(fused && inplace);
+  if (!fused && inplace && !resident) {
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
     for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-      int n, by, bx;
-      entry_rows(a, idx, tag, blk, n, by, bx);
+      const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
       const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
       for (int i = tid; i < Pr * (C / 8); i += kThreads) {
         const int rp = i / (C / 8), k = i % (C / 8);
@@ -434,13 +359,13 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     grid_barrier(a.gbar, gridDim.x);
     rimsrc = a.rim_buf;
   }
-  if (resident && (int)blockIdx.x >= B) {  // idle CTA: drain the weight copy, release TMEM
+  if (!have) {  // idle CTA: drain the weight copy, release TMEM
     tc::mbar_wait(&wbar, 0);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
-    epoch_finish(a, tag);
+    slot_finish(a, tag);
     return;
   }
 
@@ -449,10 +374,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   const int q = warp & 3;           // TMEM lane quarter of this warp
   const int tpar = warp >> 2;       // tile parity handled by this warp
 
-  for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-    const bool first = blk == (int)blockIdx.x;
-    int n = n0, by = by0, bx = bx0;
-    if (!first) entry_rows(a, idx, tag, blk, n, by, bx);
+  for (int blk = blockIdx.x;;) {
+    const int n = n0, by = by0, bx = bx0;
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
 
     // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
@@ -631,6 +554,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     tc::fence_after();
 
     if (inplace && resident) grid_wait(a.gbar, (unsigned)B);  // neighbours have read my rim
+    if (!rims_done) {  // fused in place: every rim snapshotted before my first store
+      slot_all_done(a);
+      rims_done = true;
+    }
     trace(a.trace, 10);
     // ---- 7. epilogue 3: +b3, + residual, store the block's clipped output window
     for (int t = tpar; t < K::NT2; t += 2) {
@@ -669,11 +596,20 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     tc::fence_before();
     __syncthreads();
     trace(a.trace, 11);
+    blk += gridDim.x;
+    if (fused) {
+      if (!slot_entry(a, tag, blk, n0, by0, bx0)) break;
+    } else {
+      if (blk >= B) break;
+      n0 = __ldcg(idx + 3 * blk);
+      by0 = __ldcg(idx + 3 * blk + 1);
+      bx0 = __ldcg(idx + 3 * blk + 2);
+    }
   }
 
   tc::fence_after();
   if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
-  epoch_finish(a, tag);
+  slot_finish(a, tag);
 }
 
 // Pre-pack W1/W2/W3 (transposed into the K-major plane layout) and the float params into
@@ -881,31 +817,36 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   bool weights_ready = false;
   trace(a.trace, 1);
   tc::pdl_wait();
-  int B;
+  int B = 0;
   const int32_t* idx = a.idx;
   unsigned tag = 0;
-  if (a.mask) {
-    const int Tc = g.n * g.gy * g.gx;
-    if (a.cst && (Tc + (int)gridDim.x - 1) / (int)gridDim.x <= kEpochMaxPer && gridDim.x <= 4096) {
-      tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
-      B = epoch_compact(a, tag);
-    } else {
-      B = fused_compact(a);
-    }
+  const bool inplace = a.x == a.out;
+  const bool fused = a.mask != nullptr;
+  int n1 = 0, by1 = 0, bx1 = 0;
+  bool have;
+  if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
+    tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
+    slot_produce<C, BS>(a, tag, inplace);
     idx = a.idx_out;
+    have = slot_entry(a, tag, pair, n1, by1, bx1);
   } else {
     B = ld_count(a.count, a.cap);
+    have = pair < B;
+    if (have) {
+      n1 = __ldcg(idx + 3 * pair);
+      by1 = __ldcg(idx + 3 * pair + 1);
+      bx1 = __ldcg(idx + 3 * pair + 2);
+    }
   }
   trace(a.trace, 2);
-  const bool inplace = a.x == a.out;
-  const bool resident = B <= npairs;
-  const __nv_bfloat16* rimsrc = nullptr;
-  if (inplace && !resident) {  // streamed in place: snapshot every block's rim first
+  const bool resident = !fused && B <= npairs;
+  const __nv_bfloat16* rimsrc = (fused && inplace) ? a.rim_buf : nullptr;
+  bool rims_done = !(fused && inplace);
+  if (!fused && inplace && !resident) {  // streamed in place: snapshot every block's rim first
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
     for (int blk = blockIdx.x; blk < B; blk += gridDim.x) {
-      int n, by, bx;
-      entry_rows(a, idx, tag, blk, n, by, bx);
+      const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
       const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
       for (int i = tid; i < Pr * (C / 8); i += kThreads) {
         const int rp = i / (C / 8), k = i % (C / 8);
@@ -921,22 +862,21 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     grid_barrier(a.gbar, gridDim.x);
     rimsrc = a.rim_buf;
   }
-  if (resident && pair >= B) {  // idle pair
+  if (!have) {  // idle pair
     tc::mbar_wait(&wbar, 0);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
-    epoch_finish(a, tag);
+    slot_finish(a, tag);
     return;
   }
   const Rim rim{BS, BS, 1};
   const int P = rim.pixels();
   uint8_t* A2peer = rank > 0 ? cl.map_shared_rank(A2, rank - 1) : nullptr;
 
-  for (int blk = pair; blk < B; blk += npairs) {
-    int n, by, bx;
-    entry_rows(a, idx, tag, blk, n, by, bx);
+  for (int blk = pair;;) {
+    const int n = n1, by = by1, bx = bx1;
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
     // ---- 1. stage my half of the window (pixels [128*rank, 128*rank + 128))
     constexpr int TOT = 128 * (C / 8);
@@ -1101,6 +1041,10 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     phase ^= 1;
     tc::fence_after();
     if (inplace && resident) grid_wait(a.gbar, 2u * (unsigned)B);
+    if (!rims_done) {  // fused in place: every rim snapshotted before my first store
+      slot_all_done(a);
+      rims_done = true;
+    }
     trace(a.trace, 10);
     // ---- 7. epilogue 3: +b3 + residual, my column half of my rows
 #pragma unroll
@@ -1125,11 +1069,24 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     tc::fence_before();
     __syncthreads();
     trace(a.trace, 11);
-    if (blk + npairs < B) cl.sync();  // partner done with my A2 before it writes the next halo
+    blk += npairs;
+    bool next;
+    if (fused) {
+      next = slot_entry(a, tag, blk, n1, by1, bx1);
+    } else {
+      next = blk < B;
+      if (next) {
+        n1 = __ldcg(idx + 3 * blk);
+        by1 = __ldcg(idx + 3 * blk + 1);
+        bx1 = __ldcg(idx + 3 * blk + 2);
+      }
+    }
+    if (!next) break;
+    cl.sync();  // partner done with my A2 before it writes the next block's halo rows
   }
   tc::fence_after();
   if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
-  epoch_finish(a, tag);
+  slot_finish(a, tag);
 }
 
 template <int C, int MC, int BS>

@@ -462,3 +462,26 @@ def test_unit_cta_pair_variant_bit_identical_to_single_cta(cuda_device, density,
         assert torch.equal(a, b) and torch.equal(a, c)
         outs.append(a)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("cin,block,density", [(128, 16, 1.0), (128, 16, 0.3), (64, 8, 0.5), (32, 16, 0.05)])
+def test_sparse_conv_double_buffered_bit_identical(cuda_device, cin, block, density):
+    """The double-buffered tcgen05 conv (window/accumulator ping-pong, warp-specialised)
+    computes exactly what the single-buffered kernel computes, over many blocks per CTA."""
+    lib = _lib.load()
+    rng = np.random.default_rng(cin * block)
+    h, w = 330, 290
+    x = torch.from_numpy(rng.standard_normal((2, h, w, cin)).astype(np.float32)).bfloat16()
+    wt = torch.from_numpy((rng.standard_normal((3, 3, cin, cin)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16()
+    fb = P.FilterBank(wt, torch.from_numpy(rng.standard_normal(cin).astype(np.float32)).bfloat16())
+    m = P.synth_mask_topleft((2, h, w), 1.0 - density)
+    p = _conv((3, 3), (1, 1), True, cin)
+    outs = []
+    for flags in (2, 0):
+        old = lib.sbn_debug_set_flags(flags)
+        try:
+            outs.append(P.sparse_conv2d(P.Tensor4D(x), m, fb, p, (block, block)).data)
+            torch.cuda.synchronize()
+        finally:
+            lib.sbn_debug_set_flags(old)
+    assert torch.equal(outs[0], outs[1])
