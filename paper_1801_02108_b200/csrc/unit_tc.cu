@@ -158,7 +158,7 @@ __device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag, bool
         a.idx_out[3 * pos] = fr;
         a.idx_out[3 * pos + 1] = rr / g.gx;
         a.idx_out[3 * pos + 2] = rr % g.gx;
-        st_release_u32(&a.etag[pos], tag);
+        if (!inplace) st_release_u32(&a.etag[pos], tag);
       }
     }
     __syncthreads();
@@ -180,6 +180,10 @@ __device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag, bool
           reinterpret_cast<uint4*>(a.rim_buf)[((size_t)pos * P + rp) * (C / 8) + k] = v;
         }
       }
+      // publish this round's entries only once their rims are in place
+      __threadfence();
+      __syncthreads();
+      if (tid < 32 && s_slot[tid] >= 0) st_release_u32(&a.etag[s_slot[tid]], tag);
     }
   }
   __syncthreads();
