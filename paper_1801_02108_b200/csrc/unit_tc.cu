@@ -101,14 +101,14 @@ __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162
 
 // ---- slot compaction (fused mask reduction of the single-kernel sparse_residual_unit).
 // Producers: CTA c tests candidates c, c+G, ... against the mask, claims list slots for its
-// active ones with ONE atomic per round, writes each entry, publishes it with the launch's
-// tag (release), and — in place — snapshots that block's halo rim into rim_buf[slot].
-// Then it increments `done`.  Consumers only wait for the entry they process (or for
-// done == G to learn that no more entries are coming); the in-place hazard needs all rims
-// snapshotted before any interior store, i.e. done == G just before epilogue 3.  Nothing is
+// active ones with ONE atomic per round, writes each entry and publishes it with the
+// launch's tag (release); then it increments `done`.  Consumers only wait for the entry
+// they process (or for done == G to learn that no more entries are coming).  In place,
+// the halo hazard is resolved just before the first store (slot_before_store).  Nothing is
 // reset on the critical path: the last CTA out clears the words and bumps the epoch, and
 // tags make stale entries from earlier launches invisible.
-//   words (sync ws, u32): [8] epoch, [9] seen, [10] slot counter, [11] done
+//   words (sync ws, u32): [8] epoch, [9] seen, [10] slot counter, [11] done, [12] staged,
+//                         [13..14] grid barrier (streamed in-place only)
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -118,19 +118,15 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int C, int BS>
-__device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag, bool inplace) {
+__device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag) {
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int s_flag[32];
-  __shared__ int s_slot[32];
   __shared__ int s_base;
   unsigned* w = a.gbar + 8;
   const int T = g.n * g.gy * g.gx;
   const int area = g.bh * g.bw;
   const int G = gridDim.x;
-  const Rim rim{BS, BS, 1};
-  const int P = rim.pixels();
   for (int r0 = blockIdx.x; r0 < T; r0 += 32 * G) {
     const int nj = min(32, (T - r0 + G - 1) / G);
     if (tid < 32) s_flag[tid] = 0;
@@ -150,47 +146,73 @@ __device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag, bool
       const unsigned bal = __ballot_sync(0xffffffffu, on);
       if (lane == 0) s_base = bal ? (int)atomicAdd(w + 2, (unsigned)__popc(bal)) : 0;
       __syncwarp();
-      s_slot[lane] = on ? s_base + __popc(bal & ((1u << lane) - 1u)) : -1;
       if (on) {
-        const int pos = s_slot[lane];
+        const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
         const int cand = r0 + lane * G;
         const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
         a.idx_out[3 * pos] = fr;
         a.idx_out[3 * pos + 1] = rr / g.gx;
         a.idx_out[3 * pos + 2] = rr % g.gx;
-        if (!inplace) st_release_u32(&a.etag[pos], tag);
+        st_release_u32(&a.etag[pos], tag);
       }
-    }
-    __syncthreads();
-    if (inplace) {  // snapshot the rims of this round's active blocks
-      for (int j = 0; j < nj; ++j) {
-        const int pos = s_slot[j];
-        if (pos < 0) continue;
-        const int cand = r0 + j * G;
-        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-        const int ys = g.oy + (rr / g.gx) * g.sy, xs = g.ox + (rr % g.gx) * g.sx;
-        for (int i = tid; i < P * (C / 8); i += kThreads) {
-          const int rp = i / (C / 8), k = i % (C / 8);
-          int wy, wx;
-          rim.coord(rp, wy, wx);
-          const int y = ys + wy, xx = xs + wx;
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-            v = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)fr * g.h + y) * g.w + xx) * (C / 8) + k);
-          reinterpret_cast<uint4*>(a.rim_buf)[((size_t)pos * P + rp) * (C / 8) + k] = v;
-        }
-      }
-      // publish this round's entries only once their rims are in place
-      __threadfence();
-      __syncthreads();
-      if (tid < 32 && s_slot[tid] >= 0) st_release_u32(&a.etag[s_slot[tid]], tag);
     }
   }
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    atomicAdd(w + 3, 1u);  // this producer is done (entries + rims published)
+    atomicAdd(w + 3, 1u);  // this producer is done
   }
+}
+
+// In-place fused: called by every consumer CTA after staging its FIRST window.
+__device__ __forceinline__ void slot_staged(const TcArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.gbar + 12, 1u);
+  }
+}
+
+// In-place fused, before the first store of the first block.  If every block had its own
+// consumer (B <= ncons) all windows were staged from x before any store: wait until all
+// B * ctas_per_block consumers have staged.  Otherwise (more blocks than consumers) the
+// rims of the blocks processed in later rounds are snapshotted now, by all CTAs, behind a
+// grid barrier (every CTA is active then).  Returns true when later rounds must read rims
+// from the snapshot.
+template <int C, int BS>
+__device__ __forceinline__ bool slot_before_store(const TcArgs& a, int ncons, int ctas_per_block) {
+  __shared__ int s_B;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* w = a.gbar + 8;
+    while (ld_acquire_u32(w + 3) != gridDim.x) __nanosleep(32);
+    s_B = (int)ld_acquire_u32(w + 2);
+    if (blockIdx.x == 0) *a.count_out = s_B;
+    if (s_B <= ncons)
+      while (ld_acquire_u32(a.gbar + 12) < (unsigned)(s_B * ctas_per_block)) __nanosleep(32);
+  }
+  __syncthreads();
+  const int B = s_B;
+  if (B <= ncons) return false;
+  const Geo& g = a.g;
+  const Rim r{BS, BS, 1};
+  const int Pr = r.pixels();
+  for (int blk = ncons + blockIdx.x; blk < B; blk += gridDim.x) {
+    const int n = __ldcg(a.idx_out + 3 * blk), by = __ldcg(a.idx_out + 3 * blk + 1), bx = __ldcg(a.idx_out + 3 * blk + 2);
+    const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+    for (int i = threadIdx.x; i < Pr * (C / 8); i += kThreads) {
+      const int rp = i / (C / 8), k = i % (C / 8);
+      int wy, wx;
+      r.coord(rp, wy, wx);
+      const int y = ys + wy, xx = xs + wx;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+        v = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
+      reinterpret_cast<uint4*>(a.rim_buf)[((size_t)blk * Pr + rp) * (C / 8) + k] = v;
+    }
+  }
+  grid_barrier(a.gbar + 13, gridDim.x);
+  return true;
 }
 
 // Entry `blk` of this launch: returns false when the list is complete and shorter.
@@ -227,20 +249,6 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
   return s_e[3] != 0;
 }
 
-// All producers done (rims snapshotted); returns the final block count.
-__device__ __forceinline__ int slot_all_done(const TcArgs& a) {
-  __shared__ int s_B;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned* w = a.gbar + 8;
-    while (ld_acquire_u32(w + 3) != gridDim.x) __nanosleep(32);
-    s_B = (int)ld_acquire_u32(w + 2);
-    if (blockIdx.x == 0) *a.count_out = s_B;
-  }
-  __syncthreads();
-  return s_B;
-}
-
 // Last CTA out clears the words and bumps the epoch (all CTAs have read them).
 __device__ __forceinline__ void slot_finish(const TcArgs& a, unsigned tag) {
   if (!tag) return;
@@ -252,6 +260,7 @@ __device__ __forceinline__ void slot_finish(const TcArgs& a, unsigned tag) {
       w[1] = 0u;
       w[2] = 0u;
       w[3] = 0u;
+      w[4] = 0u;  // staged counter
       w[0] = tag;  // next launch uses tag + 1
       __threadfence();
     }
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   bool have;
   if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
     tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
-    slot_produce<C, BS>(a, tag, inplace);
+    slot_produce(a, tag);
     idx = a.idx_out;
     have = slot_entry(a, tag, blockIdx.x, n0, by0, bx0);
   } else {
@@ -333,16 +342,17 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   }
   trace(a.trace, 2);
   // In place, a block's halo rim is its neighbours' interior, which they overwrite.
-  //  fused:     rims were snapshotted by the producers; wait for all of them before the
-  //             first store (slot_all_done).
+  //  fused:     windows are staged straight from x; before the first store,
+  //             slot_before_store waits until every block's consumer has staged (or, with
+  //             more blocks than consumers, snapshots the later rounds' rims).
   //  resident (B <= grid): every block has its own CTA; all windows are staged before
   //                        any CTA writes (split grid barrier: arrive after staging, wait
   //                        before epilogue 3).
   //  streamed (B > grid):  rims of all blocks are snapshotted first (grid barrier),
   //                        then windows read interiors from x and rims from the snapshot.
   const bool resident = !fused && B <= (int)gridDim.x;
-  const __nv_bfloat16* rimsrc = (fused && inplace) ? a.rim_buf : a.rim;
-  bool rims_done = !(fused && inplace);
+  const __nv_bfloat16* rimsrc = a.rim;
+  bool first_store = fused && inplace;  // slot_before_store still pending
   if (!fused && inplace && !resident) {
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
@@ -404,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     // in place + resident: announce "my window is read"; the matching wait sits right
     // before the first store of epilogue 3, so it overlaps the three GEMMs
     if (inplace && resident) grid_arrive(a.gbar);
+    if (first_store) slot_staged(a);
     trace(a.trace, 4);
     if (!weights_ready) {
       tc::mbar_wait(&wbar, 0);
@@ -558,9 +569,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     tc::fence_after();
 
     if (inplace && resident) grid_wait(a.gbar, (unsigned)B);  // neighbours have read my rim
-    if (!rims_done) {  // fused in place: every rim snapshotted before my first store
-      slot_all_done(a);
-      rims_done = true;
+    if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
+      if (slot_before_store<C, BS>(a, (int)gridDim.x, 1)) rimsrc = a.rim_buf;
+      first_store = false;
     }
     trace(a.trace, 10);
     // ---- 7. epilogue 3: +b3, + residual, store the block's clipped output window
@@ -830,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   bool have;
   if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
     tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
-    slot_produce<C, BS>(a, tag, inplace);
+    slot_produce(a, tag);
     idx = a.idx_out;
     have = slot_entry(a, tag, pair, n1, by1, bx1);
   } else {
@@ -844,8 +855,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   }
   trace(a.trace, 2);
   const bool resident = !fused && B <= npairs;
-  const __nv_bfloat16* rimsrc = (fused && inplace) ? a.rim_buf : nullptr;
-  bool rims_done = !(fused && inplace);
+  const __nv_bfloat16* rimsrc = nullptr;
+  bool first_store = fused && inplace;  // slot_before_store still pending
   if (!fused && inplace && !resident) {  // streamed in place: snapshot every block's rim first
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
@@ -903,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     }
     trace(a.trace, 3);
     if (inplace && resident) grid_arrive(a.gbar);
+    if (first_store) slot_staged(a);
     trace(a.trace, 4);
     if (!weights_ready) {
       tc::mbar_wait(&wbar, 0);
@@ -1045,9 +1057,9 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     phase ^= 1;
     tc::fence_after();
     if (inplace && resident) grid_wait(a.gbar, 2u * (unsigned)B);
-    if (!rims_done) {  // fused in place: every rim snapshotted before my first store
-      slot_all_done(a);
-      rims_done = true;
+    if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
+      if (slot_before_store<C, BS>(a, npairs, 2)) rimsrc = a.rim_buf;
+      first_store = false;
     }
     trace(a.trace, 10);
     // ---- 7. epilogue 3: +b3 + residual, my column half of my rows
