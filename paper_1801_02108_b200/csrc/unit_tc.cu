@@ -249,6 +249,27 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
   return s_e[3] != 0;
 }
 
+// Prefetch block `blk`'s in-image window rows into L2 (one bulk prefetch per row), so the
+// next iteration's window loads hit L2.  Fused mode: only if the entry is already published.
+template <int C, int BS>
+__device__ __forceinline__ void prefetch_window(const TcArgs& a, const int32_t* idx, unsigned tag,
+                                                int blk) {
+  const Geo& g = a.g;
+  if (threadIdx.x >= 32 || blk >= g.n * g.gy * g.gx) return;
+  if (tag) {
+    if (ld_acquire_u32(&a.etag[blk]) != tag) return;
+  } else if (blk >= ld_count(a.count, a.cap)) {
+    return;
+  }
+  const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
+  const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+  const int x0 = max(xs, 0), x1 = min(xs + BS, g.w);
+  const int wy = threadIdx.x;
+  const int y = ys + wy;
+  if (wy < BS && y >= 0 && y < g.h && x1 > x0)
+    tc::prefetch_l2(a.x + (((size_t)n * g.h + y) * g.w + x0) * C, (uint32_t)((x1 - x0) * C * 2));
+}
+
 // Last CTA out clears the words and bumps the epoch (all CTAs have read them).
 __device__ __forceinline__ void slot_finish(const TcArgs& a, unsigned tag) {
   if (!tag) return;
@@ -391,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   for (int blk = blockIdx.x;;) {
     const int n = n0, by = by0, bx = bx0;
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+    prefetch_window<C, BS>(a, idx, tag, blk + gridDim.x);
 
     // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
     constexpr int TOT = K::NPIX * (C / 8);
@@ -892,6 +914,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
 
   for (int blk = pair;;) {
     const int n = n1, by = by1, bx = bx1;
+    if (rank == 0) prefetch_window<C, BS>(a, idx, tag, blk + npairs);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
     // ---- 1. stage my half of the window (pixels [128*rank, 128*rank + 128))
     constexpr int TOT = 128 * (C / 8);
@@ -1208,7 +1231,9 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
   a.packed = (const uint8_t*)packed;
   a.rim_buf = (__nv_bfloat16*)rim_buf;
   a.gbar = gbar;
-  if (!(debug_flags() & kDebugNoPair)) {
+  // The CTA pair halves a block's latency chain but also halves the number of blocks in
+  // flight; it wins only when the candidate list is short (about one block per pair).
+  if (!(debug_flags() & kDebugNoPair) && cap <= 4 * sm_count() * 2) {
     if (c == 64 && m == 32 && g.bh == 16) return launch_pair<64, 32, 16>(a, cap, s);
     if (c == 64 && m == 64 && g.bh == 16) return launch_pair<64, 64, 16>(a, cap, s);
     if (c == 128 && m == 64 && g.bh == 16) return launch_pair<128, 64, 16>(a, cap, s);
