@@ -54,6 +54,14 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
                    const uint8_t* mask = nullptr, int32_t* idx_out = nullptr,
                    int32_t* count_out = nullptr, unsigned long long* cst = nullptr,
                    unsigned int* etag = nullptr);
+// wide tcgen05 path (unit_wide.cu): three chained implicit-GEMM launches over the stacked
+// active windows, for channel counts whose weights do not fit one CTA's shared memory
+bool unit_wide_supported(int dtype, int c, int m, const Geo& g, int halo, int pre_act);
+size_t unit_wide_packed_bytes(int c, int m);
+size_t unit_wide_stack_bytes(int m, const Geo& g);
+int unit_wide_pack(const sbn_unit_params* p, int c, int m, void* img, cudaStream_t s);
+int unit_wide_launch(const void* x, void* out, int c, int m, const Geo& g, const void* packed,
+                     const int32_t* idx, const int32_t* count, int cap, void* stacks, cudaStream_t s);
 // epoch compaction handles up to this many mask candidates per CTA (else fused_compact)
 constexpr int kEpochMaxPerHost = 1024;
 constexpr int kEpochMaxCtas = 4096;

@@ -249,9 +249,22 @@ int unit_rim_snapshot(const void* x, int es, int c, const Geo& g, int halo, cons
 //                    | rim snapshot (in-place calls) | packed tc image or SIMT scratch]
 constexpr size_t kBarBytes = 256;
 
+// wide tcgen05 path: [256 B | S1/S2 stacks | packed image (when none is given)]
+size_t unit_workspace_wide(int c, int m, const Geo& g) {
+  return kBarBytes + unit_wide_stack_bytes(m, g) + align_up(unit_wide_packed_bytes(c, m), 256);
+}
+
+// which tensor-core variant applies: 1 single-kernel unit, 2 wide (three launches), 0 none
+int unit_tc_kind(int dtype, int c, int m, const Geo& g, int halo, int pre_act) {
+  if (!(debug_flags() & kDebugForceWide) && unit_tc_supported(dtype, c, m, g, halo, pre_act)) return 1;
+  if (unit_wide_supported(dtype, c, m, g, halo, pre_act)) return 2;
+  return 0;
+}
+
 size_t unit_workspace(int dtype, int c, int m, const Geo& g, int halo, int algo, bool tc) {
   const int es = dtype_size(dtype);
   const int cap = g.n * g.gy * g.gx;
+  if (tc && unit_tc_kind(dtype, c, m, g, halo, 1) == 2) return unit_workspace_wide(c, m, g);
   size_t ws = kBarBytes + rim_bytes(es, c, g, halo, cap);
   if (tc) ws += align_up(unit_tc_packed_bytes(c, m, g), 256);  // packing when no image given
   if (!tc) {
@@ -270,15 +283,18 @@ using namespace sbn;
 extern "C" int sbn_residual_unit_algo(int dtype, int c, int m, const sbn_geometry* gp, int halo,
                                       int pre_act) {
   if (!gp) return SBN_ALGO_SIMT;
-  return unit_tc_supported(dtype, c, m, to_geo(gp), halo, pre_act) ? SBN_ALGO_TCGEN05
-                                                                   : SBN_ALGO_SIMT;
+  return unit_tc_kind(dtype, c, m, to_geo(gp), halo, pre_act) ? SBN_ALGO_TCGEN05 : SBN_ALGO_SIMT;
 }
 
 extern "C" size_t sbn_residual_unit_packed_bytes(int dtype, int c, int m, const sbn_geometry* gp,
                                                  int halo, int pre_act) {
   if (!gp) return 0;
   Geo g = to_geo(gp);
-  return unit_tc_supported(dtype, c, m, g, halo, pre_act) ? unit_tc_packed_bytes(c, m, g) : 0;
+  switch (unit_tc_kind(dtype, c, m, g, halo, pre_act)) {
+    case 1: return unit_tc_packed_bytes(c, m, g);
+    case 2: return unit_wide_packed_bytes(c, m);
+    default: return 0;
+  }
 }
 
 extern "C" int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
@@ -287,9 +303,10 @@ extern "C" int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c
   int st = check_geo(gp);
   if (st) return st;
   Geo g = to_geo(gp);
-  SBN_CHECK_ARG(unit_tc_supported(dtype, c, m, g, halo, pre_act), SBN_ERR_UNSUPPORTED,
-                "tcgen05 residual unit does not support this config");
+  const int kind = unit_tc_kind(dtype, c, m, g, halo, pre_act);
+  SBN_CHECK_ARG(kind != 0, SBN_ERR_UNSUPPORTED, "tcgen05 residual unit does not support this config");
   SBN_CHECK_ARG(p && packed, SBN_ERR_INVALID, "null argument");
+  if (kind == 2) return unit_wide_pack(p, c, m, packed, (cudaStream_t)stream);
   return unit_tc_pack(p, c, m, g, packed, (cudaStream_t)stream);
 }
 
@@ -297,7 +314,7 @@ extern "C" size_t sbn_residual_unit_workspace(int dtype, int c, int m, const sbn
                                               int halo, int algo) {
   if (!gp || dtype_size(dtype) == 0) return 0;
   Geo g = to_geo(gp);
-  const bool tc = algo != SBN_ALGO_SIMT && unit_tc_supported(dtype, c, m, g, halo, 1);
+  const bool tc = algo != SBN_ALGO_SIMT && unit_tc_kind(dtype, c, m, g, halo, 1) != 0;
   return unit_workspace(dtype, c, m, g, halo, algo, tc);
 }
 
@@ -321,14 +338,26 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
   SBN_CHECK_ARG(x && out && idx && count, SBN_ERR_INVALID, "null pointer argument");
   Geo g = to_geo(gp);
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tc_ok = unit_tc_supported(dtype, c, m, g, halo, pre_act);
+  const int kind = unit_tc_kind(dtype, c, m, g, halo, pre_act);
   if (algo == SBN_ALGO_TCGEN05)
-    SBN_CHECK_ARG(tc_ok, SBN_ERR_UNSUPPORTED, "tcgen05 residual unit does not support this config");
-  const bool use_tc = tc_ok && algo != SBN_ALGO_SIMT;
+    SBN_CHECK_ARG(kind != 0, SBN_ERR_UNSUPPORTED, "tcgen05 residual unit does not support this config");
+  const bool use_tc = kind != 0 && algo != SBN_ALGO_SIMT;
   const size_t need = unit_workspace(dtype, c, m, g, halo, algo, use_tc);
   const bool inplace = (x == out);
   const void* rim = nullptr;
   uint8_t* wsb = (uint8_t*)ws;
+  if (use_tc && kind == 2) {  // wide: three launches; kernel order resolves the in-place rims
+    SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
+                  "residual unit needs a %zu-byte workspace", need);
+    uint8_t* stacks = wsb + kBarBytes;
+    const void* packed = p->tc_packed;
+    if (!packed) {
+      packed = stacks + unit_wide_stack_bytes(m, g);
+      st = unit_wide_pack(p, c, m, (void*)packed, s);
+      if (st) return st;
+    }
+    return unit_wide_launch(x, out, c, m, g, packed, idx, count, cap, stacks, s);
+  }
   const size_t rb = kBarBytes + rim_bytes(dtype_size(dtype), c, g, halo, cap);
   if (inplace && halo > 0) {
     SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
@@ -418,9 +447,10 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
   uint8_t* rmws = sync8 + kBarBytes + kCstBytes;
   Geo g = to_geo(gp);
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tc = algo != SBN_ALGO_SIMT && unit_tc_supported(dtype, c, m, g, halo, pre_act);
+  const bool tc = algo != SBN_ALGO_SIMT && unit_tc_kind(dtype, c, m, g, halo, pre_act) == 1;
   if (algo == SBN_ALGO_TCGEN05)
-    SBN_CHECK_ARG(tc, SBN_ERR_UNSUPPORTED, "tcgen05 residual unit does not support this config");
+    SBN_CHECK_ARG(unit_tc_kind(dtype, c, m, g, halo, pre_act) != 0, SBN_ERR_UNSUPPORTED,
+                  "tcgen05 residual unit does not support this config");
   if (tc) {
     SBN_CHECK_ARG(gp->sy == gp->obh && gp->sx == gp->obw && gp->bh - 2 * halo == gp->obh &&
                       gp->oh == gp->h && gp->ow == gp->w,

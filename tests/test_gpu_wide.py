@@ -1,0 +1,112 @@
+"""GPU parity of the wide tcgen05 residual unit (unit_wide.cu: three chained implicit-GEMM
+launches over the stacked active windows) — the path of the BASELINE config-4 backbone
+stages (c = 96/192/256/384, m = c/2, blocks 16/16/10/6).
+
+bf16 against the fp32 oracle on bf16-rounded inputs/weights, rel_err <= 2e-2 (north star);
+inactive pixels bit-identical to x; in place == functional bit for bit.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_1801_02108_b200 as P
+from paper_1801_02108_b200 import _lib
+from paper_1801_02108_b200.layers import residual_unit_algo
+from oracle import sbnet_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FORCE_WIDE = 4  # SBN_DEBUG_FORCE_WIDE
+
+
+def _np(t):
+    t = t.data if isinstance(t, P.Tensor4D) else t
+    return t.float().detach().cpu().numpy()
+
+
+def _case(seed, n, h, w, c, m, density):
+    rng = np.random.default_rng(seed)
+    x = torch.from_numpy(rng.standard_normal((n, h, w, c)).astype(np.float32)).bfloat16()
+    u = P.random_unit_params(rng, c, m)
+    mk = np.concatenate([P.synth_mask_blobs((1, h, w), 1.0 - density, seed + i).numpy()
+                         for i in range(n)])
+    return x, u, P.BinaryMask(mk)
+
+
+def _oracle(x_bf16, u, mk, block):
+    def r(a):
+        return torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()
+    ud = {"pre": u.pre_activation}
+    for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
+        ud[f"w{i}"], ud[f"b{i}"] = r(fb.weights), r(fb.bias)
+        ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
+    return O.sparse_residual_unit(x_bf16.float().numpy(), mk.numpy(), ud, block)
+
+
+# (c, m, block, h, w): the four config-4 stage shapes (sizes cut for the oracle), plus
+# ragged borders (h, w not multiples of the output block)
+WIDE = [(96, 48, 16, 72, 60), (192, 96, 16, 60, 44), (256, 128, 10, 41, 37), (384, 192, 6, 26, 22),
+        (128, 64, 12, 50, 34)]
+
+
+@pytest.mark.parametrize("c,m,block,h,w", WIDE)
+def test_wide_unit_vs_fp32_oracle(cuda_device, c, m, block, h, w):
+    x, u, mk = _case(c + block, 2, h, w, c, m, 0.3)
+    spec = P.unit_spec(tuple(x.shape), (block, block))
+    assert residual_unit_algo(torch.bfloat16, u, spec) == "tcgen05"
+    ref = _oracle(x, u, mk, (block, block))
+    outs = []
+    for inplace in (False, True):
+        xt = P.Tensor4D(x.clone().cuda())
+        y = P.sparse_residual_unit(xt, mk, u, (block, block), inplace=inplace)
+        outs.append(y.data.cpu())
+        err = O.rel_err(_np(y), ref)
+        assert err <= 2e-2, (c, m, block, inplace, err)
+    assert torch.equal(outs[0], outs[1]), "in place differs from functional"
+    # inactive pixels are bit-identical to x
+    g = O.unit_geometry(h, w, (block, block))
+    reg = O.active_region(g, O.reduce_mask(mk.numpy(), g), x.shape[0])
+    assert torch.equal(outs[0][~torch.from_numpy(reg)], x[~torch.from_numpy(reg)])
+
+
+def test_wide_unit_full_and_empty_mask(cuda_device):
+    x, u, _ = _case(3, 1, 40, 36, 192, 96, 0.5)
+    full = P.BinaryMask(np.ones((1, 40, 36), np.uint8))
+    y = P.sparse_residual_unit(P.Tensor4D(x.cuda()), full, u, (16, 16))
+    assert O.rel_err(_np(y), _oracle(x, u, full, (16, 16))) <= 2e-2
+    empty = P.BinaryMask(np.zeros((1, 40, 36), np.uint8))
+    y0 = P.sparse_residual_unit(P.Tensor4D(x.cuda()), empty, u, (16, 16))
+    assert torch.equal(y0.data.cpu(), x)
+
+
+@pytest.mark.parametrize("block", [16, 8])
+def test_wide_matches_single_kernel_unit(cuda_device, block):
+    """Where both tcgen05 variants apply (c=64, m=32) they agree (accumulation order of
+    the 3x3 differs, so within bf16 rounding, not bit for bit)."""
+    lib = _lib.load()
+    x, u1, mk = _case(11, 2, 96, 80, 64, 32, 0.25)
+    _, u2, _ = _case(11, 2, 96, 80, 64, 32, 0.25)  # separate packed-image caches
+    a = P.sparse_residual_unit(P.Tensor4D(x.cuda()), mk, u1, (block, block)).data.float().cpu()
+    prev = lib.sbn_debug_set_flags(FORCE_WIDE)
+    try:
+        b = P.sparse_residual_unit(P.Tensor4D(x.cuda()), mk, u2, (block, block)).data.float().cpu()
+    finally:
+        lib.sbn_debug_set_flags(prev)
+    assert O.rel_err(b.numpy(), a.numpy()) <= 1e-2
+    ref = _oracle(x, u1, mk, (block, block))
+    assert O.rel_err(b.numpy(), ref) <= 2e-2
+
+
+def test_wide_stage_chain(cuda_device):
+    """A stage of 3 chained wide units sharing one index list (run_stage) against the
+    oracle applied unit by unit on the same bf16-rounded weights."""
+    rng = np.random.default_rng(5)
+    cfg = P.StageConfig(unit_count=3, channels=(96, 48, 96), block_size=(16, 16))
+    stage = P.build_stage(cfg, rng)
+    x = torch.from_numpy(rng.standard_normal((1, 64, 56, 96)).astype(np.float32)).bfloat16()
+    mk = P.synth_mask_blobs((1, 64, 56), 0.7, 2)
+    res = P.run_stage(stage, P.Tensor4D(x.cuda()), mk)
+    ref = x.clone()
+    for u in stage.units:
+        ref = torch.from_numpy(_oracle(ref, u, mk, (16, 16))).bfloat16()
+    assert O.rel_err(_np(res.output), ref.float().numpy()) <= 2e-2
