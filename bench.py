@@ -440,6 +440,69 @@ def run_batched(P, torch, dev, time_graph, u, hbm_peak, unit_fn):
     return out
 
 
+def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, per_stage=True):
+    """BASELINE config 4 (config 5 per-GPU shard when frames = 64/G): the 4-stage sparse
+    detector backbone (perf.DETECTOR_STAGES: [3, 6, 6, 3] bottleneck units, 96/192/256/384
+    channels, dense stride-2 cuDNN projections) on `frames` 800x700 BEV frames with seeded
+    blob masks, sparse (one index list per stage, in-place tcgen05 units) vs the dense
+    backbone (cuDNN convs + BN/ReLU), both captured in CUDA graphs."""
+    import numpy as np
+    from paper_1801_02108_b200 import perf
+    from paper_1801_02108_b200.layers import residual_unit_algo
+    hh, ww, cin = perf.DETECTOR_INPUT
+    bb = P.build_backbone(perf.detector_stage_configs(), np.random.default_rng(4))
+    x = torch.randn(frames, hh, ww, cin, device=dev).bfloat16()
+    mk = np.concatenate([P.synth_mask_blobs((1, hh, ww), 1.0 - density, s).numpy() for s in range(frames)])
+    mask = P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False)
+    xt = P.Tensor4D(x)
+    res = P.run_backbone(bb, xt, mask)  # warm: weight images, scratch buffers
+    dres = P.run_backbone(bb, xt, mask, sparse=False)
+    torch.cuda.synchronize()
+
+    def timed(fn, n=reps):
+        g, st = time_graph(torch, fn, n, 2, soak_s=0.05)
+        with torch.cuda.stream(st):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(st)
+            g.replay()
+            b_.record(st)
+            b_.synchronize()
+        del g
+        return a_.elapsed_time(b_) / n
+
+    def sp(k):
+        for _ in range(k):
+            P.run_backbone(bb, xt, mask)
+
+    def de(k):
+        for _ in range(k):
+            P.run_backbone(bb, xt, mask, sparse=False)
+    t_sp, t_de = timed(sp), timed(de)
+    f_sp, f_de = perf.flops_backbone(res, bb.stages, True), perf.flops_backbone(dres, bb.stages, False)
+    out = {"workload": f"config4: 4-stage sparse detector backbone, N={frames} x {hh}x{ww}x{cin} bf16, "
+                       f"{density:.0%} blob masks (seeds 0..{frames - 1})",
+           "frames": frames, "sparse_ms": round(t_sp, 4), "dense_ms": round(t_de, 4),
+           "frames_per_s": round(frames / (t_sp * 1e-3), 1), "frames_per_s_dense": round(frames / (t_de * 1e-3), 1),
+           "speedup_vs_dense": round(t_de / t_sp, 3),
+           "tflops_alg_sparse": round(f_sp / (t_sp * 1e-3) / 1e12, 1),
+           "tflops_alg_dense": round(f_de / (t_de * 1e-3) / 1e12, 1), "stages": []}
+    if per_stage:
+        inp = xt
+        for i, (stg, r) in enumerate(zip(bb.stages, res)):
+            m_i = stg.config.channels[1]
+            t1 = timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask) for _ in range(k)])
+            t2 = timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False) for _ in range(k)])
+            n_, h_, w_, c_ = r.output.dims
+            out["stages"].append({"stage": i + 2, "hw": [h_, w_], "c": c_, "m": m_i,
+                                  "block": stg.config.block_size[0], "units": stg.config.unit_count,
+                                  "blocks": int(r.indices.count),
+                                  "density": round(float(r.mask.data.float().mean()), 4),
+                                  "algo": residual_unit_algo(torch.bfloat16, stg.units[0], r.spec),
+                                  "sparse_ms": round(t1, 4), "dense_ms": round(t2, 4)})
+            inp = r.output
+    return out
+
+
 def run_gather_scatter(P, torch, dev, time_graph, hbm_peak):
     """sbn_gather / sbn_scatter(add) on 800x700x128 bf16 with a full mask and 16x16 blocks
     (config-3 sizes, 100% density: ~190 MB block stack); algorithmic bytes = in-image

@@ -21,38 +21,73 @@
 // interior), so there is no rim snapshot and no grid barrier.  Launches chain with
 // programmatic dependent launch; S1/S2 stay mostly in L2.
 //
-// Warp roles per persistent CTA (320 threads):
-//   warps 0-3  A producers: per 128-row tile and K-chunk, load the rows (16-B vectors,
-//              all in flight), apply the transform, store the K-major plane layout of
-//              tc_util.cuh into an SA-deep ring
-//   warps 4-7  epilogue: tcgen05.ld of the accumulator (TMEM lane quarter = warp % 4),
-//              transform, vector stores; double-buffered accumulators when 2*N <= 512
-//   warp 8     W producer: cp.async.bulk of pre-packed weight chunks through an SW ring
-//   warp 9     MMA issuer (one thread): tcgen05.mma M=128, N<=256 per instruction
+// Operands arrive by TMA (cp.async.bulk.tensor): one box per 16-byte channel plane lands
+// as R rows x 16 B — exactly the K-major plane layout of tc_util.cuh.  IN gathers straight
+// from x with a 4-D map (C, W, H, N) and a box of (8 ch, b, hb rows, 1 frame) at the
+// block's (possibly negative) window origin: TMA zero-fills out-of-image pixels, so the
+// gather's halo semantics (`blocks.py:66-73`) come for free.  MID/OUT read the stacks
+// through 2-D maps.
+//
+// Warp roles per persistent CTA (576 threads):
+//   warps 0-7   IN only: BN1 + ReLU in place on each landed chunk (pair-of-planes
+//               mapping, conflict-free)
+//   warps 8-15  epilogue: tcgen05.ld of the accumulator (TMEM lane quarter = warp % 4,
+//               two warps per quarter split the columns), transform, vector stores;
+//               double-buffered accumulators when 2*N <= 512
+//   warp 16     loader: TMA boxes of A chunks into an SA-deep ring, weight chunks (all
+//               resident, or streamed through an SW ring)
+//   warp 17     MMA issuer (one thread): tcgen05.mma M=128, N<=256 per instruction
 #include "unit.cuh"
 #include "tc_util.cuh"
+
+#include <cuda.h>  // CUtensorMap (TMA descriptors)
+#include <cstring>
 
 namespace sbn {
 namespace {
 
-constexpr int kAThreads = 128;
-constexpr int kEThreads = 128;
+constexpr int kAThreads = 256;
+constexpr int kEThreads = 256;
 constexpr int kWideThreads = kAThreads + kEThreads + 64;
 constexpr int kMaxRows = 168;  // staged rows of a MID tile: 128 + 2*b + 2 (b <= 18)
 
 enum { kIn = 1, kMid = 2, kOut = 3 };
 
+constexpr int kBudget = 210 * 1024;
+
+// K-chunk choice: the largest of {K (<= 96), 64, 32, 16} that keeps ALL weight chunks
+// resident in shared memory next to a 3-deep A ring; 0 when no chunking does (weights
+// are then streamed through a ring).
+template <int K, int N, int MODE>
+constexpr int resident_kc() {
+  constexpr int taps = MODE == kMid ? 9 : 1;
+  constexpr int ra = MODE == kMid ? kMaxRows : 128;
+  constexpr long wbytes = (long)taps * K * N * 2;
+  constexpr int pref = K <= 96 ? K : (K % 64 == 0 ? 64 : 32);
+  constexpr int cands[4] = {pref, 64, 32, 16};
+  for (int i = 0; i < 4; ++i) {
+    const int kc = cands[i];
+    if (kc > pref || K % kc != 0 || kc % 16 != 0) continue;
+    const long ach = (long)(kc / 8) * ra * 16;
+    if (3 * ach + wbytes + 8192 <= kBudget) return kc;
+  }
+  return 0;
+}
+
 template <int K, int N, int MODE>
 struct WCfg {
   static constexpr int TAPS = MODE == kMid ? 9 : 1;
-  static constexpr int KC = K <= 96 ? K : (K % 64 == 0 ? 64 : 32);
+  static constexpr int RKC = resident_kc<K, N, MODE>();
+  static constexpr bool RES = RKC != 0;  // weights resident for the whole kernel
+  static constexpr int KC = RES ? RKC : (K % 64 == 0 ? 64 : 32);
   static_assert(K % KC == 0 && KC % 16 == 0, "K chunking");
   static constexpr int NKC = K / KC;
+  static constexpr int P = KC / 8;         // 16-byte planes per chunk
   static constexpr int RA = MODE == kMid ? kMaxRows : 128;
-  static constexpr int PA = RA * 16 + 16;  // A plane stride (16-B pad: conflict-free staging)
-  static constexpr int ACH = (KC / 8) * PA;
+  static constexpr int PA = RA * 16;       // A plane stride (multiple of 128: TMA destination)
+  static constexpr int ACH = P * PA;
   static constexpr int PW = N * 16;
-  static constexpr int WCH = (KC / 8) * PW;
+  static constexpr int WCH = P * PW;
   static constexpr int NSPLIT = N > 256 ? 2 : 1;
   static constexpr int NS = N / NSPLIT;
   static_assert(N % NSPLIT == 0 && NS % 16 == 0 && NS <= 256, "UMMA N");
@@ -63,20 +98,31 @@ struct WCfg {
   static constexpr int NPAR = MODE == kIn ? 2 * K + 3 * N : MODE == kMid ? 3 * N : N;
   static constexpr int al(int v) { return (v + 127) / 128 * 128; }
   static constexpr int PARB = al(NPAR * 4);
-  static constexpr int BUDGET = 210 * 1024;
-  static constexpr int SA = (4 * ACH + 2 * WCH + PARB <= BUDGET) ? 4 : (3 * ACH + 2 * WCH + PARB <= BUDGET) ? 3 : 2;
-  static constexpr int SW = (SA * ACH + 4 * WCH + PARB <= BUDGET) ? 4 : (SA * ACH + 3 * WCH + PARB <= BUDGET) ? 3 : 2;
-  static_assert(SA * ACH + SW * WCH + PARB <= BUDGET, "shared memory budget");
-  static constexpr int OFF_W = SA * ACH;
-  static constexpr int OFF_PAR = OFF_W + SW * WCH;
-  static constexpr int SMEM = OFF_PAR + PARB;
-  static constexpr int ITEMS = (RA * (KC / 8) + kAThreads - 1) / kAThreads;
   static constexpr int CHUNKS = NKC * TAPS;                       // weight chunks per tile
   static constexpr size_t WBYTES = (size_t)CHUNKS * WCH;          // packed weight bytes
+  // resident: A ring as deep as fits (<= 6); streamed: A ring 2..4, W ring 2..4
+  static constexpr int SA = RES ? ((int)((kBudget - (long)WBYTES - PARB) / ACH) > 6 ? 6 : (int)((kBudget - (long)WBYTES - PARB) / ACH))
+                                : (4 * ACH + 2 * WCH + PARB <= kBudget) ? 4 : (3 * ACH + 2 * WCH + PARB <= kBudget) ? 3 : 2;
+  static constexpr int SW = RES ? 0 : (SA * ACH + 4 * WCH + PARB <= kBudget) ? 4 : (SA * ACH + 3 * WCH + PARB <= kBudget) ? 3 : 2;
+  static constexpr long WREG = RES ? (long)WBYTES : (long)SW * WCH;
+  static_assert(SA >= 2 && SA * ACH + WREG + PARB <= kBudget, "shared memory budget");
+  static constexpr int OFF_W = SA * ACH;
+  static constexpr int OFF_PAR = OFF_W + (int)WREG;
+  static constexpr int SMEM = OFF_PAR + PARB;
+  static constexpr int ITEMS = (128 * P + kAThreads - 1) / kAThreads;  // IN transform pieces per thread
 };
 
-struct WArgs {
-  const __nv_bfloat16* src;  // IN: x    MID: S1    OUT: S2
+// IN transform piece i of a chunk (128 rows x P planes): consecutive thread PAIRS take
+// consecutive rows, the two threads of a pair two adjacent planes, so a warp touches 16
+// rows of 2 planes — conflict-free smem.
+__device__ __forceinline__ void item_rk(int i, int& r, int& k8) {
+  const int q = i >> 1;
+  r = q & 127;
+  k8 = 2 * (q >> 7) + (i & 1);
+}
+
+struct __align__(64) WArgs {
+  CUtensorMap tmap;          // A operand: IN x (C, W, H, N) | MID S1 (m, rows) | OUT S2 (m, rows)
   __nv_bfloat16* dst;        // IN: S1   MID: S2    OUT: out
   const uint8_t* wpk;        // this GEMM's packed weight chunks
   const float* par;          // this GEMM's parameter vectors
@@ -84,37 +130,68 @@ struct WArgs {
   const int32_t* idx;
   const int32_t* count;
   int cap;
+  int hb, S, G;              // IN: window rows per slab, slabs per block, slabs per tile
+  int slab_rows;             // IN: tile rows per slab (hb*b rounded to 8: 128-B aligned TMA boxes)
+  int box_rows;              // MID: rows per A box (128 + 2b + 2, rounded to 8)
+  unsigned long long* trace; // diagnostics: CTA 0 event stamps (sbn_debug_set_trace)
 };
 
-__device__ __forceinline__ void abar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// CTA 0 event log (diagnostics): slot ev*64 + tile, tiles < 64
+enum { kEvPub = 0, kEvMma = 1, kEvAcc = 2, kEvEpi = 3, kEvIss = 4, kEvLoad = 5 };
+__device__ __forceinline__ void wtrace(const WArgs& a, int ev, int t) {
+  if (a.trace && blockIdx.x == 0 && t < 64) {
+    a.trace[ev * 64 + t] = gtimer();
+    a.trace[1024 + ev * 64 + t] = clock64();
+  }
+}
 
-// rows of the GEMM for B active blocks of size b
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+// tiles of the GEMM for B active blocks of size b
 template <int MODE>
-__device__ __forceinline__ long total_rows(int B, int b) {
-  return MODE == kOut ? (long)B * (b - 2) * (b - 2) : (long)B * b * b;
+__device__ __forceinline__ int tile_count(const WArgs& a, int B, int b) {
+  if (MODE == kIn) return (B * a.S + a.G - 1) / a.G;
+  const long rows = MODE == kOut ? (long)B * (b - 2) * (b - 2) : (long)B * b * b;
+  return (int)((rows + 127) / 128);
 }
 
 template <int K, int N, int MODE>
-__global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
+__global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid_constant__ WArgs a) {
   using Q = WCfg<K, N, MODE>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t a_full[Q::SA], a_empty[Q::SA], w_full[Q::SW], w_empty[Q::SW];
+  constexpr int SWB = Q::SW > 0 ? Q::SW : 1;
+  __shared__ uint64_t a_load[Q::SA], a_full[Q::SA], a_empty[Q::SA], w_full[SWB], w_empty[SWB];
   __shared__ uint64_t acc_full[Q::NACC], acc_empty[Q::NACC];
   __shared__ uint32_t tslot;
-  __shared__ long long rowoff[Q::RA];
   uint8_t* Aring = smem;
   uint8_t* Wring = smem + Q::OFF_W;
   float* par = reinterpret_cast<float*>(smem + Q::OFF_PAR);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Geo& g = a.g;
   const int b = g.bh;
+  constexpr int kLWarp = (kAThreads + kEThreads) / 32, kMWarp = kLWarp + 1;
 
   if (tid == 0) {
     for (int s = 0; s < Q::SA; ++s) {
-      tc::mbar_init(&a_full[s], kAThreads);
+      tc::mbar_init(&a_load[s], 1);
+      tc::mbar_init(&a_full[s], MODE == kIn ? kAThreads : 1);
       tc::mbar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < Q::SW; ++s) {
+    for (int s = 0; s < SWB; ++s) {
       tc::mbar_init(&w_full[s], 1);
       tc::mbar_init(&w_empty[s], 1);
     }
@@ -124,6 +201,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
     }
     tc::mbar_fence_init();
   }
+  if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
   for (int i = tid; i < Q::NPAR; i += kWideThreads) par[i] = a.par[i];
   if (warp == 0) tc::tmem_alloc<Q::TALLOC>(&tslot);
   tc::fence_before();
@@ -131,117 +209,157 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
   tc::fence_after();
   const uint32_t tmem = tslot;
   tc::pdl_trigger();
+  if (Q::RES && tid == kLWarp * 32) {
+    // resident weights: every chunk lands once, under the previous kernel's tail (weights
+    // do not depend on it), completion on w_full[0]
+    tc::mbar_expect_tx(&w_full[0], (uint32_t)Q::WBYTES);
+    for (int c = 0; c < Q::CHUNKS; ++c)
+      tc::bulk_g2s(Wring + (size_t)c * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[0]);
+  }
   tc::pdl_wait();  // the previous launch's S1 / S2 / x and the index list are visible
   const int B = ld_count(a.count, a.cap);
-  const long TR = total_rows<MODE>(B, b);
-  const int ntiles = (int)((TR + 127) / 128);
+  const int ntiles = tile_count<MODE>(a, B, b);
 
-  if (warp < 4) {
-    // ------------------------------------------------ A producers
-    const int rows = MODE == kMid ? 128 + 2 * b + 2 : 128;
-    const int bb = b * b;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      abar_sync();  // everyone is done with the previous tile's rowoff
-      for (int r = tid; r < Q::RA; r += kAThreads) {
-        const long gr = (long)tile * 128 + r;
-        long long off = -1;
-        if (r < rows && gr < TR) {
-          if (MODE == kIn) {
-            const int j = (int)(gr / bb), p = (int)(gr - (long)j * bb);
-            const int n = __ldg(a.idx + 3 * j), by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-            const int y = g.oy + by * g.sy + p / b, x = g.ox + bx * g.sx + p % b;
-            if (y >= 0 && y < g.h && x >= 0 && x < g.w) off = (((long long)n * g.h + y) * g.w + x) * K;
-          } else {
-            off = gr * K;
-          }
-        }
-        rowoff[r] = off;
-      }
-      abar_sync();
-      for (int kc = 0; kc < Q::NKC; ++kc, ++it) {
-        const int s = it % Q::SA;
-        tc::mbar_wait(&a_empty[s], ((it / Q::SA) & 1) ^ 1);
-        uint8_t* A = Aring + s * Q::ACH;
-        uint4 raw[Q::ITEMS];
+  if (tid < kAThreads) {
+    // ------------------------------------------------ IN: BN1 + ReLU on landed chunks
+    if (MODE == kIn) {
+      const float* s1 = par;
+      const float* t1 = par + K;
+      int c = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int kc = 0; kc < Q::NKC; ++kc, ++c) {
+          const int s = c % Q::SA;
+          tc::mbar_wait(&a_load[s], (c / Q::SA) & 1);
+          uint8_t* A = Aring + s * Q::ACH;
+          uint4 raw[Q::ITEMS];
+          uint32_t sa_[Q::ITEMS];
 #pragma unroll
-        for (int j = 0; j < Q::ITEMS; ++j) {
-          const int i = tid + j * kAThreads;
-          const int r = i / (Q::KC / 8), k8 = i % (Q::KC / 8);
-          raw[j] = make_uint4(0, 0, 0, 0);
-          if (r < Q::RA) {
-            const long long off = rowoff[r];
-            if (off >= 0) raw[j] = __ldg(reinterpret_cast<const uint4*>(a.src + off + kc * Q::KC) + k8);
+          for (int j = 0; j < Q::ITEMS; ++j) {
+            const int i = tid + j * kAThreads;
+            int r, k8;
+            item_rk(i, r, k8);
+            sa_[j] = tc::smem_u32(A + k8 * Q::PA + r * 16);
+            if (i < 128 * Q::P)
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(raw[j].x), "=r"(raw[j].y), "=r"(raw[j].z), "=r"(raw[j].w)
+                           : "r"(sa_[j]));
           }
-        }
 #pragma unroll
-        for (int j = 0; j < Q::ITEMS; ++j) {
-          const int i = tid + j * kAThreads;
-          const int r = i / (Q::KC / 8), k8 = i % (Q::KC / 8);
-          if (r >= Q::RA) break;
-          uint4 v = raw[j];
-          if (MODE == kIn && rowoff[r] >= 0) {
-            const float* s1 = par;
-            const float* t1 = par + K;
+          for (int j = 0; j < Q::ITEMS; ++j) {
+            const int i = tid + j * kAThreads;
+            if (i >= 128 * Q::P) break;
+            int r, k8;
+            item_rk(i, r, k8);
+            const float4* sv = reinterpret_cast<const float4*>(s1 + kc * Q::KC + k8 * 8);
+            const float4* tv = reinterpret_cast<const float4*>(t1 + kc * Q::KC + k8 * 8);
+            const float4 sa = sv[0], sb = sv[1], ta = tv[0], tb = tv[1];
+            const float sc[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+            const float sh[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[j]);
             uint32_t o[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const float2 f = __bfloat1622float2(h[e]);
-              const int ch = kc * Q::KC + k8 * 8 + 2 * e;
-              o[e] = tc::pack_bf16(fmaxf(__fadd_rn(__fmul_rn(f.x, s1[ch]), t1[ch]), 0.f),
-                                   fmaxf(__fadd_rn(__fmul_rn(f.y, s1[ch + 1]), t1[ch + 1]), 0.f));
+              o[e] = tc::pack_bf16(fmaxf(fmaf(f.x, sc[2 * e], sh[2 * e]), 0.f),
+                                   fmaxf(fmaf(f.y, sc[2 * e + 1], sh[2 * e + 1]), 0.f));
             }
-            v = make_uint4(o[0], o[1], o[2], o[3]);
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sa_[j]), "r"(o[0]), "r"(o[1]),
+                         "r"(o[2]), "r"(o[3])
+                         : "memory");
           }
-          *reinterpret_cast<uint4*>(A + k8 * Q::PA + r * 16) = v;
+          tc::fence_async_smem();
+          tc::mbar_arrive(&a_full[s]);
+          if (tid == 0 && kc == Q::NKC - 1) wtrace(a, kEvPub, c / Q::NKC);
         }
-        tc::fence_async_smem();
-        tc::mbar_arrive(&a_full[s]);
-      }
     }
-  } else if (warp < 8) {
+  } else if (tid < kAThreads + kEThreads) {
     // ------------------------------------------------ epilogue
-    const int qd = warp & 3;
+    // warp w drains TMEM lane quarter w % 4; the two warps of a quarter take alternate
+    // 16-column chunks.  IN: relu(acc*s2 + t2'), x in-bounds (t2' = b1*s2 + t2, folded at
+    // pack time); MID: relu(acc*s3 + t3'); OUT: x + acc + b3.  One bf16 rounding each.
+    const int ew = warp - kAThreads / 32;
+    const int qd = warp & 3, half = ew >> 2;
     const int r = qd * 32 + lane;
     const int bb = b * b, ob = b - 2;
+    const long TR = MODE == kOut ? (long)B * ob * ob : (long)B * bb;
+    constexpr int NCH = N / 16;                 // 16-column chunks
+    constexpr int MYCH = (NCH + 1) / 2;         // chunks of this half (upper bound)
+    constexpr int PG = MODE == kOut ? (MYCH < 6 ? MYCH : 6) : 0;  // residual chunks prefetched a tile ahead
+    const float* sc = MODE == kIn ? par + 2 * K + N : par + N;  // IN: s2 | MID: s3
+    const float* sh = sc + N;                                     // t2' | t3'
+    // per-row metadata of a tile; the block-index loads (IN, OUT) are issued one tile
+    // ahead (idx_next) and consumed by meta() after the current tile's drain
+    int xn = 0, xby = 0, xbx = 0;
+    auto idx_next = [&](int tile) {
+      const long gr = (long)tile * 128 + r;
+      int j = -1;
+      if (MODE == kIn) {
+        const int i = r / a.slab_rows, sl = tile * a.G + i;
+        if (i < a.G && sl < B * a.S) j = sl / a.S;
+      } else if (MODE == kOut && gr < TR) {
+        j = (int)(gr / (ob * ob));
+      }
+      if (j >= 0) {
+        xn = __ldg(a.idx + 3 * j);
+        xby = __ldg(a.idx + 3 * j + 1);
+        xbx = __ldg(a.idx + 3 * j + 2);
+      }
+    };
+    bool store = false, valid = true;
+    __nv_bfloat16* dp = a.dst;
+    uint4 res[PG > 0 ? 2 * PG : 1];
+    auto meta = [&](int tile) {
+      const long gr = (long)tile * 128 + r;
+      store = (MODE == kIn || gr < TR) && tile < ntiles;
+      valid = true;
+      dp = a.dst;
+      if (!store) return;
+      if (MODE == kIn) {
+        // tile = G slabs of hb window rows; this row -> (block j, window row wy, col wx)
+        const int i = r / a.slab_rows, rr = r - i * a.slab_rows;
+        const int sl = tile * a.G + i;
+        const int j = sl / a.S, q = sl - j * a.S;
+        const int wy = q * a.hb + rr / b, wx = rr % b;
+        store = i < a.G && sl < B * a.S && rr < a.hb * b && wy < b;
+        const int y = g.oy + xby * g.sy + wy, x = g.ox + xbx * g.sx + wx;
+        valid = y >= 0 && y < g.h && x >= 0 && x < g.w;
+        dp = a.dst + ((long)j * bb + wy * b + wx) * N;
+      } else if (MODE == kMid) {
+        const int j = (int)(gr / bb), p = (int)(gr - (long)j * bb);
+        const int oy = p / b, ox = p % b;
+        store = oy < ob && ox < ob;
+        dp = a.dst + ((long)j * ob * ob + oy * ob + ox) * N;
+      } else {
+        const int j = (int)(gr / (ob * ob)), p = (int)(gr - (long)j * ob * ob);
+        const int oy = p / ob, ox = p % ob;
+        const int Y = xby * g.obh + oy, X = xbx * g.obw + ox;
+        store = Y < g.oh && X < g.ow;
+        dp = a.dst + (((long)xn * g.oh + Y) * g.ow + X) * N;  // residual read from the same row
+#pragma unroll
+        for (int e = 0; e < PG; ++e) {
+          const int c0 = 16 * (2 * e + half);
+          if (store && c0 < N) {
+            res[2 * e] = reinterpret_cast<const uint4*>(dp + c0)[0];
+            res[2 * e + 1] = reinterpret_cast<const uint4*>(dp + c0)[1];
+          }
+        }
+      }
+    };
+    idx_next(blockIdx.x);
+    meta(blockIdx.x);
     int k = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
       const int buf = Q::NACC == 2 ? (k & 1) : 0;
       const int use = Q::NACC == 2 ? (k >> 1) : k;
-      const long gr = (long)tile * 128 + r;
-      bool store = gr < TR;
-      bool valid = true;  // IN: in-bounds pixel
-      __nv_bfloat16* dp = nullptr;
-      const __nv_bfloat16* xp = nullptr;
-      if (store) {
-        if (MODE == kIn) {
-          const int j = (int)(gr / bb), p = (int)(gr - (long)j * bb);
-          const int n = __ldg(a.idx + 3 * j), by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-          const int y = g.oy + by * g.sy + p / b, x = g.ox + bx * g.sx + p % b;
-          valid = y >= 0 && y < g.h && x >= 0 && x < g.w;
-          (void)n;
-          dp = a.dst + gr * N;
-        } else if (MODE == kMid) {
-          const int j = (int)(gr / bb), p = (int)(gr - (long)j * bb);
-          const int oy = p / b, ox = p % b;
-          store = oy < ob && ox < ob;
-          dp = a.dst + ((long)j * ob * ob + oy * ob + ox) * N;
-        } else {
-          const int j = (int)(gr / (ob * ob)), p = (int)(gr - (long)j * ob * ob);
-          const int oy = p / ob, ox = p % ob;
-          const int n = __ldg(a.idx + 3 * j), by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-          const int Y = by * g.obh + oy, X = bx * g.obw + ox;
-          store = Y < g.oh && X < g.ow;
-          dp = a.dst + (((long)n * g.oh + Y) * g.ow + X) * N;
-          xp = dp;  // the residual: out holds x's values (clone or in place)
-        }
-      }
+      idx_next(tile + gridDim.x);
+      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * N;
       tc::mbar_wait(&acc_full[buf], use & 1);
       tc::fence_after();
-      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * N;
-#pragma unroll 2
-      for (int c0 = 0; c0 < N; c0 += 16) {
+      if (ew == 0 && lane == 0) wtrace(a, kEvAcc, k);
+#pragma unroll
+      for (int e = 0; e < MYCH; ++e) {
+        const int c0 = 16 * (2 * e + half);
+        if (c0 >= N) break;  // warp-uniform
         float v[16];
         tc::tmem_ld16(acc + c0, v);
         if (!store) continue;
@@ -249,28 +367,32 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
         if (MODE == kOut) {
           const float* b3 = par;
           uint4 xr[2];
-          xr[0] = reinterpret_cast<const uint4*>(xp + c0)[0];
-          xr[1] = reinterpret_cast<const uint4*>(xp + c0)[1];
+          if (e < PG) {
+            xr[0] = res[2 * (e < PG ? e : 0)];
+            xr[1] = res[2 * (e < PG ? e : 0) + 1];
+          } else {
+            xr[0] = reinterpret_cast<const uint4*>(dp + c0)[0];
+            xr[1] = reinterpret_cast<const uint4*>(dp + c0)[1];
+          }
           const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(xr);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float2 xf = __bfloat1622float2(xh[e]);
-            const float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b3[c0 + 2 * e]));
-            const float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b3[c0 + 2 * e + 1]));
-            o[e] = tc::pack_bf16(__fadd_rn(xf.x, u0), __fadd_rn(xf.y, u1));
+          for (int q = 0; q < 8; q += 2) {
+            const float4 b4 = *reinterpret_cast<const float4*>(b3 + c0 + 2 * q);
+            const float2 x0 = __bfloat1622float2(xh[q]), x1 = __bfloat1622float2(xh[q + 1]);
+            o[q] = tc::pack_bf16(x0.x + (v[2 * q] + b4.x), x0.y + (v[2 * q + 1] + b4.y));
+            o[q + 1] = tc::pack_bf16(x1.x + (v[2 * q + 2] + b4.z), x1.y + (v[2 * q + 3] + b4.w));
           }
         } else {
-          // IN: +b1, bn2, relu, x valid      MID: +b2, bn3, relu
-          const float* bi = MODE == kIn ? par + 2 * K : par;
-          const float* sc = bi + N;
-          const float* sh = sc + N;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + bi[c0 + 2 * e]));
-            float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + bi[c0 + 2 * e + 1]));
-            u0 = fmaxf(__fadd_rn(__fmul_rn(u0, sc[c0 + 2 * e]), sh[c0 + 2 * e]), 0.f);
-            u1 = fmaxf(__fadd_rn(__fmul_rn(u1, sc[c0 + 2 * e + 1]), sh[c0 + 2 * e + 1]), 0.f);
-            o[e] = valid ? tc::pack_bf16(u0, u1) : 0u;
+          for (int q = 0; q < 8; q += 2) {
+            const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q);
+            const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q);
+            const float u0 = fmaxf(fmaf(v[2 * q], s4.x, t4.x), 0.f);
+            const float u1 = fmaxf(fmaf(v[2 * q + 1], s4.y, t4.y), 0.f);
+            const float u2 = fmaxf(fmaf(v[2 * q + 2], s4.z, t4.z), 0.f);
+            const float u3 = fmaxf(fmaf(v[2 * q + 3], s4.w, t4.w), 0.f);
+            o[q] = valid ? tc::pack_bf16(u0, u1) : 0u;
+            o[q + 1] = valid ? tc::pack_bf16(u2, u3) : 0u;
           }
         }
         uint4* op = reinterpret_cast<uint4*>(dp + c0);
@@ -279,18 +401,76 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
       }
       tc::fence_before();
       tc::mbar_arrive(&acc_empty[buf]);
+      if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
+      meta(tile + gridDim.x);
     }
-  } else if (warp == 8) {
-    // ------------------------------------------------ W producer
+  } else if (warp == kLWarp) {
+    // ------------------------------------------------ loader: A boxes (+ streamed weights)
     if (lane == 0) {
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int c = 0; c < Q::CHUNKS; ++c, ++it) {
-          const int s = it % Q::SW;
-          tc::mbar_wait(&w_empty[s], ((it / Q::SW) & 1) ^ 1);
-          tc::mbar_expect_tx(&w_full[s], Q::WCH);
-          tc::bulk_g2s(Wring + s * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[s]);
+      const int bb = b * b;
+      int c = 0, wit = 0;
+      // IN: the block-index triples of the NEXT tile's slabs are loaded one tile ahead
+      int nj[4], nn[4], nby[4], nbx[4];
+      auto idx_load = [&](int tile) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int sl = tile * a.G + i;
+          nj[i] = (i < a.G && sl < B * a.S) ? sl : -1;
+          if (nj[i] >= 0) {
+            const int j = sl / a.S;
+            nn[i] = __ldg(a.idx + 3 * j);
+            nby[i] = __ldg(a.idx + 3 * j + 1);
+            nbx[i] = __ldg(a.idx + 3 * j + 2);
+          }
         }
+      };
+      if (MODE == kIn) idx_load(blockIdx.x);
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int cj[4], cn[4], cby[4], cbx[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          cj[i] = nj[i];
+          cn[i] = nn[i];
+          cby[i] = nby[i];
+          cbx[i] = nbx[i];
+        }
+        if (MODE == kIn) idx_load(tile + gridDim.x);
+        if (c % Q::NKC == 0) wtrace(a, kEvIss, c / Q::NKC);
+        for (int kc = 0; kc < Q::NKC; ++kc, ++c) {
+          const int s = c % Q::SA;
+          tc::mbar_wait(&a_empty[s], ((c / Q::SA) & 1) ^ 1);
+          uint8_t* A = Aring + s * Q::ACH;
+          uint64_t* bar = MODE == kIn ? &a_load[s] : &a_full[s];
+          if (MODE == kIn) {
+            int boxes = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) boxes += cj[i] >= 0;
+            tc::mbar_expect_tx(bar, (uint32_t)(boxes * Q::P * 16 * b * a.hb));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (cj[i] < 0) continue;
+              const int q = cj[i] - (cj[i] / a.S) * a.S;
+              const int x0 = g.ox + cbx[i] * g.sx, y0 = g.oy + cby[i] * g.sy + q * a.hb;
+              for (int k8 = 0; k8 < Q::P; ++k8)
+                tma_4d(A + k8 * Q::PA + i * a.slab_rows * 16, &a.tmap, kc * Q::KC + 8 * k8, x0, y0, cn[i], bar);
+            }
+          } else {
+            const int rows = MODE == kMid ? a.box_rows : 128;
+            tc::mbar_expect_tx(bar, (uint32_t)(Q::P * 16 * rows));
+            for (int k8 = 0; k8 < Q::P; ++k8)
+              tma_2d(A + k8 * Q::PA, &a.tmap, kc * Q::KC + 8 * k8, tile * 128, bar);
+          }
+          if (!Q::RES) {  // streamed weights: this chunk's taps
+            for (int tap = 0; tap < Q::TAPS; ++tap, ++wit) {
+              const int sw = wit % SWB;
+              tc::mbar_wait(&w_empty[sw], ((wit / SWB) & 1) ^ 1);
+              tc::mbar_expect_tx(&w_full[sw], Q::WCH);
+              tc::bulk_g2s(Wring + sw * Q::WCH, a.wpk + (size_t)(kc * Q::TAPS + tap) * Q::WCH, Q::WCH, &w_full[sw]);
+            }
+          }
+        }
+        (void)bb;
+      }
     }
     __syncwarp();
   } else {
@@ -298,23 +478,28 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, Q::NS);
       int ait = 0, wit = 0, k = 0;
+      if (Q::RES) tc::mbar_wait(&w_full[0], 0);
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
         const int buf = Q::NACC == 2 ? (k & 1) : 0;
         const int use = Q::NACC == 2 ? (k >> 1) : k;
         tc::mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc::fence_after();
+        wtrace(a, kEvMma, k);
         const uint32_t acc = tmem + buf * N;
         for (int kc = 0; kc < Q::NKC; ++kc, ++ait) {
           const int sa = ait % Q::SA;
           tc::mbar_wait(&a_full[sa], (ait / Q::SA) & 1);
           tc::fence_after();
+          if (MODE != kIn && kc == Q::NKC - 1) wtrace(a, kEvPub, k);
           const uint32_t abase = tc::smem_u32(Aring + sa * Q::ACH);
           for (int tap = 0; tap < Q::TAPS; ++tap, ++wit) {
-            const int sw = wit % Q::SW;
-            tc::mbar_wait(&w_full[sw], (wit / Q::SW) & 1);
-            tc::fence_after();
+            const int sw = Q::RES ? 0 : wit % SWB;
+            if (!Q::RES) {
+              tc::mbar_wait(&w_full[sw], (wit / SWB) & 1);
+              tc::fence_after();
+            }
             const int shift = MODE == kMid ? (tap / 3) * b + (tap % 3) : 0;
-            const uint32_t wbase = tc::smem_u32(Wring + sw * Q::WCH);
+            const uint32_t wbase = tc::smem_u32(Wring + (Q::RES ? (kc * Q::TAPS + tap) * Q::WCH : sw * Q::WCH));
 #pragma unroll
             for (int kk = 0; kk < Q::KC / 16; ++kk)
 #pragma unroll
@@ -323,7 +508,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
                              tc::desc_kmajor_noswz(abase + 2 * kk * Q::PA + shift * 16, Q::PA, 128),
                              tc::desc_kmajor_noswz(wbase + 2 * kk * Q::PW + h * Q::NS * 16, Q::PW, 128),
                              idesc, (kc | tap | kk) > 0);
-            tc::mma_commit(&w_empty[sw]);
+            if (!Q::RES) tc::mma_commit(&w_empty[sw]);
           }
           tc::mma_commit(&a_empty[sa]);
         }
@@ -332,6 +517,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
     }
     __syncwarp();
   }
+  if (Q::RES && tid == kLWarp * 32) tc::mbar_wait(&w_full[0], 0);  // no copy in flight at exit
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -342,7 +528,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(WArgs a) {
 // A chunk c of a GEMM with K-chunk KC, N columns: KC/8 planes of N rows x 16 B,
 // element (n, k) at (k/8)*N*16 + n*16 + (k%8)*2 — the kernel's B-operand layout.  MID
 // chunks are ordered (kc, tap).
-//   params (floats): IN  s1 t1 [c] b1 s2 t2 [m]   MID b2 s3 t3 [m]   OUT b3 [c]
+//   params (floats): IN  s1 t1 [c] b1 s2 t2' [m]   MID b2 s3 t3' [m]   OUT b3 [c]
+//   (t2' = b1*s2 + t2, t3' = b2*s3 + t3: the conv bias folded into the next BN)
 struct WLayout {
   size_t w1, w2, w3, p1, p2, p3, total;
 };
@@ -402,24 +589,24 @@ __global__ void unit_wide_pack_kernel(sbn_unit_params p, uint8_t* __restrict__ i
     p1[C + i] = ((const float*)p.bn1_shift)[i];
     p3[i] = bf(p.b3, i);
   }
-  for (int i = t0; i < M; i += stride) {
+  for (int i = t0; i < M; i += stride) {  // conv bias folded into the following BN shift
+    const float s2 = ((const float*)p.bn2_scale)[i], s3 = ((const float*)p.bn3_scale)[i];
     p1[2 * C + i] = bf(p.b1, i);
-    p1[2 * C + M + i] = ((const float*)p.bn2_scale)[i];
-    p1[2 * C + 2 * M + i] = ((const float*)p.bn2_shift)[i];
+    p1[2 * C + M + i] = s2;
+    p1[2 * C + 2 * M + i] = fmaf(bf(p.b1, i), s2, ((const float*)p.bn2_shift)[i]);
     p2[i] = bf(p.b2, i);
-    p2[M + i] = ((const float*)p.bn3_scale)[i];
-    p2[2 * M + i] = ((const float*)p.bn3_shift)[i];
+    p2[M + i] = s3;
+    p2[2 * M + i] = fmaf(bf(p.b2, i), s3, ((const float*)p.bn3_shift)[i]);
   }
 }
 
 template <int K, int N, int MODE>
-int launch_wide(const WArgs& a, long max_rows, cudaStream_t s, const char* what) {
+int launch_wide(const WArgs& a, long max_tiles, cudaStream_t s, const char* what) {
   using Q = WCfg<K, N, MODE>;
   auto kern = unit_wide_kernel<K, N, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
-  const long tiles = (max_rows + 127) / 128;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(tiles < sm_count() ? (tiles < 1 ? 1 : tiles) : sm_count()));
+  cfg.gridDim = dim3((unsigned)(max_tiles < sm_count() ? (max_tiles < 1 ? 1 : max_tiles) : sm_count()));
   cfg.blockDim = dim3(kWideThreads);
   cfg.dynamicSmemBytes = Q::SMEM;
   cfg.stream = s;
@@ -432,36 +619,84 @@ int launch_wide(const WArgs& a, long max_rows, cudaStream_t s, const char* what)
   return launch_status(what);
 }
 
+// TMA descriptor over a bf16 tensor: dims/strides innermost first (strides in bytes, for
+// dims 1..rank-1), box in elements, no swizzle, out-of-bounds elements read as zero.
+int encode_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+               const uint32_t* box) {
+  uint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base),
+                                            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SBN_ERR_CUDA;
+  }
+  return SBN_OK;
+}
+
 template <int C, int M>
 int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const int32_t* idx,
              const int32_t* count, int cap, uint8_t* s1, uint8_t* s2, cudaStream_t s) {
   constexpr WLayout L = wide_layout<C, M>();
   const int b = g.bh;
   WArgs a;
+  memset(&a, 0, sizeof(a));
   a.g = g;
   a.idx = idx;
   a.count = count;
   a.cap = cap;
+  // IN slabs: hb window rows of one block per slab, G slabs per 128-row tile
+  a.hb = b * b <= 128 ? b : 128 / b;
+  a.S = (b + a.hb - 1) / a.hb;
+  a.slab_rows = (a.hb * b + 7) / 8 * 8;
+  a.G = 128 / a.slab_rows < 4 ? 128 / a.slab_rows : 4;
+  a.box_rows = (128 + 2 * b + 2 + 7) / 8 * 8;
+  // diagnostics: stamps of ONE of the three launches, selected by debug flag bits 3-4
+  const int tsel = (debug_flags() >> 3) & 3;
+  unsigned long long* tb = trace_buffer();
+  a.trace = tsel == 0 ? tb : nullptr;
+  const long rows1 = (long)cap * b * b, rows2 = (long)cap * (b - 2) * (b - 2);
   // IN: x windows -> S1
-  a.src = (const __nv_bfloat16*)x;
+  {
+    const uint64_t dims[4] = {(uint64_t)C, (uint64_t)g.w, (uint64_t)g.h, (uint64_t)g.n};
+    const uint64_t str[3] = {(uint64_t)C * 2, (uint64_t)g.w * C * 2, (uint64_t)g.h * g.w * C * 2};
+    const uint32_t box[4] = {8, (uint32_t)b, (uint32_t)a.hb, 1};
+    int st = encode_map(&a.tmap, x, 4, dims, str, box);
+    if (st) return st;
+  }
   a.dst = (__nv_bfloat16*)s1;
   a.wpk = img + L.w1;
   a.par = (const float*)(img + L.p1);
-  int st = launch_wide<C, M, kIn>(a, (long)cap * b * b, s, "residual_unit_wide_in");
+  int st = launch_wide<C, M, kIn>(a, ((long)cap * a.S + a.G - 1) / a.G, s, "residual_unit_wide_in");
   if (st) return st;
   // MID: S1 -> S2 (3x3 valid)
-  a.src = (const __nv_bfloat16*)s1;
+  {
+    const uint64_t dims[2] = {(uint64_t)M, (uint64_t)rows1};
+    const uint64_t str[1] = {(uint64_t)M * 2};
+    const uint32_t box[2] = {8, (uint32_t)a.box_rows};
+    st = encode_map(&a.tmap, s1, 2, dims, str, box);
+    if (st) return st;
+  }
   a.dst = (__nv_bfloat16*)s2;
   a.wpk = img + L.w2;
   a.par = (const float*)(img + L.p2);
-  st = launch_wide<M, M, kMid>(a, (long)cap * b * b, s, "residual_unit_wide_mid");
+  a.trace = tsel == 1 ? tb : nullptr;
+  st = launch_wide<M, M, kMid>(a, (rows1 + 127) / 128, s, "residual_unit_wide_mid");
   if (st) return st;
   // OUT: S2 -> out (+ residual), in place or into the clone
-  a.src = (const __nv_bfloat16*)s2;
+  {
+    const uint64_t dims[2] = {(uint64_t)M, (uint64_t)rows2};
+    const uint64_t str[1] = {(uint64_t)M * 2};
+    const uint32_t box[2] = {8, 128};
+    st = encode_map(&a.tmap, s2, 2, dims, str, box);
+    if (st) return st;
+  }
   a.dst = (__nv_bfloat16*)out;
   a.wpk = img + L.w3;
   a.par = (const float*)(img + L.p3);
-  return launch_wide<M, C, kOut>(a, (long)cap * (b - 2) * (b - 2), s, "residual_unit_wide_out");
+  a.trace = tsel == 2 ? tb : nullptr;
+  return launch_wide<M, C, kOut>(a, (rows2 + 127) / 128, s, "residual_unit_wide_out");
 }
 
 // (c, m) instantiations: BASELINE config-4 stages (m = c/2) and the small unit shapes

@@ -110,3 +110,18 @@ def test_wide_stage_chain(cuda_device):
     for u in stage.units:
         ref = torch.from_numpy(_oracle(ref, u, mk, (16, 16))).bfloat16()
     assert O.rel_err(_np(res.output), ref.float().numpy()) <= 2e-2
+
+
+@pytest.mark.parametrize("block", [3, 5, 6, 7, 9, 12, 16, 18])
+def test_wide_unit_block_sizes(cuda_device, block):
+    """Slab packing of the TMA-fed IN kernel (several small blocks per 128-row tile, or
+    a block split over several tiles) for every block size shape class."""
+    x, u, mk = _case(40 + block, 2, 37, 41, 64, 32, 0.35)
+    lib = _lib.load()
+    prev = lib.sbn_debug_set_flags(FORCE_WIDE)
+    try:
+        y = P.sparse_residual_unit(P.Tensor4D(x.cuda()), mk, u, (block, block))
+    finally:
+        lib.sbn_debug_set_flags(prev)
+    ref = _oracle(x, u, mk, (block, block))
+    assert O.rel_err(_np(y), ref) <= 2e-2
