@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl",
                     help="process-group backend (nccl; gloo only to smoke-test the multi-rank "
                          "plumbing with several ranks sharing one GPU)")
+    ap.add_argument("--no-backbone", action="store_true", help="skip the config-4/5 backbone legs")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -324,6 +325,29 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # ---- config 5: N=64 frames of the config-4 backbone, batch-sharded 64/world per rank,
+    #      no collective on the hot path; time = max over ranks (CUDA events)
+    config5 = None
+    if not args.no_backbone and 64 % world == 0:
+        per = 64 // world
+        leg = run_backbone_leg(P, torch, dev, time_graph, per, 0.2, reps=3, per_stage=False,
+                               first_seed=rank * per, dense=(world == 1))
+        t5 = leg["sparse_ms"]
+        if world > 1:
+            tt = torch.tensor([t5], device=cdev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t5 = float(tt.item())
+        config5 = {"workload": "config5: 64 frames of the config-4 backbone (800x700x32 bf16, 20% blob masks, "
+                               "seeds 0..63), batch-sharded 64/world per GPU, no collective",
+                   "frames_total": 64, "frames_per_rank": per, "ms_max_over_ranks": round(t5, 4),
+                   "frames_per_s": round(64 / (t5 * 1e-3), 1), "scaling": "strong",
+                   "rank0": leg}
+
+    # ---- config 4: the backbone on N=8 frames, per-stage breakdown, vs the dense backbone
+    backbone = None
+    if not args.no_backbone and rank == 0:
+        backbone = run_backbone_leg(P, torch, dev, time_graph, 8, 0.2)
+
     # ---- density sweep (sparse vs dense, same protocol, fewer steps)
     sweep = None
     if not args.no_sweep and rank == 0:
@@ -404,6 +428,8 @@ def run_ours(args):
             "conv_sweep": conv_sweep,
             "gather_scatter": gs,
             "batched": batched,
+            "backbone": backbone,
+            "config5": config5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -440,7 +466,8 @@ def run_batched(P, torch, dev, time_graph, u, hbm_peak, unit_fn):
     return out
 
 
-def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, per_stage=True):
+def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, per_stage=True,
+                     first_seed=0, dense=True):
     """BASELINE config 4 (config 5 per-GPU shard when frames = 64/G): the 4-stage sparse
     detector backbone (perf.DETECTOR_STAGES: [3, 6, 6, 3] bottleneck units, 96/192/256/384
     channels, dense stride-2 cuDNN projections) on `frames` 800x700 BEV frames with seeded
@@ -452,11 +479,12 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
     hh, ww, cin = perf.DETECTOR_INPUT
     bb = P.build_backbone(perf.detector_stage_configs(), np.random.default_rng(4))
     x = torch.randn(frames, hh, ww, cin, device=dev).bfloat16()
-    mk = np.concatenate([P.synth_mask_blobs((1, hh, ww), 1.0 - density, s).numpy() for s in range(frames)])
+    mk = np.concatenate([P.synth_mask_blobs((1, hh, ww), 1.0 - density, first_seed + s).numpy()
+                         for s in range(frames)])
     mask = P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False)
     xt = P.Tensor4D(x)
     res = P.run_backbone(bb, xt, mask)  # warm: weight images, scratch buffers
-    dres = P.run_backbone(bb, xt, mask, sparse=False)
+    dres = P.run_backbone(bb, xt, mask, sparse=False) if dense else None
     torch.cuda.synchronize()
 
     def timed(fn, n=reps):
@@ -477,21 +505,27 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
     def de(k):
         for _ in range(k):
             P.run_backbone(bb, xt, mask, sparse=False)
-    t_sp, t_de = timed(sp), timed(de)
-    f_sp, f_de = perf.flops_backbone(res, bb.stages, True), perf.flops_backbone(dres, bb.stages, False)
+    t_sp = timed(sp)
+    f_sp = perf.flops_backbone(res, bb.stages, True)
     out = {"workload": f"config4: 4-stage sparse detector backbone, N={frames} x {hh}x{ww}x{cin} bf16, "
-                       f"{density:.0%} blob masks (seeds 0..{frames - 1})",
-           "frames": frames, "sparse_ms": round(t_sp, 4), "dense_ms": round(t_de, 4),
-           "frames_per_s": round(frames / (t_sp * 1e-3), 1), "frames_per_s_dense": round(frames / (t_de * 1e-3), 1),
-           "speedup_vs_dense": round(t_de / t_sp, 3),
+                       f"{density:.0%} blob masks (seeds {first_seed}..{first_seed + frames - 1})",
+           "frames": frames, "sparse_ms": round(t_sp, 4),
+           "frames_per_s": round(frames / (t_sp * 1e-3), 1),
            "tflops_alg_sparse": round(f_sp / (t_sp * 1e-3) / 1e12, 1),
-           "tflops_alg_dense": round(f_de / (t_de * 1e-3) / 1e12, 1), "stages": []}
+           "density_achieved": round(float(mk.mean()), 4), "stages": []}
+    if dense:
+        t_de = timed(de)
+        f_de = perf.flops_backbone(dres, bb.stages, False)
+        out.update({"dense_ms": round(t_de, 4), "frames_per_s_dense": round(frames / (t_de * 1e-3), 1),
+                    "speedup_vs_dense": round(t_de / t_sp, 3),
+                    "tflops_alg_dense": round(f_de / (t_de * 1e-3) / 1e12, 1)})
     if per_stage:
         inp = xt
         for i, (stg, r) in enumerate(zip(bb.stages, res)):
             m_i = stg.config.channels[1]
             t1 = timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask) for _ in range(k)])
-            t2 = timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False) for _ in range(k)])
+            t2 = (timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False) for _ in range(k)])
+                  if dense else float("nan"))
             n_, h_, w_, c_ = r.output.dims
             out["stages"].append({"stage": i + 2, "hw": [h_, w_], "c": c_, "m": m_i,
                                   "block": stg.config.block_size[0], "units": stg.config.unit_count,
