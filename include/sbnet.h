@@ -108,6 +108,16 @@ int sbn_scatter(const void* blocks, int dtype, int c, const sbn_geometry* g, con
                 const int32_t* count, int cap, int add, int transpose, void* dst,
                 sbn_stream_t stream);
 
+/* Copy each active block's region between two frames of identical shape at the same
+ * coordinates: region 0 = the input window clipped to the image, region 1 = the clipped
+ * output window.  Either pointer may be pinned host memory (UVA): this moves exactly the
+ * bytes a sparse layer reads / writes between a host-resident frame and its device
+ * staging copy (the host-frame path of sparse_residual_unit).  No reference counterpart:
+ * the reference operates on host arrays in place of this transfer. */
+int sbn_copy_block_regions(const void* src, void* dst, int dtype, int c, const sbn_geometry* g,
+                           const int32_t* idx, const int32_t* count, int cap, int region,
+                           sbn_stream_t stream);
+
 /* Fused sparse_conv2d body (`layers.py:27-47` after reduce_mask): gather -> valid
  * conv (kh, kw, stride sh, sw) -> (+bias) -> scatter into dst (n, oh, ow, cout), all in
  * one kernel; the block stack never touches HBM.  w: HWIO; bias nullable.

@@ -53,6 +53,7 @@ _PROTOS = {
     "sbn_gather": (_I, [_P, _I, _I, _G, _P, _P, _I, _I, _P, _P]),
     "sbn_in_bounds": (_I, [_G, _P, _P, _I, _P, _P]),
     "sbn_scatter": (_I, [_P, _I, _I, _G, _P, _P, _I, _I, _I, _P, _P]),
+    "sbn_copy_block_regions": (_I, [_P, _P, _I, _I, _G, _P, _P, _I, _I, _P]),
     "sbn_sparse_conv": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _G, _P, _P, _P, _P, _P, _I, _P, _P,
                              C.c_size_t, _I, _P]),
     "sbn_sparse_conv_packed_bytes": (C.c_size_t, [_I, _I, _I, _I, _I, _I, _I, _G]),

@@ -56,6 +56,38 @@ gather_rows_kernel(const uint8_t* __restrict__ x, Geo g, int pix_bytes,
   }
 }
 
+// Frame-to-frame copy of each active block's region at identical coordinates: region 0 =
+// the input window clipped to the image, region 1 = the clipped output (write) window.
+// Used to move only the bytes a sparse layer touches between a host-resident frame
+// (pinned, UVA) and its device staging copy; warp per region row, 16-B vectors.
+template <int VS>
+__global__ void __launch_bounds__(kThreads)
+copy_regions_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, Geo g, int pix_bytes,
+                    const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int cap, int region) {
+  using V = typename VecT<VS>::type;
+  const int B = ld_count(count, cap);
+  const int lane = threadIdx.x & 31;
+  const long nwarps = (long)gridDim.x * (kThreads / 32);
+  const int rh = region == 0 ? g.bh : g.obh;
+  const int fh = region == 0 ? g.h : g.oh, fw = region == 0 ? g.w : g.ow;
+  for (long r = blockIdx.x * (long)(kThreads / 32) + (threadIdx.x >> 5); r < (long)B * rh; r += nwarps) {
+    const int b = (int)(r / rh), ry = (int)(r - (long)b * rh);
+    const int n = __ldg(idx + 3 * b), by = __ldg(idx + 3 * b + 1), bx = __ldg(idx + 3 * b + 2);
+    const int y = region == 0 ? g.oy + by * g.sy + ry : by * g.obh + ry;
+    if (y < 0 || y >= fh) continue;
+    int x0 = region == 0 ? g.ox + bx * g.sx : bx * g.obw;
+    int x1 = x0 + (region == 0 ? g.bw : g.obw);
+    x0 = max(x0, 0);
+    x1 = min(x1, fw);
+    if (x1 <= x0) continue;
+    const size_t off = (((size_t)n * fh + y) * fw + x0) * pix_bytes;
+    const V* s = reinterpret_cast<const V*>(src + off);
+    V* d = reinterpret_cast<V*>(dst + off);
+    const int nvec = (x1 - x0) * pix_bytes / VS;
+    for (int k = lane; k < nvec; k += 32) d[k] = s[k];
+  }
+}
+
 template <typename E>
 __global__ void __launch_bounds__(kThreads)
 gather_transpose_kernel(const E* __restrict__ x, Geo g, int c, const int32_t* __restrict__ idx,
@@ -276,4 +308,29 @@ extern "C" int sbn_scatter(const void* blk, int dtype, int c, const sbn_geometry
     default: launch_scatter<2, uint8_t, false>(blk, g, pix, idx, count, cap, dst, s); break;
   }
   return launch_status("scatter");
+}
+
+extern "C" int sbn_copy_block_regions(const void* src, void* dst, int dtype, int c, const sbn_geometry* gp,
+                                      const int32_t* idx, const int32_t* count, int cap, int region,
+                                      sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  const int es = dtype_size(dtype);
+  SBN_CHECK_ARG(es > 0, SBN_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
+  SBN_CHECK_ARG(c > 0, SBN_ERR_SHAPE, "channels must be > 0");
+  SBN_CHECK_ARG(region == 0 || region == 1, SBN_ERR_INVALID, "region must be 0 (window) or 1 (output)");
+  if (cap <= 0) return SBN_OK;
+  SBN_CHECK_ARG(src && dst && idx && count, SBN_ERR_INVALID, "null pointer argument");
+  Geo g = to_geo(gp);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int pix = c * es;
+  const long rows = (long)cap * (region == 0 ? g.bh : g.obh);
+  const unsigned grid = (unsigned)grid_for(rows * 32, kThreads);
+  switch (pick_vec(pix, src, dst)) {
+    case 16: copy_regions_kernel<16><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;
+    case 8: copy_regions_kernel<8><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;
+    case 4: copy_regions_kernel<4><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;
+    default: copy_regions_kernel<2><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;
+  }
+  return launch_status("copy_block_regions");
 }

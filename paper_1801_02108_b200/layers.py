@@ -60,6 +60,16 @@ class _Scratch(threading.local):
             self.bufs[key] = b
         return b
 
+    def frame(self, shape, dtype, device) -> torch.Tensor:
+        """Device staging frame of the host-frame unit path, cached per (device, stream,
+        shape, dtype); its content outside the copied regions is never read."""
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream, "frame", tuple(shape), dtype)
+        b = self.bufs.get(key)
+        if b is None:
+            b = torch.empty(shape, dtype=dtype, device=device)
+            self.bufs[key] = b
+        return b
+
 
 _SCRATCH = _Scratch()
 
@@ -293,7 +303,7 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
                          block_size: tuple[int, int], halo: int = 1,
                          bn_mode: BnMode = BnMode.INFERENCE,
                          _shared: tuple[BlockSpec, BlockIndexList] | None = None,
-                         inplace: bool = False, algo="auto") -> Tensor4D:
+                         inplace: bool = False, algo="auto", blocking: bool = True) -> Tensor4D:
     """Residual unit inside one gather/scatter pair (reference `layers.py:203-229`);
     inactive pixels stay bit-identical to x.
 
@@ -301,11 +311,20 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
     scatter-adds into the clone).  ``inplace=True`` updates x's storage directly — the
     paper's fused scatter-add; the kernel snapshots the halo rims first, so neighbours'
     writes never leak into a window.
+
+    ``inplace=True`` on a PINNED HOST frame updates the host frame: only the active
+    blocks' input windows travel host->device and only their output windows travel back
+    (`_host_frame_unit`).  With ``blocking=False`` that update is asynchronous on the
+    current stream (synchronise before reading the frame), like ``copy_(non_blocking=True)``.
     """
     if u.channels != x.dims[3]:
         raise ShapeMismatchError(f"unit channels {u.channels} != input channels {x.dims[3]}")
     if bn_mode is not BnMode.INFERENCE:
         raise UnsupportedConfigError("sparse_residual_unit: inference-mode BN only (training is out of scope)")
+    if inplace and _shared is None and not x.nhwc().is_cuda and x.nhwc().is_pinned():
+        _check_mask(x, mask)
+        _host_frame_unit(x.nhwc(), mask, u, block_size, halo, algo, blocking)
+        return x
     xt = cuda(x.nhwc())
     if inplace and x.nhwc().is_cuda and xt.data_ptr() == x.nhwc().data_ptr():
         out = xt
@@ -319,6 +338,34 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
         spec, idx = _shared
         residual_unit_into(out, out if (out is xt) else xt, u, spec, idx, halo, algo)
     return Tensor4D.from_nhwc(out, x.layout)
+
+
+def _host_frame_unit(xh: torch.Tensor, mask: BinaryMask, u: ResidualUnitParams, block_size,
+                     halo: int, algo, blocking: bool) -> None:
+    """In-place unit on a pinned host frame (UVA): mask -> device, ordered reduce_mask,
+    the active blocks' input windows host -> device staging frame (sbn_copy_block_regions
+    reads host memory over PCIe), the fused unit in place on the staging frame, and the
+    active output windows device -> host frame.  PCIe carries the mask plus exactly the
+    bytes the sparse layer reads and writes, instead of two full frames."""
+    if not xh.is_contiguous():
+        raise ShapeMismatchError("host-frame unit needs a contiguous pinned NHWC frame")
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n, _, _, c = xh.shape
+    spec = unit_spec(tuple(xh.shape), block_size, halo)
+    stage = _SCRATCH.frame(xh.shape, xh.dtype, dev)
+    md = cuda(mask.data, dev)
+    idx = reduce_mask(BinaryMask(md, validate=False), spec)
+    g = spec.c_geometry(n)
+    dt = dtype_code(xh.dtype)
+    sh = _lib.stream_handle(dev)
+    _lib.check(lib.sbn_copy_block_regions(xh.data_ptr(), stage.data_ptr(), dt, c, C.byref(g), idx.rows.data_ptr(),
+                                          idx.count_dev.data_ptr(), idx.capacity, 0, sh), "copy_block_regions")
+    residual_unit_into(stage, stage, u, spec, idx, halo, algo)
+    _lib.check(lib.sbn_copy_block_regions(stage.data_ptr(), xh.data_ptr(), dt, c, C.byref(g), idx.rows.data_ptr(),
+                                          idx.count_dev.data_ptr(), idx.capacity, 1, sh), "copy_block_regions")
+    if blocking:
+        torch.cuda.current_stream(dev).synchronize()
 
 
 def sparse_residual_unit_into(out: torch.Tensor, src: torch.Tensor, mask: torch.Tensor,

@@ -485,3 +485,21 @@ def test_sparse_conv_double_buffered_bit_identical(cuda_device, cin, block, dens
         finally:
             lib.sbn_debug_set_flags(old)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("c,m,block", [(64, 32, 16), (96, 48, 16), (64, 32, 8)])
+def test_residual_unit_host_frame_inplace_bit_identical(cuda_device, c, m, block):
+    """inplace=True on a pinned HOST frame (only the active windows cross PCIe) gives the
+    device path's result bit for bit, in the caller's host buffer."""
+    x, u, mk = _bf16_unit_case(3, 200, 184, c, m, 0.2, (block, block))
+    dev_out = P.sparse_residual_unit(P.Tensor4D(x.cuda()), mk, u, (block, block)).data.cpu()
+    hx = x.clone().pin_memory()
+    hm = P.BinaryMask(mk.data.cpu().pin_memory(), validate=False)
+    r = P.sparse_residual_unit(P.Tensor4D(hx), hm, u, (block, block), inplace=True)
+    assert r.data.data_ptr() == hx.data_ptr()
+    assert torch.equal(hx, dev_out)
+    # asynchronous form: same result after a stream sync
+    hx2 = x.clone().pin_memory()
+    P.sparse_residual_unit(P.Tensor4D(hx2), hm, u, (block, block), inplace=True, blocking=False)
+    torch.cuda.synchronize()
+    assert torch.equal(hx2, dev_out)
