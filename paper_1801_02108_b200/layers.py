@@ -340,6 +340,52 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
     return Tensor4D.from_nhwc(out, x.layout)
 
 
+class _HostFramePlan:
+    """Everything the host-frame unit call needs, resolved once per (unit parameters,
+    frame shape, dtype, block size, halo, algo, stream): the device staging frame, a
+    device mask buffer, the index list, workspaces, the packed weight image and the
+    geometry struct.  Per call only the mask copy and four C-ABI calls remain."""
+
+    def __init__(self, u: ResidualUnitParams, shape, dtype, block_size, halo, algo, dev, stream):
+        lib = _lib.load()
+        n, h, w, c = shape
+        self.lib = lib
+        self.spec = unit_spec(tuple(shape), block_size, halo)
+        self.g = self.spec.c_geometry(n)
+        self.c, self.m, self.halo, self.pre = c, u.mid_channels, halo, int(u.pre_activation)
+        self.dt = dtype_code(dtype)
+        self.algo = _algo(algo)
+        self.stage = torch.empty(shape, dtype=dtype, device=dev)
+        self.md = torch.empty((n, h, w), dtype=torch.uint8, device=dev)
+        self.cap = max(1, n * self.spec.grid_count[0] * self.spec.grid_count[1])
+        self.rows = torch.empty((self.cap, 3), dtype=torch.int32, device=dev)
+        self.count = torch.empty((1,), dtype=torch.int32, device=dev)
+        gb = C.byref(self.g)
+        self.rmws = torch.zeros(max(int(lib.sbn_reduce_mask_workspace(gb)), 4096), dtype=torch.uint8, device=dev)
+        nb = lib.sbn_residual_unit_workspace(self.dt, c, self.m, gb, halo, self.algo)
+        self.ws = torch.zeros(max(int(nb), 1 << 16), dtype=torch.uint8, device=dev)  # barrier words start at 0
+        self.up = u.c_params(dtype, dev, self.g if self.algo != _lib.SBN_ALGO_SIMT else None, halo)
+        self.thr = 1.0 / (self.spec.block_size[0] * self.spec.block_size[1])
+        self.sh = stream.cuda_stream
+
+    def run(self, xh: torch.Tensor, mask_data: torch.Tensor) -> None:
+        lib, gb, sh = self.lib, C.byref(self.g), self.sh
+        self.md.copy_(mask_data, non_blocking=True)
+        _lib.check(lib.sbn_reduce_mask(self.md.data_ptr(), gb, _lib.SBN_POOL_MAX, self.thr, self.rows.data_ptr(),
+                                       self.count.data_ptr(), self.rmws.data_ptr(), self.rmws.numel(), sh),
+                   "reduce_mask")
+        _lib.check(lib.sbn_copy_block_regions(xh.data_ptr(), self.stage.data_ptr(), self.dt, self.c, gb,
+                                              self.rows.data_ptr(), self.count.data_ptr(), self.cap, 0, sh),
+                   "copy_block_regions")
+        _lib.check(lib.sbn_residual_unit(self.stage.data_ptr(), self.dt, self.c, self.m, gb, self.halo, self.pre,
+                                         C.byref(self.up), self.rows.data_ptr(), self.count.data_ptr(), self.cap,
+                                         self.stage.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self.algo, sh),
+                   "sparse_residual_unit")
+        _lib.check(lib.sbn_copy_block_regions(self.stage.data_ptr(), xh.data_ptr(), self.dt, self.c, gb,
+                                              self.rows.data_ptr(), self.count.data_ptr(), self.cap, 1, sh),
+                   "copy_block_regions")
+
+
 def _host_frame_unit(xh: torch.Tensor, mask: BinaryMask, u: ResidualUnitParams, block_size,
                      halo: int, algo, blocking: bool) -> None:
     """In-place unit on a pinned host frame (UVA): mask -> device, ordered reduce_mask,
@@ -349,23 +395,16 @@ def _host_frame_unit(xh: torch.Tensor, mask: BinaryMask, u: ResidualUnitParams, 
     bytes the sparse layer reads and writes, instead of two full frames."""
     if not xh.is_contiguous():
         raise ShapeMismatchError("host-frame unit needs a contiguous pinned NHWC frame")
-    lib = _lib.load()
     dev = torch.device("cuda", torch.cuda.current_device())
-    n, _, _, c = xh.shape
-    spec = unit_spec(tuple(xh.shape), block_size, halo)
-    stage = _SCRATCH.frame(xh.shape, xh.dtype, dev)
-    md = cuda(mask.data, dev)
-    idx = reduce_mask(BinaryMask(md, validate=False), spec)
-    g = spec.c_geometry(n)
-    dt = dtype_code(xh.dtype)
-    sh = _lib.stream_handle(dev)
-    _lib.check(lib.sbn_copy_block_regions(xh.data_ptr(), stage.data_ptr(), dt, c, C.byref(g), idx.rows.data_ptr(),
-                                          idx.count_dev.data_ptr(), idx.capacity, 0, sh), "copy_block_regions")
-    residual_unit_into(stage, stage, u, spec, idx, halo, algo)
-    _lib.check(lib.sbn_copy_block_regions(stage.data_ptr(), xh.data_ptr(), dt, c, C.byref(g), idx.rows.data_ptr(),
-                                          idx.count_dev.data_ptr(), idx.capacity, 1, sh), "copy_block_regions")
+    stream = torch.cuda.current_stream(dev)
+    key = ("host", tuple(xh.shape), xh.dtype, tuple(block_size), halo, str(algo), str(dev), stream.cuda_stream)
+    plan = u._cache.get(key)
+    if plan is None:
+        plan = _HostFramePlan(u, xh.shape, xh.dtype, block_size, halo, algo, dev, stream)
+        u._cache[key] = plan
+    plan.run(xh, mask.data)
     if blocking:
-        torch.cuda.current_stream(dev).synchronize()
+        stream.synchronize()
 
 
 def sparse_residual_unit_into(out: torch.Tensor, src: torch.Tensor, mask: torch.Tensor,
