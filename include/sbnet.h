@@ -108,6 +108,17 @@ int sbn_scatter(const void* blocks, int dtype, int c, const sbn_geometry* g, con
                 const int32_t* count, int cap, int add, int transpose, void* dst,
                 sbn_stream_t stream);
 
+/* gather_grad (`blocks.py:162-188`): adjoint of gather.  dx (n, h, w, c) is fully written:
+ * each element is the sum of the covering active blocks' values of gblk (cap, bh, bw, c)
+ * in ascending block order starting from zero (the reference's `+=` sequence: bit-exact
+ * for F32/F64; BF16 accumulates in fp32).  ws: sbn_gather_grad_workspace bytes (block
+ * table), scratch.  scatter_grad (`blocks.py:191-204`) needs no entry of its own: it is
+ * sbn_gather over the output grid (h, w = out size, block = stride = out block, origin 0). */
+size_t sbn_gather_grad_workspace(const sbn_geometry* g);
+int sbn_gather_grad(const void* gblk, int dtype, int c, const sbn_geometry* g, const int32_t* idx,
+                    const int32_t* count, int cap, void* dx, void* ws, size_t ws_bytes,
+                    sbn_stream_t stream);
+
 /* Copy each active block's region between two frames of identical shape at the same
  * coordinates: region 0 = the input window clipped to the image, region 1 = the clipped
  * output window.  Either pointer may be pinned host memory (UVA): this moves exactly the

@@ -260,11 +260,90 @@ def gen_config1(bc):
                         idx=idx.entries, y=y.data, chosen=chosen)
 
 
+def gen_grads(bc):
+    """Training path: gather_grad / scatter_grad (`blocks.py:162-204`),
+    sparse_conv2d_grads (`layers.py:50-65`), sparse_residual_unit_grads (`layers.py:232-270`),
+    TRAIN_STATS sparse_batch_norm (`layers.py:68-82`)."""
+    rng = np.random.default_rng(6000)
+    out = {}
+    for i in range(20):  # gather_grad / scatter_grad
+        n, h, w, c, co, k, s, same, b = _conv_case(rng)
+        pad = bc.Padding.SAME if same else bc.Padding.VALID
+        dims = (n, h, w, c)
+        spec = bc.compute_block_spec(dims, bc.ConvParams(k, s, pad, co), b)
+        m = _mask(rng, n, h, w, KINDS[i % len(KINDS)])
+        idx = bc.reduce_mask(bc.BinaryMask(m), spec)
+        dt = np.float64 if i % 3 == 2 else np.float32
+        g = bc.gather(bc.Tensor4D(np.zeros(dims, dt)), idx, spec)
+        gblk = rng.standard_normal((idx.count, *spec.block_size, c)).astype(dt)
+        gg = bc.gather_grad(g.with_tensor(bc.Tensor4D(gblk)), spec, dims)
+        gout = rng.standard_normal((n, *spec.out_size, c)).astype(dt)
+        sg = bc.scatter_grad(bc.Tensor4D(gout), idx, spec)
+        out[f"g{i}_cfg"] = np.asarray([h, w, *k, *s, int(same), *b, n, c], np.int64)
+        out[f"g{i}_mask"], out[f"g{i}_idx"] = m, idx.entries
+        out[f"g{i}_gblk"], out[f"g{i}_gather_grad"] = gblk, gg.data
+        out[f"g{i}_gout"], out[f"g{i}_scatter_grad"] = gout, sg.tensor.data
+    for i in range(12):  # sparse_conv2d_grads
+        n, h, w, c, co, k, s, same, b = _conv_case(rng)
+        h, w = min(h, 24), min(w, 24)
+        b = (max(min(b[0], h + 4), k[0]), max(min(b[1], w + 4), k[1]))
+        b = (k[0] + s[0] * ((b[0] - k[0]) // s[0]), k[1] + s[1] * ((b[1] - k[1]) // s[1]))
+        pad = bc.Padding.SAME if same else bc.Padding.VALID
+        p = bc.ConvParams(k, s, pad, co)
+        m = _mask(rng, n, h, w, KINDS[i % len(KINDS)])
+        dt = np.float64 if i % 2 else np.float32
+        x = rng.standard_normal((n, h, w, c)).astype(dt)
+        wt = rng.standard_normal((*k, c, co)).astype(dt)
+        bias = rng.standard_normal(co).astype(dt)
+        gout = rng.standard_normal((n, *p.out_size(h, w), co)).astype(dt)
+        dx, dw, db = bc.sparse_conv2d_grads(bc.Tensor4D(x), bc.BinaryMask(m), bc.FilterBank(wt, bias), p, b,
+                                            bc.Tensor4D(gout))
+        out[f"v{i}_cfg"] = np.asarray([h, w, *k, *s, int(same), *b, n, c, co], np.int64)
+        out[f"v{i}_x"], out[f"v{i}_mask"], out[f"v{i}_w"], out[f"v{i}_b"] = x, m, wt, bias
+        out[f"v{i}_gout"], out[f"v{i}_dx"], out[f"v{i}_dw"], out[f"v{i}_db"] = gout, dx.data, dw, db
+    for i in range(10):  # sparse_residual_unit_grads (pre-activation)
+        n = int(rng.integers(1, 3))
+        c = int(rng.integers(2, 7))
+        m_ = int(rng.integers(2, 7))
+        h = int(rng.integers(8, 30))
+        w = int(rng.integers(8, 30))
+        halo = [1, 1, 2][i % 3]
+        bs = int(rng.integers(2 * halo + 2, 13))
+        mk = _mask(rng, n, h, w, KINDS[i % len(KINDS)])
+        dt = np.float64 if i % 2 else np.float32
+        x = rng.standard_normal((n, h, w, c)).astype(dt)
+        u = bc.random_unit_params(rng, c, m_, dt)
+        gout = rng.standard_normal((n, h, w, c)).astype(dt)
+        dx, dws = bc.sparse_residual_unit_grads(bc.Tensor4D(x), bc.BinaryMask(mk), u, (bs, bs),
+                                                bc.Tensor4D(gout), halo=halo)
+        out[f"u{i}_cfg"] = np.asarray([n, h, w, c, m_, bs, halo, 1], np.int64)
+        out[f"u{i}_x"], out[f"u{i}_mask"], out[f"u{i}_gout"], out[f"u{i}_dx"] = x, mk, gout, dx.data
+        for nm in ("conv1", "conv2", "conv3"):
+            out[f"u{i}_d{nm}_w"], out[f"u{i}_d{nm}_b"] = dws[nm]
+        for key, val in _unit_arrays(u).items():
+            out[f"u{i}_{key}"] = val
+    for i in range(4):  # TRAIN_STATS sparse batch norm over gathered blocks
+        n, h, w, c = 1, int(rng.integers(10, 30)), int(rng.integers(10, 30)), int(rng.integers(1, 6))
+        spec = bc.compute_block_spec((n, h, w, c), bc.ConvParams((3, 3), (1, 1), bc.Padding.SAME, c), (6, 6))
+        m = _mask(rng, n, h, w, "0.5")
+        idx = bc.reduce_mask(bc.BinaryMask(m), spec)
+        x = rng.standard_normal((n, h, w, c))
+        blocks = bc.gather(bc.Tensor4D(x), idx, spec)
+        gam, bet = rng.random(c) + 0.5, rng.standard_normal(c)
+        bn = bc.BnParams(gam, bet, np.zeros(c), np.ones(c))
+        if idx.count == 0:
+            continue
+        y, (mean, var) = bc.sparse_batch_norm(blocks, bn, bc.BnMode.TRAIN_STATS)
+        out[f"b{i}_stack"], out[f"b{i}_gamma"], out[f"b{i}_beta"] = blocks.tensor.data, gam, bet
+        out[f"b{i}_y"], out[f"b{i}_mean"], out[f"b{i}_var"] = y.tensor.data, mean, var
+    np.savez_compressed(os.path.join(OUT, "grads.npz"), **out)
+
+
 def main():
     bc = _ref()
     os.makedirs(OUT, exist_ok=True)
     for fn in (gen_geometry, gen_reduce_mask, gen_gather_scatter, gen_sparse_conv, gen_residual,
-               gen_masks, gen_units, gen_config1):
+               gen_masks, gen_units, gen_config1, gen_grads):
         fn(bc)
         print("wrote", fn.__name__)
 

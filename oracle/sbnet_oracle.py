@@ -31,6 +31,8 @@ __all__ = [
     "conv_nhwc", "bn_scale_shift", "bn_apply", "unit_branch", "sparse_conv2d",
     "dense_conv2d", "sparse_residual_unit", "dense_residual_unit", "unit_geometry",
     "rel_err", "active_region",
+    "gather_grad", "scatter_grad", "conv_nhwc_grads", "sparse_conv2d_grads",
+    "sparse_residual_unit_grads", "sparse_batch_norm_train",
 ]
 
 
@@ -330,6 +332,123 @@ def sparse_residual_unit(x, mask, u: dict, block, halo: int = 1, shared=None):
 def dense_residual_unit(x, u: dict):
     """Dense oracle of the unit, SAME 3x3 (reference ``layers.py:194-200``)."""
     return x + unit_branch(x, u, (1, 1), 0)
+
+
+# --------------------------------------------------------------------------- training path
+
+def gather_grad(gblk: np.ndarray, idx: np.ndarray, g: Geometry, dims) -> np.ndarray:
+    """Adjoint of gather: block gradients accumulated over their (overlapping) input
+    windows, clipped, in index order into zeros (reference ``blocks.py:162-188``)."""
+    out = np.zeros(dims, gblk.dtype)
+    for b, (i, by, bx) in enumerate(idx):
+        ys, xs, y0, x0, y1, x1 = _window(g, by, bx)
+        if y1 > y0 and x1 > x0:
+            out[i, y0:y1, x0:x1] += gblk[b, y0 - ys:y1 - ys, x0 - xs:x1 - xs]
+    return out
+
+
+def scatter_grad(gout: np.ndarray, idx: np.ndarray, g: Geometry) -> np.ndarray:
+    """Adjoint of scatter: the upstream gradient over each block's clipped write window,
+    zero outside the image (reference ``blocks.py:191-204``)."""
+    oh, ow = g.out_size
+    obh, obw = g.out_block
+    out = np.zeros((len(idx), obh, obw, gout.shape[3]), gout.dtype)
+    for b, (i, by, bx) in enumerate(idx):
+        y0, x0 = by * obh, bx * obw
+        y1, x1 = min(y0 + obh, oh), min(x0 + obw, ow)
+        out[b, :y1 - y0, :x1 - x0] = gout[i, y0:y1, x0:x1]
+    return out
+
+
+def conv_nhwc_grads(a: np.ndarray, wts: np.ndarray, stride, pad, gout: np.ndarray):
+    """(dx, dw, db) of ``conv_nhwc`` (reference ``ops.py:167-197``): per tap, dW is the
+    patch/gradient contraction and dx accumulates gradient @ W^T at the tap's strided
+    input positions."""
+    n, h, w, _ = a.shape
+    kh, kw, _, _ = wts.shape
+    oh, ow = gout.shape[1], gout.shape[2]
+    dx = np.zeros_like(a)
+    dw = np.zeros(wts.shape, a.dtype)
+    wt = wts.astype(a.dtype, copy=False)
+    for i in range(kh):
+        oy = np.arange(oh)
+        iy = oy * stride[0] + i - pad[0]
+        vy = (iy >= 0) & (iy < h)
+        if not vy.any():
+            continue
+        for j in range(kw):
+            ox = np.arange(ow)
+            ix = ox * stride[1] + j - pad[1]
+            vx = (ix >= 0) & (ix < w)
+            if not vx.any():
+                continue
+            patch = a[:, iy[vy]][:, :, ix[vx]]
+            gg = gout[:, oy[vy]][:, :, ox[vx]]
+            dw[i, j] = np.einsum("nyxc,nyxk->ck", patch, gg)
+            dx[:, iy[vy][0]:iy[vy][-1] + 1:stride[0], ix[vx][0]:ix[vx][-1] + 1:stride[1]] += gg @ wt[i, j].T
+    return dx, dw, gout.sum(axis=(0, 1, 2))
+
+
+def sparse_conv2d_grads(x, mask, wts, bias, stride, same: bool, block, gout, pool="max", threshold=None):
+    """Input/weight/bias gradients of sparse_conv2d (reference ``layers.py:50-65``)."""
+    n, h, w, _ = x.shape
+    g = geometry(h, w, wts.shape[:2], stride, same, block)
+    idx = reduce_mask(mask, g, pool, threshold)
+    if len(idx) == 0:
+        return np.zeros_like(x), np.zeros_like(wts), np.zeros(wts.shape[3], x.dtype)
+    dxb, dw, db = conv_nhwc_grads(gather(x, idx, g), wts, stride, (0, 0), scatter_grad(gout, idx, g))
+    return gather_grad(dxb, idx, g, x.shape), dw, db
+
+
+def sparse_residual_unit_grads(x, mask, u: dict, block, gout, halo: int = 1):
+    """Input and conv-weight gradients of the pre-activation inference-BN sparse unit
+    (reference ``layers.py:232-270``): the branch is recomputed on the gathered stack with
+    its intermediates, then differentiated back through 1x1 / ReLU / BN scale / crop /
+    3x3 / in-bounds map / 1x1 / ReLU / BN1 scale, and gather_grad'ed onto gout."""
+    n, h, w, _ = x.shape
+    g = unit_geometry(h, w, block, halo)
+    idx = reduce_mask(mask, g, "max")
+    if len(idx) == 0:
+        z = {k: (np.zeros_like(u[f"w{k[-1]}"]), np.zeros(u[f"w{k[-1]}"].shape[3])) for k in ("conv1", "conv2", "conv3")}
+        return gout.copy(), z
+    a = gather(x, idx, g)
+    conv2_pad = (0, 0) if halo >= 1 else (1, 1)
+    crop = halo - 1 if halo >= 1 else 0
+    valid = in_bounds_map(idx, g).astype(x.dtype)
+    b1 = bn_apply(a, u["bn1"])
+    r1 = np.maximum(b1, 0)
+    c1 = conv_nhwc(r1, u["w1"], u["b1"])
+    b2 = bn_apply(c1, u["bn2"])
+    r2 = np.maximum(b2, 0) * valid[..., None]
+    c2 = conv_nhwc(r2, u["w2"], u["b2"], (1, 1), conv2_pad)
+    c2c = c2[:, crop:c2.shape[1] - crop, crop:c2.shape[2] - crop] if crop else c2
+    b3 = bn_apply(c2c, u["bn3"])
+    r3 = np.maximum(b3, 0)
+
+    def sc(bn, dt):
+        return (bn["gamma"] / np.sqrt(bn["var"] + bn.get("eps", 1e-5))).astype(dt)
+
+    gb = scatter_grad(gout, idx, g)
+    d_r3, dw3, db3 = conv_nhwc_grads(r3, u["w3"], (1, 1), (0, 0), gb)
+    d_c2c = d_r3 * (b3 > 0) * sc(u["bn3"], d_r3.dtype)
+    if crop:
+        pd = np.zeros(c2.shape, d_c2c.dtype)
+        pd[:, crop:-crop, crop:-crop, :] = d_c2c
+        d_c2c = pd
+    d_r2, dw2, db2 = conv_nhwc_grads(r2, u["w2"], (1, 1), conv2_pad, d_c2c)
+    d_c1 = d_r2 * valid[..., None] * (b2 > 0) * sc(u["bn2"], d_r2.dtype)
+    d_r1, dw1, db1 = conv_nhwc_grads(r1, u["w1"], (1, 1), (0, 0), d_c1)
+    d_a0 = d_r1 * (b1 > 0) * sc(u["bn1"], d_r1.dtype)
+    return gout + gather_grad(d_a0, idx, g, x.shape), {"conv1": (dw1, db1), "conv2": (dw2, db2),
+                                                       "conv3": (dw3, db3)}
+
+
+def sparse_batch_norm_train(stack: np.ndarray, gamma, beta, eps: float = 1e-5):
+    """TRAIN_STATS batch norm over the gathered positions only (reference ``layers.py:68-82``)."""
+    mean = stack.mean(axis=(0, 1, 2))
+    var = stack.var(axis=(0, 1, 2))
+    scale = (gamma / np.sqrt(var + eps)).astype(stack.dtype)
+    return (stack - mean.astype(stack.dtype)) * scale + np.asarray(beta).astype(stack.dtype), mean, var
 
 
 # --------------------------------------------------------------------------- metrics

@@ -168,6 +168,71 @@ def scatter_transpose(blocks: GatheredBlocks, out_spec: BlockSpec, dst: Tensor4D
     return _scatter(blocks, out_spec, dst, add=False)
 
 
+# ---- training path (adjoints) ---------------------------------------------------------
+
+def gather_grad(g_blocks: GatheredBlocks, spec: BlockSpec, dst_dims, dtype=None) -> Tensor4D:
+    """Adjoint of gather: block gradients summed over their (overlapping) input windows
+    (reference `blocks.py:162-188`).  One pixel-centric launch (`sbn_gather_grad`): every
+    element is the covering blocks' values added in index order from zero — the
+    reference's canonical order, so f32/f64 results are bit-exact, with no atomics."""
+    if g_blocks.spec != spec:
+        raise GeometryError("gradient block geometry does not match spec")
+    n, h, w, c = (int(v) for v in dst_dims)
+    if (h, w) != tuple(spec.input_size):
+        raise ShapeMismatchError(f"destination spatial dims {(h, w)} != spec input size {spec.input_size}")
+    bd = g_blocks.tensor.dims
+    if (bd[1], bd[2]) != tuple(spec.block_size):
+        raise ShapeMismatchError(f"gradient block dims {(bd[1], bd[2])} != block size {spec.block_size}")
+    if g_blocks.tensor.layout is Layout.CHANNELS_FIRST:
+        raise GeometryError("gather_grad expects ChannelsLast block gradients")
+    lib = _lib.load()
+    blk = cuda(g_blocks.tensor.data)
+    if dtype is not None:
+        blk = blk.to(dtype if isinstance(dtype, torch.dtype) else torch.from_numpy(np.zeros(1, dtype)).dtype)
+    out = torch.empty((n, h, w, c), dtype=blk.dtype, device=blk.device)
+    idx = g_blocks.indices.to_device(blk.device)
+    g = spec.c_geometry(n)
+    ws = torch.empty(max(1, int(lib.sbn_gather_grad_workspace(C.byref(g)))), dtype=torch.uint8, device=blk.device)
+    B = g_blocks.count
+    st = lib.sbn_gather_grad(blk.data_ptr() if B else None, dtype_code(blk.dtype), c, C.byref(g),
+                             idx.rows.data_ptr(), idx.count_dev.data_ptr(), B, out.data_ptr(), ws.data_ptr(),
+                             ws.numel(), _lib.stream_handle(blk.device))
+    _lib.check(st, "gather_grad")
+    return Tensor4D(out)
+
+
+def _out_grid_spec_geometry(spec: BlockSpec, n: int) -> _lib.Geometry:
+    """Geometry of a gather over the disjoint OUTPUT grid: image = out size, block =
+    stride = out block, origin 0 (windows never overlap; the tail is zero-filled)."""
+    g = spec.c_geometry(n)
+    g.h, g.w = spec.out_size
+    g.bh, g.bw = spec.out_block_size
+    g.sy, g.sx = spec.out_block_size
+    g.oy = g.ox = 0
+    return g
+
+
+def scatter_grad(g_out: Tensor4D, idx: BlockIndexList, out_spec: BlockSpec) -> GatheredBlocks:
+    """Adjoint of scatter: the upstream gradient over each block's disjoint, clipped write
+    window (reference `blocks.py:191-204`) — `sbn_gather` over the output grid."""
+    n, oh, ow, c = g_out.dims
+    if (oh, ow) != tuple(out_spec.out_size):
+        raise ShapeMismatchError(f"gradient spatial dims {(oh, ow)} != conv output {out_spec.out_size}")
+    _check_indices(idx, out_spec, n)
+    lib = _lib.load()
+    t = _nhwc_cuda(g_out)
+    idx.to_device(t.device)
+    B = idx.count
+    obh, obw = out_spec.out_block_size
+    out = torch.empty((B, obh, obw, c), dtype=t.dtype, device=t.device)
+    if B:
+        g = _out_grid_spec_geometry(out_spec, n)
+        st = lib.sbn_gather(t.data_ptr(), dtype_code(t.dtype), c, C.byref(g), idx.rows.data_ptr(),
+                            idx.count_dev.data_ptr(), B, 0, out.data_ptr(), _lib.stream_handle(t.device))
+        _lib.check(st, "scatter_grad")
+    return GatheredBlocks(Tensor4D(out), out_spec, idx)
+
+
 # ---- north-star (uber/sbnet op) spellings -------------------------------------------
 
 def sparse_gather(x: Tensor4D, idx: BlockIndexList, spec: BlockSpec,

@@ -88,6 +88,58 @@ copy_regions_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, 
   }
 }
 
+// gather_grad (`blocks.py:162-188`): block table (frame, by, bx) -> stack row, -1 inactive.
+__global__ void block_table_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int cap,
+                                   Geo g, int32_t* __restrict__ table) {
+  const int B = ld_count(count, cap);
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+    const int n = idx[3 * b], by = idx[3 * b + 1], bx = idx[3 * b + 2];
+    table[((size_t)n * g.gy + by) * g.gx + bx] = b;
+  }
+}
+
+// Pixel-centric adjoint of gather: every element of dx is written once — the sum of the
+// covering blocks' gradient values in ascending stack order (= ascending (by, bx) within
+// the frame), starting from zero.  That is the reference's `out += blk` sequence in index
+// order, so f32/f64 results are bit-exact and no atomics are needed (bf16 accumulates
+// in fp32 and rounds once).
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+gather_grad_kernel(const T* __restrict__ gblk, Geo g, int c, const int32_t* __restrict__ table,
+                   T* __restrict__ dx) {
+  using A = typename Acc<T>::type;
+  const long total = (long)g.n * g.h * g.w * c;
+  for (long i = blockIdx.x * (long)kThreads + threadIdx.x; i < total; i += (long)gridDim.x * kThreads) {
+    const int ch = (int)(i % c);
+    long p = i / c;
+    const int x = (int)(p % g.w);
+    p /= g.w;
+    const int y = (int)(p % g.h);
+    const int n = (int)(p / g.h);
+    // covering grid rows: oy + by*sy <= y < oy + by*sy + bh
+    const int ry = y - g.oy, rx = x - g.ox;
+    int by0 = ry - g.bh + 1 > 0 ? (ry - g.bh + 1 + g.sy - 1) / g.sy : 0;
+    int by1 = ry / g.sy;
+    int bx0 = rx - g.bw + 1 > 0 ? (rx - g.bw + 1 + g.sx - 1) / g.sx : 0;
+    int bx1 = rx / g.sx;
+    by1 = min(by1, g.gy - 1);
+    bx1 = min(bx1, g.gx - 1);
+    T acc = T(0);
+    A accf = A(0);
+    for (int by = by0; by <= by1; ++by)
+      for (int bx = bx0; bx <= bx1; ++bx) {
+        const int b = __ldg(table + ((size_t)n * g.gy + by) * g.gx + bx);
+        if (b < 0) continue;
+        const int wy = ry - by * g.sy, wx = rx - bx * g.sx;
+        const T v = __ldg(gblk + (((size_t)b * g.bh + wy) * g.bw + wx) * c + ch);
+        if constexpr (sizeof(T) == 2) accf += to_acc(v);
+        else acc = acc + v;
+      }
+    if constexpr (sizeof(T) == 2) dx[i] = from_acc<T>(accf);
+    else dx[i] = acc;
+  }
+}
+
 template <typename E>
 __global__ void __launch_bounds__(kThreads)
 gather_transpose_kernel(const E* __restrict__ x, Geo g, int c, const int32_t* __restrict__ idx,
@@ -333,4 +385,39 @@ extern "C" int sbn_copy_block_regions(const void* src, void* dst, int dtype, int
     default: copy_regions_kernel<2><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;
   }
   return launch_status("copy_block_regions");
+}
+
+extern "C" size_t sbn_gather_grad_workspace(const sbn_geometry* gp) {
+  if (!gp) return 0;
+  return (size_t)gp->n * gp->gy * gp->gx * sizeof(int32_t);
+}
+
+extern "C" int sbn_gather_grad(const void* gblk, int dtype, int c, const sbn_geometry* gp, const int32_t* idx,
+                               const int32_t* count, int cap, void* dx, void* ws, size_t ws_bytes,
+                               sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  const int es = dtype_size(dtype);
+  SBN_CHECK_ARG(es > 0, SBN_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
+  SBN_CHECK_ARG(c > 0, SBN_ERR_SHAPE, "channels must be > 0");
+  SBN_CHECK_ARG(dx && idx && count, SBN_ERR_INVALID, "null pointer argument");
+  SBN_CHECK_ARG(ws && ws_bytes >= sbn_gather_grad_workspace(gp), SBN_ERR_WORKSPACE,
+                "gather_grad needs a %zu-byte workspace", sbn_gather_grad_workspace(gp));
+  SBN_CHECK_ARG(cap <= 0 || gblk, SBN_ERR_INVALID, "null block gradient");
+  Geo g = to_geo(gp);
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* table = (int32_t*)ws;
+  cudaMemsetAsync(table, 0xFF, sbn_gather_grad_workspace(gp), s);
+  if (cap > 0) {
+    block_table_kernel<<<(unsigned)grid_for(cap, kThreads), kThreads, 0, s>>>(idx, count, cap, g, table);
+    st = launch_status("gather_grad_table");
+    if (st) return st;
+  }
+  const unsigned grid = (unsigned)grid_for((long)g.n * g.h * g.w * c, kThreads);
+  switch (dtype) {
+    case SBN_F32: gather_grad_kernel<float><<<grid, kThreads, 0, s>>>((const float*)gblk, g, c, table, (float*)dx); break;
+    case SBN_F64: gather_grad_kernel<double><<<grid, kThreads, 0, s>>>((const double*)gblk, g, c, table, (double*)dx); break;
+    default: gather_grad_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>((const __nv_bfloat16*)gblk, g, c, table, (__nv_bfloat16*)dx); break;
+  }
+  return launch_status("gather_grad");
 }

@@ -18,7 +18,7 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib
-from .blocks import GatheredBlocks
+from .blocks import GatheredBlocks, gather, gather_grad, in_bounds_map, scatter_grad
 from .errors import EmptyBlockListError, GeometryError, ShapeMismatchError, UnsupportedConfigError
 from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, bn_inference,
                   dense_conv_nhwc, exact_fp32)
@@ -138,6 +138,103 @@ def sparse_conv_algo(dtype: torch.dtype, f: FilterBank, p: ConvParams, spec: Blo
     a = _lib.load(False).sbn_sparse_conv_algo(dtype_code(dtype), f.c_in, f.c_out, *p.kernel,
                                               *p.stride, C.byref(g))
     return "tcgen05" if a == _lib.SBN_ALGO_TCGEN05 else "simt"
+
+
+def _conv_grads_stack(a: torch.Tensor, w_hwio: torch.Tensor, stride, pad, g: torch.Tensor):
+    """(dx, dw, db) of a conv on an NHWC stack (reference `ops.py:167-197`): the stack-
+    level data and weight gradients are cuDNN's (exact fp32, no TF32), bias = sum."""
+    from torch.nn.grad import conv2d_input, conv2d_weight
+    xin = a.permute(0, 3, 1, 2)
+    go = g.permute(0, 3, 1, 2)
+    w = w_hwio.permute(3, 2, 0, 1).contiguous()
+    with exact_fp32():
+        dx = conv2d_input(tuple(xin.shape), w, go, stride=tuple(stride), padding=tuple(pad))
+        dw = conv2d_weight(xin, tuple(w.shape), go, stride=tuple(stride), padding=tuple(pad))
+    return (dx.permute(0, 2, 3, 1).contiguous(), dw.permute(2, 3, 1, 0).contiguous(),
+            g.sum(dim=(0, 1, 2)))
+
+
+def sparse_conv2d_grads(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
+                        block_size: tuple[int, int], g_out: Tensor4D, pool: PoolMode = PoolMode.MAX,
+                        threshold: float | None = None):
+    """Input / weight / bias gradients of sparse_conv2d for upstream gradient g_out
+    (reference `layers.py:50-65`): gather (sbn_gather) -> scatter_grad (sbn_gather over the
+    output grid) -> per-block conv gradients on the stack -> gather_grad
+    (sbn_gather_grad).  Returns (dx Tensor4D, dw HWIO tensor, db tensor) on the device."""
+    _check_mask(x, mask)
+    spec = compute_block_spec(x.dims, p, block_size)
+    idx = reduce_mask(mask, spec, pool, threshold)
+    xt = cuda(x.nhwc())
+    w, _ = f.device_tensors(xt.dtype, xt.device)
+    if idx.count == 0:
+        return (Tensor4D.from_nhwc(torch.zeros_like(xt), x.layout), torch.zeros_like(w),
+                torch.zeros(f.c_out, dtype=xt.dtype, device=xt.device))
+    g = gather(Tensor4D(xt), idx, spec)
+    gb = scatter_grad(g_out, idx, spec)
+    dxb, dw, db = _conv_grads_stack(g.tensor.data, w, p.stride, (0, 0), cuda(gb.tensor.data))
+    dx = gather_grad(g.with_tensor(Tensor4D(dxb)), spec, x.dims)
+    return Tensor4D.from_nhwc(dx.nhwc(), x.layout), dw, db
+
+
+def sparse_residual_unit_grads(x: Tensor4D, mask: BinaryMask, u: "ResidualUnitParams",
+                               block_size: tuple[int, int], g_out: Tensor4D, halo: int = 1):
+    """Input and conv-weight gradients of the pre-activation, inference-BN sparse unit
+    (reference `layers.py:232-270`).  The branch is recomputed on the gathered stack with
+    its intermediates, differentiated back through 1x1 / ReLU / BN scale / crop / 3x3 /
+    in-bounds map / 1x1 / ReLU / BN1 scale, and gather_grad'ed onto g_out.
+    Returns (dx, {"conv1": (dw, db), "conv2": ..., "conv3": ...}) on the device."""
+    if not u.pre_activation:
+        raise UnsupportedConfigError("gradients implemented for the pre-activation chain only")
+    _check_mask(x, mask)
+    if u.channels != x.dims[3]:
+        raise ShapeMismatchError(f"unit channels {u.channels} != input channels {x.dims[3]}")
+    spec = unit_spec(x.dims, block_size, halo)
+    idx = reduce_mask(mask, spec, PoolMode.MAX)
+    xt = cuda(x.nhwc())
+    dt, dev = xt.dtype, xt.device
+    if dt not in (torch.float32, torch.float64):
+        raise UnsupportedConfigError("residual-unit gradients are float32/float64 (as the reference)")
+    ws = {}
+    for nm in ("conv1", "conv2", "conv3"):
+        fb = getattr(u, nm)
+        wt, bt = fb.device_tensors(dt, dev)
+        ws[nm] = (wt, bt if bt is not None else torch.zeros(fb.c_out, dtype=dt, device=dev))
+    if idx.count == 0:
+        return g_out, {nm: (torch.zeros_like(ws[nm][0]), torch.zeros_like(ws[nm][1])) for nm in ws}
+    a = gather(Tensor4D(xt), idx, spec).tensor.data
+    conv2_pad = (0, 0) if halo >= 1 else (1, 1)
+    crop = halo - 1 if halo >= 1 else 0
+    valid = in_bounds_map(idx, spec, x.dims[0]).to(dt)[..., None]
+    s1, t1 = u.bn1.folded(dt, dev)
+    s2, t2 = u.bn2.folded(dt, dev)
+    s3, t3 = u.bn3.folded(dt, dev)
+
+    def conv(t, nm, pad=(0, 0)):
+        return dense_conv_nhwc(t, ws[nm][0], ws[nm][1], (1, 1), pad)
+
+    with exact_fp32():
+        b1 = a * s1 + t1
+        r1 = torch.relu(b1)
+        b2 = conv(r1, "conv1") * s2 + t2
+        r2 = torch.relu(b2) * valid
+        c2 = conv(r2, "conv2", conv2_pad)
+        c2c = c2[:, crop:c2.shape[1] - crop, crop:c2.shape[2] - crop] if crop else c2
+        b3 = c2c * s3 + t3
+        r3 = torch.relu(b3)
+        gb = cuda(scatter_grad(g_out, idx, spec).tensor.data)
+        d_r3, dw3, db3 = _conv_grads_stack(r3, ws["conv3"][0], (1, 1), (0, 0), gb)
+        d_c2c = d_r3 * (b3 > 0).to(dt) * s3
+        if crop:
+            d_c2 = torch.zeros(c2.shape, dtype=dt, device=dev)
+            d_c2[:, crop:-crop, crop:-crop] = d_c2c
+            d_c2c = d_c2
+        d_r2, dw2, db2 = _conv_grads_stack(r2, ws["conv2"][0], (1, 1), conv2_pad, d_c2c)
+        d_c1 = d_r2 * valid * (b2 > 0).to(dt) * s2
+        d_r1, dw1, db1 = _conv_grads_stack(r1, ws["conv1"][0], (1, 1), (0, 0), d_c1)
+        d_a0 = d_r1 * (b1 > 0).to(dt) * s1
+    d_branch = gather_grad(GatheredBlocks(Tensor4D(d_a0.contiguous()), spec, idx), spec, x.dims)
+    dx = cuda(g_out.nhwc()) + d_branch.data
+    return Tensor4D.from_nhwc(dx, x.layout), {"conv1": (dw1, db1), "conv2": (dw2, db2), "conv3": (dw3, db3)}
 
 
 def sparse_batch_norm(blocks: GatheredBlocks, bn: BnParams, mode: BnMode = BnMode.INFERENCE):

@@ -122,3 +122,62 @@ def test_oracle_vs_live_reference_random():
                                 var=bn.running_var, eps=bn.epsilon)
         got = O.sparse_residual_unit(x, mk.data, ud, (bs, bs))
         assert O.rel_err(got, ref) <= 1e-6
+
+
+# ----------------------------------------------------------------------------- training path
+
+def _geo(cfg):
+    h, w, k, s, same, b = conv_cfg(cfg)
+    return O.geometry(h, w, k, s, same, b)
+
+
+def test_gather_scatter_grad_match_reference_golden():
+    z = load("grads")
+    for cs in cases(z, "g"):
+        g = _geo(cs["cfg"])
+        n, c = int(cs["cfg"][9]), int(cs["cfg"][10])
+        idx = cs["idx"]
+        assert np.array_equal(O.reduce_mask(cs["mask"], g), idx)
+        dims = (n, *g.in_size, c)
+        gg = O.gather_grad(cs["gblk"], idx, g, dims)
+        assert gg.dtype == cs["gather_grad"].dtype and np.array_equal(gg, cs["gather_grad"])
+        assert np.array_equal(O.scatter_grad(cs["gout"], idx, g), cs["scatter_grad"])
+
+
+def test_sparse_conv2d_grads_match_reference_golden():
+    z = load("grads")
+    for cs in cases(z, "v"):
+        h, w, k, s, same, b = conv_cfg(cs["cfg"])
+        dx, dw, db = O.sparse_conv2d_grads(cs["x"], cs["mask"], cs["w"], cs["b"], s, same, b, cs["gout"])
+        tol = 1e-12 if cs["x"].dtype == np.float64 else 1e-5
+        for got, ref in ((dx, cs["dx"]), (dw, cs["dw"]), (db, cs["db"])):
+            assert O.rel_err(got, ref) <= tol
+
+
+def _unit_from(cs):
+    u = {"pre": True}
+    for i in (1, 2, 3):
+        u[f"w{i}"], u[f"b{i}"] = cs[f"conv{i}_w"], cs[f"conv{i}_b"]
+        u[f"bn{i}"] = {"gamma": cs[f"bn{i}_gamma"], "beta": cs[f"bn{i}_beta"], "mean": cs[f"bn{i}_mean"],
+                       "var": cs[f"bn{i}_var"], "eps": 1e-5}
+    return u
+
+
+def test_sparse_residual_unit_grads_match_reference_golden():
+    z = load("grads")
+    for cs in cases(z, "u"):
+        n, h, w, c, m, bs, halo, _ = (int(v) for v in cs["cfg"])
+        dx, dws = O.sparse_residual_unit_grads(cs["x"], cs["mask"], _unit_from(cs), (bs, bs), cs["gout"], halo)
+        tol = 1e-12 if cs["x"].dtype == np.float64 else 1e-5
+        assert O.rel_err(dx, cs["dx"]) <= tol
+        for nm in ("conv1", "conv2", "conv3"):
+            assert O.rel_err(dws[nm][0], cs[f"d{nm}_w"]) <= tol
+            assert O.rel_err(dws[nm][1], cs[f"d{nm}_b"]) <= tol
+
+
+def test_sparse_batch_norm_train_matches_reference_golden():
+    z = load("grads")
+    for cs in cases(z, "b"):
+        y, mean, var = O.sparse_batch_norm_train(cs["stack"], cs["gamma"], cs["beta"])
+        assert O.rel_err(y, cs["y"]) <= 1e-12
+        assert O.rel_err(mean, cs["mean"]) <= 1e-12 and O.rel_err(var, cs["var"]) <= 1e-12
