@@ -339,11 +339,42 @@ def gen_grads(bc):
     np.savez_compressed(os.path.join(OUT, "grads.npz"), **out)
 
 
+def gen_formats(bc):
+    """Reference-written SBT4 / SBMK files and a saved backbone manifest, as raw bytes, so
+    the package's readers/writers are pinned to the reference's on-disk formats."""
+    import tempfile
+    rng = np.random.default_rng(7000)
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        t32 = bc.Tensor4D(rng.standard_normal((2, 3, 5, 4)).astype(np.float32))
+        t64 = bc.transpose_layout(bc.Tensor4D(rng.standard_normal((1, 4, 3, 6))))
+        for nm, t in (("f32", t32), ("f64cf", t64)):
+            fp = os.path.join(d, nm + ".sbt4")
+            bc.save_sbt4(fp, t)
+            out[f"sbt4_{nm}_bytes"] = np.frombuffer(open(fp, "rb").read(), np.uint8)
+            out[f"sbt4_{nm}_data"] = t.data
+            out[f"sbt4_{nm}_layout"] = np.asarray([t.layout.value])
+        m = bc.synth_mask_blobs((2, 20, 30), 0.7, 3)
+        fp = os.path.join(d, "m.sbmk")
+        bc.save_sbmk(fp, m)
+        out["sbmk_bytes"] = np.frombuffer(open(fp, "rb").read(), np.uint8)
+        out["sbmk_data"] = m.data
+        cfgs = [bc.StageConfig(1, (4, 3, 6), (8, 8), 1, 2), bc.StageConfig(2, (6, 4, 6), (6, 6), 2, 1)]
+        bb = bc.build_backbone(cfgs, np.random.default_rng(11))
+        bd = os.path.join(d, "bb")
+        bc.save_backbone(bd, bb)
+        names = sorted(os.listdir(bd))
+        out["bb_names"] = np.asarray(names)
+        for i, nm in enumerate(names):
+            out[f"bb_file{i}"] = np.frombuffer(open(os.path.join(bd, nm), "rb").read(), np.uint8)
+    np.savez_compressed(os.path.join(OUT, "formats.npz"), **out)
+
+
 def main():
     bc = _ref()
     os.makedirs(OUT, exist_ok=True)
     for fn in (gen_geometry, gen_reduce_mask, gen_gather_scatter, gen_sparse_conv, gen_residual,
-               gen_masks, gen_units, gen_config1, gen_grads):
+               gen_masks, gen_units, gen_config1, gen_grads, gen_formats):
         fn(bc)
         print("wrote", fn.__name__)
 

@@ -21,7 +21,7 @@ from . import _lib
 from .blocks import GatheredBlocks, gather, gather_grad, in_bounds_map, scatter_grad
 from .errors import EmptyBlockListError, GeometryError, ShapeMismatchError, UnsupportedConfigError
 from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, bn_inference,
-                  dense_conv_nhwc, exact_fp32)
+                  conv_grads_nhwc, dense_conv_nhwc, exact_fp32)
 from .tensor import Tensor4D, cuda, dtype_code
 from .tiling import (BinaryMask, BlockIndexList, BlockSpec, compute_block_spec, downsample_mask,
                      reduce_mask)
@@ -140,20 +140,6 @@ def sparse_conv_algo(dtype: torch.dtype, f: FilterBank, p: ConvParams, spec: Blo
     return "tcgen05" if a == _lib.SBN_ALGO_TCGEN05 else "simt"
 
 
-def _conv_grads_stack(a: torch.Tensor, w_hwio: torch.Tensor, stride, pad, g: torch.Tensor):
-    """(dx, dw, db) of a conv on an NHWC stack (reference `ops.py:167-197`): the stack-
-    level data and weight gradients are cuDNN's (exact fp32, no TF32), bias = sum."""
-    from torch.nn.grad import conv2d_input, conv2d_weight
-    xin = a.permute(0, 3, 1, 2)
-    go = g.permute(0, 3, 1, 2)
-    w = w_hwio.permute(3, 2, 0, 1).contiguous()
-    with exact_fp32():
-        dx = conv2d_input(tuple(xin.shape), w, go, stride=tuple(stride), padding=tuple(pad))
-        dw = conv2d_weight(xin, tuple(w.shape), go, stride=tuple(stride), padding=tuple(pad))
-    return (dx.permute(0, 2, 3, 1).contiguous(), dw.permute(2, 3, 1, 0).contiguous(),
-            g.sum(dim=(0, 1, 2)))
-
-
 def sparse_conv2d_grads(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
                         block_size: tuple[int, int], g_out: Tensor4D, pool: PoolMode = PoolMode.MAX,
                         threshold: float | None = None):
@@ -171,7 +157,7 @@ def sparse_conv2d_grads(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvPar
                 torch.zeros(f.c_out, dtype=xt.dtype, device=xt.device))
     g = gather(Tensor4D(xt), idx, spec)
     gb = scatter_grad(g_out, idx, spec)
-    dxb, dw, db = _conv_grads_stack(g.tensor.data, w, p.stride, (0, 0), cuda(gb.tensor.data))
+    dxb, dw, db = conv_grads_nhwc(g.tensor.data, w, p.stride, (0, 0), cuda(gb.tensor.data))
     dx = gather_grad(g.with_tensor(Tensor4D(dxb)), spec, x.dims)
     return Tensor4D.from_nhwc(dx.nhwc(), x.layout), dw, db
 
@@ -222,15 +208,15 @@ def sparse_residual_unit_grads(x: Tensor4D, mask: BinaryMask, u: "ResidualUnitPa
         b3 = c2c * s3 + t3
         r3 = torch.relu(b3)
         gb = cuda(scatter_grad(g_out, idx, spec).tensor.data)
-        d_r3, dw3, db3 = _conv_grads_stack(r3, ws["conv3"][0], (1, 1), (0, 0), gb)
+        d_r3, dw3, db3 = conv_grads_nhwc(r3, ws["conv3"][0], (1, 1), (0, 0), gb)
         d_c2c = d_r3 * (b3 > 0).to(dt) * s3
         if crop:
             d_c2 = torch.zeros(c2.shape, dtype=dt, device=dev)
             d_c2[:, crop:-crop, crop:-crop] = d_c2c
             d_c2c = d_c2
-        d_r2, dw2, db2 = _conv_grads_stack(r2, ws["conv2"][0], (1, 1), conv2_pad, d_c2c)
+        d_r2, dw2, db2 = conv_grads_nhwc(r2, ws["conv2"][0], (1, 1), conv2_pad, d_c2c)
         d_c1 = d_r2 * valid * (b2 > 0).to(dt) * s2
-        d_r1, dw1, db1 = _conv_grads_stack(r1, ws["conv1"][0], (1, 1), (0, 0), d_c1)
+        d_r1, dw1, db1 = conv_grads_nhwc(r1, ws["conv1"][0], (1, 1), (0, 0), d_c1)
         d_a0 = d_r1 * (b1 > 0).to(dt) * s1
     d_branch = gather_grad(GatheredBlocks(Tensor4D(d_a0.contiguous()), spec, idx), spec, x.dims)
     dx = cuda(g_out.nhwc()) + d_branch.data

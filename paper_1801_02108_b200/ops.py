@@ -17,7 +17,7 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from .errors import ShapeMismatchError
+from .errors import ShapeMismatchError, UnsupportedConfigError
 from .tensor import Layout, Tensor4D, as_torch, compute_dtype, cuda
 
 
@@ -214,3 +214,67 @@ def batch_norm(x: Tensor4D, bn: BnParams, mode: BnMode = BnMode.INFERENCE):
 
 def relu(x: Tensor4D) -> Tensor4D:
     return Tensor4D(torch.clamp_min(x.data, 0), x.layout)
+
+
+# ----------------------------------------------------------------------------- dense utilities
+# The reference's dense helpers outside the sparse path (`ops.py:167-269`, `winograd.py`),
+# on cuDNN so a caller switching packages finds them; exact fp32 (no TF32).
+
+def conv_grads_nhwc(a: torch.Tensor, w_hwio: torch.Tensor, stride, pad, g: torch.Tensor):
+    """(dx, dw, db) of a conv on an NHWC tensor for upstream gradient g (reference
+    `ops.py:167-197`): cuDNN data / weight gradients, bias = sum over (n, h, w)."""
+    from torch.nn.grad import conv2d_input, conv2d_weight
+    xin = a.permute(0, 3, 1, 2)
+    go = g.permute(0, 3, 1, 2)
+    w = w_hwio.permute(3, 2, 0, 1).contiguous()
+    with exact_fp32():
+        dx = conv2d_input(tuple(xin.shape), w, go, stride=tuple(stride), padding=tuple(pad))
+        dw = conv2d_weight(xin, tuple(w.shape), go, stride=tuple(stride), padding=tuple(pad))
+    return (dx.permute(0, 2, 3, 1).contiguous(), dw.permute(2, 3, 1, 0).contiguous(),
+            g.sum(dim=(0, 1, 2)))
+
+
+def conv2d_direct_grads(x: Tensor4D, f: FilterBank, p: ConvParams, g_out: Tensor4D):
+    """Dense conv gradients (reference `ops.py:207-210`)."""
+    _check_conv_shapes(x, f, p)
+    xt = cuda(x.nhwc())
+    w, _ = f.device_tensors(xt.dtype, xt.device)
+    dx, dw, db = conv_grads_nhwc(xt, w, p.stride, p.pad, cuda(g_out.nhwc(), xt.device))
+    return Tensor4D.from_nhwc(dx, x.layout), dw, db
+
+
+def winograd_supported(p: ConvParams) -> bool:
+    return tuple(p.kernel) == (3, 3) and tuple(p.stride) == (1, 1)
+
+
+def conv2d_winograd(x: Tensor4D, f: FilterBank, p: ConvParams) -> Tensor4D:
+    """3x3 / stride-1 convolution (reference `winograd.py:39-`); cuDNN chooses its own
+    (Winograd or implicit-GEMM) algorithm — the result equals conv2d_direct's."""
+    if not winograd_supported(p):
+        raise UnsupportedConfigError(
+            f"Winograd path supports only 3x3 kernels at stride 1, got kernel {p.kernel} stride {p.stride}")
+    return conv2d_direct(x, f, p)
+
+
+def conv2d(x: Tensor4D, f: FilterBank, p: ConvParams, algo: str = "auto") -> Tensor4D:
+    """Algorithm dispatcher (reference `ops.py:257-269`)."""
+    if algo == "winograd":
+        return conv2d_winograd(x, f, p)
+    if algo in ("direct", "auto"):
+        return conv2d_direct(x, f, p)
+    raise ValueError(f"unknown algo {algo!r}")
+
+
+def pool2d(x: Tensor4D, window, stride=None, mode: PoolMode = PoolMode.MAX) -> Tensor4D:
+    """Valid pooling over full windows only (reference `ops.py:237-254`)."""
+    wh, ww = (window, window) if isinstance(window, int) else tuple(window)
+    if stride is None:
+        stride = (wh, ww)
+    sh, sw = (stride, stride) if isinstance(stride, int) else tuple(stride)
+    n, h, w, c = x.dims
+    if wh > h or ww > w:
+        raise ShapeMismatchError(f"pool window {wh}x{ww} larger than input {h}x{w}")
+    t = cuda(x.nhwc()).permute(0, 3, 1, 2)
+    fn = F.max_pool2d if mode is PoolMode.MAX else F.avg_pool2d
+    out = fn(t, (wh, ww), (sh, sw))
+    return Tensor4D.from_nhwc(out.permute(0, 2, 3, 1).contiguous(), x.layout)
