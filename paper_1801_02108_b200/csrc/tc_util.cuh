@@ -29,6 +29,20 @@ __device__ __forceinline__ uint64_t desc_kmajor_noswz(uint32_t saddr, uint32_t l
   return d;
 }
 
+// K-major swizzled operand (rows of 64 B (SWIZZLE_64B, layout 4) or 128 B (SWIZZLE_128B,
+// layout 2), 8-row atoms at SBO bytes), as TMA writes it with the matching swizzle mode.
+// A k-step inside the row is a +32 B start-address change (the swizzle is a function of
+// the absolute address, so it stays consistent).
+__device__ __forceinline__ uint64_t desc_kmajor_swz(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;  // LBO (unused for swizzled K-major) = 1
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7u) << 61;
+  return d;
+}
+
 // kind::f16 instruction descriptor: bf16 x bf16 -> f32, A/B K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4)                       // D format: F32

@@ -63,11 +63,13 @@ constexpr int resident_kc() {
   constexpr int taps = MODE == kMid ? 9 : 1;
   constexpr int ra = MODE == kMid ? kMaxRows : 128;
   constexpr long wbytes = (long)taps * K * N * 2;
-  constexpr int pref = K <= 96 ? K : (K % 64 == 0 ? 64 : 32);
+  // IN stages its operand as swizzled rows of KC channels (64 -> SWIZZLE_128B, 32 ->
+  // SWIZZLE_64B); MID/OUT use the 16-byte plane layout
+  constexpr int pref = MODE == kIn ? (K % 64 == 0 ? 64 : 32) : K <= 96 ? K : (K % 64 == 0 ? 64 : 32);
   constexpr int cands[4] = {pref, 64, 32, 16};
   for (int i = 0; i < 4; ++i) {
     const int kc = cands[i];
-    if (kc > pref || K % kc != 0 || kc % 16 != 0) continue;
+    if (kc > pref || K % kc != 0 || kc % 16 != 0 || (MODE == kIn && kc != 64 && kc != 32)) continue;
     const long ach = (long)(kc / 8) * ra * 16;
     if (3 * ach + wbytes + 8192 <= kBudget) return kc;
   }
@@ -81,6 +83,9 @@ struct WCfg {
   static constexpr bool RES = RKC != 0;  // weights resident for the whole kernel
   static constexpr int KC = RES ? RKC : (K % 64 == 0 ? 64 : 32);
   static_assert(K % KC == 0 && KC % 16 == 0, "K chunking");
+  static_assert(MODE != kIn || KC == 64 || KC == 32, "IN: swizzled 128-B / 64-B rows");
+  static constexpr int ROWB = KC * 2;                      // IN: bytes per staged row
+  static constexpr uint32_t SWZ = KC == 64 ? 2u : 4u;      // IN: UMMA layout type (SW128 / SW64)
   static constexpr int NKC = K / KC;
   static constexpr int P = KC / 8;         // 16-byte planes per chunk
   static constexpr int RA = MODE == kMid ? kMaxRows : 128;
@@ -112,17 +117,14 @@ struct WCfg {
   static constexpr int ITEMS = (128 * P + kAThreads - 1) / kAThreads;  // IN transform pieces per thread
 };
 
-// IN transform piece i of a chunk (128 rows x P planes): consecutive thread PAIRS take
-// consecutive rows, the two threads of a pair two adjacent planes, so a warp touches 16
-// rows of 2 planes — conflict-free smem.
-__device__ __forceinline__ void item_rk(int i, int& r, int& k8) {
-  const int q = i >> 1;
-  r = q & 127;
-  k8 = 2 * (q >> 7) + (i & 1);
-}
+// Stacks S1 / S2 are stored PLANE-MAJOR: plane k (channels 8k..8k+7) of row r at
+// (k * rows_alloc + r) * 16 bytes, so a tile's plane is one contiguous run (a 1-D bulk
+// copy) and the epilogues' row-per-lane stores are coalesced.  rows_alloc carries
+// kStackPad spare rows so MID's over-reading last tile stays inside the allocation.
+constexpr int kStackPad = 256;
 
 struct __align__(64) WArgs {
-  CUtensorMap tmap;          // A operand: IN x (C, W, H, N) | MID S1 (m, rows) | OUT S2 (m, rows)
+  CUtensorMap tmap;          // IN: x as (C, W, H, N), swizzled KC-channel boxes
   __nv_bfloat16* dst;        // IN: S1   MID: S2    OUT: out
   const uint8_t* wpk;        // this GEMM's packed weight chunks
   const float* par;          // this GEMM's parameter vectors
@@ -133,11 +135,14 @@ struct __align__(64) WArgs {
   int hb, S, G;              // IN: window rows per slab, slabs per block, slabs per tile
   int slab_rows;             // IN: tile rows per slab (hb*b rounded to 8: 128-B aligned TMA boxes)
   int box_rows;              // MID: rows per A box (128 + 2b + 2, rounded to 8)
+  const uint8_t* stack;      // MID / OUT: plane-major source stack
+  long src_rows;             // MID / OUT: rows_alloc of the source stack (plane stride / 16)
+  long dst_rows;             // IN / MID: rows_alloc of the destination stack
   unsigned long long* trace; // diagnostics: CTA 0 event stamps (sbn_debug_set_trace)
 };
 
 // CTA 0 event log (diagnostics): slot ev*64 + tile, tiles < 64
-enum { kEvPub = 0, kEvMma = 1, kEvAcc = 2, kEvEpi = 3, kEvIss = 4, kEvLoad = 5 };
+enum { kEvPub = 0, kEvMma = 1, kEvAcc = 2, kEvEpi = 3, kEvIss = 4, kEvLoad = 5, kEvCIss = 7, kEvCData = 8, kEvCPub = 11 };
 __device__ __forceinline__ void wtrace(const WArgs& a, int ev, int t) {
   if (a.trace && blockIdx.x == 0 && t < 64) {
     a.trace[ev * 64 + t] = gtimer();
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
     }
     tc::mbar_fence_init();
   }
-  if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
+  if (MODE == kIn && tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
   for (int i = tid; i < Q::NPAR; i += kWideThreads) par[i] = a.par[i];
   if (warp == 0) tc::tmem_alloc<Q::TALLOC>(&tslot);
   tc::fence_before();
@@ -223,53 +228,54 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   if (tid < kAThreads) {
     // ------------------------------------------------ IN: BN1 + ReLU on landed chunks
     if (MODE == kIn) {
-      const float* s1 = par;
-      const float* t1 = par + K;
+      // one 16-B piece per item: consecutive threads walk the pieces of consecutive rows
+      // (conflict-free); the piece in physical slot q of row r holds channel group
+      // q ^ swizzle(r) of the chunk
+      const float* s1 = par;  // packed sign / shift pairs (see unit_wide_pack_kernel)
+      constexpr int PR = Q::ROWB / 16;  // pieces per row
       int c = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
         for (int kc = 0; kc < Q::NKC; ++kc, ++c) {
           const int s = c % Q::SA;
           tc::mbar_wait(&a_load[s], (c / Q::SA) & 1);
+          if (tid == 0) wtrace(a, kEvCData, c);
           uint8_t* A = Aring + s * Q::ACH;
           uint4 raw[Q::ITEMS];
-          uint32_t sa_[Q::ITEMS];
 #pragma unroll
           for (int j = 0; j < Q::ITEMS; ++j) {
             const int i = tid + j * kAThreads;
-            int r, k8;
-            item_rk(i, r, k8);
-            sa_[j] = tc::smem_u32(A + k8 * Q::PA + r * 16);
-            if (i < 128 * Q::P)
+            if (i < 128 * PR)
               asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                            : "=r"(raw[j].x), "=r"(raw[j].y), "=r"(raw[j].z), "=r"(raw[j].w)
-                           : "r"(sa_[j]));
+                           : "r"(tc::smem_u32(A + i * 16)));
           }
 #pragma unroll
           for (int j = 0; j < Q::ITEMS; ++j) {
             const int i = tid + j * kAThreads;
-            if (i >= 128 * Q::P) break;
-            int r, k8;
-            item_rk(i, r, k8);
-            const float4* sv = reinterpret_cast<const float4*>(s1 + kc * Q::KC + k8 * 8);
-            const float4* tv = reinterpret_cast<const float4*>(t1 + kc * Q::KC + k8 * 8);
-            const float4 sa = sv[0], sb = sv[1], ta = tv[0], tb = tv[1];
-            const float sc[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
-            const float sh[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
+            if (i >= 128 * PR) break;
+            const int r = i / PR, qp = i % PR;
+            const int grp = qp ^ (Q::KC == 64 ? (r & 7) : ((r >> 1) & 3));
+            // relu(sgn * x + v) in packed bf16 (|s1| lives in W1)
+            const uint4 sg4 = *reinterpret_cast<const uint4*>(s1 + (kc * Q::KC + grp * 8) / 2);
+            const uint4 vv4 = *reinterpret_cast<const uint4*>(s1 + K / 2 + (kc * Q::KC + grp * 8) / 2);
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[j]);
+            const __nv_bfloat162* hs = reinterpret_cast<const __nv_bfloat162*>(&sg4);
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&vv4);
+            const __nv_bfloat162 z2 = __float2bfloat162_rn(0.f);
             uint32_t o[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h[e]);
-              o[e] = tc::pack_bf16(fmaxf(fmaf(f.x, sc[2 * e], sh[2 * e]), 0.f),
-                                   fmaxf(fmaf(f.y, sc[2 * e + 1], sh[2 * e + 1]), 0.f));
+              const __nv_bfloat162 y = __hmax2(__hfma2(h[e], hs[e], hv[e]), z2);
+              o[e] = *reinterpret_cast<const uint32_t*>(&y);
             }
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sa_[j]), "r"(o[0]), "r"(o[1]),
-                         "r"(o[2]), "r"(o[3])
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(A + i * 16)), "r"(o[0]),
+                         "r"(o[1]), "r"(o[2]), "r"(o[3])
                          : "memory");
           }
           tc::fence_async_smem();
           tc::mbar_arrive(&a_full[s]);
           if (tid == 0 && kc == Q::NKC - 1) wtrace(a, kEvPub, c / Q::NKC);
+          if (tid == 0) wtrace(a, kEvCPub, c);
         }
     }
   } else if (tid < kAThreads + kEThreads) {
@@ -306,7 +312,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       }
     };
     bool store = false, valid = true;
-    __nv_bfloat16* dp = a.dst;
+    __nv_bfloat16* dp = a.dst;   // OUT: the output pixel row
+    long drow = 0;               // IN / MID: destination row of the plane-major stack
     uint4 res[PG > 0 ? 2 * PG : 1];
     auto meta = [&](int tile) {
       const long gr = (long)tile * 128 + r;
@@ -323,12 +330,12 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
         store = i < a.G && sl < B * a.S && rr < a.hb * b && wy < b;
         const int y = g.oy + xby * g.sy + wy, x = g.ox + xbx * g.sx + wx;
         valid = y >= 0 && y < g.h && x >= 0 && x < g.w;
-        dp = a.dst + ((long)j * bb + wy * b + wx) * N;
+        drow = (long)j * bb + wy * b + wx;
       } else if (MODE == kMid) {
         const int j = (int)(gr / bb), p = (int)(gr - (long)j * bb);
         const int oy = p / b, ox = p % b;
         store = oy < ob && ox < ob;
-        dp = a.dst + ((long)j * ob * ob + oy * ob + ox) * N;
+        drow = (long)j * ob * ob + oy * ob + ox;
       } else {
         const int j = (int)(gr / (ob * ob)), p = (int)(gr - (long)j * ob * ob);
         const int oy = p / ob, ox = p % ob;
@@ -395,9 +402,15 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             o[q + 1] = valid ? tc::pack_bf16(u2, u3) : 0u;
           }
         }
-        uint4* op = reinterpret_cast<uint4*>(dp + c0);
-        op[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        op[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        if (MODE == kOut) {
+          uint4* op = reinterpret_cast<uint4*>(dp + c0);
+          op[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          op[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {  // plane-major stack: lanes hold consecutive rows -> coalesced 16-B stores
+          uint4* pl = reinterpret_cast<uint4*>(a.dst) + (long)(c0 / 8) * a.dst_rows + drow;
+          pl[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          pl[a.dst_rows] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
       }
       tc::fence_before();
       tc::mbar_arrive(&acc_empty[buf]);
@@ -441,24 +454,27 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           tc::mbar_wait(&a_empty[s], ((c / Q::SA) & 1) ^ 1);
           uint8_t* A = Aring + s * Q::ACH;
           uint64_t* bar = MODE == kIn ? &a_load[s] : &a_full[s];
+          wtrace(a, kEvCIss, c);
           if (MODE == kIn) {
             int boxes = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) boxes += cj[i] >= 0;
-            tc::mbar_expect_tx(bar, (uint32_t)(boxes * Q::P * 16 * b * a.hb));
+            tc::mbar_expect_tx(bar, (uint32_t)(boxes * Q::ROWB * b * a.hb));
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               if (cj[i] < 0) continue;
               const int q = cj[i] - (cj[i] / a.S) * a.S;
               const int x0 = g.ox + cbx[i] * g.sx, y0 = g.oy + cby[i] * g.sy + q * a.hb;
-              for (int k8 = 0; k8 < Q::P; ++k8)
-                tma_4d(A + k8 * Q::PA + i * a.slab_rows * 16, &a.tmap, kc * Q::KC + 8 * k8, x0, y0, cn[i], bar);
+              // one box of (KC ch, b, hb rows) lands as swizzled KC-channel rows
+              tma_4d(A + i * a.slab_rows * Q::ROWB, &a.tmap, kc * Q::KC, x0, y0, cn[i], bar);
             }
           } else {
             const int rows = MODE == kMid ? a.box_rows : 128;
             tc::mbar_expect_tx(bar, (uint32_t)(Q::P * 16 * rows));
             for (int k8 = 0; k8 < Q::P; ++k8)
-              tma_2d(A + k8 * Q::PA, &a.tmap, kc * Q::KC + 8 * k8, tile * 128, bar);
+              tc::bulk_g2s(A + k8 * Q::PA,
+                           a.stack + ((long)(kc * Q::P + k8) * a.src_rows + (long)tile * 128) * 16,
+                           (uint32_t)(rows * 16), bar);
           }
           if (!Q::RES) {  // streamed weights: this chunk's taps
             for (int tap = 0; tap < Q::TAPS; ++tap, ++wit) {
@@ -505,7 +521,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
 #pragma unroll
               for (int h = 0; h < Q::NSPLIT; ++h)
                 tc::mma_bf16(acc + h * Q::NS,
-                             tc::desc_kmajor_noswz(abase + 2 * kk * Q::PA + shift * 16, Q::PA, 128),
+                             MODE == kIn ? tc::desc_kmajor_swz(abase + kk * 32, 8 * Q::ROWB, Q::SWZ)
+                                         : tc::desc_kmajor_noswz(abase + 2 * kk * Q::PA + shift * 16, Q::PA, 128),
                              tc::desc_kmajor_noswz(wbase + 2 * kk * Q::PW + h * Q::NS * 16, Q::PW, 128),
                              idesc, (kc | tap | kk) > 0);
             if (!Q::RES) tc::mma_commit(&w_empty[sw]);
@@ -528,7 +545,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
 // A chunk c of a GEMM with K-chunk KC, N columns: KC/8 planes of N rows x 16 B,
 // element (n, k) at (k/8)*N*16 + n*16 + (k%8)*2 — the kernel's B-operand layout.  MID
 // chunks are ordered (kc, tap).
-//   params (floats): IN  s1 t1 [c] b1 s2 t2' [m]   MID b2 s3 t3' [m]   OUT b3 [c]
+//   params (floats): IN  sgn|v (bf16x2) t1 [c] b1 s2 t2' [m]   MID b2 s3 t3' [m]   OUT b3 [c]
 //   (t2' = b1*s2 + t2, t3' = b2*s3 + t3: the conv bias folded into the next BN)
 struct WLayout {
   size_t w1, w2, w3, p1, p2, p3, total;
@@ -562,11 +579,16 @@ __global__ void unit_wide_pack_kernel(sbn_unit_params p, uint8_t* __restrict__ i
   const __nv_bfloat16* w3 = (const __nv_bfloat16*)p.w3;
   const int stride = gridDim.x * blockDim.x;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
-  // W1 (1, 1, C, M): B[n = co][k = ci]
+  // BN1 + ReLU is applied in packed bf16 as relu(sgn*x + v) with the per-channel scale
+  // |s1| folded into W1's rows: relu(x*s1 + t1) = |s1| * relu(sgn(s1)*x + t1/|s1|).
+  const float* s1v = (const float*)p.bn1_scale;
+  const float* t1v = (const float*)p.bn1_shift;
+  // W1 (1, 1, C, M): B[n = co][k = ci] = W1[ci, co] * |s1[ci]|
   for (int i = t0; i < C * M; i += stride) {
     const int ci = i / M, co = i % M;
     const int kc = ci / Q1::KC, k = ci % Q1::KC;
-    *reinterpret_cast<__nv_bfloat16*>(img + L.w1 + (size_t)kc * Q1::WCH + (k / 8) * Q1::PW + co * 16 + (k % 8) * 2) = w1[i];
+    *reinterpret_cast<__nv_bfloat16*>(img + L.w1 + (size_t)kc * Q1::WCH + (k / 8) * Q1::PW + co * 16 + (k % 8) * 2) =
+        __float2bfloat16_rn(__bfloat162float(w1[i]) * fabsf(s1v[ci]));
   }
   // W2 (3, 3, M, M): chunk (kc, tap)
   for (int i = t0; i < 9 * M * M; i += stride) {
@@ -584,16 +606,25 @@ __global__ void unit_wide_pack_kernel(sbn_unit_params p, uint8_t* __restrict__ i
   float* p2 = reinterpret_cast<float*>(img + L.p2);
   float* p3 = reinterpret_cast<float*>(img + L.p3);
   auto bf = [](const void* q, int i) { return __bfloat162float(((const __nv_bfloat16*)q)[i]); };
+  // IN params: words [0, C/2) sign pairs, [C/2, C) v = t1/|s1| pairs (bf16x2); [C, 2C) t1
+  __nv_bfloat16* sg = reinterpret_cast<__nv_bfloat16*>(p1);
+  __nv_bfloat16* vv = reinterpret_cast<__nv_bfloat16*>(p1 + C / 2);
   for (int i = t0; i < C; i += stride) {
-    p1[i] = ((const float*)p.bn1_scale)[i];
-    p1[C + i] = ((const float*)p.bn1_shift)[i];
+    const float a = fabsf(s1v[i]);
+    sg[i] = __float2bfloat16_rn(s1v[i] < 0.f ? -1.f : 1.f);
+    vv[i] = __float2bfloat16_rn(a > 0.f ? t1v[i] / a : 0.f);
+    p1[C + i] = t1v[i];
     p3[i] = bf(p.b3, i);
   }
   for (int i = t0; i < M; i += stride) {  // conv bias folded into the following BN shift
     const float s2 = ((const float*)p.bn2_scale)[i], s3 = ((const float*)p.bn3_scale)[i];
+    // channels with s1 == 0 contribute the constant relu(t1) * W1 (their W1 rows are zero)
+    float extra = 0.f;
+    for (int c = 0; c < C; ++c)
+      if (s1v[c] == 0.f) extra += fmaxf(t1v[c], 0.f) * __bfloat162float(w1[c * M + i]);
     p1[2 * C + i] = bf(p.b1, i);
     p1[2 * C + M + i] = s2;
-    p1[2 * C + 2 * M + i] = fmaf(bf(p.b1, i), s2, ((const float*)p.bn2_shift)[i]);
+    p1[2 * C + 2 * M + i] = fmaf(bf(p.b1, i) + extra, s2, ((const float*)p.bn2_shift)[i]);
     p2[i] = bf(p.b2, i);
     p2[M + i] = s3;
     p2[2 * M + i] = fmaf(bf(p.b2, i), s3, ((const float*)p.bn3_shift)[i]);
@@ -620,9 +651,9 @@ int launch_wide(const WArgs& a, long max_tiles, cudaStream_t s, const char* what
 }
 
 // TMA descriptor over a bf16 tensor: dims/strides innermost first (strides in bytes, for
-// dims 1..rank-1), box in elements, no swizzle, out-of-bounds elements read as zero.
+// dims 1..rank-1), box in elements, out-of-bounds elements read as zero.
 int encode_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-               const uint32_t* box) {
+               const uint32_t* box, CUtensorMapSwizzle swz) {
   // resolved through the runtime (no link-time libcuda dependency: the library must load
   // on GPU-less build hosts)
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -642,7 +673,7 @@ int encode_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
   uint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base),
                                             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -672,47 +703,41 @@ int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const i
   const int tsel = (debug_flags() >> 3) & 3;
   unsigned long long* tb = trace_buffer();
   a.trace = tsel == 0 ? tb : nullptr;
-  const long rows1 = (long)cap * b * b, rows2 = (long)cap * (b - 2) * (b - 2);
-  // IN: x windows -> S1
+  const long rows1 = (long)cap * b * b + kStackPad, rows2 = (long)cap * (b - 2) * (b - 2) + kStackPad;
+  // IN: x windows -> S1 (4-D map, box = KC channels x b x hb rows, swizzled rows)
   {
+    using Q = WCfg<C, M, kIn>;
     const uint64_t dims[4] = {(uint64_t)C, (uint64_t)g.w, (uint64_t)g.h, (uint64_t)g.n};
     const uint64_t str[3] = {(uint64_t)C * 2, (uint64_t)g.w * C * 2, (uint64_t)g.h * g.w * C * 2};
-    const uint32_t box[4] = {8, (uint32_t)b, (uint32_t)a.hb, 1};
-    int st = encode_map(&a.tmap, x, 4, dims, str, box);
+    const uint32_t box[4] = {(uint32_t)Q::KC, (uint32_t)b, (uint32_t)a.hb, 1};
+    int st = encode_map(&a.tmap, x, 4, dims, str, box,
+                        Q::KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (st) return st;
   }
   a.dst = (__nv_bfloat16*)s1;
+  a.dst_rows = rows1;
   a.wpk = img + L.w1;
   a.par = (const float*)(img + L.p1);
   int st = launch_wide<C, M, kIn>(a, ((long)cap * a.S + a.G - 1) / a.G, s, "residual_unit_wide_in");
   if (st) return st;
-  // MID: S1 -> S2 (3x3 valid)
-  {
-    const uint64_t dims[2] = {(uint64_t)M, (uint64_t)rows1};
-    const uint64_t str[1] = {(uint64_t)M * 2};
-    const uint32_t box[2] = {8, (uint32_t)a.box_rows};
-    st = encode_map(&a.tmap, s1, 2, dims, str, box);
-    if (st) return st;
-  }
+  // MID: S1 -> S2 (3x3 valid); plane runs by 1-D bulk copies
+  a.stack = s1;
+  a.src_rows = rows1;
   a.dst = (__nv_bfloat16*)s2;
+  a.dst_rows = rows2;
   a.wpk = img + L.w2;
   a.par = (const float*)(img + L.p2);
   a.trace = tsel == 1 ? tb : nullptr;
-  st = launch_wide<M, M, kMid>(a, (rows1 + 127) / 128, s, "residual_unit_wide_mid");
+  st = launch_wide<M, M, kMid>(a, ((long)cap * b * b + 127) / 128, s, "residual_unit_wide_mid");
   if (st) return st;
   // OUT: S2 -> out (+ residual), in place or into the clone
-  {
-    const uint64_t dims[2] = {(uint64_t)M, (uint64_t)rows2};
-    const uint64_t str[1] = {(uint64_t)M * 2};
-    const uint32_t box[2] = {8, 128};
-    st = encode_map(&a.tmap, s2, 2, dims, str, box);
-    if (st) return st;
-  }
+  a.stack = s2;
+  a.src_rows = rows2;
   a.dst = (__nv_bfloat16*)out;
   a.wpk = img + L.w3;
   a.par = (const float*)(img + L.p3);
   a.trace = tsel == 2 ? tb : nullptr;
-  return launch_wide<M, C, kOut>(a, (rows2 + 127) / 128, s, "residual_unit_wide_out");
+  return launch_wide<M, C, kOut>(a, ((long)cap * (b - 2) * (b - 2) + 127) / 128, s, "residual_unit_wide_out");
 }
 
 // (c, m) instantiations: BASELINE config-4 stages (m = c/2) and the small unit shapes
@@ -750,13 +775,16 @@ size_t unit_wide_packed_bytes(int c, int m) {
   return 0;
 }
 
-size_t unit_wide_stack_bytes(int m, const Geo& g) {
-  const size_t cap = (size_t)g.n * g.gy * g.gx;
-  const size_t b = g.bh;
-  const size_t s1 = (cap * b * b * m * 2 + 255) / 256 * 256;
-  const size_t s2 = (cap * (b - 2) * (b - 2) * m * 2 + 255) / 256 * 256;
-  return s1 + s2;
+static size_t stack1_bytes(int m, const Geo& g) {
+  const size_t cap = (size_t)g.n * g.gy * g.gx, b = g.bh;
+  return ((cap * b * b + kStackPad) * m * 2 + 255) / 256 * 256;
 }
+static size_t stack2_bytes(int m, const Geo& g) {
+  const size_t cap = (size_t)g.n * g.gy * g.gx, b = g.bh;
+  return ((cap * (b - 2) * (b - 2) + kStackPad) * m * 2 + 255) / 256 * 256;
+}
+
+size_t unit_wide_stack_bytes(int m, const Geo& g) { return stack1_bytes(m, g) + stack2_bytes(m, g); }
 
 int unit_wide_pack(const sbn_unit_params* p, int c, int m, void* img, cudaStream_t s) {
 #define X(C_, M_)                                                                        \
@@ -774,8 +802,7 @@ int unit_wide_pack(const sbn_unit_params* p, int c, int m, void* img, cudaStream
 int unit_wide_launch(const void* x, void* out, int c, int m, const Geo& g, const void* packed,
                      const int32_t* idx, const int32_t* count, int cap, void* stacks, cudaStream_t s) {
   uint8_t* s1 = (uint8_t*)stacks;
-  const size_t b = g.bh;
-  uint8_t* s2 = s1 + ((size_t)cap * b * b * m * 2 + 255) / 256 * 256;
+  uint8_t* s2 = s1 + stack1_bytes(m, g);
 #define X(C_, M_) \
   if (c == C_ && m == M_) return run_wide<C_, M_>(x, out, g, (const uint8_t*)packed, idx, count, cap, s1, s2, s);
   SBN_UNIT_WIDE_CONFIGS(X)
