@@ -53,7 +53,7 @@ constexpr int kMaxRows = 168;  // staged rows of a MID tile: 128 + 2*b + 2 (b <=
 
 enum { kIn = 1, kMid = 2, kOut = 3 };
 
-constexpr int kBudget = 210 * 1024;
+constexpr int kBudget = 216 * 1024;
 
 // K-chunk choice: the largest of {K (<= 96), 64, 32, 16} that keeps ALL weight chunks
 // resident in shared memory next to a 3-deep A ring; 0 when no chunking does (weights
@@ -71,7 +71,8 @@ constexpr int resident_kc() {
     const int kc = cands[i];
     if (kc > pref || K % kc != 0 || kc % 16 != 0 || (MODE == kIn && kc != 64 && kc != 32)) continue;
     const long ach = (long)(kc / 8) * ra * 16;
-    if (3 * ach + wbytes + 8192 <= kBudget) return kc;
+    const long stg = MODE == kOut ? 128L * ((N <= 192 ? N : 128) * 2 + 16) : 0;
+    if (2 * ach + wbytes + 8192 + stg <= kBudget) return kc;
   }
   return 0;
 }
@@ -103,17 +104,24 @@ struct WCfg {
   static constexpr int NPAR = MODE == kIn ? 2 * K + 3 * N : MODE == kMid ? 3 * N : N;
   static constexpr int al(int v) { return (v + 127) / 128 * 128; }
   static constexpr int PARB = al(NPAR * 4);
+  // OUT: the epilogue stages bf16(acc + b3) for GS columns at a time, then copies whole
+  // pixel rows with the residual add (coalesced 16-B lanes along each row)
+  static constexpr int GS = MODE != kOut ? 0 : (N <= 192 ? N : 128);
+  static constexpr int SPITCH = GS * 2 + 16;
+  static constexpr int STGB = MODE == kOut ? 128 * SPITCH : 0;
   static constexpr int CHUNKS = NKC * TAPS;                       // weight chunks per tile
   static constexpr size_t WBYTES = (size_t)CHUNKS * WCH;          // packed weight bytes
   // resident: A ring as deep as fits (<= 6); streamed: A ring 2..4, W ring 2..4
-  static constexpr int SA = RES ? ((int)((kBudget - (long)WBYTES - PARB) / ACH) > 6 ? 6 : (int)((kBudget - (long)WBYTES - PARB) / ACH))
-                                : (4 * ACH + 2 * WCH + PARB <= kBudget) ? 4 : (3 * ACH + 2 * WCH + PARB <= kBudget) ? 3 : 2;
-  static constexpr int SW = RES ? 0 : (SA * ACH + 4 * WCH + PARB <= kBudget) ? 4 : (SA * ACH + 3 * WCH + PARB <= kBudget) ? 3 : 2;
+  static constexpr int BUD = kBudget - STGB;
+  static constexpr int SA = RES ? ((int)((BUD - (long)WBYTES - PARB) / ACH) > 6 ? 6 : (int)((BUD - (long)WBYTES - PARB) / ACH))
+                                : (4 * ACH + 2 * WCH + PARB <= BUD) ? 4 : (3 * ACH + 2 * WCH + PARB <= BUD) ? 3 : 2;
+  static constexpr int SW = RES ? 0 : (SA * ACH + 4 * WCH + PARB <= BUD) ? 4 : (SA * ACH + 3 * WCH + PARB <= BUD) ? 3 : 2;
   static constexpr long WREG = RES ? (long)WBYTES : (long)SW * WCH;
-  static_assert(SA >= 2 && SA * ACH + WREG + PARB <= kBudget, "shared memory budget");
+  static_assert(SA >= 2 && SA * ACH + WREG + PARB <= BUD, "shared memory budget");
   static constexpr int OFF_W = SA * ACH;
   static constexpr int OFF_PAR = OFF_W + (int)WREG;
-  static constexpr int SMEM = OFF_PAR + PARB;
+  static constexpr int OFF_STG = OFF_PAR + PARB;
+  static constexpr int SMEM = OFF_STG + STGB;
   static constexpr int ITEMS = (128 * P + kAThreads - 1) / kAThreads;  // IN transform pieces per thread
 };
 
@@ -182,6 +190,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   __shared__ uint64_t a_load[Q::SA], a_full[Q::SA], a_empty[Q::SA], w_full[SWB], w_empty[SWB];
   __shared__ uint64_t acc_full[Q::NACC], acc_empty[Q::NACC];
   __shared__ uint32_t tslot;
+  __shared__ long long rowdst[MODE == kOut ? 128 : 1];  // OUT: element offset of a row's pixel, -1 skip
   uint8_t* Aring = smem;
   uint8_t* Wring = smem + Q::OFF_W;
   float* par = reinterpret_cast<float*>(smem + Q::OFF_PAR);
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
     const long TR = MODE == kOut ? (long)B * ob * ob : (long)B * bb;
     constexpr int NCH = N / 16;                 // 16-column chunks
     constexpr int MYCH = (NCH + 1) / 2;         // chunks of this half (upper bound)
-    constexpr int PG = MODE == kOut ? (MYCH < 6 ? MYCH : 6) : 0;  // residual chunks prefetched a tile ahead
+    constexpr int PG = 0;  // (OUT reads its residual in the staged copy phase)
     const float* sc = MODE == kIn ? par + 2 * K + N : par + N;  // IN: s2 | MID: s3
     const float* sh = sc + N;                                     // t2' | t3'
     // per-row metadata of a tile; the block-index loads (IN, OUT) are issued one tile
@@ -363,6 +372,77 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       tc::mbar_wait(&acc_full[buf], use & 1);
       tc::fence_after();
       if (ew == 0 && lane == 0) wtrace(a, kEvAcc, k);
+      if constexpr (MODE == kOut) {
+        // staged OUT epilogue: phase 1 writes bf16(acc + b3) of GS columns of this row to
+        // smem; phase 2 walks (row, 16-B chunk) items so consecutive lanes cover one pixel
+        // row: residual loads and stores are coalesced 16-B vectors
+        constexpr int GS = Q::GS, CHR = GS * 2 / 16;
+        constexpr int IT2 = (128 * CHR + kEThreads - 1) / kEThreads;
+        static_assert(N % GS == 0, "staging groups");
+        uint8_t* stg = smem + Q::OFF_STG;
+        const int et = tid - kAThreads;
+        const float* b3 = par;
+        if (half == 0) rowdst[r] = store ? (long long)(dp - a.dst) : -1;
+        for (int g0 = 0; g0 < N; g0 += GS) {
+#pragma unroll
+          for (int e = 0; e < (GS / 16 + 1) / 2; ++e) {
+            const int cg = 16 * (2 * e + half);  // column inside the group
+            if (cg >= GS) break;                 // warp-uniform
+            float v[16];
+            tc::tmem_ld16(acc + g0 + cg, v);
+            uint32_t o[8];
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+              const float4 b4 = *reinterpret_cast<const float4*>(b3 + g0 + cg + 2 * q);
+              o[q] = tc::pack_bf16(v[2 * q] + b4.x, v[2 * q + 1] + b4.y);
+              o[q + 1] = tc::pack_bf16(v[2 * q + 2] + b4.z, v[2 * q + 3] + b4.w);
+            }
+            uint4* sp = reinterpret_cast<uint4*>(stg + r * Q::SPITCH + cg * 2);
+            sp[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            sp[1] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+          if (g0 + GS >= N) {  // TMEM fully drained: release the accumulator early
+            tc::fence_before();
+            tc::mbar_arrive(&acc_empty[buf]);
+          }
+          asm volatile("bar.sync 2, %0;" ::"n"(kEThreads) : "memory");
+          constexpr int BATCH = IT2 < 6 ? IT2 : 6;  // residual loads in flight per thread
+#pragma unroll 1
+          for (int jb = 0; jb < IT2; jb += BATCH) {
+          uint4 xr[BATCH];
+#pragma unroll
+          for (int jj = 0; jj < BATCH; ++jj) {
+            const int it = et + (jb + jj) * kEThreads;
+            const int row = it / CHR, ch = it % CHR;
+            const long long off = (jb + jj < IT2 && it < 128 * CHR) ? rowdst[row] : -1;
+            if (off >= 0) xr[jj] = reinterpret_cast<const uint4*>(a.dst + off + g0)[ch];
+          }
+#pragma unroll
+          for (int jj = 0; jj < BATCH; ++jj) {
+            const int j = jb + jj;
+            if (j >= IT2) break;
+            const int it = et + j * kEThreads;
+            const int row = it / CHR, ch = it % CHR;
+            const long long off = it < 128 * CHR ? rowdst[row] : -1;
+            if (off < 0) continue;
+            const uint4 sv = *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[jj]);
+            const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&sv);
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 xf = __bfloat1622float2(xh[q]), uf = __bfloat1622float2(uh[q]);
+              o[q] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
+            }
+            reinterpret_cast<uint4*>(a.dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+          }
+          asm volatile("bar.sync 2, %0;" ::"n"(kEThreads) : "memory");  // staging / rowdst reuse
+        }
+        if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
+        meta(tile + gridDim.x);
+        continue;
+      }
 #pragma unroll
       for (int e = 0; e < MYCH; ++e) {
         const int c0 = 16 * (2 * e + half);
