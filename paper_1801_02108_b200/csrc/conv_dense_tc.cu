@@ -1,0 +1,360 @@
+// tcgen05 / TMEM dense 3x3 convolution with any stride and the bias fused into the
+// epilogue (bf16 in/out, fp32 accumulate): the stage-transition projection of
+// `run_stage` (reference `layers.py:316-318`, a dense stride-s 3x3 conv + bias) for the
+// BASELINE config-4 backbone, which otherwise runs cuDNN plus a separate bias-add pass
+// over the whole output.
+//
+// Implicit GEMM without im2col: a tile is 8 x 16 output pixels (M = 128 rows).  For each
+// (K-chunk, tap) the A operand is ONE 4-D TMA box of x — (KC channels, 16*s, 8*s, 1)
+// with element strides (1, s, s, 1) at (kc*KC, s*ox0 + kx - pad, s*oy0 + ky - pad, n):
+// exactly the 128 input pixels the tap reads, zero-filled outside the image (= SAME /
+// VALID padding), landing as swizzled KC-channel rows (SWIZZLE_128B for KC=64, 64B for
+// KC=32).  B is the tap's (COUT x KC) weight chunk, pre-packed in the K-major plane
+// layout, resident in smem when all 9*CIN*COUT fit, streamed through a ring otherwise.
+//
+// Warp roles per persistent CTA (320 threads): warps 0-7 epilogue (TMEM lane quarter =
+// warp % 4, two warps per quarter split the columns; +bias -> bf16 staged in smem, then
+// copied out along whole output pixel rows, coalesced), warp 8 TMA / bulk loader, warp 9
+// MMA issuer.  Double-buffered accumulators when 2*COUT <= 512 columns.
+#include "tma_util.cuh"
+
+#include <cstring>
+
+namespace sbn {
+namespace {
+
+constexpr int kCE = 256;                 // epilogue threads
+constexpr int kCThreads = kCE + 64;
+constexpr int kCBudget = 214 * 1024;
+
+template <int CIN, int COUT>
+struct CCfg {
+  static constexpr int KC = CIN % 64 == 0 ? 64 : 32;
+  static_assert(CIN % KC == 0, "CIN must be a multiple of 32");
+  static constexpr int NKC = CIN / KC;
+  static constexpr int ROWB = KC * 2;
+  static constexpr uint32_t SWZ = KC == 64 ? 2u : 4u;
+  static constexpr int ACH = 128 * ROWB;
+  static constexpr int PW = COUT * 16;
+  static constexpr int WCH = (KC / 8) * PW;
+  static constexpr int CHUNKS = NKC * 9;
+  static constexpr long WBYTES = (long)CHUNKS * WCH;
+  static constexpr int NSPLIT = COUT > 256 ? 2 : 1;
+  static constexpr int NS = COUT / NSPLIT;
+  static_assert(COUT % NSPLIT == 0 && NS % 16 == 0 && NS <= 256, "UMMA N");
+  static constexpr int NACC = 2 * COUT <= 512 ? 2 : 1;
+  static constexpr int TCOLS = NACC * COUT;
+  static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+  static constexpr int GS = COUT <= 192 ? COUT : 128;  // staged columns per pass
+  static_assert(COUT % GS == 0, "staging groups");
+  static constexpr int SPITCH = GS * 2 + 16;
+  static constexpr int STGB = 128 * SPITCH;
+  static constexpr int PARB = (COUT * 4 + 127) / 128 * 128;
+  static constexpr bool RES = 3 * ACH + WBYTES + STGB + PARB <= kCBudget;
+  static constexpr int SA_R = (int)((kCBudget - WBYTES - STGB - PARB) / ACH);
+  static constexpr int SA = RES ? (SA_R > 6 ? 6 : SA_R) : 3;
+  static constexpr int SW = RES ? 0 : ((SA * ACH + 4 * WCH + STGB + PARB <= kCBudget) ? 4 : (SA * ACH + 3 * WCH + STGB + PARB <= kCBudget) ? 3 : 2);
+  static constexpr long WREG = RES ? WBYTES : (long)SW * WCH;
+  static_assert(SA >= 2 && SA * ACH + WREG + STGB + PARB <= kCBudget, "shared memory budget");
+  static constexpr int OFF_W = SA * ACH;
+  static constexpr int OFF_STG = OFF_W + (int)WREG;
+  static constexpr int OFF_PAR = OFF_STG + STGB;
+  static constexpr int SMEM = OFF_PAR + PARB;
+};
+
+struct __align__(64) CArgs {
+  CUtensorMap tmap;       // x as (C, W, H, N), box (KC, 16s, 8s, 1), element strides (1, s, s, 1)
+  __nv_bfloat16* out;     // (n, oh, ow, COUT)
+  const uint8_t* wpk;     // packed weight chunks (kc, tap)
+  const float* bias;      // COUT floats (zeros when the layer has none)
+  int n, oh, ow, sy, sx, py, px;
+  int tiles_y, tiles_x;
+};
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_constant__ CArgs a) {
+  using Q = CCfg<CIN, COUT>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int SWB = Q::SW > 0 ? Q::SW : 1;
+  __shared__ uint64_t a_full[Q::SA], a_empty[Q::SA], w_full[SWB], w_empty[SWB];
+  __shared__ uint64_t acc_full[Q::NACC], acc_empty[Q::NACC];
+  __shared__ uint32_t tslot;
+  __shared__ long long rowdst[128];
+  uint8_t* Aring = smem;
+  uint8_t* Wring = smem + Q::OFF_W;
+  uint8_t* stg = smem + Q::OFF_STG;
+  float* bias = reinterpret_cast<float*>(smem + Q::OFF_PAR);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kLWarp = kCE / 32, kMWarp = kLWarp + 1;
+
+  if (tid == 0) {
+    for (int s = 0; s < Q::SA; ++s) {
+      tc::mbar_init(&a_full[s], 1);
+      tc::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < SWB; ++s) {
+      tc::mbar_init(&w_full[s], 1);
+      tc::mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < Q::NACC; ++s) {
+      tc::mbar_init(&acc_full[s], 1);
+      tc::mbar_init(&acc_empty[s], kCE);
+    }
+    tc::mbar_fence_init();
+  }
+  if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
+  for (int i = tid; i < COUT; i += kCThreads) bias[i] = a.bias[i];
+  if (warp == 0) tc::tmem_alloc<Q::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_trigger();
+  if (Q::RES && tid == kLWarp * 32) {  // weights do not depend on the previous launch
+    tc::mbar_expect_tx(&w_full[0], (uint32_t)Q::WBYTES);
+    for (int c = 0; c < Q::CHUNKS; ++c)
+      tc::bulk_g2s(Wring + (size_t)c * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[0]);
+  }
+  tc::pdl_wait();
+  const int ntiles = a.n * a.tiles_y * a.tiles_x;
+
+  if (warp < kLWarp) {
+    // ------------------------------------------------ epilogue
+    const int qd = warp & 3, half = warp >> 2;
+    const int r = qd * 32 + lane;
+    constexpr int CHR = Q::GS * 2 / 16;
+    constexpr int IT2 = (128 * CHR + kCE - 1) / kCE;
+    constexpr int BATCH = IT2 < 8 ? IT2 : 8;
+    int k = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+      const int buf = Q::NACC == 2 ? (k & 1) : 0;
+      const int use = Q::NACC == 2 ? (k >> 1) : k;
+      const int tx = tile % a.tiles_x, ty = (tile / a.tiles_x) % a.tiles_y, n = tile / (a.tiles_x * a.tiles_y);
+      const int Y = ty * 8 + r / 16, X = tx * 16 + r % 16;
+      if (half == 0)
+        rowdst[r] = (Y < a.oh && X < a.ow) ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
+      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * COUT;
+      tc::mbar_wait(&acc_full[buf], use & 1);
+      tc::fence_after();
+      for (int g0 = 0; g0 < COUT; g0 += Q::GS) {
+#pragma unroll
+        for (int e = 0; e < (Q::GS / 16 + 1) / 2; ++e) {
+          const int cg = 16 * (2 * e + half);
+          if (cg >= Q::GS) break;  // warp-uniform
+          float v[16];
+          tc::tmem_ld16(acc + g0 + cg, v);
+          uint32_t o[8];
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias + g0 + cg + 2 * q);
+            o[q] = tc::pack_bf16(v[2 * q] + b4.x, v[2 * q + 1] + b4.y);
+            o[q + 1] = tc::pack_bf16(v[2 * q + 2] + b4.z, v[2 * q + 3] + b4.w);
+          }
+          uint4* sp = reinterpret_cast<uint4*>(stg + r * Q::SPITCH + cg * 2);
+          sp[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          sp[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+        if (g0 + Q::GS >= COUT) {  // accumulator drained: the next tile's MMAs may start
+          tc::fence_before();
+          tc::mbar_arrive(&acc_empty[buf]);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kCE) : "memory");
+        // copy out: consecutive threads take consecutive 16-B chunks of one output row
+#pragma unroll 1
+        for (int jb = 0; jb < IT2; jb += BATCH) {
+#pragma unroll
+          for (int jj = 0; jj < BATCH; ++jj) {
+            const int it = tid + (jb + jj) * kCE;
+            if (jb + jj >= IT2 || it >= 128 * CHR) break;
+            const int row = it / CHR, ch = it % CHR;
+            const long long off = rowdst[row];
+            if (off < 0) continue;
+            reinterpret_cast<uint4*>(a.out + off + g0)[ch] =
+                *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kCE) : "memory");  // staging / rowdst reuse
+      }
+    }
+  } else if (warp == kLWarp) {
+    // ------------------------------------------------ loader
+    if (lane == 0) {
+      int c = 0, wit = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tx = tile % a.tiles_x, ty = (tile / a.tiles_x) % a.tiles_y, n = tile / (a.tiles_x * a.tiles_y);
+        const int x0 = tx * 16 * a.sx - a.px, y0 = ty * 8 * a.sy - a.py;
+        for (int kc = 0; kc < Q::NKC; ++kc)
+          for (int tap = 0; tap < 9; ++tap, ++c) {
+            const int s = c % Q::SA;
+            tc::mbar_wait(&a_empty[s], ((c / Q::SA) & 1) ^ 1);
+            tc::mbar_expect_tx(&a_full[s], (uint32_t)Q::ACH);
+            tma_4d(Aring + s * Q::ACH, &a.tmap, kc * Q::KC, x0 + tap % 3, y0 + tap / 3, n, &a_full[s]);
+            if (!Q::RES) {
+              const int sw = wit % SWB;
+              tc::mbar_wait(&w_empty[sw], ((wit / SWB) & 1) ^ 1);
+              tc::mbar_expect_tx(&w_full[sw], Q::WCH);
+              tc::bulk_g2s(Wring + sw * Q::WCH, a.wpk + (size_t)(kc * 9 + tap) * Q::WCH, Q::WCH, &w_full[sw]);
+              ++wit;
+            }
+          }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, Q::NS);
+      if (Q::RES) tc::mbar_wait(&w_full[0], 0);
+      int c = 0, wit = 0, k = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int buf = Q::NACC == 2 ? (k & 1) : 0;
+        const int use = Q::NACC == 2 ? (k >> 1) : k;
+        tc::mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t acc = tmem + buf * COUT;
+        for (int kc = 0; kc < Q::NKC; ++kc)
+          for (int tap = 0; tap < 9; ++tap, ++c) {
+            const int s = c % Q::SA;
+            tc::mbar_wait(&a_full[s], (c / Q::SA) & 1);
+            const int sw = Q::RES ? 0 : wit % SWB;
+            if (!Q::RES) tc::mbar_wait(&w_full[sw], (wit / SWB) & 1);
+            tc::fence_after();
+            const uint32_t abase = tc::smem_u32(Aring + s * Q::ACH);
+            const uint32_t wbase = tc::smem_u32(Wring + (Q::RES ? (kc * 9 + tap) * Q::WCH : sw * Q::WCH));
+#pragma unroll
+            for (int kk = 0; kk < Q::KC / 16; ++kk)
+#pragma unroll
+              for (int h = 0; h < Q::NSPLIT; ++h)
+                tc::mma_bf16(acc + h * Q::NS, tc::desc_kmajor_swz(abase + kk * 32, 8 * Q::ROWB, Q::SWZ),
+                             tc::desc_kmajor_noswz(wbase + 2 * kk * Q::PW + h * Q::NS * 16, Q::PW, 128), idesc,
+                             (kc | tap | kk) > 0);
+            tc::mma_commit(&a_empty[s]);
+            if (!Q::RES) {
+              tc::mma_commit(&w_empty[sw]);
+              ++wit;
+            }
+          }
+        tc::mma_commit(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  }
+  if (Q::RES && tid == kLWarp * 32) tc::mbar_wait(&w_full[0], 0);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free<Q::TALLOC>(tmem);
+}
+
+// W (3, 3, CIN, COUT) HWIO -> chunks (kc, tap) of (COUT rows x KC) in the K-major plane layout
+template <int CIN, int COUT>
+__global__ void conv_dense_pack_kernel(const __nv_bfloat16* __restrict__ w, uint8_t* __restrict__ img) {
+  using Q = CCfg<CIN, COUT>;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 9 * CIN * COUT; i += gridDim.x * blockDim.x) {
+    const int tap = i / (CIN * COUT), rr = i % (CIN * COUT), ci = rr / COUT, co = rr % COUT;
+    const int kc = ci / Q::KC, kq = ci % Q::KC;
+    *reinterpret_cast<__nv_bfloat16*>(img + (size_t)(kc * 9 + tap) * Q::WCH + (kq / 8) * Q::PW + co * 16 +
+                                      (kq % 8) * 2) = w[i];
+  }
+}
+
+template <int CIN, int COUT>
+int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int px, int oh, int ow,
+                 const void* wpk, const float* bias, void* out, cudaStream_t s) {
+  using Q = CCfg<CIN, COUT>;
+  CArgs a;
+  memset(&a, 0, sizeof(a));
+  const uint64_t dims[4] = {(uint64_t)CIN, (uint64_t)w, (uint64_t)h, (uint64_t)n};
+  const uint64_t str[3] = {(uint64_t)CIN * 2, (uint64_t)w * CIN * 2, (uint64_t)h * w * CIN * 2};
+  const uint32_t box[4] = {(uint32_t)Q::KC, (uint32_t)(16 * sx), (uint32_t)(8 * sy), 1};
+  const uint32_t es[4] = {1, (uint32_t)sx, (uint32_t)sy, 1};
+  int st = encode_map(&a.tmap, x, 4, dims, str, box, Q::KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, es);
+  if (st) return st;
+  a.out = (__nv_bfloat16*)out;
+  a.wpk = (const uint8_t*)wpk;
+  a.bias = bias;
+  a.n = n;
+  a.oh = oh;
+  a.ow = ow;
+  a.sy = sy;
+  a.sx = sx;
+  a.py = py;
+  a.px = px;
+  a.tiles_y = (oh + 7) / 8;
+  a.tiles_x = (ow + 15) / 16;
+  const long tiles = (long)n * a.tiles_y * a.tiles_x;
+  auto kern = conv_dense_kernel<CIN, COUT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(tiles < sm_count() ? (tiles < 1 ? 1 : tiles) : sm_count()));
+  cfg.blockDim = dim3(kCThreads);
+  cfg.dynamicSmemBytes = Q::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+  return launch_status("dense_conv_tcgen05");
+}
+
+// (CIN, COUT): the config-4 stage projections and square shapes
+#define SBN_DENSE_CONV_CONFIGS(X) \
+  X(32, 96)                       \
+  X(96, 192)                      \
+  X(192, 256)                     \
+  X(256, 384)                     \
+  X(32, 32)                       \
+  X(64, 64)                       \
+  X(128, 128)
+
+}  // namespace
+
+}  // namespace sbn
+
+using namespace sbn;
+
+extern "C" int sbn_dense_conv_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw) {
+  if (dtype != SBN_BF16 || kh != 3 || kw != 3 || sh < 1 || sw < 1 || sh > 3 || sw > 3) return 0;
+#define X(CI, CO) if (cin == CI && cout == CO) return CCfg<CI, CO>::SMEM <= max_smem_optin() ? 1 : 0;
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  return 0;
+}
+
+extern "C" size_t sbn_dense_conv_packed_bytes(int cin, int cout) {
+#define X(CI, CO) if (cin == CI && cout == CO) return (size_t)CCfg<CI, CO>::WBYTES;
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  return 0;
+}
+
+extern "C" int sbn_dense_conv_pack(const void* w, int cin, int cout, void* packed, sbn_stream_t stream) {
+  SBN_CHECK_ARG(w && packed, SBN_ERR_INVALID, "null argument");
+#define X(CI, CO)                                                                                          \
+  if (cin == CI && cout == CO) {                                                                           \
+    conv_dense_pack_kernel<CI, CO><<<128, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)w,         \
+                                                                          (uint8_t*)packed);               \
+    return launch_status("dense_conv_pack");                                                              \
+  }
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 dense conv instantiation for cin=%d cout=%d", cin, cout);
+  return SBN_ERR_UNSUPPORTED;
+}
+
+extern "C" int sbn_dense_conv(const void* x, int n, int h, int w, int cin, int cout, int sh, int sw, int ph,
+                              int pw, int oh, int ow, const void* packed, const float* bias, void* out,
+                              sbn_stream_t stream) {
+  SBN_CHECK_ARG(x && packed && bias && out, SBN_ERR_INVALID, "null pointer argument");
+  SBN_CHECK_ARG(n > 0 && h > 0 && w > 0 && oh > 0 && ow > 0, SBN_ERR_SHAPE, "bad dims");
+  SBN_CHECK_ARG(sbn_dense_conv_supported(SBN_BF16, cin, cout, 3, 3, sh, sw), SBN_ERR_UNSUPPORTED,
+                "tcgen05 dense conv does not support cin=%d cout=%d stride (%d,%d)", cin, cout, sh, sw);
+  cudaStream_t s = (cudaStream_t)stream;
+#define X(CI, CO) \
+  if (cin == CI && cout == CO) return launch_dense<CI, CO>(x, n, h, w, sh, sw, ph, pw, oh, ow, packed, bias, out, s);
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  return SBN_ERR_UNSUPPORTED;
+}

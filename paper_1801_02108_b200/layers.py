@@ -21,7 +21,7 @@ from . import _lib
 from .blocks import GatheredBlocks, gather, gather_grad, in_bounds_map, scatter_grad
 from .errors import EmptyBlockListError, GeometryError, ShapeMismatchError, UnsupportedConfigError
 from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, bn_inference,
-                  conv_grads_nhwc, dense_conv_nhwc, exact_fp32)
+                  conv_grads_nhwc, dense_conv_nhwc, exact_fp32, projection_conv)
 from .tensor import Tensor4D, cuda, dtype_code
 from .tiling import (BinaryMask, BlockIndexList, BlockSpec, compute_block_spec, downsample_mask,
                      reduce_mask)
@@ -588,8 +588,7 @@ def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: b
     owned = False
     if stage.projection is not None:
         p = ConvParams((3, 3), (cfg.stride, cfg.stride), Padding.SAME, cfg.channels[2])
-        w, b = stage.projection.device_tensors(t.dtype, t.device)
-        t = dense_conv_nhwc(t, w, b, p.stride, p.pad)
+        t = projection_conv(t, stage.projection, p)
         owned = True
     if not sparse:
         for u in stage.units:

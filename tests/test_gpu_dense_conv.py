@@ -1,0 +1,34 @@
+"""tcgen05 dense 3x3 conv with fused bias (sbn_dense_conv): the config-4 stage projections
+(stride 2) and square stride-1 shapes vs cuDNN in fp32 on the same bf16-rounded inputs;
+bf16 output rounding -> rel_err <= 1e-2."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1801_02108_b200 as P
+from paper_1801_02108_b200.ops import projection_conv
+from oracle import sbnet_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,stride,same", [
+    (2, 50, 38, 32, 96, 2, True), (1, 37, 29, 96, 192, 2, True), (2, 22, 19, 192, 256, 2, True),
+    (1, 14, 12, 256, 384, 2, True), (1, 40, 33, 64, 64, 1, True), (2, 17, 35, 128, 128, 1, False),
+    (1, 24, 24, 32, 32, 3, True)])
+def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, same):
+    rng = np.random.default_rng(cin + cout + stride)
+    x = torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16().cuda()
+    wt = (rng.standard_normal((3, 3, cin, cout)) / np.sqrt(9 * cin)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    f = P.FilterBank(torch.from_numpy(wt).bfloat16(), torch.from_numpy(b).bfloat16())
+    p = P.ConvParams((3, 3), (stride, stride), P.Padding.SAME if same else P.Padding.VALID, cout)
+    lib = P._lib.load() if hasattr(P, "_lib") else None
+    from paper_1801_02108_b200 import _lib
+    assert _lib.load().sbn_dense_conv_supported(2, cin, cout, 3, 3, stride, stride) == 1
+    y = projection_conv(x, f, p).float().cpu().numpy()
+    fb32 = P.FilterBank(torch.from_numpy(wt).bfloat16().float(), torch.from_numpy(b).bfloat16().float())
+    ref = P.conv2d_direct(P.Tensor4D(x.float()), fb32, p).data.cpu().numpy()
+    assert y.shape == ref.shape
+    assert O.rel_err(y, ref) <= 1e-2
+    del lib
