@@ -266,19 +266,24 @@ def run_ours(args):
     except Exception:
         pass
 
-    # ---- dense comparator (cuDNN bf16, same frames, CUDA graph)
-    def dense_steps(k):
-        for i in range(k):
-            P.dense_residual_unit(P.Tensor4D(xs[i % nf]), u)
-
-    gd, sd = time_graph(torch, dense_steps, max(nf, args.steps // 10), 3, soak_s=0.2)
-    with torch.cuda.stream(sd):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(sd)
-        gd.replay()
-        e1.record(sd)
-        e1.synchronize()
-    dense_ms = e0.elapsed_time(e1) / max(nf, args.steps // 10)
+    # ---- dense comparators (same frames, CUDA graphs): (1) the reference's math in eager
+    #      torch on cuDNN — separate conv / BN / ReLU kernels, the paper's style of baseline;
+    #      (2) cuDNN at its best — BN folded into the convs, ReLU fused (cudnn_convolution_relu)
+    def dense_time(fused):
+        def dense_steps(k):
+            for i in range(k):
+                P.dense_residual_unit(P.Tensor4D(xs[i % nf]), u, fused=fused)
+        nd = max(nf, args.steps // 10)
+        gd, sd = time_graph(torch, dense_steps, nd, 3, soak_s=0.2)
+        with torch.cuda.stream(sd):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(sd)
+            gd.replay()
+            b_.record(sd)
+            b_.synchronize()
+        return a_.elapsed_time(b_) / nd
+    dense_ms = dense_time(False)
+    dense_fused_ms = dense_time(True)
 
     # ---- e2e: pinned HOST frame + mask -> public API (sparse_residual_unit, inplace=True on
     #      the host frame) -> host frame updated, every step.  The call moves the mask plus
@@ -390,7 +395,8 @@ def run_ours(args):
                 b_.synchronize()
             t_sp = a_.elapsed_time(b_) / 200
             sweep[f"{d:.1f}"] = {"density_achieved": round(float(mk.data.float().mean()), 4),
-                                 "sparse_ms": round(t_sp, 5), "speedup_vs_dense": round(dense_ms / t_sp, 3)}
+                                 "sparse_ms": round(t_sp, 5), "speedup_vs_dense": round(dense_ms / t_sp, 3),
+                                 "speedup_vs_dense_fused": round(dense_fused_ms / t_sp, 3)}
 
     # ---- config 3: single 3x3 conv, 800x700x128 bf16, top-left masks (paper protocol,
     #      PAPER.md:397-398), blocks 8/16, sparse (reduce_mask + tcgen05 fused conv into a
@@ -431,6 +437,10 @@ def run_ours(args):
                        "algo": algo, "parallelism": f"batch-shard x{world}", "cuda_graph": True},
             "ms_per_step_dense": round(dense_ms, 5),
             "speedup_vs_dense": round(dense_ms / ms_step, 3),
+            "dense": "eager cuDNN convs + separate BN/ReLU kernels (the reference's dense math, paper-style baseline)",
+            "ms_per_step_dense_fused": round(dense_fused_ms, 5),
+            "speedup_vs_dense_fused": round(dense_fused_ms / ms_step, 3),
+            "dense_fused": "cuDNN with BN folded into the convs and ReLU fused (cudnn_convolution_relu)",
             "e2e": {"value": round(world * 1e3 / e2e_ms, 2), "unit": UNIT,
                     "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "api": "sparse_residual_unit(Tensor4D(pinned host frame), pinned host mask, inplace=True)",
@@ -512,7 +522,9 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
     mask = P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False)
     xt = P.Tensor4D(x)
     res = P.run_backbone(bb, xt, mask)  # warm: weight images, scratch buffers
-    dres = P.run_backbone(bb, xt, mask, sparse=False) if dense else None
+    dres = P.run_backbone(bb, xt, mask, sparse=False, dense_fused=False) if dense else None
+    if dense:
+        P.run_backbone(bb, xt, mask, sparse=False, dense_fused=True)
     torch.cuda.synchronize()
 
     def timed(fn, n=reps):
@@ -532,7 +544,11 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
 
     def de(k):
         for _ in range(k):
-            P.run_backbone(bb, xt, mask, sparse=False)
+            P.run_backbone(bb, xt, mask, sparse=False, dense_fused=False)
+
+    def def_(k):
+        for _ in range(k):
+            P.run_backbone(bb, xt, mask, sparse=False, dense_fused=True)
     t_sp = timed(sp)
     f_sp = perf.flops_backbone(res, bb.stages, True)
     out = {"workload": f"config4: 4-stage sparse detector backbone, N={frames} x {hh}x{ww}x{cin} bf16, "
@@ -542,17 +558,22 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
            "tflops_alg_sparse": round(f_sp / (t_sp * 1e-3) / 1e12, 1),
            "density_achieved": round(float(mk.mean()), 4), "stages": []}
     if dense:
-        t_de = timed(de)
+        t_de, t_df = timed(de), timed(def_)
         f_de = perf.flops_backbone(dres, bb.stages, False)
         out.update({"dense_ms": round(t_de, 4), "frames_per_s_dense": round(frames / (t_de * 1e-3), 1),
                     "speedup_vs_dense": round(t_de / t_sp, 3),
-                    "tflops_alg_dense": round(f_de / (t_de * 1e-3) / 1e12, 1)})
+                    "tflops_alg_dense": round(f_de / (t_de * 1e-3) / 1e12, 1),
+                    "dense_fused_ms": round(t_df, 4), "speedup_vs_dense_fused": round(t_df / t_sp, 3),
+                    "dense_note": "dense = eager cuDNN convs + separate BN/ReLU; dense_fused = BN folded, ReLU "
+                                  "fused (cudnn_convolution_relu); both use the same tcgen05 projections"})
     if per_stage:
         inp = xt
         for i, (stg, r) in enumerate(zip(bb.stages, res)):
             m_i = stg.config.channels[1]
             t1 = timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask) for _ in range(k)])
-            t2 = (timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False) for _ in range(k)])
+            t2 = (timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False, dense_fused=False)
+                                                     for _ in range(k)]) if dense else float("nan"))
+            t3 = (timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False) for _ in range(k)])
                   if dense else float("nan"))
             n_, h_, w_, c_ = r.output.dims
             out["stages"].append({"stage": i + 2, "hw": [h_, w_], "c": c_, "m": m_i,
@@ -560,7 +581,8 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
                                   "blocks": int(r.indices.count),
                                   "density": round(float(r.mask.data.float().mean()), 4),
                                   "algo": residual_unit_algo(torch.bfloat16, stg.units[0], r.spec),
-                                  "sparse_ms": round(t1, 4), "dense_ms": round(t2, 4)})
+                                  "sparse_ms": round(t1, 4), "dense_ms": round(t2, 4),
+                                  "dense_fused_ms": round(t3, 4)})
             inp = r.output
     return out
 
@@ -649,11 +671,12 @@ def run_conv_sweep(P, torch, dev, time_graph):
             b_.synchronize()
         return a_.elapsed_time(b_) / reps
 
-    def dense(k):
+    def dense(k):  # cuDNN conv without the bias term: a lower bound for the dense layer
         for i in range(k):
-            dense_conv_nhwc(xs[i % nfr], wd, bd, (1, 1), (1, 1))
+            dense_conv_nhwc(xs[i % nfr], wd, None, (1, 1), (1, 1))
     dense_ms = timed(dense)
     res = {"workload": "config3: 3x3 SAME conv, N=1 800x700x128 bf16, top-left mask", "dense_ms": round(dense_ms, 5),
+           "dense": "cuDNN bf16 conv, channels-last, bias omitted (lower bound of the dense layer)",
            "flops_dense": 2 * Hc * Wc * 9 * Cc * Cc, "rows": []}
     for d in (0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 0.9, 1.0):
         mk = P.synth_mask_topleft((1, Hc, Wc), 1.0 - d).cuda()

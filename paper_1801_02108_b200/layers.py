@@ -355,6 +355,34 @@ def unit_spec(x_dims, block_size, halo: int = 1) -> BlockSpec:
     return compute_block_spec(x_dims, eff, block_size)
 
 
+def _dense_unit_bf16(t: torch.Tensor, u: "ResidualUnitParams") -> torch.Tensor:
+    """The dense comparator of the bf16 unit at cuDNN's best: BN2/BN3 folded into conv1/conv2
+    (per-output-channel weight scale + bias) with ReLU fused into the convolution
+    (cudnn_convolution_relu), BN1+ReLU as one addcmul + in-place relu, conv3 + bias, then
+    the residual add.  Same math as `_dense_branch` up to bf16 rounding."""
+    key = ("dense_fused", str(t.device))
+    if key not in u._cache:
+        def fold(fb, bn):
+            w, b = fb.device_tensors(torch.float32, t.device)
+            b = b if b is not None else torch.zeros(fb.c_out, device=t.device)
+            sc, sh = bn.folded(torch.float32, t.device)
+            wf = (w * sc).permute(3, 2, 0, 1).contiguous(memory_format=torch.channels_last).to(torch.bfloat16)
+            return wf, (b * sc + sh).to(torch.bfloat16)
+        s1, t1 = u.bn1.folded(torch.float32, t.device)
+        w1, b1 = fold(u.conv1, u.bn2)
+        w2, b2 = fold(u.conv2, u.bn3)
+        w3, b3 = u.conv3.device_tensors(torch.bfloat16, t.device)
+        w3 = w3.permute(3, 2, 0, 1).contiguous(memory_format=torch.channels_last)
+        u._cache[key] = (s1.to(torch.bfloat16), t1.to(torch.bfloat16), w1, b1, w2, b2, w3, b3)
+    s1, t1, w1, b1, w2, b2, w3, b3 = u._cache[key]
+    x = t.permute(0, 3, 1, 2)  # NCHW view of NHWC memory (channels_last)
+    a = torch.addcmul(t1.view(1, -1, 1, 1), x, s1.view(1, -1, 1, 1)).relu_()
+    c1 = torch.cudnn_convolution_relu(a, w1, b1, (1, 1), (0, 0), (1, 1), 1)
+    c2 = torch.cudnn_convolution_relu(c1, w2, b2, (1, 1), (1, 1), (1, 1), 1)
+    y = F.conv2d(c2, w3, b3)
+    return (x + y).permute(0, 2, 3, 1).contiguous()
+
+
 def _dense_branch(t: torch.Tensor, u: ResidualUnitParams) -> torch.Tensor:
     dt, dev = t.dtype, t.device
     w1, b1 = u.conv1.device_tensors(dt, dev)
@@ -371,7 +399,7 @@ def _dense_branch(t: torch.Tensor, u: ResidualUnitParams) -> torch.Tensor:
 
 
 def dense_residual_unit(x: Tensor4D, u: ResidualUnitParams,
-                        bn_mode: BnMode = BnMode.INFERENCE) -> Tensor4D:
+                        bn_mode: BnMode = BnMode.INFERENCE, fused: bool = True) -> Tensor4D:
     """Dense unit with SAME 3x3 (reference `layers.py:194-200`) on cuDNN: the dense
     comparator of the sparse unit."""
     if u.channels != x.dims[3]:
@@ -379,6 +407,8 @@ def dense_residual_unit(x: Tensor4D, u: ResidualUnitParams,
     if bn_mode is not BnMode.INFERENCE:
         raise UnsupportedConfigError("dense_residual_unit: inference-mode BN only")
     t = cuda(x.nhwc())
+    if fused and t.dtype == torch.bfloat16 and u.pre_activation:
+        return Tensor4D.from_nhwc(_dense_unit_bf16(t, u), x.layout)
     return Tensor4D.from_nhwc(t + _dense_branch(t, u), x.layout)
 
 
@@ -579,7 +609,7 @@ def build_stage(cfg: StageConfig, rng: np.random.Generator, dtype=np.float32,
 
 
 def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
-              bn_mode: BnMode = BnMode.INFERENCE, algo="auto") -> StageResult:
+              bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True) -> StageResult:
     """Dense stride-s projection (cuDNN), then residual units sharing ONE index list
     computed from the downsampled mask (reference `layers.py:311-329`).  The units run
     in place on the stage's private activation buffer (one clone at most)."""
@@ -592,7 +622,8 @@ def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: b
         owned = True
     if not sparse:
         for u in stage.units:
-            t = t + _dense_branch(t, u)
+            t = (_dense_unit_bf16(t, u) if (dense_fused and t.dtype == torch.bfloat16 and u.pre_activation)
+                 else t + _dense_branch(t, u))
         return StageResult(Tensor4D.from_nhwc(t, x.layout), None, None, None)
     mask = downsample_mask(base_mask, cfg.mask_scale)
     if mask.dims != tuple(t.shape[:3]):
@@ -622,10 +653,10 @@ def build_backbone(stage_cfgs, rng: np.random.Generator, dtype=np.float32,
 
 
 def run_backbone(bb: Backbone, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
-                 bn_mode: BnMode = BnMode.INFERENCE, algo="auto") -> list[StageResult]:
+                 bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True) -> list[StageResult]:
     results = []
     for stage in bb.stages:
-        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo)
+        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo, dense_fused)
         results.append(res)
         x = res.output
     return results

@@ -125,3 +125,18 @@ def test_wide_unit_block_sizes(cuda_device, block):
         lib.sbn_debug_set_flags(prev)
     ref = _oracle(x, u, mk, (block, block))
     assert O.rel_err(_np(y), ref) <= 2e-2
+
+
+def test_fused_dense_comparator_matches_reference_math(cuda_device):
+    """The bf16 dense comparator (folded BN + fused conv/ReLU) equals the dense unit of the
+    fp32 oracle within bf16 rounding."""
+    x, u, _ = _case(21, 1, 40, 36, 96, 48, 0.5)
+    y = P.dense_residual_unit(P.Tensor4D(x.cuda()), u).data.float().cpu().numpy()
+    def r(a):
+        return torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()
+    ud = {"pre": True}
+    for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
+        ud[f"w{i}"], ud[f"b{i}"] = r(fb.weights), r(fb.bias)
+        ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
+    ref = O.dense_residual_unit(x.float().numpy(), ud)
+    assert O.rel_err(y, ref) <= 2e-2
