@@ -123,7 +123,7 @@ struct WCfg {
   static constexpr int OFF_PAR = OFF_W + (int)WREG;
   static constexpr int OFF_STG = OFF_PAR + PARB;
   static constexpr int SMEM = OFF_STG + STGB;
-  static constexpr int ITEMS = (128 * P + kAThreads - 1) / kAThreads;  // IN transform pieces per thread
+  static constexpr int ITEMS = (128 * P + kAThreads / 2 - 1) / (kAThreads / 2);  // IN pieces per thread
 };
 
 // Stacks S1 / S2 are stored PLANE-MAJOR: plane k (channels 8k..8k+7) of row r at
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   if (tid == 0) {
     for (int s = 0; s < Q::SA; ++s) {
       tc::mbar_init(&a_load[s], 1);
-      tc::mbar_init(&a_full[s], MODE == kIn ? kAThreads : 1);
+      tc::mbar_init(&a_full[s], MODE == kIn ? kAThreads / 2 : 1);
       tc::mbar_init(&a_empty[s], 1);
     }
     for (int s = 0; s < SWB; ++s) {
@@ -225,19 +225,23 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       // one 16-B piece per item: consecutive threads walk the pieces of consecutive rows
       // (conflict-free); the piece in physical slot q of row r holds channel group
       // q ^ swizzle(r) of the chunk
+      // two groups of 4 warps take alternate chunks, so two chunks are in flight
       const float* s1 = par;  // packed sign / shift pairs (see unit_wide_pack_kernel)
       constexpr int PR = Q::ROWB / 16;  // pieces per row
+      constexpr int TG = kAThreads / 2;
+      const int grp_id = tid / TG, gt = tid % TG;
       int c = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
         for (int kc = 0; kc < Q::NKC; ++kc, ++c) {
+          if ((c & 1) != grp_id) continue;
           const int s = c % Q::SA;
           tc::mbar_wait(&a_load[s], (c / Q::SA) & 1);
-          if (tid == 0) wtrace(a, kEvCData, c);
+          if (gt == 0) wtrace(a, kEvCData, c);
           uint8_t* A = Aring + s * Q::ACH;
           uint4 raw[Q::ITEMS];
 #pragma unroll
           for (int j = 0; j < Q::ITEMS; ++j) {
-            const int i = tid + j * kAThreads;
+            const int i = gt + j * TG;
             if (i < 128 * PR)
               asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                            : "=r"(raw[j].x), "=r"(raw[j].y), "=r"(raw[j].z), "=r"(raw[j].w)
@@ -245,7 +249,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           }
 #pragma unroll
           for (int j = 0; j < Q::ITEMS; ++j) {
-            const int i = tid + j * kAThreads;
+            const int i = gt + j * TG;
             if (i >= 128 * PR) break;
             const int r = i / PR, qp = i % PR;
             const int grp = qp ^ (Q::KC == 64 ? (r & 7) : ((r >> 1) & 3));
@@ -268,8 +272,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           }
           tc::fence_async_smem();
           tc::mbar_arrive(&a_full[s]);
-          if (tid == 0 && kc == Q::NKC - 1) wtrace(a, kEvPub, c / Q::NKC);
-          if (tid == 0) wtrace(a, kEvCPub, c);
+          if (gt == 0 && kc == Q::NKC - 1) wtrace(a, kEvPub, c / Q::NKC);
+          if (gt == 0) wtrace(a, kEvCPub, c);
         }
     }
   } else if (tid < kAThreads + kEThreads) {
@@ -572,6 +576,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           tc::mbar_wait(&a_full[sa], (ait / Q::SA) & 1);
           tc::fence_after();
           if (MODE != kIn && kc == Q::NKC - 1) wtrace(a, kEvPub, k);
+          if (MODE != kIn) wtrace(a, kEvCData, ait);
           const uint32_t abase = tc::smem_u32(Aring + sa * Q::ACH);
           for (int tap = 0; tap < Q::TAPS; ++tap, ++wit) {
             const int sw = Q::RES ? 0 : wit % SWB;
@@ -593,6 +598,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             if (!Q::RES) tc::mma_commit(&w_empty[sw]);
           }
           tc::mma_commit(&a_empty[sa]);
+          if (MODE != kIn) wtrace(a, kEvCPub, ait);  // MID/OUT: chunk's MMAs issued
         }
         tc::mma_commit(&acc_full[buf]);
       }
