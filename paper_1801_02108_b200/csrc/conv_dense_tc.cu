@@ -63,13 +63,39 @@ struct CCfg {
 };
 
 struct __align__(64) CArgs {
-  CUtensorMap tmap;       // x as (C, W, H, N), box (KC, 16s, 8s, 1), element strides (1, s, s, 1)
+  CUtensorMap tmap;       // x as (C, W, H, N), box (KC, tw*s, th*s, 1), element strides (1, s, s, 1)
   __nv_bfloat16* out;     // (n, oh, ow, COUT)
   const uint8_t* wpk;     // packed weight chunks (kc, tap)
-  const float* bias;      // COUT floats (zeros when the layer has none)
+  const float* bias;      // COUT floats (dense mode) ...
+  const __nv_bfloat16* bias_bf16;  // ... or bf16 / null (sparse mode, sparse_conv2d's FilterBank)
   int n, oh, ow, sy, sx, py, px;
-  int tiles_y, tiles_x;
+  int tiles_y, tiles_x;   // dense mode: 8 x 16 output tiles
+  int th, tw;             // output rows / cols per tile (dense 8 x 16; sparse: the out block)
+  // sparse mode (idx != null): tile j = active block j of the list; its window starts at
+  // (goy + by*gsy, gox + bx*gsx) and its output block at (by*th, bx*tw)
+  const int32_t* idx;
+  const int32_t* count;
+  int cap, gsy, gsx, goy, gox;
 };
+
+// tile -> (frame, first output row / col, first input row / col of tap (0, 0))
+__device__ __forceinline__ void conv_tile(const CArgs& a, int tile, int& n, int& oy0, int& ox0, int& iy0, int& ix0) {
+  if (a.idx) {
+    n = __ldg(a.idx + 3 * tile);
+    const int by = __ldg(a.idx + 3 * tile + 1), bx = __ldg(a.idx + 3 * tile + 2);
+    oy0 = by * a.th;
+    ox0 = bx * a.tw;
+    iy0 = a.goy + by * a.gsy;
+    ix0 = a.gox + bx * a.gsx;
+  } else {
+    const int tx = tile % a.tiles_x, ty = (tile / a.tiles_x) % a.tiles_y;
+    n = tile / (a.tiles_x * a.tiles_y);
+    oy0 = ty * a.th;
+    ox0 = tx * a.tw;
+    iy0 = oy0 * a.sy - a.py;
+    ix0 = ox0 * a.sx - a.px;
+  }
+}
 
 template <int CIN, int COUT>
 __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_constant__ CArgs a) {
@@ -103,7 +129,8 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     tc::mbar_fence_init();
   }
   if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
-  for (int i = tid; i < COUT; i += kCThreads) bias[i] = a.bias[i];
+  for (int i = tid; i < COUT; i += kCThreads)
+    bias[i] = a.bias ? a.bias[i] : a.bias_bf16 ? __bfloat162float(a.bias_bf16[i]) : 0.f;
   if (warp == 0) tc::tmem_alloc<Q::TALLOC>(&tslot);
   tc::fence_before();
   __syncthreads();
@@ -116,7 +143,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       tc::bulk_g2s(Wring + (size_t)c * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[0]);
   }
   tc::pdl_wait();
-  const int ntiles = a.n * a.tiles_y * a.tiles_x;
+  const int ntiles = a.idx ? ld_count(a.count, a.cap) : a.n * a.tiles_y * a.tiles_x;
 
   if (warp < kLWarp) {
     // ------------------------------------------------ epilogue
@@ -129,10 +156,11 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
       const int buf = Q::NACC == 2 ? (k & 1) : 0;
       const int use = Q::NACC == 2 ? (k >> 1) : k;
-      const int tx = tile % a.tiles_x, ty = (tile / a.tiles_x) % a.tiles_y, n = tile / (a.tiles_x * a.tiles_y);
-      const int Y = ty * 8 + r / 16, X = tx * 16 + r % 16;
+      int n, oy0, ox0, iy0, ix0;
+      conv_tile(a, tile, n, oy0, ox0, iy0, ix0);
+      const int Y = oy0 + r / a.tw, X = ox0 + r % a.tw;
       if (half == 0)
-        rowdst[r] = (Y < a.oh && X < a.ow) ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
+        rowdst[r] = (r < a.th * a.tw && Y < a.oh && X < a.ow) ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
       const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * COUT;
       tc::mbar_wait(&acc_full[buf], use & 1);
       tc::fence_after();
@@ -181,13 +209,14 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     if (lane == 0) {
       int c = 0, wit = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tx = tile % a.tiles_x, ty = (tile / a.tiles_x) % a.tiles_y, n = tile / (a.tiles_x * a.tiles_y);
-        const int x0 = tx * 16 * a.sx - a.px, y0 = ty * 8 * a.sy - a.py;
+        int n, oy0, ox0, y0, x0;
+        conv_tile(a, tile, n, oy0, ox0, y0, x0);
+        const uint32_t bytes = (uint32_t)(a.th * a.tw * Q::ROWB);
         for (int kc = 0; kc < Q::NKC; ++kc)
           for (int tap = 0; tap < 9; ++tap, ++c) {
             const int s = c % Q::SA;
             tc::mbar_wait(&a_empty[s], ((c / Q::SA) & 1) ^ 1);
-            tc::mbar_expect_tx(&a_full[s], (uint32_t)Q::ACH);
+            tc::mbar_expect_tx(&a_full[s], bytes);
             tma_4d(Aring + s * Q::ACH, &a.tmap, kc * Q::KC, x0 + tap % 3, y0 + tap / 3, n, &a_full[s]);
             if (!Q::RES) {
               const int sw = wit % SWB;
@@ -260,13 +289,16 @@ __global__ void conv_dense_pack_kernel(const __nv_bfloat16* __restrict__ w, uint
 
 template <int CIN, int COUT>
 int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int px, int oh, int ow,
-                 const void* wpk, const float* bias, void* out, cudaStream_t s) {
+                 const void* wpk, const float* bias, void* out, cudaStream_t s,
+                 const Geo* sparse = nullptr, const int32_t* idx = nullptr, const int32_t* count = nullptr,
+                 int cap = 0, const __nv_bfloat16* bias_bf16 = nullptr) {
   using Q = CCfg<CIN, COUT>;
   CArgs a;
   memset(&a, 0, sizeof(a));
+  const int th = sparse ? sparse->obh : 8, tw = sparse ? sparse->obw : 16;
   const uint64_t dims[4] = {(uint64_t)CIN, (uint64_t)w, (uint64_t)h, (uint64_t)n};
   const uint64_t str[3] = {(uint64_t)CIN * 2, (uint64_t)w * CIN * 2, (uint64_t)h * w * CIN * 2};
-  const uint32_t box[4] = {(uint32_t)Q::KC, (uint32_t)(16 * sx), (uint32_t)(8 * sy), 1};
+  const uint32_t box[4] = {(uint32_t)Q::KC, (uint32_t)(tw * sx), (uint32_t)(th * sy), 1};
   const uint32_t es[4] = {1, (uint32_t)sx, (uint32_t)sy, 1};
   int st = encode_map(&a.tmap, x, 4, dims, str, box, Q::KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, es);
   if (st) return st;
@@ -280,9 +312,22 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   a.sx = sx;
   a.py = py;
   a.px = px;
-  a.tiles_y = (oh + 7) / 8;
-  a.tiles_x = (ow + 15) / 16;
-  const long tiles = (long)n * a.tiles_y * a.tiles_x;
+  a.bias_bf16 = bias_bf16;
+  a.th = th;
+  a.tw = tw;
+  a.tiles_y = (oh + th - 1) / th;
+  a.tiles_x = (ow + tw - 1) / tw;
+  long tiles = (long)n * a.tiles_y * a.tiles_x;
+  if (sparse) {
+    a.idx = idx;
+    a.count = count;
+    a.cap = cap;
+    a.gsy = sparse->sy;
+    a.gsx = sparse->sx;
+    a.goy = sparse->oy;
+    a.gox = sparse->ox;
+    tiles = cap;
+  }
   auto kern = conv_dense_kernel<CIN, COUT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
@@ -296,7 +341,7 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, a);
-  return launch_status("dense_conv_tcgen05");
+  return launch_status(sparse ? "sparse_conv_tcgen05_tma" : "dense_conv_tcgen05");
 }
 
 // (CIN, COUT): the config-4 stage projections and square shapes
@@ -310,6 +355,49 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   X(128, 128)
 
 }  // namespace
+
+// Sparse 3x3 conv (any stride <= 3) through the same kernel: tile = active block, the out
+// block (obh x obw <= 128 pixels) = one strided TMA box per (K-chunk, tap).
+bool sparse_conv_tma_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g) {
+  if (dtype != SBN_BF16 || kh != 3 || kw != 3 || sh != sw || sh < 1 || sh > 3) return false;
+  if (g.obh * g.obw > 128 || g.obw * sw > 256 || g.obh * sh > 256) return false;
+#define X(CI, CO) if (cin == CI && cout == CO) return CCfg<CI, CO>::SMEM <= max_smem_optin();
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  return false;
+}
+
+size_t sparse_conv_tma_packed_bytes(int cin, int cout) {
+#define X(CI, CO) if (cin == CI && cout == CO) return (size_t)CCfg<CI, CO>::WBYTES;
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  return 0;
+}
+
+int sparse_conv_tma_pack(const void* w, int cin, int cout, void* img, cudaStream_t s) {
+#define X(CI, CO)                                                                                          \
+  if (cin == CI && cout == CO) {                                                                           \
+    conv_dense_pack_kernel<CI, CO><<<128, 256, 0, s>>>((const __nv_bfloat16*)w, (uint8_t*)img);          \
+    return launch_status("sparse_conv_tma_pack");                                                          \
+  }
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d", cin, cout);
+  return SBN_ERR_UNSUPPORTED;
+}
+
+int sparse_conv_tma(const void* x, int cin, int cout, int sh, int sw, const Geo& g, const void* wpk,
+                    const void* bias, const int32_t* idx, const int32_t* count, int cap, void* dst,
+                    cudaStream_t s) {
+#define X(CI, CO)                                                                                           \
+  if (cin == CI && cout == CO)                                                                              \
+    return launch_dense<CI, CO>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, idx, \
+                                count, cap, (const __nv_bfloat16*)bias);
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
+  set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d", cin, cout);
+  return SBN_ERR_UNSUPPORTED;
+}
 
 }  // namespace sbn
 

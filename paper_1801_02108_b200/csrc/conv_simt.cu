@@ -104,6 +104,12 @@ int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, con
                    const int32_t* idx, const int32_t* count, int cap, void* dst, cudaStream_t s);
 size_t sparse_conv_tc_packed_bytes(int cin, int cout);
 int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_t s);
+bool sparse_conv_tma_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g);
+size_t sparse_conv_tma_packed_bytes(int cin, int cout);
+int sparse_conv_tma_pack(const void* w, int cin, int cout, void* img, cudaStream_t s);
+int sparse_conv_tma(const void* x, int cin, int cout, int sh, int sw, const Geo& g, const void* wpk,
+                    const void* bias, const int32_t* idx, const int32_t* count, int cap, void* dst,
+                    cudaStream_t s);
 bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                               const Geo& g);
 
@@ -111,19 +117,29 @@ bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int 
 
 using namespace sbn;
 
+// tensor-core variant for a sparse conv: 1 = single-window row-shift kernel (conv_tc.cu,
+// 3x3 stride 1), 2 = strided-TMA tap GEMM (conv_dense_tc.cu, 3x3 stride <= 3, out block
+// <= 128 pixels), 0 = none (SIMT)
+static int conv_tc_kind(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g) {
+  if (sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, g)) return 1;
+  if (sparse_conv_tma_supported(dtype, cin, cout, kh, kw, sh, sw, g)) return 2;
+  return 0;
+}
+
 extern "C" int sbn_sparse_conv_algo(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                                     const sbn_geometry* gp) {
   if (!gp) return SBN_ALGO_SIMT;
-  return sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp)) ? SBN_ALGO_TCGEN05
-                                                                              : SBN_ALGO_SIMT;
+  return conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp)) ? SBN_ALGO_TCGEN05 : SBN_ALGO_SIMT;
 }
 
 extern "C" size_t sbn_sparse_conv_packed_bytes(int dtype, int cin, int cout, int kh, int kw,
                                                int sh, int sw, const sbn_geometry* gp) {
   if (!gp) return 0;
-  return sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp))
-             ? sparse_conv_tc_packed_bytes(cin, cout)
-             : 0;
+  switch (conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp))) {
+    case 1: return sparse_conv_tc_packed_bytes(cin, cout);
+    case 2: return sparse_conv_tma_packed_bytes(cin, cout);
+    default: return 0;
+  }
 }
 
 extern "C" int sbn_sparse_conv_pack(const void* w, int dtype, int cin, int cout, int kh, int kw,
@@ -131,9 +147,10 @@ extern "C" int sbn_sparse_conv_pack(const void* w, int dtype, int cin, int cout,
                                     sbn_stream_t stream) {
   int st = check_geo(gp);
   if (st) return st;
-  SBN_CHECK_ARG(sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp)),
-                SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
+  const int kind = conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp));
+  SBN_CHECK_ARG(kind != 0, SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
   SBN_CHECK_ARG(w && packed, SBN_ERR_INVALID, "null argument");
+  if (kind == 2) return sparse_conv_tma_pack(w, cin, cout, packed, (cudaStream_t)stream);
   return sparse_conv_tc_pack(w, cin, cout, packed, (cudaStream_t)stream);
 }
 
@@ -154,20 +171,21 @@ extern "C" int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int 
   SBN_CHECK_ARG(x && w && idx && count && dst, SBN_ERR_INVALID, "null pointer argument");
   Geo g = to_geo(gp);
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tc_ok = sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, g);
+  const int kind = conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, g);
   if (algo == SBN_ALGO_TCGEN05) {
-    SBN_CHECK_ARG(tc_ok, SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
+    SBN_CHECK_ARG(kind != 0, SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
   }
-  if (tc_ok && algo != SBN_ALGO_SIMT) {
+  if (kind != 0 && algo != SBN_ALGO_SIMT) {
     const void* wpk = w_packed;
     if (!wpk) {
-      const size_t nb = sparse_conv_tc_packed_bytes(cin, cout);
+      const size_t nb = kind == 1 ? sparse_conv_tc_packed_bytes(cin, cout) : sparse_conv_tma_packed_bytes(cin, cout);
       SBN_CHECK_ARG(ws && ws_bytes >= nb, SBN_ERR_WORKSPACE,
                     "tcgen05 sparse conv without a packed weight image needs a %zu-byte workspace", nb);
-      int st2 = sparse_conv_tc_pack(w, cin, cout, ws, s);
+      int st2 = kind == 1 ? sparse_conv_tc_pack(w, cin, cout, ws, s) : sparse_conv_tma_pack(w, cin, cout, ws, s);
       if (st2) return st2;
       wpk = ws;
     }
+    if (kind == 2) return sparse_conv_tma(x, cin, cout, sh, sw, g, wpk, bias, idx, count, cap, dst, s);
     return sparse_conv_tc(x, cin, cout, g, wpk, bias, idx, count, cap, dst, s);
   }
   switch (dtype) {

@@ -117,7 +117,7 @@ def sparse_conv_into(xt: torch.Tensor, out: torch.Tensor, f: FilterBank, p: Conv
     if a != _lib.SBN_ALGO_SIMT:
         nb = lib.sbn_sparse_conv_packed_bytes(dc, f.c_in, f.c_out, kh, kw, sh, sw, C.byref(g))
         if nb:
-            key = ("tc_pack", xt.dtype, str(xt.device))
+            key = ("tc_pack", xt.dtype, str(xt.device), kh, kw, sh, sw, g.bh, g.bw)  # layout depends on the kernel variant
             packed = f._cache.get(key)
             if packed is None:
                 packed = torch.empty(nb, dtype=torch.uint8, device=xt.device)

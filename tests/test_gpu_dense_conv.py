@@ -32,3 +32,25 @@ def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, sa
     assert y.shape == ref.shape
     assert O.rel_err(y, ref) <= 1e-2
     del lib
+
+
+@pytest.mark.parametrize("cin,cout,stride,block,same", [
+    (64, 64, 2, 17, True), (128, 128, 2, 13, True), (32, 96, 1, 10, True), (64, 64, 3, 24, False),
+    (96, 192, 2, 9, True)])
+def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, block, same):
+    """Strided / other-shape sparse 3x3 convs on the TMA tap-GEMM path (kernel variant 2)
+    against the fp32 oracle on bf16-rounded inputs."""
+    rng = np.random.default_rng(stride * 100 + block)
+    n, h, w = 2, 53, 47
+    x = torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16()
+    wt = torch.from_numpy((rng.standard_normal((3, 3, cin, cout)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16()
+    b = torch.from_numpy(rng.standard_normal(cout).astype(np.float32)).bfloat16()
+    mk = (rng.random((n, h, w)) < 0.03).astype(np.uint8)
+    p = P.ConvParams((3, 3), (stride, stride), P.Padding.SAME if same else P.Padding.VALID, cout)
+    spec = P.compute_block_spec((n, h, w, cin), p, (block, block))
+    from paper_1801_02108_b200.layers import sparse_conv_algo
+    assert sparse_conv_algo(torch.bfloat16, P.FilterBank(wt, b), p, spec) == "tcgen05"
+    y = P.sparse_conv2d(P.Tensor4D(x.cuda()), P.BinaryMask(mk), P.FilterBank(wt, b), p, (block, block))
+    ref = O.sparse_conv2d(x.float().numpy(), mk, wt.float().numpy(), b.float().numpy(), (stride, stride), same,
+                          (block, block))
+    assert O.rel_err(y.data.float().cpu().numpy(), ref) <= 2e-2
