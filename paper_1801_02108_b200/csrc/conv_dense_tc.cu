@@ -27,9 +27,18 @@ constexpr int kCE = 256;                 // epilogue threads
 constexpr int kCThreads = kCE + 64;
 constexpr int kCBudget = 214 * 1024;
 
+// weights resident in smem with 64-channel K-chunks?  (otherwise they stream through a ring
+// in 32-channel chunks, which keeps the per-stage footprint small enough for a deep ring)
+template <int CIN, int COUT>
+constexpr bool dense_resident() {
+  constexpr int kc = CIN % 64 == 0 ? 64 : 32;
+  constexpr int gs = COUT <= 192 ? COUT : 128;
+  return 6L * 128 * kc * 2 + 9L * CIN * COUT * 2 + 128L * (gs * 2 + 16) + COUT * 4 + 128 <= kCBudget;
+}
+
 template <int CIN, int COUT>
 struct CCfg {
-  static constexpr int KC = CIN % 64 == 0 ? 64 : 32;
+  static constexpr int KC = (CIN % 64 == 0 && dense_resident<CIN, COUT>()) ? 64 : 32;
   static_assert(CIN % KC == 0, "CIN must be a multiple of 32");
   static constexpr int NKC = CIN / KC;
   static constexpr int ROWB = KC * 2;
@@ -50,10 +59,13 @@ struct CCfg {
   static constexpr int SPITCH = GS * 2 + 16;
   static constexpr int STGB = 128 * SPITCH;
   static constexpr int PARB = (COUT * 4 + 127) / 128 * 128;
-  static constexpr bool RES = 3 * ACH + WBYTES + STGB + PARB <= kCBudget;
+  static constexpr bool RES = dense_resident<CIN, COUT>();
+  // A boxes are small and latency-bound (strided gathers): keep up to 12 in flight; the
+  // streamed case pairs every A box with a weight chunk, so both rings get the same depth
   static constexpr int SA_R = (int)((kCBudget - WBYTES - STGB - PARB) / ACH);
-  static constexpr int SA = RES ? (SA_R > 6 ? 6 : SA_R) : 3;
-  static constexpr int SW = RES ? 0 : ((SA * ACH + 4 * WCH + STGB + PARB <= kCBudget) ? 4 : (SA * ACH + 3 * WCH + STGB + PARB <= kCBudget) ? 3 : 2);
+  static constexpr int SS = (int)((kCBudget - STGB - PARB) / (ACH + WCH));
+  static constexpr int SA = RES ? (SA_R > 12 ? 12 : SA_R) : (SS > 8 ? 8 : SS);
+  static constexpr int SW = RES ? 0 : SA;
   static constexpr long WREG = RES ? WBYTES : (long)SW * WCH;
   static_assert(SA >= 2 && SA * ACH + WREG + STGB + PARB <= kCBudget, "shared memory budget");
   static constexpr int OFF_W = SA * ACH;
