@@ -338,7 +338,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   bool weights_ready = false;
 
   trace(a.trace, 1);
-  // everything above overlaps the previous kernel (reduce_mask) under PDL
+  // everything above overlaps the previous kernel (reduce_mask) under PDL; the next
+  // launch may start its own prologue now (its griddepcontrol.wait still waits for this
+  // grid to complete and flush)
+  tc::pdl_trigger();
   tc::pdl_wait();
   int n0 = 0, by0 = 0, bx0 = 0;
   int B = 0;
@@ -853,6 +856,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   uint32_t phase = 0;
   bool weights_ready = false;
   trace(a.trace, 1);
+  tc::pdl_trigger();
   tc::pdl_wait();
   int B = 0;
   const int32_t* idx = a.idx;
