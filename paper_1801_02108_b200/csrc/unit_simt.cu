@@ -254,9 +254,18 @@ size_t unit_workspace_wide(int c, int m, const Geo& g) {
   return kBarBytes + unit_wide_stack_bytes(m, g) + align_up(unit_wide_packed_bytes(c, m), 256);
 }
 
-// which tensor-core variant applies: 1 single-kernel unit, 2 wide (three launches), 0 none
+// which tensor-core variant applies: 1 single-kernel unit, 2 wide (three launches), 0 none.
+// The single kernel walks one block's latency chain per CTA; past ~2K candidate blocks the
+// pipelined three-launch unit is faster even where the single kernel fits (measured:
+// tools/wide_vs_fused.py, config-2 shapes: 48 vs 44 us at 4 frames, 723 vs 609 us at 64).
+constexpr long kFusedMaxCandidates = 2048;
 int unit_tc_kind(int dtype, int c, int m, const Geo& g, int halo, int pre_act) {
-  if (!(debug_flags() & kDebugForceWide) && unit_tc_supported(dtype, c, m, g, halo, pre_act)) return 1;
+  const long cand = (long)g.n * g.gy * g.gx;
+  if (!(debug_flags() & kDebugForceWide) && cand <= kFusedMaxCandidates &&
+      unit_tc_supported(dtype, c, m, g, halo, pre_act))
+    return 1;
+  if (unit_tc_supported(dtype, c, m, g, halo, pre_act) && !unit_wide_supported(dtype, c, m, g, halo, pre_act))
+    return 1;
   if (unit_wide_supported(dtype, c, m, g, halo, pre_act)) return 2;
   return 0;
 }
