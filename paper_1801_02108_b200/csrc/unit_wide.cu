@@ -50,6 +50,7 @@ namespace {
 constexpr int kAThreads = 256;
 constexpr int kEThreads = 256;
 constexpr int kWideThreads = kAThreads + kEThreads + 64;
+constexpr int kOutCopy = kAThreads + kEThreads;  // OUT: threads in the staged copy phase
 constexpr int kMaxRows = 168;  // staged rows of a MID tile: 128 + 2*b + 2 (b <= 18)
 
 enum { kIn = 1, kMid = 2, kOut = 3 };
@@ -276,6 +277,47 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           if (gt == 0) wtrace(a, kEvCPub, c);
         }
     }
+    if constexpr (MODE == kOut) {
+      // OUT: these warps have no operand transform; they join the epilogue's staged copy
+      // phase (residual add along pixel rows), same barrier sequence as the epilogue warps
+      constexpr int GS = Q::GS, CHR = GS * 2 / 16;
+      constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
+      constexpr int BATCH = IT2 < 6 ? IT2 : 6;
+      const uint8_t* stg = smem + Q::OFF_STG;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+        for (int g0 = 0; g0 < N; g0 += GS) {
+          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");
+#pragma unroll 1
+          for (int jb = 0; jb < IT2; jb += BATCH) {
+            uint4 xr[BATCH];
+#pragma unroll
+            for (int jj = 0; jj < BATCH; ++jj) {
+              const int it = tid + (jb + jj) * kOutCopy;
+              const long long off = (jb + jj < IT2 && it < 128 * CHR) ? rowdst[it / CHR] : -1;
+              if (off >= 0) xr[jj] = reinterpret_cast<const uint4*>(a.dst + off + g0)[it % CHR];
+            }
+#pragma unroll
+            for (int jj = 0; jj < BATCH; ++jj) {
+              const int it = tid + (jb + jj) * kOutCopy;
+              if (jb + jj >= IT2 || it >= 128 * CHR) break;
+              const int row = it / CHR, ch = it % CHR;
+              const long long off = rowdst[row];
+              if (off < 0) continue;
+              const uint4 sv = *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
+              const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[jj]);
+              const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&sv);
+              uint32_t o[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 xf = __bfloat1622float2(xh[q]), uf = __bfloat1622float2(uh[q]);
+                o[q] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
+              }
+              reinterpret_cast<uint4*>(a.dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+          }
+          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");
+        }
+    }
   } else if (tid < kAThreads + kEThreads) {
     // ------------------------------------------------ epilogue
     // warp w drains TMEM lane quarter w % 4; the two warps of a quarter take alternate
@@ -366,10 +408,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
         // smem; phase 2 walks (row, 16-B chunk) items so consecutive lanes cover one pixel
         // row: residual loads and stores are coalesced 16-B vectors
         constexpr int GS = Q::GS, CHR = GS * 2 / 16;
-        constexpr int IT2 = (128 * CHR + kEThreads - 1) / kEThreads;
+        constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
         static_assert(N % GS == 0, "staging groups");
         uint8_t* stg = smem + Q::OFF_STG;
-        const int et = tid - kAThreads;
+        const int et = tid;  // copy-phase index over the idle A warps + the epilogue warps
         const float* b3 = par;
         if (half == 0) rowdst[r] = store ? (long long)(dp - a.dst) : -1;
         for (int g0 = 0; g0 < N; g0 += GS) {
@@ -394,14 +436,14 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             tc::fence_before();
             tc::mbar_arrive(&acc_empty[buf]);
           }
-          asm volatile("bar.sync 2, %0;" ::"n"(kEThreads) : "memory");
+          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");
           constexpr int BATCH = IT2 < 6 ? IT2 : 6;  // residual loads in flight per thread
 #pragma unroll 1
           for (int jb = 0; jb < IT2; jb += BATCH) {
           uint4 xr[BATCH];
 #pragma unroll
           for (int jj = 0; jj < BATCH; ++jj) {
-            const int it = et + (jb + jj) * kEThreads;
+            const int it = et + (jb + jj) * kOutCopy;
             const int row = it / CHR, ch = it % CHR;
             const long long off = (jb + jj < IT2 && it < 128 * CHR) ? rowdst[row] : -1;
             if (off >= 0) xr[jj] = reinterpret_cast<const uint4*>(a.dst + off + g0)[ch];
@@ -410,7 +452,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           for (int jj = 0; jj < BATCH; ++jj) {
             const int j = jb + jj;
             if (j >= IT2) break;
-            const int it = et + j * kEThreads;
+            const int it = et + j * kOutCopy;
             const int row = it / CHR, ch = it % CHR;
             const long long off = it < 128 * CHR ? rowdst[row] : -1;
             if (off < 0) continue;
@@ -426,7 +468,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             reinterpret_cast<uint4*>(a.dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
           }
           }
-          asm volatile("bar.sync 2, %0;" ::"n"(kEThreads) : "memory");  // staging / rowdst reuse
+          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");  // staging / rowdst reuse
         }
         if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
         meta(tile + gridDim.x);
