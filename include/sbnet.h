@@ -129,16 +129,16 @@ int sbn_copy_block_regions(const void* src, void* dst, int dtype, int c, const s
                            const int32_t* idx, const int32_t* count, int cap, int region,
                            sbn_stream_t stream);
 
-/* Dense 3x3 convolution, any stride <= 3, bias fused (bf16, tcgen05 implicit GEMM fed by
- * strided 4-D TMA boxes): the stage-transition projection of run_stage (reference
- * `layers.py:316-318`: conv2d_direct + bias).  x (n, h, w, cin) NHWC; out (n, oh, ow, cout);
- * padding (ph, pw) zero-fill; packed: sbn_dense_conv_packed_bytes, from sbn_dense_conv_pack
- * of the HWIO weights; bias: cout floats. */
+/* Dense k x k convolution (k = 1, 3, 5; stride <= min(k, 3)), bias fused (bf16, tcgen05
+ * implicit GEMM fed by strided 4-D TMA boxes): the stage-transition projection of run_stage
+ * (reference `layers.py:316-318`: conv2d_direct + bias).  x (n, h, w, cin) NHWC; out
+ * (n, oh, ow, cout); padding (ph, pw) zero-fill; packed: sbn_dense_conv_packed_bytes, from
+ * sbn_dense_conv_pack of the HWIO weights; bias: cout floats. */
 int sbn_dense_conv_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw);
-size_t sbn_dense_conv_packed_bytes(int cin, int cout);
-int sbn_dense_conv_pack(const void* w, int cin, int cout, void* packed, sbn_stream_t stream);
-int sbn_dense_conv(const void* x, int n, int h, int w, int cin, int cout, int sh, int sw, int ph, int pw,
-                   int oh, int ow, const void* packed, const float* bias, void* out, sbn_stream_t stream);
+size_t sbn_dense_conv_packed_bytes(int cin, int cout, int k);
+int sbn_dense_conv_pack(const void* w, int cin, int cout, int k, void* packed, sbn_stream_t stream);
+int sbn_dense_conv(const void* x, int n, int h, int w, int cin, int cout, int k, int sh, int sw, int ph,
+                   int pw, int oh, int ow, const void* packed, const float* bias, void* out, sbn_stream_t stream);
 
 /* Fused sparse_conv2d body (`layers.py:27-47` after reduce_mask): gather -> valid
  * conv (kh, kw, stride sh, sw) -> (+bias) -> scatter into dst (n, oh, ow, cout), all in

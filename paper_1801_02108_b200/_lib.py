@@ -56,9 +56,9 @@ _PROTOS = {
     "sbn_copy_block_regions": (_I, [_P, _P, _I, _I, _G, _P, _P, _I, _I, _P]),
     "sbn_gather_grad_workspace": (C.c_size_t, [_G]),
     "sbn_dense_conv_supported": (_I, [_I, _I, _I, _I, _I, _I, _I]),
-    "sbn_dense_conv_packed_bytes": (C.c_size_t, [_I, _I]),
-    "sbn_dense_conv_pack": (_I, [_P, _I, _I, _P, _P]),
-    "sbn_dense_conv": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "sbn_dense_conv_packed_bytes": (C.c_size_t, [_I, _I, _I]),
+    "sbn_dense_conv_pack": (_I, [_P, _I, _I, _I, _P, _P]),
+    "sbn_dense_conv": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P]),
     "sbn_gather_grad": (_I, [_P, _I, _I, _G, _P, _P, _I, _P, _P, C.c_size_t, _P]),
     "sbn_sparse_conv": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _G, _P, _P, _P, _P, _P, _I, _P, _P,
                              C.c_size_t, _I, _P]),

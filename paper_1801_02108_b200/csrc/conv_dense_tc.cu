@@ -29,16 +29,17 @@ constexpr int kCBudget = 214 * 1024;
 
 // weights resident in smem with 64-channel K-chunks?  (otherwise they stream through a ring
 // in 32-channel chunks, which keeps the per-stage footprint small enough for a deep ring)
-template <int CIN, int COUT>
+template <int CIN, int COUT, int KS>
 constexpr bool dense_resident() {
   constexpr int kc = CIN % 64 == 0 ? 64 : 32;
   constexpr int gs = COUT <= 192 ? COUT : 128;
-  return 6L * 128 * kc * 2 + 9L * CIN * COUT * 2 + 128L * (gs * 2 + 16) + COUT * 4 + 128 <= kCBudget;
+  return 6L * 128 * kc * 2 + (long)KS * KS * CIN * COUT * 2 + 128L * (gs * 2 + 16) + COUT * 4 + 128 <= kCBudget;
 }
 
-template <int CIN, int COUT>
+template <int CIN, int COUT, int KS>
 struct CCfg {
-  static constexpr int KC = (CIN % 64 == 0 && dense_resident<CIN, COUT>()) ? 64 : 32;
+  static constexpr int TAPS = KS * KS;
+  static constexpr int KC = (CIN % 64 == 0 && dense_resident<CIN, COUT, KS>()) ? 64 : 32;
   static_assert(CIN % KC == 0, "CIN must be a multiple of 32");
   static constexpr int NKC = CIN / KC;
   static constexpr int ROWB = KC * 2;
@@ -46,7 +47,7 @@ struct CCfg {
   static constexpr int ACH = 128 * ROWB;
   static constexpr int PW = COUT * 16;
   static constexpr int WCH = (KC / 8) * PW;
-  static constexpr int CHUNKS = NKC * 9;
+  static constexpr int CHUNKS = NKC * TAPS;
   static constexpr long WBYTES = (long)CHUNKS * WCH;
   static constexpr int NSPLIT = COUT > 256 ? 2 : 1;
   static constexpr int NS = COUT / NSPLIT;
@@ -59,7 +60,7 @@ struct CCfg {
   static constexpr int SPITCH = GS * 2 + 16;
   static constexpr int STGB = 128 * SPITCH;
   static constexpr int PARB = (COUT * 4 + 127) / 128 * 128;
-  static constexpr bool RES = dense_resident<CIN, COUT>();
+  static constexpr bool RES = dense_resident<CIN, COUT, KS>();
   // A boxes are small and latency-bound (strided gathers): keep up to 12 in flight; the
   // streamed case pairs every A box with a weight chunk, so both rings get the same depth
   static constexpr int SA_R = (int)((kCBudget - WBYTES - STGB - PARB) / ACH);
@@ -109,9 +110,9 @@ __device__ __forceinline__ void conv_tile(const CArgs& a, int tile, int& n, int&
   }
 }
 
-template <int CIN, int COUT>
+template <int CIN, int COUT, int KS>
 __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_constant__ CArgs a) {
-  using Q = CCfg<CIN, COUT>;
+  using Q = CCfg<CIN, COUT, KS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int SWB = Q::SW > 0 ? Q::SW : 1;
   __shared__ uint64_t a_full[Q::SA], a_empty[Q::SA], w_full[SWB], w_empty[SWB];
@@ -225,16 +226,16 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
         conv_tile(a, tile, n, oy0, ox0, y0, x0);
         const uint32_t bytes = (uint32_t)(a.th * a.tw * Q::ROWB);
         for (int kc = 0; kc < Q::NKC; ++kc)
-          for (int tap = 0; tap < 9; ++tap, ++c) {
+          for (int tap = 0; tap < Q::TAPS; ++tap, ++c) {
             const int s = c % Q::SA;
             tc::mbar_wait(&a_empty[s], ((c / Q::SA) & 1) ^ 1);
             tc::mbar_expect_tx(&a_full[s], bytes);
-            tma_4d(Aring + s * Q::ACH, &a.tmap, kc * Q::KC, x0 + tap % 3, y0 + tap / 3, n, &a_full[s]);
+            tma_4d(Aring + s * Q::ACH, &a.tmap, kc * Q::KC, x0 + tap % KS, y0 + tap / KS, n, &a_full[s]);
             if (!Q::RES) {
               const int sw = wit % SWB;
               tc::mbar_wait(&w_empty[sw], ((wit / SWB) & 1) ^ 1);
               tc::mbar_expect_tx(&w_full[sw], Q::WCH);
-              tc::bulk_g2s(Wring + sw * Q::WCH, a.wpk + (size_t)(kc * 9 + tap) * Q::WCH, Q::WCH, &w_full[sw]);
+              tc::bulk_g2s(Wring + sw * Q::WCH, a.wpk + (size_t)(kc * Q::TAPS + tap) * Q::WCH, Q::WCH, &w_full[sw]);
               ++wit;
             }
           }
@@ -254,14 +255,14 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
         tc::fence_after();
         const uint32_t acc = tmem + buf * COUT;
         for (int kc = 0; kc < Q::NKC; ++kc)
-          for (int tap = 0; tap < 9; ++tap, ++c) {
+          for (int tap = 0; tap < Q::TAPS; ++tap, ++c) {
             const int s = c % Q::SA;
             tc::mbar_wait(&a_full[s], (c / Q::SA) & 1);
             const int sw = Q::RES ? 0 : wit % SWB;
             if (!Q::RES) tc::mbar_wait(&w_full[sw], (wit / SWB) & 1);
             tc::fence_after();
             const uint32_t abase = tc::smem_u32(Aring + s * Q::ACH);
-            const uint32_t wbase = tc::smem_u32(Wring + (Q::RES ? (kc * 9 + tap) * Q::WCH : sw * Q::WCH));
+            const uint32_t wbase = tc::smem_u32(Wring + (Q::RES ? (kc * Q::TAPS + tap) * Q::WCH : sw * Q::WCH));
 #pragma unroll
             for (int kk = 0; kk < Q::KC / 16; ++kk)
 #pragma unroll
@@ -287,24 +288,24 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
   if (warp == 0) tc::tmem_free<Q::TALLOC>(tmem);
 }
 
-// W (3, 3, CIN, COUT) HWIO -> chunks (kc, tap) of (COUT rows x KC) in the K-major plane layout
-template <int CIN, int COUT>
+// W (KS, KS, CIN, COUT) HWIO -> chunks (kc, tap) of (COUT rows x KC) in the K-major plane layout
+template <int CIN, int COUT, int KS>
 __global__ void conv_dense_pack_kernel(const __nv_bfloat16* __restrict__ w, uint8_t* __restrict__ img) {
-  using Q = CCfg<CIN, COUT>;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 9 * CIN * COUT; i += gridDim.x * blockDim.x) {
+  using Q = CCfg<CIN, COUT, KS>;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KS * KS * CIN * COUT; i += gridDim.x * blockDim.x) {
     const int tap = i / (CIN * COUT), rr = i % (CIN * COUT), ci = rr / COUT, co = rr % COUT;
     const int kc = ci / Q::KC, kq = ci % Q::KC;
-    *reinterpret_cast<__nv_bfloat16*>(img + (size_t)(kc * 9 + tap) * Q::WCH + (kq / 8) * Q::PW + co * 16 +
+    *reinterpret_cast<__nv_bfloat16*>(img + (size_t)(kc * Q::TAPS + tap) * Q::WCH + (kq / 8) * Q::PW + co * 16 +
                                       (kq % 8) * 2) = w[i];
   }
 }
 
-template <int CIN, int COUT>
+template <int CIN, int COUT, int KS>
 int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int px, int oh, int ow,
                  const void* wpk, const float* bias, void* out, cudaStream_t s,
                  const Geo* sparse = nullptr, const int32_t* idx = nullptr, const int32_t* count = nullptr,
                  int cap = 0, const __nv_bfloat16* bias_bf16 = nullptr) {
-  using Q = CCfg<CIN, COUT>;
+  using Q = CCfg<CIN, COUT, KS>;
   CArgs a;
   memset(&a, 0, sizeof(a));
   const int th = sparse ? sparse->obh : 8, tw = sparse ? sparse->obw : 16;
@@ -340,7 +341,7 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
     a.gox = sparse->ox;
     tiles = cap;
   }
-  auto kern = conv_dense_kernel<CIN, COUT>;
+  auto kern = conv_dense_kernel<CIN, COUT, KS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(tiles < sm_count() ? (tiles < 1 ? 1 : tiles) : sm_count()));
@@ -356,58 +357,62 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   return launch_status(sparse ? "sparse_conv_tcgen05_tma" : "dense_conv_tcgen05");
 }
 
-// (CIN, COUT): the config-4 stage projections and square shapes
+// (CIN, COUT, KS): the config-4 stage projections (3x3) and square shapes at 1x1 / 3x3 / 5x5
 #define SBN_DENSE_CONV_CONFIGS(X) \
-  X(32, 96)                       \
-  X(96, 192)                      \
-  X(192, 256)                     \
-  X(256, 384)                     \
-  X(32, 32)                       \
-  X(64, 64)                       \
-  X(128, 128)
+  X(32, 96, 3)                    \
+  X(96, 192, 3)                   \
+  X(192, 256, 3)                  \
+  X(256, 384, 3)                  \
+  X(32, 32, 3)                    \
+  X(64, 64, 3)                    \
+  X(128, 128, 3)                  \
+  X(64, 64, 1)                    \
+  X(128, 128, 1)                  \
+  X(32, 32, 5)                    \
+  X(64, 64, 5)
 
 }  // namespace
 
-// Sparse 3x3 conv (any stride <= 3) through the same kernel: tile = active block, the out
-// block (obh x obw <= 128 pixels) = one strided TMA box per (K-chunk, tap).
+// Sparse KxK conv (K = 1, 3, 5; stride <= K) through the same kernel: tile = active
+// block, the out block (obh x obw <= 128 pixels) = one strided TMA box per (K-chunk, tap).
 bool sparse_conv_tma_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g) {
-  if (dtype != SBN_BF16 || kh != 3 || kw != 3 || sh != sw || sh < 1 || sh > 3) return false;
+  if (dtype != SBN_BF16 || kh != kw || sh != sw || sh < 1 || sh > kh || sh > 3) return false;
   if (g.obh * g.obw > 128 || g.obw * sw > 256 || g.obh * sh > 256) return false;
-#define X(CI, CO) if (cin == CI && cout == CO) return CCfg<CI, CO>::SMEM <= max_smem_optin();
+#define X(CI, CO, KS) if (cin == CI && cout == CO && kh == KS) return CCfg<CI, CO, KS>::SMEM <= max_smem_optin();
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   return false;
 }
 
-size_t sparse_conv_tma_packed_bytes(int cin, int cout) {
-#define X(CI, CO) if (cin == CI && cout == CO) return (size_t)CCfg<CI, CO>::WBYTES;
+size_t sparse_conv_tma_packed_bytes(int cin, int cout, int k) {
+#define X(CI, CO, KS) if (cin == CI && cout == CO && k == KS) return (size_t)CCfg<CI, CO, KS>::WBYTES;
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   return 0;
 }
 
-int sparse_conv_tma_pack(const void* w, int cin, int cout, void* img, cudaStream_t s) {
-#define X(CI, CO)                                                                                          \
-  if (cin == CI && cout == CO) {                                                                           \
-    conv_dense_pack_kernel<CI, CO><<<128, 256, 0, s>>>((const __nv_bfloat16*)w, (uint8_t*)img);          \
-    return launch_status("sparse_conv_tma_pack");                                                          \
+int sparse_conv_tma_pack(const void* w, int cin, int cout, int k, void* img, cudaStream_t s) {
+#define X(CI, CO, KS)                                                                                      \
+  if (cin == CI && cout == CO && k == KS) {                                                                \
+    conv_dense_pack_kernel<CI, CO, KS><<<128, 256, 0, s>>>((const __nv_bfloat16*)w, (uint8_t*)img);      \
+    return launch_status("conv_tma_pack");                                                                 \
   }
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
-  set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d", cin, cout);
+  set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d kernel=%d", cin, cout, k);
   return SBN_ERR_UNSUPPORTED;
 }
 
-int sparse_conv_tma(const void* x, int cin, int cout, int sh, int sw, const Geo& g, const void* wpk,
+int sparse_conv_tma(const void* x, int cin, int cout, int k, int sh, int sw, const Geo& g, const void* wpk,
                     const void* bias, const int32_t* idx, const int32_t* count, int cap, void* dst,
                     cudaStream_t s) {
-#define X(CI, CO)                                                                                           \
-  if (cin == CI && cout == CO)                                                                              \
-    return launch_dense<CI, CO>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, idx, \
-                                count, cap, (const __nv_bfloat16*)bias);
+#define X(CI, CO, KS)                                                                                            \
+  if (cin == CI && cout == CO && k == KS)                                                                        \
+    return launch_dense<CI, CO, KS>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, idx, \
+                                    count, cap, (const __nv_bfloat16*)bias);
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
-  set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d", cin, cout);
+  set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d kernel=%d", cin, cout, k);
   return SBN_ERR_UNSUPPORTED;
 }
 
@@ -416,44 +421,31 @@ int sparse_conv_tma(const void* x, int cin, int cout, int sh, int sw, const Geo&
 using namespace sbn;
 
 extern "C" int sbn_dense_conv_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw) {
-  if (dtype != SBN_BF16 || kh != 3 || kw != 3 || sh < 1 || sw < 1 || sh > 3 || sw > 3) return 0;
-#define X(CI, CO) if (cin == CI && cout == CO) return CCfg<CI, CO>::SMEM <= max_smem_optin() ? 1 : 0;
+  if (dtype != SBN_BF16 || kh != kw || sh != sw || sh < 1 || sh > kh || sh > 3) return 0;
+#define X(CI, CO, KS) if (cin == CI && cout == CO && kh == KS) return CCfg<CI, CO, KS>::SMEM <= max_smem_optin() ? 1 : 0;
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   return 0;
 }
 
-extern "C" size_t sbn_dense_conv_packed_bytes(int cin, int cout) {
-#define X(CI, CO) if (cin == CI && cout == CO) return (size_t)CCfg<CI, CO>::WBYTES;
-  SBN_DENSE_CONV_CONFIGS(X)
-#undef X
-  return 0;
-}
+extern "C" size_t sbn_dense_conv_packed_bytes(int cin, int cout, int k) { return sparse_conv_tma_packed_bytes(cin, cout, k); }
 
-extern "C" int sbn_dense_conv_pack(const void* w, int cin, int cout, void* packed, sbn_stream_t stream) {
+extern "C" int sbn_dense_conv_pack(const void* w, int cin, int cout, int k, void* packed, sbn_stream_t stream) {
   SBN_CHECK_ARG(w && packed, SBN_ERR_INVALID, "null argument");
-#define X(CI, CO)                                                                                          \
-  if (cin == CI && cout == CO) {                                                                           \
-    conv_dense_pack_kernel<CI, CO><<<128, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)w,         \
-                                                                          (uint8_t*)packed);               \
-    return launch_status("dense_conv_pack");                                                              \
-  }
-  SBN_DENSE_CONV_CONFIGS(X)
-#undef X
-  set_error("no tcgen05 dense conv instantiation for cin=%d cout=%d", cin, cout);
-  return SBN_ERR_UNSUPPORTED;
+  return sparse_conv_tma_pack(w, cin, cout, k, packed, (cudaStream_t)stream);
 }
 
-extern "C" int sbn_dense_conv(const void* x, int n, int h, int w, int cin, int cout, int sh, int sw, int ph,
-                              int pw, int oh, int ow, const void* packed, const float* bias, void* out,
+extern "C" int sbn_dense_conv(const void* x, int n, int h, int w, int cin, int cout, int k, int sh, int sw,
+                              int ph, int pw, int oh, int ow, const void* packed, const float* bias, void* out,
                               sbn_stream_t stream) {
   SBN_CHECK_ARG(x && packed && bias && out, SBN_ERR_INVALID, "null pointer argument");
   SBN_CHECK_ARG(n > 0 && h > 0 && w > 0 && oh > 0 && ow > 0, SBN_ERR_SHAPE, "bad dims");
-  SBN_CHECK_ARG(sbn_dense_conv_supported(SBN_BF16, cin, cout, 3, 3, sh, sw), SBN_ERR_UNSUPPORTED,
-                "tcgen05 dense conv does not support cin=%d cout=%d stride (%d,%d)", cin, cout, sh, sw);
+  SBN_CHECK_ARG(sbn_dense_conv_supported(SBN_BF16, cin, cout, k, k, sh, sw), SBN_ERR_UNSUPPORTED,
+                "tcgen05 dense conv does not support cin=%d cout=%d kernel %d stride (%d,%d)", cin, cout, k, sh, sw);
   cudaStream_t s = (cudaStream_t)stream;
-#define X(CI, CO) \
-  if (cin == CI && cout == CO) return launch_dense<CI, CO>(x, n, h, w, sh, sw, ph, pw, oh, ow, packed, bias, out, s);
+#define X(CI, CO, KS)                                                                                       \
+  if (cin == CI && cout == CO && k == KS)                                                                   \
+    return launch_dense<CI, CO, KS>(x, n, h, w, sh, sw, ph, pw, oh, ow, packed, bias, out, s);
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   return SBN_ERR_UNSUPPORTED;

@@ -105,9 +105,9 @@ int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, con
 size_t sparse_conv_tc_packed_bytes(int cin, int cout);
 int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_t s);
 bool sparse_conv_tma_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g);
-size_t sparse_conv_tma_packed_bytes(int cin, int cout);
-int sparse_conv_tma_pack(const void* w, int cin, int cout, void* img, cudaStream_t s);
-int sparse_conv_tma(const void* x, int cin, int cout, int sh, int sw, const Geo& g, const void* wpk,
+size_t sparse_conv_tma_packed_bytes(int cin, int cout, int k);
+int sparse_conv_tma_pack(const void* w, int cin, int cout, int k, void* img, cudaStream_t s);
+int sparse_conv_tma(const void* x, int cin, int cout, int k, int sh, int sw, const Geo& g, const void* wpk,
                     const void* bias, const int32_t* idx, const int32_t* count, int cap, void* dst,
                     cudaStream_t s);
 bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
@@ -137,7 +137,7 @@ extern "C" size_t sbn_sparse_conv_packed_bytes(int dtype, int cin, int cout, int
   if (!gp) return 0;
   switch (conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp))) {
     case 1: return sparse_conv_tc_packed_bytes(cin, cout);
-    case 2: return sparse_conv_tma_packed_bytes(cin, cout);
+    case 2: return sparse_conv_tma_packed_bytes(cin, cout, kh);
     default: return 0;
   }
 }
@@ -150,7 +150,7 @@ extern "C" int sbn_sparse_conv_pack(const void* w, int dtype, int cin, int cout,
   const int kind = conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, to_geo(gp));
   SBN_CHECK_ARG(kind != 0, SBN_ERR_UNSUPPORTED, "tcgen05 sparse conv does not support this config");
   SBN_CHECK_ARG(w && packed, SBN_ERR_INVALID, "null argument");
-  if (kind == 2) return sparse_conv_tma_pack(w, cin, cout, packed, (cudaStream_t)stream);
+  if (kind == 2) return sparse_conv_tma_pack(w, cin, cout, kh, packed, (cudaStream_t)stream);
   return sparse_conv_tc_pack(w, cin, cout, packed, (cudaStream_t)stream);
 }
 
@@ -178,14 +178,14 @@ extern "C" int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int 
   if (kind != 0 && algo != SBN_ALGO_SIMT) {
     const void* wpk = w_packed;
     if (!wpk) {
-      const size_t nb = kind == 1 ? sparse_conv_tc_packed_bytes(cin, cout) : sparse_conv_tma_packed_bytes(cin, cout);
+      const size_t nb = kind == 1 ? sparse_conv_tc_packed_bytes(cin, cout) : sparse_conv_tma_packed_bytes(cin, cout, kh);
       SBN_CHECK_ARG(ws && ws_bytes >= nb, SBN_ERR_WORKSPACE,
                     "tcgen05 sparse conv without a packed weight image needs a %zu-byte workspace", nb);
-      int st2 = kind == 1 ? sparse_conv_tc_pack(w, cin, cout, ws, s) : sparse_conv_tma_pack(w, cin, cout, ws, s);
+      int st2 = kind == 1 ? sparse_conv_tc_pack(w, cin, cout, ws, s) : sparse_conv_tma_pack(w, cin, cout, kh, ws, s);
       if (st2) return st2;
       wpk = ws;
     }
-    if (kind == 2) return sparse_conv_tma(x, cin, cout, sh, sw, g, wpk, bias, idx, count, cap, dst, s);
+    if (kind == 2) return sparse_conv_tma(x, cin, cout, kh, sh, sw, g, wpk, bias, idx, count, cap, dst, s);
     return sparse_conv_tc(x, cin, cout, g, wpk, bias, idx, count, cap, dst, s);
   }
   switch (dtype) {

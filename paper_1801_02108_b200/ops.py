@@ -185,7 +185,7 @@ def dense_conv_nhwc(x: torch.Tensor, w_hwio: torch.Tensor, bias, stride, pad) ->
 
 def projection_conv(t: torch.Tensor, f: FilterBank, p: ConvParams) -> torch.Tensor:
     """Dense conv + bias of an NHWC CUDA tensor — the stage-transition projection of
-    `run_stage` (reference `layers.py:316-318`).  bf16 3x3 shapes with a tcgen05
+    `run_stage` (reference `layers.py:316-318`).  bf16 1x1 / 3x3 / 5x5 shapes with a tcgen05
     instantiation run `sbn_dense_conv` (bias fused in the epilogue: no separate bias pass);
     other shapes and dtypes run cuDNN."""
     from . import _lib
@@ -197,8 +197,9 @@ def projection_conv(t: torch.Tensor, f: FilterBank, p: ConvParams) -> torch.Tens
         key = ("dense_tc", str(t.device))
         if key not in f._cache:
             wt, bt = f.device_tensors(torch.bfloat16, t.device)
-            img = torch.empty(int(lib.sbn_dense_conv_packed_bytes(c, f.c_out)), dtype=torch.uint8, device=t.device)
-            _lib.check(lib.sbn_dense_conv_pack(wt.data_ptr(), c, f.c_out, img.data_ptr(),
+            img = torch.empty(int(lib.sbn_dense_conv_packed_bytes(c, f.c_out, kh)), dtype=torch.uint8,
+                              device=t.device)
+            _lib.check(lib.sbn_dense_conv_pack(wt.data_ptr(), c, f.c_out, kh, img.data_ptr(),
                                                _lib.stream_handle(t.device)), "dense_conv_pack")
             bf = (bt.float() if bt is not None else torch.zeros(f.c_out, device=t.device)).contiguous()
             f._cache[key] = (img, bf)
@@ -206,7 +207,7 @@ def projection_conv(t: torch.Tensor, f: FilterBank, p: ConvParams) -> torch.Tens
         oh, ow = p.out_size(h, w)
         out = torch.empty((n, oh, ow, f.c_out), dtype=t.dtype, device=t.device)
         tc_ = t.contiguous()
-        _lib.check(lib.sbn_dense_conv(tc_.data_ptr(), n, h, w, c, f.c_out, p.stride[0], p.stride[1], p.pad[0],
+        _lib.check(lib.sbn_dense_conv(tc_.data_ptr(), n, h, w, c, f.c_out, kh, p.stride[0], p.stride[1], p.pad[0],
                                       p.pad[1], oh, ow, img.data_ptr(), bf.data_ptr(), out.data_ptr(),
                                       _lib.stream_handle(t.device)), "dense_conv")
         return out

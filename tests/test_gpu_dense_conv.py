@@ -1,4 +1,4 @@
-"""tcgen05 dense 3x3 conv with fused bias (sbn_dense_conv): the config-4 stage projections
+"""tcgen05 dense 1x1 / 3x3 / 5x5 conv with fused bias (sbn_dense_conv): the config-4 stage projections
 (stride 2) and square stride-1 shapes vs cuDNN in fp32 on the same bf16-rounded inputs;
 bf16 output rounding -> rel_err <= 1e-2."""
 import numpy as np
@@ -12,20 +12,21 @@ from oracle import sbnet_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,h,w,cin,cout,stride,same", [
-    (2, 50, 38, 32, 96, 2, True), (1, 37, 29, 96, 192, 2, True), (2, 22, 19, 192, 256, 2, True),
-    (1, 14, 12, 256, 384, 2, True), (1, 40, 33, 64, 64, 1, True), (2, 17, 35, 128, 128, 1, False),
-    (1, 24, 24, 32, 32, 3, True)])
-def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, same):
-    rng = np.random.default_rng(cin + cout + stride)
+@pytest.mark.parametrize("n,h,w,cin,cout,stride,same,k", [
+    (2, 50, 38, 32, 96, 2, True, 3), (1, 37, 29, 96, 192, 2, True, 3), (2, 22, 19, 192, 256, 2, True, 3),
+    (1, 14, 12, 256, 384, 2, True, 3), (1, 40, 33, 64, 64, 1, True, 3), (2, 17, 35, 128, 128, 1, False, 3),
+    (1, 24, 24, 32, 32, 3, True, 3), (2, 31, 27, 64, 64, 1, True, 1), (1, 33, 40, 128, 128, 1, False, 1),
+    (2, 29, 23, 32, 32, 1, True, 5), (1, 26, 31, 64, 64, 2, False, 5), (1, 19, 22, 32, 32, 3, True, 5)])
+def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, same, k):
+    rng = np.random.default_rng(cin + cout + stride + 7 * k)
     x = torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16().cuda()
-    wt = (rng.standard_normal((3, 3, cin, cout)) / np.sqrt(9 * cin)).astype(np.float32)
+    wt = (rng.standard_normal((k, k, cin, cout)) / np.sqrt(k * k * cin)).astype(np.float32)
     b = rng.standard_normal(cout).astype(np.float32)
     f = P.FilterBank(torch.from_numpy(wt).bfloat16(), torch.from_numpy(b).bfloat16())
-    p = P.ConvParams((3, 3), (stride, stride), P.Padding.SAME if same else P.Padding.VALID, cout)
+    p = P.ConvParams((k, k), (stride, stride), P.Padding.SAME if same else P.Padding.VALID, cout)
     lib = P._lib.load() if hasattr(P, "_lib") else None
     from paper_1801_02108_b200 import _lib
-    assert _lib.load().sbn_dense_conv_supported(2, cin, cout, 3, 3, stride, stride) == 1
+    assert _lib.load().sbn_dense_conv_supported(2, cin, cout, k, k, stride, stride) == 1
     y = projection_conv(x, f, p).float().cpu().numpy()
     fb32 = P.FilterBank(torch.from_numpy(wt).bfloat16().float(), torch.from_numpy(b).bfloat16().float())
     ref = P.conv2d_direct(P.Tensor4D(x.float()), fb32, p).data.cpu().numpy()
@@ -34,19 +35,20 @@ def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, sa
     del lib
 
 
-@pytest.mark.parametrize("cin,cout,stride,block,same", [
-    (64, 64, 2, 17, True), (128, 128, 2, 13, True), (32, 96, 1, 10, True), (64, 64, 3, 24, False),
-    (96, 192, 2, 9, True)])
-def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, block, same):
-    """Strided / other-shape sparse 3x3 convs on the TMA tap-GEMM path (kernel variant 2)
-    against the fp32 oracle on bf16-rounded inputs."""
-    rng = np.random.default_rng(stride * 100 + block)
+@pytest.mark.parametrize("cin,cout,stride,block,same,k", [
+    (64, 64, 2, 17, True, 3), (128, 128, 2, 13, True, 3), (32, 96, 1, 10, True, 3), (64, 64, 3, 24, False, 3),
+    (96, 192, 2, 9, True, 3), (64, 64, 1, 12, True, 1), (128, 128, 1, 11, False, 1), (32, 32, 1, 14, True, 5),
+    (64, 64, 1, 20, False, 5), (64, 64, 2, 17, True, 5)])
+def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, block, same, k):
+    """Strided / other-shape sparse 1x1 / 3x3 / 5x5 convs on the TMA tap-GEMM path (kernel
+    variant 2) against the fp32 oracle on bf16-rounded inputs."""
+    rng = np.random.default_rng(stride * 100 + block + 1000 * k)
     n, h, w = 2, 53, 47
     x = torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16()
-    wt = torch.from_numpy((rng.standard_normal((3, 3, cin, cout)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16()
+    wt = torch.from_numpy((rng.standard_normal((k, k, cin, cout)) / np.sqrt(k * k * cin)).astype(np.float32)).bfloat16()
     b = torch.from_numpy(rng.standard_normal(cout).astype(np.float32)).bfloat16()
     mk = (rng.random((n, h, w)) < 0.03).astype(np.uint8)
-    p = P.ConvParams((3, 3), (stride, stride), P.Padding.SAME if same else P.Padding.VALID, cout)
+    p = P.ConvParams((k, k), (stride, stride), P.Padding.SAME if same else P.Padding.VALID, cout)
     spec = P.compute_block_spec((n, h, w, cin), p, (block, block))
     from paper_1801_02108_b200.layers import sparse_conv_algo
     assert sparse_conv_algo(torch.bfloat16, P.FilterBank(wt, b), p, spec) == "tcgen05"
