@@ -100,7 +100,7 @@ __device__ __forceinline__ int ld_count(const int32_t* count, int cap) {
 // ---- optional phase tracing (diagnostics): kernels record %globaltimer at phase
 // boundaries into trace[cta * kTraceSlots + phase] when a buffer has been set with
 // sbn_debug_set_trace() (passed to kernels as an argument; null check otherwise).
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 32;
 unsigned long long* trace_buffer();  // host side: current buffer or nullptr
 int debug_flags();                   // host side: sbn_debug_set_flags()
 enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4 };

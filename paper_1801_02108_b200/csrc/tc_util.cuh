@@ -115,6 +115,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // 16-byte asynchronous global -> shared copy (LDGSTS, no register staging); src_ok = false
 // zero-fills the destination without reading global memory
+// 16-byte global load, zero when !pred: one predicated LDG in a straight-line block, so a
+// run of these keeps every load in flight before the first use (a branchy if/else per load
+// makes the scheduler consume each result in its own block -> serial round trips).
+__device__ __forceinline__ uint4 ld_v4_pred(const void* p, bool pred) {
+  uint4 v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+      " mov.b32 %2, 0;\n mov.b32 %3, 0;\n @q ld.global.v4.u32 {%0, %1, %2, %3}, [%4];\n}"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "r"((int)pred));
+  return v;
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool src_ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
                "r"(src_ok ? 16 : 0)

@@ -426,7 +426,7 @@ extern "C" size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, co
                                                      int halo, int algo) {
   if (!gp || dtype_size(dtype) == 0) return 0;
   const size_t cap = (size_t)gp->n * gp->gy * gp->gx;
-  return al256(cap * 12) + 256 + al256(cap * 4) + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
+  return al256(cap * 12) + 256 + al256(cap * 8) + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
 }
 
 extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
@@ -448,8 +448,8 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
   uint8_t* w8 = (uint8_t*)ws;
   int32_t* idx = (int32_t*)w8;
   int32_t* count = (int32_t*)(w8 + al256((size_t)cap * 12));
-  unsigned int* etag = (unsigned int*)(w8 + al256((size_t)cap * 12) + 256);
-  uint8_t* uws = w8 + al256((size_t)cap * 12) + 256 + al256((size_t)cap * 4);  // [bar | rim | pack]
+  unsigned long long* etag = (unsigned long long*)(w8 + al256((size_t)cap * 12) + 256);
+  uint8_t* uws = w8 + al256((size_t)cap * 12) + 256 + al256((size_t)cap * 8);  // [bar | rim | pack]
   uint8_t* sync8 = (uint8_t*)sync_ws;
   unsigned int* gbar = reinterpret_cast<unsigned int*>(sync8);
   unsigned long long* cst = reinterpret_cast<unsigned long long*>(sync8 + kBarBytes);

@@ -89,7 +89,7 @@ struct TcArgs {
   unsigned long long* trace;
   const uint8_t* mask;     // non-null: fused reduce_mask (MAX) + compaction into idx/count
   unsigned long long* cst; // (unused; reserved)
-  unsigned int* etag;      // slot compaction: per-entry publication tag (scratch ws)
+  unsigned long long* etag;  // slot compaction: per-entry (launch tag << 32 | candidate) word
   int32_t* idx_out;
   int32_t* count_out;
   const int32_t* idx;
@@ -101,14 +101,19 @@ __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162
 
 // ---- slot compaction (fused mask reduction of the single-kernel sparse_residual_unit).
 // Producers: CTA c tests candidates c, c+G, ... against the mask, claims list slots for its
-// active ones with ONE atomic per round, writes each entry and publishes it with the
-// launch's tag (release); then it increments `done`.  Consumers only wait for the entry
+// active ones with ONE atomic per round, publishes each entry as one 64-bit word
+// (launch tag << 32 | candidate: a single-copy-atomic store, so no release fence and no
+// second read on the consumer side), starts the L2 prefetch of the block's window (the
+// consumer's HBM read overlaps the hand-off), then increments `done`.  Consumers only wait for the entry
 // they process (or for done == G to learn that no more entries are coming).  In place,
 // the halo hazard is resolved just before the first store (slot_before_store).  Nothing is
-// reset on the critical path: the last CTA out clears the words and bumps the epoch, and
-// tags make stale entries from earlier launches invisible.
-//   words (sync ws, u32): [8] epoch, [9] seen, [10] slot counter, [11] done, [12] staged,
-//                         [13..14] grid barrier (streamed in-place only)
+// reset on the critical path and no CTA does a global atomic on its way out: the counters
+// of launch `tag` live in ring slot tag & 1, and the LAST producer (its `done` increment
+// returns G-1, so every CTA has read the epoch) publishes the block count, bumps the epoch
+// and zeroes the other slot (its launch completed before this one passed
+// griddepcontrol.wait; the next launch will use it).  Tags make stale entries invisible.
+//   words (sync ws, u32): [8] epoch, [13..14] grid barrier (streamed in-place only),
+//                         [16 + 4 * (tag & 1) + {0 slot counter, 1 done, 2 staged}]
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -118,12 +123,44 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag) {
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned* slot_ring(const TcArgs& a, unsigned tag) { return a.gbar + 16 + 4 * (tag & 1u); }
+__device__ __forceinline__ unsigned long long slot_word(unsigned tag, int cand) {
+  return ((unsigned long long)tag << 32) | (unsigned)cand;
+}
+
+// Returns this launch's tag (epoch + 1); the epoch load overlaps the mask loads.  Thread 32
+// gets the old value of its `done` increment in `done_old`; it is only consumed by
+// slot_last_producer, after the CTA has polled for its entry (the round trip overlaps).
+template <int C, int BS>
+__device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done_old) {
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int s_flag[32];
   __shared__ int s_base;
-  unsigned* w = a.gbar + 8;
+  __shared__ unsigned s_tag;
+  unsigned ep = 0;
+  if (tid == 0) ep = ld_relaxed_u32(a.gbar + 8);
   const int T = g.n * g.gy * g.gx;
   const int area = g.bh * g.bw;
   const int G = gridDim.x;
@@ -131,46 +168,78 @@ __device__ __forceinline__ void slot_produce(const TcArgs& a, unsigned tag) {
     const int nj = min(32, (T - r0 + G - 1) / G);
     if (tid < 32) s_flag[tid] = 0;
     __syncthreads();
-    for (int e = tid; e < nj * area; e += kThreads) {
-      const int j = e / area, p = e - j * area;
-      const int cand = r0 + j * G;
-      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-      const int cy = rr / g.gx, cx = rr - cy * g.gx;
-      const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
-      if (y >= 0 && y < g.h && xx >= 0 && xx < g.w && __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx))
-        s_flag[j] = 1;
+    constexpr int U = 4;  // loads in flight per thread before any is tested
+    for (int e0 = tid; e0 < nj * area; e0 += U * kThreads) {
+      uint8_t v[U];
+      int jj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * kThreads;
+        const int j = e / area, p = e - j * area;
+        const int cand = r0 + j * G;
+        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+        const int cy = rr / g.gx, cx = rr - cy * g.gx;
+        const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
+        jj[u] = j;
+        v[u] = (e < nj * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+                   ? __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (v[u]) s_flag[jj[u]] = 1;
     }
+    if (tid == 0) s_tag = ep + 1u;
     __syncthreads();
+    trace(a.trace, 12);
+    const unsigned tag = s_tag;
     if (warp == 0) {
       const bool on = lane < nj && s_flag[lane];
       const unsigned bal = __ballot_sync(0xffffffffu, on);
-      if (lane == 0) s_base = bal ? (int)atomicAdd(w + 2, (unsigned)__popc(bal)) : 0;
+      if (lane == 0) s_base = bal ? (int)atomicAdd(slot_ring(a, tag), (unsigned)__popc(bal)) : 0;
       __syncwarp();
       if (on) {
         const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
         const int cand = r0 + lane * G;
         const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+        const int by = rr / g.gx, bx = rr % g.gx;
+        st_relaxed_u64(&a.etag[pos], slot_word(tag, cand));
         a.idx_out[3 * pos] = fr;
-        a.idx_out[3 * pos + 1] = rr / g.gx;
-        a.idx_out[3 * pos + 2] = rr % g.gx;
-        st_release_u32(&a.etag[pos], tag);
+        a.idx_out[3 * pos + 1] = by;
+        a.idx_out[3 * pos + 2] = bx;
+        const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
+        const int x0 = max(xs, 0), x1 = min(xs + BS, g.w);
+        if (x1 > x0)
+          for (int wy = max(0, -ys); wy < BS && ys + wy < g.h; ++wy)
+            tc::prefetch_l2(a.x + (((size_t)fr * g.h + ys + wy) * g.w + x0) * C, (uint32_t)((x1 - x0) * C * 2));
       }
     }
   }
+  if (T <= (int)blockIdx.x && tid == 0) s_tag = ep + 1u;  // no candidate for this CTA
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    atomicAdd(w + 3, 1u);  // this producer is done
+  const unsigned tag = s_tag;
+  if (tid == 32) done_old = atom_add_release(slot_ring(a, tag) + 1, 1u);
+  trace(a.trace, 14);
+  return tag;
+}
+
+// The last producer (done_old == G - 1: every CTA has read the epoch) publishes the block
+// count, zeroes the other ring slot and bumps the epoch.
+__device__ __forceinline__ void slot_last_producer(const TcArgs& a, unsigned tag, unsigned done_old) {
+  if (threadIdx.x == 32 && done_old == gridDim.x - 1) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    *a.count_out = (int)ld_relaxed_u32(slot_ring(a, tag));
+    unsigned* other = slot_ring(a, tag + 1u);
+    other[0] = 0u;
+    other[1] = 0u;
+    other[2] = 0u;
+    a.gbar[8] = tag;
   }
 }
 
 // In-place fused: called by every consumer CTA after staging its FIRST window.
-__device__ __forceinline__ void slot_staged(const TcArgs& a) {
+__device__ __forceinline__ void slot_staged(const TcArgs& a, unsigned tag) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(a.gbar + 12, 1u);
-  }
+  if (threadIdx.x == 0) red_add_release(slot_ring(a, tag) + 2, 1u);
 }
 
 // In-place fused, before the first store of the first block.  If every block had its own
@@ -180,16 +249,15 @@ __device__ __forceinline__ void slot_staged(const TcArgs& a) {
 // grid barrier (every CTA is active then).  Returns true when later rounds must read rims
 // from the snapshot.
 template <int C, int BS>
-__device__ __forceinline__ bool slot_before_store(const TcArgs& a, int ncons, int ctas_per_block) {
+__device__ __forceinline__ bool slot_before_store(const TcArgs& a, unsigned tag, int ncons, int ctas_per_block) {
   __shared__ int s_B;
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned* w = a.gbar + 8;
-    while (ld_acquire_u32(w + 3) != gridDim.x) __nanosleep(32);
-    s_B = (int)ld_acquire_u32(w + 2);
-    if (blockIdx.x == 0) *a.count_out = s_B;
+    unsigned* ring = slot_ring(a, tag);
+    while (ld_acquire_u32(ring + 1) != gridDim.x) __nanosleep(32);
+    s_B = (int)ld_acquire_u32(ring);
     if (s_B <= ncons)
-      while (ld_acquire_u32(a.gbar + 12) < (unsigned)(s_B * ctas_per_block)) __nanosleep(32);
+      while (ld_acquire_u32(ring + 2) < (unsigned)(s_B * ctas_per_block)) __nanosleep(32);
   }
   __syncthreads();
   const int B = s_B;
@@ -222,24 +290,30 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
   if (blk >= a.g.n * a.g.gy * a.g.gx) return false;  // more consumers than candidates
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned* w = a.gbar + 8;
+    unsigned* ring = slot_ring(a, tag);
     int ok = 0;
+    unsigned long long e = 0;
     while (true) {
-      if (ld_acquire_u32(&a.etag[blk]) == tag) {
+      e = ld_relaxed_u64(&a.etag[blk]);
+      if ((unsigned)(e >> 32) == tag) {
         ok = 1;
         break;
       }
-      if (ld_acquire_u32(w + 3) == gridDim.x) {  // all producers done
-        ok = ld_acquire_u32(&a.etag[blk]) == tag ? 1 : 0;
+      if (ld_acquire_u32(ring + 1) == gridDim.x) {  // all producers done
+        e = ld_relaxed_u64(&a.etag[blk]);
+        ok = (unsigned)(e >> 32) == tag ? 1 : 0;
         break;
       }
       __nanosleep(20);
     }
     s_e[3] = ok;
     if (ok) {
-      s_e[0] = __ldcg(a.idx_out + 3 * blk);
-      s_e[1] = __ldcg(a.idx_out + 3 * blk + 1);
-      s_e[2] = __ldcg(a.idx_out + 3 * blk + 2);
+      const Geo& g = a.g;
+      const int cand = (int)(unsigned)e;
+      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+      s_e[0] = fr;
+      s_e[1] = rr / g.gx;
+      s_e[2] = rr % g.gx;
     }
   }
   __syncthreads();
@@ -256,36 +330,25 @@ __device__ __forceinline__ void prefetch_window(const TcArgs& a, const int32_t* 
                                                 int blk) {
   const Geo& g = a.g;
   if (threadIdx.x >= 32 || blk >= g.n * g.gy * g.gx) return;
+  int n, by, bx;
   if (tag) {
-    if (ld_acquire_u32(&a.etag[blk]) != tag) return;
-  } else if (blk >= ld_count(a.count, a.cap)) {
-    return;
+    const unsigned long long e = ld_relaxed_u64(&a.etag[blk]);
+    if ((unsigned)(e >> 32) != tag) return;
+    const int cand = (int)(unsigned)e;
+    n = cand / (g.gy * g.gx);
+    const int rr = cand - n * (g.gy * g.gx);
+    by = rr / g.gx;
+    bx = rr % g.gx;
+  } else {
+    if (blk >= ld_count(a.count, a.cap)) return;
+    n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
   }
-  const int n = __ldcg(idx + 3 * blk), by = __ldcg(idx + 3 * blk + 1), bx = __ldcg(idx + 3 * blk + 2);
   const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
   const int x0 = max(xs, 0), x1 = min(xs + BS, g.w);
   const int wy = threadIdx.x;
   const int y = ys + wy;
   if (wy < BS && y >= 0 && y < g.h && x1 > x0)
     tc::prefetch_l2(a.x + (((size_t)n * g.h + y) * g.w + x0) * C, (uint32_t)((x1 - x0) * C * 2));
-}
-
-// Last CTA out clears the words and bumps the epoch (all CTAs have read them).
-__device__ __forceinline__ void slot_finish(const TcArgs& a, unsigned tag) {
-  if (!tag) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned* w = a.gbar + 8;
-    if (atomicAdd(w + 1, 1u) == gridDim.x - 1) {
-      w[1] = 0u;
-      w[2] = 0u;
-      w[3] = 0u;
-      w[4] = 0u;  // staged counter
-      w[0] = tag;  // next launch uses tag + 1
-      __threadfence();
-    }
-  }
 }
 
 template <int C, int MC, int BS>
@@ -351,10 +414,11 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   const bool fused = a.mask != nullptr;
   bool have;
   if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
-    tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
-    slot_produce(a, tag);
+    unsigned done_old = 0;
+    tag = slot_produce<C, BS>(a, done_old);
     idx = a.idx_out;
     have = slot_entry(a, tag, blockIdx.x, n0, by0, bx0);
+    slot_last_producer(a, tag, done_old);
   } else {
     if ((int)blockIdx.x < a.cap) {  // speculative: the first block's row, loaded alongside the count
       n0 = __ldg(idx + 3 * blockIdx.x);
@@ -403,7 +467,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     __syncthreads();
     tc::fence_after();
     if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
-    slot_finish(a, tag);
     return;
   }
 
@@ -415,7 +478,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   for (int blk = blockIdx.x;;) {
     const int n = n0, by = by0, bx = bx0;
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
-    prefetch_window<C, BS>(a, idx, tag, blk + gridDim.x);
 
     // ---- 1. stage the window: all loads in flight first, then BN1 + ReLU -> bf16 planes
     constexpr int TOT = K::NPIX * (C / 8);
@@ -427,19 +489,19 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
       const int p = i / (C / 8), k = i % (C / 8);
       const int wy = p / BS, wx = p % BS;
       const int y = ys + wy, xx = xs + wx;
-      raw[it] = make_uint4(0, 0, 0, 0);
-      if (i < TOT) {
-        if (rimsrc && !rim.interior(wy, wx))
-          raw[it] = *(reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
-        else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-          raw[it] = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
-      }
+      const bool from_rim = rimsrc && !rim.interior(wy, wx);
+      const bool inb = y >= 0 && y < g.h && xx >= 0 && xx < g.w;
+      const uint4* src = from_rim
+          ? reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k
+          : reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + (inb ? y : 0)) * g.w + (inb ? xx : 0)) * (C / 8) + k;
+      raw[it] = tc::ld_v4_pred(src, (i < TOT) && (from_rim || inb));
     }
     trace(a.trace, 3);
+    prefetch_window<C, BS>(a, idx, tag, blk + gridDim.x);  // after this block's loads are issued
     // in place + resident: announce "my window is read"; the matching wait sits right
     // before the first store of epilogue 3, so it overlaps the three GEMMs
     if (inplace && resident) grid_arrive(a.gbar);
-    if (first_store) slot_staged(a);
+    if (first_store) slot_staged(a, tag);
     trace(a.trace, 4);
     if (!weights_ready) {
       tc::mbar_wait(&wbar, 0);
@@ -595,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
     if (inplace && resident) grid_wait(a.gbar, (unsigned)B);  // neighbours have read my rim
     if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
-      if (slot_before_store<C, BS>(a, (int)gridDim.x, 1)) rimsrc = a.rim_buf;
+      if (slot_before_store<C, BS>(a, tag, (int)gridDim.x, 1)) rimsrc = a.rim_buf;
       first_store = false;
     }
     trace(a.trace, 10);
@@ -649,7 +711,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
   tc::fence_after();
   if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
-  slot_finish(a, tag);
 }
 
 // Pre-pack W1/W2/W3 (transposed into the K-major plane layout) and the float params into
@@ -858,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   trace(a.trace, 1);
   tc::pdl_trigger();
   tc::pdl_wait();
+  trace(a.trace, 16);
   int B = 0;
   const int32_t* idx = a.idx;
   unsigned tag = 0;
@@ -866,10 +928,11 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   int n1 = 0, by1 = 0, bx1 = 0;
   bool have;
   if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
-    tag = *reinterpret_cast<volatile unsigned*>(a.gbar + 8) + 1u;
-    slot_produce(a, tag);
+    unsigned done_old = 0;
+    tag = slot_produce<C, BS>(a, done_old);
     idx = a.idx_out;
     have = slot_entry(a, tag, pair, n1, by1, bx1);
+    slot_last_producer(a, tag, done_old);
   } else {
     B = ld_count(a.count, a.cap);
     have = pair < B;
@@ -909,7 +972,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     __syncthreads();
     tc::fence_after();
     if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
-    slot_finish(a, tag);
+    trace(a.trace, 17);
     return;
   }
   const Rim rim{BS, BS, 1};
@@ -918,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
 
   for (int blk = pair;;) {
     const int n = n1, by = by1, bx = bx1;
-    if (rank == 0) prefetch_window<C, BS>(a, idx, tag, blk + npairs);
+    trace(a.trace, 18);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
     // ---- 1. stage my half of the window (pixels [128*rank, 128*rank + 128))
     constexpr int TOT = 128 * (C / 8);
@@ -931,17 +994,17 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
       const int p = rank * 128 + pl;
       const int wy = p / BS, wx = p % BS;
       const int y = ys + wy, xx = xs + wx;
-      raw[it] = make_uint4(0, 0, 0, 0);
-      if (p < K::NPIX) {
-        if (rimsrc && !rim.interior(wy, wx))
-          raw[it] = *(reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k);
-        else if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-          raw[it] = *(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (C / 8) + k);
-      }
+      const bool from_rim = rimsrc && !rim.interior(wy, wx);
+      const bool inb = y >= 0 && y < g.h && xx >= 0 && xx < g.w;
+      const uint4* src = from_rim
+          ? reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k
+          : reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + (inb ? y : 0)) * g.w + (inb ? xx : 0)) * (C / 8) + k;
+      raw[it] = tc::ld_v4_pred(src, (p < K::NPIX) && (from_rim || inb));
     }
     trace(a.trace, 3);
+    if (rank == 0) prefetch_window<C, BS>(a, idx, tag, blk + npairs);
     if (inplace && resident) grid_arrive(a.gbar);
-    if (first_store) slot_staged(a);
+    if (first_store) slot_staged(a, tag);
     trace(a.trace, 4);
     if (!weights_ready) {
       tc::mbar_wait(&wbar, 0);
@@ -1085,7 +1148,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     tc::fence_after();
     if (inplace && resident) grid_wait(a.gbar, 2u * (unsigned)B);
     if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
-      if (slot_before_store<C, BS>(a, npairs, 2)) rimsrc = a.rim_buf;
+      if (slot_before_store<C, BS>(a, tag, npairs, 2)) rimsrc = a.rim_buf;
       first_store = false;
     }
     trace(a.trace, 10);
@@ -1129,7 +1192,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   }
   tc::fence_after();
   if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);
-  slot_finish(a, tag);
+  trace(a.trace, 17);
 }
 
 template <int C, int MC, int BS>
@@ -1225,7 +1288,7 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
                    const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
                    const int32_t* count, int cap, cudaStream_t s, const uint8_t* mask,
                    int32_t* idx_out, int32_t* count_out, unsigned long long* cst,
-                   unsigned int* etag) {
+                   unsigned long long* etag) {
   TcArgs a = make_args(x, out, nullptr, g, p, idx, count, cap);
   a.mask = mask;
   a.idx_out = idx_out;

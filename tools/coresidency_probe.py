@@ -17,12 +17,12 @@ out = x.clone()
 lib.sbn_debug_set_flags(1)  # single-CTA kernel (grid sized from the computed residency)
 residual_unit_into(out, x, u, spec, idx)
 torch.cuda.synchronize()
-buf = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(4096 * 32, dtype=torch.int64, device="cuda")
 lib.sbn_debug_set_trace(buf.data_ptr())
 residual_unit_into(out, x, u, spec, idx)
 torch.cuda.synchronize()
 lib.sbn_debug_set_trace(None)
-t = buf.view(-1, 16).cpu().numpy()
+t = buf.view(-1, 32).cpu().numpy()
 g = t[t[:, 0] > 0]
 print("grid", len(g), "blocks", idx.count)
 ent = (g[:, 0] - g[:, 0].min()) / 1e3

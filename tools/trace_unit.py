@@ -37,7 +37,7 @@ def run(f):
 for f in range(nf):
     run(f)
 torch.cuda.synchronize()
-buf = torch.zeros(4096 * 16, dtype=torch.int64, device=dev)
+buf = torch.zeros(4096 * 32, dtype=torch.int64, device=dev)
 names = ["entry", "prologue", "pdl+count", "loads", "barrier", "staged", "gemm1", "epi1", "gemm2",
          "epi2", "gemm3", "epi3"]
 for f in range(4):
@@ -51,7 +51,7 @@ for f in range(4):
     torch.cuda.synchronize()
     lib.sbn_debug_set_trace(None)
     idx = P.reduce_mask(ms[f], spec)
-    t = buf.view(-1, 16).cpu().numpy().astype(np.int64)
+    t = buf.view(-1, 32).cpu().numpy().astype(np.int64)
     B = idx.count
     act = t[t[:, 11] > 0]  # CTAs that processed a block (2 per block in the CTA-pair variant)
     t0 = act[:, 0].min()
@@ -64,3 +64,7 @@ for f in range(4):
     for nm, a_, b_ in (("gemm1 issue", 5, 12), ("gemm2 issue", 7, 13), ("gemm3 issue", 9, 14)):
         dd = (act[:, b_] - act[:, a_]) / 1e3
         print(f"   {nm:>12}: median {np.median(dd):.2f} us (issue of all MMAs + commit, thread 0)")
+    if FUSED:
+        for nm, a_, b_ in (("prologue->mask flags", 1, 12), ("flags->done", 12, 14), ("done->entry", 14, 2)):
+            dd = (act[:, b_] - act[:, a_]) / 1e3
+            print(f"   {nm:>20}: median {np.median(dd):.2f} us  max {dd.max():.2f}")
