@@ -103,8 +103,9 @@ __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162
 // Producers: CTA c tests candidates c, c+G, ... against the mask, claims list slots for its
 // active ones with ONE atomic per round, publishes each entry as one 64-bit word
 // (launch tag << 32 | candidate: a single-copy-atomic store, so no release fence and no
-// second read on the consumer side), starts the L2 prefetch of the block's window (the
-// consumer's HBM read overlaps the hand-off), then increments `done`.  Consumers only wait for the entry
+// second read on the consumer side), then increments `done`.  (An L2 prefetch of the
+// window issued here by the producer measured slower: it delays `done`, which gates the
+// in-place stores.)  Consumers only wait for the entry
 // they process (or for done == G to learn that no more entries are coming).  In place,
 // the halo hazard is resolved just before the first store (slot_before_store).  Nothing is
 // reset on the critical path and no CTA does a global atomic on its way out: the counters
@@ -156,17 +157,25 @@ template <int C, int BS>
 __device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done_old) {
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ int s_flag[32];
+  __shared__ int s_flag[32], s_fr[32], s_y0[32], s_x0[32];
   __shared__ int s_base;
   __shared__ unsigned s_tag;
   unsigned ep = 0;
   if (tid == 0) ep = ld_relaxed_u32(a.gbar + 8);
   const int T = g.n * g.gy * g.gx;
-  const int area = g.bh * g.bw;
+  constexpr int area = BS * BS;  // the unit's window (bh == bw == BS)
   const int G = gridDim.x;
   for (int r0 = blockIdx.x; r0 < T; r0 += 32 * G) {
     const int nj = min(32, (T - r0 + G - 1) / G);
-    if (tid < 32) s_flag[tid] = 0;
+    if (tid < 32) {
+      s_flag[tid] = 0;
+      const int cand = r0 + tid * G;
+      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+      const int cy = rr / g.gx, cx = rr - cy * g.gx;
+      s_fr[tid] = fr;
+      s_y0[tid] = g.oy + cy * g.sy;
+      s_x0[tid] = g.ox + cx * g.sx;
+    }
     __syncthreads();
     constexpr int U = 4;  // loads in flight per thread before any is tested
     for (int e0 = tid; e0 < nj * area; e0 += U * kThreads) {
@@ -175,11 +184,9 @@ __device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int e = e0 + u * kThreads;
-        const int j = e / area, p = e - j * area;
-        const int cand = r0 + j * G;
-        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-        const int cy = rr / g.gx, cx = rr - cy * g.gx;
-        const int y = g.oy + cy * g.sy + p / g.bw, xx = g.ox + cx * g.sx + p % g.bw;
+        const int j = min(e / area, 31), p = e % area;
+        const int fr = s_fr[j];
+        const int y = s_y0[j] + p / BS, xx = s_x0[j] + p % BS;
         jj[u] = j;
         v[u] = (e < nj * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
                    ? __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx) : (uint8_t)0;
@@ -197,6 +204,7 @@ __device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done
       const unsigned bal = __ballot_sync(0xffffffffu, on);
       if (lane == 0) s_base = bal ? (int)atomicAdd(slot_ring(a, tag), (unsigned)__popc(bal)) : 0;
       __syncwarp();
+      if (bal) trace(a.trace, 19);
       if (on) {
         const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
         const int cand = r0 + lane * G;
@@ -206,11 +214,6 @@ __device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done
         a.idx_out[3 * pos] = fr;
         a.idx_out[3 * pos + 1] = by;
         a.idx_out[3 * pos + 2] = bx;
-        const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
-        const int x0 = max(xs, 0), x1 = min(xs + BS, g.w);
-        if (x1 > x0)
-          for (int wy = max(0, -ys); wy < BS && ys + wy < g.h; ++wy)
-            tc::prefetch_l2(a.x + (((size_t)fr * g.h + ys + wy) * g.w + x0) * C, (uint32_t)((x1 - x0) * C * 2));
       }
     }
   }
@@ -249,7 +252,8 @@ __device__ __forceinline__ void slot_staged(const TcArgs& a, unsigned tag) {
 // grid barrier (every CTA is active then).  Returns true when later rounds must read rims
 // from the snapshot.
 template <int C, int BS>
-__device__ __forceinline__ bool slot_before_store(const TcArgs& a, unsigned tag, int ncons, int ctas_per_block) {
+__device__ __forceinline__ bool slot_before_store(const TcArgs& a, unsigned tag, int ncons, int ctas_per_block,
+                                                  int& nblocks) {
   __shared__ int s_B;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -261,6 +265,7 @@ __device__ __forceinline__ bool slot_before_store(const TcArgs& a, unsigned tag,
   }
   __syncthreads();
   const int B = s_B;
+  nblocks = B;
   if (B <= ncons) return false;
   const Geo& g = a.g;
   const Rim r{BS, BS, 1};
@@ -441,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   const bool resident = !fused && B <= (int)gridDim.x;
   const __nv_bfloat16* rimsrc = a.rim;
   bool first_store = fused && inplace;  // slot_before_store still pending
+  int known_B = -1;                     // block count, once slot_before_store has read it
   if (!fused && inplace && !resident) {
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
@@ -607,11 +613,11 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
       const int r = tpar * 128 + q * 32 + lane;
       const int oy = r / BS, ox = r % BS;
       const int Y = by * g.obh + oy, X = bx * g.obw + ox;
-      if (oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow) {
-        const uint4* op = reinterpret_cast<const uint4*>(a.out) + (((size_t)n * g.oh + Y) * g.ow + X) * (C / 8);
+      const bool st = oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow;
+      const uint4* op = reinterpret_cast<const uint4*>(a.out) +
+                        (((size_t)n * g.oh + (st ? Y : 0)) * g.ow + (st ? X : 0)) * (C / 8);
 #pragma unroll
-        for (int k = 0; k < (kPrefetch ? C / 8 : 1); ++k) res[k] = op[k];
-      }
+      for (int k = 0; k < (kPrefetch ? C / 8 : 1); ++k) res[k] = tc::ld_v4_pred(op + k, st);
     }
     for (int t = tpar; t < K::NT2; t += 2) {
       const int r = t * 128 + q * 32 + lane;
@@ -657,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 
     if (inplace && resident) grid_wait(a.gbar, (unsigned)B);  // neighbours have read my rim
     if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
-      if (slot_before_store<C, BS>(a, tag, (int)gridDim.x, 1)) rimsrc = a.rim_buf;
+      if (slot_before_store<C, BS>(a, tag, (int)gridDim.x, 1, known_B)) rimsrc = a.rim_buf;
       first_store = false;
     }
     trace(a.trace, 10);
@@ -700,7 +706,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     trace(a.trace, 11);
     blk += gridDim.x;
     if (fused) {
-      if (!slot_entry(a, tag, blk, n0, by0, bx0)) break;
+      // the block count is known after the in-place wait: no poll when the list is done
+      if ((known_B >= 0 && blk >= known_B) || !slot_entry(a, tag, blk, n0, by0, bx0)) break;
     } else {
       if (blk >= B) break;
       n0 = __ldcg(idx + 3 * blk);
@@ -946,6 +953,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   const bool resident = !fused && B <= npairs;
   const __nv_bfloat16* rimsrc = nullptr;
   bool first_store = fused && inplace;  // slot_before_store still pending
+  int known_B = -1;                     // block count, once slot_before_store has read it
   if (!fused && inplace && !resident) {  // streamed in place: snapshot every block's rim first
     const Rim r{BS, BS, 1};
     const int Pr = r.pixels();
@@ -1108,10 +1116,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     uint4* op = reinterpret_cast<uint4*>(a.out) +
                 (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (C / 8) + hf * (C / 16);
     uint4 res[C / 16];
-    if (store) {
 #pragma unroll
-      for (int k = 0; k < C / 16; ++k) res[k] = op[k];
-    }
+    for (int k = 0; k < C / 16; ++k) res[k] = tc::ld_v4_pred(op + k, store);
 #pragma unroll
     for (int c0 = hf * (MC / 2); c0 < (hf + 1) * (MC / 2); c0 += 16) {
       float v[16];
@@ -1148,7 +1154,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     tc::fence_after();
     if (inplace && resident) grid_wait(a.gbar, 2u * (unsigned)B);
     if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
-      if (slot_before_store<C, BS>(a, tag, npairs, 2)) rimsrc = a.rim_buf;
+      if (slot_before_store<C, BS>(a, tag, npairs, 2, known_B)) rimsrc = a.rim_buf;
       first_store = false;
     }
     trace(a.trace, 10);
@@ -1178,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     blk += npairs;
     bool next;
     if (fused) {
-      next = slot_entry(a, tag, blk, n1, by1, bx1);
+      next = !(known_B >= 0 && blk >= known_B) && slot_entry(a, tag, blk, n1, by1, bx1);
     } else {
       next = blk < B;
       if (next) {

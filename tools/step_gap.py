@@ -61,3 +61,11 @@ if len(act):
     print(f"  pdl -> exit total {tot.min():6.2f} {np.median(tot):6.2f} {tot.max():6.2f}")
     slow = act[np.argmax(act[:, 17])]
     print("  slowest CTA:", " ".join(f"{nb}={(slow[b_] - slow[16]) / 1e3:.2f}" for b_, nb in chain[1:]))
+    t1 = ts[1]
+    prod = t1[t1[:, 19] > 0]
+    for nm, a_, b_ in (("flags -> slot atomic", 12, 19), ("slot atomic -> done", 19, 14), ("pdl -> flags", 16, 12)):
+        d = (prod[:, b_] - prod[:, a_]) / 1e3
+        print(f"  producers with active blocks ({len(prod)}): {nm:>22} {d.min():6.2f} {np.median(d):6.2f} {d.max():6.2f}")
+    # consumer wait vs the producer that published its entry is not traced; show entry poll by slot order
+    ent = (act[:, 2] - act[:, 16]) / 1e3
+    print(f"  pdl -> entry for active CTAs: {ent.min():.2f} {np.median(ent):.2f} {ent.max():.2f}")
