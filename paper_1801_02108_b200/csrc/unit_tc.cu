@@ -298,18 +298,19 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
     unsigned* ring = slot_ring(a, tag);
     int ok = 0;
     unsigned long long e = 0;
-    while (true) {
+    while (true) {  // both words in flight per iteration: one round trip per poll
       e = ld_relaxed_u64(&a.etag[blk]);
+      const unsigned d = ld_relaxed_u32(ring + 1);
       if ((unsigned)(e >> 32) == tag) {
         ok = 1;
         break;
       }
-      if (ld_acquire_u32(ring + 1) == gridDim.x) {  // all producers done
+      if (d == gridDim.x) {  // all producers done: re-read the entry after an acquire
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         e = ld_relaxed_u64(&a.etag[blk]);
         ok = (unsigned)(e >> 32) == tag ? 1 : 0;
         break;
       }
-      __nanosleep(20);
     }
     s_e[3] = ok;
     if (ok) {
@@ -995,19 +996,31 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     constexpr int TOT = 128 * (C / 8);
     constexpr int ITEMS = TOT / kThreads;
     uint4 raw[ITEMS];
+    if (rimsrc == nullptr) {  // every pixel from x (cheap addressing: frame base + y * w + x)
+      const uint4* xf = reinterpret_cast<const uint4*>(a.x) + (size_t)n * g.h * g.w * (C / 8);
 #pragma unroll
-    for (int it = 0; it < ITEMS; ++it) {
-      const int i = tid + it * kThreads;
-      const int pl = i / (C / 8), k = i % (C / 8);
-      const int p = rank * 128 + pl;
-      const int wy = p / BS, wx = p % BS;
-      const int y = ys + wy, xx = xs + wx;
-      const bool from_rim = rimsrc && !rim.interior(wy, wx);
-      const bool inb = y >= 0 && y < g.h && xx >= 0 && xx < g.w;
-      const uint4* src = from_rim
-          ? reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k
-          : reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + (inb ? y : 0)) * g.w + (inb ? xx : 0)) * (C / 8) + k;
-      raw[it] = tc::ld_v4_pred(src, (p < K::NPIX) && (from_rim || inb));
+      for (int it = 0; it < ITEMS; ++it) {
+        const int i = tid + it * kThreads;
+        const int p = rank * 128 + i / (C / 8), k = i % (C / 8);
+        const int y = ys + p / BS, xx = xs + p % BS;
+        const bool ok = p < K::NPIX && (unsigned)y < (unsigned)g.h && (unsigned)xx < (unsigned)g.w;
+        raw[it] = tc::ld_v4_pred(xf + (size_t)(ok ? y * g.w + xx : 0) * (C / 8) + k, ok);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < ITEMS; ++it) {
+        const int i = tid + it * kThreads;
+        const int pl = i / (C / 8), k = i % (C / 8);
+        const int p = rank * 128 + pl;
+        const int wy = p / BS, wx = p % BS;
+        const int y = ys + wy, xx = xs + wx;
+        const bool from_rim = !rim.interior(wy, wx);
+        const bool inb = y >= 0 && y < g.h && xx >= 0 && xx < g.w;
+        const uint4* src = from_rim
+            ? reinterpret_cast<const uint4*>(rimsrc) + ((size_t)blk * P + rim.index(wy, wx)) * (C / 8) + k
+            : reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + (inb ? y : 0)) * g.w + (inb ? xx : 0)) * (C / 8) + k;
+        raw[it] = tc::ld_v4_pred(src, (p < K::NPIX) && (from_rim || inb));
+      }
     }
     trace(a.trace, 3);
     if (rank == 0) prefetch_window<C, BS>(a, idx, tag, blk + npairs);
