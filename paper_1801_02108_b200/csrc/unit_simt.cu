@@ -255,13 +255,15 @@ size_t unit_workspace_wide(int c, int m, const Geo& g) {
 }
 
 // which tensor-core variant applies: 1 single-kernel unit, 2 wide (three launches), 0 none.
-// The single kernel walks one block's latency chain per CTA; past ~2K candidate blocks the
-// pipelined three-launch unit is faster even where the single kernel fits (measured:
-// tools/wide_vs_fused.py, config-2 shapes: 48 vs 44 us at 4 frames, 723 vs 609 us at 64).
-constexpr long kFusedMaxCandidates = 2048;
+// The single kernel walks one block's latency chain per CTA; past ~8K candidate blocks the
+// pipelined three-launch unit is faster even where the single kernel fits (measured with
+// the mask-fused path, tools/wide_vs_fused.py, config-2 shapes at 20% density: 91 vs 102 us
+// at 8 frames, 183 vs 182 us at 16, 724 vs 618 us at 64).
+constexpr long kFusedMaxCandidates = 8192;
 int unit_tc_kind(int dtype, int c, int m, const Geo& g, int halo, int pre_act) {
   const long cand = (long)g.n * g.gy * g.gx;
-  if (!(debug_flags() & kDebugForceWide) && cand <= kFusedMaxCandidates &&
+  if (!(debug_flags() & kDebugForceWide) &&
+      (cand <= kFusedMaxCandidates || (debug_flags() & kDebugForceFused)) &&
       unit_tc_supported(dtype, c, m, g, halo, pre_act))
     return 1;
   if (unit_tc_supported(dtype, c, m, g, halo, pre_act) && !unit_wide_supported(dtype, c, m, g, halo, pre_act))
