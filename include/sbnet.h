@@ -121,7 +121,9 @@ int sbn_gather_grad(const void* gblk, int dtype, int c, const sbn_geometry* g, c
 
 /* Copy each active block's region between two frames of identical shape at the same
  * coordinates: region 0 = the input window clipped to the image, region 1 = the clipped
- * output window.  Either pointer may be pinned host memory (UVA): this moves exactly the
+ * output window, region 2 = the union of the active input windows (every pixel once: the
+ * overlap rims an earlier active neighbour covers are skipped; falls back to 0 when the
+ * overlap exceeds half the block).  Either pointer may be pinned host memory (UVA): this moves exactly the
  * bytes a sparse layer reads / writes between a host-resident frame and its device
  * staging copy (the host-frame path of sparse_residual_unit).  No reference counterpart:
  * the reference operates on host arrays in place of this transfer. */

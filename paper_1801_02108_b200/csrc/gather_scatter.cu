@@ -70,13 +70,37 @@ copy_regions_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, 
   const long nwarps = (long)gridDim.x * (kThreads / 32);
   const int rh = region == 0 ? g.bh : g.obh;
   const int fh = region == 0 ? g.h : g.oh, fw = region == 0 ? g.w : g.ow;
-  for (long r = blockIdx.x * (long)(kThreads / 32) + (threadIdx.x >> 5); r < (long)B * rh; r += nwarps) {
-    const int b = (int)(r / rh), ry = (int)(r - (long)b * rh);
+  const int rh2 = region == 1 ? g.obh : g.bh;
+  for (long r = blockIdx.x * (long)(kThreads / 32) + (threadIdx.x >> 5); r < (long)B * rh2; r += nwarps) {
+    const int b = (int)(r / rh2), ry = (int)(r - (long)b * rh2);
     const int n = __ldg(idx + 3 * b), by = __ldg(idx + 3 * b + 1), bx = __ldg(idx + 3 * b + 2);
-    const int y = region == 0 ? g.oy + by * g.sy + ry : by * g.obh + ry;
+    const int y = region != 1 ? g.oy + by * g.sy + ry : by * g.obh + ry;
     if (y < 0 || y >= fh) continue;
-    int x0 = region == 0 ? g.ox + bx * g.sx : bx * g.obw;
-    int x1 = x0 + (region == 0 ? g.bw : g.obw);
+    int x0 = region != 1 ? g.ox + bx * g.sx : bx * g.obw;
+    int x1 = x0 + (region != 1 ? g.bw : g.obw);
+    if (region == 2) {
+      // union of windows: skip the parts of this window that an active block earlier in
+      // the (ascending) list also covers — its left neighbour (columns < overlap), the
+      // block above (rows < overlap), above-left / above-right (corner squares).  Those
+      // are the entries just before b: scan the last gx + 1 of them, one per lane.
+      const int ovy = g.bh - g.sy, ovx = g.bw - g.sx;
+      const long key = ((long)n * g.gy + by) * g.gx + bx;
+      bool L = false, T = false, TL = false, TR = false;
+      for (int k0 = 0; k0 <= g.gx; k0 += 32) {
+        const int k = k0 + lane, e = b - 1 - k;
+        long kk = -1;
+        if (k <= g.gx && e >= 0)
+          kk = ((long)__ldg(idx + 3 * e) * g.gy + __ldg(idx + 3 * e + 1)) * g.gx + __ldg(idx + 3 * e + 2);
+        L |= __any_sync(0xffffffffu, bx > 0 && kk == key - 1);
+        T |= __any_sync(0xffffffffu, by > 0 && kk == key - g.gx);
+        TL |= __any_sync(0xffffffffu, by > 0 && bx > 0 && kk == key - g.gx - 1);
+        TR |= __any_sync(0xffffffffu, by > 0 && bx < g.gx - 1 && kk == key - g.gx + 1);
+      }
+      if (ry < ovy && T) continue;
+      const int lo = (L || (ry < ovy && TL)) ? ovx : 0, hi = (ry < ovy && TR) ? g.sx : g.bw;
+      x1 = x0 + hi;
+      x0 += lo;
+    }
     x0 = max(x0, 0);
     x1 = min(x1, fw);
     if (x1 <= x0) continue;
@@ -370,13 +394,15 @@ extern "C" int sbn_copy_block_regions(const void* src, void* dst, int dtype, int
   const int es = dtype_size(dtype);
   SBN_CHECK_ARG(es > 0, SBN_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
   SBN_CHECK_ARG(c > 0, SBN_ERR_SHAPE, "channels must be > 0");
-  SBN_CHECK_ARG(region == 0 || region == 1, SBN_ERR_INVALID, "region must be 0 (window) or 1 (output)");
+  SBN_CHECK_ARG(region >= 0 && region <= 2, SBN_ERR_INVALID,
+                "region must be 0 (window), 1 (output) or 2 (union of windows)");
+  if (region == 2 && (2 * (gp->bh - gp->sy) > gp->bh || 2 * (gp->bw - gp->sx) > gp->bw)) region = 0;
   if (cap <= 0) return SBN_OK;
   SBN_CHECK_ARG(src && dst && idx && count, SBN_ERR_INVALID, "null pointer argument");
   Geo g = to_geo(gp);
   cudaStream_t s = (cudaStream_t)stream;
   const int pix = c * es;
-  const long rows = (long)cap * (region == 0 ? g.bh : g.obh);
+  const long rows = (long)cap * (region != 1 ? g.bh : g.obh);
   const unsigned grid = (unsigned)grid_for(rows * 32, kThreads);
   switch (pick_vec(pix, src, dst)) {
     case 16: copy_regions_kernel<16><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;

@@ -488,7 +488,7 @@ class _HostFramePlan:
                                        self.count.data_ptr(), self.rmws.data_ptr(), self.rmws.numel(), sh),
                    "reduce_mask")
         _lib.check(lib.sbn_copy_block_regions(xh.data_ptr(), self.stage.data_ptr(), self.dt, self.c, gb,
-                                              self.rows.data_ptr(), self.count.data_ptr(), self.cap, 0, sh),
+                                              self.rows.data_ptr(), self.count.data_ptr(), self.cap, 2, sh),
                    "copy_block_regions")
         _lib.check(lib.sbn_residual_unit(self.stage.data_ptr(), self.dt, self.c, self.m, gb, self.halo, self.pre,
                                          C.byref(self.up), self.rows.data_ptr(), self.count.data_ptr(), self.cap,
@@ -502,9 +502,10 @@ class _HostFramePlan:
 def _host_frame_unit(xh: torch.Tensor, mask: BinaryMask, u: ResidualUnitParams, block_size,
                      halo: int, algo, blocking: bool) -> None:
     """In-place unit on a pinned host frame (UVA): mask -> device, ordered reduce_mask,
-    the active blocks' input windows host -> device staging frame (sbn_copy_block_regions
-    reads host memory over PCIe), the fused unit in place on the staging frame, and the
-    active output windows device -> host frame.  PCIe carries the mask plus exactly the
+    the union of the active blocks' input windows host -> device staging frame
+    (sbn_copy_block_regions region 2 reads each needed host pixel once over PCIe), the
+    fused unit in place on the staging frame, and the active output windows device -> host
+    frame.  PCIe carries the mask plus exactly the
     bytes the sparse layer reads and writes, instead of two full frames."""
     if not xh.is_contiguous():
         raise ShapeMismatchError("host-frame unit needs a contiguous pinned NHWC frame")

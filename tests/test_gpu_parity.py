@@ -503,3 +503,35 @@ def test_residual_unit_host_frame_inplace_bit_identical(cuda_device, c, m, block
     P.sparse_residual_unit(P.Tensor4D(hx2), hm, u, (block, block), inplace=True, blocking=False)
     torch.cuda.synchronize()
     assert torch.equal(hx2, dev_out)
+
+
+@pytest.mark.parametrize("block,density,n", [(16, 0.1, 1), (16, 0.4, 2), (8, 0.2, 1), (5, 0.3, 1)])
+def test_copy_block_regions_union_equals_windows(cuda_device, block, density, n):
+    """Region 2 (union of active windows, each pixel copied once) lands exactly the pixels
+    region 0 (every window, overlaps copied twice) lands; region 1 the output windows."""
+    import ctypes as C
+    lib = _lib.load()
+    H, W, c = 61, 47, 16
+    x = torch.randn(n, H, W, c, device=cuda_device).bfloat16()
+    mk = P.synth_mask_blobs((n, H, W), 1 - density, block).cuda()
+    spec = P.unit_spec((n, H, W, c), (block, block))
+    idx = P.reduce_mask(mk, spec)
+    idx.to_device(cuda_device)
+    g = spec.c_geometry(n)
+    outs = []
+    for region in (0, 2, 1):
+        d = torch.zeros_like(x)
+        _lib.check(lib.sbn_copy_block_regions(x.data_ptr(), d.data_ptr(), 2, c, C.byref(g), idx.rows.data_ptr(),
+                                              idx.count_dev.data_ptr(), idx.capacity, region,
+                                              _lib.stream_handle(cuda_device)), "copy")
+        outs.append(d)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    # region 1 writes exactly the clipped output windows
+    sel = torch.zeros(n, H, W, dtype=torch.bool)
+    for (fr, by, bx) in idx.rows[:idx.count].cpu().tolist():
+        oy, ox = by * spec.out_block_size[0], bx * spec.out_block_size[1]
+        sel[fr, oy:oy + spec.out_block_size[0], ox:ox + spec.out_block_size[1]] = True
+    o1 = outs[2].cpu()
+    assert torch.equal(o1[sel].view(torch.int16), x.cpu()[sel].view(torch.int16))
+    assert not o1[~sel].view(torch.int16).any()
