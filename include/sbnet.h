@@ -182,7 +182,9 @@ int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
  * produces an unordered active list (blocks write disjoint windows, so the result does
  * not depend on the order).  sync_ws: sbn_sparse_residual_unit_sync_bytes, zeroed ONCE by
  * the caller and left zeroed by every call (barrier / look-back words at fixed offsets);
- * ws: sbn_sparse_residual_unit_workspace bytes of scratch. */
+ * ws: sbn_sparse_residual_unit_workspace bytes, zeroed ONCE by the caller and kept between
+ * calls (it carries the launch epoch and the tagged block-list entries; a new zeroed ws
+ * simply restarts the epoch). */
 size_t sbn_sparse_residual_unit_sync_bytes(const sbn_geometry* g);
 size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* g, int halo,
                                           int algo);

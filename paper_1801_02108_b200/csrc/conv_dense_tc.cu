@@ -83,23 +83,34 @@ struct __align__(64) CArgs {
   const __nv_bfloat16* bias_bf16;  // ... or bf16 / null (sparse mode, sparse_conv2d's FilterBank)
   int n, oh, ow, sy, sx, py, px;
   int tiles_y, tiles_x;   // dense mode: 8 x 16 output tiles
-  int th, tw;             // output rows / cols per tile (dense 8 x 16; sparse: the out block)
-  // sparse mode (idx != null): tile j = active block j of the list; its window starts at
-  // (goy + by*gsy, gox + bx*gsx) and its output block at (by*th, bx*tw)
+  int th, tw;             // output rows / cols per tile (dense 8 x 16; sparse: <= the out block)
+  // sparse mode (idx != null): active block j of the list is covered by subs_y x subs_x
+  // tiles of th x tw outputs (one tile when obh*obw <= 128); its window starts at
+  // (goy + by*gsy, gox + bx*gsx) and its output block (obh x obw) at (by*obh, bx*obw)
   const int32_t* idx;
   const int32_t* count;
   int cap, gsy, gsx, goy, gox;
+  int obh, obw, subs_y, subs_x;
 };
 
-// tile -> (frame, first output row / col, first input row / col of tap (0, 0))
-__device__ __forceinline__ void conv_tile(const CArgs& a, int tile, int& n, int& oy0, int& ox0, int& iy0, int& ix0) {
+// tile -> (frame, first output row / col, first input row / col of tap (0, 0)); ly / lx:
+// rows / cols of the tile inside its block's output window (sparse) or th / tw (dense)
+__device__ __forceinline__ void conv_tile(const CArgs& a, int tile, int& n, int& oy0, int& ox0, int& iy0, int& ix0,
+                                          int& ly, int& lx) {
+  ly = a.th;
+  lx = a.tw;
   if (a.idx) {
-    n = __ldg(a.idx + 3 * tile);
-    const int by = __ldg(a.idx + 3 * tile + 1), bx = __ldg(a.idx + 3 * tile + 2);
-    oy0 = by * a.th;
-    ox0 = bx * a.tw;
-    iy0 = a.goy + by * a.gsy;
-    ix0 = a.gox + bx * a.gsx;
+    const int subs = a.subs_y * a.subs_x;
+    const int j = tile / subs, sub = tile - j * subs;
+    const int ty = sub / a.subs_x, tx = sub - ty * a.subs_x;
+    n = __ldg(a.idx + 3 * j);
+    const int by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
+    oy0 = by * a.obh + ty * a.th;
+    ox0 = bx * a.obw + tx * a.tw;
+    iy0 = a.goy + by * a.gsy + ty * a.th * a.sy;
+    ix0 = a.gox + bx * a.gsx + tx * a.tw * a.sx;
+    ly = min(a.th, a.obh - ty * a.th);
+    lx = min(a.tw, a.obw - tx * a.tw);
   } else {
     const int tx = tile % a.tiles_x, ty = (tile / a.tiles_x) % a.tiles_y;
     n = tile / (a.tiles_x * a.tiles_y);
@@ -156,7 +167,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       tc::bulk_g2s(Wring + (size_t)c * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[0]);
   }
   tc::pdl_wait();
-  const int ntiles = a.idx ? ld_count(a.count, a.cap) : a.n * a.tiles_y * a.tiles_x;
+  const int ntiles = a.idx ? ld_count(a.count, a.cap) * a.subs_y * a.subs_x : a.n * a.tiles_y * a.tiles_x;
 
   if (warp < kLWarp) {
     // ------------------------------------------------ epilogue
@@ -169,11 +180,12 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
       const int buf = Q::NACC == 2 ? (k & 1) : 0;
       const int use = Q::NACC == 2 ? (k >> 1) : k;
-      int n, oy0, ox0, iy0, ix0;
-      conv_tile(a, tile, n, oy0, ox0, iy0, ix0);
+      int n, oy0, ox0, iy0, ix0, ly, lx;
+      conv_tile(a, tile, n, oy0, ox0, iy0, ix0, ly, lx);
       const int Y = oy0 + r / a.tw, X = ox0 + r % a.tw;
       if (half == 0)
-        rowdst[r] = (r < a.th * a.tw && Y < a.oh && X < a.ow) ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
+        rowdst[r] = (r < a.th * a.tw && r / a.tw < ly && r % a.tw < lx && Y < a.oh && X < a.ow)
+                        ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
       const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * COUT;
       tc::mbar_wait(&acc_full[buf], use & 1);
       tc::fence_after();
@@ -222,8 +234,8 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     if (lane == 0) {
       int c = 0, wit = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int n, oy0, ox0, y0, x0;
-        conv_tile(a, tile, n, oy0, ox0, y0, x0);
+        int n, oy0, ox0, y0, x0, ly, lx;
+        conv_tile(a, tile, n, oy0, ox0, y0, x0, ly, lx);
         const uint32_t bytes = (uint32_t)(a.th * a.tw * Q::ROWB);
         for (int kc = 0; kc < Q::NKC; ++kc)
           for (int tap = 0; tap < Q::TAPS; ++tap, ++c) {
@@ -300,6 +312,26 @@ __global__ void conv_dense_pack_kernel(const __nv_bfloat16* __restrict__ w, uint
   }
 }
 
+// Sparse mode: tile an obh x obw output block with the fewest th x tw tiles (th*tw <= 128
+// GEMM rows, TMA box extents tw*sx, th*sy <= 256); one tile when the block fits.
+static bool sparse_tile_shape(int obh, int obw, int sy, int sx, int& th, int& tw, int& subs_y, int& subs_x) {
+  int best = 1 << 30;
+  for (int h = 1; h <= obh && h <= 128 && h * sy <= 256; ++h) {
+    const int w = min(min(obw, 128 / h), 256 / sx);
+    if (w < 1) continue;
+    const int t = ((obh + h - 1) / h) * ((obw + w - 1) / w);
+    if (t < best || (t == best && h * w > th * tw)) {
+      best = t;
+      th = h;
+      tw = w;
+    }
+  }
+  if (best == (1 << 30)) return false;
+  subs_y = (obh + th - 1) / th;
+  subs_x = (obw + tw - 1) / tw;
+  return true;
+}
+
 template <int CIN, int COUT, int KS>
 int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int px, int oh, int ow,
                  const void* wpk, const float* bias, void* out, cudaStream_t s,
@@ -308,7 +340,8 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   using Q = CCfg<CIN, COUT, KS>;
   CArgs a;
   memset(&a, 0, sizeof(a));
-  const int th = sparse ? sparse->obh : 8, tw = sparse ? sparse->obw : 16;
+  int th = 8, tw = 16, subs_y = 1, subs_x = 1;
+  if (sparse) sparse_tile_shape(sparse->obh, sparse->obw, sy, sx, th, tw, subs_y, subs_x);
   const uint64_t dims[4] = {(uint64_t)CIN, (uint64_t)w, (uint64_t)h, (uint64_t)n};
   const uint64_t str[3] = {(uint64_t)CIN * 2, (uint64_t)w * CIN * 2, (uint64_t)h * w * CIN * 2};
   const uint32_t box[4] = {(uint32_t)Q::KC, (uint32_t)(tw * sx), (uint32_t)(th * sy), 1};
@@ -339,7 +372,11 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
     a.gsx = sparse->sx;
     a.goy = sparse->oy;
     a.gox = sparse->ox;
-    tiles = cap;
+    a.obh = sparse->obh;
+    a.obw = sparse->obw;
+    a.subs_y = subs_y;
+    a.subs_x = subs_x;
+    tiles = (long)cap * subs_y * subs_x;
   }
   auto kern = conv_dense_kernel<CIN, COUT, KS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
@@ -377,7 +414,8 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
 // block, the out block (obh x obw <= 128 pixels) = one strided TMA box per (K-chunk, tap).
 bool sparse_conv_tma_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g) {
   if (dtype != SBN_BF16 || kh != kw || sh != sw || sh < 1 || sh > kh || sh > 3) return false;
-  if (g.obh * g.obw > 128 || g.obw * sw > 256 || g.obh * sh > 256) return false;
+  int th = 0, tw = 0, subs_y = 0, subs_x = 0;
+  if (!sparse_tile_shape(g.obh, g.obw, sh, sw, th, tw, subs_y, subs_x)) return false;
 #define X(CI, CO, KS) if (cin == CI && cout == CO && kh == KS) return CCfg<CI, CO, KS>::SMEM <= max_smem_optin();
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X

@@ -53,7 +53,7 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
                    const int32_t* count, int cap, cudaStream_t s,
                    const uint8_t* mask = nullptr, int32_t* idx_out = nullptr,
                    int32_t* count_out = nullptr, unsigned long long* cst = nullptr,
-                   unsigned long long* etag = nullptr);
+                   unsigned long long* etag = nullptr, unsigned int* slotw = nullptr);
 // wide tcgen05 path (unit_wide.cu): three chained implicit-GEMM launches over the stacked
 // active windows, for channel counts whose weights do not fit one CTA's shared memory
 bool unit_wide_supported(int dtype, int c, int m, const Geo& g, int halo, int pre_act);

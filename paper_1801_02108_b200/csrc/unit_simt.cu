@@ -428,7 +428,7 @@ extern "C" size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, co
                                                      int halo, int algo) {
   if (!gp || dtype_size(dtype) == 0) return 0;
   const size_t cap = (size_t)gp->n * gp->gy * gp->gx;
-  return al256(cap * 12) + 256 + al256(cap * 8) + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
+  return 256 + al256(cap * 8) + 256 + al256(cap * 12) + sbn_residual_unit_workspace(dtype, c, m, gp, halo, algo);
 }
 
 extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int dtype, int c, int m,
@@ -447,11 +447,16 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
                 "sparse_residual_unit needs a %zu-byte workspace", need);
   const int cap = gp->n * gp->gy * gp->gx;
   if (cap <= 0) return SBN_OK;
+  // [slot words 256 B | tagged entries cap*8 | count 256 B | index list cap*12 | unit ws]: the
+  // slot words (launch epoch) and the tagged entries sit at fixed offsets from the start, so
+  // calls with different geometries sharing one workspace never see each other's index
+  // data where they look for tags (a smaller cap's entry range is a prefix of a larger one's)
   uint8_t* w8 = (uint8_t*)ws;
-  int32_t* idx = (int32_t*)w8;
-  int32_t* count = (int32_t*)(w8 + al256((size_t)cap * 12));
-  unsigned long long* etag = (unsigned long long*)(w8 + al256((size_t)cap * 12) + 256);
-  uint8_t* uws = w8 + al256((size_t)cap * 12) + 256 + al256((size_t)cap * 8);  // [bar | rim | pack]
+  unsigned int* slotw = (unsigned int*)w8;
+  unsigned long long* etag = (unsigned long long*)(w8 + 256);
+  int32_t* count = (int32_t*)(w8 + 256 + al256((size_t)cap * 8));
+  int32_t* idx = (int32_t*)(w8 + 256 + al256((size_t)cap * 8) + 256);
+  uint8_t* uws = w8 + 256 + al256((size_t)cap * 8) + 256 + al256((size_t)cap * 12);  // [bar | rim | pack]
   uint8_t* sync8 = (uint8_t*)sync_ws;
   unsigned int* gbar = reinterpret_cast<unsigned int*>(sync8);
   unsigned long long* cst = reinterpret_cast<unsigned long long*>(sync8 + kBarBytes);
@@ -475,7 +480,7 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
     }
     const bool inplace = x == out;
     return unit_tc_launch(x, out, inplace ? uws + kBarBytes : nullptr, gbar, c, m, g, p, packed,
-                          idx, count, cap, s, mask, idx, count, cst, etag);
+                          idx, count, cap, s, mask, idx, count, cst, etag, slotw);
   }
   st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws,
                        sync_bytes - kBarBytes - kCstBytes, stream);

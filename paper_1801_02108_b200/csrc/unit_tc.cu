@@ -90,6 +90,8 @@ struct TcArgs {
   const uint8_t* mask;     // non-null: fused reduce_mask (MAX) + compaction into idx/count
   unsigned long long* cst; // (unused; reserved)
   unsigned long long* etag;  // slot compaction: per-entry (launch tag << 32 | candidate) word
+  unsigned int* sw;          // slot words: [0] epoch, [4 + 4 * (tag & 1) + {0 slot, 1 done, 2 staged}]
+                             // (same workspace as etag, fixed offsets: reset together)
   int32_t* idx_out;
   int32_t* count_out;
   const int32_t* idx;
@@ -113,8 +115,8 @@ __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162
 // returns G-1, so every CTA has read the epoch) publishes the block count, bumps the epoch
 // and zeroes the other slot (its launch completed before this one passed
 // griddepcontrol.wait; the next launch will use it).  Tags make stale entries invisible.
-//   words (sync ws, u32): [8] epoch, [13..14] grid barrier (streamed in-place only),
-//                         [16 + 4 * (tag & 1) + {0 slot counter, 1 done, 2 staged}]
+//   words: sw[0] epoch, sw[4 + 4 * (tag & 1) + {0 slot counter, 1 done, 2 staged}] (at the
+//   start of the unit workspace, before the tagged entries); sync ws [13..14] grid barrier
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -145,9 +147,15 @@ __device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
 __device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
   asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned* slot_ring(const TcArgs& a, unsigned tag) { return a.gbar + 16 + 4 * (tag & 1u); }
+__device__ __forceinline__ unsigned* slot_ring(const TcArgs& a, unsigned tag) { return a.sw + 4 + 4 * (tag & 1u); }
+// Entry word: hashed launch tag (odd multiplier: a bijection, and far from the small
+// integers / activation bits other users of a shared workspace leave behind) << 32 | candidate.
+__device__ __forceinline__ unsigned tag_hash(unsigned tag) { return tag * 0x9E3779B1u; }
 __device__ __forceinline__ unsigned long long slot_word(unsigned tag, int cand) {
-  return ((unsigned long long)tag << 32) | (unsigned)cand;
+  return ((unsigned long long)tag_hash(tag) << 32) | (unsigned)cand;
+}
+__device__ __forceinline__ bool slot_match(unsigned long long e, unsigned tag) {
+  return (unsigned)(e >> 32) == tag_hash(tag);
 }
 
 // Returns this launch's tag (epoch + 1); the epoch load overlaps the mask loads.  Thread 32
@@ -161,7 +169,7 @@ __device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done
   __shared__ int s_base;
   __shared__ unsigned s_tag;
   unsigned ep = 0;
-  if (tid == 0) ep = ld_relaxed_u32(a.gbar + 8);
+  if (tid == 0) ep = ld_relaxed_u32(a.sw);
   const int T = g.n * g.gy * g.gx;
   constexpr int area = BS * BS;  // the unit's window (bh == bw == BS)
   const int G = gridDim.x;
@@ -235,7 +243,7 @@ __device__ __forceinline__ void slot_last_producer(const TcArgs& a, unsigned tag
     other[0] = 0u;
     other[1] = 0u;
     other[2] = 0u;
-    a.gbar[8] = tag;
+    a.sw[0] = tag;
   }
 }
 
@@ -301,14 +309,14 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
     while (true) {  // both words in flight per iteration: one round trip per poll
       e = ld_relaxed_u64(&a.etag[blk]);
       const unsigned d = ld_relaxed_u32(ring + 1);
-      if ((unsigned)(e >> 32) == tag) {
+      if (slot_match(e, tag)) {
         ok = 1;
         break;
       }
       if (d == gridDim.x) {  // all producers done: re-read the entry after an acquire
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         e = ld_relaxed_u64(&a.etag[blk]);
-        ok = (unsigned)(e >> 32) == tag ? 1 : 0;
+        ok = slot_match(e, tag) ? 1 : 0;
         break;
       }
     }
@@ -339,7 +347,7 @@ __device__ __forceinline__ void prefetch_window(const TcArgs& a, const int32_t* 
   int n, by, bx;
   if (tag) {
     const unsigned long long e = ld_relaxed_u64(&a.etag[blk]);
-    if ((unsigned)(e >> 32) != tag) return;
+    if (!slot_match(e, tag)) return;
     const int cand = (int)(unsigned)e;
     n = cand / (g.gy * g.gx);
     const int rr = cand - n * (g.gy * g.gx);
@@ -1290,6 +1298,7 @@ static TcArgs make_args(const void* x, void* out, const void* rim, const Geo& g,
   a.count_out = nullptr;
   a.cst = nullptr;
   a.etag = nullptr;
+  a.sw = nullptr;
   a.idx = idx; a.count = count; a.cap = cap;
   return a;
 }
@@ -1307,13 +1316,16 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
                    const Geo& g, const sbn_unit_params* p, const void* packed, const int32_t* idx,
                    const int32_t* count, int cap, cudaStream_t s, const uint8_t* mask,
                    int32_t* idx_out, int32_t* count_out, unsigned long long* cst,
-                   unsigned long long* etag) {
+                   unsigned long long* etag, unsigned int* slotw) {
   TcArgs a = make_args(x, out, nullptr, g, p, idx, count, cap);
   a.mask = mask;
   a.idx_out = idx_out;
   a.count_out = count_out;
   a.cst = cst;
   a.etag = etag;
+  // the slot words live in the same caller workspace as the tagged entries: if that
+  // workspace is (re)allocated, epoch and entries restart together
+  a.sw = slotw;
   a.packed = (const uint8_t*)packed;
   a.rim_buf = (__nv_bfloat16*)rim_buf;
   a.gbar = gbar;

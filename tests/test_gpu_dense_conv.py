@@ -38,7 +38,9 @@ def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, sa
 @pytest.mark.parametrize("cin,cout,stride,block,same,k", [
     (64, 64, 2, 17, True, 3), (128, 128, 2, 13, True, 3), (32, 96, 1, 10, True, 3), (64, 64, 3, 24, False, 3),
     (96, 192, 2, 9, True, 3), (64, 64, 1, 10, True, 1), (128, 128, 1, 11, False, 1), (32, 32, 1, 14, True, 5),
-    (64, 64, 1, 15, False, 5), (64, 64, 2, 17, True, 5)])
+    (64, 64, 1, 15, False, 5), (64, 64, 2, 17, True, 5),
+    # blocks whose output window exceeds 128 px: several TMA tiles per block
+    (128, 128, 1, 32, True, 3), (64, 64, 2, 33, True, 3), (32, 32, 1, 24, False, 5), (64, 64, 1, 19, True, 1)])
 def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, block, same, k):
     """Strided / other-shape sparse 1x1 / 3x3 / 5x5 convs on the TMA tap-GEMM path (kernel
     variant 2) against the fp32 oracle on bf16-rounded inputs."""

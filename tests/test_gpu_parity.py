@@ -413,7 +413,7 @@ def test_sparse_conv_tc_bf16_vs_fp32_oracle(cuda_device, cin, block):
     assert O.rel_err(y, y2) <= 1e-2
 
 
-@pytest.mark.parametrize("density,nframes", [(0.1, 1), (0.3, 3), (0.9, 2)])
+@pytest.mark.parametrize("density,nframes", [(0.1, 1), (0.3, 3), (0.9, 2), (0.2, 36)])
 def test_fused_mask_unit_bit_identical_to_two_launch_path(cuda_device, density, nframes):
     """The single-kernel sparse_residual_unit (mask reduction fused, unordered block list)
     must equal the ordered reduce_mask + unit path bit for bit (blocks write disjoint
@@ -535,3 +535,27 @@ def test_copy_block_regions_union_equals_windows(cuda_device, block, density, n)
     o1 = outs[2].cpu()
     assert torch.equal(o1[sel].view(torch.int16), x.cpu()[sel].view(torch.int16))
     assert not o1[~sel].view(torch.int16).any()
+
+
+def test_fused_unit_alternating_geometries_share_workspace(cuda_device):
+    """The mask-fused unit's workspace (launch epoch + tagged block entries) is shared by
+    calls with different geometries; whatever one geometry leaves in it (index lists,
+    barrier words, rims) must never be taken for another's block entries."""
+    from paper_1801_02108_b200.layers import residual_unit_into
+    rng = np.random.default_rng(21)
+    u = P.random_unit_params(rng, 64, 32)
+    shapes = [(1, 96, 112), (4, 208, 176), (2, 150, 90), (6, 208, 176)]
+    data = []
+    for (n, h, w) in shapes:
+        x = torch.from_numpy(rng.standard_normal((n, h, w, 64)).astype(np.float32)).bfloat16().cuda()
+        mk = P.synth_mask_blobs((n, h, w), 0.7, n + h).cuda()
+        spec = P.unit_spec(tuple(x.shape), (16, 16))
+        ref = x.clone()
+        residual_unit_into(ref, x, u, spec, P.reduce_mask(mk, spec))
+        data.append((x, mk, ref))
+    for _ in range(3):
+        for x, mk, ref in data + data[::-1]:
+            assert torch.equal(P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16)).data, ref)
+            xi = x.clone()
+            P.sparse_residual_unit(P.Tensor4D(xi), mk, u, (16, 16), inplace=True)
+            assert torch.equal(xi, ref)
