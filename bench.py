@@ -682,7 +682,7 @@ def run_conv_sweep(P, torch, dev, time_graph):
            "flops_dense": 2 * Hc * Wc * 9 * Cc * Cc, "rows": []}
     for d in (0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 0.9, 1.0):
         mk = P.synth_mask_topleft((1, Hc, Wc), 1.0 - d).cuda()
-        for blk in (8, 16):
+        for blk in (8, 16, 32):
             spec = P.compute_block_spec((1, Hc, Wc, Cc), p, (blk, blk))
             algo = sparse_conv_algo(torch.bfloat16, fb, p, spec)
 

@@ -214,8 +214,11 @@ int sbn_debug_set_trace(unsigned long long* buf);
  * SBN_DEBUG_FORCE_WIDE: run the three-launch wide tcgen05 unit even where the single-kernel
  * unit applies.
  * SBN_DEBUG_FORCE_FUSED: run the single-kernel unit wherever it is supported (ignores the
- * candidate-count switch-over to the wide unit). */
-enum { SBN_DEBUG_NO_PAIR = 1, SBN_DEBUG_CONV_SINGLE_BUFFER = 2, SBN_DEBUG_FORCE_WIDE = 4, SBN_DEBUG_FORCE_FUSED = 8 };
+ * candidate-count switch-over to the wide unit).
+ * SBN_DEBUG_CONV_TMA: run sparse convs on the strided-TMA tap-GEMM kernel even where the
+ * single-window kernel applies. */
+enum { SBN_DEBUG_NO_PAIR = 1, SBN_DEBUG_CONV_SINGLE_BUFFER = 2, SBN_DEBUG_FORCE_WIDE = 4, SBN_DEBUG_FORCE_FUSED = 8,
+       SBN_DEBUG_CONV_TMA = 16 };
 int sbn_debug_set_flags(int flags);
 /* Diagnostics: occupancy the last tcgen05 unit launch computed (0: CTAs/SM of the
  * single-CTA kernel, 1: co-resident clusters of the CTA-pair kernel). */

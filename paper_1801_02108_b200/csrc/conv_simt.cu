@@ -118,10 +118,10 @@ bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int 
 using namespace sbn;
 
 // tensor-core variant for a sparse conv: 1 = single-window row-shift kernel (conv_tc.cu,
-// 3x3 stride 1), 2 = strided-TMA tap GEMM (conv_dense_tc.cu, 3x3 stride <= 3, out block
-// <= 128 pixels), 0 = none (SIMT)
+// 3x3 stride 1, blocks 8 / 16), 2 = strided-TMA tap GEMM (conv_dense_tc.cu, 1x1 / 3x3 / 5x5,
+// stride <= 3, any out block: several tiles per block above 128 pixels), 0 = none (SIMT)
 static int conv_tc_kind(int dtype, int cin, int cout, int kh, int kw, int sh, int sw, const Geo& g) {
-  if (sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, g)) return 1;
+  if (!(debug_flags() & kDebugConvTma) && sparse_conv_tc_supported(dtype, cin, cout, kh, kw, sh, sw, g)) return 1;
   if (sparse_conv_tma_supported(dtype, cin, cout, kh, kw, sh, sw, g)) return 2;
   return 0;
 }
