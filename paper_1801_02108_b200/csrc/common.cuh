@@ -103,7 +103,8 @@ __device__ __forceinline__ int ld_count(const int32_t* count, int cap) {
 constexpr int kTraceSlots = 32;
 unsigned long long* trace_buffer();  // host side: current buffer or nullptr
 int debug_flags();                   // host side: sbn_debug_set_flags()
-enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4, kDebugForceFused = 8, kDebugConvTma = 16 };
+enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4, kDebugForceFused = 8, kDebugConvTma = 16,
+       kDebugConvPair = 32 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

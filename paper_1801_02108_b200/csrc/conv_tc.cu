@@ -19,6 +19,9 @@
 //                    (+bias, bf16, clipped store).
 #include "common.cuh"
 #include "tc_util.cuh"
+#include "tma_util.cuh"
+
+#include <cstring>
 
 namespace sbn {
 namespace {
@@ -193,14 +196,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs a) {
   if (warp == 0) tc::tmem_free<K::TALLOC>(tmem);
 }
 
-// HWIO (3, 3, CIN, COUT) -> 9 tap images, each CIN/8 planes x COUT rows x 16 B.
+// HWIO (3, 3, CIN, COUT) -> 9 tap images, each CIN/8 planes x COUT rows x 16 B (single-CTA
+// kernels), followed by the CTA-pair copy: per tap two halves (output channels
+// [0, COUT/2) and [COUT/2, COUT)), each CIN/8 planes x COUT/2 rows x 16 B, so each CTA of a
+// pair fetches its half with one contiguous bulk copy.
 template <int CIN, int COUT>
 __global__ void conv_tc_pack_kernel(const __nv_bfloat16* __restrict__ w, uint8_t* __restrict__ img) {
   const int total = 9 * CIN * COUT;
+  constexpr size_t TAP = (size_t)(CIN / 8) * COUT * 16;
+  constexpr int NH = COUT / 2;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int tap = i / (CIN * COUT), r = i % (CIN * COUT), ci = r / COUT, co = r % COUT;
-    *reinterpret_cast<__nv_bfloat16*>(img + (size_t)tap * (CIN / 8) * COUT * 16 + (ci / 8) * COUT * 16 +
-                                      co * 16 + (ci % 8) * 2) = w[i];
+    *reinterpret_cast<__nv_bfloat16*>(img + (size_t)tap * TAP + (ci / 8) * COUT * 16 + co * 16 + (ci % 8) * 2) = w[i];
+    *reinterpret_cast<__nv_bfloat16*>(img + 9 * TAP + (size_t)tap * TAP + (size_t)(co / NH) * (TAP / 2) +
+                                      (ci / 8) * NH * 16 + (co % NH) * 16 + (ci % 8) * 2) = w[i];
   }
 }
 
@@ -428,6 +437,262 @@ int launch_conv_db(const ConvArgs& a, int cap, cudaStream_t s) {
   return launch_status("sparse_conv_tcgen05_db");
 }
 
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for 16x16 blocks.  The single-CTA kernels issue
+// 128 x COUT x 16 UMMAs whose A tile (4 KB) and B tile (COUT*32 B) both stream from shared
+// memory (~120 B/clk at COUT = 128 against ~128 B/clk of bandwidth), and their 8 worker warps
+// both stage windows and drain accumulators.  Here the block's two M-tiles (output rows
+// q in [0, 128) and [128, 224)) are ONE M = 256 UMMA issued by rank 0 of a 2-CTA cluster:
+//   * rank r holds window rows [8 r, 8 r + 11) — one 5-D TMA box (8 ch, 16 x, 11 y, C/8
+//     planes, 1 frame) that lands directly in the K-major plane layout (plane stride
+//     11*16*16 B), zero-filled outside the image (the gather's halo semantics);
+//   * rank r holds output channels [r COUT/2, (r+1) COUT/2) of every tap (B is split along
+//     N in cta_group::2), one contiguous bulk copy per tap from the pair copy of the packed
+//     weights; per SM an MMA reads the A tile plus half of B;
+//   * the worker warps only drain TMEM (+bias -> bf16 -> clipped store).
+// Handshakes (rank 0 owns what its MMA issuer waits on):
+//   full[s]      both weight halves of stage s landed (rank 1's TMA completes on it)  rank 0
+//   empty[s]     MMAs reading stage s done (multicast commit)               both
+//   win_full[b]  both window boxes landed (rank 1's TMA completes on it)    rank 0
+//   win_empty[b] MMAs reading window b done (multicast commit)              both
+//   acc_full[b]  accumulator b complete (multicast commit)                  both
+//   acc_empty[b] 2 x 256 worker arrivals (rank 1's arrive remotely)          rank 0
+constexpr int kPairThreads = kWorkers + 96;  // + weight loader, MMA / forwarder, window loader
+
+template <int CIN, int COUT, int BS>
+struct PairConvCfg {
+  static_assert(BS == 16 && COUT % 32 == 0, "pair conv: two M-tiles per block, N/2 a multiple of 16");
+  static constexpr int WROWS = 11;               // window rows per rank (128 + 2*BS + 2 pixels)
+  static constexpr int RA = WROWS * BS;           // local A rows
+  static constexpr int PA = RA * 16;              // plane stride = TMA box plane
+  static constexpr int ABOX = (CIN / 8) * PA;     // bytes of one window box
+  static constexpr int SZ_A = (ABOX + 1023) / 1024 * 1024;
+  static constexpr int NH = COUT / 2;            // output channels (B rows) per CTA
+  static constexpr int PWH = NH * 16;            // half-plane stride
+  static constexpr int TAPH = (CIN / 8) * PWH;   // bytes of one tap's half
+  static constexpr int TAP = (CIN / 8) * COUT * 16;  // one tap of the packed image
+  static constexpr int STAGES = (2 * SZ_A + 8 * TAPH + COUT * 4 <= 222 * 1024) ? 8
+                                : (2 * SZ_A + 6 * TAPH + COUT * 4 <= 222 * 1024) ? 6
+                                : (2 * SZ_A + 3 * TAPH + COUT * 4 <= 222 * 1024) ? 3 : 2;
+  static constexpr int WBOXR = TAPH / 128;  // weight half as a TMA box of 128-byte rows
+  static constexpr int OFF_W = 2 * SZ_A;
+  static constexpr int OFF_BIAS = OFF_W + STAGES * TAPH;
+  static constexpr int SMEM = OFF_BIAS + COUT * 4;
+  static constexpr int ACC = COUT;  // one 128-row tile per CTA
+  static constexpr int TALLOC = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
+};
+
+struct __align__(64) PairConvArgs {
+  CUtensorMap tmap;  // x as (8 ch, W, H, C/8 planes, N), box (8, 16, 11, C/8, 1)
+  CUtensorMap wmap;  // pair copy of the packed weights as 128-byte rows, box = one tap half
+  ConvArgs c;
+  unsigned long long* trace;  // diagnostics: per-CTA issuer wait totals (sbn_debug_set_trace)
+};
+
+template <int CIN, int COUT, int BS>
+__global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_kernel(const __grid_constant__ PairConvArgs pa) {
+  using P = PairConvCfg<CIN, COUT, BS>;
+  const ConvArgs& a = pa.c;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[P::STAGES], empty[P::STAGES];
+  __shared__ uint64_t win_full[2], win_empty[2], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tslot;
+  uint8_t* Wst = smem + P::OFF_W;
+  float* bias = reinterpret_cast<float*>(smem + P::OFF_BIAS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const Geo& g = a.g;
+
+  if (tid == 0) {
+    for (int s = 0; s < P::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&win_full[b], 1);
+      tc::mbar_init(&win_empty[b], 1);
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], 2 * kWorkers);
+    }
+    tc::mbar_fence_init();
+  }
+  if (tid == 10 * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&pa.tmap) : "memory");
+  if (tid == 8 * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&pa.wmap) : "memory");
+  for (int i = tid; i < COUT; i += kPairThreads) bias[i] = a.bias ? __bfloat162float(a.bias[i]) : 0.f;
+  if (warp == 0) tc::tmem_alloc_cg2<P::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast commit
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_wait();
+  const int B = ld_count(a.count, a.cap);
+
+  if (warp == 8) {
+    // ---------------- weight loader: my half (output channels) of every tap
+    if (lane == 0) {
+      int it = 0;
+      for (int blk = pair; blk < B; blk += npairs)
+        for (int tap = 0; tap < 9; ++tap, ++it) {
+          const int s = it % P::STAGES;
+          tc::mbar_wait(&empty[s], ((it / P::STAGES) & 1) ^ 1);
+          const int row = (2 * tap + (int)rank) * P::WBOXR;  // my half of this tap
+          if (rank == 0) {
+            tc::mbar_expect_tx(&full[s], 2 * P::TAPH);
+            tma_2d(Wst + s * P::TAPH, &pa.wmap, 0, row, &full[s]);
+          } else {
+            tma_2d_cg2(Wst + s * P::TAPH, &pa.wmap, 0, row, &full[s], 0);
+          }
+        }
+    }
+    __syncwarp();
+  } else if (warp == 10) {
+    // ---------------- window loader: my 11 window rows of every block, one TMA box
+    if (lane == 0) {
+      int k = 0;
+      for (int blk = pair; blk < B; blk += npairs, ++k) {
+        const int b = k & 1;
+        const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+        const int ys = g.oy + by * g.sy + (int)rank * (P::WROWS - 3), xs = g.ox + bx * g.sx;
+        tc::mbar_wait(&win_empty[b], ((k >> 1) & 1) ^ 1);
+        if (rank == 0) {
+          tc::mbar_expect_tx(&win_full[b], 2 * P::ABOX);
+          tma_5d(smem + b * P::SZ_A, &pa.tmap, 0, xs, ys, 0, n, &win_full[b]);
+        } else {
+          tma_5d_cg2(smem + b * P::SZ_A, &pa.tmap, 0, xs, ys, 0, n, &win_full[b], 0);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (rank 0): M = 256 over the pair
+      int it = 0, k = 0;
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, COUT);
+      unsigned long long t_win = 0, t_acc = 0, t_w = 0, t_iss = 0, t0 = clock64();
+      for (int blk = pair; blk < B; blk += npairs, ++k) {
+        const int b = k & 1;
+        const uint32_t use = (uint32_t)(k >> 1);
+        unsigned long long c0 = clock64();
+        tc::mbar_wait(&win_full[b], use & 1);
+        unsigned long long c1 = clock64();
+        tc::mbar_wait(&acc_empty[b], (use & 1) ^ 1);
+        unsigned long long c2 = clock64();
+        t_win += c1 - c0;
+        t_acc += c2 - c1;
+        tc::fence_after();
+        const uint8_t* A = smem + b * P::SZ_A;
+        const uint32_t acc = tmem + b * P::ACC;
+        for (int tap = 0; tap < 9; ++tap, ++it) {
+          const int s = it % P::STAGES;
+          unsigned long long c3 = clock64();
+          tc::mbar_wait(&full[s], (it / P::STAGES) & 1);
+          unsigned long long c4 = clock64();
+          t_w += c4 - c3;
+          tc::fence_after();
+          const int shift = (tap / 3) * BS + (tap % 3);
+          const uint32_t wbase = tc::smem_u32(Wst + s * P::TAPH);
+#pragma unroll
+          for (int kk = 0; kk < CIN / 16; ++kk)
+            tc::mma_bf16_cg2(acc, tc::desc_kmajor_noswz(tc::smem_u32(A + 2 * kk * P::PA + shift * 16), P::PA, 128),
+                             tc::desc_kmajor_noswz(wbase + 2 * kk * P::PWH, P::PWH, 128), idesc, (tap | kk) > 0);
+          tc::mma_commit_mc(&empty[s], 3);
+        }
+        tc::mma_commit_mc(&win_empty[b], 3);
+        tc::mma_commit_mc(&acc_full[b], 3);
+      }
+      if (pa.trace) {
+        unsigned long long* tb = pa.trace + blockIdx.x * 8;
+        tb[0] = clock64() - t0;
+        tb[1] = t_win;
+        tb[2] = t_acc;
+        tb[3] = t_w;
+        tb[4] = k;
+      }
+      (void)t_iss;
+    }
+    __syncwarp();
+  } else {
+    // ---------------- workers: drain my tile of each accumulator
+    const int q = warp & 3, tpar = warp >> 2;
+    int k = 0;
+    for (int blk = pair; blk < B; blk += npairs, ++k) {
+      const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
+      const int b = k & 1;
+      const int r = (int)rank * 128 + q * 32 + lane;
+      const int oy = r / BS, ox = r % BS;
+      const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+      const bool store = oy < g.obh && ox < g.obw && Y < g.oh && X < g.ow;
+      uint4* op = reinterpret_cast<uint4*>(a.out) +
+                  (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (COUT / 8);
+      tc::mbar_wait(&acc_full[b], (k >> 1) & 1);
+      tc::fence_after();
+      const uint32_t acc = tmem + b * P::ACC;
+#pragma unroll
+      for (int c0 = tpar * (COUT / 2); c0 < (tpar + 1) * (COUT / 2); c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(acc + ((uint32_t)(q * 32) << 16) + c0, v);
+        if (store) {
+          uint32_t o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            o[e] = tc::pack_bf16(v[2 * e] + bias[c0 + 2 * e], v[2 * e + 1] + bias[c0 + 2 * e + 1]);
+          op[c0 / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+          op[c0 / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+      }
+      tc::fence_before();
+      if (rank == 0) tc::mbar_arrive(&acc_empty[b]);
+      else tc::mbar_arrive_cluster(&acc_empty[b], 0);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // the peer's MMAs / remote arrivals are done before TMEM is freed
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free_cg2<P::TALLOC>(tmem);
+}
+
+template <int CIN, int COUT, int BS>
+int launch_conv_pair(const ConvArgs& c, int cap, cudaStream_t s) {
+  using P = PairConvCfg<CIN, COUT, BS>;
+  PairConvArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.c = c;
+  pa.trace = trace_buffer();
+  const Geo& g = c.g;
+  const uint64_t dims[5] = {8, (uint64_t)g.w, (uint64_t)g.h, (uint64_t)(CIN / 8), (uint64_t)g.n};
+  const uint64_t str[4] = {(uint64_t)CIN * 2, (uint64_t)g.w * CIN * 2, 16, (uint64_t)g.h * g.w * CIN * 2};
+  const uint32_t box[5] = {8, (uint32_t)BS, (uint32_t)P::WROWS, (uint32_t)(CIN / 8), 1};
+  int st = encode_map(&pa.tmap, c.x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st) return st;
+  const uint64_t wdims[2] = {64, (uint64_t)18 * P::WBOXR};  // 18 tap halves of WBOXR 128-byte rows
+  const uint64_t wstr[1] = {128};
+  const uint32_t wbox[2] = {64, (uint32_t)P::WBOXR};
+  st = encode_map(&pa.wmap, c.wpk + (size_t)9 * P::TAP, 2, wdims, wstr, wbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st) return st;
+  auto kern = conv_tc_pair_kernel<CIN, COUT, BS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM);
+  const int npairs = cap < sm_count() / 2 ? (cap < 1 ? 1 : cap) : sm_count() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * npairs));
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = P::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, pa);
+  return launch_status("sparse_conv_tcgen05_pair");
+}
+
 #define SBN_CONV_TC_CONFIGS(X) \
   X(128, 128, 16)              \
   X(128, 128, 8)               \
@@ -446,7 +711,7 @@ bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int 
   return false;
 }
 
-size_t sparse_conv_tc_packed_bytes(int cin, int cout) { return (size_t)9 * cin * cout * 2; }
+size_t sparse_conv_tc_packed_bytes(int cin, int cout) { return (size_t)2 * 9 * cin * cout * 2; }  // + pair copy
 
 int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_t s) {
 #define X(CI, CO, BS_) if (cin == CI && cout == CO) { conv_tc_pack_kernel<CI, CO><<<64, 256, 0, s>>>((const __nv_bfloat16*)w, (uint8_t*)img); return launch_status("sparse_conv_tc_pack"); }
@@ -467,6 +732,15 @@ int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, con
   a.idx = idx;
   a.count = count;
   a.cap = cap;
+  // CTA-pair (cta_group::2) variant: opt-in (SBN_DEBUG_CONV_PAIR) — measured slower than the
+  // double-buffered single-CTA kernel on config 3 (210 vs 175 us at 100 %, 37 vs 28 us at
+  // 10 %): the M = 256 MMA still reads ~96 B/clk of smem per SM and the per-pair weight
+  // stream (16 KB per tap per CTA) stalls the issuer 11 % of the time
+  if ((debug_flags() & kDebugConvPair) && g.bh == 16) {
+    if (cin == 128 && cout == 128) return launch_conv_pair<128, 128, 16>(a, cap, s);
+    if (cin == 64 && cout == 64) return launch_conv_pair<64, 64, 16>(a, cap, s);
+    if (cin == 32 && cout == 32) return launch_conv_pair<32, 32, 16>(a, cap, s);
+  }
   if (!(debug_flags() & kDebugConvSingleBuffer)) {
 #define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_ && DbCfg<CI, CO, BS_>::SMEM <= max_smem_optin()) return launch_conv_db<CI, CO, BS_>(a, cap, s);
     SBN_CONV_TC_CONFIGS(X)

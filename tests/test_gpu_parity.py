@@ -559,3 +559,31 @@ def test_fused_unit_alternating_geometries_share_workspace(cuda_device):
             xi = x.clone()
             P.sparse_residual_unit(P.Tensor4D(xi), mk, u, (16, 16), inplace=True)
             assert torch.equal(xi, ref)
+
+
+@pytest.mark.parametrize("cin,density", [(128, 0.3), (64, 1.0), (32, 0.5)])
+def test_sparse_conv_cta_pair_bit_identical(cuda_device, cin, density):
+    """The CTA-pair (cta_group::2, M = 256, TMA-fed 5-D window boxes, N-split weights)
+    sparse conv computes exactly what the single-CTA double-buffered kernel computes."""
+    from paper_1801_02108_b200.layers import sparse_conv_into
+    lib = _lib.load()
+    rng = np.random.default_rng(cin)
+    h, w = 150, 136
+    x = torch.from_numpy(rng.standard_normal((2, h, w, cin)).astype(np.float32)).bfloat16().cuda()
+    fb = P.FilterBank(torch.from_numpy((rng.standard_normal((3, 3, cin, cin)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16(),
+                      torch.from_numpy(rng.standard_normal(cin).astype(np.float32)).bfloat16())
+    p = _conv((3, 3), (1, 1), True, cin)
+    spec = P.compute_block_spec((2, h, w, cin), p, (16, 16))
+    mk = P.synth_mask_blobs((2, h, w), 1.0 - density, 4).cuda()
+    idx = P.reduce_mask(mk, spec)
+    outs = []
+    for flag in (lib.SBN_DEBUG_CONV_PAIR if hasattr(lib, "SBN_DEBUG_CONV_PAIR") else 32, 0):
+        old = lib.sbn_debug_set_flags(flag)
+        try:
+            o = torch.zeros_like(x)
+            sparse_conv_into(x, o, fb, p, spec, idx)
+            torch.cuda.synchronize()
+        finally:
+            lib.sbn_debug_set_flags(old)
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
