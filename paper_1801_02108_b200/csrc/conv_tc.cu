@@ -58,6 +58,7 @@ struct ConvArgs {
   const int32_t* idx;
   const int32_t* count;
   int cap;
+  unsigned long long* trace;  // diagnostics: per-CTA MMA-issuer wait totals (sbn_debug_set_trace)
 };
 
 template <int CIN, int COUT, int BS>
@@ -311,17 +312,24 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
     if (lane == 0) {
       int it = 0, k = 0;
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, COUT);
+      unsigned long long t_win = 0, t_acc = 0, t_w = 0, t0 = clock64();
       for (int blk = blockIdx.x; blk < B; blk += gridDim.x, ++k) {
         const int b = k & 1;
         const uint32_t use = (uint32_t)(k >> 1);
+        const unsigned long long c0 = clock64();
         tc::mbar_wait(&win_full[b], use & 1);
+        const unsigned long long c1 = clock64();
         tc::mbar_wait(&acc_empty[b], (use & 1) ^ 1);
+        t_win += c1 - c0;
+        t_acc += clock64() - c1;
         tc::fence_after();
         const uint8_t* A = smem + b * D::SZ_A;
         const uint32_t acc = tmem + b * D::ACC;
         for (int tap = 0; tap < 9; ++tap, ++it) {
           const int s = it % D::STAGES;
+          const unsigned long long c3 = clock64();
           tc::mbar_wait(&full[s], (it / D::STAGES) & 1);
+          t_w += clock64() - c3;
           tc::fence_after();
           const int shift = (tap / 3) * BS + (tap % 3);
           const uint32_t wbase = tc::smem_u32(Wst + s * K::TAP);
@@ -336,6 +344,14 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
         }
         tc::mma_commit(&win_empty[b]);
         tc::mma_commit(&acc_full[b]);
+      }
+      if (a.trace) {
+        unsigned long long* tb = a.trace + blockIdx.x * 8;
+        tb[0] = clock64() - t0;
+        tb[1] = t_win;
+        tb[2] = t_acc;
+        tb[3] = t_w;
+        tb[4] = k;
       }
     }
     __syncwarp();
@@ -732,6 +748,7 @@ int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, con
   a.idx = idx;
   a.count = count;
   a.cap = cap;
+  a.trace = trace_buffer();
   // CTA-pair (cta_group::2) variant: opt-in (SBN_DEBUG_CONV_PAIR) — measured slower than the
   // double-buffered single-CTA kernel on config 3 (210 vs 175 us at 100 %, 37 vs 28 us at
   // 10 %): the M = 256 MMA still reads ~96 B/clk of smem per SM and the per-pair weight

@@ -12,7 +12,7 @@ from paper_1801_02108_b200.layers import sparse_conv_into
 
 dev = torch.device("cuda", 0)
 lib = _lib.load()
-lib.sbn_debug_set_flags(32)  # CTA-pair variant
+lib.sbn_debug_set_flags(int(os.environ.get('FLAGS', 32)))  # 32: CTA-pair variant, 0: single-CTA double-buffered
 C, H, W = 128, 800, 700
 rng = np.random.default_rng(C)
 x = torch.from_numpy(rng.standard_normal((1, H, W, C)).astype(np.float32)).bfloat16().to(dev)

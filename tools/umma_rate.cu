@@ -1,0 +1,96 @@
+// UMMA issue-rate probe: cycles per tcgen05.mma (bf16, M=128, N in {64,128,256}, K=16,
+// operands from shared memory) for the SWIZZLE_NONE "plane" K-major layout the row-shift
+// kernels use vs the 128-byte-swizzled K-major layout TMA writes, with and without a
+// one-row start offset (the row-shift trick).  One CTA per SM, back-to-back MMAs into one
+// accumulator, timed with clock64 around issue + commit wait.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I paper_1801_02108_b200/csrc -o tools/bin/umma_rate tools/umma_rate.cu
+#include <cstdio>
+
+#include <cuda_bf16.h>
+#include <cstdint>
+#include "tc_util.cuh"
+
+using namespace sbn;
+
+template <int N, int MODE>  // MODE 0: noswz plane layout, 1: noswz + 1-row shift, 2: SW128, 3: SW128 + 8-row shift
+__global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* A = smem;                 // up to 64 KB
+  uint8_t* B = smem + 64 * 1024;     // up to 64 KB
+  for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::mbar_fence_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc<256>(&tslot);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = tc::idesc_bf16_f32(128, N);
+    const uint32_t a0 = tc::smem_u32(A), b0 = tc::smem_u32(B);
+    constexpr uint32_t PA = 200 * 16 + 16;  // plane stride (noswz): 200 rows
+    constexpr uint32_t PB = N * 16;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const int kk = i & 3;
+      uint64_t ad, bd;
+      if (MODE <= 1) {
+        ad = tc::desc_kmajor_noswz(a0 + 2 * kk * PA + (MODE == 1 ? 16 * (1 + (i % 7)) : 0), PA, 128);
+        bd = tc::desc_kmajor_noswz(b0 + 2 * kk * PB, PB, 128);
+      } else {
+        ad = tc::desc_kmajor_swz(a0 + kk * 32 + (MODE == 3 ? 1024 : 0), 1024, 2);
+        bd = tc::desc_kmajor_swz(b0 + kk * 32, 1024, 2);
+      }
+      tc::mma_bf16(tmem, ad, bd, idesc, i > 0);
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (threadIdx.x < 32) tc::tmem_free<256>(tmem);
+}
+
+template <int N, int MODE>
+void run(const char* name, int nsm) {
+  long long* d;
+  cudaMalloc(&d, nsm * sizeof(long long));
+  auto k = rate_kernel<N, MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+  const int iters = 4096;
+  k<<<nsm, 128, 128 * 1024>>>(d, iters);
+  k<<<nsm, 128, 128 * 1024>>>(d, iters);
+  cudaDeviceSynchronize();
+  long long h[256];
+  cudaMemcpy(h, d, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+  double m = 0;
+  for (int i = 0; i < nsm; ++i) m += h[i];
+  m /= nsm;
+  const double floor = 128.0 * N / 256.0;
+  printf("%-34s N=%3d  %6.1f cyc/MMA  (floor %5.1f, %4.0f%%)  %s\n", name, N, m / iters, floor, 100 * floor / (m / iters),
+         cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
+int main() {
+  int nsm = 148;
+  run<128, 0>("noswz plane layout", nsm);
+  run<128, 1>("noswz + row shift", nsm);
+  run<128, 2>("SW128", nsm);
+  run<128, 3>("SW128 + 8-row offset", nsm);
+  run<64, 0>("noswz plane layout", nsm);
+  run<64, 2>("SW128", nsm);
+  run<256, 0>("noswz plane layout", nsm);
+  run<256, 2>("SW128", nsm);
+  run<32, 0>("noswz plane layout", nsm);
+  run<32, 2>("SW128", nsm);
+  return 0;
+}
