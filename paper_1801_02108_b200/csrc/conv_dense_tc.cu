@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
           tc::fence_before();
           tc::mbar_arrive(&acc_empty[buf]);
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kCE) : "memory");
+        tc::named_bar<1, kCE>();
         // copy out: consecutive threads take consecutive 16-B chunks of one output row
 #pragma unroll 1
         for (int jb = 0; jb < IT2; jb += BATCH) {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
                 *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
           }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kCE) : "memory");  // staging / rowdst reuse
+        tc::named_bar<1, kCE>();  // staging / rowdst reuse
       }
     }
   } else if (warp == kLWarp) {

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs a) {
         }
       }
       tc::fence_async_smem();
-      asm volatile("bar.sync 1, %0;" ::"n"(kWorkers));
+      tc::named_bar<1, kWorkers>();
 
       if (tid == 0) {
         tc::fence_after();
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs a) {
         }
       }
       tc::fence_before();
-      asm volatile("bar.sync 1, %0;" ::"n"(kWorkers));
+      tc::named_bar<1, kWorkers>();
     }
   }
   tc::fence_before();

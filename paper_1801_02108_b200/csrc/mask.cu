@@ -230,6 +230,7 @@ reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, do
   uint8_t* flag = sm + (size_t)per * g.w * 4;                // [per * gx]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double area = (double)g.bh * (double)g.bw;
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // "I have started"
 
   if (vec) {
     const int wpr = g.w >> 2;
@@ -293,6 +294,9 @@ reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, do
   }
   if (lane == 31) wsum[warp] = incl;
   __syncthreads();
+  // every CTA of the cluster must have started before CTA 0's shared memory is written
+  // remotely (arrived right at kernel entry, so this wait is normally already satisfied)
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (warp == 0) {
     const int ws = lane < kClusterThreads / 32 ? wsum[lane] : 0;
     int wi = ws;

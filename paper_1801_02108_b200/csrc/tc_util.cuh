@@ -112,6 +112,15 @@ __device__ __forceinline__ void tmem_free_cg2(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
 }
 
+// Named barrier over a subset of warps.  The inline-asm bar.sync is not a convergence point
+// to the compiler, so reconverge the warp first (bar.sync is .aligned: every lane of a warp
+// must execute the same instance; compute-sanitizer synccheck flags it otherwise).
+template <int ID, int COUNT>
+__device__ __forceinline__ void named_bar() {
+  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");
+}
+
 // ---- fences
 __device__ __forceinline__ void fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -913,6 +913,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   const int q = warp & 3, hf = warp >> 2;  // TMEM lane quarter, column half
   const Geo& g = a.g;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // "this CTA has started": the partner's first DSMEM write (epilogue 1) waits for it
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
   trace(a.trace, 0);
   if (tid == 0) {
@@ -996,6 +998,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   const int P = rim.pixels();
   uint8_t* A2peer = rank > 0 ? cl.map_shared_rank(A2, rank - 1) : nullptr;
 
+  int round = 0;
   for (int blk = pair;;) {
     const int n = n1, by = by1, bx = bx1;
     trace(a.trace, 18);
@@ -1074,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     tc::fence_after();
     trace(a.trace, 6);
     // ---- 3. epilogue 1 -> A2 (local rows; rank>0 also feeds the previous tile's halo rows)
+    if (round == 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // partner started
     {
       const int j = q * 32 + lane;
       const int r = rank * 128 + j;
@@ -1216,6 +1220,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     }
     if (!next) break;
     cl.sync();  // partner done with my A2 before it writes the next block's halo rows
+    ++round;
   }
   tc::fence_after();
   if (warp == 0) tc::tmem_free<PK::TALLOC>(tmem);

@@ -168,6 +168,47 @@ __device__ __forceinline__ int tile_count(const WArgs& a, int B, int b) {
   return (int)((rows + 127) / 128);
 }
 
+// OUT copy phase, shared by the idle A warps and the epilogue warps (kOutCopy threads,
+// copy index `ct`): wait for the staged bf16(acc + b3) group, then along whole output pixel
+// rows load the residual, add, store (coalesced 16-B vectors), and release the staging
+// buffer.  One non-inlined body, so both warp groups reach the named barrier at the same
+// instruction.
+template <int SPITCH, int CHR, int IT2>
+__device__ __noinline__ void out_copy_phase(__nv_bfloat16* dst, const uint8_t* stg, const long long* rowdst, int g0,
+                                            int ct) {
+  constexpr int BATCH = IT2 < 6 ? IT2 : 6;  // residual loads in flight per thread
+  tc::named_bar<3, kOutCopy>();
+#pragma unroll 1
+  for (int jb = 0; jb < IT2; jb += BATCH) {
+    uint4 xr[BATCH];
+#pragma unroll
+    for (int jj = 0; jj < BATCH; ++jj) {
+      const int it = ct + (jb + jj) * kOutCopy;
+      const long long off = (jb + jj < IT2 && it < 128 * CHR) ? rowdst[it / CHR] : -1;
+      xr[jj] = tc::ld_v4_pred(reinterpret_cast<const uint4*>(dst + (off >= 0 ? off + g0 : 0)) + it % CHR, off >= 0);
+    }
+#pragma unroll
+    for (int jj = 0; jj < BATCH; ++jj) {
+      const int it = ct + (jb + jj) * kOutCopy;
+      if (jb + jj >= IT2 || it >= 128 * CHR) break;
+      const int row = it / CHR, ch = it % CHR;
+      const long long off = rowdst[row];
+      if (off < 0) continue;
+      const uint4 sv = *reinterpret_cast<const uint4*>(stg + row * SPITCH + ch * 16);
+      const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[jj]);
+      const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&sv);
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 xf = __bfloat1622float2(xh[q]), uf = __bfloat1622float2(uh[q]);
+        o[q] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
+      }
+      reinterpret_cast<uint4*>(dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  tc::named_bar<3, kOutCopy>();  // staging / rowdst reuse
+}
+
 template <int K, int N, int MODE>
 __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid_constant__ WArgs a) {
   using Q = WCfg<K, N, MODE>;
@@ -282,41 +323,9 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       // phase (residual add along pixel rows), same barrier sequence as the epilogue warps
       constexpr int GS = Q::GS, CHR = GS * 2 / 16;
       constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
-      constexpr int BATCH = IT2 < 6 ? IT2 : 6;
       const uint8_t* stg = smem + Q::OFF_STG;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int g0 = 0; g0 < N; g0 += GS) {
-          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");
-#pragma unroll 1
-          for (int jb = 0; jb < IT2; jb += BATCH) {
-            uint4 xr[BATCH];
-#pragma unroll
-            for (int jj = 0; jj < BATCH; ++jj) {
-              const int it = tid + (jb + jj) * kOutCopy;
-              const long long off = (jb + jj < IT2 && it < 128 * CHR) ? rowdst[it / CHR] : -1;
-              if (off >= 0) xr[jj] = reinterpret_cast<const uint4*>(a.dst + off + g0)[it % CHR];
-            }
-#pragma unroll
-            for (int jj = 0; jj < BATCH; ++jj) {
-              const int it = tid + (jb + jj) * kOutCopy;
-              if (jb + jj >= IT2 || it >= 128 * CHR) break;
-              const int row = it / CHR, ch = it % CHR;
-              const long long off = rowdst[row];
-              if (off < 0) continue;
-              const uint4 sv = *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
-              const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[jj]);
-              const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&sv);
-              uint32_t o[4];
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float2 xf = __bfloat1622float2(xh[q]), uf = __bfloat1622float2(uh[q]);
-                o[q] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
-              }
-              reinterpret_cast<uint4*>(a.dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
-            }
-          }
-          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");
-        }
+        for (int g0 = 0; g0 < N; g0 += GS) out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
     }
   } else if (tid < kAThreads + kEThreads) {
     // ------------------------------------------------ epilogue
@@ -411,7 +420,6 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
         constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
         static_assert(N % GS == 0, "staging groups");
         uint8_t* stg = smem + Q::OFF_STG;
-        const int et = tid;  // copy-phase index over the idle A warps + the epilogue warps
         const float* b3 = par;
         if (half == 0) rowdst[r] = store ? (long long)(dp - a.dst) : -1;
         for (int g0 = 0; g0 < N; g0 += GS) {
@@ -436,39 +444,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             tc::fence_before();
             tc::mbar_arrive(&acc_empty[buf]);
           }
-          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");
-          constexpr int BATCH = IT2 < 6 ? IT2 : 6;  // residual loads in flight per thread
-#pragma unroll 1
-          for (int jb = 0; jb < IT2; jb += BATCH) {
-          uint4 xr[BATCH];
-#pragma unroll
-          for (int jj = 0; jj < BATCH; ++jj) {
-            const int it = et + (jb + jj) * kOutCopy;
-            const int row = it / CHR, ch = it % CHR;
-            const long long off = (jb + jj < IT2 && it < 128 * CHR) ? rowdst[row] : -1;
-            if (off >= 0) xr[jj] = reinterpret_cast<const uint4*>(a.dst + off + g0)[ch];
-          }
-#pragma unroll
-          for (int jj = 0; jj < BATCH; ++jj) {
-            const int j = jb + jj;
-            if (j >= IT2) break;
-            const int it = et + j * kOutCopy;
-            const int row = it / CHR, ch = it % CHR;
-            const long long off = it < 128 * CHR ? rowdst[row] : -1;
-            if (off < 0) continue;
-            const uint4 sv = *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
-            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[jj]);
-            const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&sv);
-            uint32_t o[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float2 xf = __bfloat1622float2(xh[q]), uf = __bfloat1622float2(uh[q]);
-              o[q] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
-            }
-            reinterpret_cast<uint4*>(a.dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
-          }
-          }
-          asm volatile("bar.sync 3, %0;" ::"n"(kOutCopy) : "memory");  // staging / rowdst reuse
+          out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
         }
         if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
         meta(tile + gridDim.x);

@@ -587,3 +587,25 @@ def test_sparse_conv_cta_pair_bit_identical(cuda_device, cin, density):
             lib.sbn_debug_set_flags(old)
         outs.append(o)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("block,stride", [(16, 1), (9, 1), (17, 2)])
+def test_scatter_write_count_matches_oracle(cuda_device, block, stride):
+    """Race-freedom of the scatter (reference tests/oracles.py:49-56 write_count_map,
+    SPEC.md:270): scatter_add of all-ones blocks onto zeros counts the writes each output
+    pixel receives; it must equal the oracle's count map exactly (0 or 1: disjoint
+    interiors, no atomics needed)."""
+    n, h, w, c = 2, 83, 71, 8
+    p = _conv((3, 3), (stride, stride), True, c)
+    spec = P.compute_block_spec((n, h, w, c), p, (block, block))
+    mk = P.synth_mask_blobs((n, h, w), 0.5, block).cuda()
+    idx = P.reduce_mask(mk, spec)
+    obh, obw = spec.out_block_size
+    ones = P.GatheredBlocks(P.Tensor4D(torch.ones(idx.count, obh, obw, c, device="cuda")), spec, idx)
+    oh, ow = spec.out_size
+    got = _np(P.scatter_add(ones, spec, P.Tensor4D(torch.zeros(n, oh, ow, c, device="cuda"))))
+    want = np.zeros((n, oh, ow), np.int64)
+    for i, by, bx in idx.entries:
+        want[i, by * obh:min((by + 1) * obh, oh), bx * obw:min((bx + 1) * obw, ow)] += 1
+    assert want.max() <= 1
+    assert np.array_equal(got, np.repeat(want[..., None], c, axis=-1).astype(np.float32))

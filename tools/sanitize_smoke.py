@@ -1,0 +1,66 @@
+"""One small invocation of every hot kernel, for compute-sanitizer (memcheck / racecheck /
+synccheck): reduce_mask (ordered + cluster), gather / scatter / scatter_add / transpose,
+sparse conv (SIMT fp32, tcgen05 single-CTA, CTA-pair, strided TMA), residual unit (SIMT,
+fused mask + CTA pair in place, wide), dense conv, host-frame unit copies."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1801_02108_b200 as P
+from paper_1801_02108_b200 import _lib
+from paper_1801_02108_b200.layers import residual_unit_into, sparse_conv_into
+
+dev = torch.device("cuda", 0)
+lib = _lib.load()
+rng = np.random.default_rng(0)
+n, h, w = 2, 72, 60
+mk = P.synth_mask_blobs((n, h, w), 0.6, 1).cuda()
+
+# reduce_mask / gather / scatter
+x32 = torch.randn(n, h, w, 16, device=dev)
+p3 = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 16)
+spec = P.compute_block_spec((n, h, w, 16), p3, (16, 16))
+idx = P.reduce_mask(mk, spec)
+P.gather(P.Tensor4D(x32), idx, spec)
+spec1 = P.compute_block_spec((n, h, w, 16), P.ConvParams((1, 1), (1, 1), P.Padding.VALID, 16), (8, 8))
+idx1 = P.reduce_mask(mk, spec1)
+g1 = P.gather(P.Tensor4D(x32), idx1, spec1)
+P.scatter(g1, spec1, P.Tensor4D(torch.zeros_like(x32)))
+P.scatter_add(g1, spec1, P.Tensor4D(torch.zeros_like(x32)))
+gt = P.gather_transpose(P.Tensor4D(x32), idx1, spec1)
+P.scatter_transpose(gt, spec1, P.Tensor4D(torch.zeros_like(x32)))
+# sparse convs
+f32 = P.FilterBank(torch.randn(3, 3, 16, 16) * 0.1, torch.randn(16))
+P.sparse_conv2d(P.Tensor4D(x32), mk, f32, p3, (16, 16))
+for c, blk_, flags in ((128, 16, 0), (128, 16, 32), (64, 8, 0)):
+    x = torch.randn(n, h, w, c, device=dev).bfloat16()
+    fb = P.FilterBank((torch.randn(3, 3, c, c) / (3 * c ** 0.5)).bfloat16(), torch.randn(c).bfloat16())
+    pc = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, c)
+    old = lib.sbn_debug_set_flags(flags)
+    P.sparse_conv2d(P.Tensor4D(x), mk, fb, pc, (blk_, blk_))
+    lib.sbn_debug_set_flags(old)
+x = torch.randn(n, h, w, 64, device=dev).bfloat16()
+fb = P.FilterBank((torch.randn(3, 3, 64, 64) / 24).bfloat16(), torch.randn(64).bfloat16())
+P.sparse_conv2d(P.Tensor4D(x), mk, fb, P.ConvParams((3, 3), (2, 2), P.Padding.SAME, 64), (17, 17))
+# residual units
+u = P.random_unit_params(rng, 64, 32)
+P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16))
+xi = x.clone()
+P.sparse_residual_unit(P.Tensor4D(xi), mk, u, (16, 16), inplace=True)
+P.sparse_residual_unit(P.Tensor4D(x.float()), mk, u, (16, 16))
+old = lib.sbn_debug_set_flags(4)  # wide three-launch unit
+P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16))
+lib.sbn_debug_set_flags(old)
+# dense projection conv (tcgen05, bias fused)
+from paper_1801_02108_b200.ops import projection_conv
+xp = torch.randn(1, 50, 38, 32, device=dev).bfloat16()
+fp = P.FilterBank((torch.randn(3, 3, 32, 96) / 17).bfloat16(), torch.randn(96).bfloat16())
+projection_conv(xp, fp, P.ConvParams((3, 3), (2, 2), P.Padding.SAME, 96))
+# host-frame unit (zero-copy copies)
+hx = x.cpu().pin_memory()
+P.sparse_residual_unit(P.Tensor4D(hx), P.BinaryMask(mk.data.cpu().pin_memory()), u, (16, 16), inplace=True)
+torch.cuda.synchronize()
+print("sanitize smoke done", flush=True)
