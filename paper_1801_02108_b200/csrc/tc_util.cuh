@@ -120,6 +120,12 @@ __device__ __forceinline__ void named_bar() {
   __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");
 }
+// Non-.aligned form, for a named barrier that different warps reach from different
+// instructions (PTX: the .aligned form requires every participant to execute the same one).
+template <int ID, int COUNT>
+__device__ __forceinline__ void named_bar_any() {
+  asm volatile("barrier.sync %0, %1;" ::"n"(ID), "n"(COUNT) : "memory");
+}
 
 // ---- fences
 __device__ __forceinline__ void fence_before() {

@@ -171,13 +171,12 @@ __device__ __forceinline__ int tile_count(const WArgs& a, int B, int b) {
 // OUT copy phase, shared by the idle A warps and the epilogue warps (kOutCopy threads,
 // copy index `ct`): wait for the staged bf16(acc + b3) group, then along whole output pixel
 // rows load the residual, add, store (coalesced 16-B vectors), and release the staging
-// buffer.  One non-inlined body, so both warp groups reach the named barrier at the same
-// instruction.
+// buffer.  Inlined at both call sites, so the barrier is the non-.aligned form.
 template <int SPITCH, int CHR, int IT2>
-__device__ __noinline__ void out_copy_phase(__nv_bfloat16* dst, const uint8_t* stg, const long long* rowdst, int g0,
+__device__ __forceinline__ void out_copy_phase(__nv_bfloat16* dst, const uint8_t* stg, const long long* rowdst, int g0,
                                             int ct) {
   constexpr int BATCH = IT2 < 6 ? IT2 : 6;  // residual loads in flight per thread
-  tc::named_bar<3, kOutCopy>();
+  tc::named_bar_any<3, kOutCopy>();
 #pragma unroll 1
   for (int jb = 0; jb < IT2; jb += BATCH) {
     uint4 xr[BATCH];
@@ -206,7 +205,7 @@ __device__ __noinline__ void out_copy_phase(__nv_bfloat16* dst, const uint8_t* s
       reinterpret_cast<uint4*>(dst + off + g0)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
-  tc::named_bar<3, kOutCopy>();  // staging / rowdst reuse
+  tc::named_bar_any<3, kOutCopy>();  // staging / rowdst reuse
 }
 
 template <int K, int N, int MODE>
