@@ -255,6 +255,10 @@ struct DbCfg {
   static constexpr int OFF_BIAS = OFF_W + STAGES * K::TAP;
   static constexpr int SMEM = OFF_BIAS + COUT * 4;
   static constexpr int ACC = K::NT * COUT;  // TMEM columns per accumulator
+  // small blocks share one M-tile: BPT windows stacked at BS*BS-row pitch (8x8 blocks: 2
+  // per tile, 96 of 128 rows useful instead of 48).  A block's shifted views reach at most
+  // 2*BS+2 rows past its own outputs, i.e. only into its neighbour's garbage columns.
+  static constexpr int BPT = (K::NT == 1 && 2 * BS * BS <= 128) ? 128 / (BS * BS) : 1;
   static constexpr int TALLOC = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
   static_assert(2 * ACC <= 512, "two accumulators must fit TMEM");
 };
@@ -293,12 +297,13 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   const uint32_t tmem = tslot;
   tc::pdl_wait();
   const int B = ld_count(a.count, a.cap);
+  const int NJ = (B + D::BPT - 1) / D::BPT;  // jobs: BPT consecutive blocks of the list
 
   if (warp == 8) {
     // ---------------- producer: weight taps through the ring
     if (lane == 0) {
       int it = 0;
-      for (int blk = blockIdx.x; blk < B; blk += gridDim.x)
+      for (int job = blockIdx.x; job < NJ; job += gridDim.x)
         for (int tap = 0; tap < 9; ++tap, ++it) {
           const int s = it % D::STAGES;
           tc::mbar_wait(&empty[s], ((it / D::STAGES) & 1) ^ 1);
@@ -313,7 +318,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       int it = 0, k = 0;
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, COUT);
       unsigned long long t_win = 0, t_acc = 0, t_w = 0, t0 = clock64();
-      for (int blk = blockIdx.x; blk < B; blk += gridDim.x, ++k) {
+      for (int job = blockIdx.x; job < NJ; job += gridDim.x, ++k) {
         const int b = k & 1;
         const uint32_t use = (uint32_t)(k >> 1);
         const unsigned long long c0 = clock64();
@@ -358,18 +363,29 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   } else {
     // ---------------- workers: stage window k, drain accumulator k-1
     const int q = warp & 3, tpar = warp >> 2;
-    int pn = 0, pby = 0, pbx = 0;  // previous block (for its epilogue)
+    int pjob = 0;  // previous job (for its epilogue)
     int k = 0;
-    auto epilogue = [&](int kk, int n, int by, int bx) {
+    auto epilogue = [&](int kk, int job) {
       const int b = kk & 1;
       tc::mbar_wait(&acc_full[b], (kk >> 1) & 1);
       tc::fence_after();
       const uint32_t acc = tmem + b * D::ACC;
       for (int t = tpar; t < K::NT; t += 2) {
-        const int r = t * 128 + q * 32 + lane;
+        int r = t * 128 + q * 32 + lane;
+        int blk = job;
+        if (D::BPT > 1) {  // packed tile: this row belongs to block r / (BS*BS) of the job
+          blk = job * D::BPT + r / (BS * BS);
+          r %= BS * BS;
+        }
+        int n = 0, by = 0, bx = 0;
+        if (blk < B) {
+          n = __ldg(a.idx + 3 * blk);
+          by = __ldg(a.idx + 3 * blk + 1);
+          bx = __ldg(a.idx + 3 * blk + 2);
+        }
         const int oy = r / BS, ox = r % BS;
         const int Y = by * g.obh + oy, X = bx * g.obw + ox;
-        const bool store = oy < g.obh && ox < g.obw && Y < g.oh && X < g.ow;
+        const bool store = blk < B && oy < g.obh && ox < g.obw && Y < g.oh && X < g.ow;
         uint4* op = reinterpret_cast<uint4*>(a.out) +
                     (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (COUT / 8);
 #pragma unroll 4
@@ -389,13 +405,12 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       tc::fence_before();
       tc::mbar_arrive(&acc_empty[b]);
     };
-    for (int blk = blockIdx.x; blk < B; blk += gridDim.x, ++k) {
+    for (int job = blockIdx.x; job < NJ; job += gridDim.x, ++k) {
       const int b = k & 1;
-      const int n = __ldg(a.idx + 3 * blk), by = __ldg(a.idx + 3 * blk + 1), bx = __ldg(a.idx + 3 * blk + 2);
-      const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
       tc::mbar_wait(&win_empty[b], ((k >> 1) & 1) ^ 1);
       uint8_t* A = smem + b * D::SZ_A;
-      constexpr int TOT = BS * BS * (CIN / 8);
+      constexpr int PER = BS * BS * (CIN / 8);  // items per block window
+      constexpr int TOT = D::BPT * PER;
       constexpr int ITEMS = (TOT + kWorkers - 1) / kWorkers;
       constexpr int CH = ITEMS > 16 ? 16 : ITEMS;
 #pragma unroll 1
@@ -404,29 +419,36 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int i = tid + (base + j) * kWorkers;
-          const int p = i / (CIN / 8), kc = i % (CIN / 8);
+          const int jb = i / PER, ii = i - jb * PER;
+          const int blk = job * D::BPT + jb;
+          const int p = ii / (CIN / 8), kc = ii % (CIN / 8);
+          int n = 0, ys = 0, xs = 0;
+          if (i < TOT && blk < B) {
+            n = __ldg(a.idx + 3 * blk);
+            ys = g.oy + __ldg(a.idx + 3 * blk + 1) * g.sy;
+            xs = g.ox + __ldg(a.idx + 3 * blk + 2) * g.sx;
+          }
           const int y = ys + p / BS, xx = xs + p % BS;
           raw[j] = make_uint4(0, 0, 0, 0);
-          if (i < TOT && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+          if (i < TOT && blk < B && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
             raw[j] = __ldg(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (CIN / 8) + kc);
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int i = tid + (base + j) * kWorkers;
           if (i < TOT) {
-            const int p = i / (CIN / 8), kc = i % (CIN / 8);
+            const int jb = i / PER, ii = i - jb * PER;
+            const int p = jb * BS * BS + ii / (CIN / 8), kc = ii % (CIN / 8);
             *reinterpret_cast<uint4*>(A + kc * K::PA + p * 16) = raw[j];
           }
         }
       }
       tc::fence_async_smem();
       tc::mbar_arrive(&win_full[b]);
-      if (k > 0) epilogue(k - 1, pn, pby, pbx);
-      pn = n;
-      pby = by;
-      pbx = bx;
+      if (k > 0) epilogue(k - 1, pjob);
+      pjob = job;
     }
-    if (k > 0) epilogue(k - 1, pn, pby, pbx);
+    if (k > 0) epilogue(k - 1, pjob);
   }
   tc::fence_before();
   __syncthreads();
@@ -440,7 +462,7 @@ int launch_conv_db(const ConvArgs& a, int cap, cudaStream_t s) {
   auto kern = conv_tc_db_kernel<CIN, COUT, BS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(persistent_grid(cap, 1));
+  cfg.gridDim = dim3(persistent_grid((cap + D::BPT - 1) / D::BPT, 1));
   cfg.blockDim = dim3(kDbThreads);
   cfg.dynamicSmemBytes = D::SMEM;
   cfg.stream = s;
