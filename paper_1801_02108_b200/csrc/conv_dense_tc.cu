@@ -39,7 +39,10 @@ constexpr bool dense_resident() {
 template <int CIN, int COUT, int KS>
 struct CCfg {
   static constexpr int TAPS = KS * KS;
-  static constexpr int KC = (CIN % 64 == 0 && dense_resident<CIN, COUT, KS>()) ? 64 : 32;
+  // 64-channel K-chunks whenever CIN allows: each TMA box row is then 128 B (SWIZZLE_128B)
+  // per pixel; 32-channel chunks (64-B rows) made the per-tap boxes TMA-issue bound
+  // (block-32 sparse conv 348 -> 219 us at 100 %, 192->256 projection 84 -> 68 us)
+  static constexpr int KC = CIN % 64 == 0 ? 64 : 32;
   static_assert(CIN % KC == 0, "CIN must be a multiple of 32");
   static constexpr int NKC = CIN / KC;
   static constexpr int ROWB = KC * 2;
