@@ -699,6 +699,15 @@ def run_conv_sweep(P, torch, dev, time_graph):
             res["rows"].append({"density": d, "block": blk, "blocks": int(nb), "algo": algo,
                                 "sparse_ms": round(t, 5), "speedup_vs_dense": round(dense_ms / t, 3),
                                 "tflops_alg": round(flops / (t * 1e-3) / 1e12, 1)})
+    # the autotuner's choice (reference perf.py:167-195: fastest candidate, ties toward the
+    # smaller block) per density, from the same CUDA-graph timings
+    best = {}
+    for r in res["rows"]:
+        k = str(r["density"])
+        if k not in best or (r["sparse_ms"], r["block"]) < (best[k]["sparse_ms"], best[k]["block"]):
+            best[k] = r
+    res["autotuned_block"] = {k: {"block": v["block"], "sparse_ms": v["sparse_ms"],
+                                  "speedup_vs_dense": v["speedup_vs_dense"]} for k, v in best.items()}
     return res
 
 
