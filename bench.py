@@ -289,14 +289,14 @@ def run_ours(args):
     #      the host frame) -> host frame updated, every step.  The call moves the mask plus
     #      the active blocks' input windows host->device and their output windows back
     #      (sbn_copy_block_regions over PCIe, UVA), so PCIe carries only what the sparse
-    #      layer touches.  Four streams take frames round-robin so steps' H2D reads, kernels
-    #      and D2H writes overlap (measured: 2 streams 8.0K, 4 streams 9.6K frames/s — PCIe
-    #      zero-copy traffic then runs at ~55 of the ~57 GB/s this box sustains).
-    ne = min(nf, 4)
+    #      layer touches.  Eight streams take frames round-robin so steps' H2D reads, kernels
+    #      and D2H writes overlap (measured: 2 streams 8.0K, 4 streams 9.6K, 8 streams 9.9K
+    #      frames/s — PCIe zero-copy traffic then runs at the ~57 GB/s this box sustains).
+    ne = min(nf, 8)
     hx = [xs[f].cpu().pin_memory() for f in range(ne)]
     hm = [masks[f].data.cpu().pin_memory() for f in range(ne)]
     hmask = [P.BinaryMask(hm[f], validate=False) for f in range(ne)]
-    nst = int(os.environ.get("SBN_E2E_STREAMS", 4))  # must divide ne: a frame stays on one stream
+    nst = int(os.environ.get("SBN_E2E_STREAMS", 8))  # must divide ne: a frame stays on one stream
     e2e_streams = [torch.cuda.Stream() for _ in range(nst)]
     e2e_steps = max(ne, min(args.steps // 5, 400))
 
@@ -452,7 +452,7 @@ def run_ours(args):
                     "api": "sparse_residual_unit(Tensor4D(pinned host frame), pinned host mask, inplace=True)",
                     "path": "mask + the union of the active input windows H2D (zero-copy reads of the host frame), "
                             "reduce_mask + fused unit on the device staging frame, active output windows D2H "
-                            "into the host frame; 4 streams take frames round-robin",
+                            "into the host frame; 8 streams take frames round-robin",
                     "full_frame_copy": {"value": round(world * 1e3 / e2e_full_ms, 2), "unit": UNIT,
                                         "h2d_bytes_per_step": int(hx[0].numel() * 2 + hm[0].numel()),
                                         "d2h_bytes_per_step": int(hx[0].numel() * 2)}},
