@@ -609,3 +609,27 @@ def test_scatter_write_count_matches_oracle(cuda_device, block, stride):
         want[i, by * obh:min((by + 1) * obh, oh), bx * obw:min((bx + 1) * obw, ow)] += 1
     assert want.max() <= 1
     assert np.array_equal(got, np.repeat(want[..., None], c, axis=-1).astype(np.float32))
+
+
+def test_fused_unit_empty_and_alternating_masks(cuda_device):
+    """The mask-fused tcgen05 unit with an empty mask leaves x bit-identical (in place and
+    functional), and launches with no work interleaved with real ones keep the slot /
+    epoch protocol consistent (reference layers.py:221-222: empty list returns x)."""
+    from paper_1801_02108_b200.layers import residual_unit_into
+    rng = np.random.default_rng(31)
+    x = torch.from_numpy(rng.standard_normal((1, 160, 144, 64)).astype(np.float32)).bfloat16().cuda()
+    u = P.random_unit_params(rng, 64, 32)
+    empty = P.BinaryMask(torch.zeros(1, 160, 144, dtype=torch.uint8)).cuda()
+    blobs = P.synth_mask_blobs((1, 160, 144), 0.85, 7).cuda()
+    spec = P.unit_spec(tuple(x.shape), (16, 16))
+    ref = x.clone()
+    residual_unit_into(ref, x, u, spec, P.reduce_mask(blobs, spec))
+    for _ in range(3):
+        y = P.sparse_residual_unit(P.Tensor4D(x), empty, u, (16, 16)).data
+        assert torch.equal(y, x)
+        xi = x.clone()
+        P.sparse_residual_unit(P.Tensor4D(xi), empty, u, (16, 16), inplace=True)
+        assert torch.equal(xi, x)
+        xi = x.clone()
+        P.sparse_residual_unit(P.Tensor4D(xi), blobs, u, (16, 16), inplace=True)
+        assert torch.equal(xi, ref)
