@@ -653,7 +653,7 @@ def run_gather_scatter(P, torch, dev, time_graph, hbm_peak):
 
 def run_conv_sweep(P, torch, dev, time_graph):
     import numpy as np
-    from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_into
+    from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_masked_into
     from paper_1801_02108_b200.ops import dense_conv_nhwc
     Hc, Wc, Cc = 800, 700, 128
     nfr = 8  # 8 x 143 MB frames: inputs larger than L2
@@ -690,9 +690,9 @@ def run_conv_sweep(P, torch, dev, time_graph):
             spec = P.compute_block_spec((1, Hc, Wc, Cc), p, (blk, blk))
             algo = sparse_conv_algo(torch.bfloat16, fb, p, spec)
 
-            def sp(k, mk=mk, spec=spec):
+            def sp(k, mk=mk, spec=spec):  # sparse_conv2d's path: mask -> blocks -> conv
                 for i in range(k):
-                    sparse_conv_into(xs[i % nfr], out, fb, p, spec, P.reduce_mask(mk, spec))
+                    sparse_conv_masked_into(xs[i % nfr], out, mk.data, fb, p, spec)
             t = timed(sp)
             nb = P.reduce_mask(mk, spec).count
             flops = nb * 2 * spec.out_block_size[0] * spec.out_block_size[1] * 9 * Cc * Cc

@@ -151,6 +151,19 @@ int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int kh, int kw,
                     const sbn_geometry* g, const void* w, const void* bias, const void* w_packed,
                     const int32_t* idx, const int32_t* count, int cap, void* dst, void* ws,
                     size_t ws_bytes, int algo, sbn_stream_t stream);
+/* sparse_conv2d straight from the mask (reference `layers.py:27-47`, MAX pool with the
+ * default threshold): on the tcgen05 path ONE kernel (the mask reduction runs in front of
+ * the conv, producing an unordered block list — the output does not depend on the order);
+ * otherwise reduce_mask + sparse_conv.  sync_ws: sbn_sparse_conv_masked_sync_bytes, zeroed
+ * ONCE by the caller and kept between calls (launch epoch, counters, reduce_mask words at
+ * fixed offsets: calls of any geometry may share it); ws: ..._workspace bytes of scratch. */
+size_t sbn_sparse_conv_masked_sync_bytes(const sbn_geometry* g);
+size_t sbn_sparse_conv_masked_workspace(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
+                                        const sbn_geometry* g);
+int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dtype, int cin, int cout, int kh, int kw,
+                           int sh, int sw, const sbn_geometry* g, const void* w, const void* bias,
+                           const void* w_packed, void* dst, void* sync_ws, size_t sync_bytes, void* ws,
+                           size_t ws_bytes, int algo, sbn_stream_t stream);
 size_t sbn_sparse_conv_packed_bytes(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                                     const sbn_geometry* g);
 int sbn_sparse_conv_pack(const void* w, int dtype, int cin, int cout, int kh, int kw, int sh,

@@ -62,6 +62,10 @@ _PROTOS = {
     "sbn_gather_grad": (_I, [_P, _I, _I, _G, _P, _P, _I, _P, _P, C.c_size_t, _P]),
     "sbn_sparse_conv": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _G, _P, _P, _P, _P, _P, _I, _P, _P,
                              C.c_size_t, _I, _P]),
+    "sbn_sparse_conv_masked_sync_bytes": (C.c_size_t, [_G]),
+    "sbn_sparse_conv_masked_workspace": (C.c_size_t, [_I, _I, _I, _I, _I, _I, _I, _G]),
+    "sbn_sparse_conv_masked": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _G, _P, _P, _P, _P, _P, C.c_size_t,
+                                    _P, C.c_size_t, _I, _P]),
     "sbn_sparse_conv_packed_bytes": (C.c_size_t, [_I, _I, _I, _I, _I, _I, _I, _G]),
     "sbn_sparse_conv_pack": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _G, _P, _P]),
     "sbn_sparse_conv_algo": (_I, [_I, _I, _I, _I, _I, _I, _I, _G]),

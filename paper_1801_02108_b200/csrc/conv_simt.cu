@@ -100,6 +100,9 @@ int launch_conv_simt(const void* x, int cin, int cout, int kh, int kw, int sh, i
 
 }  // namespace
 
+int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout, Geo g, const void* wpk,
+                          const void* bias, int32_t* idx_out, int32_t* count_out, unsigned int* slotw, int cap,
+                          void* dst, cudaStream_t s);
 int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, const void* bias,
                    const int32_t* idx, const int32_t* count, int cap, void* dst, cudaStream_t s);
 size_t sparse_conv_tc_packed_bytes(int cin, int cout);
@@ -200,4 +203,63 @@ extern "C" int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int 
       set_error("unsupported dtype %d", dtype);
       return SBN_ERR_UNSUPPORTED;
   }
+}
+
+// ---- sparse_conv2d from the mask (reference `layers.py:27-47`, MAX pool with the default
+// threshold): on the tcgen05 double-buffered path the mask reduction runs inside the conv
+// kernel (one launch); otherwise sbn_reduce_mask + sbn_sparse_conv.
+//   sync_ws (zeroed ONCE by the caller, kept between calls, fixed layout so calls of any
+//   geometry may share it): [slot words: launch epoch + counters, 256 B | reduce_mask ws]
+//   ws (scratch): [index list cap*12 | count 256 B | packed weights when none are given]
+static size_t al256c(size_t v) { return (v + 255) / 256 * 256; }
+
+extern "C" size_t sbn_sparse_conv_masked_sync_bytes(const sbn_geometry* gp) {
+  return gp ? 256 + al256c(sbn_reduce_mask_workspace(gp)) : 0;
+}
+
+extern "C" size_t sbn_sparse_conv_masked_workspace(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
+                                                   const sbn_geometry* gp) {
+  if (!gp) return 0;
+  const size_t cap = (size_t)gp->n * gp->gy * gp->gx;
+  return al256c(cap * 12) + 256 + al256c(sbn_sparse_conv_packed_bytes(dtype, cin, cout, kh, kw, sh, sw, gp));
+}
+
+extern "C" int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dtype, int cin, int cout, int kh,
+                                      int kw, int sh, int sw, const sbn_geometry* gp, const void* w,
+                                      const void* bias, const void* w_packed, void* dst, void* sync_ws,
+                                      size_t sync_bytes, void* ws, size_t ws_bytes, int algo, sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  SBN_CHECK_ARG(x && mask && w && dst, SBN_ERR_INVALID, "null pointer argument");
+  SBN_CHECK_ARG(sync_ws && sync_bytes >= sbn_sparse_conv_masked_sync_bytes(gp), SBN_ERR_WORKSPACE,
+                "sparse_conv2d (masked) needs a %zu-byte zeroed sync workspace", sbn_sparse_conv_masked_sync_bytes(gp));
+  const size_t need = sbn_sparse_conv_masked_workspace(dtype, cin, cout, kh, kw, sh, sw, gp);
+  SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE, "sparse_conv2d (masked) needs a %zu-byte workspace", need);
+  const int cap = gp->n * gp->gy * gp->gx;
+  if (cap <= 0) return SBN_OK;
+  unsigned int* slotw = (unsigned int*)sync_ws;
+  uint8_t* rmws = (uint8_t*)sync_ws + 256;
+  const size_t rmb = sync_bytes - 256;
+  uint8_t* w8 = (uint8_t*)ws;
+  int32_t* idx = (int32_t*)w8;
+  int32_t* count = (int32_t*)(w8 + al256c((size_t)cap * 12));
+  uint8_t* pk = w8 + al256c((size_t)cap * 12) + 256;
+  const size_t pkb = ws_bytes - al256c((size_t)cap * 12) - 256;
+  cudaStream_t s = (cudaStream_t)stream;
+  Geo g = to_geo(gp);
+  const int kind = conv_tc_kind(dtype, cin, cout, kh, kw, sh, sw, g);
+  if (kind == 1 && algo != SBN_ALGO_SIMT) {
+    const void* wpk = w_packed;
+    if (!wpk) {
+      st = sparse_conv_tc_pack(w, cin, cout, pk, s);
+      if (st) return st;
+      wpk = pk;
+    }
+    st = sparse_conv_tc_masked(x, mask, cin, cout, g, wpk, bias, idx, count, slotw, cap, dst, s);
+    if (st != SBN_ERR_UNSUPPORTED) return st;
+  }
+  st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws, rmb, stream);
+  if (st) return st;
+  return sbn_sparse_conv(x, dtype, cin, cout, kh, kw, sh, sw, gp, w, bias, w_packed, idx, count, cap, dst,
+                         w_packed ? nullptr : pk, w_packed ? 0 : pkb, algo, stream);
 }

@@ -59,7 +59,99 @@ struct ConvArgs {
   const int32_t* count;
   int cap;
   unsigned long long* trace;  // diagnostics: per-CTA MMA-issuer wait totals (sbn_debug_set_trace)
+  // mask-fused front end (double-buffered kernel only): when `mask` is set the kernel
+  // itself reduces the mask (MAX pool over each input window) into idx (written, unordered)
+  // and *count_out, see conv_mask_compact
+  const uint8_t* mask;
+  int32_t* count_out;
+  unsigned int* slotw;  // [0] epoch, [4 + 4 * (tag & 1) + {0 slot counter, 1 done}]
 };
+
+// Mask reduction fused in front of the conv (reference `tiling.py:138-160`, MAX pool): CTA
+// c tests candidates c, c + G, ... (any mask pixel in the clipped input window), claims
+// list slots for its active ones with one atomic per round and writes their (n, by, bx);
+// then every CTA waits until all G producers are done and reads the block count.  Block
+// order does not matter (disjoint output windows).  The counters live in a 2-slot ring
+// indexed by the launch epoch; the last producer zeroes the other slot and bumps the
+// epoch, so nothing is reset on the critical path (same protocol as the fused unit).
+template <int NTHREADS>
+__device__ int conv_mask_compact(const ConvArgs& a) {
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  __shared__ int s_flag[32], s_fr[32], s_y0[32], s_x0[32];
+  __shared__ int s_base, s_B;
+  __shared__ unsigned s_tag;
+  int32_t* idx_out = const_cast<int32_t*>(a.idx);
+  unsigned ep = 0;
+  if (tid == 0) ep = tc::ld_relaxed_gpu(a.slotw);
+  const int T = g.n * g.gy * g.gx, G = gridDim.x, area = g.bh * g.bw;
+  for (int r0 = blockIdx.x; r0 < T; r0 += 32 * G) {
+    const int nj = min(32, (T - r0 + G - 1) / G);
+    if (tid < 32) {
+      s_flag[tid] = 0;
+      const int cand = r0 + tid * G;
+      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+      const int cy = rr / g.gx, cx = rr - cy * g.gx;
+      s_fr[tid] = fr;
+      s_y0[tid] = g.oy + cy * g.sy;
+      s_x0[tid] = g.ox + cx * g.sx;
+    }
+    if (tid == 0) s_tag = ep + 1u;
+    __syncthreads();
+    constexpr int U = 4;  // loads in flight per thread before any is tested
+    for (int e0 = tid; e0 < nj * area; e0 += U * NTHREADS) {
+      uint8_t v[U];
+      int jj[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * NTHREADS;
+        const int j = min(e / area, 31), p = e - j * area;
+        const int y = s_y0[j] + p / g.bw, xx = s_x0[j] + p % g.bw;
+        jj[u] = j;
+        v[u] = (e < nj * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+                   ? __ldg(a.mask + ((size_t)s_fr[j] * g.h + y) * g.w + xx) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (v[u]) s_flag[jj[u]] = 1;
+    }
+    __syncthreads();
+    const unsigned tag = s_tag;
+    if (warp == 0) {
+      const bool on = lane < nj && s_flag[lane];
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (lane == 0) s_base = bal ? (int)atomicAdd(a.slotw + 4 + 4 * (tag & 1u), (unsigned)__popc(bal)) : 0;
+      __syncwarp();
+      if (on) {
+        const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
+        const int cand = r0 + lane * G;
+        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+        idx_out[3 * pos] = fr;
+        idx_out[3 * pos + 1] = rr / g.gx;
+        idx_out[3 * pos + 2] = rr % g.gx;
+      }
+    }
+    __syncthreads();
+  }
+  if (T <= (int)blockIdx.x && tid == 0) s_tag = ep + 1u;
+  __syncthreads();
+  const unsigned tag = s_tag;
+  if (tid == 0) {
+    unsigned* ring = a.slotw + 4 + 4 * (tag & 1u);
+    if (tc::atom_add_release_gpu(ring + 1, 1u) == (unsigned)G - 1u) {  // last producer
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (a.count_out) *a.count_out = (int)tc::ld_relaxed_gpu(ring);
+      unsigned* other = a.slotw + 4 + 4 * ((tag + 1u) & 1u);
+      other[0] = 0u;
+      other[1] = 0u;
+      a.slotw[0] = tag;  // every CTA has read the epoch (it did before its done increment)
+    }
+    while (tc::ld_acquire_gpu(ring + 1) != (unsigned)G) __nanosleep(32);
+    s_B = (int)tc::ld_relaxed_gpu(ring);
+  }
+  __syncthreads();
+  return s_B;
+}
 
 template <int CIN, int COUT, int BS>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs a) {
@@ -296,7 +388,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   tc::fence_after();
   const uint32_t tmem = tslot;
   tc::pdl_wait();
-  const int B = ld_count(a.count, a.cap);
+  const int B = a.mask ? conv_mask_compact<kDbThreads>(a) : ld_count(a.count, a.cap);
   const int NJ = (B + D::BPT - 1) / D::BPT;  // jobs: BPT consecutive blocks of the list
 
   if (warp == 8) {
@@ -378,10 +470,10 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
           r %= BS * BS;
         }
         int n = 0, by = 0, bx = 0;
-        if (blk < B) {
-          n = __ldg(a.idx + 3 * blk);
-          by = __ldg(a.idx + 3 * blk + 1);
-          bx = __ldg(a.idx + 3 * blk + 2);
+        if (blk < B) {  // L2-coherent: the list may have been written by this launch
+          n = __ldcg(a.idx + 3 * blk);
+          by = __ldcg(a.idx + 3 * blk + 1);
+          bx = __ldcg(a.idx + 3 * blk + 2);
         }
         const int oy = r / BS, ox = r % BS;
         const int Y = by * g.obh + oy, X = bx * g.obw + ox;
@@ -413,25 +505,33 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       constexpr int TOT = D::BPT * PER;
       constexpr int ITEMS = (TOT + kWorkers - 1) / kWorkers;
       constexpr int CH = ITEMS > 16 ? 16 : ITEMS;
+      // the job's block origins, loaded once (L2-coherent: the list may come from this launch)
+      int jn[D::BPT], jy[D::BPT], jx[D::BPT];
+#pragma unroll
+      for (int jb = 0; jb < D::BPT; ++jb) {
+        const int blk = job * D::BPT + jb;
+        jn[jb] = 0, jy[jb] = -(1 << 20), jx[jb] = 0;  // missing block: every pixel out of image
+        if (blk < B) {
+          jn[jb] = __ldcg(a.idx + 3 * blk);
+          jy[jb] = g.oy + __ldcg(a.idx + 3 * blk + 1) * g.sy;
+          jx[jb] = g.ox + __ldcg(a.idx + 3 * blk + 2) * g.sx;
+        }
+      }
 #pragma unroll 1
       for (int base = 0; base < ITEMS; base += CH) {
         uint4 raw[CH];
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
           const int i = tid + (base + j) * kWorkers;
-          const int jb = i / PER, ii = i - jb * PER;
+          const int jb = D::BPT > 1 ? min(i / PER, D::BPT - 1) : 0, ii = i - jb * PER;
           const int blk = job * D::BPT + jb;
           const int p = ii / (CIN / 8), kc = ii % (CIN / 8);
-          int n = 0, ys = 0, xs = 0;
-          if (i < TOT && blk < B) {
-            n = __ldg(a.idx + 3 * blk);
-            ys = g.oy + __ldg(a.idx + 3 * blk + 1) * g.sy;
-            xs = g.ox + __ldg(a.idx + 3 * blk + 2) * g.sx;
-          }
+          const int n = jn[jb], ys = jy[jb], xs = jx[jb];
           const int y = ys + p / BS, xx = xs + p % BS;
-          raw[j] = make_uint4(0, 0, 0, 0);
-          if (i < TOT && blk < B && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-            raw[j] = __ldg(reinterpret_cast<const uint4*>(a.x) + (((size_t)n * g.h + y) * g.w + xx) * (CIN / 8) + kc);
+          const bool ok = i < TOT && blk < B && (unsigned)y < (unsigned)g.h && (unsigned)xx < (unsigned)g.w;
+          raw[j] = tc::ld_v4_pred(reinterpret_cast<const uint4*>(a.x) +
+                                      (((size_t)n * g.h + (ok ? y : 0)) * g.w + (ok ? xx : 0)) * (CIN / 8) + kc,
+                                  ok);
         }
 #pragma unroll
         for (int j = 0; j < CH; ++j) {
@@ -759,9 +859,36 @@ int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_
   return SBN_ERR_UNSUPPORTED;
 }
 
+// mask-fused launch: only the double-buffered kernel; returns SBN_ERR_UNSUPPORTED when that
+// variant does not apply (the caller then reduces the mask separately)
+int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout, Geo g, const void* wpk,
+                          const void* bias, int32_t* idx_out, int32_t* count_out, unsigned int* slotw, int cap,
+                          void* dst, cudaStream_t s) {
+  if (debug_flags() & (kDebugConvSingleBuffer | kDebugConvPair)) return SBN_ERR_UNSUPPORTED;
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.x = (const __nv_bfloat16*)x;
+  a.out = (__nv_bfloat16*)dst;
+  a.g = g;
+  a.wpk = (const uint8_t*)wpk;
+  a.bias = (const __nv_bfloat16*)bias;
+  a.idx = idx_out;
+  a.count = count_out;
+  a.cap = cap;
+  a.trace = trace_buffer();
+  a.mask = mask;
+  a.count_out = count_out;
+  a.slotw = slotw;
+#define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_ && DbCfg<CI, CO, BS_>::SMEM <= max_smem_optin()) return launch_conv_db<CI, CO, BS_>(a, cap, s);
+  SBN_CONV_TC_CONFIGS(X)
+#undef X
+  return SBN_ERR_UNSUPPORTED;
+}
+
 int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, const void* bias,
                    const int32_t* idx, const int32_t* count, int cap, void* dst, cudaStream_t s) {
   ConvArgs a;
+  memset(&a, 0, sizeof(a));
   a.x = (const __nv_bfloat16*)x;
   a.out = (__nv_bfloat16*)dst;
   a.g = g;

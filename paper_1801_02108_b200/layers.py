@@ -87,7 +87,6 @@ def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
     if f.kernel != tuple(p.kernel) or f.c_in != x.dims[3] or f.c_out != p.filter_count:
         raise ShapeMismatchError("filter bank does not match the conv params / input channels")
     spec = compute_block_spec(x.dims, p, block_size)
-    idx = reduce_mask(mask, spec, pool, threshold)
     xt = cuda(x.nhwc())
     n = x.dims[0]
     if dst is None:
@@ -97,8 +96,54 @@ def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
         if dst.dims != (n, spec.out_size[0], spec.out_size[1], f.c_out):
             raise ShapeMismatchError(f"destination dims {dst.dims} != conv output")
         out = cuda(dst.nhwc()).clone()
-    sparse_conv_into(xt, out, f, p, spec, idx, algo)
+    if pool == PoolMode.MAX and threshold is None:
+        # default pooling: the mask reduction runs inside the conv kernel (one launch)
+        sparse_conv_masked_into(xt, out, cuda(mask.data), f, p, spec, algo)
+    else:
+        sparse_conv_into(xt, out, f, p, spec, reduce_mask(mask, spec, pool, threshold), algo)
     return Tensor4D.from_nhwc(out, x.layout)
+
+
+def _conv_packed(lib, f: FilterBank, w: torch.Tensor, dc: int, p: ConvParams, g, device) -> torch.Tensor | None:
+    """Tensor-core weight image for (filter bank, kernel variant), packed once and cached."""
+    kh, kw = p.kernel
+    sh, sw = p.stride
+    nb = lib.sbn_sparse_conv_packed_bytes(dc, f.c_in, f.c_out, kh, kw, sh, sw, C.byref(g))
+    if not nb:
+        return None
+    key = ("tc_pack", w.dtype, str(device), kh, kw, sh, sw, g.bh, g.bw)  # layout depends on the kernel variant
+    packed = f._cache.get(key)
+    if packed is None:
+        packed = torch.empty(nb, dtype=torch.uint8, device=device)
+        _lib.check(lib.sbn_sparse_conv_pack(w.data_ptr(), dc, f.c_in, f.c_out, kh, kw, sh, sw, C.byref(g),
+                                            packed.data_ptr(), _lib.stream_handle(device)), "sparse_conv_pack")
+        f._cache[key] = packed
+    return packed
+
+
+def sparse_conv_masked_into(xt: torch.Tensor, out: torch.Tensor, mask: torch.Tensor, f: FilterBank,
+                            p: ConvParams, spec: BlockSpec, algo="auto") -> None:
+    """sparse_conv2d from the (device) mask with the default MAX pooling, stream-ordered, no
+    sync: on the tcgen05 path one kernel reduces the mask and convolves the active blocks
+    (sbn_sparse_conv_masked); otherwise reduce_mask + the fused conv."""
+    lib = _lib.load()
+    w, b = f.device_tensors(xt.dtype, xt.device)
+    g = spec.c_geometry(xt.shape[0])
+    kh, kw = p.kernel
+    sh, sw = p.stride
+    a = _algo(algo)
+    dc = dtype_code(xt.dtype)
+    packed = _conv_packed(lib, f, w, dc, p, g, xt.device) if a != _lib.SBN_ALGO_SIMT else None
+    gb = C.byref(g)
+    sync = _SCRATCH.get(int(lib.sbn_sparse_conv_masked_sync_bytes(gb)), xt.device, "conv_sync")
+    ws = _SCRATCH.get(int(lib.sbn_sparse_conv_masked_workspace(dc, f.c_in, f.c_out, kh, kw, sh, sw, gb)),
+                      xt.device, "conv_scratch")
+    st = lib.sbn_sparse_conv_masked(xt.data_ptr(), mask.data_ptr(), dc, f.c_in, f.c_out, kh, kw, sh, sw, gb,
+                                    w.data_ptr(), None if b is None else b.data_ptr(),
+                                    None if packed is None else packed.data_ptr(), out.data_ptr(),
+                                    sync.data_ptr(), sync.numel(), ws.data_ptr(), ws.numel(), a,
+                                    _lib.stream_handle(xt.device))
+    _lib.check(st, "sparse_conv2d")
 
 
 def sparse_conv_into(xt: torch.Tensor, out: torch.Tensor, f: FilterBank, p: ConvParams,

@@ -633,3 +633,30 @@ def test_fused_unit_empty_and_alternating_masks(cuda_device):
         xi = x.clone()
         P.sparse_residual_unit(P.Tensor4D(xi), blobs, u, (16, 16), inplace=True)
         assert torch.equal(xi, ref)
+
+
+@pytest.mark.parametrize("cin,block,density,nframes", [(128, 16, 0.1, 1), (64, 8, 0.4, 2), (32, 16, 1.0, 1),
+                                                       (128, 16, 0.0, 1), (64, 24, 0.3, 1)])
+def test_sparse_conv_mask_fused_bit_identical(cuda_device, cin, block, density, nframes):
+    """sparse_conv2d from the mask (one kernel on the tcgen05 double-buffered path: mask
+    reduction fused, unordered block list) equals reduce_mask + the conv bit for bit, call
+    after call and across geometries sharing the workspaces; empty masks leave zeros."""
+    from paper_1801_02108_b200.layers import sparse_conv_into, sparse_conv_masked_into
+    rng = np.random.default_rng(cin + block)
+    h, w = 131, 117
+    x = torch.from_numpy(rng.standard_normal((nframes, h, w, cin)).astype(np.float32)).bfloat16().cuda()
+    fb = P.FilterBank(torch.from_numpy((rng.standard_normal((3, 3, cin, cin)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16(),
+                      torch.from_numpy(rng.standard_normal(cin).astype(np.float32)).bfloat16())
+    p = _conv((3, 3), (1, 1), True, cin)
+    spec = P.compute_block_spec((nframes, h, w, cin), p, (block, block))
+    mk = (P.synth_mask_blobs((nframes, h, w), 1.0 - density, 5) if density > 0 else
+          P.BinaryMask(torch.zeros(nframes, h, w, dtype=torch.uint8))).cuda()
+    ref = torch.zeros(nframes, *spec.out_size, cin, dtype=torch.bfloat16, device="cuda")
+    sparse_conv_into(x, ref, fb, p, spec, P.reduce_mask(mk, spec))
+    for _ in range(3):
+        out = torch.zeros_like(ref)
+        sparse_conv_masked_into(x, out, mk.data, fb, p, spec)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    y = P.sparse_conv2d(P.Tensor4D(x), mk, fb, p, (block, block)).data
+    assert torch.equal(y, ref)
