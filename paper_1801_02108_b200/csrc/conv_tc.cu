@@ -74,41 +74,45 @@ struct ConvArgs {
 // order does not matter (disjoint output windows).  The counters live in a 2-slot ring
 // indexed by the launch epoch; the last producer zeroes the other slot and bumps the
 // epoch, so nothing is reset on the critical path (same protocol as the fused unit).
-template <int NTHREADS>
+template <int NTHREADS, int BS>
 __device__ int conv_mask_compact(const ConvArgs& a) {
+  constexpr int kMaxCand = 256;  // candidates per CTA handled in one pass (else more passes)
+  constexpr int area = BS * BS;  // the input window (bh == bw == BS on this path)
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ int s_flag[32], s_fr[32], s_y0[32], s_x0[32];
+  __shared__ uint8_t s_flag[kMaxCand];
+  __shared__ int s_fr[kMaxCand], s_y0[kMaxCand], s_x0[kMaxCand];
   __shared__ int s_base, s_B;
   __shared__ unsigned s_tag;
   int32_t* idx_out = const_cast<int32_t*>(a.idx);
   unsigned ep = 0;
   if (tid == 0) ep = tc::ld_relaxed_gpu(a.slotw);
-  const int T = g.n * g.gy * g.gx, G = gridDim.x, area = g.bh * g.bw;
-  for (int r0 = blockIdx.x; r0 < T; r0 += 32 * G) {
-    const int nj = min(32, (T - r0 + G - 1) / G);
-    if (tid < 32) {
-      s_flag[tid] = 0;
-      const int cand = r0 + tid * G;
-      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-      const int cy = rr / g.gx, cx = rr - cy * g.gx;
-      s_fr[tid] = fr;
-      s_y0[tid] = g.oy + cy * g.sy;
-      s_x0[tid] = g.ox + cx * g.sx;
+  const int T = g.n * g.gy * g.gx, G = gridDim.x, gyx = g.gy * g.gx;
+  // this CTA's candidates: blockIdx.x + j * G, j < nc
+  const int nc_all = T > (int)blockIdx.x ? (T - (int)blockIdx.x + G - 1) / G : 0;
+  for (int j0 = 0; j0 < nc_all; j0 += kMaxCand) {
+    const int nc = min(kMaxCand, nc_all - j0);
+    for (int j = tid; j < nc; j += NTHREADS) {  // candidate origins once (no divides per pixel)
+      const int cand = (int)blockIdx.x + (j0 + j) * G;
+      const int fr = cand / gyx, rr = cand - fr * gyx;
+      s_flag[j] = 0;
+      s_fr[j] = fr;
+      s_y0[j] = g.oy + (rr / g.gx) * g.sy;
+      s_x0[j] = g.ox + (rr % g.gx) * g.sx;
     }
     if (tid == 0) s_tag = ep + 1u;
     __syncthreads();
-    constexpr int U = 4;  // loads in flight per thread before any is tested
-    for (int e0 = tid; e0 < nj * area; e0 += U * NTHREADS) {
+    constexpr int U = 16;  // loads in flight per thread before any is tested
+    for (int e0 = tid; e0 < nc * area; e0 += U * NTHREADS) {
       uint8_t v[U];
       int jj[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int e = e0 + u * NTHREADS;
-        const int j = min(e / area, 31), p = e - j * area;
-        const int y = s_y0[j] + p / g.bw, xx = s_x0[j] + p % g.bw;
+        const int j = e < nc * area ? e / area : 0, p = e - j * area;
+        const int y = s_y0[j] + p / BS, xx = s_x0[j] + p % BS;
         jj[u] = j;
-        v[u] = (e < nj * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+        v[u] = (e < nc * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
                    ? __ldg(a.mask + ((size_t)s_fr[j] * g.h + y) * g.w + xx) : (uint8_t)0;
       }
 #pragma unroll
@@ -117,23 +121,29 @@ __device__ int conv_mask_compact(const ConvArgs& a) {
     }
     __syncthreads();
     const unsigned tag = s_tag;
-    if (warp == 0) {
-      const bool on = lane < nj && s_flag[lane];
-      const unsigned bal = __ballot_sync(0xffffffffu, on);
-      if (lane == 0) s_base = bal ? (int)atomicAdd(a.slotw + 4 + 4 * (tag & 1u), (unsigned)__popc(bal)) : 0;
+    if (warp == 0) {  // one slot claim for the whole pass, entries in candidate order
+      int total = 0;
+      for (int c0 = 0; c0 < nc; c0 += 32) total += __popc(__ballot_sync(0xffffffffu, c0 + lane < nc && s_flag[c0 + lane]));
+      if (lane == 0) s_base = total ? (int)atomicAdd(a.slotw + 4 + 4 * (tag & 1u), (unsigned)total) : 0;
       __syncwarp();
-      if (on) {
-        const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
-        const int cand = r0 + lane * G;
-        const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-        idx_out[3 * pos] = fr;
-        idx_out[3 * pos + 1] = rr / g.gx;
-        idx_out[3 * pos + 2] = rr % g.gx;
+      int pos = s_base;
+      for (int c0 = 0; c0 < nc; c0 += 32) {
+        const bool on = c0 + lane < nc && s_flag[c0 + lane];
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (on) {
+          const int q = pos + __popc(bal & ((1u << lane) - 1u));
+          const int cand = (int)blockIdx.x + (j0 + c0 + lane) * G;
+          const int fr = cand / gyx, rr = cand - fr * gyx;
+          idx_out[3 * q] = fr;
+          idx_out[3 * q + 1] = rr / g.gx;
+          idx_out[3 * q + 2] = rr % g.gx;
+        }
+        pos += __popc(bal);
       }
     }
     __syncthreads();
   }
-  if (T <= (int)blockIdx.x && tid == 0) s_tag = ep + 1u;
+  if (nc_all == 0 && tid == 0) s_tag = ep + 1u;
   __syncthreads();
   const unsigned tag = s_tag;
   if (tid == 0) {
@@ -388,7 +398,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   tc::fence_after();
   const uint32_t tmem = tslot;
   tc::pdl_wait();
-  const int B = a.mask ? conv_mask_compact<kDbThreads>(a) : ld_count(a.count, a.cap);
+  const int B = a.mask ? conv_mask_compact<kDbThreads, BS>(a) : ld_count(a.count, a.cap);
   const int NJ = (B + D::BPT - 1) / D::BPT;  // jobs: BPT consecutive blocks of the list
 
   if (warp == 8) {
