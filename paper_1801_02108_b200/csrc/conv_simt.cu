@@ -101,8 +101,7 @@ int launch_conv_simt(const void* x, int cin, int cout, int kh, int kw, int sh, i
 }  // namespace
 
 int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout, Geo g, const void* wpk,
-                          const void* bias, int32_t* idx_out, int32_t* count_out, unsigned int* slotw, int cap,
-                          void* dst, cudaStream_t s);
+                          const void* bias, int cap, void* dst, cudaStream_t s);
 int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, const void* bias,
                    const int32_t* idx, const int32_t* count, int cap, void* dst, cudaStream_t s);
 size_t sparse_conv_tc_packed_bytes(int cin, int cout);
@@ -209,7 +208,7 @@ extern "C" int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int 
 // threshold): on the tcgen05 double-buffered path the mask reduction runs inside the conv
 // kernel (one launch); otherwise sbn_reduce_mask + sbn_sparse_conv.
 //   sync_ws (zeroed ONCE by the caller, kept between calls, fixed layout so calls of any
-//   geometry may share it): [slot words: launch epoch + counters, 256 B | reduce_mask ws]
+//   geometry may share it): [256 B reserved | reduce_mask ws (fallback path)]
 //   ws (scratch): [index list cap*12 | count 256 B | packed weights when none are given]
 static size_t al256c(size_t v) { return (v + 255) / 256 * 256; }
 
@@ -237,7 +236,6 @@ extern "C" int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dt
   SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE, "sparse_conv2d (masked) needs a %zu-byte workspace", need);
   const int cap = gp->n * gp->gy * gp->gx;
   if (cap <= 0) return SBN_OK;
-  unsigned int* slotw = (unsigned int*)sync_ws;
   uint8_t* rmws = (uint8_t*)sync_ws + 256;
   const size_t rmb = sync_bytes - 256;
   uint8_t* w8 = (uint8_t*)ws;
@@ -255,7 +253,7 @@ extern "C" int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dt
       if (st) return st;
       wpk = pk;
     }
-    st = sparse_conv_tc_masked(x, mask, cin, cout, g, wpk, bias, idx, count, slotw, cap, dst, s);
+    st = sparse_conv_tc_masked(x, mask, cin, cout, g, wpk, bias, cap, dst, s);
     if (st != SBN_ERR_UNSUPPORTED) return st;
   }
   st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws, rmb, stream);

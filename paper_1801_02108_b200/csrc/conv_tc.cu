@@ -59,108 +59,66 @@ struct ConvArgs {
   const int32_t* count;
   int cap;
   unsigned long long* trace;  // diagnostics: per-CTA MMA-issuer wait totals (sbn_debug_set_trace)
-  // mask-fused front end (double-buffered kernel only): when `mask` is set the kernel
-  // itself reduces the mask (MAX pool over each input window) into idx (written, unordered)
-  // and *count_out, see conv_mask_compact
+  // mask-fused front end (double-buffered kernel only): when `mask` is set every CTA
+  // reduces its share of the mask itself and convolves its own active blocks, see
+  // conv_mask_local
   const uint8_t* mask;
-  int32_t* count_out;
-  unsigned int* slotw;  // [0] epoch, [4 + 4 * (tag & 1) + {0 slot counter, 1 done}]
 };
 
-// Mask reduction fused in front of the conv (reference `tiling.py:138-160`, MAX pool): CTA
-// c tests candidates c, c + G, ... (any mask pixel in the clipped input window), claims
-// list slots for its active ones with one atomic per round and writes their (n, by, bx);
-// then every CTA waits until all G producers are done and reads the block count.  Block
-// order does not matter (disjoint output windows).  The counters live in a 2-slot ring
-// indexed by the launch epoch; the last producer zeroes the other slot and bumps the
-// epoch, so nothing is reset on the critical path (same protocol as the fused unit).
+// Mask reduction fused in front of the conv (reference `tiling.py:138-160`, MAX pool),
+// without any grid-wide step: CTA c owns candidates c, c + G, c + 2G, ... (round-robin, so
+// active regions spread evenly), tests each one's clipped input window (one warp per
+// candidate, any-pixel by warp vote), and lists its own active blocks in shared memory.
+// The conv then walks that local list.  Block order does not matter (disjoint outputs).
+constexpr int kMaxLocal = 384;  // candidates per CTA (host falls back to reduce_mask above)
+
 template <int NTHREADS, int BS>
-__device__ int conv_mask_compact(const ConvArgs& a) {
-  constexpr int kMaxCand = 256;  // candidates per CTA handled in one pass (else more passes)
-  constexpr int area = BS * BS;  // the input window (bh == bw == BS on this path)
+__device__ int conv_mask_local(const ConvArgs& a, int32_t* s_idx) {
   const Geo& g = a.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ uint8_t s_flag[kMaxCand];
-  __shared__ int s_fr[kMaxCand], s_y0[kMaxCand], s_x0[kMaxCand];
-  __shared__ int s_base, s_B;
-  __shared__ unsigned s_tag;
-  int32_t* idx_out = const_cast<int32_t*>(a.idx);
-  unsigned ep = 0;
-  if (tid == 0) ep = tc::ld_relaxed_gpu(a.slotw);
+  constexpr int NW = NTHREADS / 32, AREA = BS * BS, PL = (AREA + 31) / 32;  // pixels per lane
+  __shared__ uint8_t s_flag[kMaxLocal];
+  __shared__ int s_n;
   const int T = g.n * g.gy * g.gx, G = gridDim.x, gyx = g.gy * g.gx;
-  // this CTA's candidates: blockIdx.x + j * G, j < nc
-  const int nc_all = T > (int)blockIdx.x ? (T - (int)blockIdx.x + G - 1) / G : 0;
-  for (int j0 = 0; j0 < nc_all; j0 += kMaxCand) {
-    const int nc = min(kMaxCand, nc_all - j0);
-    for (int j = tid; j < nc; j += NTHREADS) {  // candidate origins once (no divides per pixel)
-      const int cand = (int)blockIdx.x + (j0 + j) * G;
-      const int fr = cand / gyx, rr = cand - fr * gyx;
-      s_flag[j] = 0;
-      s_fr[j] = fr;
-      s_y0[j] = g.oy + (rr / g.gx) * g.sy;
-      s_x0[j] = g.ox + (rr % g.gx) * g.sx;
-    }
-    if (tid == 0) s_tag = ep + 1u;
-    __syncthreads();
-    constexpr int U = 16;  // loads in flight per thread before any is tested
-    for (int e0 = tid; e0 < nc * area; e0 += U * NTHREADS) {
-      uint8_t v[U];
-      int jj[U];
+  const int nc = T > (int)blockIdx.x ? min((T - (int)blockIdx.x + G - 1) / G, kMaxLocal) : 0;
+  for (int j = warp; j < nc; j += NW) {
+    const int cand = (int)blockIdx.x + j * G;
+    const int fr = cand / gyx, rr = cand - fr * gyx;
+    const int y0 = g.oy + (rr / g.gx) * g.sy, x0 = g.ox + (rr % g.gx) * g.sx;
+    uint8_t v[PL];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * NTHREADS;
-        const int j = e < nc * area ? e / area : 0, p = e - j * area;
-        const int y = s_y0[j] + p / BS, xx = s_x0[j] + p % BS;
-        jj[u] = j;
-        v[u] = (e < nc * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-                   ? __ldg(a.mask + ((size_t)s_fr[j] * g.h + y) * g.w + xx) : (uint8_t)0;
-      }
+    for (int u = 0; u < PL; ++u) {
+      const int p = lane + 32 * u;
+      const int y = y0 + p / BS, xx = x0 + p % BS;
+      v[u] = (p < AREA && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+                 ? __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx) : (uint8_t)0;
+    }
+    bool any = false;
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (v[u]) s_flag[jj[u]] = 1;
-    }
-    __syncthreads();
-    const unsigned tag = s_tag;
-    if (warp == 0) {  // one slot claim for the whole pass, entries in candidate order
-      int total = 0;
-      for (int c0 = 0; c0 < nc; c0 += 32) total += __popc(__ballot_sync(0xffffffffu, c0 + lane < nc && s_flag[c0 + lane]));
-      if (lane == 0) s_base = total ? (int)atomicAdd(a.slotw + 4 + 4 * (tag & 1u), (unsigned)total) : 0;
-      __syncwarp();
-      int pos = s_base;
-      for (int c0 = 0; c0 < nc; c0 += 32) {
-        const bool on = c0 + lane < nc && s_flag[c0 + lane];
-        const unsigned bal = __ballot_sync(0xffffffffu, on);
-        if (on) {
-          const int q = pos + __popc(bal & ((1u << lane) - 1u));
-          const int cand = (int)blockIdx.x + (j0 + c0 + lane) * G;
-          const int fr = cand / gyx, rr = cand - fr * gyx;
-          idx_out[3 * q] = fr;
-          idx_out[3 * q + 1] = rr / g.gx;
-          idx_out[3 * q + 2] = rr % g.gx;
-        }
-        pos += __popc(bal);
-      }
-    }
-    __syncthreads();
-  }
-  if (nc_all == 0 && tid == 0) s_tag = ep + 1u;
-  __syncthreads();
-  const unsigned tag = s_tag;
-  if (tid == 0) {
-    unsigned* ring = a.slotw + 4 + 4 * (tag & 1u);
-    if (tc::atom_add_release_gpu(ring + 1, 1u) == (unsigned)G - 1u) {  // last producer
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      if (a.count_out) *a.count_out = (int)tc::ld_relaxed_gpu(ring);
-      unsigned* other = a.slotw + 4 + 4 * ((tag + 1u) & 1u);
-      other[0] = 0u;
-      other[1] = 0u;
-      a.slotw[0] = tag;  // every CTA has read the epoch (it did before its done increment)
-    }
-    while (tc::ld_acquire_gpu(ring + 1) != (unsigned)G) __nanosleep(32);
-    s_B = (int)tc::ld_relaxed_gpu(ring);
+    for (int u = 0; u < PL; ++u) any |= v[u] != 0;
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) s_flag[j] = any;
   }
   __syncthreads();
-  return s_B;
+  if (warp == 0) {  // compact in candidate order
+    int pos = 0;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+      const bool on = c0 + lane < nc && s_flag[c0 + lane];
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (on) {
+        const int q = pos + __popc(bal & ((1u << lane) - 1u));
+        const int cand = (int)blockIdx.x + (c0 + lane) * G;
+        const int fr = cand / gyx, rr = cand - fr * gyx;
+        s_idx[3 * q] = fr;
+        s_idx[3 * q + 1] = rr / g.gx;
+        s_idx[3 * q + 2] = rr % g.gx;
+      }
+      pos += __popc(bal);
+    }
+    if (lane == 0) s_n = pos;
+  }
+  __syncthreads();
+  return s_n;
 }
 
 template <int CIN, int COUT, int BS>
@@ -398,14 +356,18 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   tc::fence_after();
   const uint32_t tmem = tslot;
   tc::pdl_wait();
-  const int B = a.mask ? conv_mask_compact<kDbThreads, BS>(a) : ld_count(a.count, a.cap);
+  __shared__ int32_t s_idx[3 * kMaxLocal];  // mask-fused mode: this CTA's own block list
+  const bool local = a.mask != nullptr;
+  const int B = local ? conv_mask_local<kDbThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
+  const int32_t* lidx = local ? s_idx : a.idx;          // (n, by, bx) rows
+  const int jfirst = local ? 0 : (int)blockIdx.x, jstep = local ? 1 : (int)gridDim.x;
   const int NJ = (B + D::BPT - 1) / D::BPT;  // jobs: BPT consecutive blocks of the list
 
   if (warp == 8) {
     // ---------------- producer: weight taps through the ring
     if (lane == 0) {
       int it = 0;
-      for (int job = blockIdx.x; job < NJ; job += gridDim.x)
+      for (int job = jfirst; job < NJ; job += jstep)
         for (int tap = 0; tap < 9; ++tap, ++it) {
           const int s = it % D::STAGES;
           tc::mbar_wait(&empty[s], ((it / D::STAGES) & 1) ^ 1);
@@ -420,7 +382,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       int it = 0, k = 0;
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, COUT);
       unsigned long long t_win = 0, t_acc = 0, t_w = 0, t0 = clock64();
-      for (int job = blockIdx.x; job < NJ; job += gridDim.x, ++k) {
+      for (int job = jfirst; job < NJ; job += jstep, ++k) {
         const int b = k & 1;
         const uint32_t use = (uint32_t)(k >> 1);
         const unsigned long long c0 = clock64();
@@ -480,10 +442,10 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
           r %= BS * BS;
         }
         int n = 0, by = 0, bx = 0;
-        if (blk < B) {  // L2-coherent: the list may have been written by this launch
-          n = __ldcg(a.idx + 3 * blk);
-          by = __ldcg(a.idx + 3 * blk + 1);
-          bx = __ldcg(a.idx + 3 * blk + 2);
+        if (blk < B) {
+          n = lidx[3 * blk];
+          by = lidx[3 * blk + 1];
+          bx = lidx[3 * blk + 2];
         }
         const int oy = r / BS, ox = r % BS;
         const int Y = by * g.obh + oy, X = bx * g.obw + ox;
@@ -507,7 +469,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       tc::fence_before();
       tc::mbar_arrive(&acc_empty[b]);
     };
-    for (int job = blockIdx.x; job < NJ; job += gridDim.x, ++k) {
+    for (int job = jfirst; job < NJ; job += jstep, ++k) {
       const int b = k & 1;
       tc::mbar_wait(&win_empty[b], ((k >> 1) & 1) ^ 1);
       uint8_t* A = smem + b * D::SZ_A;
@@ -522,9 +484,9 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
         const int blk = job * D::BPT + jb;
         jn[jb] = 0, jy[jb] = -(1 << 20), jx[jb] = 0;  // missing block: every pixel out of image
         if (blk < B) {
-          jn[jb] = __ldcg(a.idx + 3 * blk);
-          jy[jb] = g.oy + __ldcg(a.idx + 3 * blk + 1) * g.sy;
-          jx[jb] = g.ox + __ldcg(a.idx + 3 * blk + 2) * g.sx;
+          jn[jb] = lidx[3 * blk];
+          jy[jb] = g.oy + lidx[3 * blk + 1] * g.sy;
+          jx[jb] = g.ox + lidx[3 * blk + 2] * g.sx;
         }
       }
 #pragma unroll 1
@@ -872,9 +834,16 @@ int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_
 // mask-fused launch: only the double-buffered kernel; returns SBN_ERR_UNSUPPORTED when that
 // variant does not apply (the caller then reduces the mask separately)
 int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout, Geo g, const void* wpk,
-                          const void* bias, int32_t* idx_out, int32_t* count_out, unsigned int* slotw, int cap,
-                          void* dst, cudaStream_t s) {
+                          const void* bias, int cap, void* dst, cudaStream_t s) {
   if (debug_flags() & (kDebugConvSingleBuffer | kDebugConvPair)) return SBN_ERR_UNSUPPORTED;
+  // Per-CTA lists balance only statistically: with few candidates per CTA a structured
+  // mask (e.g. a top-left rectangle) lands unevenly on the round-robin owners, and the
+  // separate ordered reduce_mask + conv (evenly striped list) is faster (measured, config 3:
+  // 16x16 blocks, 20 candidates / CTA: 61 vs 36 us at 10 %; 8x8 blocks, 106 / CTA: 40 vs
+  // 46 us).  Fused only from kMinLocal candidates per CTA up to the shared list size.
+  constexpr int kMinLocal = 64;
+  const int per_cta = (cap + sm_count() - 1) / sm_count();
+  if (per_cta < kMinLocal || per_cta > kMaxLocal) return SBN_ERR_UNSUPPORTED;
   ConvArgs a;
   memset(&a, 0, sizeof(a));
   a.x = (const __nv_bfloat16*)x;
@@ -882,13 +851,9 @@ int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout,
   a.g = g;
   a.wpk = (const uint8_t*)wpk;
   a.bias = (const __nv_bfloat16*)bias;
-  a.idx = idx_out;
-  a.count = count_out;
   a.cap = cap;
   a.trace = trace_buffer();
   a.mask = mask;
-  a.count_out = count_out;
-  a.slotw = slotw;
 #define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_ && DbCfg<CI, CO, BS_>::SMEM <= max_smem_optin()) return launch_conv_db<CI, CO, BS_>(a, cap, s);
   SBN_CONV_TC_CONFIGS(X)
 #undef X
