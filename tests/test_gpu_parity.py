@@ -660,3 +660,42 @@ def test_sparse_conv_mask_fused_bit_identical(cuda_device, cin, block, density, 
         assert torch.equal(out, ref)
     y = P.sparse_conv2d(P.Tensor4D(x), mk, fb, p, (block, block)).data
     assert torch.equal(y, ref)
+
+
+@pytest.mark.parametrize("cin,block", [(128, 16), (64, 8), (32, 16)])
+def test_sparse_conv_tc_mask_monotonicity(cuda_device, cin, block):
+    """Reference test_layers.py:58-70 on the tcgen05 path (bf16): growing the mask never
+    changes the output on the smaller mask's active write regions (per-block compute is
+    independent of which other blocks are active)."""
+    rng = np.random.default_rng(2 + cin)
+    n, h, w = 1, 96, 88
+    x = P.Tensor4D(torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16().cuda())
+    fb = P.FilterBank(torch.from_numpy((rng.standard_normal((3, 3, cin, cin)) / np.sqrt(9 * cin)).astype(np.float32)).bfloat16(),
+                      torch.from_numpy(rng.standard_normal(cin).astype(np.float32)).bfloat16())
+    p = _conv((3, 3), (1, 1), True, cin)
+    small = P.BinaryMask((rng.random((n, h, w)) < 0.004).astype(np.uint8))
+    grown = P.BinaryMask(np.maximum(small.numpy(), (rng.random((n, h, w)) < 0.004).astype(np.uint8)))
+    spec = P.compute_block_spec(x.dims, p, (block, block))
+    geo = O.geometry(h, w, (3, 3), (1, 1), True, (block, block))
+    region = O.active_region(geo, O.reduce_mask(small.numpy(), geo), n)
+    a = _np(P.sparse_conv2d(x, small, fb, p, (block, block)))
+    b = _np(P.sparse_conv2d(x, grown, fb, p, (block, block)))
+    assert region.any() and np.array_equal(a[region], b[region])
+
+
+@pytest.mark.parametrize("c,m", [(64, 32), (128, 64)])
+def test_tc_residual_unit_zero_weights_is_identity(cuda_device, c, m):
+    """Reference test_layers.py:120-133 on the tcgen05 unit (bf16, fused mask, in place and
+    functional): zero convolutions with identity BN leave x bit-identical."""
+    def fb(kh, kw, ci, co):
+        return P.FilterBank(torch.zeros(kh, kw, ci, co, dtype=torch.bfloat16), torch.zeros(co, dtype=torch.bfloat16))
+    u = P.ResidualUnitParams(fb(1, 1, c, m), fb(3, 3, m, m), fb(1, 1, m, c),
+                             P.BnParams.identity(c), P.BnParams.identity(m), P.BnParams.identity(m))
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.standard_normal((1, 64, 80, c)).astype(np.float32)).bfloat16().cuda()
+    mask = P.BinaryMask.full(1, 64, 80)
+    out = P.sparse_residual_unit(P.Tensor4D(x), mask, u, (16, 16)).data
+    assert torch.equal(out, x)
+    xi = x.clone()
+    P.sparse_residual_unit(P.Tensor4D(xi), mask, u, (16, 16), inplace=True)
+    assert torch.equal(xi, x)
