@@ -1,3 +1,5 @@
+"""Repeat the fused / two-launch / CTA-pair unit variants on one input and count bit
+mismatches (used to chase the workspace-aliasing bug fixed by fixed-offset slot words)."""
 import sys; sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 import paper_1801_02108_b200 as P

@@ -1,3 +1,5 @@
+"""Wide three-launch unit on 64 config-2 frames (graph-timed): A/B probe for unit_wide.cu
+changes; argv[1] labels the run."""
 import os, sys
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
