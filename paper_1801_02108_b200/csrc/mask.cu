@@ -384,6 +384,12 @@ extern "C" size_t sbn_reduce_mask_workspace(const sbn_geometry* g) {
   return 16 + 8 * (tiles > 0 ? tiles : 1);
 }
 
+// The cluster kernel (one cluster, up to 16 CTAs) wins only while each CTA has a few block
+// rows; beyond that the one-CTA-per-row look-back kernel is faster (tools/reduce_mask_time.py:
+// 8 x 400x350, 16x16 blocks: 20.6 -> 9.1 us; 800x700, 8x8: 9.5 -> 6.8 us; 800x700, 16x16
+// (4 rows / CTA) stays on the cluster: 5.6 us vs 6.7).
+constexpr int kClusterMaxRowsPerCta = 4;
+
 extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int pool,
                                double threshold, int32_t* idx, int32_t* count, void* ws,
                                size_t ws_bytes, sbn_stream_t stream) {
@@ -409,7 +415,7 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
     const int per = (int)((tiles + cl - 1) / cl);
     cl = (int)((tiles + per - 1) / per);
     const size_t smem = (size_t)per * g.w * 4 + (size_t)per * g.gx;
-    if (smem <= 160 * 1024) {
+    if (smem <= 160 * 1024 && per <= kClusterMaxRowsPerCta) {
       const int vec = ((g.w & 3) == 0) && (((uintptr_t)mask & 3) == 0) && g.bh < 256;
       static bool attr = false;
       if (!attr) {
