@@ -339,7 +339,7 @@ reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, do
 }
 
 __global__ void downsample_kernel(const uint8_t* __restrict__ in, int n, int h, int w, int f,
-                                  int oh, int ow, uint8_t* __restrict__ out) {
+                                  int oh, int ow, uint8_t* __restrict__ out, int vec4) {
   const long total = (long)n * oh * ow;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
        i += (long)gridDim.x * blockDim.x) {
@@ -348,11 +348,19 @@ __global__ void downsample_kernel(const uint8_t* __restrict__ in, int n, int h, 
     const int oy = (int)(r % oh);
     const int fr = (int)(r / oh);
     const int ya = oy * f, yb = min(ya + f, h), xa = ox * f, xb = min(xa + f, w);
-    uint8_t v = 0;
     const uint8_t* p = in + (size_t)fr * h * w;
-    for (int y = ya; y < yb && !v; ++y)
-      for (int x = xa; x < xb; ++x) v = max(v, __ldg(p + (size_t)y * w + x));
-    out[i] = v;
+    // no early exit: every row's loads are independent, so they stay in flight together
+    // (an any-found exit made the f rows f serial round trips)
+    uint32_t m4 = 0;
+    if (vec4) {  // 4-byte words: w, f and the base are multiples of 4 (so are xa and xb)
+      for (int y = ya; y < yb; ++y)
+        for (int x = xa; x < xb; x += 4) m4 = __vmaxu4(m4, __ldg(reinterpret_cast<const uint32_t*>(p + (size_t)y * w + x)));
+      m4 = max(max(m4 & 0xffu, (m4 >> 8) & 0xffu), max((m4 >> 16) & 0xffu, m4 >> 24));
+    } else {
+      for (int y = ya; y < yb; ++y)
+        for (int x = xa; x < xb; ++x) m4 = max(m4, (uint32_t)__ldg(p + (size_t)y * w + x));
+    }
+    out[i] = (uint8_t)m4;
   }
 }
 
@@ -463,8 +471,9 @@ extern "C" int sbn_downsample_mask(const uint8_t* in, int n, int h, int w, int f
   const int threads = 256;
   long blocks = (total + threads - 1) / threads;
   if (blocks > (long)sm_count() * 32) blocks = (long)sm_count() * 32;
+  const int vec4 = (w % 4 == 0) && (factor % 4 == 0) && ((uintptr_t)in % 4 == 0);
   downsample_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(in, n, h, w, factor,
-                                                                           oh, ow, out);
+                                                                           oh, ow, out, vec4);
   return launch_status("downsample_mask");
 }
 
