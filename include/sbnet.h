@@ -130,6 +130,13 @@ int sbn_gather_grad(const void* gblk, int dtype, int c, const sbn_geometry* g, c
 int sbn_copy_block_regions(const void* src, void* dst, int dtype, int c, const sbn_geometry* g,
                            const int32_t* idx, const int32_t* count, int cap, int region,
                            sbn_stream_t stream);
+/* The same window regions (0 input windows, 1 output windows) between a CHANNELS_FIRST
+ * (n, c, h, w) tensor and a CHANNELS_LAST one of the same logical dims: dir 0 copies
+ * NCHW src -> NHWC dst, dir 1 NHWC src -> NCHW dst (bit-exact transposing copies), so
+ * CHANNELS_FIRST callers reach the NHWC kernels at the cost of the active windows only. */
+int sbn_copy_block_regions_t(const void* src, void* dst, int dtype, int c, const sbn_geometry* g,
+                             const int32_t* idx, const int32_t* count, int cap, int region, int dir,
+                             sbn_stream_t stream);
 
 /* Dense k x k convolution (k = 1, 3, 5; stride <= min(k, 3)), bias fused (bf16, tcgen05
  * implicit GEMM fed by strided 4-D TMA boxes): the stage-transition projection of run_stage

@@ -54,6 +54,7 @@ _PROTOS = {
     "sbn_in_bounds": (_I, [_G, _P, _P, _I, _P, _P]),
     "sbn_scatter": (_I, [_P, _I, _I, _G, _P, _P, _I, _I, _I, _P, _P]),
     "sbn_copy_block_regions": (_I, [_P, _P, _I, _I, _G, _P, _P, _I, _I, _P]),
+    "sbn_copy_block_regions_t": (_I, [_P, _P, _I, _I, _G, _P, _P, _I, _I, _I, _P]),
     "sbn_gather_grad_workspace": (C.c_size_t, [_G]),
     "sbn_dense_conv_supported": (_I, [_I, _I, _I, _I, _I, _I, _I]),
     "sbn_dense_conv_packed_bytes": (C.c_size_t, [_I, _I, _I]),

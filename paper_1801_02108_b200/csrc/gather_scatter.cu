@@ -112,6 +112,67 @@ copy_regions_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, 
   }
 }
 
+// Window regions between a CHANNELS_FIRST (n, c, h, w) tensor and a CHANNELS_LAST staging
+// tensor of the same logical dims (dir 0: NCHW -> NHWC, dir 1: NHWC -> NCHW), so the NHWC
+// tensor-core paths serve CHANNELS_FIRST callers at sparse cost (only the active windows
+// are transposed).  One CTA per (block, window row), transposed through shared memory:
+// the NCHW side moves one element per lane along a channel row (16 lanes x 16 channels,
+// no index divisions), the NHWC side moves 16-byte vectors of VEC channels along a pixel.
+// A pure copy, bit-exact.
+template <typename E>
+__global__ void __launch_bounds__(256) copy_regions_t_kernel(const E* __restrict__ src, E* __restrict__ dst, Geo g,
+                                                             int c, const int32_t* __restrict__ idx,
+                                                             const int32_t* __restrict__ count, int cap, int region,
+                                                             int dir) {
+  constexpr int VEC = 16 / sizeof(E);  // channels per 16-byte vector (host checks c % VEC == 0)
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  E* tile = reinterpret_cast<E*>(sm_raw);  // [c][LP]
+  const int B = ld_count(count, cap);
+  const int rh = region == 1 ? g.obh : g.bh, rw = region == 1 ? g.obw : g.bw;
+  const int fh = region == 1 ? g.oh : g.h, fw = region == 1 ? g.ow : g.w;
+  const int LP = rw + 1;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // NCHW side: 16 pixels x 16 channels
+  const int CV = c / VEC;                                    // NHWC side: vectors per pixel
+  for (long item = blockIdx.x; item < (long)B * rh; item += gridDim.x) {
+    const int b = (int)(item / rh), ry = (int)(item - (long)b * rh);
+    const int n = __ldg(idx + 3 * b), by = __ldg(idx + 3 * b + 1), bx = __ldg(idx + 3 * b + 2);
+    const int y = region == 1 ? by * g.obh + ry : g.oy + by * g.sy + ry;
+    if (y < 0 || y >= fh) continue;  // uniform per CTA
+    int x0 = region == 1 ? bx * g.obw : g.ox + bx * g.sx;
+    const int x1 = min(x0 + rw, fw);
+    x0 = max(x0, 0);
+    const int L = x1 - x0;
+    if (L <= 0) continue;
+    const size_t plane = (size_t)fh * fw;
+    if (dir == 0) {  // NCHW -> tile -> NHWC
+      for (int x = tx; x < L; x += 16)
+        for (int ch = ty; ch < c; ch += 16) tile[ch * LP + x] = src[((size_t)n * c + ch) * plane + (size_t)y * fw + x0 + x];
+      __syncthreads();
+      uint4* d = reinterpret_cast<uint4*>(dst + (((size_t)n * fh + y) * fw + x0) * c);
+      for (int j = threadIdx.x; j < L * CV; j += blockDim.x) {
+        const int x = j / CV, k = j - x * CV;
+        E v[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) v[e] = tile[(k * VEC + e) * LP + x];
+        d[j] = *reinterpret_cast<const uint4*>(v);
+      }
+    } else {  // NHWC -> tile -> NCHW
+      const uint4* sv = reinterpret_cast<const uint4*>(src + (((size_t)n * fh + y) * fw + x0) * c);
+      for (int j = threadIdx.x; j < L * CV; j += blockDim.x) {
+        const int x = j / CV, k = j - x * CV;
+        const uint4 q = sv[j];
+        const E* v = reinterpret_cast<const E*>(&q);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) tile[(k * VEC + e) * LP + x] = v[e];
+      }
+      __syncthreads();
+      for (int x = tx; x < L; x += 16)
+        for (int ch = ty; ch < c; ch += 16) dst[((size_t)n * c + ch) * plane + (size_t)y * fw + x0 + x] = tile[ch * LP + x];
+    }
+    __syncthreads();
+  }
+}
+
 // gather_grad (`blocks.py:162-188`): block table (frame, by, bx) -> stack row, -1 inactive.
 __global__ void block_table_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int cap,
                                    Geo g, int32_t* __restrict__ table) {
@@ -411,6 +472,38 @@ extern "C" int sbn_copy_block_regions(const void* src, void* dst, int dtype, int
     default: copy_regions_kernel<2><<<grid, kThreads, 0, s>>>((const uint8_t*)src, (uint8_t*)dst, g, pix, idx, count, cap, region); break;
   }
   return launch_status("copy_block_regions");
+}
+
+extern "C" int sbn_copy_block_regions_t(const void* src, void* dst, int dtype, int c, const sbn_geometry* gp,
+                                        const int32_t* idx, const int32_t* count, int cap, int region, int dir,
+                                        sbn_stream_t stream) {
+  int st = check_geo(gp);
+  if (st) return st;
+  const int es = dtype_size(dtype);
+  SBN_CHECK_ARG(es > 0, SBN_ERR_UNSUPPORTED, "unsupported dtype %d", dtype);
+  SBN_CHECK_ARG(c > 0, SBN_ERR_SHAPE, "channels must be > 0");
+  SBN_CHECK_ARG(region == 0 || region == 1, SBN_ERR_INVALID, "region must be 0 (window) or 1 (output)");
+  SBN_CHECK_ARG(dir == 0 || dir == 1, SBN_ERR_INVALID, "dir must be 0 (NCHW -> NHWC) or 1 (NHWC -> NCHW)");
+  if (cap <= 0) return SBN_OK;
+  SBN_CHECK_ARG(src && dst && idx && count, SBN_ERR_INVALID, "null pointer argument");
+  Geo g = to_geo(gp);
+  const int rw = region == 1 ? g.obw : g.bw;
+  const size_t smem = (size_t)c * (rw + 1) * es;
+  SBN_CHECK_ARG(smem <= 96 * 1024, SBN_ERR_UNSUPPORTED, "row tile of %zu bytes too large", smem);
+  SBN_CHECK_ARG((c * es) % 16 == 0 && ((uintptr_t)src % 16) == 0 && ((uintptr_t)dst % 16) == 0, SBN_ERR_UNSUPPORTED,
+                "channels-first window copy needs 16-byte pixel rows (c * elem_size %% 16 == 0)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const long items = (long)cap * (region == 1 ? g.obh : g.bh);
+  const unsigned grid = (unsigned)(items < (long)sm_count() * 8 ? (items < 1 ? 1 : items) : (long)sm_count() * 8);
+#define LAUNCH(E)                                                                                          \
+  {                                                                                                        \
+    auto kern = copy_regions_t_kernel<E>;                                                                  \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kern<<<grid, 256, smem, s>>>((const E*)src, (E*)dst, g, c, idx, count, cap, region, dir);              \
+  }
+  if (es == 2) LAUNCH(uint16_t) else if (es == 4) LAUNCH(uint32_t) else LAUNCH(uint64_t)
+#undef LAUNCH
+  return launch_status("copy_block_regions_t");
 }
 
 extern "C" size_t sbn_gather_grad_workspace(const sbn_geometry* gp) {

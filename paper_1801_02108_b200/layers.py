@@ -22,7 +22,7 @@ from .blocks import GatheredBlocks, gather, gather_grad, in_bounds_map, scatter_
 from .errors import EmptyBlockListError, GeometryError, ShapeMismatchError, UnsupportedConfigError
 from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, bn_inference,
                   conv_grads_nhwc, dense_conv_nhwc, exact_fp32, projection_conv)
-from .tensor import Tensor4D, cuda, dtype_code
+from .tensor import Layout, Tensor4D, cuda, dtype_code
 from .tiling import (BinaryMask, BlockIndexList, BlockSpec, compute_block_spec, downsample_mask,
                      reduce_mask)
 
@@ -60,10 +60,11 @@ class _Scratch(threading.local):
             self.bufs[key] = b
         return b
 
-    def frame(self, shape, dtype, device) -> torch.Tensor:
-        """Device staging frame of the host-frame unit path, cached per (device, stream,
-        shape, dtype); its content outside the copied regions is never read."""
-        key = (str(device), torch.cuda.current_stream(device).cuda_stream, "frame", tuple(shape), dtype)
+    def frame(self, shape, dtype, device, tag: str = "frame") -> torch.Tensor:
+        """Device staging frame (host-frame unit path, CHANNELS_FIRST windows), cached per
+        (device, stream, tag, shape, dtype); its content outside the copied regions is
+        never read."""
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream, tag, tuple(shape), dtype)
         b = self.bufs.get(key)
         if b is None:
             b = torch.empty(shape, dtype=dtype, device=device)
@@ -87,6 +88,9 @@ def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
     if f.kernel != tuple(p.kernel) or f.c_in != x.dims[3] or f.c_out != p.filter_count:
         raise ShapeMismatchError("filter bank does not match the conv params / input channels")
     spec = compute_block_spec(x.dims, p, block_size)
+    if (x.layout is Layout.CHANNELS_FIRST and (dst is None or dst.layout is Layout.CHANNELS_FIRST)
+            and _cf_windows_ok(x.dtype, x.dims[3], f.c_out)):
+        return _sparse_conv2d_channels_first(x, mask, f, p, spec, pool, threshold, dst, algo)
     xt = cuda(x.nhwc())
     n = x.dims[0]
     if dst is None:
@@ -102,6 +106,48 @@ def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
     else:
         sparse_conv_into(xt, out, f, p, spec, reduce_mask(mask, spec, pool, threshold), algo)
     return Tensor4D.from_nhwc(out, x.layout)
+
+
+def _cf_windows_ok(dtype: torch.dtype, *channels: int) -> bool:
+    """The window transposes move 16-byte pixel vectors: c * element size % 16 == 0."""
+    es = torch.empty((), dtype=dtype).element_size()
+    return all(ch * es % 16 == 0 for ch in channels)
+
+
+def _copy_windows_t(src: torch.Tensor, dst: torch.Tensor, c: int, spec: BlockSpec, idx: BlockIndexList,
+                    region: int, to_channels_last: bool) -> None:
+    """Active window regions between a CHANNELS_FIRST tensor and an NHWC staging tensor
+    (sbn_copy_block_regions_t; region 0 input windows, 1 output windows)."""
+    lib = _lib.load()
+    g = spec.c_geometry(src.shape[0])
+    _lib.check(lib.sbn_copy_block_regions_t(src.data_ptr(), dst.data_ptr(), dtype_code(src.dtype), c, C.byref(g),
+                                            idx.rows.data_ptr(), idx.count_dev.data_ptr(), idx.capacity, region,
+                                            0 if to_channels_last else 1, _lib.stream_handle(src.device)),
+               "copy_block_regions_t")
+
+
+def _sparse_conv2d_channels_first(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
+                                  spec: BlockSpec, pool, threshold, dst, algo) -> Tensor4D:
+    """sparse_conv2d for CHANNELS_FIRST storage at sparse cost: the active input windows
+    are transposed into an NHWC staging frame, the NHWC conv runs there, and only the
+    active output windows are transposed back (no full-tensor layout conversion)."""
+    xc = cuda(x.data)  # (n, c, h, w)
+    n, h, w, c = x.dims
+    oh, ow = spec.out_size
+    idx = reduce_mask(mask, spec, pool, threshold)
+    idx.to_device(xc.device)
+    stage_in = _SCRATCH.frame((n, h, w, c), xc.dtype, xc.device, tag="cf_conv_in")
+    stage_out = _SCRATCH.frame((n, oh, ow, f.c_out), xc.dtype, xc.device, tag="cf_conv_out")
+    _copy_windows_t(xc, stage_in, c, spec, idx, 0, True)
+    sparse_conv_into(stage_in, stage_out, f, p, spec, idx, algo)
+    if dst is None:
+        out = torch.zeros((n, f.c_out, oh, ow), dtype=xc.dtype, device=xc.device)
+    else:
+        if dst.dims != (n, oh, ow, f.c_out):
+            raise ShapeMismatchError(f"destination dims {dst.dims} != conv output")
+        out = cuda(dst.data).clone()
+    _copy_windows_t(stage_out, out, f.c_out, spec, idx, 1, False)
+    return Tensor4D(out, Layout.CHANNELS_FIRST)
 
 
 def _conv_packed(lib, f: FilterBank, w: torch.Tensor, dc: int, p: ConvParams, g, device) -> torch.Tensor | None:
@@ -483,6 +529,8 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
         _check_mask(x, mask)
         _host_frame_unit(x.nhwc(), mask, u, block_size, halo, algo, blocking)
         return x
+    if x.layout is Layout.CHANNELS_FIRST and _cf_windows_ok(x.dtype, x.dims[3]):
+        return _unit_channels_first(x, mask, u, block_size, halo, _shared, inplace, algo)
     xt = cuda(x.nhwc())
     if inplace and x.nhwc().is_cuda and xt.data_ptr() == x.nhwc().data_ptr():
         out = xt
@@ -496,6 +544,29 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
         spec, idx = _shared
         residual_unit_into(out, out if (out is xt) else xt, u, spec, idx, halo, algo)
     return Tensor4D.from_nhwc(out, x.layout)
+
+
+def _unit_channels_first(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams, block_size, halo: int,
+                         _shared, inplace: bool, algo) -> Tensor4D:
+    """sparse_residual_unit for CHANNELS_FIRST storage at sparse cost: active input windows
+    -> NHWC staging frame (transposing copy), the unit in place there, active output
+    windows -> the (n, c, h, w) result; ``inplace`` updates x's own storage."""
+    xc = cuda(x.data)
+    n, h, w, c = x.dims
+    if _shared is None:
+        _check_mask(x, mask)
+        spec = unit_spec(x.dims, block_size, halo)
+        idx = reduce_mask(mask, spec)
+    else:
+        spec, idx = _shared
+    idx.to_device(xc.device)
+    stage = _SCRATCH.frame((n, h, w, c), xc.dtype, xc.device, tag="cf_unit")
+    _copy_windows_t(xc, stage, c, spec, idx, 0, True)
+    residual_unit_into(stage, stage, u, spec, idx, halo, algo)
+    same = inplace and x.data.is_cuda and xc.data_ptr() == x.data.data_ptr()
+    out = xc if same else xc.clone()
+    _copy_windows_t(stage, out, c, spec, idx, 1, False)
+    return x if same else Tensor4D(out, Layout.CHANNELS_FIRST)
 
 
 class _HostFramePlan:

@@ -699,3 +699,48 @@ def test_tc_residual_unit_zero_weights_is_identity(cuda_device, c, m):
     xi = x.clone()
     P.sparse_residual_unit(P.Tensor4D(xi), mask, u, (16, 16), inplace=True)
     assert torch.equal(xi, x)
+
+
+@pytest.mark.parametrize("dtype,c,block", [(torch.bfloat16, 64, 16), (torch.float32, 16, 8), (torch.bfloat16, 128, 8)])
+def test_channels_first_sparse_conv_matches_channels_last(cuda_device, dtype, c, block):
+    """CHANNELS_FIRST sparse_conv2d (active windows transposed into an NHWC staging frame,
+    outputs transposed back) equals the CHANNELS_LAST result bit for bit, and keeps dst
+    outside the active write regions."""
+    rng = np.random.default_rng(c + block)
+    n, h, w = 2, 75, 61
+    x = torch.from_numpy(rng.standard_normal((n, h, w, c)).astype(np.float32)).to(dtype).cuda()
+    fb = P.FilterBank(torch.from_numpy((rng.standard_normal((3, 3, c, c)) / np.sqrt(9 * c)).astype(np.float32)).to(dtype),
+                      torch.from_numpy(rng.standard_normal(c).astype(np.float32)).to(dtype))
+    p = _conv((3, 3), (1, 1), True, c)
+    mk = P.synth_mask_blobs((n, h, w), 0.8, 3).cuda()
+    ref = P.sparse_conv2d(P.Tensor4D(x), mk, fb, p, (block, block)).data
+    xcf = P.Tensor4D(x.permute(0, 3, 1, 2).contiguous(), P.Layout.CHANNELS_FIRST)
+    ycf = P.sparse_conv2d(xcf, mk, fb, p, (block, block))
+    assert ycf.layout is P.Layout.CHANNELS_FIRST
+    assert torch.equal(ycf.data.permute(0, 2, 3, 1), ref)
+    dst = P.Tensor4D(torch.full((n, c, h, w), 7.0, dtype=dtype, device="cuda"), P.Layout.CHANNELS_FIRST)
+    yd = P.sparse_conv2d(xcf, mk, fb, p, (block, block), dst=dst).data.permute(0, 2, 3, 1)
+    spec = P.compute_block_spec((n, h, w, c), p, (block, block))
+    geo = O.geometry(h, w, (3, 3), (1, 1), True, (block, block))
+    reg = torch.from_numpy(O.active_region(geo, O.reduce_mask(mk.numpy(), geo), n)).cuda()
+    assert torch.equal(yd[reg], ref[reg]) and bool((yd[~reg] == 7.0).all())
+
+
+@pytest.mark.parametrize("c,m,inplace", [(64, 32, False), (64, 32, True), (128, 64, True)])
+def test_channels_first_residual_unit_matches_channels_last(cuda_device, c, m, inplace):
+    """CHANNELS_FIRST sparse_residual_unit (windows through an NHWC staging frame) equals
+    the CHANNELS_LAST result bit for bit; inplace updates x's own storage."""
+    rng = np.random.default_rng(c)
+    x = torch.from_numpy(rng.standard_normal((1, 96, 80, c)).astype(np.float32)).bfloat16().cuda()
+    u = P.random_unit_params(rng, c, m)
+    mk = P.synth_mask_blobs((1, 96, 80), 0.8, 4).cuda()
+    ref = P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16)).data
+    xcf = P.Tensor4D(x.permute(0, 3, 1, 2).contiguous(), P.Layout.CHANNELS_FIRST)
+    keep = xcf.data.clone()
+    y = P.sparse_residual_unit(xcf, mk, u, (16, 16), inplace=inplace)
+    assert y.layout is P.Layout.CHANNELS_FIRST
+    assert torch.equal(y.data.permute(0, 2, 3, 1), ref)
+    if inplace:
+        assert y is xcf and torch.equal(xcf.data.permute(0, 2, 3, 1), ref)
+    else:
+        assert torch.equal(xcf.data, keep)
