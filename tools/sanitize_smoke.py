@@ -62,5 +62,9 @@ projection_conv(xp, fp, P.ConvParams((3, 3), (2, 2), P.Padding.SAME, 96))
 # host-frame unit (zero-copy copies)
 hx = x.cpu().pin_memory()
 P.sparse_residual_unit(P.Tensor4D(hx), P.BinaryMask(mk.data.cpu().pin_memory()), u, (16, 16), inplace=True)
+# CHANNELS_FIRST paths (transposing window copies)
+xcf = P.Tensor4D(x.permute(0, 3, 1, 2).contiguous(), P.Layout.CHANNELS_FIRST)
+P.sparse_residual_unit(xcf, mk, u, (16, 16), inplace=True)
+P.sparse_conv2d(xcf, mk, fb, P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 64), (16, 16))
 torch.cuda.synchronize()
 print("sanitize smoke done", flush=True)
