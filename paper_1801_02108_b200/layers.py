@@ -726,10 +726,11 @@ def build_stage(cfg: StageConfig, rng: np.random.Generator, dtype=np.float32,
 
 
 def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
-              bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True) -> StageResult:
-    """Dense stride-s projection (cuDNN), then residual units sharing ONE index list
-    computed from the downsampled mask (reference `layers.py:311-329`).  The units run
-    in place on the stage's private activation buffer (one clone at most)."""
+              bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True,
+              _mask_at_scale: BinaryMask | None = None) -> StageResult:
+    """Dense stride-s projection (tcgen05, bias fused), then residual units sharing ONE
+    index list computed from the downsampled mask (reference `layers.py:311-329`).  The
+    units run in place on the stage's private activation buffer (one clone at most)."""
     cfg = stage.config
     t = cuda(x.nhwc())
     owned = False
@@ -742,7 +743,7 @@ def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: b
             t = (_dense_unit_bf16(t, u) if (dense_fused and t.dtype == torch.bfloat16 and u.pre_activation)
                  else t + _dense_branch(t, u))
         return StageResult(Tensor4D.from_nhwc(t, x.layout), None, None, None)
-    mask = downsample_mask(base_mask, cfg.mask_scale)
+    mask = _mask_at_scale if _mask_at_scale is not None else downsample_mask(base_mask, cfg.mask_scale)
     if mask.dims != tuple(t.shape[:3]):
         raise ShapeMismatchError(f"mask dims {mask.dims} != tensor (n, h, w) {tuple(t.shape[:3])}")
     spec = unit_spec(tuple(t.shape), cfg.block_size, halo=1)
@@ -772,8 +773,17 @@ def build_backbone(stage_cfgs, rng: np.random.Generator, dtype=np.float32,
 def run_backbone(bb: Backbone, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
                  bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True) -> list[StageResult]:
     results = []
+    prev_scale, prev_mask = 1, base_mask
     for stage in bb.stages:
-        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo, dense_fused)
+        # max-pool downsampling composes exactly (ceil dims, window = stride): each stage's
+        # mask comes from the previous stage's mask when the scale ratio is an integer,
+        # reading the small mask instead of the full-resolution one
+        sc = stage.config.mask_scale
+        m_s = None
+        if sparse and base_mask is not None and sc % prev_scale == 0:
+            m_s = downsample_mask(prev_mask, sc // prev_scale)
+            prev_scale, prev_mask = sc, m_s
+        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo, dense_fused, _mask_at_scale=m_s)
         results.append(res)
         x = res.output
     return results

@@ -744,3 +744,18 @@ def test_channels_first_residual_unit_matches_channels_last(cuda_device, c, m, i
         assert y is xcf and torch.equal(xcf.data.permute(0, 2, 3, 1), ref)
     else:
         assert torch.equal(xcf.data, keep)
+
+
+def test_backbone_hierarchical_stage_masks_equal_direct_downsample(cuda_device):
+    """run_backbone derives each stage's mask from the previous stage's (max-pool composes
+    exactly with ceil dims); every stage mask equals downsample_mask(base, scale)."""
+    from paper_1801_02108_b200 import perf
+    rng = np.random.default_rng(8)
+    cfgs = perf.detector_stage_configs()
+    bb = P.build_backbone(cfgs, rng)
+    n, h, w = 1, 203, 171  # odd sizes: ceil dims at every level
+    x = P.Tensor4D(torch.from_numpy(rng.standard_normal((n, h, w, cfgs[0].channels[0])).astype(np.float32)).bfloat16().cuda())
+    base = P.BinaryMask((rng.random((n, h, w)) < 0.05).astype(np.uint8)).cuda()
+    res = P.run_backbone(bb, x, base)
+    for r, c in zip(res, cfgs):
+        assert torch.equal(r.mask.data, P.downsample_mask(base, c.mask_scale).data)
