@@ -95,6 +95,10 @@ class ClockSampler:
         if self.ok:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            t_end = time.time() + 0.5  # the timed region starts only once sampling runs
+            while not self.samples and time.time() < t_end:
+                time.sleep(0.0002)
+            self._first = len(self.samples)
         return self
 
     def __exit__(self, *exc):
@@ -104,8 +108,10 @@ class ClockSampler:
 
     def summary(self):
         rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and name != "gpu_idle"]
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max, "reasons": rs, "samples": len(self.samples)}
+        # the sample(s) taken before the timed region started are dropped when others exist
+        smp = self.samples[getattr(self, "_first", 0):] or self.samples
+        return {"sm_mhz": statistics.median(smp) if smp else None,
+                "sm_max_mhz": self.max, "reasons": rs, "samples": len(smp)}
 
 
 # ----------------------------------------------------------------------------- workload
