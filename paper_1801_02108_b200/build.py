@@ -23,6 +23,7 @@ LIB = os.path.join(PKG, "libsbnet.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("SBN_NVCC_EXTRA", "").split()  # A/B experiments (e.g. -DSBN_DENSE_MAX_STREAM=16)
 
 
 def nvcc() -> str:

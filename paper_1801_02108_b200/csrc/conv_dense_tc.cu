@@ -25,15 +25,32 @@ namespace {
 
 constexpr int kCE = 256;                 // epilogue threads
 constexpr int kCThreads = kCE + 64;
-constexpr int kCBudget = 214 * 1024;
+#ifndef SBN_DENSE_BUDGET_KB
+#define SBN_DENSE_BUDGET_KB 220
+#endif
+#ifndef SBN_DENSE_RES_STAGES
+#define SBN_DENSE_RES_STAGES 3  // resident weights need only a 3-deep A ring (c=96: 166 KB of weights stay resident)
+#endif
+constexpr int kCBudget = SBN_DENSE_BUDGET_KB * 1024;
+#ifndef SBN_DENSE_MAX_STREAM
+#define SBN_DENSE_MAX_STREAM 8
+#endif
+constexpr int kMaxStream = SBN_DENSE_MAX_STREAM;  // streamed-weights ring depth cap
 
 // weights resident in smem with 64-channel K-chunks?  (otherwise they stream through a ring
 // in 32-channel chunks, which keeps the per-stage footprint small enough for a deep ring)
+// channel counts padded to the UMMA granule (16): K padding is zero-filled by TMA (the box
+// runs past the tensor's channel extent) and by the packed weights, N padding is dropped
+// by the epilogue
+constexpr int pad16(int c) { return (c + 15) / 16 * 16; }
+constexpr int dense_kc(int cp) { return cp % 64 == 0 ? 64 : cp % 32 == 0 ? 32 : 16; }
+
 template <int CIN, int COUT, int KS>
 constexpr bool dense_resident() {
-  constexpr int kc = CIN % 64 == 0 ? 64 : 32;
-  constexpr int gs = COUT <= 192 ? COUT : 128;
-  return 6L * 128 * kc * 2 + (long)KS * KS * CIN * COUT * 2 + 128L * (gs * 2 + 16) + COUT * 4 + 128 <= kCBudget;
+  constexpr int cp = pad16(CIN), np = pad16(COUT);
+  constexpr int kc = dense_kc(cp);
+  constexpr int gs = np <= 192 ? np : 128;
+  return (long)SBN_DENSE_RES_STAGES * 128 * kc * 2 + (long)KS * KS * cp * np * 2 + 128L * (gs * 2 + 16) + np * 4 + 128 <= kCBudget;
 }
 
 template <int CIN, int COUT, int KS>
@@ -42,33 +59,36 @@ struct CCfg {
   // 64-channel K-chunks whenever CIN allows: each TMA box row is then 128 B (SWIZZLE_128B)
   // per pixel; 32-channel chunks (64-B rows) made the per-tap boxes TMA-issue bound
   // (block-32 sparse conv 348 -> 219 us at 100 %, 192->256 projection 84 -> 68 us)
-  static constexpr int KC = CIN % 64 == 0 ? 64 : 32;
-  static_assert(CIN % KC == 0, "CIN must be a multiple of 32");
-  static constexpr int NKC = CIN / KC;
+  // (16-channel chunks, 32-B rows, SWIZZLE_32B, for CIN = 16 / 48 / 80 ...)
+  static constexpr int CP = pad16(CIN), NP = pad16(COUT);  // padded K / N extents
+  static constexpr int KC = dense_kc(CP);
+  static_assert(CP % KC == 0, "K chunking");
+  static_assert(COUT % 8 == 0, "output pixel rows must be whole 16-byte chunks");
+  static constexpr int NKC = CP / KC;
   static constexpr int ROWB = KC * 2;
-  static constexpr uint32_t SWZ = KC == 64 ? 2u : 4u;
+  static constexpr uint32_t SWZ = KC == 64 ? 2u : KC == 32 ? 4u : 6u;
   static constexpr int ACH = 128 * ROWB;
-  static constexpr int PW = COUT * 16;
+  static constexpr int PW = NP * 16;
   static constexpr int WCH = (KC / 8) * PW;
   static constexpr int CHUNKS = NKC * TAPS;
   static constexpr long WBYTES = (long)CHUNKS * WCH;
-  static constexpr int NSPLIT = COUT > 256 ? 2 : 1;
-  static constexpr int NS = COUT / NSPLIT;
-  static_assert(COUT % NSPLIT == 0 && NS % 16 == 0 && NS <= 256, "UMMA N");
-  static constexpr int NACC = 2 * COUT <= 512 ? 2 : 1;
-  static constexpr int TCOLS = NACC * COUT;
+  static constexpr int NSPLIT = NP > 256 ? 2 : 1;
+  static constexpr int NS = NP / NSPLIT;
+  static_assert(NP % NSPLIT == 0 && NS % 16 == 0 && NS <= 256, "UMMA N");
+  static constexpr int NACC = 2 * NP <= 512 ? 2 : 1;
+  static constexpr int TCOLS = NACC * NP;
   static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
-  static constexpr int GS = COUT <= 192 ? COUT : 128;  // staged columns per pass
-  static_assert(COUT % GS == 0, "staging groups");
+  static constexpr int GS = NP <= 192 ? NP : 128;  // staged columns per pass
+  static_assert(NP % GS == 0, "staging groups");
   static constexpr int SPITCH = GS * 2 + 16;
   static constexpr int STGB = 128 * SPITCH;
-  static constexpr int PARB = (COUT * 4 + 127) / 128 * 128;
+  static constexpr int PARB = (NP * 4 + 127) / 128 * 128;
   static constexpr bool RES = dense_resident<CIN, COUT, KS>();
   // A boxes are small and latency-bound (strided gathers): keep up to 12 in flight; the
   // streamed case pairs every A box with a weight chunk, so both rings get the same depth
   static constexpr int SA_R = (int)((kCBudget - WBYTES - STGB - PARB) / ACH);
   static constexpr int SS = (int)((kCBudget - STGB - PARB) / (ACH + WCH));
-  static constexpr int SA = RES ? (SA_R > 12 ? 12 : SA_R) : (SS > 8 ? 8 : SS);
+  static constexpr int SA = RES ? (SA_R > 12 ? 12 : SA_R) : (SS > kMaxStream ? kMaxStream : SS);
   static constexpr int SW = RES ? 0 : SA;
   static constexpr long WREG = RES ? WBYTES : (long)SW * WCH;
   static_assert(SA >= 2 && SA * ACH + WREG + STGB + PARB <= kCBudget, "shared memory budget");
@@ -94,20 +114,38 @@ struct __align__(64) CArgs {
   const int32_t* count;
   int cap, gsy, gsx, goy, gox;
   int obh, obw, subs_y, subs_x;
+  // mask-fused sparse mode (mask != null, idx == null): the work units are (candidate
+  // block, sub-tile) pairs; CTA c owns units c, c + G, ... (at most kMaxLocalTma), tests
+  // each unit's candidate window against the mask itself and convolves the active ones —
+  // no reduce_mask launch, no grid-wide step (used when every CTA owns <= 2 units, so the
+  // local lists are as balanced as a striped global list)
+  const uint8_t* mask;
+  int gy, gx, wbh, wbw;   // candidate grid and window (= block) size
+  int n_h, n_w;           // input (= mask) height / width
 };
+
+constexpr int kMaxLocalTma = 4;
 
 // tile -> (frame, first output row / col, first input row / col of tap (0, 0)); ly / lx:
 // rows / cols of the tile inside its block's output window (sparse) or th / tw (dense)
-__device__ __forceinline__ void conv_tile(const CArgs& a, int tile, int& n, int& oy0, int& ox0, int& iy0, int& ix0,
-                                          int& ly, int& lx) {
+__device__ __forceinline__ void conv_tile(const CArgs& a, const int32_t* lidx, int tile, int& n, int& oy0, int& ox0,
+                                          int& iy0, int& ix0, int& ly, int& lx) {
   ly = a.th;
   lx = a.tw;
-  if (a.idx) {
+  if (lidx) {
     const int subs = a.subs_y * a.subs_x;
-    const int j = tile / subs, sub = tile - j * subs;
+    int j = tile, sub;
+    if (a.mask) {  // local list: (n, by, bx, sub) per unit
+      sub = lidx[4 * j + 3];
+      j *= 4;
+    } else {
+      j = tile / subs;
+      sub = tile - j * subs;
+      j *= 3;
+    }
     const int ty = sub / a.subs_x, tx = sub - ty * a.subs_x;
-    n = __ldg(a.idx + 3 * j);
-    const int by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
+    n = lidx[j];
+    const int by = lidx[j + 1], bx = lidx[j + 2];
     oy0 = by * a.obh + ty * a.th;
     ox0 = bx * a.obw + tx * a.tw;
     iy0 = a.goy + by * a.gsy + ty * a.th * a.sy;
@@ -156,8 +194,8 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     tc::mbar_fence_init();
   }
   if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
-  for (int i = tid; i < COUT; i += kCThreads)
-    bias[i] = a.bias ? a.bias[i] : a.bias_bf16 ? __bfloat162float(a.bias_bf16[i]) : 0.f;
+  for (int i = tid; i < Q::NP; i += kCThreads)
+    bias[i] = i >= COUT ? 0.f : a.bias ? a.bias[i] : a.bias_bf16 ? __bfloat162float(a.bias_bf16[i]) : 0.f;
   if (warp == 0) tc::tmem_alloc<Q::TALLOC>(&tslot);
   tc::fence_before();
   __syncthreads();
@@ -170,7 +208,42 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       tc::bulk_g2s(Wring + (size_t)c * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[0]);
   }
   tc::pdl_wait();
-  const int ntiles = a.idx ? ld_count(a.count, a.cap) * a.subs_y * a.subs_x : a.n * a.tiles_y * a.tiles_x;
+  __shared__ int32_t s_idx[4 * kMaxLocalTma];
+  __shared__ int s_nloc;
+  const bool local = a.mask != nullptr;
+  int nblk = 0;
+  if (local) {  // reference tiling.py:138-160 (MAX pool): active iff any window pixel is set
+    const int subs = a.subs_y * a.subs_x;
+    const int U = a.n * a.gy * a.gx * subs, G = gridDim.x, gyx = a.gy * a.gx, area = a.wbh * a.wbw;
+    if (tid == 0) s_nloc = 0;
+    __syncthreads();
+    for (int k = 0; k < kMaxLocalTma; ++k) {
+      const int unit = (int)blockIdx.x + k * G;
+      if (unit >= U) break;  // uniform
+      const int cand = unit / subs, sub = unit - cand * subs;
+      const int fr = cand / gyx, rr = cand - fr * gyx, by = rr / a.gx, bx = rr - by * a.gx;
+      const int y0 = a.goy + by * a.gsy, x0 = a.gox + bx * a.gsx;
+      bool any = false;
+      for (int p = tid; p < area; p += kCThreads) {
+        const int y = y0 + p / a.wbw, xx = x0 + p % a.wbw;
+        if (y >= 0 && y < a.n_h && xx >= 0 && xx < a.n_w) any |= __ldg(a.mask + ((size_t)fr * a.n_h + y) * a.n_w + xx) != 0;
+      }
+      if (__syncthreads_or(any) && tid == 0) {
+        s_idx[4 * s_nloc] = fr;
+        s_idx[4 * s_nloc + 1] = by;
+        s_idx[4 * s_nloc + 2] = bx;
+        s_idx[4 * s_nloc + 3] = sub;
+        ++s_nloc;
+      }
+    }
+    __syncthreads();
+    nblk = s_nloc;
+  } else if (a.idx) {
+    nblk = ld_count(a.count, a.cap);
+  }
+  const int32_t* lidx = local ? s_idx : a.idx;
+  const int t0 = local ? 0 : (int)blockIdx.x, tstep = local ? 1 : (int)gridDim.x;
+  const int ntiles = local ? nblk : lidx ? nblk * a.subs_y * a.subs_x : a.n * a.tiles_y * a.tiles_x;
 
   if (warp < kLWarp) {
     // ------------------------------------------------ epilogue
@@ -180,19 +253,19 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     constexpr int IT2 = (128 * CHR + kCE - 1) / kCE;
     constexpr int BATCH = IT2 < 8 ? IT2 : 8;
     int k = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    for (int tile = t0; tile < ntiles; tile += tstep, ++k) {
       const int buf = Q::NACC == 2 ? (k & 1) : 0;
       const int use = Q::NACC == 2 ? (k >> 1) : k;
       int n, oy0, ox0, iy0, ix0, ly, lx;
-      conv_tile(a, tile, n, oy0, ox0, iy0, ix0, ly, lx);
+      conv_tile(a, lidx, tile, n, oy0, ox0, iy0, ix0, ly, lx);
       const int Y = oy0 + r / a.tw, X = ox0 + r % a.tw;
       if (half == 0)
         rowdst[r] = (r < a.th * a.tw && r / a.tw < ly && r % a.tw < lx && Y < a.oh && X < a.ow)
                         ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
-      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * COUT;
+      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * Q::NP;
       tc::mbar_wait(&acc_full[buf], use & 1);
       tc::fence_after();
-      for (int g0 = 0; g0 < COUT; g0 += Q::GS) {
+      for (int g0 = 0; g0 < Q::NP; g0 += Q::GS) {
 #pragma unroll
         for (int e = 0; e < (Q::GS / 16 + 1) / 2; ++e) {
           const int cg = 16 * (2 * e + half);
@@ -210,7 +283,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
           sp[0] = make_uint4(o[0], o[1], o[2], o[3]);
           sp[1] = make_uint4(o[4], o[5], o[6], o[7]);
         }
-        if (g0 + Q::GS >= COUT) {  // accumulator drained: the next tile's MMAs may start
+        if (g0 + Q::GS >= Q::NP) {  // accumulator drained: the next tile's MMAs may start
           tc::fence_before();
           tc::mbar_arrive(&acc_empty[buf]);
         }
@@ -224,7 +297,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
             if (jb + jj >= IT2 || it >= 128 * CHR) break;
             const int row = it / CHR, ch = it % CHR;
             const long long off = rowdst[row];
-            if (off < 0) continue;
+            if (off < 0 || (Q::NP != COUT && g0 * 2 / 16 + ch >= COUT * 2 / 16)) continue;  // N padding
             reinterpret_cast<uint4*>(a.out + off + g0)[ch] =
                 *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
           }
@@ -236,9 +309,9 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     // ------------------------------------------------ loader
     if (lane == 0) {
       int c = 0, wit = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = t0; tile < ntiles; tile += tstep) {
         int n, oy0, ox0, y0, x0, ly, lx;
-        conv_tile(a, tile, n, oy0, ox0, y0, x0, ly, lx);
+        conv_tile(a, lidx, tile, n, oy0, ox0, y0, x0, ly, lx);
         const uint32_t bytes = (uint32_t)(a.th * a.tw * Q::ROWB);
         for (int kc = 0; kc < Q::NKC; ++kc)
           for (int tap = 0; tap < Q::TAPS; ++tap, ++c) {
@@ -263,12 +336,12 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, Q::NS);
       if (Q::RES) tc::mbar_wait(&w_full[0], 0);
       int c = 0, wit = 0, k = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+      for (int tile = t0; tile < ntiles; tile += tstep, ++k) {
         const int buf = Q::NACC == 2 ? (k & 1) : 0;
         const int use = Q::NACC == 2 ? (k >> 1) : k;
         tc::mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc::fence_after();
-        const uint32_t acc = tmem + buf * COUT;
+        const uint32_t acc = tmem + buf * Q::NP;
         for (int kc = 0; kc < Q::NKC; ++kc)
           for (int tap = 0; tap < Q::TAPS; ++tap, ++c) {
             const int s = c % Q::SA;
@@ -307,11 +380,13 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
 template <int CIN, int COUT, int KS>
 __global__ void conv_dense_pack_kernel(const __nv_bfloat16* __restrict__ w, uint8_t* __restrict__ img) {
   using Q = CCfg<CIN, COUT, KS>;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KS * KS * CIN * COUT; i += gridDim.x * blockDim.x) {
-    const int tap = i / (CIN * COUT), rr = i % (CIN * COUT), ci = rr / COUT, co = rr % COUT;
+  constexpr int CP = Q::CP, NP = Q::NP;  // padded entries are written as zeros
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KS * KS * CP * NP; i += gridDim.x * blockDim.x) {
+    const int tap = i / (CP * NP), rr = i % (CP * NP), ci = rr / NP, co = rr % NP;
     const int kc = ci / Q::KC, kq = ci % Q::KC;
     *reinterpret_cast<__nv_bfloat16*>(img + (size_t)(kc * Q::TAPS + tap) * Q::WCH + (kq / 8) * Q::PW + co * 16 +
-                                      (kq % 8) * 2) = w[i];
+                                      (kq % 8) * 2) =
+        ci < CIN && co < COUT ? w[((size_t)tap * CIN + ci) * COUT + co] : __float2bfloat16(0.f);
   }
 }
 
@@ -339,7 +414,7 @@ template <int CIN, int COUT, int KS>
 int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int px, int oh, int ow,
                  const void* wpk, const float* bias, void* out, cudaStream_t s,
                  const Geo* sparse = nullptr, const int32_t* idx = nullptr, const int32_t* count = nullptr,
-                 int cap = 0, const __nv_bfloat16* bias_bf16 = nullptr) {
+                 int cap = 0, const __nv_bfloat16* bias_bf16 = nullptr, const uint8_t* mask = nullptr) {
   using Q = CCfg<CIN, COUT, KS>;
   CArgs a;
   memset(&a, 0, sizeof(a));
@@ -349,7 +424,8 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   const uint64_t str[3] = {(uint64_t)CIN * 2, (uint64_t)w * CIN * 2, (uint64_t)h * w * CIN * 2};
   const uint32_t box[4] = {(uint32_t)Q::KC, (uint32_t)(tw * sx), (uint32_t)(th * sy), 1};
   const uint32_t es[4] = {1, (uint32_t)sx, (uint32_t)sy, 1};
-  int st = encode_map(&a.tmap, x, 4, dims, str, box, Q::KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, es);
+  int st = encode_map(&a.tmap, x, 4, dims, str, box,
+                      Q::KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : Q::KC == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, es);
   if (st) return st;
   a.out = (__nv_bfloat16*)out;
   a.wpk = (const uint8_t*)wpk;
@@ -380,6 +456,21 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
     a.subs_y = subs_y;
     a.subs_x = subs_x;
     tiles = (long)cap * subs_y * subs_x;
+    if (mask) {  // one CTA per candidate up to the SM count, <= kMaxLocalTma candidates each
+      a.idx = nullptr;
+      a.mask = mask;
+      a.gy = sparse->gy;
+      a.gx = sparse->gx;
+      a.wbh = sparse->bh;
+      a.wbw = sparse->bw;
+      a.n_h = h;
+      a.n_w = w;
+      tiles = (long)sparse->n * sparse->gy * sparse->gx * subs_y * subs_x;  // (candidate, sub-tile) units
+      if (tiles > (long)kMaxLocalTma * sm_count()) {
+        set_error("mask-fused tap-GEMM conv: %ld units exceed %d per CTA", tiles, kMaxLocalTma);
+        return SBN_ERR_UNSUPPORTED;
+      }
+    }
   }
   auto kern = conv_dense_kernel<CIN, COUT, KS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
@@ -409,7 +500,10 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   X(64, 64, 1)                    \
   X(128, 128, 1)                  \
   X(32, 32, 5)                    \
-  X(64, 64, 5)
+  X(64, 64, 5)                    \
+  X(24, 24, 3)                    \
+  X(48, 48, 3)                    \
+  X(96, 96, 3)
 
 }  // namespace
 
@@ -454,6 +548,23 @@ int sparse_conv_tma(const void* x, int cin, int cout, int k, int sh, int sw, con
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   set_error("no tcgen05 tap-GEMM conv instantiation for cin=%d cout=%d kernel=%d", cin, cout, k);
+  return SBN_ERR_UNSUPPORTED;
+}
+
+// Mask-fused variant for small grids (<= 2 (candidate, sub-tile) units per SM: the local lists
+// are then as balanced as a striped global list); SBN_ERR_UNSUPPORTED above that, and the
+// caller reduces the mask separately.
+int sparse_conv_tma_masked(const void* x, const uint8_t* mask, int cin, int cout, int k, int sh, int sw,
+                           const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s) {
+  int th = 0, tw = 0, subs_y = 1, subs_x = 1;
+  if (!sparse_tile_shape(g.obh, g.obw, sh, sw, th, tw, subs_y, subs_x)) return SBN_ERR_UNSUPPORTED;
+  if ((long)g.n * g.gy * g.gx * subs_y * subs_x > 2L * sm_count()) return SBN_ERR_UNSUPPORTED;
+#define X(CI, CO, KS)                                                                                            \
+  if (cin == CI && cout == CO && k == KS)                                                                        \
+    return launch_dense<CI, CO, KS>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, nullptr, \
+                                    nullptr, g.n * g.gy * g.gx, (const __nv_bfloat16*)bias, mask);
+  SBN_DENSE_CONV_CONFIGS(X)
+#undef X
   return SBN_ERR_UNSUPPORTED;
 }
 

@@ -114,6 +114,8 @@ int sparse_conv_tma(const void* x, int cin, int cout, int k, int sh, int sw, con
                     cudaStream_t s);
 bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                               const Geo& g);
+int sparse_conv_tma_masked(const void* x, const uint8_t* mask, int cin, int cout, int k, int sh, int sw,
+                           const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s);
 
 }  // namespace sbn
 
@@ -254,6 +256,16 @@ extern "C" int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dt
       wpk = pk;
     }
     st = sparse_conv_tc_masked(x, mask, cin, cout, g, wpk, bias, cap, dst, s);
+    if (st != SBN_ERR_UNSUPPORTED) return st;
+  }
+  if (kind == 2 && algo != SBN_ALGO_SIMT && (long)cap <= 2L * sm_count()) {  // small grids: one launch
+    const void* wpk = w_packed;
+    if (!wpk) {
+      st = sparse_conv_tma_pack(w, cin, cout, kh, pk, s);
+      if (st) return st;
+      wpk = pk;
+    }
+    st = sparse_conv_tma_masked(x, mask, cin, cout, kh, sh, sw, g, wpk, bias, dst, s);
     if (st != SBN_ERR_UNSUPPORTED) return st;
   }
   st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws, rmb, stream);

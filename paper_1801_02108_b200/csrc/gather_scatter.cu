@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256) copy_regions_t_kernel(const E* __restrict
       uint4* d = reinterpret_cast<uint4*>(dst + (((size_t)n * fh + y) * fw + x0) * c);
       for (int j = threadIdx.x; j < L * CV; j += blockDim.x) {
         const int x = j / CV, k = j - x * CV;
-        E v[VEC];
+        __align__(16) E v[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) v[e] = tile[(k * VEC + e) * LP + x];
         d[j] = *reinterpret_cast<const uint4*>(v);

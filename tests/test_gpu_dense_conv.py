@@ -16,7 +16,9 @@ pytestmark = pytest.mark.gpu
     (2, 50, 38, 32, 96, 2, True, 3), (1, 37, 29, 96, 192, 2, True, 3), (2, 22, 19, 192, 256, 2, True, 3),
     (1, 14, 12, 256, 384, 2, True, 3), (1, 40, 33, 64, 64, 1, True, 3), (2, 17, 35, 128, 128, 1, False, 3),
     (1, 24, 24, 32, 32, 3, True, 3), (2, 31, 27, 64, 64, 1, True, 1), (1, 33, 40, 128, 128, 1, False, 1),
-    (2, 29, 23, 32, 32, 1, True, 5), (1, 26, 31, 64, 64, 2, False, 5), (1, 19, 22, 32, 32, 3, True, 5)])
+    (2, 29, 23, 32, 32, 1, True, 5), (1, 26, 31, 64, 64, 2, False, 5), (1, 19, 22, 32, 32, 3, True, 5),
+    # channel counts off the 32 / 64 grid: 16-channel K-chunks (48), K and N padded to 32 (24)
+    (2, 33, 41, 24, 24, 1, True, 3), (1, 45, 38, 48, 48, 1, True, 3), (1, 30, 27, 96, 96, 2, True, 3)])
 def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, same, k):
     rng = np.random.default_rng(cin + cout + stride + 7 * k)
     x = torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16().cuda()
@@ -40,7 +42,10 @@ def test_dense_conv_tc_vs_cudnn_fp32(cuda_device, n, h, w, cin, cout, stride, sa
     (96, 192, 2, 9, True, 3), (64, 64, 1, 10, True, 1), (128, 128, 1, 11, False, 1), (32, 32, 1, 14, True, 5),
     (64, 64, 1, 15, False, 5), (64, 64, 2, 17, True, 5),
     # blocks whose output window exceeds 128 px: several TMA tiles per block
-    (128, 128, 1, 32, True, 3), (64, 64, 2, 33, True, 3), (32, 32, 1, 24, False, 5), (64, 64, 1, 19, True, 1)])
+    (128, 128, 1, 32, True, 3), (64, 64, 2, 33, True, 3), (32, 32, 1, 24, False, 5), (64, 64, 1, 19, True, 1),
+    # the paper's Table-1 channel counts (24 / 48 / 96)
+    (24, 24, 1, 8, True, 3), (24, 24, 1, 16, True, 3), (48, 48, 1, 8, True, 3), (48, 48, 1, 16, True, 3),
+    (96, 96, 1, 8, True, 3), (96, 96, 1, 32, True, 3)])
 def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, block, same, k):
     """Strided / other-shape sparse 1x1 / 3x3 / 5x5 convs on the TMA tap-GEMM path (kernel
     variant 2) against the fp32 oracle on bf16-rounded inputs."""
@@ -58,3 +63,32 @@ def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, b
     ref = O.sparse_conv2d(x.float().numpy(), mk, wt.float().numpy(), b.float().numpy(), (stride, stride), same,
                           (block, block))
     assert O.rel_err(y.data.float().cpu().numpy(), ref) <= 2e-2
+
+
+@pytest.mark.parametrize("cin,k,stride,block,hw,density", [
+    (96, 3, 1, 8, (50, 88), 0.1), (24, 3, 1, 32, (400, 704), 0.1), (48, 3, 1, 16, (61, 77), 0.0),
+    (64, 1, 1, 10, (45, 52), 1.0), (32, 5, 2, 17, (70, 66), 0.3), (96, 3, 1, 8, (130, 140), 0.1)])
+def test_mask_fused_tap_gemm_conv_equals_reduce_mask_then_conv(cuda_device, cin, k, stride, block, hw, density):
+    """sparse_conv2d's one-launch path on the tap-GEMM kernel (every CTA tests its own <= 2
+    candidates; used when the candidate grid is at most 2x the SM count — the last case is
+    above that and takes reduce_mask + conv) writes exactly what reduce_mask + the listed
+    conv write, and nothing outside the active output blocks."""
+    from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_into, sparse_conv_masked_into
+    rng = np.random.default_rng(cin + block + hw[0])
+    h, w = hw
+    x = torch.from_numpy(rng.standard_normal((1, h, w, cin)).astype(np.float32)).bfloat16().cuda()
+    f = P.FilterBank(torch.from_numpy((rng.standard_normal((k, k, cin, cin)) / np.sqrt(k * k * cin)).astype(np.float32)).bfloat16(),
+                     torch.from_numpy(rng.standard_normal(cin).astype(np.float32)).bfloat16())
+    p = P.ConvParams((k, k), (stride, stride), P.Padding.SAME, cin)
+    spec = P.compute_block_spec((1, h, w, cin), p, (block, block))
+    assert sparse_conv_algo(torch.bfloat16, f, p, spec) == "tcgen05"
+    mk = P.synth_mask_topleft((1, h, w), 1.0 - density).cuda()
+    oh, ow = spec.out_size
+    a = torch.full((1, oh, ow, cin), 3.0, dtype=torch.bfloat16, device="cuda")
+    b = a.clone()
+    sparse_conv_masked_into(x, a, mk.data, f, p, spec)
+    sparse_conv_into(x, b, f, p, spec, P.reduce_mask(mk, spec))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    if density == 0.0:
+        assert bool((a == 3.0).all())

@@ -701,13 +701,14 @@ def test_tc_residual_unit_zero_weights_is_identity(cuda_device, c, m):
     assert torch.equal(xi, x)
 
 
-@pytest.mark.parametrize("dtype,c,block", [(torch.bfloat16, 64, 16), (torch.float32, 16, 8), (torch.bfloat16, 128, 8)])
-def test_channels_first_sparse_conv_matches_channels_last(cuda_device, dtype, c, block):
+@pytest.mark.parametrize("dtype,c,block,w", [(torch.bfloat16, 64, 16, 61), (torch.float32, 16, 8, 61), (torch.bfloat16, 128, 8, 61),
+                                             (torch.bfloat16, 64, 16, 62), (torch.bfloat16, 32, 8, 64)])
+def test_channels_first_sparse_conv_matches_channels_last(cuda_device, dtype, c, block, w):
     """CHANNELS_FIRST sparse_conv2d (active windows transposed into an NHWC staging frame,
     outputs transposed back) equals the CHANNELS_LAST result bit for bit, and keeps dst
     outside the active write regions."""
-    rng = np.random.default_rng(c + block)
-    n, h, w = 2, 75, 61
+    rng = np.random.default_rng(c + block + w)
+    n, h = 2, 75  # odd widths take the 2-byte NCHW path, even widths the aligned 4-byte pairs
     x = torch.from_numpy(rng.standard_normal((n, h, w, c)).astype(np.float32)).to(dtype).cuda()
     fb = P.FilterBank(torch.from_numpy((rng.standard_normal((3, 3, c, c)) / np.sqrt(9 * c)).astype(np.float32)).to(dtype),
                       torch.from_numpy(rng.standard_normal(c).astype(np.float32)).to(dtype))
@@ -726,14 +727,14 @@ def test_channels_first_sparse_conv_matches_channels_last(cuda_device, dtype, c,
     assert torch.equal(yd[reg], ref[reg]) and bool((yd[~reg] == 7.0).all())
 
 
-@pytest.mark.parametrize("c,m,inplace", [(64, 32, False), (64, 32, True), (128, 64, True)])
-def test_channels_first_residual_unit_matches_channels_last(cuda_device, c, m, inplace):
+@pytest.mark.parametrize("c,m,inplace,w", [(64, 32, False, 80), (64, 32, True, 80), (128, 64, True, 80), (64, 32, True, 79)])
+def test_channels_first_residual_unit_matches_channels_last(cuda_device, c, m, inplace, w):
     """CHANNELS_FIRST sparse_residual_unit (windows through an NHWC staging frame) equals
     the CHANNELS_LAST result bit for bit; inplace updates x's own storage."""
     rng = np.random.default_rng(c)
-    x = torch.from_numpy(rng.standard_normal((1, 96, 80, c)).astype(np.float32)).bfloat16().cuda()
+    x = torch.from_numpy(rng.standard_normal((1, 96, w, c)).astype(np.float32)).bfloat16().cuda()
     u = P.random_unit_params(rng, c, m)
-    mk = P.synth_mask_blobs((1, 96, 80), 0.8, 4).cuda()
+    mk = P.synth_mask_blobs((1, 96, w), 0.8, 4).cuda()
     ref = P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16)).data
     xcf = P.Tensor4D(x.permute(0, 3, 1, 2).contiguous(), P.Layout.CHANNELS_FIRST)
     keep = xcf.data.clone()
