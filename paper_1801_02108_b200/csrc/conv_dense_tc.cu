@@ -128,24 +128,27 @@ constexpr int kMaxLocalTma = 4;
 
 // tile -> (frame, first output row / col, first input row / col of tap (0, 0)); ly / lx:
 // rows / cols of the tile inside its block's output window (sparse) or th / tw (dense)
+template <bool LOCAL>
 __device__ __forceinline__ void conv_tile(const CArgs& a, const int32_t* lidx, int tile, int& n, int& oy0, int& ox0,
                                           int& iy0, int& ix0, int& ly, int& lx) {
   ly = a.th;
   lx = a.tw;
-  if (lidx) {
-    const int subs = a.subs_y * a.subs_x;
-    int j = tile, sub;
-    if (a.mask) {  // local list: (n, by, bx, sub) per unit
-      sub = lidx[4 * j + 3];
-      j *= 4;
+  if (LOCAL || a.idx) {
+    int by, bx, sub;
+    if constexpr (LOCAL) {  // this CTA's local list in shared memory: (n, by, bx, sub) per unit
+      n = lidx[4 * tile];
+      by = lidx[4 * tile + 1];
+      bx = lidx[4 * tile + 2];
+      sub = lidx[4 * tile + 3];
     } else {
-      j = tile / subs;
+      const int subs = a.subs_y * a.subs_x;
+      const int j = tile / subs;
       sub = tile - j * subs;
-      j *= 3;
+      n = __ldg(a.idx + 3 * j);
+      by = __ldg(a.idx + 3 * j + 1);
+      bx = __ldg(a.idx + 3 * j + 2);
     }
     const int ty = sub / a.subs_x, tx = sub - ty * a.subs_x;
-    n = lidx[j];
-    const int by = lidx[j + 1], bx = lidx[j + 2];
     oy0 = by * a.obh + ty * a.th;
     ox0 = bx * a.obw + tx * a.tw;
     iy0 = a.goy + by * a.gsy + ty * a.th * a.sy;
@@ -162,7 +165,7 @@ __device__ __forceinline__ void conv_tile(const CArgs& a, const int32_t* lidx, i
   }
 }
 
-template <int CIN, int COUT, int KS>
+template <int CIN, int COUT, int KS, bool LOCAL>
 __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_constant__ CArgs a) {
   using Q = CCfg<CIN, COUT, KS>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -194,8 +197,10 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     tc::mbar_fence_init();
   }
   if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
-  for (int i = tid; i < Q::NP; i += kCThreads)
-    bias[i] = i >= COUT ? 0.f : a.bias ? a.bias[i] : a.bias_bf16 ? __bfloat162float(a.bias_bf16[i]) : 0.f;
+  for (int i = tid; i < COUT; i += kCThreads)
+    bias[i] = a.bias ? a.bias[i] : a.bias_bf16 ? __bfloat162float(a.bias_bf16[i]) : 0.f;
+  if constexpr (Q::NP != COUT)
+    for (int i = COUT + tid; i < Q::NP; i += kCThreads) bias[i] = 0.f;
   if (warp == 0) tc::tmem_alloc<Q::TALLOC>(&tslot);
   tc::fence_before();
   __syncthreads();
@@ -208,11 +213,9 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       tc::bulk_g2s(Wring + (size_t)c * Q::WCH, a.wpk + (size_t)c * Q::WCH, Q::WCH, &w_full[0]);
   }
   tc::pdl_wait();
-  __shared__ int32_t s_idx[4 * kMaxLocalTma];
+  __shared__ int32_t s_idx[LOCAL ? 4 * kMaxLocalTma : 1];
   __shared__ int s_nloc;
-  const bool local = a.mask != nullptr;
-  int nblk = 0;
-  if (local) {  // reference tiling.py:138-160 (MAX pool): active iff any window pixel is set
+  if constexpr (LOCAL) {  // reference tiling.py:138-160 (MAX pool): active iff any window pixel is set
     const int subs = a.subs_y * a.subs_x;
     const int U = a.n * a.gy * a.gx * subs, G = gridDim.x, gyx = a.gy * a.gx, area = a.wbh * a.wbw;
     if (tid == 0) s_nloc = 0;
@@ -237,13 +240,10 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       }
     }
     __syncthreads();
-    nblk = s_nloc;
-  } else if (a.idx) {
-    nblk = ld_count(a.count, a.cap);
   }
-  const int32_t* lidx = local ? s_idx : a.idx;
-  const int t0 = local ? 0 : (int)blockIdx.x, tstep = local ? 1 : (int)gridDim.x;
-  const int ntiles = local ? nblk : lidx ? nblk * a.subs_y * a.subs_x : a.n * a.tiles_y * a.tiles_x;
+  const int32_t* lidx = s_idx;  // read only in LOCAL mode
+  const int ntiles = LOCAL ? s_nloc
+                           : a.idx ? ld_count(a.count, a.cap) * a.subs_y * a.subs_x : a.n * a.tiles_y * a.tiles_x;
 
   if (warp < kLWarp) {
     // ------------------------------------------------ epilogue
@@ -253,11 +253,11 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     constexpr int IT2 = (128 * CHR + kCE - 1) / kCE;
     constexpr int BATCH = IT2 < 8 ? IT2 : 8;
     int k = 0;
-    for (int tile = t0; tile < ntiles; tile += tstep, ++k) {
+    for (int tile = LOCAL ? 0 : blockIdx.x; tile < ntiles; tile += LOCAL ? 1 : gridDim.x, ++k) {
       const int buf = Q::NACC == 2 ? (k & 1) : 0;
       const int use = Q::NACC == 2 ? (k >> 1) : k;
       int n, oy0, ox0, iy0, ix0, ly, lx;
-      conv_tile(a, lidx, tile, n, oy0, ox0, iy0, ix0, ly, lx);
+      conv_tile<LOCAL>(a, lidx, tile, n, oy0, ox0, iy0, ix0, ly, lx);
       const int Y = oy0 + r / a.tw, X = ox0 + r % a.tw;
       if (half == 0)
         rowdst[r] = (r < a.th * a.tw && r / a.tw < ly && r % a.tw < lx && Y < a.oh && X < a.ow)
@@ -309,9 +309,9 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
     // ------------------------------------------------ loader
     if (lane == 0) {
       int c = 0, wit = 0;
-      for (int tile = t0; tile < ntiles; tile += tstep) {
+      for (int tile = LOCAL ? 0 : blockIdx.x; tile < ntiles; tile += LOCAL ? 1 : gridDim.x) {
         int n, oy0, ox0, y0, x0, ly, lx;
-        conv_tile(a, lidx, tile, n, oy0, ox0, y0, x0, ly, lx);
+        conv_tile<LOCAL>(a, lidx, tile, n, oy0, ox0, y0, x0, ly, lx);
         const uint32_t bytes = (uint32_t)(a.th * a.tw * Q::ROWB);
         for (int kc = 0; kc < Q::NKC; ++kc)
           for (int tap = 0; tap < Q::TAPS; ++tap, ++c) {
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_c
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, Q::NS);
       if (Q::RES) tc::mbar_wait(&w_full[0], 0);
       int c = 0, wit = 0, k = 0;
-      for (int tile = t0; tile < ntiles; tile += tstep, ++k) {
+      for (int tile = LOCAL ? 0 : blockIdx.x; tile < ntiles; tile += LOCAL ? 1 : gridDim.x, ++k) {
         const int buf = Q::NACC == 2 ? (k & 1) : 0;
         const int use = Q::NACC == 2 ? (k >> 1) : k;
         tc::mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
@@ -472,7 +472,7 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
       }
     }
   }
-  auto kern = conv_dense_kernel<CIN, COUT, KS>;
+  auto kern = mask ? conv_dense_kernel<CIN, COUT, KS, true> : conv_dense_kernel<CIN, COUT, KS, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(tiles < sm_count() ? (tiles < 1 ? 1 : tiles) : sm_count()));
