@@ -142,7 +142,10 @@ int sbn_copy_block_regions_t(const void* src, void* dst, int dtype, int c, const
  * implicit GEMM fed by strided 4-D TMA boxes): the stage-transition projection of run_stage
  * (reference `layers.py:316-318`: conv2d_direct + bias).  x (n, h, w, cin) NHWC; out
  * (n, oh, ow, cout); padding (ph, pw) zero-fill; packed: sbn_dense_conv_packed_bytes, from
- * sbn_dense_conv_pack of the HWIO weights; bias: cout floats. */
+ * sbn_dense_conv_pack of the HWIO weights; bias: cout floats.  Channel counts need only be
+ * multiples of 8 (16-byte pixel rows): K and N are padded to the 16-wide UMMA granule inside
+ * (TMA zero-fills the K padding, the packed image holds zero rows/columns, the epilogue drops
+ * the N padding); instantiated shapes are reported by sbn_dense_conv_supported. */
 int sbn_dense_conv_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw);
 size_t sbn_dense_conv_packed_bytes(int cin, int cout, int k);
 int sbn_dense_conv_pack(const void* w, int cin, int cout, int k, void* packed, sbn_stream_t stream);
@@ -159,8 +162,10 @@ int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int kh, int kw,
                     const int32_t* idx, const int32_t* count, int cap, void* dst, void* ws,
                     size_t ws_bytes, int algo, sbn_stream_t stream);
 /* sparse_conv2d straight from the mask (reference `layers.py:27-47`, MAX pool with the
- * default threshold): on the tcgen05 path ONE kernel (the mask reduction runs in front of
- * the conv, producing an unordered block list — the output does not depend on the order);
+ * default threshold): ONE kernel where the tcgen05 kernels allow it — the 3x3 row-shift
+ * conv with >= 64 candidates per CTA, and the tap-GEMM conv on grids of at most two
+ * (candidate block, sub-tile) units per SM — each CTA tests its own candidates' windows and
+ * convolves the active ones (unordered; the output does not depend on the order);
  * otherwise reduce_mask + sparse_conv.  sync_ws: sbn_sparse_conv_masked_sync_bytes, zeroed
  * ONCE by the caller and kept between calls (launch epoch, counters, reduce_mask words at
  * fixed offsets: calls of any geometry may share it); ws: ..._workspace bytes of scratch. */

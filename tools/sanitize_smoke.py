@@ -45,6 +45,13 @@ for c, blk_, flags in ((128, 16, 0), (128, 16, 32), (64, 8, 0)):
 x = torch.randn(n, h, w, 64, device=dev).bfloat16()
 fb = P.FilterBank((torch.randn(3, 3, 64, 64) / 24).bfloat16(), torch.randn(64).bfloat16())
 P.sparse_conv2d(P.Tensor4D(x), mk, fb, P.ConvParams((3, 3), (2, 2), P.Padding.SAME, 64), (17, 17))
+# tap-GEMM conv at the paper's Table-1 channel counts: mask-fused one-launch mode (small
+# grids: 135 and 192 units) and list mode (48 channels, 16-channel K-chunks)
+for (hh, ww, c, blk_) in ((50, 88, 96, 8), (100, 176, 24, 32), (200, 352, 48, 16)):
+    xt = torch.randn(1, hh, ww, c, device=dev).bfloat16()
+    ft = P.FilterBank((torch.randn(3, 3, c, c) / (3 * c ** 0.5)).bfloat16(), torch.randn(c).bfloat16())
+    P.sparse_conv2d(P.Tensor4D(xt), P.synth_mask_topleft((1, hh, ww), 0.9).cuda(), ft,
+                    P.ConvParams((3, 3), (1, 1), P.Padding.SAME, c), (blk_, blk_))
 # residual units
 u = P.random_unit_params(rng, 64, 32)
 P.sparse_residual_unit(P.Tensor4D(x), mk, u, (16, 16))
