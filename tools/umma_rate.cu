@@ -90,6 +90,12 @@ int main() {
   run<64, 2>("SW128", nsm);
   run<256, 0>("noswz plane layout", nsm);
   run<256, 2>("SW128", nsm);
+  run<48, 0>("noswz plane layout", nsm);
+  run<48, 1>("noswz + row shift", nsm);
+  run<96, 0>("noswz plane layout", nsm);
+  run<96, 1>("noswz + row shift", nsm);
+  run<64, 1>("noswz + row shift", nsm);
+  run<32, 1>("noswz + row shift", nsm);
   run<32, 0>("noswz plane layout", nsm);
   run<32, 2>("SW128", nsm);
   return 0;
