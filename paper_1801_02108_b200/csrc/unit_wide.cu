@@ -51,7 +51,10 @@ constexpr int kAThreads = 256;
 constexpr int kEThreads = 256;
 constexpr int kWideThreads = kAThreads + kEThreads + 64;
 constexpr int kOutCopy = kAThreads + kEThreads;  // OUT: threads in the staged copy phase
-constexpr int kMaxRows = 168;  // staged rows of a MID tile: 128 + 2*b + 2 (b <= 18)
+#ifndef SBN_WIDE_MAX_ROWS
+#define SBN_WIDE_MAX_ROWS 200
+#endif
+constexpr int kMaxRows = SBN_WIDE_MAX_ROWS;  // staged rows of a MID tile: 128 + 2*b + 2 (200: b <= 35; backbone time unchanged vs 168)
 
 enum { kIn = 1, kMid = 2, kOut = 3 };
 

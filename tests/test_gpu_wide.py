@@ -46,7 +46,9 @@ def _oracle(x_bf16, u, mk, block):
 # (c, m, block, h, w): the four config-4 stage shapes (sizes cut for the oracle), plus
 # ragged borders (h, w not multiples of the output block)
 WIDE = [(96, 48, 16, 72, 60), (192, 96, 16, 60, 44), (256, 128, 10, 41, 37), (384, 192, 6, 26, 22),
-        (128, 64, 12, 50, 34)]
+        (128, 64, 12, 50, 34),
+        # large blocks (MID tiles of up to 128 + 2*35 + 2 staged rows)
+        (96, 48, 32, 70, 66), (192, 96, 27, 61, 50), (384, 192, 35, 40, 38)]
 
 
 @pytest.mark.parametrize("c,m,block,h,w", WIDE)
@@ -112,7 +114,7 @@ def test_wide_stage_chain(cuda_device):
     assert O.rel_err(_np(res.output), ref.float().numpy()) <= 2e-2
 
 
-@pytest.mark.parametrize("block", [3, 5, 6, 7, 9, 12, 16, 18])
+@pytest.mark.parametrize("block", [3, 5, 6, 7, 9, 12, 16, 18, 24, 32, 35])
 def test_wide_unit_block_sizes(cuda_device, block):
     """Slab packing of the TMA-fed IN kernel (several small blocks per 128-row tile, or
     a block split over several tiles) for every block size shape class."""
