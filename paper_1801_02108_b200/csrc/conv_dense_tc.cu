@@ -32,6 +32,10 @@ constexpr int kCThreads = kCE + 64;
 #define SBN_DENSE_RES_STAGES 3  // resident weights need only a 3-deep A ring (c=96: 166 KB of weights stay resident)
 #endif
 constexpr int kCBudget = SBN_DENSE_BUDGET_KB * 1024;
+#ifndef SBN_DENSE_HALF_BUDGET_KB
+#define SBN_DENSE_HALF_BUDGET_KB 108
+#endif
+constexpr int kHalfBudget = SBN_DENSE_HALF_BUDGET_KB * 1024;  // per CTA at two CTAs / SM
 #ifndef SBN_DENSE_MAX_STREAM
 #define SBN_DENSE_MAX_STREAM 8
 #endif
@@ -88,7 +92,12 @@ struct CCfg {
   // streamed case pairs every A box with a weight chunk, so both rings get the same depth
   static constexpr int SA_R = (int)((kCBudget - WBYTES - STGB - PARB) / ACH);
   static constexpr int SS = (int)((kCBudget - STGB - PARB) / (ACH + WCH));
-  static constexpr int SA = RES ? (SA_R > 12 ? 12 : SA_R) : (SS > kMaxStream ? kMaxStream : SS);
+  // small shapes (resident weights, >= 4 A stages within half the SM's shared memory) run
+  // two CTAs per SM: twice the tiles in flight for the latency-bound small-channel convs
+  static constexpr int SA_2 = RES ? (int)((kHalfBudget - WBYTES - STGB - PARB) / ACH) : 0;
+  static constexpr int CPS = SA_2 >= 4 ? 2 : 1;  // CTAs per SM
+  static constexpr int SA = CPS == 2 ? (SA_2 > 12 ? 12 : SA_2)
+                                     : RES ? (SA_R > 12 ? 12 : SA_R) : (SS > kMaxStream ? kMaxStream : SS);
   static constexpr int SW = RES ? 0 : SA;
   static constexpr long WREG = RES ? WBYTES : (long)SW * WCH;
   static_assert(SA >= 2 && SA * ACH + WREG + STGB + PARB <= kCBudget, "shared memory budget");
@@ -166,7 +175,7 @@ __device__ __forceinline__ void conv_tile(const CArgs& a, const int32_t* lidx, i
 }
 
 template <int CIN, int COUT, int KS, bool LOCAL>
-__global__ void __launch_bounds__(kCThreads, 1) conv_dense_kernel(const __grid_constant__ CArgs a) {
+__global__ void __launch_bounds__(kCThreads, CCfg<CIN, COUT, KS>::CPS) conv_dense_kernel(const __grid_constant__ CArgs a) {
   using Q = CCfg<CIN, COUT, KS>;
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int SWB = Q::SW > 0 ? Q::SW : 1;
@@ -475,7 +484,8 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
   auto kern = mask ? conv_dense_kernel<CIN, COUT, KS, true> : conv_dense_kernel<CIN, COUT, KS, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(tiles < sm_count() ? (tiles < 1 ? 1 : tiles) : sm_count()));
+  const long slots = (long)Q::CPS * sm_count();
+  cfg.gridDim = dim3((unsigned)(tiles < slots ? (tiles < 1 ? 1 : tiles) : slots));
   cfg.blockDim = dim3(kCThreads);
   cfg.dynamicSmemBytes = Q::SMEM;
   cfg.stream = s;
