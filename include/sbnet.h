@@ -163,8 +163,8 @@ int sbn_sparse_conv(const void* x, int dtype, int cin, int cout, int kh, int kw,
                     size_t ws_bytes, int algo, sbn_stream_t stream);
 /* sparse_conv2d straight from the mask (reference `layers.py:27-47`, MAX pool with the
  * default threshold): ONE kernel where the tcgen05 kernels allow it — the 3x3 row-shift
- * conv with >= 64 candidates per CTA, and the tap-GEMM conv on grids of at most two
- * (candidate block, sub-tile) units per SM — each CTA tests its own candidates' windows and
+ * conv with >= 64 candidates per CTA, and the tap-GEMM conv on grids of at most four
+ * (candidate block, sub-tile) units per CTA slot — each CTA tests its own candidates' windows and
  * convolves the active ones (unordered; the output does not depend on the order);
  * otherwise reduce_mask + sparse_conv.  sync_ws: sbn_sparse_conv_masked_sync_bytes, zeroed
  * ONCE by the caller and kept between calls (launch epoch, counters, reduce_mask words at

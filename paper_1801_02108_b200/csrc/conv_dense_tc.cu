@@ -134,6 +134,10 @@ struct __align__(64) CArgs {
 };
 
 constexpr int kMaxLocalTma = 4;
+#ifndef SBN_FUSED_UNITS_PER_CTA
+#define SBN_FUSED_UNITS_PER_CTA 4  // mask-fused mode only while every CTA owns <= this many units (2 vs 4: conv-3 block 16 12.3 vs 8.7 us)
+#endif
+static_assert(SBN_FUSED_UNITS_PER_CTA <= kMaxLocalTma, "local list size");
 
 // tile -> (frame, first output row / col, first input row / col of tap (0, 0)); ly / lx:
 // rows / cols of the tile inside its block's output window (sparse) or th / tw (dense)
@@ -475,7 +479,7 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
       a.n_h = h;
       a.n_w = w;
       tiles = (long)sparse->n * sparse->gy * sparse->gx * subs_y * subs_x;  // (candidate, sub-tile) units
-      if (tiles > (long)kMaxLocalTma * sm_count()) {
+      if (tiles > (long)kMaxLocalTma * Q::CPS * sm_count()) {
         set_error("mask-fused tap-GEMM conv: %ld units exceed %d per CTA", tiles, kMaxLocalTma);
         return SBN_ERR_UNSUPPORTED;
       }
@@ -568,10 +572,12 @@ int sparse_conv_tma_masked(const void* x, const uint8_t* mask, int cin, int cout
                            const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s) {
   int th = 0, tw = 0, subs_y = 1, subs_x = 1;
   if (!sparse_tile_shape(g.obh, g.obw, sh, sw, th, tw, subs_y, subs_x)) return SBN_ERR_UNSUPPORTED;
-  if ((long)g.n * g.gy * g.gx * subs_y * subs_x > 2L * sm_count()) return SBN_ERR_UNSUPPORTED;
+  const long units = (long)g.n * g.gy * g.gx * subs_y * subs_x;
 #define X(CI, CO, KS)                                                                                            \
   if (cin == CI && cout == CO && k == KS)                                                                        \
-    return launch_dense<CI, CO, KS>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, nullptr, \
+    return units > (long)SBN_FUSED_UNITS_PER_CTA * CCfg<CI, CO, KS>::CPS * sm_count()                          \
+               ? SBN_ERR_UNSUPPORTED                                                                             \
+               : launch_dense<CI, CO, KS>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, nullptr, \
                                     nullptr, g.n * g.gy * g.gx, (const __nv_bfloat16*)bias, mask);
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X

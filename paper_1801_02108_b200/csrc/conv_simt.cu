@@ -258,7 +258,7 @@ extern "C" int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dt
     st = sparse_conv_tc_masked(x, mask, cin, cout, g, wpk, bias, cap, dst, s);
     if (st != SBN_ERR_UNSUPPORTED) return st;
   }
-  if (kind == 2 && algo != SBN_ALGO_SIMT && (long)cap <= 2L * sm_count()) {  // small grids: one launch
+  if (kind == 2 && algo != SBN_ALGO_SIMT && (long)cap <= 8L * sm_count()) {  // small grids: one launch
     const void* wpk = w_packed;
     if (!wpk) {
       st = sparse_conv_tma_pack(w, cin, cout, kh, pk, s);
