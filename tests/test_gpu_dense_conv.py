@@ -67,12 +67,13 @@ def test_sparse_conv_strided_tc_vs_fp32_oracle(cuda_device, cin, cout, stride, b
 
 @pytest.mark.parametrize("cin,k,stride,block,hw,density", [
     (96, 3, 1, 8, (50, 88), 0.1), (24, 3, 1, 32, (400, 704), 0.1), (48, 3, 1, 16, (61, 77), 0.0),
-    (64, 1, 1, 10, (45, 52), 1.0), (32, 5, 2, 17, (70, 66), 0.3), (96, 3, 1, 8, (130, 140), 0.1)])
+    (64, 1, 1, 10, (45, 52), 1.0), (32, 5, 2, 17, (70, 66), 0.3), (96, 3, 1, 8, (130, 140), 0.1),
+    (96, 3, 1, 8, (200, 200), 0.1)])
 def test_mask_fused_tap_gemm_conv_equals_reduce_mask_then_conv(cuda_device, cin, k, stride, block, hw, density):
-    """sparse_conv2d's one-launch path on the tap-GEMM kernel (every CTA tests its own <= 2
-    candidates; used when the candidate grid is at most 2x the SM count — the last case is
-    above that and takes reduce_mask + conv) writes exactly what reduce_mask + the listed
-    conv write, and nothing outside the active output blocks."""
+    """sparse_conv2d's one-launch path on the tap-GEMM kernel (every CTA tests its own <= 4
+    (candidate, sub-tile) units; the last case, 1156 units on 148 slots, is above that and
+    takes reduce_mask + conv) writes exactly what reduce_mask + the listed conv write, and
+    nothing outside the active output blocks."""
     from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_into, sparse_conv_masked_into
     rng = np.random.default_rng(cin + block + hw[0])
     h, w = hw
