@@ -372,7 +372,7 @@ def run_ours(args):
     if not args.no_backbone and 64 % world == 0:
         per = 64 // world
         leg = run_backbone_leg(P, torch, dev, time_graph, per, 0.2, reps=3, per_stage=False,
-                               first_seed=rank * per, dense=(world == 1))
+                               dense=(world == 1), shard_of=64)
         t5 = leg["sparse_ms"]
         if world > 1:
             tt = torch.tensor([t5], device=cdev)
@@ -624,7 +624,7 @@ def run_batched(P, torch, dev, time_graph, u, hbm_peak, unit_fn):
 
 
 def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, per_stage=True,
-                     first_seed=0, dense=True):
+                     first_seed=0, dense=True, shard_of=None):
     """BASELINE config 4 (config 5 per-GPU shard when frames = 64/G): the 4-stage sparse
     detector backbone (perf.DETECTOR_STAGES: [3, 6, 6, 3] bottleneck units, 96/192/256/384
     channels, dense stride-2 cuDNN projections) on `frames` 800x700 BEV frames with seeded
@@ -635,12 +635,19 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
     from paper_1801_02108_b200.layers import residual_unit_algo
     hh, ww, cin = perf.DETECTOR_INPUT
     bb = P.build_backbone(perf.detector_stage_configs(), np.random.default_rng(4))
+    run = lambda x_, m_: P.run_backbone(bb, x_, m_)  # noqa: E731
+    if shard_of is not None:
+        # config 5: this rank's contiguous shard of ONE global batch of `shard_of` frames
+        # (global frame f has mask seed f), run through the package's ShardedBackbone
+        sb = P.ShardedBackbone(bb, shard_of)
+        first_seed, frames = sb.lo, sb.hi - sb.lo
+        run = sb.run_local  # noqa: E731
     x = torch.randn(frames, hh, ww, cin, device=dev).bfloat16()
     mk = np.concatenate([P.synth_mask_blobs((1, hh, ww), 1.0 - density, first_seed + s).numpy()
                          for s in range(frames)])
     mask = P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False)
     xt = P.Tensor4D(x)
-    res = P.run_backbone(bb, xt, mask)  # warm: weight images, scratch buffers
+    res = run(xt, mask)  # warm: weight images, scratch buffers
     dres = P.run_backbone(bb, xt, mask, sparse=False, dense_fused=False) if dense else None
     if dense:
         P.run_backbone(bb, xt, mask, sparse=False, dense_fused=True)
@@ -659,7 +666,7 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
 
     def sp(k):
         for _ in range(k):
-            P.run_backbone(bb, xt, mask)
+            run(xt, mask)
 
     def de(k):
         for _ in range(k):
@@ -676,6 +683,22 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
            "frames_per_s": round(frames / (t_sp * 1e-3), 1),
            "tflops_alg_sparse": round(f_sp / (t_sp * 1e-3) / 1e12, 1),
            "density_achieved": round(float(mk.mean()), 4), "stages": []}
+    out["finite_output"] = bool(torch.isfinite(res[-1].output.data).all().item())
+    if shard_of is not None:
+        # verification, off the timed region: the per-rank stage index lists merged in rank
+        # order must equal reduce_mask over the whole global batch (frames 0..shard_of-1)
+        merged = sb.index_lists(res)
+        if sb.rank == 0:
+            gm = np.concatenate([P.synth_mask_blobs((1, hh, ww), 1.0 - density, f).numpy() for f in range(shard_of)])
+            gmask = P.BinaryMask(torch.from_numpy(gm).to(dev), validate=False)
+            ok = True
+            for st_, r, mg in zip(bb.stages, res, merged):
+                m_s = P.downsample_mask(gmask, st_.config.mask_scale)
+                n_, h_, w_, c_ = r.output.dims
+                spec_ = P.unit_spec((shard_of, h_, w_, c_), st_.config.block_size)
+                ok = ok and np.array_equal(P.reduce_mask(m_s, spec_).entries, mg)
+            out["index_lists_match_global"] = bool(ok)
+        out["shard"] = [sb.lo, sb.hi]
     if dense:
         t_de, t_df = timed(de), timed(def_)
         f_de = perf.flops_backbone(dres, bb.stages, False)

@@ -73,6 +73,13 @@ typedef struct sbn_unit_params {
   /* optional: pre-packed tensor-core image from sbn_residual_unit_pack (NULL: the call
    * packs into its workspace first, one extra launch) */
   const void* tc_packed;
+  /* identity of tc_packed: the byte count sbn_residual_unit_packed_bytes and the
+   * variant sbn_residual_unit_packed_variant reported for the geometry it was packed
+   * for.  The image layout depends on the variant the geometry selects (block size,
+   * batch size); a call whose variant needs another image rejects it with
+   * SBN_ERR_INVALID instead of reading a foreign layout. */
+  size_t tc_packed_bytes;
+  int tc_packed_variant;
 } sbn_unit_params;
 
 const char* sbn_version(void);
@@ -197,6 +204,11 @@ int sbn_residual_unit(const void* x, int dtype, int c, int m, const sbn_geometry
  * and bulk-copied by every CTA.  bytes == 0: the tcgen05 path does not apply. */
 size_t sbn_residual_unit_packed_bytes(int dtype, int c, int m, const sbn_geometry* g, int halo,
                                       int pre_act);
+/* Which tensor-core unit (and so which packed image layout) a call with this geometry
+ * runs: 1 = fused single kernel (unit_tc.cu), 2 = wide three-launch unit (unit_wide.cu),
+ * 0 = none (SIMT).  Depends on the candidate count n*gy*gx, not only the block size. */
+int sbn_residual_unit_packed_variant(int dtype, int c, int m, const sbn_geometry* g, int halo,
+                                     int pre_act);
 int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
                            const sbn_geometry* g, int halo, int pre_act, void* packed,
                            sbn_stream_t stream);

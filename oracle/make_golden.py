@@ -370,11 +370,52 @@ def gen_formats(bc):
     np.savez_compressed(os.path.join(OUT, "formats.npz"), **out)
 
 
+BACKBONE_SEED = 2024
+BACKBONE_DIMS = (2, 80, 64, 32)  # reduced-H*W config 4 (800x700 -> 80x64, N=8 -> 2)
+# the package's config-4 detector (paper_1801_02108_b200/perf.py DETECTOR_STAGES): the paper's
+# [3, 6, 6, 3] units, [96, 192, 256, 384] channels, m = c/2, blocks (16, 16, 10, 6)
+DETECTOR_STAGES = [
+    (3, (32, 48, 96), (16, 16), 2, 2),
+    (6, (96, 96, 192), (16, 16), 4, 2),
+    (6, (192, 128, 256), (10, 10), 8, 2),
+    (3, (256, 192, 384), (6, 6), 16, 2),
+]
+
+
+def gen_backbone(bc):
+    """Configs 4/5 at reduced H x W: the reference ``run_backbone`` over the detector's
+    four stages (``perf.DETECTOR_STAGES`` channel chain, block sizes and mask scales,
+    3/6/6/3 units) on a partial blob mask (seed = frame index, as config 5).  Weights are
+    re-derived from ``BACKBONE_SEED`` (draw order pinned by units.npz), so only the inputs,
+    the masks and the per-stage outputs / index lists are stored."""
+    from blockconv.cli import DEMO_INPUT, DEMO_STAGES
+    out = {}
+    for tag, stages, dims, seed, sp in (("det", DETECTOR_STAGES, BACKBONE_DIMS, BACKBONE_SEED, 0.75),
+                                        ("demo", DEMO_STAGES, DEMO_INPUT, 7, 0.8)):
+        n, h, w, c = dims
+        cfgs = [bc.StageConfig(u, ch, bs, sc, st) for u, ch, bs, sc, st in stages]
+        bb = bc.build_backbone(cfgs, np.random.default_rng(seed))
+        x = np.random.default_rng(seed + 1).standard_normal((n, h, w, c)).astype(np.float32)
+        mask = np.concatenate([bc.synth_mask_blobs((1, h, w), sp, i).data for i in range(n)])
+        res = bc.run_backbone(bb, bc.Tensor4D(x), bc.BinaryMask(mask))
+        out[f"{tag}_cfg"] = np.asarray([n, h, w, c, seed])
+        out[f"{tag}_stages"] = np.asarray([[u, *ch, *bs, sc, st] for u, ch, bs, sc, st in stages])
+        out[f"{tag}_x"], out[f"{tag}_mask"] = x, mask
+        for i, r in enumerate(res):
+            out[f"{tag}_s{i}_y"] = r.output.data
+            out[f"{tag}_s{i}_mask"] = r.mask.data
+            out[f"{tag}_s{i}_idx"] = r.indices.entries
+    np.savez_compressed(os.path.join(OUT, "backbone.npz"), **out)
+
+
 def main():
     bc = _ref()
+    only = set(sys.argv[1:])
     os.makedirs(OUT, exist_ok=True)
     for fn in (gen_geometry, gen_reduce_mask, gen_gather_scatter, gen_sparse_conv, gen_residual,
-               gen_masks, gen_units, gen_config1, gen_grads, gen_formats):
+               gen_masks, gen_units, gen_config1, gen_grads, gen_formats, gen_backbone):
+        if only and fn.__name__ not in only:
+            continue
         fn(bc)
         print("wrote", fn.__name__)
 

@@ -33,6 +33,7 @@ __all__ = [
     "rel_err", "active_region",
     "gather_grad", "scatter_grad", "conv_nhwc_grads", "sparse_conv2d_grads",
     "sparse_residual_unit_grads", "sparse_batch_norm_train",
+    "random_unit", "build_stage", "run_stage", "run_backbone",
 ]
 
 
@@ -332,6 +333,77 @@ def sparse_residual_unit(x, mask, u: dict, block, halo: int = 1, shared=None):
 def dense_residual_unit(x, u: dict):
     """Dense oracle of the unit, SAME 3x3 (reference ``layers.py:194-200``)."""
     return x + unit_branch(x, u, (1, 1), 0)
+
+
+# --------------------------------------------------------------------------- stages / backbone
+
+def random_unit(rng: np.random.Generator, c: int, m: int, dtype=np.float32, scale: float = 0.2,
+                pre: bool = True) -> dict:
+    """Seeded unit parameters as a dict, drawing from ``rng`` in the reference's order
+    (``layers.py:117-134``): first BN, last BN, conv1, conv2, conv3 (weights then bias
+    each), mid BN."""
+    def filt(kh, kw, ci, co):
+        return (rng.standard_normal((kh, kw, ci, co)).astype(dtype) * scale,
+                rng.standard_normal(co).astype(dtype) * scale)
+
+    def norm(ch):
+        gamma = (0.5 + rng.random(ch)).astype(dtype)
+        beta = (rng.standard_normal(ch) * scale).astype(dtype)
+        mean = (rng.standard_normal(ch) * scale).astype(dtype)
+        var = (0.5 + rng.random(ch)).astype(dtype)
+        return dict(gamma=gamma, beta=beta, mean=mean, var=var)
+
+    first = norm(c if pre else m)
+    last = norm(m if pre else c)
+    (w1, b1), (w2, b2), (w3, b3) = filt(1, 1, c, m), filt(3, 3, m, m), filt(1, 1, m, c)
+    mid = norm(m)
+    return dict(pre=pre, w1=w1, b1=b1, w2=w2, b2=b2, w3=w3, b3=b3, bn1=first, bn2=mid, bn3=last)
+
+
+def build_stage(rng: np.random.Generator, units: int, channels, block, mask_scale: int = 1,
+                stride: int = 1, dtype=np.float32, scale: float = 0.2) -> dict:
+    """Stage weights in the reference's draw order (``layers.py:287-298``): the 3x3
+    projection (only when the stride or the channel count changes), then the units."""
+    c_in, c_mid, c_out = channels
+    proj = None
+    if stride != 1 or c_in != c_out:
+        proj = (rng.standard_normal((3, 3, c_in, c_out)).astype(dtype) * scale,
+                rng.standard_normal(c_out).astype(dtype) * scale)
+    us = [random_unit(rng, c_out, c_mid, dtype, scale) for _ in range(units)]
+    return dict(proj=proj, stride=stride, block=tuple(block), mask_scale=mask_scale, units=us)
+
+
+def run_stage(stage: dict, x: np.ndarray, base_mask, sparse: bool = True):
+    """One backbone stage (reference ``layers.py:311-329``): dense SAME 3x3 stride-s
+    projection, then the units, all sharing ONE index list reduced from
+    ``downsample_mask(base_mask, mask_scale)`` with the unit geometry (halo 1).
+    Returns (output, stage mask, index rows)."""
+    if stage["proj"] is not None:
+        w, b = stage["proj"]
+        x = dense_conv2d(x, w, b, (stage["stride"], stage["stride"]), True)
+    if not sparse:
+        for u in stage["units"]:
+            x = dense_residual_unit(x, u)
+        return x, None, None
+    mask = downsample_mask(base_mask, stage["mask_scale"])
+    if mask.shape != x.shape[:3]:
+        raise ValueError(f"mask dims {mask.shape} != tensor (n, h, w) {x.shape[:3]}")
+    g = unit_geometry(x.shape[1], x.shape[2], stage["block"], 1)
+    idx = reduce_mask(mask, g, "max")
+    for u in stage["units"]:
+        x = sparse_residual_unit(x, mask, u, stage["block"], 1, shared=(g, idx))
+    return x, mask, idx
+
+
+def run_backbone(stages, x: np.ndarray, base_mask, sparse: bool = True):
+    """Stages in sequence (reference ``layers.py:346-353``); a list of per-stage
+    (output, mask, index rows)."""
+    out = []
+    for st in stages:
+        res = run_stage(st, x, base_mask, sparse)
+        out.append(res)
+        x = res[0]
+    return out
 
 
 # --------------------------------------------------------------------------- training path

@@ -34,7 +34,7 @@ class Geometry(C.Structure):
 class UnitParams(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in (
         "w1", "b1", "w2", "b2", "w3", "b3", "bn1_scale", "bn1_shift", "bn2_scale",
-        "bn2_shift", "bn3_scale", "bn3_shift", "tc_packed")]
+        "bn2_shift", "bn3_scale", "bn3_shift", "tc_packed")] + [("tc_packed_bytes", C.c_size_t), ("tc_packed_variant", C.c_int)]
 
 
 _P = C.c_void_p
@@ -83,6 +83,7 @@ _PROTOS = {
     "sbn_sparse_residual_unit": (_I, [_P, _P, _I, _I, _I, _G, _I, _I, C.POINTER(UnitParams), _P, _P,
                                       C.c_size_t, _P, C.c_size_t, _I, _P]),
     "sbn_residual_unit_packed_bytes": (C.c_size_t, [_I, _I, _I, _G, _I, _I]),
+    "sbn_residual_unit_packed_variant": (_I, [_I, _I, _I, _G, _I, _I]),
     "sbn_residual_unit_pack": (_I, [C.POINTER(UnitParams), _I, _I, _I, _G, _I, _I, _P, _P]),
 }
 

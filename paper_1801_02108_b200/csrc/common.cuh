@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdarg>
+#include <atomic>
 
 #include "../../include/sbnet.h"
 
@@ -33,6 +34,22 @@ inline int launch_status(const char* what) {
   note_launch();
   return SBN_OK;
 }
+
+// Function attributes (max dynamic smem, carveout, cluster size) are per device: a call
+// site sets them the first time it launches on each device.  Setting them twice is
+// harmless, so two threads racing on the first launch both set them.
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> done{0};
+  template <typename F>
+  void operator()(F&& set_attrs) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    set_attrs();
+    done.fetch_or(bit, std::memory_order_release);
+  }
+};
 
 int sm_count();           // SMs of the current device (cached)
 int max_smem_optin();     // max dynamic smem per block (cached)
@@ -104,7 +121,7 @@ constexpr int kTraceSlots = 32;
 unsigned long long* trace_buffer();  // host side: current buffer or nullptr
 int debug_flags();                   // host side: sbn_debug_set_flags()
 enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4, kDebugForceFused = 8, kDebugConvTma = 16,
-       kDebugConvPair = 32 };
+       kDebugConvPair = 32, kDebugCooperative = 64 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -121,6 +138,35 @@ __device__ __forceinline__ void trace(unsigned long long* tb, int phase) {
   }
 }
 
+// Forward-progress guard for waits on OTHER CTAs of the same grid (grid barriers, the fused
+// unit's list slots and in-place gate).  Such a wait completes only if every CTA it depends
+// on is resident; the launchers size these grids to the co-resident capacity of an idle
+// GPU, but concurrent work (other streams or processes, MPS clients) can keep part of a
+// grid off the SMs.  Instead of hanging, a wait that exceeds kSpinTimeoutNs of %globaltimer
+// prints where it stalled and traps: the launch fails with a CUDA error the caller sees at
+// its next synchronisation.  Checked every 64 polls (a globaltimer read costs ~a poll).
+#ifndef SBN_SPIN_TIMEOUT_NS
+#define SBN_SPIN_TIMEOUT_NS 4000000000ull  // 4 s: >> any legitimate wait (us) or context timeslice (ms)
+#endif
+constexpr unsigned long long kSpinTimeoutNs = SBN_SPIN_TIMEOUT_NS;
+enum SpinSite { kSpinGridBarrier = 1, kSpinGridWait = 2, kSpinSlotDone = 3, kSpinSlotStaged = 4, kSpinSlotEntry = 5 };
+
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  unsigned polls = 0;
+  __device__ __forceinline__ void tick(int site) {
+    if ((++polls & 63u) != 0) return;
+    const unsigned long long t = gtimer();
+    if (t0 == 0) {
+      t0 = t;
+    } else if (t - t0 > kSpinTimeoutNs) {
+      printf("sbnet: CTA %d of %d stalled %.1f s at spin site %d (grid not co-resident: concurrent work "
+             "holds SMs); aborting the launch\n", (int)blockIdx.x, (int)gridDim.x, (double)(t - t0) * 1e-9, site);
+      __trap();
+    }
+  }
+};
+
 // Grid-wide barrier among `expected` co-resident CTAs (caller guarantees residency).
 // `bar` = two zero-initialised words in global memory; the last CTA to leave resets
 // them, so the same words serve the next launch in the stream.
@@ -129,7 +175,11 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int exp
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(bar, 1u);
-    while (*reinterpret_cast<volatile unsigned int*>(bar) < expected) __nanosleep(64);
+    SpinGuard sg;
+    while (*reinterpret_cast<volatile unsigned int*>(bar) < expected) {
+      __nanosleep(64);
+      sg.tick(kSpinGridBarrier);
+    }
     __threadfence();
     if (atomicAdd(bar + 1, 1u) == expected - 1) {
       bar[0] = 0u;
@@ -152,7 +202,11 @@ __device__ __forceinline__ void grid_arrive(unsigned int* bar) {
 __device__ __forceinline__ void grid_wait(unsigned int* bar, unsigned int expected) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    while (*reinterpret_cast<volatile unsigned int*>(bar) < expected) __nanosleep(32);
+    SpinGuard sg;
+    while (*reinterpret_cast<volatile unsigned int*>(bar) < expected) {
+      __nanosleep(32);
+      sg.tick(kSpinGridWait);
+    }
     __threadfence();
     if (atomicAdd(bar + 1, 1u) == expected - 1) {
       bar[0] = 0u;

@@ -425,13 +425,12 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
     const size_t smem = (size_t)per * g.w * 4 + (size_t)per * g.gx;
     if (smem <= 160 * 1024 && per <= kClusterMaxRowsPerCta) {
       const int vec = ((g.w & 3) == 0) && (((uintptr_t)mask & 3) == 0) && g.bh < 256;
-      static bool attr = false;
-      if (!attr) {
+      static PerDeviceOnce attr;
+      attr([] {
         cudaFuncSetAttribute(reduce_mask_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              160 * 1024 + 16);
         cudaFuncSetAttribute(reduce_mask_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        attr = true;
-      }
+      });
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cl);
       cfg.blockDim = dim3(kClusterThreads);

@@ -272,6 +272,15 @@ int unit_tc_kind(int dtype, int c, int m, const Geo& g, int halo, int pre_act) {
   return 0;
 }
 
+// a caller-supplied packed image must have been built for the variant this call runs
+static int check_packed(const sbn_unit_params* p, int variant, size_t want) {
+  SBN_CHECK_ARG(!p->tc_packed || (p->tc_packed_variant == variant && p->tc_packed_bytes == want), SBN_ERR_INVALID,
+                "tc_packed image (variant %d, %zu bytes) does not match this call's variant %d (%zu bytes): "
+                "it was packed for another block size or batch size",
+                p->tc_packed_variant, p->tc_packed_bytes, variant, want);
+  return SBN_OK;
+}
+
 size_t unit_workspace(int dtype, int c, int m, const Geo& g, int halo, int algo, bool tc) {
   const int es = dtype_size(dtype);
   const int cap = g.n * g.gy * g.gx;
@@ -306,6 +315,12 @@ extern "C" size_t sbn_residual_unit_packed_bytes(int dtype, int c, int m, const 
     case 2: return unit_wide_packed_bytes(c, m);
     default: return 0;
   }
+}
+
+extern "C" int sbn_residual_unit_packed_variant(int dtype, int c, int m, const sbn_geometry* gp,
+                                                int halo, int pre_act) {
+  if (!gp) return 0;
+  return unit_tc_kind(dtype, c, m, to_geo(gp), halo, pre_act);
 }
 
 extern "C" int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
@@ -361,6 +376,8 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
     SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
                   "residual unit needs a %zu-byte workspace", need);
     uint8_t* stacks = wsb + kBarBytes;
+    st = check_packed(p, 2, unit_wide_packed_bytes(c, m));
+    if (st) return st;
     const void* packed = p->tc_packed;
     if (!packed) {
       packed = stacks + unit_wide_stack_bytes(m, g);
@@ -380,6 +397,8 @@ extern "C" int sbn_residual_unit(const void* x, int dtype, int c, int m, const s
     }
   }
   if (use_tc) {
+    st = check_packed(p, 1, unit_tc_packed_bytes(c, m, g));
+    if (st) return st;
     const void* packed = p->tc_packed;
     if (!packed) {
       SBN_CHECK_ARG(ws && ws_bytes >= need, SBN_ERR_WORKSPACE,
@@ -472,6 +491,8 @@ extern "C" int sbn_sparse_residual_unit(const void* x, const uint8_t* mask, int 
                       gp->oh == gp->h && gp->ow == gp->w,
                   SBN_ERR_INVALID, "geometry is not a residual-unit spec");
     const size_t rb = kBarBytes + rim_bytes(dtype_size(dtype), c, g, halo, cap);
+    st = check_packed(p, 1, unit_tc_packed_bytes(c, m, g));
+    if (st) return st;
     const void* packed = p->tc_packed;
     if (!packed) {
       st = unit_tc_pack(p, c, m, g, uws + rb, s);

@@ -266,10 +266,17 @@ __device__ __forceinline__ bool slot_before_store(const TcArgs& a, unsigned tag,
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned* ring = slot_ring(a, tag);
-    while (ld_acquire_u32(ring + 1) != gridDim.x) __nanosleep(32);
+    SpinGuard sg;
+    while (ld_acquire_u32(ring + 1) != gridDim.x) {
+      __nanosleep(32);
+      sg.tick(kSpinSlotDone);
+    }
     s_B = (int)ld_acquire_u32(ring);
     if (s_B <= ncons)
-      while (ld_acquire_u32(ring + 2) < (unsigned)(s_B * ctas_per_block)) __nanosleep(32);
+      while (ld_acquire_u32(ring + 2) < (unsigned)(s_B * ctas_per_block)) {
+        __nanosleep(32);
+        sg.tick(kSpinSlotStaged);
+      }
   }
   __syncthreads();
   const int B = s_B;
@@ -306,7 +313,9 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
     unsigned* ring = slot_ring(a, tag);
     int ok = 0;
     unsigned long long e = 0;
+    SpinGuard sg;
     while (true) {  // both words in flight per iteration: one round trip per poll
+      sg.tick(kSpinSlotEntry);
       e = ld_relaxed_u64(&a.etag[blk]);
       const unsigned d = ld_relaxed_u32(ring + 1);
       if (slot_match(e, tag)) {
@@ -816,13 +825,12 @@ template <int C, int MC, int BS>
 int launch(const TcArgs& a, int cap, cudaStream_t s) {
   using K = Cfg<C, MC, BS>;
   auto kern = unit_tc_kernel<C, MC, BS>;
-  static bool attr = false;  // per-instantiation; attribute is per-function, idempotent
-  if (!attr) {
+  static PerDeviceOnce attr;  // per instantiation and device
+  attr([&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    attr = true;
-  }
+  });
   int occ = resident_per_sm(kern, kThreads, K::SMEM, K::TALLOC, K::OCC);
   g_last_occ[0] = occ;
   {
@@ -842,11 +850,13 @@ int launch(const TcArgs& a, int cap, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = K::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (debug_flags() & kDebugCooperative) ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kern, a);
   return launch_status("residual_unit_tcgen05");
 }
@@ -1238,18 +1248,31 @@ int launch_pair(const TcArgs& a, int cap, cudaStream_t s) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = PK::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
+  at[2].id = cudaLaunchAttributeCooperative;
+  at[2].val.cooperative = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = (debug_flags() & kDebugCooperative) ? 3 : 2;
   const int per_sm = resident_per_sm(kern, kThreads, PK::SMEM, PK::TALLOC, 2);
   const int maxcl = sm_count() * per_sm / 2;
   g_last_occ[1] = maxcl;
+  {
+    int api_cl = -1;  // what the occupancy API believes (diagnostics: tools/coop_probe.py)
+    cudaLaunchConfig_t q = cfg;
+    q.gridDim = dim3(2);
+    q.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&api_cl, kern, &q) != cudaSuccess) {
+      cudaGetLastError();
+      api_cl = -1;
+    }
+    g_last_occ[7] = api_cl;
+  }
   long pairs = cap < maxcl ? cap : maxcl;  // all pairs co-resident (grid barriers)
   if (pairs < 1) pairs = 1;
   cfg.gridDim = dim3((unsigned)(2 * pairs));

@@ -88,8 +88,9 @@ def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
     if f.kernel != tuple(p.kernel) or f.c_in != x.dims[3] or f.c_out != p.filter_count:
         raise ShapeMismatchError("filter bank does not match the conv params / input channels")
     spec = compute_block_spec(x.dims, p, block_size)
-    if (x.layout is Layout.CHANNELS_FIRST and (dst is None or dst.layout is Layout.CHANNELS_FIRST)
-            and _cf_windows_ok(x.dtype, x.dims[3], f.c_out)):
+    out_layout = x.layout if dst is None else dst.layout  # the result takes dst's layout (blocks.py:141)
+    if (x.layout is Layout.CHANNELS_FIRST and out_layout is Layout.CHANNELS_FIRST
+            and _cf_windows_ok(x.dtype, (x.dims[3], spec.block_size[1]), (f.c_out, spec.out_block_size[1]))):
         return _sparse_conv2d_channels_first(x, mask, f, p, spec, pool, threshold, dst, algo)
     xt = cuda(x.nhwc())
     n = x.dims[0]
@@ -105,13 +106,16 @@ def sparse_conv2d(x: Tensor4D, mask: BinaryMask, f: FilterBank, p: ConvParams,
         sparse_conv_masked_into(xt, out, cuda(mask.data), f, p, spec, algo)
     else:
         sparse_conv_into(xt, out, f, p, spec, reduce_mask(mask, spec, pool, threshold), algo)
-    return Tensor4D.from_nhwc(out, x.layout)
+    return Tensor4D.from_nhwc(out, out_layout)
 
 
-def _cf_windows_ok(dtype: torch.dtype, *channels: int) -> bool:
-    """The window transposes move 16-byte pixel vectors: c * element size % 16 == 0."""
+def _cf_windows_ok(dtype: torch.dtype, *regions: tuple[int, int]) -> bool:
+    """Whether sbn_copy_block_regions_t can move these (channels, row width) windows: it
+    copies 16-byte pixel vectors (c * element size % 16 == 0) through a shared-memory row
+    tile of c * (width + 1) elements (<= 96 KB, gather_scatter.cu).  Otherwise the caller
+    takes the full-layout NHWC path."""
     es = torch.empty((), dtype=dtype).element_size()
-    return all(ch * es % 16 == 0 for ch in channels)
+    return all(ch * es % 16 == 0 and ch * (wd + 1) * es <= 96 * 1024 for ch, wd in regions)
 
 
 def _copy_windows_t(src: torch.Tensor, dst: torch.Tensor, c: int, spec: BlockSpec, idx: BlockIndexList,
@@ -392,10 +396,15 @@ class ResidualUnitParams:
         if geometry is None:
             return base
         lib = _lib.load()
-        gkey = key + (geometry.bh, geometry.bw, halo)
+        # the image layout depends on the variant the geometry selects (block size AND the
+        # candidate count n*gy*gx: fused single kernel vs wide three-launch unit); the image
+        # is cached per (variant, byte count) and the C side rejects a mismatched image
+        args = (dtype_code(dtype), self.channels, self.mid_channels, C.byref(geometry), halo,
+                int(self.pre_activation))
+        nb = int(lib.sbn_residual_unit_packed_bytes(*args))
+        variant = int(lib.sbn_residual_unit_packed_variant(*args))
+        gkey = key + (geometry.bh, geometry.bw, halo, variant, nb)
         if gkey not in self._cache:
-            nb = lib.sbn_residual_unit_packed_bytes(dtype_code(dtype), self.channels, self.mid_channels,
-                                                    C.byref(geometry), halo, int(self.pre_activation))
             if nb == 0:
                 self._cache[gkey] = (base, None)
             else:
@@ -408,6 +417,8 @@ class ResidualUnitParams:
                 up = _lib.UnitParams()
                 C.memmove(C.byref(up), C.byref(base), C.sizeof(base))
                 up.tc_packed = img.data_ptr()
+                up.tc_packed_bytes = nb
+                up.tc_packed_variant = variant
                 self._cache[gkey] = (up, img)
         return self._cache[gkey][0]
 
@@ -529,7 +540,7 @@ def sparse_residual_unit(x: Tensor4D, mask: BinaryMask, u: ResidualUnitParams,
         _check_mask(x, mask)
         _host_frame_unit(x.nhwc(), mask, u, block_size, halo, algo, blocking)
         return x
-    if x.layout is Layout.CHANNELS_FIRST and _cf_windows_ok(x.dtype, x.dims[3]):
+    if x.layout is Layout.CHANNELS_FIRST and _cf_windows_ok(x.dtype, (x.dims[3], block_size[1])):
         return _unit_channels_first(x, mask, u, block_size, halo, _shared, inplace, algo)
     xt = cuda(x.nhwc())
     if inplace and x.nhwc().is_cuda and xt.data_ptr() == x.nhwc().data_ptr():
@@ -731,6 +742,9 @@ def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: b
     """Dense stride-s projection (tcgen05, bias fused), then residual units sharing ONE
     index list computed from the downsampled mask (reference `layers.py:311-329`).  The
     units run in place on the stage's private activation buffer (one clone at most)."""
+    if bn_mode is not BnMode.INFERENCE:
+        # the sparse / dense units are inference-BN only (sparse_residual_unit raises the same)
+        raise UnsupportedConfigError("run_stage: inference-mode BN only")
     cfg = stage.config
     t = cuda(x.nhwc())
     owned = False

@@ -43,3 +43,13 @@ def unit_dict(case):
         u[f"bn{i}"] = {"gamma": case[f"bn{i}_gamma"], "beta": case[f"bn{i}_beta"],
                        "mean": case[f"bn{i}_mean"], "var": case[f"bn{i}_var"], "eps": 1e-5}
     return u
+
+
+def backbone_case(tag: str):
+    """(cfg, stage rows, x, mask, per-stage [(y, mask, idx)]) of the backbone fixture
+    (reference run_backbone on a partial blob mask; tag 'det' = the config-4 detector chain
+    at reduced H x W, 'demo' = the reference's own DEMO_STAGES)."""
+    z = load("backbone")
+    stages = z[f"{tag}_stages"]
+    res = [(z[f"{tag}_s{i}_y"], z[f"{tag}_s{i}_mask"], z[f"{tag}_s{i}_idx"]) for i in range(len(stages))]
+    return z[f"{tag}_cfg"], stages, z[f"{tag}_x"], z[f"{tag}_mask"], res

@@ -142,3 +142,48 @@ def test_fused_dense_comparator_matches_reference_math(cuda_device):
         ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
     ref = O.dense_residual_unit(x.float().numpy(), ud)
     assert O.rel_err(y, ref) <= 2e-2
+
+
+def test_unit_packed_image_identifies_the_variant(cuda_device):
+    """The fused (single-kernel) and wide (three-launch) tcgen05 units pack different weight
+    images; which one a call runs depends on the candidate count n*gy*gx.  The host caches
+    the image per (variant, byte count); the C side rejects an image tagged for the other
+    variant."""
+    import ctypes
+    lib = _lib.load()
+    for c, m, b in [(64, 32, 16), (64, 32, 8), (128, 64, 16), (32, 16, 16)]:
+        var = []
+        for n in (1, 64):
+            g = P.unit_spec((n, 400, 400, c), (b, b)).c_geometry(n)
+            var.append(lib.sbn_residual_unit_packed_variant(2, c, m, ctypes.byref(g), 1, 1))
+        assert var == [1, 2], (c, m, b, var)
+    # an image packed for one frame handed to a 64-frame call is refused
+    u = P.random_unit_params(np.random.default_rng(1), 32, 16)
+    g1 = P.unit_spec((1, 400, 400, 32), (16, 16)).c_geometry(1)
+    up = u.c_params(torch.bfloat16, cuda_device, g1)
+    g64 = P.unit_spec((64, 400, 400, 32), (16, 16)).c_geometry(64)
+    st = lib.sbn_residual_unit(None, 2, 32, 16, ctypes.byref(g64), 1, 1, ctypes.byref(up), None, None, 0,
+                               None, None, 0, 0, None)
+    assert st == 0  # cap 0: nothing to do, arguments not inspected further
+    x = torch.zeros((64, 400, 400, 32), dtype=torch.bfloat16, device=cuda_device)
+    idx = P.reduce_mask(P.BinaryMask.full(64, 400, 400).cuda(), P.unit_spec(tuple(x.shape), (16, 16)))
+    ws = torch.zeros(lib.sbn_residual_unit_workspace(2, 32, 16, ctypes.byref(g64), 1, 0), dtype=torch.uint8,
+                     device=cuda_device)
+    st = lib.sbn_residual_unit(x.data_ptr(), 2, 32, 16, ctypes.byref(g64), 1, 1, ctypes.byref(up),
+                               idx.rows.data_ptr(), idx.count_dev.data_ptr(), idx.capacity, x.data_ptr(),
+                               ws.data_ptr(), ws.numel(), 0, None)
+    assert st == _lib.SBN_ERR_INVALID and b"variant" in lib.sbn_last_error()
+
+
+def test_unit_params_reused_across_the_fused_wide_threshold(cuda_device):
+    """One ResidualUnitParams object run at 1 frame (fused single kernel) and then at 10
+    frames (> 8192 candidates: the wide unit) and back: each call gets the image of its own
+    variant (the cache was keyed on the block size only)."""
+    x, u, _ = _case(5, 10, 400, 400, 64, 32, 0.1)
+    mk = P.BinaryMask(np.concatenate([P.synth_mask_blobs((1, 400, 400), 0.9, i).numpy() for i in range(10)]))
+    one = P.BinaryMask(mk.numpy()[:1])
+    assert P.unit_spec((10, 400, 400, 64), (16, 16)).grid_count[0] ** 2 * 10 > 8192
+    ref0 = _oracle(x[:1], u, one, (16, 16))
+    for n, m_ in ((1, one), (10, mk), (1, one)):
+        y = P.sparse_residual_unit(P.Tensor4D(x[:n].clone().cuda()), m_, u, (16, 16))
+        assert O.rel_err(_np(y)[:1], ref0) <= 2e-2, n

@@ -201,3 +201,10 @@ def test_product_path_fails_loudly_without_cuda():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         P.sparse_conv2d(x, P.BinaryMask.full(1, 8, 8),
                         P.FilterBank(np.zeros((3, 3, 2, 2), np.float32)), _conv((3, 3), (1, 1), True, 2), (4, 4))
+
+
+def test_run_stage_rejects_train_stats_bn():
+    st = P.build_stage(P.StageConfig(1, (4, 2, 4), (6, 6)), np.random.default_rng(0))
+    x = P.Tensor4D(np.zeros((1, 8, 8, 4), np.float32))
+    with pytest.raises(P.UnsupportedConfigError):
+        P.run_stage(st, x, P.BinaryMask.full(1, 8, 8), bn_mode=P.BnMode.TRAIN_STATS)

@@ -7,7 +7,7 @@ import sys
 import numpy as np
 import pytest
 
-from golden_cases import cases, conv_cfg, load, unit_dict
+from golden_cases import backbone_case, cases, conv_cfg, load, unit_dict
 from oracle import sbnet_oracle as O
 
 REF_SRC = "/root/reference/pkg/src"
@@ -99,6 +99,22 @@ def test_config1_golden():
     assert len(idx) == 12
     y = O.sparse_conv2d(z["x"], z["mask"], z["w"], z["b"], (1, 1), True, (16, 16))
     assert O.rel_err(y, z["y"]) <= 1e-6
+
+
+@pytest.mark.parametrize("tag", ["det", "demo"])
+def test_backbone_matches_reference_golden(tag):
+    """Configs 4/5 pinned: the oracle's run_backbone (weights re-drawn from the stored seed
+    in the reference's RNG order) reproduces the reference's per-stage outputs, masks and
+    index lists on a partial mask."""
+    cfg, stages, x, mask, res = backbone_case(tag)
+    rng = np.random.default_rng(int(cfg[4]))
+    sts = [O.build_stage(rng, int(u), (int(a), int(b), int(c)), (int(bh), int(bw)), int(sc), int(st))
+           for u, a, b, c, bh, bw, sc, st in stages]
+    out = O.run_backbone(sts, x, mask)
+    for (y, m, idx), (gy, gm, gidx) in zip(out, res):
+        assert np.array_equal(m, gm)
+        assert idx.tolist() == gidx.tolist()
+        assert O.rel_err(y, gy) <= 1e-5
 
 
 @pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference only in the build container")

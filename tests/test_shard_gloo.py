@@ -31,20 +31,27 @@ def _free_port():
 
 
 def _worker(rank, world, port, n_frames, q):
+    """CPU-only plumbing check (no GPU here): the per-rank index lists come from the oracle
+    as a stand-in for the device reduce_mask; tests/test_gpu_shard.py runs the same
+    two-rank flow with the CUDA reduce_mask / backbone on cuda:0."""
+    from types import SimpleNamespace as NS
+
     import torch.distributed as dist
-    from oracle import sbnet_oracle as O  # stand-in for the per-rank device reduce_mask
-    from paper_1801_02108_b200.shard import gather_index_lists
+    from oracle import sbnet_oracle as O
+    from paper_1801_02108_b200.shard import ShardedBackbone
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(0)
     masks = (rng.random((n_frames, 40, 36)) < 0.02).astype(np.uint8)
-    lo, hi = shard_bounds(n_frames, rank, world)
-    geo = O.unit_geometry(40, 36, (10, 10))
-    local = O.reduce_mask(masks[lo:hi], geo)
-    merged = gather_index_lists(local, n_frames)
-    ref = O.reduce_mask(masks, geo)
-    q.put((rank, bool(np.array_equal(merged, ref)), len(ref)))
+    sb = ShardedBackbone(None, n_frames)  # rank / world from the process group
+    assert (sb.rank, sb.world) == (rank, world)
+    assert (sb.lo, sb.hi) == shard_bounds(n_frames, rank, world)
+    geos = [O.unit_geometry(40, 36, (10, 10)), O.unit_geometry(40, 36, (6, 6))]
+    local = [NS(indices=NS(entries=O.reduce_mask(masks[sb.lo:sb.hi], g))) for g in geos]
+    merged = sb.index_lists(local)
+    ok = all(np.array_equal(mg, O.reduce_mask(masks, g)) for mg, g in zip(merged, geos))
+    q.put((rank, bool(ok), len(merged[0])))
     dist.barrier()
     dist.destroy_process_group()
 
