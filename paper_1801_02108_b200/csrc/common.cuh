@@ -151,6 +151,8 @@ __device__ __forceinline__ void trace(unsigned long long* tb, int phase) {
 constexpr unsigned long long kSpinTimeoutNs = SBN_SPIN_TIMEOUT_NS;
 enum SpinSite { kSpinGridBarrier = 1, kSpinGridWait = 2, kSpinSlotDone = 3, kSpinSlotStaged = 4, kSpinSlotEntry = 5 };
 
+__device__ unsigned int g_spin_reported = 0u;
+
 struct SpinGuard {
   unsigned long long t0 = 0;
   unsigned polls = 0;
@@ -160,7 +162,8 @@ struct SpinGuard {
     if (t0 == 0) {
       t0 = t;
     } else if (t - t0 > kSpinTimeoutNs) {
-      printf("sbnet: CTA %d of %d stalled %.1f s at spin site %d (grid not co-resident: concurrent work "
+      if (atomicExch(&g_spin_reported, 1u) == 0u)  // one report per module load
+        printf("sbnet: CTA %d of %d stalled %.1f s at spin site %d (grid not co-resident: concurrent work "
              "holds SMs); aborting the launch\n", (int)blockIdx.x, (int)gridDim.x, (double)(t - t0) * 1e-9, site);
       __trap();
     }

@@ -243,6 +243,7 @@ __device__ __forceinline__ void slot_last_producer(const TcArgs& a, unsigned tag
     other[0] = 0u;
     other[1] = 0u;
     other[2] = 0u;
+    other[3] = 0u;  // spare ring word: kept zero like the others
     a.sw[0] = tag;
   }
 }
@@ -1088,6 +1089,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     trace(a.trace, 6);
     // ---- 3. epilogue 1 -> A2 (local rows; rank>0 also feeds the previous tile's halo rows)
     if (round == 0) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // partner started
+    trace(a.trace, 20);
     {
       const int j = q * 32 + lane;
       const int r = rank * 128 + j;
@@ -1116,6 +1118,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
         }
       }
     }
+    trace(a.trace, 21);
     tc::fence_before();
     asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
     cl.sync();  // A2 halo rows from the partner have landed
@@ -1153,6 +1156,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     uint4 res[C / 16];
 #pragma unroll
     for (int k = 0; k < C / 16; ++k) res[k] = tc::ld_v4_pred(op + k, store);
+    trace(a.trace, 22);
 #pragma unroll
     for (int c0 = hf * (MC / 2); c0 < (hf + 1) * (MC / 2); c0 += 16) {
       float v[16];
@@ -1187,6 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     tc::mbar_wait(&bar, phase);
     phase ^= 1;
     tc::fence_after();
+    trace(a.trace, 23);
     if (inplace && resident) grid_wait(a.gbar, 2u * (unsigned)B);
     if (first_store) {  // fused in place: neighbours staged / later rims snapshotted
       if (slot_before_store<C, BS>(a, tag, npairs, 2, known_B)) rimsrc = a.rim_buf;

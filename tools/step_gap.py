@@ -51,7 +51,9 @@ for i, t in enumerate(ts):
 t = ts[1]
 act = t[t[:, 11] > 0]
 chain = [(16, "pdl"), (12, "flags"), (14, "done"), (2, "entry"), (18, "loop top"), (3, "loads"), (4, "staged"), (5, "A1"),
-         (6, "gemm1"), (7, "epi1"), (8, "gemm2"), (9, "epi2"), (10, "gemm3+wait"), (11, "epi3"), (17, "exit")]
+         (6, "gemm1"), (20, "clwait"), (21, "epi1 st"), (7, "cl.sync"), (13, "g2 issued"), (8, "gemm2"), (22, "res ld"),
+         (9, "epi2"), (23, "gemm3"), (10, "gate"), (11, "epi3"), (17, "exit")]
+chain = [c for c in chain if len(act) and (act[:, c[0]] > 0).all()]  # phases this kernel records
 if len(act):
     print(f"active CTAs {len(act)}; phase (min / median / max us):")
     for (a_, na), (b_, nb) in zip(chain, chain[1:]):
@@ -64,6 +66,8 @@ if len(act):
     t1 = ts[1]
     prod = t1[t1[:, 19] > 0]
     for nm, a_, b_ in (("flags -> slot atomic", 12, 19), ("slot atomic -> done", 19, 14), ("pdl -> flags", 16, 12)):
+        if not len(prod):
+            break
         d = (prod[:, b_] - prod[:, a_]) / 1e3
         print(f"  producers with active blocks ({len(prod)}): {nm:>22} {d.min():6.2f} {np.median(d):6.2f} {d.max():6.2f}")
     # consumer wait vs the producer that published its entry is not traced; show entry poll by slot order
