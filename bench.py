@@ -52,6 +52,8 @@ def parse():
                          "plumbing with several ranks sharing one GPU)")
     ap.add_argument("--no-backbone", action="store_true", help="skip the config-4/5 backbone legs")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32 (config 1, fp32 unit) timings")
+    ap.add_argument("--no-reduce-mask-bw", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -291,6 +293,40 @@ def run_ours(args):
         return a_.elapsed_time(b_) / nd
     dense_ms = dense_time(False)
     dense_fused_ms = dense_time(True)
+    # (3) this repo's own tcgen05 unit over a FULL mask: the dense layer computed by the fused
+    #     kernel (every block; windows overlap by the 1-pixel halo, so ~1.31x the dense work)
+    full_mask = P.BinaryMask.full(1, H, W).cuda()
+
+    def own_dense_steps(k):
+        for i in range(k):
+            sparse_residual_unit_into(xs[i % nf], xs[i % nf], full_mask.data, u, spec)
+    nd_ = max(nf, args.steps // 10)
+    gd_, sd_ = time_graph(torch, own_dense_steps, nd_, 3, soak_s=0.2)
+    with torch.cuda.stream(sd_):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(sd_)
+        gd_.replay()
+        b_.record(sd_)
+        b_.synchronize()
+    dense_own_ms = a_.elapsed_time(b_) / nd_
+    del gd_
+    # dense-layer roofline: minimal traffic = read x + write y once; FLOPs of the 3 convs
+    dense_bytes = 2 * H * W * C * 2
+    dense_flops = 2 * H * W * (C * M + 9 * M * M + M * C)
+    bf16_peak = peaks.get("bf16_tflops", 1665.5)
+
+    def dense_reading(ms, what):
+        return {"ms": round(ms, 5), "what": what,
+                "hbm_frac": round(dense_bytes / (ms * 1e-3) / 1e9 / hbm_peak, 4),
+                "tflops": round(dense_flops / (ms * 1e-3) / 1e12, 1),
+                "speedup_of_sparse": round(ms / ms_step, 3)}
+    dense_readings = {
+        "eager_cudnn": dense_reading(dense_ms, "eager cuDNN convs + separate BN / ReLU kernels"),
+        "cudnn_fused": dense_reading(dense_fused_ms, "cuDNN, BN folded into the convs, ReLU fused"),
+        "own_tcgen05_full_mask": dense_reading(dense_own_ms, "this repo's fused tcgen05 unit over a full mask"),
+        "bound": {"bytes": dense_bytes, "flops": dense_flops, "hbm_bound_ms": round(dense_bytes / hbm_peak / 1e6, 5),
+                  "note": "minimal dense traffic = read x + write y (41 MB); HBM-bound (~320 flop/B ridge vs 104 flop/B)"}}
+    best_dense_ms = min(dense_ms, dense_fused_ms, dense_own_ms)
 
     # ---- e2e: pinned HOST frame + mask -> public API (sparse_residual_unit, inplace=True on
     #      the host frame) -> host frame updated, every step.  The call moves the mask plus
@@ -407,9 +443,12 @@ def run_ours(args):
                 b_.record(ss)
                 b_.synchronize()
             t_sp = a_.elapsed_time(b_) / 200
+            sb_ = unit_bytes(P, spec, P.reduce_mask(mk, spec).entries) + H * W
             sweep[f"{d:.1f}"] = {"density_achieved": round(float(mk.data.float().mean()), 4),
                                  "sparse_ms": round(t_sp, 5), "speedup_vs_dense": round(dense_ms / t_sp, 3),
-                                 "speedup_vs_dense_fused": round(dense_fused_ms / t_sp, 3)}
+                                 "speedup_vs_dense_fused": round(dense_fused_ms / t_sp, 3),
+                                 "speedup_vs_best_dense": round(best_dense_ms / t_sp, 3),
+                                 "alg_bytes": int(sb_), "hbm_frac": round(sb_ / (t_sp * 1e-3) / 1e9 / hbm_peak, 4)}
 
     # ---- config 3: single 3x3 conv, 800x700x128 bf16, top-left masks (paper protocol,
     #      PAPER.md:397-398), blocks 8/16, sparse (reduce_mask + tcgen05 fused conv into a
@@ -433,7 +472,25 @@ def run_ours(args):
     if not args.no_paper_tables and rank == 0:
         paper_tables = run_paper_tables(P, torch, dev, time_graph)
 
-    # ---- CPU baseline: the oracle port of the reference's sparse_residual_unit
+    # ---- self-check after the timed regions: the timed ring frames were updated in place
+    #      thousands of times (they saturate), so one step on a pristine frame is compared
+    #      with the fp32 oracle (bf16-rounded weights) and checked finite
+    spot = None
+    if rank == 0:
+        spot = spot_check(P, torch, dev, u, spec, blk, masks[0])
+
+    # ---- fp32 timings: BASELINE config 1 (fp32 sparse conv, the reference's own CPU case) and
+    #      the config-2 unit at the reference's precision (SIMT kernels)
+    fp32 = None
+    if rank == 0 and not args.no_fp32:
+        fp32 = run_fp32(P, torch, dev, time_graph, u, masks[0])
+
+    # ---- reduce_mask at a bandwidth-relevant size: N=64 x 800x700 masks (35.8 MB)
+    rmbw = None
+    if rank == 0 and not args.no_reduce_mask_bw:
+        rmbw = run_reduce_mask_bw(P, torch, dev, time_graph, hbm_peak)
+
+    # ---- CPU baseline: the reference's sparse_residual_unit (baseline/_ref) and the oracle port
     cpu = None
     if rank == 0 and not args.no_cpu:
         # pristine frame 0 (the ring frames have been updated in place by the timed steps)
@@ -459,6 +516,12 @@ def run_ours(args):
             "ms_per_step_dense_fused": round(dense_fused_ms, 5),
             "speedup_vs_dense_fused": round(dense_fused_ms / ms_step, 3),
             "dense_fused": "cuDNN with BN folded into the convs and ReLU fused (cudnn_convolution_relu)",
+            "ms_per_step_dense_own": round(dense_own_ms, 5),
+            "speedup_vs_best_dense": round(best_dense_ms / ms_step, 3),
+            "dense_readings": dense_readings,
+            "spot_check": spot,
+            "fp32": fp32,
+            "reduce_mask_bw": rmbw,
             "e2e": {"value": round(world * 1e3 / e2e_ms, 2), "unit": UNIT,
                     "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                     "api": "sparse_residual_unit(Tensor4D(pinned host frame), pinned host mask, inplace=True)",
@@ -677,11 +740,16 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
             P.run_backbone(bb, xt, mask, sparse=False, dense_fused=True)
     t_sp = timed(sp)
     f_sp = perf.flops_backbone(res, bb.stages, True)
+    try:
+        tpeak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", 1665.5)
+    except Exception:
+        tpeak = 1665.5
     out = {"workload": f"config4: 4-stage sparse detector backbone, N={frames} x {hh}x{ww}x{cin} bf16, "
                        f"{density:.0%} blob masks (seeds {first_seed}..{first_seed + frames - 1})",
            "frames": frames, "sparse_ms": round(t_sp, 4),
            "frames_per_s": round(frames / (t_sp * 1e-3), 1),
            "tflops_alg_sparse": round(f_sp / (t_sp * 1e-3) / 1e12, 1),
+           "frac_sparse": round(f_sp / (t_sp * 1e-3) / 1e12 / tpeak, 4),
            "density_achieved": round(float(mk.mean()), 4), "stages": []}
     out["finite_output"] = bool(torch.isfinite(res[-1].output.data).all().item())
     if shard_of is not None:
@@ -718,7 +786,10 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
             t3 = (timed(lambda k, stg=stg, inp=inp: [P.run_stage(stg, inp, mask, sparse=False) for _ in range(k)])
                   if dense else float("nan"))
             n_, h_, w_, c_ = r.output.dims
-            out["stages"].append({"stage": i + 2, "hw": [h_, w_], "c": c_, "m": m_i,
+            f_st = perf.flops_backbone([r], [stg], True)
+            out["stages"].append({"tflops_alg": round(f_st / (t1 * 1e-3) / 1e12, 1),
+                                  "frac": round(f_st / (t1 * 1e-3) / 1e12 / tpeak, 4),
+                                  "stage": i + 2, "hw": [h_, w_], "c": c_, "m": m_i,
                                   "block": stg.config.block_size[0], "units": stg.config.unit_count,
                                   "blocks": int(r.indices.count),
                                   "density": round(float(r.mask.data.float().mean()), 4),
@@ -727,6 +798,105 @@ def run_backbone_leg(P, torch, dev, time_graph, frames=8, density=0.2, reps=5, p
                                   "dense_fused_ms": round(t3, 4)})
             inp = r.output
     return out
+
+
+def _timed_graph(torch, time_graph, fn, reps, warm=2, soak=0.05):
+    g, st = time_graph(torch, fn, reps, warm, soak_s=soak)
+    with torch.cuda.stream(st):
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(st)
+        g.replay()
+        b_.record(st)
+        b_.synchronize()
+    del g
+    return a_.elapsed_time(b_) / reps
+
+
+def spot_check(P, torch, dev, u, spec, blk, mask0):
+    """One public-API step (in place) on a pristine seeded frame vs the fp32 oracle."""
+    import numpy as np
+    from oracle import sbnet_oracle as O
+    from paper_1801_02108_b200.layers import sparse_residual_unit_into
+    x0 = torch.from_numpy(np.random.default_rng(1000).standard_normal((1, H, W, C), dtype=np.float32)).bfloat16()
+    y = x0.to(dev)
+    sparse_residual_unit_into(y, y, mask0.data, u, spec)
+    got = y.float().cpu().numpy()
+    ud = _oracle_unit(u)
+    r = lambda a: torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()  # noqa: E731
+    for i in (1, 2, 3):
+        ud[f"w{i}"], ud[f"b{i}"] = r(ud[f"w{i}"]), r(ud[f"b{i}"])
+    ref = O.sparse_residual_unit(x0.float().numpy(), mask0.numpy(), ud, blk)
+    err = O.rel_err(got, ref)
+    return {"what": "one in-place step on a pristine frame vs the fp32 oracle (bf16-rounded weights)",
+            "finite": bool(np.isfinite(got).all()), "rel_err": float(f"{err:.3e}"), "tolerance": 2e-2,
+            "ok": bool(np.isfinite(got).all() and err <= 2e-2)}
+
+
+def run_fp32(P, torch, dev, time_graph, u, mask10):
+    """fp32 paths (the reference's precision, tensor.py:31-32): BASELINE config 1 (reduce_mask
+    -> gather -> 3x3 conv -> scatter, 64x64x16, 12 of 25 blocks, as tests/golden/config1.npz)
+    and the config-2 unit (400x400x64, 10% blobs) on the SIMT kernels, CUDA graphs over rings
+    of distinct frames."""
+    import numpy as np
+    from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_masked_into, sparse_residual_unit_into, \
+        residual_unit_algo
+    z = np.load(os.path.join(ROOT, "tests", "golden", "config1.npz"))
+    p = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 16)
+    spec1 = P.compute_block_spec((1, 64, 64, 16), p, (16, 16))
+    fb = P.FilterBank(z["w"], z["b"])
+    nfr = 64
+    xs1 = [torch.randn(1, 64, 64, 16, device=dev) for _ in range(nfr)]
+    m1 = torch.from_numpy(z["mask"]).to(dev)
+    out1 = torch.zeros(1, 64, 64, 16, device=dev)
+    t1 = _timed_graph(torch, time_graph, lambda k: [sparse_conv_masked_into(xs1[i % nfr], out1, m1, fb, p, spec1)
+                                                    for i in range(k)], 400)
+    nb1 = int(P.reduce_mask(P.BinaryMask(z["mask"]), spec1).count)
+    f1 = nb1 * 2 * 14 * 14 * 9 * 16 * 16
+    b1 = (nb1 * 256 * 16 + nb1 * 196 * 16) * 4
+    spec2 = P.unit_spec((1, H, W, C), (16, 16))
+    nf2 = 8
+    xs2 = [torch.randn(1, H, W, C, device=dev) for _ in range(nf2)]
+    t2 = _timed_graph(torch, time_graph, lambda k: [sparse_residual_unit_into(xs2[i % nf2], xs2[i % nf2], mask10.data,
+                                                                              u, spec2) for i in range(k)], 40)
+    b2 = unit_bytes(P, spec2, P.reduce_mask(mask10, spec2).entries, es=4) + H * W
+    return {"config1": {"workload": "config1: 3x3 SAME conv, 64x64x16 fp32, block 16, 12/25 blocks (golden case)",
+                        "algo": sparse_conv_algo(torch.float32, fb, p, spec1), "blocks": nb1, "ms": round(t1, 5),
+                        "frames_per_s": round(1e3 / t1, 1), "gflops_alg": round(f1 / (t1 * 1e-3) / 1e9, 1),
+                        "GBps_alg": round(b1 / (t1 * 1e-3) / 1e9, 1)},
+            "config2_unit_fp32": {"workload": f"config2 unit in fp32: N=1 {H}x{W}x{C}, 10% blobs, 16x16, in place",
+                                  "algo": residual_unit_algo(torch.float32, u, spec2), "ms": round(t2, 5),
+                                  "frames_per_s": round(1e3 / t2, 1), "GBps_alg": round(b2 / (t2 * 1e-3) / 1e9, 1)}}
+
+
+def run_reduce_mask_bw(P, torch, dev, time_graph, hbm_peak):
+    """sbn_reduce_mask on N=64 x 800x700 uint8 masks (35.8 MB: config 5's batch), 16x16 unit
+    blocks, 20% blobs: algorithmic bytes = n*h*w mask bytes + 12 B per active block."""
+    import ctypes as Cc
+    from paper_1801_02108_b200 import _lib
+    lib = _lib.load()
+    n, h, w = 64, 800, 700
+    mk = P.synth_mask_blobs((n, h, w), 0.8, 5).cuda()
+    spec = P.unit_spec((n, h, w, 32), (16, 16))
+    g = spec.c_geometry(n)
+    cap = n * spec.grid_count[0] * spec.grid_count[1]
+    rows = torch.empty((cap, 3), dtype=torch.int32, device=dev)
+    cnt = torch.empty((1,), dtype=torch.int32, device=dev)
+    ws = torch.zeros(max(int(lib.sbn_reduce_mask_workspace(Cc.byref(g))), 4096), dtype=torch.uint8, device=dev)
+    thr = 1.0 / 256
+
+    def rm(k):
+        for _ in range(k):
+            _lib.check(lib.sbn_reduce_mask(mk.data.data_ptr(), Cc.byref(g), _lib.SBN_POOL_MAX, thr, rows.data_ptr(),
+                                           cnt.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle(dev)),
+                       "reduce_mask")
+    t = _timed_graph(torch, time_graph, rm, 50)
+    nb = int(cnt.item())
+    byts = n * h * w + 12 * nb
+    import numpy as np
+    same = bool(np.array_equal(rows[:nb].cpu().numpy().astype(np.int64), P.reduce_mask(mk, spec).entries))
+    return {"workload": "reduce_mask, N=64 x 800x700 u8 masks (20% blobs), 16x16 unit blocks (MAX)",
+            "blocks": nb, "indices_match_public_api": same, "ms": round(t, 5), "alg_bytes": byts, "GBps": round(byts / (t * 1e-3) / 1e9, 1),
+            "hbm_frac": round(byts / (t * 1e-3) / 1e9 / hbm_peak, 4)}
 
 
 def run_gather_scatter(P, torch, dev, time_graph, hbm_peak):
@@ -817,9 +987,27 @@ def run_conv_sweep(P, torch, dev, time_graph):
         for i in range(k):
             dense_conv_nhwc(xs[i % nfr], wd, None, (1, 1), (1, 1))
     dense_ms = timed(dense)
+    from paper_1801_02108_b200.ops import projection_conv
+
+    def dense_own(k):  # this repo's tcgen05 TMA tap-GEMM conv over the full frame (bias fused)
+        for i in range(k):
+            projection_conv(xs[i % nfr], fb, p)
+    dense_own_ms = timed(dense_own)
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        peaks = {}
+    tpeak = peaks.get("bf16_tflops", 1665.5)
+    fd = 2 * Hc * Wc * 9 * Cc * Cc
+    best_dense = min(dense_ms, dense_own_ms)
     res = {"workload": "config3: 3x3 SAME conv, N=1 800x700x128 bf16, top-left mask", "dense_ms": round(dense_ms, 5),
            "dense": "cuDNN bf16 conv, channels-last, bias omitted (lower bound of the dense layer)",
-           "flops_dense": 2 * Hc * Wc * 9 * Cc * Cc, "rows": []}
+           "dense_own_ms": round(dense_own_ms, 5),
+           "dense_own": "this repo's tcgen05 tap-GEMM conv (conv_dense_tc.cu) over the full frame, bias fused",
+           "dense_frac": round(fd / (dense_ms * 1e-3) / 1e12 / tpeak, 4),
+           "dense_own_frac": round(fd / (dense_own_ms * 1e-3) / 1e12 / tpeak, 4),
+           "peak_tflops": tpeak, "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else "fallback",
+           "flops_dense": fd, "rows": []}
     for d in (0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 0.9, 1.0):
         mk = P.synth_mask_topleft((1, Hc, Wc), 1.0 - d).cuda()
         for blk in (8, 16, 32):
@@ -834,7 +1022,9 @@ def run_conv_sweep(P, torch, dev, time_graph):
             flops = nb * 2 * spec.out_block_size[0] * spec.out_block_size[1] * 9 * Cc * Cc
             res["rows"].append({"density": d, "block": blk, "blocks": int(nb), "algo": algo,
                                 "sparse_ms": round(t, 5), "speedup_vs_dense": round(dense_ms / t, 3),
-                                "tflops_alg": round(flops / (t * 1e-3) / 1e12, 1)})
+                                "speedup_vs_best_dense": round(best_dense / t, 3),
+                                "tflops_alg": round(flops / (t * 1e-3) / 1e12, 1),
+                                "frac": round(flops / (t * 1e-3) / 1e12 / tpeak, 4)})
     # the autotuner's choice (reference perf.py:167-195: fastest candidate, ties toward the
     # smaller block) per density, from the same CUDA-graph timings
     best = {}
@@ -843,29 +1033,75 @@ def run_conv_sweep(P, torch, dev, time_graph):
         if k not in best or (r["sparse_ms"], r["block"]) < (best[k]["sparse_ms"], best[k]["block"]):
             best[k] = r
     res["autotuned_block"] = {k: {"block": v["block"], "sparse_ms": v["sparse_ms"],
-                                  "speedup_vs_dense": v["speedup_vs_dense"]} for k, v in best.items()}
+                                  "speedup_vs_dense": v["speedup_vs_dense"],
+                                  "speedup_vs_best_dense": v["speedup_vs_best_dense"], "frac": v["frac"]}
+                              for k, v in best.items()}
     return res
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_pkg():
+    """The UNMODIFIED reference package (`blockconv`), pip-installed into baseline/_ref
+    (DESIGN.md §4 records the install), or None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "blockconv")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import blockconv
+    return blockconv
+
+
+def _time_reference_unit(bc, x, mk, blk, seconds, max_iters=None):
+    """The reference's own sparse_residual_unit through its public API, timed by its own
+    benchmark_layer (perf.py:139-154): 1 warm-up, then as many iterations as fill `seconds`
+    (one probe call sizes the sample)."""
+    import numpy as np
+    u = bc.random_unit_params(np.random.default_rng(0), C, M)  # same draws as the bench's unit
+    xr, mr = bc.Tensor4D(np.ascontiguousarray(x)), bc.BinaryMask(mk)
+    fn = lambda: bc.sparse_residual_unit(xr, mr, u, blk)  # noqa: E731
+    t0 = time.perf_counter()
+    fn()
+    probe = time.perf_counter() - t0
+    iters = max(3, int(seconds / max(probe, 1e-6)))
+    if max_iters:
+        iters = min(iters, max_iters)
+    r = bc.benchmark_layer(fn, warmup=1, iters=iters)
+    return r, u
+
+
 def cpu_baseline(seconds, x_dev, mask, u, blk):
-    """Oracle port of the reference sparse_residual_unit (numpy, all host threads) on a
-    bounded sample: the same frame repeated until `seconds` elapse."""
+    """The reference's CPU path on the box's host cores, same frame / mask / unit: the real
+    reference from baseline/_ref when installed (kind "reference"), and the oracle port
+    (numpy restatement, kind "port") timed beside it on a bounded sample."""
     import numpy as np
     from oracle import sbnet_oracle as O
     x = x_dev.float().cpu().numpy()
     mk = mask.numpy()
+    cores = len(os.sched_getaffinity(0))
     ud = _oracle_unit(u)
+    half = seconds / 2
     t0 = time.perf_counter()
     n = 0
     while True:
         O.sparse_residual_unit(x, mk, ud, blk)
         n += 1
-        if time.perf_counter() - t0 >= seconds:
+        if time.perf_counter() - t0 >= half:
             break
     el = time.perf_counter() - t0
-    cores = len(os.sched_getaffinity(0))
-    return {"value": round(n / el, 3), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{n} x sparse_residual_unit on one {H}x{W}x{C} frame (fp32, bf16-rounded inputs), {el:.1f}s"}
+    port = {"value": round(n / el, 3), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{n} x oracle sparse_residual_unit on one {H}x{W}x{C} frame (fp32, bf16-rounded inputs), {el:.1f}s"}
+    bc = _reference_pkg()
+    if bc is None:
+        return port
+    r, ur = _time_reference_unit(bc, x, mk, blk, half)
+    assert np.array_equal(ur.conv2.weights, u.conv2.weights), "reference unit draws differ"
+    return {"value": round(1e9 / r.mean_ns, 3), "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{r.timed_iters} x blockconv.sparse_residual_unit (baseline/_ref, unmodified) on one "
+                      f"{H}x{W}x{C} frame, fp32 (bf16-rounded inputs), benchmark_layer mean "
+                      f"{r.mean_ns / 1e6:.2f} ms (std {r.std_ns / 1e6:.2f}, min {r.min_ns / 1e6:.2f})",
+            "port": port}
 
 
 def _oracle_unit(u):
@@ -877,14 +1113,16 @@ def _oracle_unit(u):
 
 
 def run_reference(args):
-    """Reference arm: the reference's CPU algorithm (oracle port; the reference itself is
-    pure Python and cannot travel to the box) on the host cores, same workload/metric."""
+    """Reference arm: the UNMODIFIED reference (`blockconv` from baseline/_ref, pure Python +
+    numpy) through its public sparse_residual_unit, timed by its own benchmark_layer on the
+    host cores, same workload/metric.  The oracle port (numpy restatement) is timed beside it
+    and reported under "port"; when baseline/_ref is absent the port is the arm."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
     ncores = len(os.sched_getaffinity(0))
     for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ[v] = str(ncores)
+        os.environ[v] = str(ncores)  # before numpy loads (reference cli.py:103-107)
     import numpy as np
     from oracle import sbnet_oracle as O
     import paper_1801_02108_b200.perf as perf
@@ -903,15 +1141,26 @@ def run_reference(args):
     for _ in range(steps):
         O.sparse_residual_unit(x, mk, ud, blk)
     el = time.perf_counter() - t0
-    v = steps / el
+    port = {"value": round(steps / el, 3), "unit": UNIT, "cores": ncores, "kind": "port",
+            "ms_per_step": round(el / steps * 1e3, 3),
+            "sample": f"{steps} oracle steps (requested {args.steps}, capped at 60 for runtime)"}
+    bc = _reference_pkg()
+    if bc is not None:
+        r, _ = _time_reference_unit(bc, x, mk, blk, seconds=1e9, max_iters=steps)
+        v, ms, kind = 1e9 / r.mean_ns, r.mean_ns / 1e6, "reference"
+        sample = (f"{r.timed_iters} x blockconv.sparse_residual_unit (baseline/_ref, unmodified) after 1 warm-up, "
+                  f"benchmark_layer mean {ms:.2f} ms (std {r.std_ns / 1e6:.2f}, min {r.min_ns / 1e6:.2f}); "
+                  f"requested {args.steps} steps, capped at 60 for runtime")
+    else:
+        v, ms, kind, sample = port["value"], port["ms_per_step"], "port", port["sample"]
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
             "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": steps, "warmup": warm,
-            "ms_per_step": round(el / steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"config2: sparse ResNet bottleneck unit, N=1 {H}x{W}x{C}, "
                                    f"{args.density:.0%} blob mask, {blk[0]}x{blk[1]} blocks (CPU, numpy)"},
-            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": ncores, "kind": "port",
-                             "sample": f"{steps} steps (requested {args.steps}, capped at 60 for runtime)"},
+            "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": ncores, "kind": kind, "sample": sample},
+            "port": port,
             "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

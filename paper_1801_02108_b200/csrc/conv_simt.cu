@@ -5,33 +5,49 @@
 // precision path (fp32 FFMA / fp64 DFMA) used for the reference's 1e-5..1e-4 parity
 // tolerances; the bf16 tensor-core path is conv_tc.cu.
 //
-// One persistent CTA per active block (reads the device-side block count): the input
-// window is staged once in shared memory with zero-filled halo (the gather of
-// `blocks.py:57-74`), each thread produces (pixel, cout) outputs with the per-tap
-// accumulation order of `ops.py:145-164`, and results are stored straight into the
-// block's clipped, disjoint output window (the scatter of `blocks.py:125-142`).
+// Work item = (active block, output slice): a block's obh*obw*cout outputs are split over
+// `splits` CTAs so small batches still fill the GPU (config 1: 12 blocks x 6 slices).  Each
+// CTA stages the block's input window once in shared memory with zero-filled halo (the
+// gather of `blocks.py:57-74`) and, when they fit, the whole filter bank (staged once per
+// CTA; both operands then come from shared memory: a warp's threads read consecutive
+// output channels of one pixel, so weight reads are conflict-free and window reads are
+// broadcasts).  Each output keeps the per-tap accumulation order of `ops.py:145-164`
+// (sum over input channels per tap, taps added in (i, j) order, bias last) and is stored
+// straight into the block's clipped, disjoint output window (the scatter of
+// `blocks.py:125-142`).  Persistent grid over the items (device-side block count).
 #include "common.cuh"
 
 namespace sbn {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr size_t kWeightSmemMax = 64 * 1024;  // stage the filter bank when it fits next to the window
 
-template <typename T, bool SMEM>
+template <typename T, bool SMEM, bool WSMEM>
 __global__ void __launch_bounds__(kThreads)
 sparse_conv_simt_kernel(const T* __restrict__ x, Geo g, int cin, int cout, int kh, int kw, int sh,
                         int sw, const T* __restrict__ w, const T* __restrict__ bias,
                         const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
-                        int cap, T* __restrict__ dst) {
+                        int cap, T* __restrict__ dst, int splits) {
   using A = typename Acc<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   A* win = reinterpret_cast<A*>(smem_raw);
+  const int win_elems = SMEM ? g.bh * g.bw * cin : 0;
+  A* wts = win + win_elems;
+  if (WSMEM) {  // filter bank (HWIO), once per CTA
+    const int nw = kh * kw * cin * cout;
+    for (int e = threadIdx.x; e < nw; e += kThreads) wts[e] = to_acc(__ldg(w + e));
+    // (made visible by the __syncthreads after the first window)
+  }
   const int B = ld_count(count, cap);
-  const int win_elems = g.bh * g.bw * cin;
-  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+  const int total = g.obh * g.obw * cout;
+  int staged = -1;  // block whose window is in smem
+  for (int it = blockIdx.x; it < B * splits; it += gridDim.x) {
+    const int b = it / splits, sl = it - b * splits;
     const int n = __ldg(idx + 3 * b), by = __ldg(idx + 3 * b + 1), bx = __ldg(idx + 3 * b + 2);
     const int ys = g.oy + by * g.sy, xs = g.ox + bx * g.sx;
-    if (SMEM) {
+    if (SMEM && staged != b) {
+      if (staged >= 0) __syncthreads();  // previous block's reads are done
       for (int e = threadIdx.x; e < win_elems; e += kThreads) {
         const int ci = e % cin;
         const int p = e / cin;
@@ -43,9 +59,12 @@ sparse_conv_simt_kernel(const T* __restrict__ x, Geo g, int cin, int cout, int k
         win[e] = v;
       }
       __syncthreads();
+      staged = b;
+    } else if (WSMEM && !SMEM && staged < 0) {
+      __syncthreads();
+      staged = b;
     }
-    const int total = g.obh * g.obw * cout;
-    for (int o = threadIdx.x; o < total; o += kThreads) {
+    for (int o = sl * kThreads + threadIdx.x; o < total; o += splits * kThreads) {
       const int co = o % cout;
       const int p = o / cout;
       const int oyb = p / g.obw, oxb = p - oyb * g.obw;
@@ -56,17 +75,25 @@ sparse_conv_simt_kernel(const T* __restrict__ x, Geo g, int cin, int cout, int k
         const int wy = oyb * sh + i;
         for (int j = 0; j < kw; ++j) {
           const int wx = oxb * sw + j;
-          const T* wp = w + ((size_t)(i * kw + j) * cin) * cout + co;
+          const size_t wo = ((size_t)(i * kw + j) * cin) * cout + co;
           A tap = A(0);
           if (SMEM) {
             const A* xp = win + (wy * g.bw + wx) * cin;
-            for (int ci = 0; ci < cin; ++ci) tap += xp[ci] * to_acc(__ldg(wp + (size_t)ci * cout));
+            if (WSMEM) {
+              const A* wp = wts + wo;
+#pragma unroll 4
+              for (int ci = 0; ci < cin; ++ci) tap += xp[ci] * wp[(size_t)ci * cout];
+            } else {
+              const T* wp = w + wo;
+#pragma unroll 4
+              for (int ci = 0; ci < cin; ++ci) tap += xp[ci] * to_acc(__ldg(wp + (size_t)ci * cout));
+            }
           } else {
             const int y = ys + wy, xx = xs + wx;
             if (y < 0 || y >= g.h || xx < 0 || xx >= g.w) continue;
             const T* xp = x + (((size_t)n * g.h + y) * g.w + xx) * cin;
             for (int ci = 0; ci < cin; ++ci)
-              tap += to_acc(__ldg(xp + ci)) * to_acc(__ldg(wp + (size_t)ci * cout));
+              tap += to_acc(__ldg(xp + ci)) * (WSMEM ? wts[wo + (size_t)ci * cout] : to_acc(__ldg(w + wo + (size_t)ci * cout)));
           }
           acc += tap;
         }
@@ -74,8 +101,17 @@ sparse_conv_simt_kernel(const T* __restrict__ x, Geo g, int cin, int cout, int k
       if (bias) acc += to_acc(__ldg(bias + co));
       dst[(((size_t)n * g.oh + Y) * g.ow + X) * cout + co] = from_acc<T>(acc);
     }
-    if (SMEM) __syncthreads();
   }
+}
+
+template <typename T, bool SMEM, bool WSMEM>
+void launch_conv_simt_variant(size_t smem, int grid, cudaStream_t s, const void* x, Geo g, int cin, int cout, int kh,
+                              int kw, int sh, int sw, const void* w, const void* bias, const int32_t* idx,
+                              const int32_t* count, int cap, void* dst, int splits) {
+  auto k = sparse_conv_simt_kernel<T, SMEM, WSMEM>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, kThreads, smem, s>>>((const T*)x, g, cin, cout, kh, kw, sh, sw, (const T*)w, (const T*)bias, idx, count,
+                                 cap, (T*)dst, splits);
 }
 
 template <typename T>
@@ -83,17 +119,27 @@ int launch_conv_simt(const void* x, int cin, int cout, int kh, int kw, int sh, i
                      const void* w, const void* bias, const int32_t* idx, const int32_t* count,
                      int cap, void* dst, cudaStream_t s) {
   using A = typename Acc<T>::type;
-  const size_t smem = (size_t)g.bh * g.bw * cin * sizeof(A);
-  const int grid = persistent_grid(cap, 4);
-  if (smem <= 96 * 1024) {
-    auto k = sparse_conv_simt_kernel<T, true>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, kThreads, smem, s>>>((const T*)x, g, cin, cout, kh, kw, sh, sw, (const T*)w,
-                                   (const T*)bias, idx, count, cap, (T*)dst);
+  const size_t win_b = (size_t)g.bh * g.bw * cin * sizeof(A);
+  const size_t w_b = (size_t)kh * kw * cin * cout * sizeof(A);
+  // slices per block: about two outputs per thread, at most 16 CTAs per block
+  const long total = (long)g.obh * g.obw * cout;
+  int splits = (int)((total + 2 * kThreads - 1) / (2 * kThreads));
+  splits = splits < 1 ? 1 : splits > 16 ? 16 : splits;
+  const int grid = persistent_grid((int)((long)cap * splits < (1L << 30) ? (long)cap * splits : (1L << 30)), 4);
+  const bool wsm = w_b <= kWeightSmemMax;
+  if (win_b + (wsm ? w_b : 0) <= 96 * 1024) {
+    if (wsm)
+      launch_conv_simt_variant<T, true, true>(win_b + w_b, grid, s, x, g, cin, cout, kh, kw, sh, sw, w, bias, idx,
+                                              count, cap, dst, splits);
+    else
+      launch_conv_simt_variant<T, true, false>(win_b, grid, s, x, g, cin, cout, kh, kw, sh, sw, w, bias, idx,
+                                               count, cap, dst, splits);
+  } else if (wsm) {
+    launch_conv_simt_variant<T, false, true>(w_b, grid, s, x, g, cin, cout, kh, kw, sh, sw, w, bias, idx, count, cap,
+                                             dst, splits);
   } else {
-    sparse_conv_simt_kernel<T, false><<<grid, kThreads, 0, s>>>(
-        (const T*)x, g, cin, cout, kh, kw, sh, sw, (const T*)w, (const T*)bias, idx, count, cap,
-        (T*)dst);
+    launch_conv_simt_variant<T, false, false>(0, grid, s, x, g, cin, cout, kh, kw, sh, sw, w, bias, idx, count, cap,
+                                              dst, splits);
   }
   return launch_status("sparse_conv_simt");
 }
