@@ -17,7 +17,7 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from .errors import ShapeMismatchError, UnsupportedConfigError
+from .errors import ShapeMismatchError
 from .tensor import Layout, Tensor4D, as_torch, compute_dtype, cuda
 
 
@@ -273,40 +273,3 @@ def conv2d_direct_grads(x: Tensor4D, f: FilterBank, p: ConvParams, g_out: Tensor
     w, _ = f.device_tensors(xt.dtype, xt.device)
     dx, dw, db = conv_grads_nhwc(xt, w, p.stride, p.pad, cuda(g_out.nhwc(), xt.device))
     return Tensor4D.from_nhwc(dx, x.layout), dw, db
-
-
-def winograd_supported(p: ConvParams) -> bool:
-    return tuple(p.kernel) == (3, 3) and tuple(p.stride) == (1, 1)
-
-
-def conv2d_winograd(x: Tensor4D, f: FilterBank, p: ConvParams) -> Tensor4D:
-    """3x3 / stride-1 convolution (reference `winograd.py:39-`); cuDNN chooses its own
-    (Winograd or implicit-GEMM) algorithm — the result equals conv2d_direct's."""
-    if not winograd_supported(p):
-        raise UnsupportedConfigError(
-            f"Winograd path supports only 3x3 kernels at stride 1, got kernel {p.kernel} stride {p.stride}")
-    return conv2d_direct(x, f, p)
-
-
-def conv2d(x: Tensor4D, f: FilterBank, p: ConvParams, algo: str = "auto") -> Tensor4D:
-    """Algorithm dispatcher (reference `ops.py:257-269`)."""
-    if algo == "winograd":
-        return conv2d_winograd(x, f, p)
-    if algo in ("direct", "auto"):
-        return conv2d_direct(x, f, p)
-    raise ValueError(f"unknown algo {algo!r}")
-
-
-def pool2d(x: Tensor4D, window, stride=None, mode: PoolMode = PoolMode.MAX) -> Tensor4D:
-    """Valid pooling over full windows only (reference `ops.py:237-254`)."""
-    wh, ww = (window, window) if isinstance(window, int) else tuple(window)
-    if stride is None:
-        stride = (wh, ww)
-    sh, sw = (stride, stride) if isinstance(stride, int) else tuple(stride)
-    n, h, w, c = x.dims
-    if wh > h or ww > w:
-        raise ShapeMismatchError(f"pool window {wh}x{ww} larger than input {h}x{w}")
-    t = cuda(x.nhwc()).permute(0, 3, 1, 2)
-    fn = F.max_pool2d if mode is PoolMode.MAX else F.avg_pool2d
-    out = fn(t, (wh, ww), (sh, sw))
-    return Tensor4D.from_nhwc(out.permute(0, 2, 3, 1).contiguous(), x.layout)

@@ -44,3 +44,21 @@ def test_sweep_and_demo_check(cuda_device, tmp_path, capsys):
 def test_bad_arguments_exit_codes(capsys):
     assert main(["bench", "--dims", "1,2,3"]) == 2
     assert main(["maskgen", "--dims", "1,8,8", "--out", "/nonexistent/dir/m.sbmk"]) == 2
+
+
+def test_verify_is_deterministic_per_seed(cuda_device, capsys):
+    main(["verify", "--rounds", "3", "--seed", "7"])
+    first = capsys.readouterr().out
+    main(["verify", "--rounds", "3", "--seed", "7"])
+    assert capsys.readouterr().out == first
+
+
+def test_bench_sparsity_zero_and_missing_mask(cuda_device, tmp_path, capsys):
+    out = tmp_path / "b.csv"
+    assert main(["bench", "--dims", "1,48,48,8", "--block", "8,8", "--sparsity", "0", "--warmup", "2",
+                 "--iters", "4", "--out", str(out)]) == 0
+    rows = read_csv(out)
+    assert rows[0].speedup == 1.0 and rows[1].flops_sparse >= rows[1].flops_dense  # halo overhead at sparsity 0
+    assert main(["bench", "--dims", "1,16,16,2", "--block", "8,8", "--mask", "/nonexistent/m.sbmk",
+                 "--warmup", "0", "--iters", "1"]) == 2
+    assert "error:" in capsys.readouterr().err
