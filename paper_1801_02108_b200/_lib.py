@@ -12,7 +12,8 @@ import threading
 from .errors import (BlockConvError, GeometryError, ShapeMismatchError, UnsupportedConfigError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsbnet.so")
+# SBN_LIB_PATH: load an alternative build (A/B experiments of compile-time variants, tools/)
+LIB_PATH = os.environ.get("SBN_LIB_PATH") or os.path.join(_HERE, "libsbnet.so")
 
 SBN_F32, SBN_F64, SBN_BF16 = 0, 1, 2
 SBN_POOL_MAX, SBN_POOL_AVG = 0, 1
