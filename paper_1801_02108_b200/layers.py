@@ -738,7 +738,7 @@ def build_stage(cfg: StageConfig, rng: np.random.Generator, dtype=np.float32,
 
 def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
               bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True,
-              _mask_at_scale: BinaryMask | None = None) -> StageResult:
+              _mask_at_scale: BinaryMask | None = None, _plan=None) -> StageResult:
     """Dense stride-s projection (tcgen05, bias fused), then residual units sharing ONE
     index list computed from the downsampled mask (reference `layers.py:311-329`).  The
     units run in place on the stage's private activation buffer (one clone at most)."""
@@ -757,11 +757,17 @@ def run_stage(stage: Stage, x: Tensor4D, base_mask: BinaryMask | None, sparse: b
             t = (_dense_unit_bf16(t, u) if (dense_fused and t.dtype == torch.bfloat16 and u.pre_activation)
                  else t + _dense_branch(t, u))
         return StageResult(Tensor4D.from_nhwc(t, x.layout), None, None, None)
-    mask = _mask_at_scale if _mask_at_scale is not None else downsample_mask(base_mask, cfg.mask_scale)
+    if _plan is not None:  # mask, spec and index list prepared ahead (run_backbone's side stream)
+        mask, spec, idx, ready = _plan
+        torch.cuda.current_stream(t.device).wait_event(ready)
+    else:
+        mask = _mask_at_scale if _mask_at_scale is not None else downsample_mask(base_mask, cfg.mask_scale)
+        spec = None
     if mask.dims != tuple(t.shape[:3]):
         raise ShapeMismatchError(f"mask dims {mask.dims} != tensor (n, h, w) {tuple(t.shape[:3])}")
-    spec = unit_spec(tuple(t.shape), cfg.block_size, halo=1)
-    idx = reduce_mask(mask, spec, PoolMode.MAX)
+    if spec is None:
+        spec = unit_spec(tuple(t.shape), cfg.block_size, halo=1)
+        idx = reduce_mask(mask, spec, PoolMode.MAX)
     if not owned:
         t = t.clone()
     for u in stage.units:
@@ -784,20 +790,74 @@ def build_backbone(stage_cfgs, rng: np.random.Generator, dtype=np.float32,
     return Backbone(tuple(build_stage(cfg, rng, dtype, scale) for cfg in stage_cfgs))
 
 
+class _SideStreams(threading.local):
+    """One side stream per device for the backbone's mask pipeline."""
+
+    def __init__(self):
+        self.s = {}
+
+    def get(self, device) -> torch.cuda.Stream:
+        key = str(device)
+        if key not in self.s:
+            self.s[key] = torch.cuda.Stream(device=device)
+        return self.s[key]
+
+
+_SIDE = _SideStreams()
+
+
+def _stage_out_hw(stage: Stage, h: int, w: int) -> tuple[int, int]:
+    s = stage.config.stride if stage.projection is not None else 1
+    return (h - 1) // s + 1, (w - 1) // s + 1  # SAME 3x3 stride-s projection
+
+
+def _mask_plans(bb: Backbone, x: Tensor4D, base_mask: BinaryMask):
+    """Every stage's downsampled mask, unit geometry and index list, computed on a side
+    stream while the main stream runs the stages: the masks depend only on the base mask,
+    so the mask kernels (latency-bound, a few SMs) overlap the projections and units
+    instead of sitting between them.  Max-pool downsampling composes exactly (ceil dims,
+    window = stride): each stage's mask comes from the previous stage's when the scale
+    ratio is an integer, reading the small mask instead of the full-resolution one."""
+    main = torch.cuda.current_stream()
+    side = _SIDE.get(main.device)
+    side.wait_stream(main)  # the base mask (and x) are ready
+    plans = []
+    n, h, w, _ = x.dims
+    prev_scale, prev_mask = 1, base_mask
+    with torch.cuda.stream(side):
+        for stage in bb.stages:
+            h, w = _stage_out_hw(stage, h, w)
+            sc = stage.config.mask_scale
+            if sc % prev_scale == 0:
+                m_s = downsample_mask(prev_mask, sc // prev_scale)
+                prev_scale, prev_mask = sc, m_s
+            else:
+                m_s = downsample_mask(base_mask, sc)
+            if m_s.dims != (n, h, w):
+                raise ShapeMismatchError(f"mask dims {m_s.dims} != stage tensor (n, h, w) {(n, h, w)}")
+            spec = unit_spec((n, h, w, stage.config.channels[2]), stage.config.block_size, halo=1)
+            idx = reduce_mask(m_s, spec, PoolMode.MAX)
+            for t_ in (m_s.data, idx.rows, idx.count_dev):  # consumed on the main stream
+                if isinstance(t_, torch.Tensor) and t_.is_cuda:
+                    t_.record_stream(main)
+            ready = torch.cuda.Event()
+            ready.record(side)
+            plans.append((m_s, spec, idx, ready))
+    return plans
+
+
 def run_backbone(bb: Backbone, x: Tensor4D, base_mask: BinaryMask | None, sparse: bool = True,
                  bn_mode: BnMode = BnMode.INFERENCE, algo="auto", dense_fused: bool = True) -> list[StageResult]:
+    """Stages in sequence (reference `layers.py:346-353`); the sparse path prepares every
+    stage's mask and index list up front on a side stream (_mask_plans)."""
+    plans = [None] * len(bb.stages)
+    if sparse and base_mask is not None and bb.stages:
+        xt = cuda(x.nhwc())
+        plans = _mask_plans(bb, Tensor4D.from_nhwc(xt, x.layout), BinaryMask(cuda(base_mask.data), validate=False))
+        x = Tensor4D.from_nhwc(xt, x.layout)
     results = []
-    prev_scale, prev_mask = 1, base_mask
-    for stage in bb.stages:
-        # max-pool downsampling composes exactly (ceil dims, window = stride): each stage's
-        # mask comes from the previous stage's mask when the scale ratio is an integer,
-        # reading the small mask instead of the full-resolution one
-        sc = stage.config.mask_scale
-        m_s = None
-        if sparse and base_mask is not None and sc % prev_scale == 0:
-            m_s = downsample_mask(prev_mask, sc // prev_scale)
-            prev_scale, prev_mask = sc, m_s
-        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo, dense_fused, _mask_at_scale=m_s)
+    for stage, plan in zip(bb.stages, plans):
+        res = run_stage(stage, x, base_mask, sparse, bn_mode, algo, dense_fused, _plan=plan)
         results.append(res)
         x = res.output
     return results
