@@ -361,7 +361,21 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   const int B = local ? conv_mask_local<kDbThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
   const int32_t* lidx = local ? s_idx : a.idx;          // (n, by, bx) rows
   const int jfirst = local ? 0 : (int)blockIdx.x, jstep = local ? 1 : (int)gridDim.x;
-  const int NJ = (B + D::BPT - 1) / D::BPT;  // jobs: BPT consecutive blocks of the list
+  // jobs: BPT consecutive blocks of the list.  Tail split (list mode, two M-tiles per
+  // block): when B = q*G + R with 0 < 2R <= G, the last R blocks become 2R half-block jobs
+  // (one M-tile each), so no CTA runs q+1 whole blocks while most run q (config 3 at 10 %,
+  // 16x16: 304 blocks on 148 CTAs = 2.05 rounds -> 2.5 instead of 3 block-times).
+  int NJ = (B + D::BPT - 1) / D::BPT, whole = NJ;
+  if (K::NT == 2 && D::BPT == 1 && !local) {
+    const int R = B % (int)gridDim.x;
+    if (R > 0 && 2 * R <= (int)gridDim.x) {
+      whole = B - R;
+      NJ = whole + 2 * R;
+    }
+  }
+  // first block of a job and the M-tiles it computes (bit t: tile t)
+  auto job_blk = [&](int job) { return job < whole ? job * D::BPT : whole + ((job - whole) >> 1); };
+  auto job_tiles = [&](int job) { return job < whole ? (1 << K::NT) - 1 : 1 << ((job - whole) & 1); };
 
   if (warp == 8) {
     // ---------------- producer: weight taps through the ring
@@ -402,10 +416,12 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
           tc::fence_after();
           const int shift = (tap / 3) * BS + (tap % 3);
           const uint32_t wbase = tc::smem_u32(Wst + s * K::TAP);
+          const int tm = job_tiles(job);
 #pragma unroll
           for (int t = 0; t < K::NT; ++t)
 #pragma unroll
             for (int kk = 0; kk < CIN / 16; ++kk)
+              if (tm >> t & 1)
               tc::mma_bf16(acc + t * COUT,
                            tc::desc_kmajor_noswz(tc::smem_u32(A + 2 * kk * K::PA + (t * 128 + shift) * 16), K::PA, 128),
                            tc::desc_kmajor_noswz(wbase + 2 * kk * K::PW, K::PW, 128), idesc, (tap | kk) > 0);
@@ -434,9 +450,11 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       tc::mbar_wait(&acc_full[b], (kk >> 1) & 1);
       tc::fence_after();
       const uint32_t acc = tmem + b * D::ACC;
+      const int tm = job_tiles(job);
       for (int t = tpar; t < K::NT; t += 2) {
+        if (!(tm >> t & 1)) continue;  // half-block job: the other M-tile is another CTA's
         int r = t * 128 + q * 32 + lane;
-        int blk = job;
+        int blk = job_blk(job);
         if (D::BPT > 1) {  // packed tile: this row belongs to block r / (BS*BS) of the job
           blk = job * D::BPT + r / (BS * BS);
           r %= BS * BS;
@@ -481,7 +499,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
       int jn[D::BPT], jy[D::BPT], jx[D::BPT];
 #pragma unroll
       for (int jb = 0; jb < D::BPT; ++jb) {
-        const int blk = job * D::BPT + jb;
+        const int blk = job_blk(job) + jb;
         jn[jb] = 0, jy[jb] = -(1 << 20), jx[jb] = 0;  // missing block: every pixel out of image
         if (blk < B) {
           jn[jb] = lidx[3 * blk];
@@ -496,7 +514,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
         for (int j = 0; j < CH; ++j) {
           const int i = tid + (base + j) * kWorkers;
           const int jb = D::BPT > 1 ? min(i / PER, D::BPT - 1) : 0, ii = i - jb * PER;
-          const int blk = job * D::BPT + jb;
+          const int blk = job_blk(job) + jb;
           const int p = ii / (CIN / 8), kc = ii % (CIN / 8);
           const int n = jn[jb], ys = jy[jb], xs = jx[jb];
           const int y = ys + p / BS, xx = xs + p % BS;
