@@ -267,6 +267,22 @@ int sbn_debug_last_occupancy(int which);
  * gpu_launches claim). */
 uint64_t sbn_launch_count(void);
 
+/* Convolution gradients (training path; reference `conv2d_grads_nhwc`, `ops.py:167-197`) of
+ * a direct NHWC convolution x (n, h, w, cin) * W (kh, kw, cin, cout), stride (sh, sw),
+ * zero padding (ph, pw), for an upstream gradient g (n, oh, ow, cout):
+ *   sbn_conv_grad_input:  dx (n, h, w, cin) = sum over taps of g . W[i, j]^T (overwritten)
+ *   sbn_conv_grad_weight: dw (kh, kw, cin, cout) and, when db != NULL, db (cout); the sums
+ *     over output positions are deterministic (fixed segments reduced in order), through a
+ *     caller workspace of sbn_conv_grad_weight_workspace bytes.
+ * F32 / F64 / BF16 (accumulated in float / double / float). */
+int sbn_conv_grad_input(const void* g, int dtype, int n, int h, int w, int cin, int oh, int ow, int cout,
+                        const void* wt, int kh, int kw, int sh, int sw, int ph, int pw, void* dx,
+                        sbn_stream_t stream);
+size_t sbn_conv_grad_weight_workspace(int dtype, int n, int oh, int ow, int cin, int cout, int kh, int kw);
+int sbn_conv_grad_weight(const void* x, const void* g, int dtype, int n, int h, int w, int cin, int oh,
+                         int ow, int cout, int kh, int kw, int sh, int sw, int ph, int pw, void* dw,
+                         void* db, void* ws, size_t ws_bytes, sbn_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,9 @@ _PROTOS = {
                                       C.c_size_t, _P, C.c_size_t, _I, _P]),
     "sbn_residual_unit_packed_bytes": (C.c_size_t, [_I, _I, _I, _G, _I, _I]),
     "sbn_residual_unit_packed_variant": (_I, [_I, _I, _I, _G, _I, _I]),
+    "sbn_conv_grad_input": (_I, [_P, _I] + [_I] * 7 + [_P] + [_I] * 6 + [_P, _P]),
+    "sbn_conv_grad_weight_workspace": (C.c_size_t, [_I] * 8),
+    "sbn_conv_grad_weight": (_I, [_P, _P, _I] + [_I] * 13 + [_P, _P, _P, C.c_size_t, _P]),
     "sbn_residual_unit_pack": (_I, [C.POINTER(UnitParams), _I, _I, _I, _G, _I, _I, _P, _P]),
 }
 

@@ -253,17 +253,30 @@ def relu(x: Tensor4D) -> Tensor4D:
 # on cuDNN so a caller switching packages finds them; exact fp32 (no TF32).
 
 def conv_grads_nhwc(a: torch.Tensor, w_hwio: torch.Tensor, stride, pad, g: torch.Tensor):
-    """(dx, dw, db) of a conv on an NHWC tensor for upstream gradient g (reference
-    `ops.py:167-197`): cuDNN data / weight gradients, bias = sum over (n, h, w)."""
-    from torch.nn.grad import conv2d_input, conv2d_weight
-    xin = a.permute(0, 3, 1, 2)
-    go = g.permute(0, 3, 1, 2)
-    w = w_hwio.permute(3, 2, 0, 1).contiguous()
-    with exact_fp32():
-        dx = conv2d_input(tuple(xin.shape), w, go, stride=tuple(stride), padding=tuple(pad))
-        dw = conv2d_weight(xin, tuple(w.shape), go, stride=tuple(stride), padding=tuple(pad))
-    return (dx.permute(0, 2, 3, 1).contiguous(), dw.permute(2, 3, 1, 0).contiguous(),
-            g.sum(dim=(0, 1, 2)))
+    """(dx, dw, db) of a conv on an NHWC CUDA tensor for upstream gradient g (reference
+    `ops.py:167-197`): the native gradient kernels (csrc/conv_grad.cu), deterministic."""
+    import ctypes as C
+    from . import _lib
+    from .tensor import dtype_code
+    lib = _lib.load()
+    a, g = a.contiguous(), g.contiguous()
+    w = w_hwio.to(a.dtype).contiguous()
+    n, h, wd, cin = a.shape
+    kh, kw, _, cout = w.shape
+    oh, ow = g.shape[1], g.shape[2]
+    (sh, sw), (ph, pw) = tuple(stride), tuple(pad)
+    dt, sh_ = dtype_code(a.dtype), _lib.stream_handle(a.device)
+    dx = torch.empty_like(a)
+    _lib.check(lib.sbn_conv_grad_input(g.data_ptr(), dt, n, h, wd, cin, oh, ow, cout, w.data_ptr(), kh, kw, sh, sw,
+                                       ph, pw, dx.data_ptr(), sh_), "conv_grad_input")
+    dw = torch.empty_like(w)
+    db = torch.empty(cout, dtype=a.dtype, device=a.device)
+    ws = torch.empty(int(lib.sbn_conv_grad_weight_workspace(dt, n, oh, ow, cin, cout, kh, kw)), dtype=torch.uint8,
+                     device=a.device)
+    _lib.check(lib.sbn_conv_grad_weight(a.data_ptr(), g.data_ptr(), dt, n, h, wd, cin, oh, ow, cout, kh, kw, sh, sw,
+                                        ph, pw, dw.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(), sh_),
+               "conv_grad_weight")
+    return dx, dw, db
 
 
 def conv2d_direct_grads(x: Tensor4D, f: FilterBank, p: ConvParams, g_out: Tensor4D):

@@ -141,3 +141,31 @@ def test_zero_mask_gives_zero_gradients(cuda_device):
     g_out = P.Tensor4D(rng.standard_normal((1, 12, 12, 2)))
     dx, dw, db = P.sparse_conv2d_grads(x, P.BinaryMask.empty(1, 12, 12), f, p, (6, 6), g_out)
     assert not _np(dx).any() and not _np(dw).any() and not _np(db).any()
+
+
+@pytest.mark.parametrize("dt,tol", [(torch.float64, 1e-12), (torch.float32, 1e-5)])
+def test_native_conv_grads_vs_autograd_and_deterministic(cuda_device, dt, tol):
+    """csrc/conv_grad.cu against torch autograd of F.conv2d (same math), at sizes that
+    split the weight-gradient reduction into several segments; repeated calls bit-identical."""
+    import torch.nn.functional as F
+
+    from paper_1801_02108_b200.ops import conv_grads_nhwc
+    g_ = torch.Generator(device="cuda").manual_seed(0)
+    for (n, h, w, c, co, k, s, p) in ((4, 40, 36, 16, 12, 3, 1, 1), (2, 33, 29, 8, 20, 5, 2, 2), (3, 17, 19, 6, 7, 1, 1, 0)):
+        x = torch.randn(n, h, w, c, device="cuda", dtype=dt, generator=g_)
+        wt = torch.randn(k, k, c, co, device="cuda", dtype=dt, generator=g_)
+        oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        go = torch.randn(n, oh, ow, co, device="cuda", dtype=dt, generator=g_)
+        dx, dw, db = conv_grads_nhwc(x, wt, (s, s), (p, p), go)
+        xr = x.permute(0, 3, 1, 2).clone().requires_grad_()
+        wr = wt.permute(3, 2, 0, 1).clone().requires_grad_()
+        br = torch.zeros(co, device="cuda", dtype=dt, requires_grad=True)
+        torch.backends.cudnn.allow_tf32 = False
+        y = F.conv2d(xr, wr, br, stride=s, padding=p)
+        y.backward(go.permute(0, 3, 1, 2))
+        rel = lambda a, b: float((a - b).abs().max() / b.abs().max())  # noqa: E731
+        assert rel(dx, xr.grad.permute(0, 2, 3, 1)) <= tol
+        assert rel(dw, wr.grad.permute(2, 3, 1, 0)) <= tol
+        assert rel(db, br.grad) <= tol
+        dx2, dw2, db2 = conv_grads_nhwc(x, wt, (s, s), (p, p), go)
+        assert torch.equal(dx, dx2) and torch.equal(dw, dw2) and torch.equal(db, db2)
