@@ -13,6 +13,9 @@ import bench  # noqa: E402
 import paper_1801_02108_b200 as P  # noqa: E402
 from paper_1801_02108_b200.layers import sparse_residual_unit_into  # noqa: E402
 
+from paper_1801_02108_b200 import _lib  # noqa: E402
+
+_lib.load().sbn_debug_set_flags(int(os.environ.get("SBN_FLAGS", 0)))  # kernel-variant A/B
 H, W, C, M = 400, 400, 64, 32
 u = P.random_unit_params(np.random.default_rng(0), C, M)
 spec = P.unit_spec((1, H, W, C), (16, 16))
