@@ -760,3 +760,47 @@ def test_backbone_hierarchical_stage_masks_equal_direct_downsample(cuda_device):
     res = P.run_backbone(bb, x, base)
     for r, c in zip(res, cfgs):
         assert torch.equal(r.mask.data, P.downsample_mask(base, c.mask_scale).data)
+
+
+@pytest.mark.parametrize("block,density", [(16, 0.1), (16, 0.3), (8, 0.1), (32, 0.1)])
+def test_sparse_conv_config3_size_vs_fp32_oracle(cuda_device, block, density):
+    """BASELINE config 3 at full size (1 x 800 x 700 x 128 bf16, 3x3 SAME, top-left mask) through
+    the public sparse_conv2d — the kernels the bench times: several blocks per CTA
+    (double-buffered windows), the half-block tail jobs (16x16 at 30 %: 896 blocks on 148 CTAs),
+    mask-fused lists (8x8) and the TMA tap-GEMM (32x32) — against the fp32 oracle on
+    bf16-rounded inputs (2e-2, north star); inactive pixels exactly zero."""
+    rng = np.random.default_rng(block * 100 + int(density * 10))
+    h, w, c = 800, 700, 128
+    x = torch.from_numpy(rng.standard_normal((1, h, w, c), dtype=np.float32)).bfloat16()
+    wt = torch.from_numpy((rng.standard_normal((3, 3, c, c)) / np.sqrt(9 * c)).astype(np.float32)).bfloat16()
+    bias = torch.from_numpy(rng.standard_normal(c).astype(np.float32)).bfloat16()
+    m = P.synth_mask_topleft((1, h, w), 1.0 - density)
+    p = _conv((3, 3), (1, 1), True, c)
+    y = _np(P.sparse_conv2d(P.Tensor4D(x.cuda()), m.cuda(), P.FilterBank(wt, bias), p, (block, block)))
+    ref = O.sparse_conv2d(x.float().numpy(), m.numpy(), wt.float().numpy(), bias.float().numpy(),
+                          (1, 1), True, (block, block))
+    err = O.rel_err(y, ref)
+    print(f"config 3 block {block} density {density}: rel_err {err:.2e}")
+    assert err <= 2e-2
+    geo = O.geometry(h, w, (3, 3), (1, 1), True, (block, block))
+    reg = O.active_region(geo, O.reduce_mask(m.numpy(), geo), 1)
+    assert np.all(y[~reg] == 0)
+
+
+def test_bf16_scatter_add_vs_oracle(cuda_device):
+    """bf16 scatter in add mode: one bf16 add per element (x + block, rounded once), i.e. the
+    fp32 oracle's sum rounded to bf16; pixels outside the active windows keep dst."""
+    rng = np.random.default_rng(11)
+    x = torch.from_numpy(rng.standard_normal((2, 70, 58, 64)).astype(np.float32)).bfloat16()
+    m = (rng.random((2, 70, 58)) < 0.03).astype(np.uint8)
+    spec = P.compute_block_spec(tuple(x.shape), _conv((3, 3), (1, 1), True, 64), (16, 16))
+    geo = O.geometry(70, 58, (3, 3), (1, 1), True, (16, 16))
+    idx = P.reduce_mask(P.BinaryMask(m), spec)
+    ri = O.reduce_mask(m, geo)
+    assert len(ri) > 0
+    g = P.gather(P.Tensor4D(x), idx, spec)
+    blk = torch.from_numpy(rng.standard_normal((len(ri), 14, 14, 64)).astype(np.float32)).bfloat16()
+    out = P.scatter_add(g.with_tensor(P.Tensor4D(blk)), spec, P.Tensor4D(x))
+    ref = O.scatter(blk.float().numpy(), ri, geo, x.float().numpy(), add=True)
+    ref_bf16 = torch.from_numpy(ref).bfloat16().float().numpy()
+    assert np.array_equal(_np(out), ref_bf16)
