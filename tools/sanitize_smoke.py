@@ -73,5 +73,21 @@ P.sparse_residual_unit(P.Tensor4D(hx), P.BinaryMask(mk.data.cpu().pin_memory()),
 xcf = P.Tensor4D(x.permute(0, 3, 1, 2).contiguous(), P.Layout.CHANNELS_FIRST)
 P.sparse_residual_unit(xcf, mk, u, (16, 16), inplace=True)
 P.sparse_conv2d(xcf, mk, fb, P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 64), (16, 16))
+# round 2: native conv gradients (segmented weight-gradient reduction), the sliced SIMT conv
+# with a staged filter bank (fp32, 12 blocks), the half-block tail jobs of the tcgen05 conv
+# (B % grid small: 2*R <= grid), and the backbone's side-stream mask pipeline
+from paper_1801_02108_b200.ops import conv_grads_nhwc
+xg = torch.randn(3, 40, 36, 8, device=dev, dtype=torch.float64)
+wg = torch.randn(3, 3, 8, 6, device=dev, dtype=torch.float64)
+conv_grads_nhwc(xg, wg, (1, 1), (1, 1), torch.randn(3, 40, 36, 6, device=dev, dtype=torch.float64))
+xs1 = torch.randn(1, 64, 64, 16, device=dev)
+P.sparse_conv2d(P.Tensor4D(xs1), P.synth_mask_blobs((1, 64, 64), 0.5, 3).cuda(), f32, p3, (16, 16))
+xt3 = torch.randn(1, 180, 200, 128, device=dev).bfloat16()  # 195 blocks on 148 CTAs: 47 split
+ft3 = P.FilterBank((torch.randn(3, 3, 128, 128) / 34).bfloat16(), torch.randn(128).bfloat16())
+P.sparse_conv2d(P.Tensor4D(xt3), P.synth_mask_topleft((1, 180, 200), 0.0).cuda(), ft3,
+                P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 128), (16, 16), pool=P.PoolMode.MAX, threshold=1 / 256)
+bb = P.build_backbone([P.StageConfig(1, (8, 12, 24), (16, 16), 1, 1), P.StageConfig(1, (24, 24, 48), (12, 12), 2, 2)],
+                      np.random.default_rng(1))
+P.run_backbone(bb, P.Tensor4D(torch.randn(1, 60, 52, 8, device=dev)), P.synth_mask_blobs((1, 60, 52), 0.7, 2).cuda())
 torch.cuda.synchronize()
 print("sanitize smoke done", flush=True)
