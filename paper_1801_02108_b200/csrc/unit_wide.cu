@@ -63,6 +63,12 @@ constexpr int kBudget = 216 * 1024;
 // K-chunk choice: the largest of {K (<= 96), 64, 32, 16} that keeps ALL weight chunks
 // resident in shared memory next to a 3-deep A ring; 0 when no chunking does (weights
 // are then streamed through a ring).
+// OUT with N <= 96: the residual tiles are prefetched into shared memory by the (otherwise
+// idle) A warps, two tiles ahead of the epilogue.  Wider N would have to give up A-ring depth
+// for the buffers (measured slower at N = 192 with one buffer), so they keep the copy phase.
+constexpr int out_res_bufs(int mode, int n) { return mode != kOut || n > 96 ? 0 : 2; }
+constexpr long out_res_bytes(int mode, int n) { return (long)out_res_bufs(mode, n) * 128L * (n * 2 + 16); }
+
 template <int K, int N, int MODE>
 constexpr int resident_kc() {
   constexpr int taps = MODE == kMid ? 9 : 1;
@@ -76,7 +82,7 @@ constexpr int resident_kc() {
     const int kc = cands[i];
     if (kc > pref || K % kc != 0 || kc % 16 != 0 || (MODE == kIn && kc != 64 && kc != 32)) continue;
     const long ach = (long)(kc / 8) * ra * 16;
-    const long stg = MODE == kOut ? 128L * ((N <= 192 ? N : 128) * 2 + 16) : 0;
+    const long stg = (MODE == kOut ? 128L * ((N <= 192 ? N : 128) * 2 + 16) : 0) + out_res_bytes(MODE, N);
     if (2 * ach + wbytes + 8192 + stg <= kBudget) return kc;
   }
   return 0;
@@ -114,10 +120,13 @@ struct WCfg {
   static constexpr int GS = MODE != kOut ? 0 : (N <= 192 ? N : 128);
   static constexpr int SPITCH = GS * 2 + 16;
   static constexpr int STGB = MODE == kOut ? 128 * SPITCH : 0;
+  static constexpr int NRB = out_res_bufs(MODE, N);      // prefetched residual tiles (OUT)
+  static constexpr bool PF = NRB > 0;
+  static constexpr int RESB = 128 * SPITCH;              // one residual tile, same pitch as stg
   static constexpr int CHUNKS = NKC * TAPS;                       // weight chunks per tile
   static constexpr size_t WBYTES = (size_t)CHUNKS * WCH;          // packed weight bytes
   // resident: A ring as deep as fits (<= 6); streamed: A ring 2..4, W ring 2..4
-  static constexpr int BUD = kBudget - STGB;
+  static constexpr int BUD = kBudget - STGB - NRB * RESB;
   static constexpr int SA = RES ? ((int)((BUD - (long)WBYTES - PARB) / ACH) > 6 ? 6 : (int)((BUD - (long)WBYTES - PARB) / ACH))
                                 : (4 * ACH + 2 * WCH + PARB <= BUD) ? 4 : (3 * ACH + 2 * WCH + PARB <= BUD) ? 3 : 2;
   static constexpr int SW = RES ? 0 : (SA * ACH + 4 * WCH + PARB <= BUD) ? 4 : (SA * ACH + 3 * WCH + PARB <= BUD) ? 3 : 2;
@@ -126,7 +135,8 @@ struct WCfg {
   static constexpr int OFF_W = SA * ACH;
   static constexpr int OFF_PAR = OFF_W + (int)WREG;
   static constexpr int OFF_STG = OFF_PAR + PARB;
-  static constexpr int SMEM = OFF_STG + STGB;
+  static constexpr int OFF_RES = OFF_STG + STGB;
+  static constexpr int SMEM = OFF_RES + NRB * RESB;
   static constexpr int ITEMS = (128 * P + kAThreads / 2 - 1) / (kAThreads / 2);  // IN pieces per thread
 };
 
@@ -220,6 +230,9 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   __shared__ uint64_t acc_full[Q::NACC], acc_empty[Q::NACC];
   __shared__ uint32_t tslot;
   __shared__ long long rowdst[MODE == kOut ? 128 : 1];  // OUT: element offset of a row's pixel, -1 skip
+  constexpr int NRBS = Q::NRB > 0 ? Q::NRB : 1;
+  __shared__ long long rowres[NRBS][Q::PF ? 128 : 1];    // OUT prefetch: row offsets of a buffered tile
+  __shared__ uint64_t res_full[NRBS], res_empty[NRBS];
   uint8_t* Aring = smem;
   uint8_t* Wring = smem + Q::OFF_W;
   float* par = reinterpret_cast<float*>(smem + Q::OFF_PAR);
@@ -237,6 +250,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
     for (int s = 0; s < SWB; ++s) {
       tc::mbar_init(&w_full[s], 1);
       tc::mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < NRBS; ++s) {
+      tc::mbar_init(&res_full[s], 2 * kAThreads);  // a st.shared release + a cp.async completion per A thread
+      tc::mbar_init(&res_empty[s], kEThreads);
     }
     for (int s = 0; s < Q::NACC; ++s) {
       tc::mbar_init(&acc_full[s], 1);
@@ -320,7 +337,43 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           if (gt == 0) wtrace(a, kEvCPub, c);
         }
     }
-    if constexpr (MODE == kOut) {
+    if constexpr (MODE == kOut && Q::PF) {
+      // OUT, one staging group: these warps prefetch each tile's residual (x at the output
+      // pixels, in place) into a shared buffer NRB tiles ahead of the epilogue — row
+      // offsets from the block list, then 16-byte cp.async along pixel rows — so the
+      // epilogue's copy reads both operands from shared memory and only stores.  Tiles are
+      // disjoint in the output, so reading x ahead of earlier tiles' stores is safe; IN read
+      // every window before this launch began (kernel order).
+      constexpr int CHR = N * 2 / 16;
+      const int ob = b - 2;
+      const long TR = (long)B * ob * ob;
+      int kk = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++kk) {
+        const int rb = kk % Q::NRB;
+        tc::mbar_wait(&res_empty[rb], ((kk / Q::NRB) & 1) ^ 1);
+        if (tid < 128) {
+          const long gr = (long)tile * 128 + tid;
+          long long off = -1;
+          if (gr < TR) {
+            const int j = (int)(gr / (ob * ob)), pp = (int)(gr - (long)j * ob * ob);
+            const int Y = __ldg(a.idx + 3 * j + 1) * g.obh + pp / ob, X = __ldg(a.idx + 3 * j + 2) * g.obw + pp % ob;
+            if (Y < g.oh && X < g.ow) off = (((long long)__ldg(a.idx + 3 * j) * g.oh + Y) * g.ow + X) * N;
+          }
+          rowres[rb][tid] = off;
+        }
+        tc::named_bar<4, kAThreads>();  // this tile's row offsets are visible to every A thread
+        uint8_t* rbuf = smem + Q::OFF_RES + rb * Q::RESB;
+        for (int it = tid; it < 128 * CHR; it += kAThreads) {
+          const int row = it / CHR, ch = it - row * CHR;
+          const long long off = rowres[rb][row];
+          tc::cp_async16(rbuf + row * Q::SPITCH + ch * 16, a.dst + (off >= 0 ? off + ch * 8 : 0), off >= 0);
+        }
+        tc::mbar_arrive(&res_full[rb]);  // releases the row offsets
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&res_full[rb]))
+                     : "memory");
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    } else if constexpr (MODE == kOut) {
       // OUT: these warps have no operand transform; they join the epilogue's staged copy
       // phase (residual add along pixel rows), same barrier sequence as the epilogue warps
       constexpr int GS = Q::GS, CHR = GS * 2 / 16;
@@ -446,7 +499,33 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             tc::fence_before();
             tc::mbar_arrive(&acc_empty[buf]);
           }
-          out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
+          if constexpr (Q::PF) {
+            // staged bf16(acc + b3) + the prefetched residual -> out, coalesced along rows
+            const int et = tid - kAThreads, rb = k % Q::NRB;
+            tc::named_bar<5, kEThreads>();               // the whole tile is staged
+            tc::mbar_wait(&res_full[rb], (k / Q::NRB) & 1);  // its residual has landed
+            const uint8_t* rbuf = smem + Q::OFF_RES + rb * Q::RESB;
+            for (int it = et; it < 128 * CHR; it += kEThreads) {
+              const int row = it / CHR, ch = it - row * CHR;
+              const long long off = rowres[rb][row];
+              if (off < 0) continue;
+              const uint4 sv = *reinterpret_cast<const uint4*>(stg + row * Q::SPITCH + ch * 16);
+              const uint4 xv = *reinterpret_cast<const uint4*>(rbuf + row * Q::SPITCH + ch * 16);
+              const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
+              const __nv_bfloat162* uh = reinterpret_cast<const __nv_bfloat162*>(&sv);
+              uint32_t o[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float2 xf = __bfloat1622float2(xh[q]), uf = __bfloat1622float2(uh[q]);
+                o[q] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
+              }
+              reinterpret_cast<uint4*>(a.dst + off)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            tc::mbar_arrive(&res_empty[rb]);
+            tc::named_bar<5, kEThreads>();  // staging buffer reuse
+          } else {
+            out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
+          }
         }
         if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
         meta(tile + gridDim.x);
