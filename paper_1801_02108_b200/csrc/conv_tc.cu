@@ -60,9 +60,12 @@ struct ConvArgs {
   int cap;
   unsigned long long* trace;  // diagnostics: per-CTA MMA-issuer wait totals (sbn_debug_set_trace)
   // mask-fused front end (double-buffered kernel only): when `mask` is set every CTA
-  // reduces its share of the mask itself and convolves its own active blocks, see
-  // conv_mask_local
+  // reduces its share of the mask itself (conv_mask_local) and then either convolves its
+  // own active blocks (gidx == nullptr), or publishes them into one global list
+  // (conv_mask_global) that every CTA strides through as in list mode
   const uint8_t* mask;
+  unsigned* sw;    // global list: [0] launch epoch, [4 + 4 * (tag & 1) + {0 claimed, 1 done}]
+  int32_t* gidx;   // global list rows (cap x 3)
 };
 
 // Mask reduction fused in front of the conv (reference `tiling.py:138-160`, MAX pool),
@@ -119,6 +122,49 @@ __device__ int conv_mask_local(const ConvArgs& a, int32_t* s_idx) {
   }
   __syncthreads();
   return s_n;
+}
+
+// Global list from the per-CTA lists (few candidates per CTA, where per-CTA lists balance
+// badly on structured masks): one atomic per CTA claims list slots, the rows are stored,
+// and every CTA then waits until all G CTAs have published (the grid is at most one CTA
+// per SM, so it is co-resident) and strides through the list like the ordered list mode —
+// one launch instead of reduce_mask + conv, in an order that does not matter (disjoint
+// outputs).  The counters of launch `tag` live in ring slot tag & 1; the last CTA to
+// publish (every CTA has read the epoch by then) zeroes the other slot and bumps the epoch.
+template <int NTHREADS, int BS>
+__device__ int conv_mask_global(const ConvArgs& a, int32_t* s_idx) {
+  __shared__ unsigned s_tag;
+  __shared__ int s_base, s_B;
+  if (threadIdx.x == 0) s_tag = *reinterpret_cast<volatile unsigned*>(a.sw) + 1u;
+  const int nl = conv_mask_local<NTHREADS, BS>(a, s_idx);  // ends with __syncthreads
+  const unsigned tag = s_tag;
+  unsigned* ring = a.sw + 4 + 4 * (tag & 1u);
+  if (threadIdx.x == 0) s_base = nl ? (int)atomicAdd(ring, (unsigned)nl) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * nl; i += NTHREADS) a.gidx[3 * s_base + i] = s_idx[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ring + 1) : "memory");
+    if (old == gridDim.x - 1) {  // last to publish: recycle the other slot, advance the epoch
+      unsigned* other = a.sw + 4 + 4 * ((tag + 1u) & 1u);
+      other[0] = 0u;
+      other[1] = 0u;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.sw), "r"(tag) : "memory");
+    }
+    SpinGuard sg;
+    unsigned d;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(ring + 1) : "memory");
+      if (d == gridDim.x) break;
+      __nanosleep(32);
+      sg.tick(kSpinSlotDone);
+    }
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(ring) : "memory");
+    s_B = (int)d;
+  }
+  __syncthreads();
+  return s_B;
 }
 
 template <int CIN, int COUT, int BS>
@@ -357,9 +403,11 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   const uint32_t tmem = tslot;
   tc::pdl_wait();
   __shared__ int32_t s_idx[3 * kMaxLocal];  // mask-fused mode: this CTA's own block list
-  const bool local = a.mask != nullptr;
-  const int B = local ? conv_mask_local<kDbThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
-  const int32_t* lidx = local ? s_idx : a.idx;          // (n, by, bx) rows
+  const bool global = a.mask != nullptr && a.gidx != nullptr;  // mask-fused, one global list
+  const bool local = a.mask != nullptr && !global;             // mask-fused, per-CTA lists
+  const int B = global ? conv_mask_global<kDbThreads, BS>(a, s_idx)
+                       : local ? conv_mask_local<kDbThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
+  const int32_t* lidx = local ? s_idx : global ? a.gidx : a.idx;  // (n, by, bx) rows
   const int jfirst = local ? 0 : (int)blockIdx.x, jstep = local ? 1 : (int)gridDim.x;
   // jobs: BPT consecutive blocks of the list.  Tail split (list mode, two M-tiles per
   // block): when B = q*G + R with 0 < 2R <= G, the last R blocks become 2R half-block jobs
@@ -852,18 +900,24 @@ int sparse_conv_tc_pack(const void* w, int cin, int cout, void* img, cudaStream_
 // mask-fused launch: only the double-buffered kernel; returns SBN_ERR_UNSUPPORTED when that
 // variant does not apply (the caller then reduces the mask separately)
 int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout, Geo g, const void* wpk,
-                          const void* bias, int cap, void* dst, cudaStream_t s) {
+                          const void* bias, int cap, void* dst, cudaStream_t s, unsigned* slotw, int32_t* gidx) {
   if (debug_flags() & (kDebugConvSingleBuffer | kDebugConvPair)) return SBN_ERR_UNSUPPORTED;
   // Per-CTA lists balance only statistically: with few candidates per CTA a structured
-  // mask (e.g. a top-left rectangle) lands unevenly on the round-robin owners, and the
-  // separate ordered reduce_mask + conv (evenly striped list) is faster (measured, config 3:
-  // 16x16 blocks, 20 candidates / CTA: 61 vs 36 us at 10 %; 8x8 blocks, 106 / CTA: 40 vs
-  // 46 us).  Fused only from kMinLocal candidates per CTA up to the shared list size.
+  // mask (e.g. a top-left rectangle) lands unevenly on the round-robin owners (measured,
+  // config 3: 16x16 blocks, 20 candidates / CTA: 61 vs 36 us at 10 % against the ordered
+  // reduce_mask + conv); 8x8 blocks, 106 / CTA: 40 vs 46 us.  So from kMinLocal candidates per
+  // CTA the CTAs keep their own lists; below it they publish one global list in the same
+  // launch (conv_mask_global: evenly striped like the ordered list, no reduce_mask launch).
   constexpr int kMinLocal = 64;
   const int per_cta = (cap + sm_count() - 1) / sm_count();
-  if (per_cta < kMinLocal || per_cta > kMaxLocal) return SBN_ERR_UNSUPPORTED;
+  if (per_cta > kMaxLocal || (per_cta < kMinLocal && (!slotw || !gidx || (debug_flags() & kDebugNoGlobalList))))
+    return SBN_ERR_UNSUPPORTED;
   ConvArgs a;
   memset(&a, 0, sizeof(a));
+  if (per_cta < kMinLocal) {
+    a.sw = slotw;
+    a.gidx = gidx;
+  }
   a.x = (const __nv_bfloat16*)x;
   a.out = (__nv_bfloat16*)dst;
   a.g = g;
