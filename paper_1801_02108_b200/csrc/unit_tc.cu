@@ -897,7 +897,14 @@ struct PairCfg {
   static constexpr int OFF_B2 = OFF_B1 + (K::OFF_B2 - K::OFF_B1);
   static constexpr int OFF_B3 = OFF_B1 + (K::OFF_B3 - K::OFF_B1);
   static constexpr int OFF_PAR = OFF_B1 + (K::OFF_PAR - K::OFF_B1);
-  static constexpr int SMEM = OFF_B1 + IMG;
+  // raw x of this CTA's 128 window pixels plus (rank 0) the partner's first BS + 1 (the
+  // residual of epilogue 3: output row o is window pixel o + BS + 1), 16-byte chunks
+  // XOR-swizzled by pixel
+  static constexpr int RAW_ROWS = 128 + BS + 1;
+  static constexpr int OFF_RAW = OFF_B1 + IMG;
+  static constexpr int SZ_RAW = al(RAW_ROWS * C * 2);
+  static constexpr int RSW = (C / 8 < 8 ? C / 8 : 8) - 1;  // swizzle mask
+  static constexpr int SMEM = OFF_RAW + SZ_RAW;
   static constexpr int COL1 = 0, COL2 = MC, COL3 = 2 * MC;
   static constexpr int TCOLS = 2 * MC + C;
   static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
@@ -917,6 +924,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   uint8_t* B1 = smem + PK::OFF_B1;
   uint8_t* B2 = smem + PK::OFF_B2;
   uint8_t* B3 = smem + PK::OFF_B3;
+  uint4* RAW = reinterpret_cast<uint4*>(smem + PK::OFF_RAW);
   float* par = reinterpret_cast<float*>(smem + PK::OFF_PAR);
   float* s1 = par;
   float* t1 = s1 + C;
@@ -1076,6 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
         o[e] = tc::pack_bf16(v0, v1);
       }
       *reinterpret_cast<uint4*>(A1 + k * PK::P1 + pl * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      RAW[pl * (C / 8) + (k ^ (pl & PK::RSW))] = raw[it];
     }
     tc::fence_async_smem();
     __syncthreads();
@@ -1127,10 +1136,17 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
         }
       }
     }
+    if (rank > 0) {  // my first BS + 1 raw pixels: the residuals of the partner's last rows
+      uint4* peer = cl.map_shared_rank(RAW, rank - 1);
+      for (int t = tid; t < (BS + 1) * (C / 8); t += kThreads) {
+        const int pl = t / (C / 8), k = t % (C / 8);
+        peer[(128 + pl) * (C / 8) + (k ^ ((128 + pl) & PK::RSW))] = RAW[pl * (C / 8) + (k ^ (pl & PK::RSW))];
+      }
+    }
     trace(a.trace, 21);
     tc::fence_before();
     asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
-    cl.sync();  // A2 halo rows from the partner have landed
+    cl.sync();  // A2 halo rows (and residual pixels) from the partner have landed
     tc::fence_async_smem();
     trace(a.trace, 7);
     // ---- 4. GEMM2: 9 row-shifted views of A2 (local rows 0 .. 127 + shift)
@@ -1162,7 +1178,6 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     const bool store = oy < BS - 2 && ox < BS - 2 && Y < g.oh && X < g.ow;
     uint4* op = reinterpret_cast<uint4*>(a.out) +
                 (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (C / 8) + hf * (C / 16);
-    uint4 res[C / 16];  // (loaded after the A3 stores: in front of them, 1.7 % slower)
     trace(a.trace, 22);
 #pragma unroll
     for (int c0 = hf * (MC / 2); c0 < (hf + 1) * (MC / 2); c0 += 16) {
@@ -1180,8 +1195,6 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
       *reinterpret_cast<uint4*>(A3 + (c0 / 8) * PK::P3 + j * 16) = make_uint4(o[0], o[1], o[2], o[3]);
       *reinterpret_cast<uint4*>(A3 + (c0 / 8 + 1) * PK::P3 + j * 16) = make_uint4(o[4], o[5], o[6], o[7]);
     }
-#pragma unroll
-    for (int k = 0; k < C / 16; ++k) res[k] = tc::ld_v4_pred(op + k, store);
     tc::fence_before();
     tc::fence_async_smem();
     __syncthreads();
@@ -1207,24 +1220,36 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
       first_store = false;
     }
     trace(a.trace, 10);
-    // ---- 7. epilogue 3: +b3 + residual, my column half of my rows
+    // ---- 7. epilogue 3: +b3 + residual (x at window pixel o_row + BS + 1, staged by this
+    //      CTA or, for rank 0's last rows, pushed by the partner in epilogue 1), my column
+    //      half of my rows
+    const uint4* rsrc = RAW;
+    const int rpl = o_row + BS + 1 - rank * 128;
+    constexpr int EW = (C / 2) % 32 == 0 ? 32 : 16;  // columns per TMEM load (one wait each)
 #pragma unroll
-    for (int cc = 0; cc < C / 2; cc += 16) {
-      const int c0 = hf * (C / 2) + cc;
-      float v[16];
-      tc::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + PK::COL3 + c0, v);
+    for (int cc = 0; cc < C / 2; cc += EW) {
+      float v[EW];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + PK::COL3 + hf * (C / 2) + cc;
+      if constexpr (EW == 32) tc::tmem_ld32(ta, v);
+      else tc::tmem_ld16(ta, v);
       if (store) {
-        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&res[cc / 8]);
-        uint32_t o[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float2 xf = __bfloat1622float2(xh[e]);
-          const float u0 = __bfloat162float(__float2bfloat16_rn(v[2 * e] + b3[c0 + 2 * e]));
-          const float u1 = __bfloat162float(__float2bfloat16_rn(v[2 * e + 1] + b3[c0 + 2 * e + 1]));
-          o[e] = tc::pack_bf16(__fadd_rn(xf.x, u0), __fadd_rn(xf.y, u1));
+        for (int h = 0; h < EW / 16; ++h) {
+          const int c0 = hf * (C / 2) + cc + 16 * h;
+          const uint4 r0 = rsrc[rpl * (C / 8) + ((c0 / 8) ^ (rpl & PK::RSW))];
+          const uint4 r1 = rsrc[rpl * (C / 8) + ((c0 / 8 + 1) ^ (rpl & PK::RSW))];
+          const uint32_t xw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+          uint32_t o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float2 xf = make_float2(__uint_as_float(xw[e] << 16), __uint_as_float(xw[e] & 0xffff0000u));
+            const float u0 = __bfloat162float(__float2bfloat16_rn(v[16 * h + 2 * e] + b3[c0 + 2 * e]));
+            const float u1 = __bfloat162float(__float2bfloat16_rn(v[16 * h + 2 * e + 1] + b3[c0 + 2 * e + 1]));
+            o[e] = tc::pack_bf16(__fadd_rn(xf.x, u0), __fadd_rn(xf.y, u1));
+          }
+          op[(cc + 16 * h) / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+          op[(cc + 16 * h) / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
         }
-        op[cc / 8] = make_uint4(o[0], o[1], o[2], o[3]);
-        op[cc / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
       }
     }
     tc::fence_before();
