@@ -151,6 +151,8 @@ struct __align__(64) WArgs {
   __nv_bfloat16* dst;        // IN: S1   MID: S2    OUT: out
   const uint8_t* wpk;        // this GEMM's packed weight chunks
   const float* par;          // this GEMM's parameter vectors
+  const uint8_t* wpk2;       // fused IN+MID: W2 chunks
+  const float* par2;         // fused IN+MID: MID's parameter vectors
   Geo g;
   const int32_t* idx;
   const int32_t* count;
@@ -711,6 +713,447 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   if (warp == 0) tc::tmem_free<Q::TALLOC>(tmem);
 }
 
+// ---- fused IN + MID for 16x16 blocks: S1 never leaves shared memory.
+// A block's window is exactly two 128-row tiles (window rows 0-7 and 8-15), so one CTA
+// runs the whole 3x3 of a block on its own: GEMM1 of both tiles -> A2 (the S1 rows of the
+// block, plane layout, in shared memory) -> GEMM2 as 9 row-shifted views of A2 -> S2.
+// Persistent CTAs take blocks j = blockIdx.x + k * gridDim.x.  The MMA issuer runs GEMM1 of
+// block k+1 ahead of GEMM2 of block k, so the GEMM1 epilogue of k+1 (warps 8-11) overlaps
+// GEMM2 of k and the GEMM2 epilogue of k (warps 12-15) overlaps GEMM2 of k+1.  The MMA
+// order per accumulator equals IN's / MID's (k-steps of GEMM1; (K-chunk, tap, k-step) of
+// GEMM2), so S2 is bit-identical to the three-launch path's.  OUT then runs unchanged.
+//   warps 0-7   BN1 + ReLU on landed window chunks (IN's code)
+//   warps 8-11  epilogue 1: TMEM -> relu(acc*s2 + t2') * in-bounds -> A2 (bf16, smem)
+//   warps 12-15 epilogue 2: TMEM -> relu(acc*s3 + t3') -> S2 stack (global, plane-major)
+//   warp 16     loader: window chunks by 4-D TMA, W1 (+ W2) resident or W2 streamed
+//   warp 17     MMA issuer
+constexpr int kFB = 16;                  // block size of the fused variant
+// CTA-0 event stamps per block k (diagnostics, tools/trace_fused.py)
+enum { kFevLoad = 0, kFevLanded = 1, kFevBn = 2, kFevG1 = 3, kFevE1 = 4, kFevG2 = 5, kFevE2a = 6, kFevE2 = 7, kFevG1s = 8, kFevG2e = 9, kFevE1s = 10 };
+constexpr int kFR2 = 296;                // A2 rows: 256 + 2*16 + 2 = 290, rounded to 8
+constexpr int kFPA2 = kFR2 * 16;         // A2 plane stride
+constexpr int kFBudget = 232448 - 1024;  // opt-in dynamic smem minus the static barriers
+
+template <int C, int M>
+struct FCfg {
+  using Q1 = WCfg<C, M, kIn>;
+  using Q2 = WCfg<M, M, kMid>;
+  static constexpr int KC1 = Q1::KC, NKC1 = C / KC1, ROWB = KC1 * 2;
+  static constexpr uint32_t SWZ = Q1::SWZ;
+  static constexpr int ACH = 128 * ROWB;          // one window chunk: 128 rows x KC1 ch (swizzled)
+  static constexpr int WCH1 = Q1::WCH, PW1 = Q1::PW;
+  static constexpr int W1B = (int)Q1::WBYTES;
+  static constexpr int KC2 = Q2::KC, NKC2 = M / KC2, P2 = KC2 / 8;
+  static constexpr int WCH2 = Q2::WCH, PW2 = Q2::PW;
+  static constexpr int W2B = (int)Q2::WBYTES;
+  static constexpr int A2B = (M / 8) * kFPA2;
+  static constexpr int PAR1 = Q1::NPAR, PAR2 = Q2::NPAR;
+  static constexpr int PARB = (PAR1 + PAR2) * 4 / 128 * 128 + 128;
+  static constexpr int ITEMS = Q1::ITEMS;
+  // the window ring holds whole tiles: a slot = NKC1 chunks (one TMA box each) completing
+  // on one barrier, BN'd by one group, consumed by one MMA wait and released by one commit
+  // (the single MMA thread spends ~500 cycles of wait + commit latency per ring step)
+  static constexpr int TSB = NKC1 * ACH;
+  // budget: prefer two A2 buffers, then W2 resident, then the deepest window ring (<= two
+  // blocks of tiles)
+  static constexpr long FIX2 = 2L * A2B + W1B + PARB;
+  static constexpr bool RES2 = FIX2 + W2B + 2L * TSB <= kFBudget;
+  static constexpr int SW0 = RES2 ? 0 : 4;
+  static constexpr long WREG0 = RES2 ? (long)W2B : (long)SW0 * WCH2;
+  static constexpr int NA2 = FIX2 + WREG0 + 2L * TSB <= kFBudget ? 2 : 1;
+  static constexpr long FIX = (long)NA2 * A2B + W1B + PARB + WREG0;
+  static constexpr int SAF = (int)((kFBudget - FIX) / TSB);
+  // even: the two BN groups take alternate tiles, so with an even ring every slot always
+  // belongs to the same group (an odd ring would let a group wait on a slot two phases
+  // ahead of the tile it expects)
+  static constexpr int SA0 = SAF > 4 ? 4 : SAF;
+  static constexpr int SA = SA0 / 2 * 2;
+  // streamed W2: what is left deepens the weight ring
+  static constexpr int SWX = RES2 ? 0 : (int)((kFBudget - FIX - (long)SA * TSB) / WCH2);
+  static constexpr int SW = RES2 ? 0 : (SW0 + SWX > 12 ? 12 : SW0 + SWX);
+  static constexpr long WREG2 = RES2 ? (long)W2B : (long)SW * WCH2;
+  static constexpr int SWB = SW > 0 ? SW : 1;
+  // TMEM: NB1 GEMM1 tile accumulators (M columns each) + two GEMM2 block accumulators (2M)
+  static constexpr int NB1 = (512 / M - 4) >= 4 ? 4 : (512 / M - 4);
+  static constexpr bool OK = M % 16 == 0 && M <= 256 && NB1 >= 1 && SA >= 2 && C % KC1 == 0 && RES2;
+  static constexpr int COL2 = (NB1 > 0 ? NB1 : 1) * M;
+  static constexpr int TCOLS = COL2 + 4 * M;
+  static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
+  static constexpr bool BOTH_FIRST = NB1 >= 4;  // GEMM1 of both tiles of k+1 before GEMM2 of k
+  static constexpr int OFF_A2 = SA * TSB;
+  static constexpr int OFF_W1 = OFF_A2 + NA2 * A2B;
+  static constexpr int OFF_W2 = OFF_W1 + W1B;
+  static constexpr int OFF_PAR = OFF_W2 + (int)WREG2;
+  static constexpr int SMEM = OFF_PAR + PARB;
+};
+
+// The issue order shared by the loader and the MMA issuer: GEMM1 tiles g1(k, t) and GEMM2
+// blocks g2(k), k over this CTA's nb blocks.
+// 32 accumulator columns [g0, g0 + 32) of this thread's TMEM lane (16 when only 16 remain),
+// one load and one wait
+template <int M>
+__device__ __forceinline__ void tmem_ld_group(uint32_t acc, int g0, float (&v)[32]) {
+  if (g0 + 32 <= M) {
+    tc::tmem_ld32(acc + g0, v);
+  } else {
+    float h[16];
+    tc::tmem_ld16(acc + g0, h);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = h[i];
+    if (g0 + 16 < M) {
+      tc::tmem_ld16(acc + g0 + 16, h);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[16 + i] = h[i];
+    } else {
+#pragma unroll
+      for (int i = 16; i < 32; ++i) v[i] = 0.f;
+    }
+  }
+}
+
+template <bool BOTH_FIRST, typename G1, typename G2>
+__device__ __forceinline__ void fused_schedule(int nb, G1&& g1, G2&& g2) {
+  if (nb <= 0) return;
+  g1(0, 0);
+  g1(0, 1);
+  for (int k = 0; k < nb; ++k) {
+    const bool more = k + 1 < nb;
+    if (more) g1(k + 1, 0);
+    if (BOTH_FIRST) {
+      if (more) g1(k + 1, 1);
+      g2(k);
+    } else {
+      g2(k);
+      if (more) g1(k + 1, 1);
+    }
+  }
+}
+
+template <int C, int M>
+__global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const __grid_constant__ WArgs a) {
+  using F = FCfg<C, M>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t a_load[F::SA], a_full[F::SA], a_empty[F::SA], w_full[F::SWB], w_empty[F::SWB], wres;
+  __shared__ uint64_t a2_full[F::NA2], a2_empty[F::NA2], acc1_full[F::NB1], acc1_empty[F::NB1];
+  __shared__ uint64_t acc2_full[2], acc2_empty[2];
+  __shared__ uint32_t tslot;
+  uint8_t* A1 = smem;
+  uint8_t* A2 = smem + F::OFF_A2;
+  uint8_t* W1 = smem + F::OFF_W1;
+  uint8_t* W2 = smem + F::OFF_W2;
+  float* par1 = reinterpret_cast<float*>(smem + F::OFF_PAR);
+  float* par2 = par1 + F::PAR1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Geo& g = a.g;
+  constexpr int kLWarp = 16, kMWarp = 17;
+
+  if (tid == 0) {
+    for (int s = 0; s < F::SA; ++s) {
+      tc::mbar_init(&a_load[s], 1);
+      tc::mbar_init(&a_full[s], kAThreads / 2);
+      tc::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < F::SWB; ++s) {
+      tc::mbar_init(&w_full[s], 1);
+      tc::mbar_init(&w_empty[s], 1);
+    }
+    tc::mbar_init(&wres, 1);
+    for (int s = 0; s < F::NA2; ++s) {
+      tc::mbar_init(&a2_full[s], 128);
+      tc::mbar_init(&a2_empty[s], 1);
+    }
+    for (int s = 0; s < F::NB1; ++s) {
+      tc::mbar_init(&acc1_full[s], 1);
+      tc::mbar_init(&acc1_empty[s], 128);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&acc2_full[s], 1);
+      tc::mbar_init(&acc2_empty[s], 128);
+    }
+    tc::mbar_fence_init();
+  }
+  if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
+  for (int i = tid; i < F::PAR1; i += kWideThreads) par1[i] = a.par[i];
+  for (int i = tid; i < F::PAR2; i += kWideThreads) par2[i] = a.par2[i];
+  if (warp == 0) tc::tmem_alloc<F::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_trigger();
+  if (tid == kLWarp * 32) {
+    // resident weights land under the previous kernel's tail (they do not depend on it)
+    tc::mbar_expect_tx(&wres, (uint32_t)(F::W1B + (F::RES2 ? F::W2B : 0)));
+    for (int c = 0; c < F::Q1::CHUNKS; ++c)
+      tc::bulk_g2s(W1 + (size_t)c * F::WCH1, a.wpk + (size_t)c * F::WCH1, F::WCH1, &wres);
+    if (F::RES2)
+      for (int c = 0; c < F::Q2::CHUNKS; ++c)
+        tc::bulk_g2s(W2 + (size_t)c * F::WCH2, a.wpk2 + (size_t)c * F::WCH2, F::WCH2, &wres);
+  }
+  tc::pdl_wait();  // x and the index list of the previous launches are visible
+  const int B = ld_count(a.count, a.cap);
+  const int G = gridDim.x;
+  const int nb = B > (int)blockIdx.x ? (B - 1 - (int)blockIdx.x) / G + 1 : 0;
+
+  if (tid < kAThreads) {
+    // ------------------------------------------------ BN1 + ReLU on landed chunks (as IN)
+    const float* s1 = par1;
+    constexpr int PR = F::ROWB / 16;
+    constexpr int TG = kAThreads / 2;
+    const int grp_id = tid / TG, gt = tid % TG;
+    int tl = 0;
+    for (int k = 0; k < nb; ++k)
+      for (int t = 0; t < 2; ++t, ++tl) {
+        if ((tl & 1) != grp_id) continue;
+        const int s = tl % F::SA;
+        tc::mbar_wait(&a_load[s], (tl / F::SA) & 1);
+        if (gt == 0 && t == 0) wtrace(a, kFevLanded, k);
+        for (int kc = 0; kc < F::NKC1; ++kc) {
+          uint8_t* A = A1 + s * F::TSB + kc * F::ACH;
+          uint4 raw[F::ITEMS];
+#pragma unroll
+          for (int j = 0; j < F::ITEMS; ++j) {
+            const int i = gt + j * TG;
+            if (i < 128 * PR)
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(raw[j].x), "=r"(raw[j].y), "=r"(raw[j].z), "=r"(raw[j].w)
+                           : "r"(tc::smem_u32(A + i * 16)));
+          }
+#pragma unroll
+          for (int j = 0; j < F::ITEMS; ++j) {
+            const int i = gt + j * TG;
+            if (i >= 128 * PR) break;
+            const int r = i / PR, qp = i % PR;
+            const int grp = qp ^ (F::KC1 == 64 ? (r & 7) : ((r >> 1) & 3));
+            const uint4 sg4 = *reinterpret_cast<const uint4*>(s1 + (kc * F::KC1 + grp * 8) / 2);
+            const uint4 vv4 = *reinterpret_cast<const uint4*>(s1 + C / 2 + (kc * F::KC1 + grp * 8) / 2);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[j]);
+            const __nv_bfloat162* hs = reinterpret_cast<const __nv_bfloat162*>(&sg4);
+            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&vv4);
+            const __nv_bfloat162 z2 = __float2bfloat162_rn(0.f);
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __nv_bfloat162 y = __hmax2(__hfma2(h[e], hs[e], hv[e]), z2);
+              o[e] = *reinterpret_cast<const uint32_t*>(&y);
+            }
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(A + i * 16)), "r"(o[0]),
+                         "r"(o[1]), "r"(o[2]), "r"(o[3])
+                         : "memory");
+          }
+        }
+        tc::fence_async_smem();
+        tc::mbar_arrive(&a_full[s]);
+        if (gt == 0 && t == 1) wtrace(a, kFevBn, k);
+      }
+  } else if (warp < 12) {
+    // ------------------------------------------------ epilogue 1: TMEM -> A2 (S1 rows)
+    const int qd = warp & 3, r = qd * 32 + lane;
+    const float* sc = par1 + 2 * C + M;  // s2
+    const float* sh = sc + M;            // t2' (b1 folded)
+    for (int k = 0; k < nb; ++k) {
+      const int j = (int)blockIdx.x + k * G;
+      const int by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
+      const int ab = k % F::NA2;
+      tc::mbar_wait(&a2_empty[ab], ((k / F::NA2) & 1) ^ 1);
+      uint8_t* A2b = A2 + ab * F::A2B;
+      for (int t = 0; t < 2; ++t) {
+        const int ti = 2 * k + t, b1 = ti % F::NB1;
+        const int p = t * 128 + r, wy = p >> 4, wx = p & 15;
+        const int y = g.oy + by * g.sy + wy, x = g.ox + bx * g.sx + wx;
+        const bool valid = y >= 0 && y < g.h && x >= 0 && x < g.w;
+        tc::mbar_wait(&acc1_full[b1], (ti / F::NB1) & 1);
+        tc::fence_after();
+        if (t == 0 && r == 0) wtrace(a, kFevE1s, k);
+        const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + b1 * M;
+#pragma unroll
+        for (int g0 = 0; g0 < M; g0 += 32) {
+          float v[32];
+          tmem_ld_group<M>(acc, g0, v);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int c0 = g0 + 16 * hh;
+            if (c0 >= M) break;
+            uint32_t o[8];
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+              const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q);
+              const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q);
+              const float* w = v + 16 * hh;
+              const float u0 = fmaxf(fmaf(w[2 * q], s4.x, t4.x), 0.f);
+              const float u1 = fmaxf(fmaf(w[2 * q + 1], s4.y, t4.y), 0.f);
+              const float u2 = fmaxf(fmaf(w[2 * q + 2], s4.z, t4.z), 0.f);
+              const float u3 = fmaxf(fmaf(w[2 * q + 3], s4.w, t4.w), 0.f);
+              o[q] = valid ? tc::pack_bf16(u0, u1) : 0u;
+              o[q + 1] = valid ? tc::pack_bf16(u2, u3) : 0u;
+            }
+            uint8_t* pl = A2b + (c0 / 8) * kFPA2 + p * 16;
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl)), "r"(o[0]), "r"(o[1]),
+                         "r"(o[2]), "r"(o[3])
+                         : "memory");
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl + kFPA2)), "r"(o[4]),
+                         "r"(o[5]), "r"(o[6]), "r"(o[7])
+                         : "memory");
+          }
+        }
+        tc::fence_before();
+        tc::mbar_arrive(&acc1_empty[b1]);
+      }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&a2_full[ab]);
+      if (r == 0) wtrace(a, kFevE1, k);
+    }
+  } else if (warp < 16) {
+    // ------------------------------------------------ epilogue 2: TMEM -> S2 stack
+    const int qd = warp & 3, r = qd * 32 + lane;
+    const float* sc = par2 + M;  // s3
+    const float* sh = sc + M;    // t3' (b2 folded)
+    constexpr int OB = kFB - 2;
+    for (int k = 0; k < nb; ++k) {
+      const int j = (int)blockIdx.x + k * G, b2 = k & 1;
+      tc::mbar_wait(&acc2_full[b2], (k >> 1) & 1);
+      tc::fence_after();
+      if (r == 0) wtrace(a, kFevE2a, k);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = u * 128 + r, oy = q >> 4, ox = q & 15;
+        const bool store = oy < OB && ox < OB;
+        const long drow = (long)j * OB * OB + oy * OB + ox;
+        const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + F::COL2 + b2 * 2 * M + u * M;
+#pragma unroll
+        for (int g0 = 0; g0 < M; g0 += 32) {
+          float v[32];
+          tmem_ld_group<M>(acc, g0, v);
+          if (!store) continue;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int c0 = g0 + 16 * hh;
+            if (c0 >= M) break;
+            const float* w = v + 16 * hh;
+            uint32_t o[8];
+#pragma unroll
+            for (int q2 = 0; q2 < 8; q2 += 2) {
+              const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q2);
+              const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q2);
+              o[q2] = tc::pack_bf16(fmaxf(fmaf(w[2 * q2], s4.x, t4.x), 0.f), fmaxf(fmaf(w[2 * q2 + 1], s4.y, t4.y), 0.f));
+              o[q2 + 1] =
+                  tc::pack_bf16(fmaxf(fmaf(w[2 * q2 + 2], s4.z, t4.z), 0.f), fmaxf(fmaf(w[2 * q2 + 3], s4.w, t4.w), 0.f));
+            }
+            uint4* pl = reinterpret_cast<uint4*>(a.dst) + (long)(c0 / 8) * a.dst_rows + drow;
+            pl[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            pl[a.dst_rows] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&acc2_empty[b2]);
+      if (r == 0) wtrace(a, kFevE2, k);
+    }
+  } else if (warp == kLWarp) {
+    // ------------------------------------------------ loader
+    if (lane == 0) {
+      int tl = 0, wit = 0;
+      int cur_k = -1, cn = 0, cy = 0, cx = 0;
+      auto g1 = [&](int k, int t) {
+        if (k != cur_k) {
+          const int j = (int)blockIdx.x + k * G;
+          cn = __ldg(a.idx + 3 * j);
+          cy = g.oy + __ldg(a.idx + 3 * j + 1) * g.sy;
+          cx = g.ox + __ldg(a.idx + 3 * j + 2) * g.sx;
+          cur_k = k;
+        }
+        const int s = tl % F::SA;
+        tc::mbar_wait(&a_empty[s], ((tl / F::SA) & 1) ^ 1);
+        if (t == 0) wtrace(a, kFevLoad, k);
+        tc::mbar_expect_tx(&a_load[s], (uint32_t)F::TSB);
+        for (int kc = 0; kc < F::NKC1; ++kc)
+          tma_4d(A1 + s * F::TSB + kc * F::ACH, &a.tmap, kc * F::KC1, cx, cy + 8 * t, cn, &a_load[s]);
+        ++tl;
+      };
+      auto g2 = [&](int) {
+        if constexpr (F::RES2) return;
+        for (int kc = 0; kc < F::NKC2; ++kc)
+          for (int tap = 0; tap < 9; ++tap, ++wit) {
+            const int sw = wit % F::SWB;
+            tc::mbar_wait(&w_empty[sw], ((wit / F::SWB) & 1) ^ 1);
+            tc::mbar_expect_tx(&w_full[sw], F::WCH2);
+            tc::bulk_g2s(W2 + sw * F::WCH2, a.wpk2 + (size_t)(kc * 9 + tap) * F::WCH2, F::WCH2, &w_full[sw]);
+          }
+      };
+      fused_schedule<F::BOTH_FIRST>(nb, g1, g2);
+    }
+    __syncwarp();
+  } else if (warp == kMWarp) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, M);
+      int tl = 0, wit = 0;
+      tc::mbar_wait(&wres, 0);
+      auto g1 = [&](int k, int t) {
+        const int ti = 2 * k + t, b1 = ti % F::NB1;
+        tc::mbar_wait(&acc1_empty[b1], ((ti / F::NB1) & 1) ^ 1);
+        tc::fence_after();
+        if (t == 0) wtrace(a, kFevG1s, k);
+        const uint32_t acc = tmem + b1 * M;
+        const int s = tl % F::SA;
+        tc::mbar_wait(&a_full[s], (tl / F::SA) & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kc = 0; kc < F::NKC1; ++kc) {
+          const uint32_t abase = tc::smem_u32(A1 + s * F::TSB + kc * F::ACH);
+          const uint32_t wbase = tc::smem_u32(W1 + kc * F::WCH1);
+#pragma unroll
+          for (int kk = 0; kk < F::KC1 / 16; ++kk)
+            tc::mma_bf16(acc, tc::desc_kmajor_swz(abase + kk * 32, 8 * F::ROWB, F::SWZ),
+                         tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW1, F::PW1, 128), idesc, (kc | kk) > 0);
+        }
+        tc::mma_commit(&a_empty[s]);
+        ++tl;
+        tc::mma_commit(&acc1_full[b1]);
+        if (t == 1) wtrace(a, kFevG1, k);
+      };
+      auto g2 = [&](int k) {
+        const int b2 = k & 1, ab = k % F::NA2;
+        tc::mbar_wait(&acc2_empty[b2], ((k >> 1) & 1) ^ 1);
+        tc::mbar_wait(&a2_full[ab], (k / F::NA2) & 1);
+        tc::fence_after();
+        wtrace(a, kFevG2, k);
+        const uint32_t acc = tmem + F::COL2 + b2 * 2 * M;
+        const uint32_t a2base = tc::smem_u32(A2 + ab * F::A2B);
+        for (int kc = 0; kc < F::NKC2; ++kc)
+          for (int tap = 0; tap < 9; ++tap, ++wit) {
+            const int sw = F::RES2 ? 0 : wit % F::SWB;
+            if (!F::RES2) {
+              tc::mbar_wait(&w_full[sw], (wit / F::SWB) & 1);
+              tc::fence_after();
+            }
+            const uint32_t wbase = tc::smem_u32(W2 + (F::RES2 ? (kc * 9 + tap) * F::WCH2 : sw * F::WCH2));
+            const int shift = (tap / 3) * kFB + (tap % 3);
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+              for (int kk = 0; kk < F::KC2 / 16; ++kk)
+                tc::mma_bf16(acc + u * M,
+                             tc::desc_kmajor_noswz(a2base + (kc * F::P2 + 2 * kk) * kFPA2 + (u * 128 + shift) * 16,
+                                                   kFPA2, 128),
+                             tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW2, F::PW2, 128), idesc, (kc | tap | kk) > 0);
+            if (!F::RES2) tc::mma_commit(&w_empty[sw]);
+          }
+        tc::mma_commit(&a2_empty[ab]);
+        tc::mma_commit(&acc2_full[b2]);
+        wtrace(a, kFevG2e, k);
+      };
+      fused_schedule<F::BOTH_FIRST>(nb, g1, g2);
+    }
+    __syncwarp();
+  }
+  if (tid == kLWarp * 32) tc::mbar_wait(&wres, 0);  // no copy in flight at exit
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free<F::TALLOC>(tmem);
+}
+
 // ---- packed image: [W1 chunks | W2 chunks | W3 chunks | params], regions 128-B aligned.
 // A chunk c of a GEMM with K-chunk KC, N columns: KC/8 planes of N rows x 16 B,
 // element (n, k) at (k/8)*N*16 + n*16 + (k%8)*2 — the kernel's B-operand layout.  MID
@@ -820,6 +1263,44 @@ int launch_wide(const WArgs& a, long max_tiles, cudaStream_t s, const char* what
   return launch_status(what);
 }
 
+// the fused IN + MID launch applies to 16x16 blocks when its buffers fit
+template <int C, int M>
+bool fused_ok(int b) {
+  if constexpr (FCfg<C, M>::OK) {
+    return b == kFB && FCfg<C, M>::SMEM <= max_smem_optin() && !(debug_flags() & kDebugWideUnfused);
+  } else {
+    (void)b;
+    return false;
+  }
+}
+
+template <int C, int M>
+int launch_fused(const WArgs& a, long cap, cudaStream_t s) {
+  if constexpr (FCfg<C, M>::OK) {
+    using F = FCfg<C, M>;
+    auto kern = unit_wide_fused_kernel<C, M>;
+    static PerDeviceOnce once;
+    once([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM); });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(cap < sm_count() ? (cap < 1 ? 1 : cap) : sm_count()));
+    cfg.blockDim = dim3(kWideThreads);
+    cfg.dynamicSmemBytes = F::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a);
+    return launch_status("residual_unit_wide_in_mid");
+  } else {
+    (void)a;
+    (void)cap;
+    (void)s;
+    return SBN_ERR_UNSUPPORTED;
+  }
+}
+
 template <int C, int M>
 int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const int32_t* idx,
              const int32_t* count, int cap, uint8_t* s1, uint8_t* s2, cudaStream_t s) {
@@ -852,21 +1333,33 @@ int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const i
                         Q::KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (st) return st;
   }
-  a.dst = (__nv_bfloat16*)s1;
-  a.dst_rows = rows1;
-  a.wpk = img + L.w1;
-  a.par = (const float*)(img + L.p1);
-  int st = launch_wide<C, M, kIn>(a, ((long)cap * a.S + a.G - 1) / a.G, s, "residual_unit_wide_in");
-  if (st) return st;
-  // MID: S1 -> S2 (3x3 valid); plane runs by 1-D bulk copies
-  a.stack = s1;
-  a.src_rows = rows1;
-  a.dst = (__nv_bfloat16*)s2;
-  a.dst_rows = rows2;
-  a.wpk = img + L.w2;
-  a.par = (const float*)(img + L.p2);
-  a.trace = tsel == 1 ? tb : nullptr;
-  st = launch_wide<M, M, kMid>(a, ((long)cap * b * b + 127) / 128, s, "residual_unit_wide_mid");
+  int st = 0;
+  if (fused_ok<C, M>(b)) {
+    // IN + MID in one launch: window -> A2 in shared memory -> S2
+    a.dst = (__nv_bfloat16*)s2;
+    a.dst_rows = rows2;
+    a.wpk = img + L.w1;
+    a.par = (const float*)(img + L.p1);
+    a.wpk2 = img + L.w2;
+    a.par2 = (const float*)(img + L.p2);
+    st = launch_fused<C, M>(a, cap, s);
+  } else {
+    a.dst = (__nv_bfloat16*)s1;
+    a.dst_rows = rows1;
+    a.wpk = img + L.w1;
+    a.par = (const float*)(img + L.p1);
+    st = launch_wide<C, M, kIn>(a, ((long)cap * a.S + a.G - 1) / a.G, s, "residual_unit_wide_in");
+    if (st) return st;
+    // MID: S1 -> S2 (3x3 valid); plane runs by 1-D bulk copies
+    a.stack = s1;
+    a.src_rows = rows1;
+    a.dst = (__nv_bfloat16*)s2;
+    a.dst_rows = rows2;
+    a.wpk = img + L.w2;
+    a.par = (const float*)(img + L.p2);
+    a.trace = tsel == 1 ? tb : nullptr;
+    st = launch_wide<M, M, kMid>(a, ((long)cap * b * b + 127) / 128, s, "residual_unit_wide_mid");
+  }
   if (st) return st;
   // OUT: S2 -> out (+ residual), in place or into the clone
   a.stack = s2;

@@ -1,0 +1,98 @@
+"""GPU parity of the fused IN+MID launch of the wide tcgen05 unit (unit_wide.cu,
+`unit_wide_fused_kernel`: 16x16 blocks, the S1 rows of a block stay in shared memory).
+
+The fused launch issues the tensor-core k-steps of every accumulator in the same order as
+the three-launch path (IN -> S1 stack -> MID), so its S2 stack and therefore the unit's
+output must be BIT-identical to the three-launch path's (SBN_DEBUG_WIDE_UNFUSED = 256 forces
+that one).  Both are also checked against the fp32 oracle (north star: bf16 <= 2e-2).
+Cases cover the config-4 stage shapes (c = 96 / 192), the small shapes (32, 64, 128), ragged
+frame borders, many blocks per CTA (ring wrap-around of every buffer), a single block and a
+full mask.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_1801_02108_b200 as P
+from paper_1801_02108_b200 import _lib
+from oracle import sbnet_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FORCE_WIDE = 4      # SBN_DEBUG_FORCE_WIDE: the wide unit even where the single kernel applies
+WIDE_UNFUSED = 256  # SBN_DEBUG_WIDE_UNFUSED: IN and MID as two launches
+
+
+def _case(seed, n, h, w, c, m, density):
+    rng = np.random.default_rng(seed)
+    x = torch.from_numpy(rng.standard_normal((n, h, w, c)).astype(np.float32)).bfloat16()
+    u = P.random_unit_params(rng, c, m)
+    if density >= 1.0:
+        mk = np.ones((n, h, w), np.uint8)
+    else:
+        mk = np.concatenate([P.synth_mask_blobs((1, h, w), 1.0 - density, seed + i).numpy() for i in range(n)])
+    return x, u, P.BinaryMask(mk)
+
+
+def _run(x, mk, u, flags, inplace=False):
+    lib = _lib.load()
+    prev = lib.sbn_debug_set_flags(flags)
+    try:
+        y = P.sparse_residual_unit(P.Tensor4D(x.clone().cuda()), mk, u, (16, 16), inplace=inplace)
+        torch.cuda.synchronize()
+    finally:
+        lib.sbn_debug_set_flags(prev)
+    return y.data.cpu()
+
+
+def _oracle(x_bf16, u, mk):
+    def r(a):
+        return torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()
+    ud = {"pre": u.pre_activation}
+    for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
+        ud[f"w{i}"], ud[f"b{i}"] = r(fb.weights), r(fb.bias)
+        ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
+    return O.sparse_residual_unit(x_bf16.float().numpy(), mk.numpy(), ud, (16, 16))
+
+
+# (c, m, n, h, w, density)
+CASES = [
+    (96, 48, 2, 72, 60, 0.3),     # config-4 stage-0 shape, ragged borders
+    (192, 96, 2, 60, 44, 0.3),    # stage-1 shape (W2 streamed, one GEMM1 accumulator)
+    (64, 32, 2, 96, 80, 0.25),    # config-2 shape
+    (32, 16, 1, 50, 47, 0.5),
+    (128, 64, 1, 64, 64, 0.4),
+    (96, 48, 1, 30, 30, 1.0),     # full mask, one frame of 3x3 blocks
+    (192, 96, 1, 16, 16, 1.0),    # 2x2 blocks, three of them clipped by the frame border
+]
+
+
+@pytest.mark.parametrize("c,m,n,h,w,density", CASES)
+def test_fused_in_mid_bit_identical_to_three_launches(cuda_device, c, m, n, h, w, density):
+    x, u, mk = _case(c + h, n, h, w, c, m, density)
+    fused = _run(x, mk, u, FORCE_WIDE)
+    three = _run(x, mk, u, FORCE_WIDE | WIDE_UNFUSED)
+    assert torch.equal(fused, three), (c, m, n, h, w, (fused.float() - three.float()).abs().max().item())
+    err = O.rel_err(fused.float().numpy(), _oracle(x, u, mk))
+    assert err <= 2e-2, err
+    # in place == functional
+    assert torch.equal(_run(x, mk, u, FORCE_WIDE, inplace=True), fused)
+
+
+@pytest.mark.parametrize("c,m", [(96, 48), (192, 96), (64, 32), (128, 64)])
+def test_fused_in_mid_many_blocks_per_cta(cuda_device, c, m):
+    """Several hundred to a few thousand active blocks: every CTA walks many blocks, so the
+    window ring, both A2 buffers, the GEMM1/GEMM2 accumulators and (c = 192) the streamed W2
+    ring wrap around many times."""
+    n, h, w = (12, 200, 176) if c == 192 else (3, 400, 352)
+    x, u, mk = _case(7 + c, n, h, w, c, m, 0.35)
+    fused = _run(x, mk, u, FORCE_WIDE)
+    three = _run(x, mk, u, FORCE_WIDE | WIDE_UNFUSED)
+    assert torch.equal(fused, three)
+    assert torch.isfinite(fused.float()).all()
+
+
+def test_fused_in_mid_empty_mask(cuda_device):
+    x, u, _ = _case(3, 2, 40, 36, 96, 48, 0.5)
+    empty = P.BinaryMask(np.zeros((2, 40, 36), np.uint8))
+    assert torch.equal(_run(x, empty, u, FORCE_WIDE), x)

@@ -1,6 +1,6 @@
 """Sparse config-4 backbone only (no dense legs): whole-backbone and per-stage times from
 CUDA graphs, N frames at a density; for A/B runs of compile-time variants
-(SBN_LIB_PATH=... python tools/backbone_stages.py [frames] [density])."""
+(SBN_LIB_PATH=... SBN_FLAGS=... python tools/backbone_stages.py [frames] [density])."""
 import json
 import os
 import sys
@@ -16,6 +16,9 @@ from paper_1801_02108_b200 import perf  # noqa: E402
 frames = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 dens = float(sys.argv[2]) if len(sys.argv) > 2 else 0.2
 dev = torch.device("cuda", 0)
+if os.environ.get("SBN_FLAGS"):  # runtime debug flags (e.g. 256: wide unit IN and MID as two launches)
+    from paper_1801_02108_b200 import _lib
+    _lib.load().sbn_debug_set_flags(int(os.environ["SBN_FLAGS"]))
 hh, ww, cin = perf.DETECTOR_INPUT
 bb = P.build_backbone(perf.detector_stage_configs(), np.random.default_rng(4))
 x = P.Tensor4D(torch.randn(frames, hh, ww, cin, device=dev).bfloat16())
@@ -23,7 +26,7 @@ mk = np.concatenate([P.synth_mask_blobs((1, hh, ww), 1.0 - dens, s).numpy() for 
 mask = P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False)
 res = P.run_backbone(bb, x, mask)
 torch.cuda.synchronize()
-out = {"lib": os.environ.get("SBN_LIB_PATH", "default"), "frames": frames,
+out = {"lib": os.environ.get("SBN_LIB_PATH", "default"), "flags": os.environ.get("SBN_FLAGS", "0"), "frames": frames,
        "total_ms": round(bench._timed_graph(torch, bench.time_graph, lambda k: [P.run_backbone(bb, x, mask)
                                                                                for _ in range(k)], 5), 4),
        "stages_ms": []}

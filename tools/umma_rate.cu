@@ -12,7 +12,10 @@
 
 using namespace sbn;
 
-template <int N, int MODE>  // MODE 0: noswz plane layout, 1: noswz + 1-row shift, 2: SW128, 3: SW128 + 8-row shift
+// MODE 0: noswz plane layout, 1: noswz + 1-row shift, 2: SW128, 3: SW128 + 8-row shift,
+// 4: A SW64 (64-B rows, as the wide unit's IN / fused window chunks of 32 channels) x B plane layout,
+// 5: A SW128 x B plane layout
+template <int N, int MODE>
 __global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -41,6 +44,12 @@ __global__ void __launch_bounds__(128, 1) rate_kernel(long long* out, int iters)
       uint64_t ad, bd;
       if (MODE <= 1) {
         ad = tc::desc_kmajor_noswz(a0 + 2 * kk * PA + (MODE == 1 ? 16 * (1 + (i % 7)) : 0), PA, 128);
+        bd = tc::desc_kmajor_noswz(b0 + 2 * kk * PB, PB, 128);
+      } else if (MODE == 4) {
+        ad = tc::desc_kmajor_swz(a0 + (kk & 1) * 32, 512, 4);
+        bd = tc::desc_kmajor_noswz(b0 + 2 * kk * PB, PB, 128);
+      } else if (MODE == 5) {
+        ad = tc::desc_kmajor_swz(a0 + kk * 32, 1024, 2);
         bd = tc::desc_kmajor_noswz(b0 + 2 * kk * PB, PB, 128);
       } else {
         ad = tc::desc_kmajor_swz(a0 + kk * 32 + (MODE == 3 ? 1024 : 0), 1024, 2);
@@ -98,5 +107,10 @@ int main() {
   run<32, 1>("noswz + row shift", nsm);
   run<32, 0>("noswz plane layout", nsm);
   run<32, 2>("SW128", nsm);
+  run<48, 4>("A SW64 x B plane", nsm);
+  run<48, 5>("A SW128 x B plane", nsm);
+  run<96, 4>("A SW64 x B plane", nsm);
+  run<96, 5>("A SW128 x B plane", nsm);
+  run<32, 5>("A SW128 x B plane", nsm);
   return 0;
 }

@@ -7,7 +7,7 @@ import paper_1801_02108_b200 as P
 from paper_1801_02108_b200 import _lib
 from paper_1801_02108_b200.layers import residual_unit_into
 dev = torch.device("cuda", 0)
-lib = _lib.load(); lib.sbn_debug_set_flags(4)
+lib = _lib.load(); lib.sbn_debug_set_flags(4 | int(os.environ.get("SBN_FLAGS", "0")))
 x = torch.randn(64, 400, 400, 64, device=dev).bfloat16()
 mk = P.synth_mask_blobs((64, 400, 400), 0.8, 3).cuda()
 spec = P.unit_spec(tuple(x.shape), (16, 16)); idx = P.reduce_mask(mk, spec)
