@@ -151,8 +151,11 @@ struct __align__(64) WArgs {
   __nv_bfloat16* dst;        // IN: S1   MID: S2    OUT: out
   const uint8_t* wpk;        // this GEMM's packed weight chunks
   const float* par;          // this GEMM's parameter vectors
-  const uint8_t* wpk2;       // fused IN+MID: W2 chunks
-  const float* par2;         // fused IN+MID: MID's parameter vectors
+  const uint8_t* wpk2;       // fused unit: W2 chunks
+  const float* par2;         // fused unit: MID's parameter vectors
+  const uint8_t* wpk3;       // fused unit: W3 chunks
+  const float* par3;         // fused unit: OUT's parameter vectors
+  const __nv_bfloat16* rim;  // fused unit in place: rim snapshot (cap, 60, C), else null
   Geo g;
   const int32_t* idx;
   const int32_t* count;
@@ -713,31 +716,42 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   if (warp == 0) tc::tmem_free<Q::TALLOC>(tmem);
 }
 
-// ---- fused IN + MID for 16x16 blocks: S1 never leaves shared memory.
+// ---- fused unit for 16x16 blocks: IN, MID and OUT in one launch, S1 / S2 never leave
+// shared memory.
 // A block's window is exactly two 128-row tiles (window rows 0-7 and 8-15), so one CTA
-// runs the whole 3x3 of a block on its own: GEMM1 of both tiles -> A2 (the S1 rows of the
-// block, plane layout, in shared memory) -> GEMM2 as 9 row-shifted views of A2 -> S2.
-// Persistent CTAs take blocks j = blockIdx.x + k * gridDim.x.  The MMA issuer runs GEMM1 of
-// block k+1 ahead of GEMM2 of block k, so the GEMM1 epilogue of k+1 (warps 8-11) overlaps
-// GEMM2 of k and the GEMM2 epilogue of k (warps 12-15) overlaps GEMM2 of k+1.  The MMA
-// order per accumulator equals IN's / MID's (k-steps of GEMM1; (K-chunk, tap, k-step) of
-// GEMM2), so S2 is bit-identical to the three-launch path's.  OUT then runs unchanged.
-//   warps 0-7   BN1 + ReLU on landed window chunks (IN's code)
+// runs the whole bottleneck of a block on its own: GEMM1 of both tiles -> A2 (the S1 rows
+// of the block, plane layout) -> GEMM2 as 9 row-shifted views of A2 -> A3 (the S2 rows) ->
+// GEMM3 -> + b3 + x -> the block's interior.  Persistent CTAs take blocks
+// j = blockIdx.x + k * gridDim.x; the tensor pipe runs GEMM1(k+1), GEMM2(k), GEMM3(k-1)
+// back to back while the epilogues of the other blocks drain TMEM.  The MMA order per
+// accumulator equals IN's / MID's / OUT's (k-steps of GEMM1 and GEMM3; (K-chunk, tap,
+// k-step) of GEMM2) and the roundings are the same, so the output is bit-identical to the
+// three-launch path.
+// In place (x == out) a block's window rim is its neighbours' interior, which other CTAs
+// overwrite while this launch runs: the rims of all active blocks are snapshotted first
+// (unit_rim_snapshot, a separate launch) and the BN warps take rim pixels from the
+// snapshot.  Interior pixels are written only by their own block, after it read them.
+//   warps 0-3   BN1 + ReLU on landed window tiles (rim pixels from the snapshot)
+//   warps 4-7   epilogue 3: TMEM -> x + bf16(acc + b3) -> out (the block's interior)
 //   warps 8-11  epilogue 1: TMEM -> relu(acc*s2 + t2') * in-bounds -> A2 (bf16, smem)
-//   warps 12-15 epilogue 2: TMEM -> relu(acc*s3 + t3') -> S2 stack (global, plane-major)
-//   warp 16     loader: window chunks by 4-D TMA, W1 (+ W2) resident or W2 streamed
+//   warps 12-15 epilogue 2: TMEM -> relu(acc*s3 + t3') -> A3 (smem)
+//   warp 16     loader: window tiles by 4-D TMA (NKC1 boxes per tile); weights resident
 //   warp 17     MMA issuer
 constexpr int kFB = 16;                  // block size of the fused variant
+constexpr int kFBnThreads = 128;         // BN warps 0-3
 // CTA-0 event stamps per block k (diagnostics, tools/trace_fused.py)
-enum { kFevLoad = 0, kFevLanded = 1, kFevBn = 2, kFevG1 = 3, kFevE1 = 4, kFevG2 = 5, kFevE2a = 6, kFevE2 = 7, kFevG1s = 8, kFevG2e = 9, kFevE1s = 10 };
+enum { kFevLoad = 0, kFevLanded = 1, kFevBn = 2, kFevG1 = 3, kFevE1 = 4, kFevG2 = 5, kFevE2a = 6, kFevE2 = 7,
+       kFevG1s = 8, kFevG3 = 9, kFevE1s = 10, kFevE3 = 11 };
 constexpr int kFR2 = 296;                // A2 rows: 256 + 2*16 + 2 = 290, rounded to 8
 constexpr int kFPA2 = kFR2 * 16;         // A2 plane stride
+constexpr int kFPA3 = 256 * 16;          // A3 plane stride (rows q = oy*16 + ox of both tiles)
 constexpr int kFBudget = 232448 - 1024;  // opt-in dynamic smem minus the static barriers
 
 template <int C, int M>
 struct FCfg {
   using Q1 = WCfg<C, M, kIn>;
   using Q2 = WCfg<M, M, kMid>;
+  using Q3 = WCfg<M, C, kOut>;
   static constexpr int KC1 = Q1::KC, NKC1 = C / KC1, ROWB = KC1 * 2;
   static constexpr uint32_t SWZ = Q1::SWZ;
   static constexpr int ACH = 128 * ROWB;          // one window chunk: 128 rows x KC1 ch (swizzled)
@@ -746,73 +760,56 @@ struct FCfg {
   static constexpr int KC2 = Q2::KC, NKC2 = M / KC2, P2 = KC2 / 8;
   static constexpr int WCH2 = Q2::WCH, PW2 = Q2::PW;
   static constexpr int W2B = (int)Q2::WBYTES;
+  static constexpr int PW3 = Q3::PW, W3B = (int)Q3::WBYTES;
   static constexpr int A2B = (M / 8) * kFPA2;
-  static constexpr int PAR1 = Q1::NPAR, PAR2 = Q2::NPAR;
-  static constexpr int PARB = (PAR1 + PAR2) * 4 / 128 * 128 + 128;
-  static constexpr int ITEMS = Q1::ITEMS;
+  static constexpr int A3B = (M / 8) * kFPA3;
+  static constexpr int PAR1 = Q1::NPAR, PAR2 = Q2::NPAR, PAR3 = Q3::NPAR;
+  static constexpr int PARB = (PAR1 + PAR2 + PAR3) * 4 / 128 * 128 + 128;
   // the window ring holds whole tiles: a slot = NKC1 chunks (one TMA box each) completing
   // on one barrier, BN'd by one group, consumed by one MMA wait and released by one commit
   // (the single MMA thread spends ~500 cycles of wait + commit latency per ring step)
   static constexpr int TSB = NKC1 * ACH;
-  // budget: prefer two A2 buffers, then W2 resident, then the deepest window ring (<= two
-  // blocks of tiles)
-  static constexpr long FIX2 = 2L * A2B + W1B + PARB;
-  static constexpr bool RES2 = FIX2 + W2B + 2L * TSB <= kFBudget;
-  static constexpr int SW0 = RES2 ? 0 : 4;
-  static constexpr long WREG0 = RES2 ? (long)W2B : (long)SW0 * WCH2;
-  static constexpr int NA2 = FIX2 + WREG0 + 2L * TSB <= kFBudget ? 2 : 1;
-  static constexpr long FIX = (long)NA2 * A2B + W1B + PARB + WREG0;
+  static constexpr long FIX = 2L * A2B + A3B + W1B + W2B + W3B + PARB;
   static constexpr int SAF = (int)((kFBudget - FIX) / TSB);
-  // even: the two BN groups take alternate tiles, so with an even ring every slot always
-  // belongs to the same group (an odd ring would let a group wait on a slot two phases
-  // ahead of the tile it expects)
-  static constexpr int SA0 = SAF > 4 ? 4 : SAF;
-  static constexpr int SA = SA0 / 2 * 2;
-  // streamed W2: what is left deepens the weight ring
-  static constexpr int SWX = RES2 ? 0 : (int)((kFBudget - FIX - (long)SA * TSB) / WCH2);
-  static constexpr int SW = RES2 ? 0 : (SW0 + SWX > 12 ? 12 : SW0 + SWX);
-  static constexpr long WREG2 = RES2 ? (long)W2B : (long)SW * WCH2;
-  static constexpr int SWB = SW > 0 ? SW : 1;
-  // TMEM: NB1 GEMM1 tile accumulators (M columns each) + two GEMM2 block accumulators (2M)
-  static constexpr int NB1 = (512 / M - 4) >= 4 ? 4 : (512 / M - 4);
-  static constexpr bool OK = M % 16 == 0 && M <= 256 && NB1 >= 1 && SA >= 2 && C % KC1 == 0 && RES2;
+  static constexpr int SA = SAF > 4 ? 4 : SAF;  // <= two blocks of tiles
+  // TMEM: NB1 GEMM1 tile accumulators (M columns each), two GEMM2 block accumulators (2M),
+  // one GEMM3 block accumulator (2C)
+  static constexpr int NB1R = (512 - 4 * M - 2 * C) / M;
+  static constexpr int NB1 = NB1R >= 4 ? 4 : NB1R;
+  // (the in-place rim snapshot, 60 pixels x C per block, reuses the S1 stack: b*b x M per block)
+  static constexpr bool OK = M % 16 == 0 && C % 16 == 0 && C <= 256 && NB1 >= 1 && SA >= 2 && C % KC1 == 0 &&
+                             60 * C <= 256 * M;
   static constexpr int COL2 = (NB1 > 0 ? NB1 : 1) * M;
-  static constexpr int TCOLS = COL2 + 4 * M;
+  static constexpr int COL3 = COL2 + 4 * M;
+  static constexpr int TCOLS = COL3 + 2 * C;
   static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
   static constexpr bool BOTH_FIRST = NB1 >= 4;  // GEMM1 of both tiles of k+1 before GEMM2 of k
-  static constexpr int OFF_A2 = SA * TSB;
-  static constexpr int OFF_W1 = OFF_A2 + NA2 * A2B;
+  static constexpr int OFF_A2 = (SA > 0 ? SA : 1) * TSB;
+  static constexpr int OFF_A3 = OFF_A2 + 2 * A2B;
+  static constexpr int OFF_W1 = OFF_A3 + A3B;
   static constexpr int OFF_W2 = OFF_W1 + W1B;
-  static constexpr int OFF_PAR = OFF_W2 + (int)WREG2;
+  static constexpr int OFF_W3 = OFF_W2 + W2B;
+  static constexpr int OFF_PAR = OFF_W3 + W3B;
   static constexpr int SMEM = OFF_PAR + PARB;
 };
 
-// The issue order shared by the loader and the MMA issuer: GEMM1 tiles g1(k, t) and GEMM2
-// blocks g2(k), k over this CTA's nb blocks.
-// 32 accumulator columns [g0, g0 + 32) of this thread's TMEM lane (16 when only 16 remain),
-// one load and one wait
-template <int M>
-__device__ __forceinline__ void tmem_ld_group(uint32_t acc, int g0, float (&v)[32]) {
-  if (g0 + 32 <= M) {
-    tc::tmem_ld32(acc + g0, v);
-  } else {
-    float h[16];
-    tc::tmem_ld16(acc + g0, h);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = h[i];
-    if (g0 + 16 < M) {
-      tc::tmem_ld16(acc + g0 + 16, h);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[16 + i] = h[i];
-    } else {
-#pragma unroll
-      for (int i = 16; i < 32; ++i) v[i] = 0.f;
-    }
-  }
+// per-block stamps (CTA 0) only in a diagnostics build: the stamps' live registers make the
+// single-thread MMA issuer spill at 96 registers per thread
+//   tools/build_variant.sh trace -DSBN_TRACE_FUSED; SBN_LIB_PATH=tools/bin/trace.so python tools/trace_fused.py
+__device__ __forceinline__ void ftrace(const WArgs& a, int ev, int k) {
+#ifdef SBN_TRACE_FUSED
+  wtrace(a, ev, k);
+#else
+  (void)a;
+  (void)ev;
+  (void)k;
+#endif
 }
 
-template <bool BOTH_FIRST, typename G1, typename G2>
-__device__ __forceinline__ void fused_schedule(int nb, G1&& g1, G2&& g2) {
+// The issue order shared by the loader and the MMA issuer: GEMM1 tiles g1(k, t), GEMM2
+// blocks g2(k), GEMM3 blocks g3(k), k over this CTA's nb blocks.
+template <bool BOTH_FIRST, typename G1, typename G2, typename G3>
+__device__ __forceinline__ void fused_schedule(int nb, G1&& g1, G2&& g2, G3&& g3) {
   if (nb <= 0) return;
   g1(0, 0);
   g1(0, 1);
@@ -826,6 +823,23 @@ __device__ __forceinline__ void fused_schedule(int nb, G1&& g1, G2&& g2) {
       g2(k);
       if (more) g1(k + 1, 1);
     }
+    if (k > 0) g3(k - 1);
+  }
+  g3(nb - 1);
+}
+
+// 32 accumulator columns [g0, g0 + 32) of this thread's TMEM lane (16 when only 16 remain)
+template <int N>
+__device__ __forceinline__ void tmem_ld_group(uint32_t acc, int g0, float (&v)[32]) {
+  if (g0 + 32 <= N) {
+    tc::tmem_ld32(acc + g0, v);
+  } else {
+    float h[16];
+    tc::tmem_ld16(acc + g0, h);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = h[i];
+#pragma unroll
+    for (int i = 16; i < 32; ++i) v[i] = 0.f;
   }
 }
 
@@ -833,48 +847,51 @@ template <int C, int M>
 __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const __grid_constant__ WArgs a) {
   using F = FCfg<C, M>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t a_load[F::SA], a_full[F::SA], a_empty[F::SA], w_full[F::SWB], w_empty[F::SWB], wres;
-  __shared__ uint64_t a2_full[F::NA2], a2_empty[F::NA2], acc1_full[F::NB1], acc1_empty[F::NB1];
-  __shared__ uint64_t acc2_full[2], acc2_empty[2];
+  __shared__ uint64_t a_load[F::SA], a_full[F::SA], a_empty[F::SA], wres;
+  __shared__ uint64_t a2_full[2], a2_empty[2], acc1_full[F::NB1], acc1_empty[F::NB1];
+  __shared__ uint64_t acc2_full[2], acc2_empty[2], a3_full, a3_empty, acc3_full, acc3_empty;
   __shared__ uint32_t tslot;
   uint8_t* A1 = smem;
   uint8_t* A2 = smem + F::OFF_A2;
+  uint8_t* A3 = smem + F::OFF_A3;
   uint8_t* W1 = smem + F::OFF_W1;
   uint8_t* W2 = smem + F::OFF_W2;
+  uint8_t* W3 = smem + F::OFF_W3;
   float* par1 = reinterpret_cast<float*>(smem + F::OFF_PAR);
   float* par2 = par1 + F::PAR1;
+  float* par3 = par2 + F::PAR2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Geo& g = a.g;
   constexpr int kLWarp = 16, kMWarp = 17;
+  constexpr int OB = kFB - 2;
 
   if (tid == 0) {
     for (int s = 0; s < F::SA; ++s) {
       tc::mbar_init(&a_load[s], 1);
-      tc::mbar_init(&a_full[s], kAThreads / 2);
+      tc::mbar_init(&a_full[s], kFBnThreads);
       tc::mbar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < F::SWB; ++s) {
-      tc::mbar_init(&w_full[s], 1);
-      tc::mbar_init(&w_empty[s], 1);
-    }
     tc::mbar_init(&wres, 1);
-    for (int s = 0; s < F::NA2; ++s) {
+    for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&a2_full[s], 128);
       tc::mbar_init(&a2_empty[s], 1);
+      tc::mbar_init(&acc2_full[s], 1);
+      tc::mbar_init(&acc2_empty[s], 128);
     }
     for (int s = 0; s < F::NB1; ++s) {
       tc::mbar_init(&acc1_full[s], 1);
       tc::mbar_init(&acc1_empty[s], 128);
     }
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(&acc2_full[s], 1);
-      tc::mbar_init(&acc2_empty[s], 128);
-    }
+    tc::mbar_init(&a3_full, 128);
+    tc::mbar_init(&a3_empty, 1);
+    tc::mbar_init(&acc3_full, 1);
+    tc::mbar_init(&acc3_empty, 128);
     tc::mbar_fence_init();
   }
   if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
   for (int i = tid; i < F::PAR1; i += kWideThreads) par1[i] = a.par[i];
   for (int i = tid; i < F::PAR2; i += kWideThreads) par2[i] = a.par2[i];
+  for (int i = tid; i < F::PAR3; i += kWideThreads) par3[i] = a.par3[i];
   if (warp == 0) tc::tmem_alloc<F::TALLOC>(&tslot);
   tc::fence_before();
   __syncthreads();
@@ -883,69 +900,146 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
   tc::pdl_trigger();
   if (tid == kLWarp * 32) {
     // resident weights land under the previous kernel's tail (they do not depend on it)
-    tc::mbar_expect_tx(&wres, (uint32_t)(F::W1B + (F::RES2 ? F::W2B : 0)));
+    tc::mbar_expect_tx(&wres, (uint32_t)(F::W1B + F::W2B + F::W3B));
     for (int c = 0; c < F::Q1::CHUNKS; ++c)
       tc::bulk_g2s(W1 + (size_t)c * F::WCH1, a.wpk + (size_t)c * F::WCH1, F::WCH1, &wres);
-    if (F::RES2)
-      for (int c = 0; c < F::Q2::CHUNKS; ++c)
-        tc::bulk_g2s(W2 + (size_t)c * F::WCH2, a.wpk2 + (size_t)c * F::WCH2, F::WCH2, &wres);
+    for (int c = 0; c < F::Q2::CHUNKS; ++c)
+      tc::bulk_g2s(W2 + (size_t)c * F::WCH2, a.wpk2 + (size_t)c * F::WCH2, F::WCH2, &wres);
+    for (int c = 0; c < F::Q3::CHUNKS; ++c)
+      tc::bulk_g2s(W3 + (size_t)c * F::Q3::WCH, a.wpk3 + (size_t)c * F::Q3::WCH, F::Q3::WCH, &wres);
   }
-  tc::pdl_wait();  // x and the index list of the previous launches are visible
+  tc::pdl_wait();  // x, the rim snapshot and the index list of the previous launches are visible
   const int B = ld_count(a.count, a.cap);
   const int G = gridDim.x;
   const int nb = B > (int)blockIdx.x ? (B - 1 - (int)blockIdx.x) / G + 1 : 0;
 
-  if (tid < kAThreads) {
-    // ------------------------------------------------ BN1 + ReLU on landed chunks (as IN)
+  if (warp < 4) {
+    // ------------------------------------------------ BN1 + ReLU on landed tiles (as IN)
+    // all BN threads work on one tile at a time (the loader runs SA tiles ahead)
     const float* s1 = par1;
     constexpr int PR = F::ROWB / 16;
-    constexpr int TG = kAThreads / 2;
-    const int grp_id = tid / TG, gt = tid % TG;
+    constexpr int TG = kFBnThreads;
+    constexpr int IT = 128 * PR / TG;  // pieces per thread per chunk
+    constexpr int BATCH = IT < 8 ? IT : 8;
+    static_assert(IT % BATCH == 0 && TG % PR == 0, "BN batches");
+    // physical 16-B slot of logical channel group q in row r (the TMA swizzle)
+    auto swz = [](int r) { return F::KC1 == 64 ? (r & 7) : ((r >> 1) & 3); };
+    const int gt = tid;
+    const Rim rim{kFB, kFB, 1};
     int tl = 0;
-    for (int k = 0; k < nb; ++k)
+    for (int k = 0; k < nb; ++k) {
+      const int j = (int)blockIdx.x + k * G;
       for (int t = 0; t < 2; ++t, ++tl) {
-        if ((tl & 1) != grp_id) continue;
         const int s = tl % F::SA;
         tc::mbar_wait(&a_load[s], (tl / F::SA) & 1);
-        if (gt == 0 && t == 0) wtrace(a, kFevLanded, k);
+        if (gt == 0 && t == 0) ftrace(a, kFevLanded, k);
+        if (a.rim) {
+          // in place: the rim pixels of the landed window may already hold a neighbour's
+          // output; overwrite them with the snapshot (16-B cp.async per piece, one wait)
+#pragma unroll 1
+          for (int kc = 0; kc < F::NKC1; ++kc) {
+            uint8_t* A = A1 + s * F::TSB + kc * F::ACH;
+#pragma unroll 4
+            for (int jj = 0; jj < IT; ++jj) {
+              const int i = gt + jj * TG;
+              const int r = i / PR, grp = i % PR;
+              const int wy = 8 * t + (r >> 4), wx = r & 15;
+              if (wy == 0 || wy == kFB - 1 || wx == 0 || wx == kFB - 1)
+                tc::cp_async16(A + r * F::ROWB + (grp ^ swz(r)) * 16,
+                               a.rim + ((size_t)j * rim.pixels() + rim.index(wy, wx)) * C + kc * F::KC1 + grp * 8, true);
+            }
+          }
+          tc::cp_async_commit();
+          tc::cp_async_wait<0>();
+        }
+#pragma unroll 1
         for (int kc = 0; kc < F::NKC1; ++kc) {
           uint8_t* A = A1 + s * F::TSB + kc * F::ACH;
-          uint4 raw[F::ITEMS];
+          // this thread's logical channel group is fixed (TG % PR == 0): its BN vectors
+          // are loaded once per chunk
+          const int grp = gt % PR;
+          const uint4 sg4 = *reinterpret_cast<const uint4*>(s1 + (kc * F::KC1 + grp * 8) / 2);
+          const uint4 vv4 = *reinterpret_cast<const uint4*>(s1 + C / 2 + (kc * F::KC1 + grp * 8) / 2);
+#pragma unroll 1
+          for (int b0 = 0; b0 < IT; b0 += BATCH) {
+            uint4 raw[BATCH];
 #pragma unroll
-          for (int j = 0; j < F::ITEMS; ++j) {
-            const int i = gt + j * TG;
-            if (i < 128 * PR)
+            for (int jj = 0; jj < BATCH; ++jj) {
+              const int r = (gt + (b0 + jj) * TG) / PR;
               asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                           : "=r"(raw[j].x), "=r"(raw[j].y), "=r"(raw[j].z), "=r"(raw[j].w)
-                           : "r"(tc::smem_u32(A + i * 16)));
-          }
-#pragma unroll
-          for (int j = 0; j < F::ITEMS; ++j) {
-            const int i = gt + j * TG;
-            if (i >= 128 * PR) break;
-            const int r = i / PR, qp = i % PR;
-            const int grp = qp ^ (F::KC1 == 64 ? (r & 7) : ((r >> 1) & 3));
-            const uint4 sg4 = *reinterpret_cast<const uint4*>(s1 + (kc * F::KC1 + grp * 8) / 2);
-            const uint4 vv4 = *reinterpret_cast<const uint4*>(s1 + C / 2 + (kc * F::KC1 + grp * 8) / 2);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[j]);
-            const __nv_bfloat162* hs = reinterpret_cast<const __nv_bfloat162*>(&sg4);
-            const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&vv4);
-            const __nv_bfloat162 z2 = __float2bfloat162_rn(0.f);
-            uint32_t o[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const __nv_bfloat162 y = __hmax2(__hfma2(h[e], hs[e], hv[e]), z2);
-              o[e] = *reinterpret_cast<const uint32_t*>(&y);
+                           : "=r"(raw[jj].x), "=r"(raw[jj].y), "=r"(raw[jj].z), "=r"(raw[jj].w)
+                           : "r"(tc::smem_u32(A + r * F::ROWB + (grp ^ swz(r)) * 16)));
             }
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(A + i * 16)), "r"(o[0]),
-                         "r"(o[1]), "r"(o[2]), "r"(o[3])
-                         : "memory");
+#pragma unroll
+            for (int jj = 0; jj < BATCH; ++jj) {
+              const int r = (gt + (b0 + jj) * TG) / PR;
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[jj]);
+              const __nv_bfloat162* hs = reinterpret_cast<const __nv_bfloat162*>(&sg4);
+              const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&vv4);
+              const __nv_bfloat162 z2 = __float2bfloat162_rn(0.f);
+              uint32_t o[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const __nv_bfloat162 y = __hmax2(__hfma2(h[e], hs[e], hv[e]), z2);
+                o[e] = *reinterpret_cast<const uint32_t*>(&y);
+              }
+              asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(A + r * F::ROWB + (grp ^ swz(r)) * 16)),
+                           "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                           : "memory");
+            }
           }
         }
         tc::fence_async_smem();
         tc::mbar_arrive(&a_full[s]);
-        if (gt == 0 && t == 1) wtrace(a, kFevBn, k);
+        if (gt == 0 && t == 1) ftrace(a, kFevBn, k);
       }
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------ epilogue 3: TMEM -> x + bf16(acc + b3) -> out
+    // OUT's epilogue at the block's clipped interior; the residual is read from out (= x in
+    // place, the clone of x otherwise).  Each thread issues its row's C / 8 residual loads
+    // before it drains the accumulator, so they are all in flight at once.
+    const int qd = warp & 3, r = qd * 32 + lane;
+    const uint32_t lanes = (uint32_t)(qd * 32) << 16;
+    const float* b3 = par3;
+    for (int k = 0; k < nb; ++k) {
+      const int j = (int)blockIdx.x + k * G;
+      const int n = __ldg(a.idx + 3 * j), by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
+      tc::mbar_wait(&acc3_full, k & 1);
+      tc::fence_after();
+#pragma unroll 1
+      for (int u = 0; u < 2; ++u) {
+        const int q = u * 128 + r, oy = q >> 4, ox = q & 15;
+        const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+        const bool store = oy < OB && ox < OB && Y < g.oh && X < g.ow;
+        uint4* dp = reinterpret_cast<uint4*>(a.dst + (((long)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * C);
+        uint4 xr[C / 8];
+#pragma unroll
+        for (int e = 0; e < C / 8; ++e) xr[e] = tc::ld_v4_pred(dp + e, store);
+        const uint32_t acc = tmem + lanes + F::COL3 + u * C;
+#pragma unroll
+        for (int c0 = 0; c0 < C; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(acc + c0, v);
+          uint32_t o[8];
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) {
+            const float2 bb = *reinterpret_cast<const float2*>(b3 + c0 + 2 * q2);
+            const __nv_bfloat162 st = __floats2bfloat162_rn(v[2 * q2] + bb.x, v[2 * q2 + 1] + bb.y);
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[c0 / 8 + q2 / 4]);
+            const float2 uf = __bfloat1622float2(st), xf = __bfloat1622float2(xh[q2 % 4]);
+            o[q2] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
+          }
+          if (store) {
+            dp[c0 / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+            dp[c0 / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive(&acc3_empty);
+      if (r == 0) ftrace(a, kFevE3, k);
+    }
   } else if (warp < 12) {
     // ------------------------------------------------ epilogue 1: TMEM -> A2 (S1 rows)
     const int qd = warp & 3, r = qd * 32 + lane;
@@ -954,8 +1048,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
     for (int k = 0; k < nb; ++k) {
       const int j = (int)blockIdx.x + k * G;
       const int by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-      const int ab = k % F::NA2;
-      tc::mbar_wait(&a2_empty[ab], ((k / F::NA2) & 1) ^ 1);
+      const int ab = k & 1;
+      tc::mbar_wait(&a2_empty[ab], ((k >> 1) & 1) ^ 1);
       uint8_t* A2b = A2 + ab * F::A2B;
       for (int t = 0; t < 2; ++t) {
         const int ti = 2 * k + t, b1 = ti % F::NB1;
@@ -964,7 +1058,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         const bool valid = y >= 0 && y < g.h && x >= 0 && x < g.w;
         tc::mbar_wait(&acc1_full[b1], (ti / F::NB1) & 1);
         tc::fence_after();
-        if (t == 0 && r == 0) wtrace(a, kFevE1s, k);
+        if (t == 0 && r == 0) ftrace(a, kFevE1s, k);
         const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + b1 * M;
 #pragma unroll
         for (int g0 = 0; g0 < M; g0 += 32) {
@@ -974,12 +1068,12 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
           for (int hh = 0; hh < 2; ++hh) {
             const int c0 = g0 + 16 * hh;
             if (c0 >= M) break;
+            const float* w = v + 16 * hh;
             uint32_t o[8];
 #pragma unroll
             for (int q = 0; q < 8; q += 2) {
               const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q);
               const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q);
-              const float* w = v + 16 * hh;
               const float u0 = fmaxf(fmaf(w[2 * q], s4.x, t4.x), 0.f);
               const float u1 = fmaxf(fmaf(w[2 * q + 1], s4.y, t4.y), 0.f);
               const float u2 = fmaxf(fmaf(w[2 * q + 2], s4.z, t4.z), 0.f);
@@ -1001,30 +1095,28 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
       }
       tc::fence_async_smem();
       tc::mbar_arrive(&a2_full[ab]);
-      if (r == 0) wtrace(a, kFevE1, k);
+      if (r == 0) ftrace(a, kFevE1, k);
     }
   } else if (warp < 16) {
-    // ------------------------------------------------ epilogue 2: TMEM -> S2 stack
+    // ------------------------------------------------ epilogue 2: TMEM -> A3 (S2 rows)
     const int qd = warp & 3, r = qd * 32 + lane;
-    const float* sc = par2 + M;  // s3
-    const float* sh = sc + M;    // t3' (b2 folded)
-    constexpr int OB = kFB - 2;
-    for (int k = 0; k < nb; ++k) {
-      const int j = (int)blockIdx.x + k * G, b2 = k & 1;
+    const uint32_t lanes = (uint32_t)(qd * 32) << 16;
+    auto epi2 = [&](int k) {
+      const float* sc = par2 + M;  // s3
+      const float* sh = sc + M;    // t3' (b2 folded)
+      const int b2 = k & 1;
       tc::mbar_wait(&acc2_full[b2], (k >> 1) & 1);
+      tc::mbar_wait(&a3_empty, (k & 1) ^ 1);  // GEMM3 of the previous block has read A3
       tc::fence_after();
-      if (r == 0) wtrace(a, kFevE2a, k);
+      if (r == 0) ftrace(a, kFevE2a, k);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int q = u * 128 + r, oy = q >> 4, ox = q & 15;
-        const bool store = oy < OB && ox < OB;
-        const long drow = (long)j * OB * OB + oy * OB + ox;
-        const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + F::COL2 + b2 * 2 * M + u * M;
+        const int q = u * 128 + r;
+        const uint32_t acc = tmem + lanes + F::COL2 + b2 * 2 * M + u * M;
 #pragma unroll
         for (int g0 = 0; g0 < M; g0 += 32) {
           float v[32];
           tmem_ld_group<M>(acc, g0, v);
-          if (!store) continue;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int c0 = g0 + 16 * hh;
@@ -1039,20 +1131,27 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
               o[q2 + 1] =
                   tc::pack_bf16(fmaxf(fmaf(w[2 * q2 + 2], s4.z, t4.z), 0.f), fmaxf(fmaf(w[2 * q2 + 3], s4.w, t4.w), 0.f));
             }
-            uint4* pl = reinterpret_cast<uint4*>(a.dst) + (long)(c0 / 8) * a.dst_rows + drow;
-            pl[0] = make_uint4(o[0], o[1], o[2], o[3]);
-            pl[a.dst_rows] = make_uint4(o[4], o[5], o[6], o[7]);
+            uint8_t* pl = A3 + (c0 / 8) * kFPA3 + q * 16;
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl)), "r"(o[0]), "r"(o[1]),
+                         "r"(o[2]), "r"(o[3])
+                         : "memory");
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl + kFPA3)), "r"(o[4]),
+                         "r"(o[5]), "r"(o[6]), "r"(o[7])
+                         : "memory");
           }
         }
       }
+      tc::fence_async_smem();
+      tc::mbar_arrive(&a3_full);
       tc::fence_before();
       tc::mbar_arrive(&acc2_empty[b2]);
-      if (r == 0) wtrace(a, kFevE2, k);
-    }
+      if (r == 0) ftrace(a, kFevE2, k);
+    };
+    for (int k = 0; k < nb; ++k) epi2(k);
   } else if (warp == kLWarp) {
     // ------------------------------------------------ loader
     if (lane == 0) {
-      int tl = 0, wit = 0;
+      int tl = 0;
       int cur_k = -1, cn = 0, cy = 0, cx = 0;
       auto g1 = [&](int k, int t) {
         if (k != cur_k) {
@@ -1064,36 +1163,26 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         }
         const int s = tl % F::SA;
         tc::mbar_wait(&a_empty[s], ((tl / F::SA) & 1) ^ 1);
-        if (t == 0) wtrace(a, kFevLoad, k);
+        if (t == 0) ftrace(a, kFevLoad, k);
         tc::mbar_expect_tx(&a_load[s], (uint32_t)F::TSB);
         for (int kc = 0; kc < F::NKC1; ++kc)
           tma_4d(A1 + s * F::TSB + kc * F::ACH, &a.tmap, kc * F::KC1, cx, cy + 8 * t, cn, &a_load[s]);
         ++tl;
       };
-      auto g2 = [&](int) {
-        if constexpr (F::RES2) return;
-        for (int kc = 0; kc < F::NKC2; ++kc)
-          for (int tap = 0; tap < 9; ++tap, ++wit) {
-            const int sw = wit % F::SWB;
-            tc::mbar_wait(&w_empty[sw], ((wit / F::SWB) & 1) ^ 1);
-            tc::mbar_expect_tx(&w_full[sw], F::WCH2);
-            tc::bulk_g2s(W2 + sw * F::WCH2, a.wpk2 + (size_t)(kc * 9 + tap) * F::WCH2, F::WCH2, &w_full[sw]);
-          }
-      };
-      fused_schedule<F::BOTH_FIRST>(nb, g1, g2);
+      fused_schedule<F::BOTH_FIRST>(nb, g1, [](int) {}, [](int) {});
     }
     __syncwarp();
   } else if (warp == kMWarp) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, M);
-      int tl = 0, wit = 0;
+      int tl = 0;
       tc::mbar_wait(&wres, 0);
       auto g1 = [&](int k, int t) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(128, M);
         const int ti = 2 * k + t, b1 = ti % F::NB1;
         tc::mbar_wait(&acc1_empty[b1], ((ti / F::NB1) & 1) ^ 1);
         tc::fence_after();
-        if (t == 0) wtrace(a, kFevG1s, k);
+        if (t == 0) ftrace(a, kFevG1s, k);
         const uint32_t acc = tmem + b1 * M;
         const int s = tl % F::SA;
         tc::mbar_wait(&a_full[s], (tl / F::SA) & 1);
@@ -1110,24 +1199,22 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         tc::mma_commit(&a_empty[s]);
         ++tl;
         tc::mma_commit(&acc1_full[b1]);
-        if (t == 1) wtrace(a, kFevG1, k);
+        if (t == 1) ftrace(a, kFevG1, k);
       };
       auto g2 = [&](int k) {
-        const int b2 = k & 1, ab = k % F::NA2;
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(128, M);
+        const int b2 = k & 1;
         tc::mbar_wait(&acc2_empty[b2], ((k >> 1) & 1) ^ 1);
-        tc::mbar_wait(&a2_full[ab], (k / F::NA2) & 1);
+        tc::mbar_wait(&a2_full[b2], (k >> 1) & 1);
         tc::fence_after();
-        wtrace(a, kFevG2, k);
+        ftrace(a, kFevG2, k);
         const uint32_t acc = tmem + F::COL2 + b2 * 2 * M;
-        const uint32_t a2base = tc::smem_u32(A2 + ab * F::A2B);
+        const uint32_t a2base = tc::smem_u32(A2 + b2 * F::A2B);
+#pragma unroll 1
         for (int kc = 0; kc < F::NKC2; ++kc)
-          for (int tap = 0; tap < 9; ++tap, ++wit) {
-            const int sw = F::RES2 ? 0 : wit % F::SWB;
-            if (!F::RES2) {
-              tc::mbar_wait(&w_full[sw], (wit / F::SWB) & 1);
-              tc::fence_after();
-            }
-            const uint32_t wbase = tc::smem_u32(W2 + (F::RES2 ? (kc * 9 + tap) * F::WCH2 : sw * F::WCH2));
+#pragma unroll 1
+          for (int tap = 0; tap < 9; ++tap) {  // (rolled: the unrolled tap loop made the issuer spill)
+            const uint32_t wbase = tc::smem_u32(W2 + (kc * 9 + tap) * F::WCH2);
             const int shift = (tap / 3) * kFB + (tap % 3);
 #pragma unroll
             for (int u = 0; u < 2; ++u)
@@ -1137,13 +1224,28 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
                              tc::desc_kmajor_noswz(a2base + (kc * F::P2 + 2 * kk) * kFPA2 + (u * 128 + shift) * 16,
                                                    kFPA2, 128),
                              tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW2, F::PW2, 128), idesc, (kc | tap | kk) > 0);
-            if (!F::RES2) tc::mma_commit(&w_empty[sw]);
           }
-        tc::mma_commit(&a2_empty[ab]);
+        tc::mma_commit(&a2_empty[b2]);
         tc::mma_commit(&acc2_full[b2]);
-        wtrace(a, kFevG2e, k);
       };
-      fused_schedule<F::BOTH_FIRST>(nb, g1, g2);
+      auto g3 = [&](int k) {
+        constexpr uint32_t idesc = tc::idesc_bf16_f32(128, C);
+        tc::mbar_wait(&acc3_empty, (k & 1) ^ 1);
+        tc::mbar_wait(&a3_full, k & 1);
+        tc::fence_after();
+        ftrace(a, kFevG3, k);
+        const uint32_t a3base = tc::smem_u32(A3), wbase = tc::smem_u32(W3);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int kk = 0; kk < M / 16; ++kk)
+            tc::mma_bf16(tmem + F::COL3 + u * C,
+                         tc::desc_kmajor_noswz(a3base + 2 * kk * kFPA3 + u * 128 * 16, kFPA3, 128),
+                         tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW3, F::PW3, 128), idesc, kk > 0);
+        tc::mma_commit(&a3_empty);
+        tc::mma_commit(&acc3_full);
+      };
+      fused_schedule<F::BOTH_FIRST>(nb, g1, g2, g3);
     }
     __syncwarp();
   }
@@ -1263,7 +1365,7 @@ int launch_wide(const WArgs& a, long max_tiles, cudaStream_t s, const char* what
   return launch_status(what);
 }
 
-// the fused IN + MID launch applies to 16x16 blocks when its buffers fit
+// the fused one-launch unit applies to 16x16 blocks when its buffers fit
 template <int C, int M>
 bool fused_ok(int b) {
   if constexpr (FCfg<C, M>::OK) {
@@ -1292,7 +1394,7 @@ int launch_fused(const WArgs& a, long cap, cudaStream_t s) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, a);
-    return launch_status("residual_unit_wide_in_mid");
+    return launch_status("residual_unit_wide_fused");
   } else {
     (void)a;
     (void)cap;
@@ -1335,31 +1437,37 @@ int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const i
   }
   int st = 0;
   if (fused_ok<C, M>(b)) {
-    // IN + MID in one launch: window -> A2 in shared memory -> S2
-    a.dst = (__nv_bfloat16*)s2;
-    a.dst_rows = rows2;
+    // the whole unit in one launch; in place, the rims of the active windows are
+    // snapshotted first (into the S1 stack, which this path does not use)
+    if (x == out) {
+      st = unit_rim_snapshot(x, 2, C, g, 1, idx, count, cap, s1, s);
+      if (st) return st;
+      a.rim = (const __nv_bfloat16*)s1;
+    }
+    a.dst = (__nv_bfloat16*)out;
     a.wpk = img + L.w1;
     a.par = (const float*)(img + L.p1);
     a.wpk2 = img + L.w2;
     a.par2 = (const float*)(img + L.p2);
-    st = launch_fused<C, M>(a, cap, s);
-  } else {
-    a.dst = (__nv_bfloat16*)s1;
-    a.dst_rows = rows1;
-    a.wpk = img + L.w1;
-    a.par = (const float*)(img + L.p1);
-    st = launch_wide<C, M, kIn>(a, ((long)cap * a.S + a.G - 1) / a.G, s, "residual_unit_wide_in");
-    if (st) return st;
-    // MID: S1 -> S2 (3x3 valid); plane runs by 1-D bulk copies
-    a.stack = s1;
-    a.src_rows = rows1;
-    a.dst = (__nv_bfloat16*)s2;
-    a.dst_rows = rows2;
-    a.wpk = img + L.w2;
-    a.par = (const float*)(img + L.p2);
-    a.trace = tsel == 1 ? tb : nullptr;
-    st = launch_wide<M, M, kMid>(a, ((long)cap * b * b + 127) / 128, s, "residual_unit_wide_mid");
+    a.wpk3 = img + L.w3;
+    a.par3 = (const float*)(img + L.p3);
+    return launch_fused<C, M>(a, cap, s);
   }
+  a.dst = (__nv_bfloat16*)s1;
+  a.dst_rows = rows1;
+  a.wpk = img + L.w1;
+  a.par = (const float*)(img + L.p1);
+  st = launch_wide<C, M, kIn>(a, ((long)cap * a.S + a.G - 1) / a.G, s, "residual_unit_wide_in");
+  if (st) return st;
+  // MID: S1 -> S2 (3x3 valid); plane runs by 1-D bulk copies
+  a.stack = s1;
+  a.src_rows = rows1;
+  a.dst = (__nv_bfloat16*)s2;
+  a.dst_rows = rows2;
+  a.wpk = img + L.w2;
+  a.par = (const float*)(img + L.p2);
+  a.trace = tsel == 1 ? tb : nullptr;
+  st = launch_wide<M, M, kMid>(a, ((long)cap * b * b + 127) / 128, s, "residual_unit_wide_mid");
   if (st) return st;
   // OUT: S2 -> out (+ residual), in place or into the clone
   a.stack = s2;

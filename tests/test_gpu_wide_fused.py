@@ -1,13 +1,16 @@
-"""GPU parity of the fused IN+MID launch of the wide tcgen05 unit (unit_wide.cu,
-`unit_wide_fused_kernel`: 16x16 blocks, the S1 rows of a block stay in shared memory).
+"""GPU parity of the one-launch wide tcgen05 unit (unit_wide.cu, `unit_wide_fused_kernel`:
+16x16 blocks; the S1 / S2 rows of a block stay in shared memory, the in-place rims come
+from a snapshot taken before the launch).
 
 The fused launch issues the tensor-core k-steps of every accumulator in the same order as
-the three-launch path (IN -> S1 stack -> MID), so its S2 stack and therefore the unit's
-output must be BIT-identical to the three-launch path's (SBN_DEBUG_WIDE_UNFUSED = 256 forces
-that one).  Both are also checked against the fp32 oracle (north star: bf16 <= 2e-2).
-Cases cover the config-4 stage shapes (c = 96 / 192), the small shapes (32, 64, 128), ragged
-frame borders, many blocks per CTA (ring wrap-around of every buffer), a single block and a
-full mask.
+the three-launch path (IN -> S1 stack -> MID -> S2 stack -> OUT) and rounds the same
+values, so the unit's output must be BIT-identical to the three-launch path's
+(SBN_DEBUG_WIDE_UNFUSED = 256 forces that one), in place and functional.  Both are also
+checked against the fp32 oracle (north star: bf16 <= 2e-2).  Cases cover the config-4
+stage-0 shape (c = 96) and the config-2 shape (64), ragged frame borders, many blocks per
+CTA (ring wrap-around of every buffer), a full mask and an empty one.  The c = 192 / 128
+shapes do not fit the one-launch kernel (weights + buffers > shared memory) and must keep
+running the three launches.
 """
 import numpy as np
 import pytest
@@ -58,7 +61,7 @@ def _oracle(x_bf16, u, mk):
 # (c, m, n, h, w, density)
 CASES = [
     (96, 48, 2, 72, 60, 0.3),     # config-4 stage-0 shape, ragged borders
-    (192, 96, 2, 60, 44, 0.3),    # stage-1 shape (W2 streamed, one GEMM1 accumulator)
+    (192, 96, 2, 60, 44, 0.3),    # stage-1 shape: three launches (does not fit one CTA)
     (64, 32, 2, 96, 80, 0.25),    # config-2 shape
     (32, 16, 1, 50, 47, 0.5),
     (128, 64, 1, 64, 64, 0.4),
@@ -68,31 +71,52 @@ CASES = [
 
 
 @pytest.mark.parametrize("c,m,n,h,w,density", CASES)
-def test_fused_in_mid_bit_identical_to_three_launches(cuda_device, c, m, n, h, w, density):
+def test_fused_unit_bit_identical_to_three_launches(cuda_device, c, m, n, h, w, density):
     x, u, mk = _case(c + h, n, h, w, c, m, density)
     fused = _run(x, mk, u, FORCE_WIDE)
     three = _run(x, mk, u, FORCE_WIDE | WIDE_UNFUSED)
     assert torch.equal(fused, three), (c, m, n, h, w, (fused.float() - three.float()).abs().max().item())
     err = O.rel_err(fused.float().numpy(), _oracle(x, u, mk))
     assert err <= 2e-2, err
-    # in place == functional
+    # in place (rim snapshot) == functional == three launches in place
     assert torch.equal(_run(x, mk, u, FORCE_WIDE, inplace=True), fused)
+    assert torch.equal(_run(x, mk, u, FORCE_WIDE | WIDE_UNFUSED, inplace=True), fused)
 
 
 @pytest.mark.parametrize("c,m", [(96, 48), (192, 96), (64, 32), (128, 64)])
-def test_fused_in_mid_many_blocks_per_cta(cuda_device, c, m):
-    """Several hundred to a few thousand active blocks: every CTA walks many blocks, so the
-    window ring, both A2 buffers, the GEMM1/GEMM2 accumulators and (c = 192) the streamed W2
-    ring wrap around many times."""
+def test_fused_unit_many_blocks_per_cta(cuda_device, c, m):
+    """Several hundred to a few thousand active blocks, in place: every CTA walks many blocks
+    (the window ring, both A2 buffers, A3 and the accumulators wrap around many times) while
+    other CTAs overwrite the interiors that its windows' rims cover."""
     n, h, w = (12, 200, 176) if c == 192 else (3, 400, 352)
     x, u, mk = _case(7 + c, n, h, w, c, m, 0.35)
-    fused = _run(x, mk, u, FORCE_WIDE)
-    three = _run(x, mk, u, FORCE_WIDE | WIDE_UNFUSED)
+    fused = _run(x, mk, u, FORCE_WIDE, inplace=True)
+    three = _run(x, mk, u, FORCE_WIDE | WIDE_UNFUSED, inplace=True)
     assert torch.equal(fused, three)
     assert torch.isfinite(fused.float()).all()
 
 
-def test_fused_in_mid_empty_mask(cuda_device):
+def test_fused_unit_empty_mask(cuda_device):
     x, u, _ = _case(3, 2, 40, 36, 96, 48, 0.5)
     empty = P.BinaryMask(np.zeros((2, 40, 36), np.uint8))
     assert torch.equal(_run(x, empty, u, FORCE_WIDE), x)
+
+
+def test_fused_unit_stage_chain(cuda_device):
+    """run_stage on the config-4 stage-0 shape (3 in-place one-launch units sharing one index
+    list, each with its own rim snapshot) == the same stage on the three-launch path."""
+    rng = np.random.default_rng(9)
+    cfg = P.StageConfig(unit_count=3, channels=(96, 48, 96), block_size=(16, 16))
+    stage = P.build_stage(cfg, rng)
+    x = torch.from_numpy(rng.standard_normal((2, 120, 104, 96)).astype(np.float32)).bfloat16()
+    mk = P.BinaryMask(np.concatenate([P.synth_mask_blobs((1, 120, 104), 0.7, s).numpy() for s in (1, 2)]))
+    lib = _lib.load()
+    outs = []
+    for flags in (0, WIDE_UNFUSED):
+        prev = lib.sbn_debug_set_flags(flags)
+        try:
+            outs.append(P.run_stage(stage, P.Tensor4D(x.clone().cuda()), mk).output.data.cpu())
+            torch.cuda.synchronize()
+        finally:
+            lib.sbn_debug_set_flags(prev)
+    assert torch.equal(outs[0], outs[1])

@@ -1,9 +1,11 @@
-"""CTA-0 event timeline of the fused IN+MID wide-unit launch (unit_wide_fused_kernel) on a
+"""CTA-0 event timeline of the one-launch wide unit (unit_wide_fused_kernel) on a
 config-4 stage (16x16 blocks): per block k of CTA 0, when the loader issued its first
 window chunk (load), the first chunk landed (landed), BN1 finished the last chunk (bn),
 GEMM1 of both tiles was issued (g1), epilogue 1 published A2 (e1), GEMM2 was issued (g2),
 epilogue 2 saw its accumulator (e2a) and released it (e2); microseconds from the first
-stamp; g1s / g2e / e1s: GEMM1 issue start, GEMM2 issue end, epilogue 1 start.
+stamp; g1s / g3 / e1s / e3: GEMM1 issue start, GEMM3 issue, epilogue 1 start, epilogue 3 done.
+Needs the diagnostics build: tools/build_variant.sh trace -DSBN_TRACE_FUSED, then
+SBN_LIB_PATH=tools/bin/trace.so.
     python tools/trace_fused.py [stage 2|3] [frames]"""
 import os
 import sys
@@ -39,7 +41,7 @@ residual_unit_into(x, x, u, spec, idx)
 torch.cuda.synchronize()
 lib.sbn_debug_set_trace(None)
 lib.sbn_debug_set_flags(prev)
-names = ["load", "landed", "bn", "g1", "e1", "g2", "e2a", "e2", "g1s", "g2e", "e1s"]
+names = ["load", "landed", "bn", "g1", "e1", "g2", "e2a", "e2", "g1s", "g3", "e1s", "e3"]
 t = buf.cpu().numpy()[:len(names) * 64].reshape(len(names), 64).astype(np.int64)
 nb = int((t[0] > 0).sum())
 t0 = t[t > 0].min()
