@@ -58,6 +58,8 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
 // active windows, for channel counts whose weights do not fit one CTA's shared memory
 bool unit_wide_supported(int dtype, int c, int m, const Geo& g, int halo, int pre_act);
 size_t unit_wide_packed_bytes(int c, int m);
+// the wide unit runs as ONE launch for this shape (16x16 blocks, buffers fit one CTA)
+bool unit_wide_one_launch(int c, int m, const Geo& g);
 size_t unit_wide_stack_bytes(int m, const Geo& g);
 int unit_wide_pack(const sbn_unit_params* p, int c, int m, void* img, cudaStream_t s);
 int unit_wide_launch(const void* x, void* out, int c, int m, const Geo& g, const void* packed,

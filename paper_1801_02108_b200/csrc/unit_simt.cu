@@ -254,16 +254,19 @@ size_t unit_workspace_wide(int c, int m, const Geo& g) {
   return kBarBytes + unit_wide_stack_bytes(m, g) + align_up(unit_wide_packed_bytes(c, m), 256);
 }
 
-// which tensor-core variant applies: 1 single-kernel unit, 2 wide (three launches), 0 none.
-// The single kernel walks one block's latency chain per CTA; past ~8K candidate blocks the
-// pipelined three-launch unit is faster even where the single kernel fits (measured with
-// the mask-fused path, tools/wide_vs_fused.py, config-2 shapes at 20% density: 91 vs 102 us
-// at 8 frames, 183 vs 182 us at 16, 724 vs 618 us at 64).
-constexpr long kFusedMaxCandidates = 8192;
+// which tensor-core variant applies: 1 single-kernel unit, 2 wide (pipelined persistent
+// launches), 0 none.  The single kernel walks one block's latency chain per CTA; past ~4K
+// candidate blocks the pipelined wide unit (one launch for 16x16 blocks) is faster even
+// where the single kernel fits (tools/wide_vs_fused.py, config-2 shapes, mask-fused public
+// path, single vs wide: 10 % density 34.9 vs 45.9 us at 4 frames (3.4K candidates), 48.3 vs
+// 47.0 at 6, 60.7 vs 54.3 at 8, 402.8 vs 242.8 at 64; 20 %: 49.9 vs 50.8 at 4, 76.4 vs 63.4
+// at 6, 724.9 vs 425.5 at 64).  Where the wide unit is still three launches (blocks other
+// than 16x16) the crossover is ~8K candidates (8 frames: 91 vs 102 us at 20 %).
 int unit_tc_kind(int dtype, int c, int m, const Geo& g, int halo, int pre_act) {
   const long cand = (long)g.n * g.gy * g.gx;
+  const long max_single = unit_wide_one_launch(c, m, g) ? 4096 : 8192;
   if (!(debug_flags() & kDebugForceWide) &&
-      (cand <= kFusedMaxCandidates || (debug_flags() & kDebugForceFused)) &&
+      (cand <= max_single || (debug_flags() & kDebugForceFused)) &&
       unit_tc_supported(dtype, c, m, g, halo, pre_act))
     return 1;
   if (unit_tc_supported(dtype, c, m, g, halo, pre_act) && !unit_wide_supported(dtype, c, m, g, halo, pre_act))

@@ -1507,6 +1507,14 @@ bool unit_wide_supported(int dtype, int c, int m, const Geo& g, int halo, int pr
   return false;
 }
 
+bool unit_wide_one_launch(int c, int m, const Geo& g) {
+  if (g.bh != g.bw) return false;
+#define X(C_, M_) if (c == C_ && m == M_) return fused_ok<C_, M_>(g.bh);
+  SBN_UNIT_WIDE_CONFIGS(X)
+#undef X
+  return false;
+}
+
 size_t unit_wide_packed_bytes(int c, int m) {
 #define X(C_, M_) if (c == C_ && m == M_) return wide_layout<C_, M_>().total;
   SBN_UNIT_WIDE_CONFIGS(X)

@@ -177,12 +177,12 @@ def test_unit_packed_image_identifies_the_variant(cuda_device):
 
 def test_unit_params_reused_across_the_fused_wide_threshold(cuda_device):
     """One ResidualUnitParams object run at 1 frame (fused single kernel) and then at 10
-    frames (> 8192 candidates: the wide unit) and back: each call gets the image of its own
+    frames (> 4096 candidates: the wide unit) and back: each call gets the image of its own
     variant (the cache was keyed on the block size only)."""
     x, u, _ = _case(5, 10, 400, 400, 64, 32, 0.1)
     mk = P.BinaryMask(np.concatenate([P.synth_mask_blobs((1, 400, 400), 0.9, i).numpy() for i in range(10)]))
     one = P.BinaryMask(mk.numpy()[:1])
-    assert P.unit_spec((10, 400, 400, 64), (16, 16)).grid_count[0] ** 2 * 10 > 8192
+    assert P.unit_spec((10, 400, 400, 64), (16, 16)).grid_count[0] ** 2 * 10 > 4096
     ref0 = _oracle(x[:1], u, one, (16, 16))
     for n, m_ in ((1, one), (10, mk), (1, one)):
         y = P.sparse_residual_unit(P.Tensor4D(x[:n].clone().cuda()), m_, u, (16, 16))
