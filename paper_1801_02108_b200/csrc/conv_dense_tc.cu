@@ -389,17 +389,327 @@ __global__ void __launch_bounds__(kCThreads, CCfg<CIN, COUT, KS>::CPS) conv_dens
   if (warp == 0) tc::tmem_free<Q::TALLOC>(tmem);
 }
 
+// ---- CTA-pair (cta_group::2) dense projection: two 8 x 16 output tiles per pair as ONE
+// M = 256 UMMA issued by rank 0.  B is split along N (rank r holds output channels
+// [r*NS/2, (r+1)*NS/2) of every N-slice of every weight chunk), so each SM stores / streams
+// half of the weights: the config-4 stage-1 projection (96 -> 192) keeps its half (166 KB)
+// resident for the whole launch, and the wider ones (192 -> 256, 256 -> 384) stream half the
+// bytes per tile.  (The single-CTA kernel re-streams all 9 * CIN * COUT weights from L2 for
+// every 128-pixel tile once they exceed shared memory: 332 KB per tile at 96 -> 192.)
+// Handshakes (rank 0 owns what its MMA issuer waits on):
+//   a_full[s]    both ranks' A boxes of stage s landed (rank 1's TMA completes on it)   rank 0
+//   w_full[s]    both weight halves of stage s landed (streamed)                       rank 0
+//   *_empty[s]   MMAs reading stage s done (multicast commit)                          both
+//   acc_full[b]  accumulator b complete (multicast commit)                             both
+//   acc_empty[b] 2 x kCE epilogue arrivals (rank 1's arrive remotely)                  rank 0
+//   wpeer        rank 1's resident half landed (remote arrive)                         rank 0
+template <int CIN, int COUT, int KS>
+struct PCfg {
+  using Q = CCfg<CIN, COUT, KS>;
+  static constexpr int TAPS = Q::TAPS, KC = Q::KC, NKC = Q::NKC, ROWB = Q::ROWB, ACH = Q::ACH;
+  static constexpr uint32_t SWZ = Q::SWZ;
+  static constexpr int NP = Q::NP, NSPLIT = Q::NSPLIT, NS = Q::NS, NHS = NS / 2;
+  static constexpr int PWR = (NP / 2) * 16;      // plane stride of a rank's half chunk
+  static constexpr int WCHR = (KC / 8) * PWR;    // one (kc, tap) half chunk
+  static constexpr int CHUNKS = Q::CHUNKS;
+  static constexpr long WBYTESR = (long)CHUNKS * WCHR;
+  static constexpr int GS = NP % 64 == 0 ? 64 : NP;  // staged columns per pass (small staging buffer)
+  static constexpr int SPITCH = GS * 2 + 16;
+  static constexpr int STGB = 128 * SPITCH;
+  static constexpr int PARB = Q::PARB;
+  static constexpr int NACC = Q::NACC, TALLOC = Q::TALLOC;
+  static constexpr bool RES = 3L * ACH + WBYTESR + STGB + PARB <= kCBudget;
+  static constexpr int SA_R = (int)((kCBudget - WBYTESR - STGB - PARB) / ACH);
+  static constexpr int SS = (int)((kCBudget - STGB - PARB) / (ACH + WCHR));
+  static constexpr int SA = RES ? (SA_R > 12 ? 12 : SA_R) : (SS > kMaxStream ? kMaxStream : SS);
+  static constexpr int SW = RES ? 0 : SA;
+  static constexpr long WREG = RES ? WBYTESR : (long)SW * WCHR;
+  static constexpr int OFF_W = SA * ACH;
+  static constexpr int OFF_STG = OFF_W + (int)WREG;
+  static constexpr int OFF_PAR = OFF_STG + STGB;
+  static constexpr int SMEM = OFF_PAR + PARB;
+  static constexpr int WBOXR = WCHR / 128;      // a half chunk as a TMA box of 128-byte rows
+  // used for the dense projections whose weights the single-CTA kernel must stream, when the
+  // pair still keeps >= 5 A boxes in flight: these convs are bound by the TMA box rate (one
+  // box of 128 strided pixel rows per (K-chunk, tap)), so a shallower A ring loses more than
+  // the halved weight stream saves (96 -> 192 with resident halves and 4 A stages: stage 1 of
+  // the backbone 0.546 -> 0.549 ms; 192 -> 256 / 256 -> 384 streamed: 0.353 -> 0.346,
+  // 0.204 -> 0.199 ms)
+  static constexpr bool USE = !Q::RES && NHS % 8 == 0 && SA >= 5 && WBOXR <= 256 && WCHR % 128 == 0 &&
+                              SMEM <= 227 * 1024;
+};
+
+struct __align__(64) PArgs {
+  CArgs c;
+  CUtensorMap wmap;  // the pair copy of the packed weights as 128-byte rows, box = one half chunk
+};
+
+template <int CIN, int COUT, int KS>
+__global__ void __launch_bounds__(kCThreads, 1) conv_dense_pair_kernel(const __grid_constant__ PArgs pa) {
+  using P = PCfg<CIN, COUT, KS>;
+  const CArgs& a = pa.c;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int SWB = P::SW > 0 ? P::SW : 1;
+  __shared__ uint64_t a_full[P::SA], a_empty[P::SA], w_full[SWB], w_empty[SWB];
+  __shared__ uint64_t acc_full[P::NACC], acc_empty[P::NACC], wres, wpeer;
+  __shared__ uint32_t tslot;
+  __shared__ long long rowdst[128];
+  uint8_t* Aring = smem;
+  uint8_t* Wring = smem + P::OFF_W;
+  uint8_t* stg = smem + P::OFF_STG;
+  float* bias = reinterpret_cast<float*>(smem + P::OFF_PAR);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  constexpr int kLWarp = kCE / 32;
+
+  if (tid == 0) {
+    for (int s = 0; s < P::SA; ++s) {
+      tc::mbar_init(&a_full[s], 1);
+      tc::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < SWB; ++s) {
+      tc::mbar_init(&w_full[s], 1);
+      tc::mbar_init(&w_empty[s], 1);
+    }
+    for (int s = 0; s < P::NACC; ++s) {
+      tc::mbar_init(&acc_full[s], 1);
+      tc::mbar_init(&acc_empty[s], 2 * kCE);
+    }
+    tc::mbar_init(&wres, 1);
+    tc::mbar_init(&wpeer, 1);
+    tc::mbar_fence_init();
+  }
+  if (tid == kLWarp * 32) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&pa.wmap) : "memory");
+  }
+  for (int i = tid; i < COUT; i += kCThreads) bias[i] = a.bias ? a.bias[i] : 0.f;
+  if constexpr (P::NP != COUT)
+    for (int i = COUT + tid; i < P::NP; i += kCThreads) bias[i] = 0.f;
+  if (warp == 0) tc::tmem_alloc_cg2<P::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast commit
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_trigger();
+  const uint8_t* wpair = a.wpk + (size_t)P::Q::WBYTES;  // the pair copy follows the single image
+  if (P::RES && tid == kLWarp * 32) {  // my half of every chunk, resident (independent of the previous launch)
+    tc::mbar_expect_tx(&wres, (uint32_t)P::WBYTESR);
+    for (int c = 0; c < P::CHUNKS; ++c)
+      tc::bulk_g2s(Wring + (size_t)c * P::WCHR, wpair + ((size_t)c * 2 + rank) * P::WCHR, P::WCHR, &wres);
+  }
+  tc::pdl_wait();
+  const int ntiles = a.n * a.tiles_y * a.tiles_x;
+  const int nptiles = (ntiles + 1) / 2;  // an odd last tile pairs with an empty (zero) one
+
+  if (warp < kLWarp) {
+    // ------------------------------------------------ epilogue (my tile of each pair tile)
+    const int qd = warp & 3, half = warp >> 2;
+    const int r = qd * 32 + lane;
+    constexpr int CHR = P::GS * 2 / 16;
+    constexpr int IT2 = (128 * CHR + kCE - 1) / kCE;
+    int k = 0;
+    for (int pt = pair; pt < nptiles; pt += npairs, ++k) {
+      const int buf = P::NACC == 2 ? (k & 1) : 0;
+      const int use = P::NACC == 2 ? (k >> 1) : k;
+      const int tile = 2 * pt + (int)rank;
+      int n, oy0, ox0, iy0, ix0, ly, lx;
+      conv_tile<false>(a, nullptr, tile, n, oy0, ox0, iy0, ix0, ly, lx);
+      const int Y = oy0 + r / a.tw, X = ox0 + r % a.tw;
+      if (half == 0)
+        rowdst[r] = (tile < ntiles && r < a.th * a.tw && Y < a.oh && X < a.ow)
+                        ? (((long long)n * a.oh + Y) * a.ow + X) * COUT : -1;
+      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * P::NP;
+      tc::mbar_wait(&acc_full[buf], use & 1);
+      tc::fence_after();
+      for (int g0 = 0; g0 < P::NP; g0 += P::GS) {
+#pragma unroll
+        for (int e = 0; e < (P::GS / 16 + 1) / 2; ++e) {
+          const int cg = 16 * (2 * e + half);
+          if (cg >= P::GS) break;  // warp-uniform
+          float v[16];
+          tc::tmem_ld16(acc + g0 + cg, v);
+          uint32_t o[8];
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias + g0 + cg + 2 * q);
+            o[q] = tc::pack_bf16(v[2 * q] + b4.x, v[2 * q + 1] + b4.y);
+            o[q + 1] = tc::pack_bf16(v[2 * q + 2] + b4.z, v[2 * q + 3] + b4.w);
+          }
+          uint4* sp = reinterpret_cast<uint4*>(stg + r * P::SPITCH + cg * 2);
+          sp[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          sp[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+        if (g0 + P::GS >= P::NP) {  // accumulator drained: the next pair tile's MMAs may start
+          tc::fence_before();
+          if (rank == 0) tc::mbar_arrive(&acc_empty[buf]);
+          else tc::mbar_arrive_cluster(&acc_empty[buf], 0);
+        }
+        tc::named_bar<1, kCE>();
+#pragma unroll
+        for (int jj = 0; jj < IT2; ++jj) {
+          const int it = tid + jj * kCE;
+          if (it >= 128 * CHR) break;
+          const int row = it / CHR, ch = it % CHR;
+          const long long off = rowdst[row];
+          if (off < 0 || (P::NP != COUT && g0 * 2 / 16 + ch >= COUT * 2 / 16)) continue;  // N padding
+          reinterpret_cast<uint4*>(a.out + off + g0)[ch] = *reinterpret_cast<const uint4*>(stg + row * P::SPITCH + ch * 16);
+        }
+        tc::named_bar<1, kCE>();  // staging / rowdst reuse
+      }
+    }
+  } else if (warp == kLWarp) {
+    // ------------------------------------------------ loader: my tile's A boxes, my weight halves
+    if (lane == 0) {
+      if (P::RES && rank == 1) {  // tell rank 0's issuer that my resident half has landed
+        tc::mbar_wait(&wres, 0);
+        tc::mbar_arrive_cluster(&wpeer, 0);
+      }
+      int c = 0, wit = 0;
+      const uint32_t bytes = (uint32_t)(a.th * a.tw * P::ROWB);
+      for (int pt = pair; pt < nptiles; pt += npairs) {
+        const int tile = 2 * pt + (int)rank;
+        int n, oy0, ox0, y0, x0, ly, lx;
+        conv_tile<false>(a, nullptr, tile < ntiles ? tile : 0, n, oy0, ox0, y0, x0, ly, lx);
+        if (tile >= ntiles) n = a.n;  // past the last frame: TMA zero-fills the whole box
+        for (int kc = 0; kc < P::NKC; ++kc)
+          for (int tap = 0; tap < P::TAPS; ++tap, ++c) {
+            const int s = c % P::SA;
+            tc::mbar_wait(&a_empty[s], ((c / P::SA) & 1) ^ 1);
+            if (rank == 0) {
+              tc::mbar_expect_tx(&a_full[s], 2 * bytes);
+              tma_4d(Aring + s * P::ACH, &a.tmap, kc * P::KC, x0 + tap % KS, y0 + tap / KS, n, &a_full[s]);
+            } else {
+              tma_4d_cg2(Aring + s * P::ACH, &a.tmap, kc * P::KC, x0 + tap % KS, y0 + tap / KS, n, &a_full[s], 0);
+            }
+            if (!P::RES) {
+              const int sw = wit % SWB;
+              tc::mbar_wait(&w_empty[sw], ((wit / SWB) & 1) ^ 1);
+              const int row = ((kc * P::TAPS + tap) * 2 + (int)rank) * P::WBOXR;
+              if (rank == 0) {
+                tc::mbar_expect_tx(&w_full[sw], 2 * P::WCHR);
+                tma_2d(Wring + sw * P::WCHR, &pa.wmap, 0, row, &w_full[sw]);
+              } else {
+                tma_2d_cg2(Wring + sw * P::WCHR, &pa.wmap, 0, row, &w_full[sw], 0);
+              }
+              ++wit;
+            }
+          }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------ MMA issuer (rank 0): M = 256 over the pair
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, P::NS);
+      if (P::RES) {
+        tc::mbar_wait(&wres, 0);
+        tc::mbar_wait(&wpeer, 0);
+      }
+      int c = 0, wit = 0, k = 0;
+      for (int pt = pair; pt < nptiles; pt += npairs, ++k) {
+        const int buf = P::NACC == 2 ? (k & 1) : 0;
+        const int use = P::NACC == 2 ? (k >> 1) : k;
+        tc::mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t acc = tmem + buf * P::NP;
+        for (int kc = 0; kc < P::NKC; ++kc)
+          for (int tap = 0; tap < P::TAPS; ++tap, ++c) {
+            const int s = c % P::SA;
+            tc::mbar_wait(&a_full[s], (c / P::SA) & 1);
+            const int sw = P::RES ? 0 : wit % SWB;
+            if (!P::RES) tc::mbar_wait(&w_full[sw], (wit / SWB) & 1);
+            tc::fence_after();
+            const uint32_t abase = tc::smem_u32(Aring + s * P::ACH);
+            const uint32_t wbase = tc::smem_u32(Wring + (P::RES ? (kc * P::TAPS + tap) * P::WCHR : sw * P::WCHR));
+#pragma unroll
+            for (int kk = 0; kk < P::KC / 16; ++kk)
+#pragma unroll
+              for (int h = 0; h < P::NSPLIT; ++h)
+                tc::mma_bf16_cg2(acc + h * P::NS, tc::desc_kmajor_swz(abase + kk * 32, 8 * P::ROWB, P::SWZ),
+                                 tc::desc_kmajor_noswz(wbase + 2 * kk * P::PWR + h * P::NHS * 16, P::PWR, 128), idesc,
+                                 (kc | tap | kk) > 0);
+            tc::mma_commit_mc(&a_empty[s], 3);
+            if (!P::RES) {
+              tc::mma_commit_mc(&w_empty[sw], 3);
+              ++wit;
+            }
+          }
+        tc::mma_commit_mc(&acc_full[buf], 3);
+      }
+    }
+    __syncwarp();
+  }
+  if (P::RES && tid == kLWarp * 32 && rank == 0) tc::mbar_wait(&wres, 0);
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // the peer's MMAs / remote arrivals are done before TMEM is freed
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free_cg2<P::TALLOC>(tmem);
+}
+
+template <int CIN, int COUT, int KS>
+int launch_dense_pair(const CArgs& c, cudaStream_t s) {
+  using P = PCfg<CIN, COUT, KS>;
+  if constexpr (P::USE) {
+    PArgs pa;
+    memset(&pa, 0, sizeof(pa));
+    pa.c = c;
+    const uint64_t wdims[2] = {64, (uint64_t)P::CHUNKS * 2 * P::WBOXR};  // every half chunk, 128-byte rows
+    const uint64_t wstr[1] = {128};
+    const uint32_t wbox[2] = {64, (uint32_t)P::WBOXR};
+    int st = encode_map(&pa.wmap, c.wpk + (size_t)P::Q::WBYTES, 2, wdims, wstr, wbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (st) return st;
+    auto kern = conv_dense_pair_kernel<CIN, COUT, KS>;
+    static PerDeviceOnce once;
+    once([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM); });
+    const long nptiles = ((long)c.n * c.tiles_y * c.tiles_x + 1) / 2;
+    const long maxp = sm_count() / 2;
+    const long npairs = nptiles < maxp ? (nptiles < 1 ? 1 : nptiles) : maxp;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * npairs));
+    cfg.blockDim = dim3(kCThreads);
+    cfg.dynamicSmemBytes = P::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, kern, pa);
+    return launch_status("dense_conv_tcgen05_pair");
+  } else {
+    (void)c;
+    (void)s;
+    return SBN_ERR_UNSUPPORTED;
+  }
+}
+
 // W (KS, KS, CIN, COUT) HWIO -> chunks (kc, tap) of (COUT rows x KC) in the K-major plane layout
+// (+ for the CTA-pair shapes, a second copy after it: chunk (kc, tap) split into the two
+// ranks' halves, rank r holding rows [r*NS/2, (r+1)*NS/2) of every N-slice)
 template <int CIN, int COUT, int KS>
 __global__ void conv_dense_pack_kernel(const __nv_bfloat16* __restrict__ w, uint8_t* __restrict__ img) {
   using Q = CCfg<CIN, COUT, KS>;
+  using P = PCfg<CIN, COUT, KS>;
   constexpr int CP = Q::CP, NP = Q::NP;  // padded entries are written as zeros
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KS * KS * CP * NP; i += gridDim.x * blockDim.x) {
     const int tap = i / (CP * NP), rr = i % (CP * NP), ci = rr / NP, co = rr % NP;
     const int kc = ci / Q::KC, kq = ci % Q::KC;
+    const __nv_bfloat16 v = ci < CIN && co < COUT ? w[((size_t)tap * CIN + ci) * COUT + co] : __float2bfloat16(0.f);
     *reinterpret_cast<__nv_bfloat16*>(img + (size_t)(kc * Q::TAPS + tap) * Q::WCH + (kq / 8) * Q::PW + co * 16 +
-                                      (kq % 8) * 2) =
-        ci < CIN && co < COUT ? w[((size_t)tap * CIN + ci) * COUT + co] : __float2bfloat16(0.f);
+                                      (kq % 8) * 2) = v;
+    if constexpr (P::USE) {
+      const int h = co / P::NS, within = co % P::NS, rk = within / P::NHS, row = h * P::NHS + within % P::NHS;
+      *reinterpret_cast<__nv_bfloat16*>(img + Q::WBYTES + ((size_t)(kc * Q::TAPS + tap) * 2 + rk) * P::WCHR +
+                                        (kq / 8) * P::PWR + row * 16 + (kq % 8) * 2) = v;
+    }
   }
 }
 
@@ -485,6 +795,7 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
       }
     }
   }
+  if (!sparse && PCfg<CIN, COUT, KS>::USE && !(debug_flags() & kDebugDenseSingle)) return launch_dense_pair<CIN, COUT, KS>(a, s);
   auto kern = mask ? conv_dense_kernel<CIN, COUT, KS, true> : conv_dense_kernel<CIN, COUT, KS, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
@@ -534,7 +845,8 @@ bool sparse_conv_tma_supported(int dtype, int cin, int cout, int kh, int kw, int
 }
 
 size_t sparse_conv_tma_packed_bytes(int cin, int cout, int k) {
-#define X(CI, CO, KS) if (cin == CI && cout == CO && k == KS) return (size_t)CCfg<CI, CO, KS>::WBYTES;
+#define X(CI, CO, KS) \
+  if (cin == CI && cout == CO && k == KS) return (size_t)CCfg<CI, CO, KS>::WBYTES * (PCfg<CI, CO, KS>::USE ? 2 : 1);
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   return 0;

@@ -45,6 +45,18 @@ __device__ __forceinline__ void tma_5d_cg2(void* dst, const CUtensorMap* map, in
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(rb)
       : "memory");
 }
+// CTA-pair form of tma_4d: lands in THIS CTA's smem, completes on the mbarrier at `bar`'s
+// offset in CTA `rank` of the pair
+__device__ __forceinline__ void tma_4d_cg2(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                           uint64_t* bar, uint32_t rank) {
+  uint32_t rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(tc::smem_u32(bar)), "r"(rank));
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(rb)
+      : "memory");
+}
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(

@@ -93,3 +93,36 @@ def test_mask_fused_tap_gemm_conv_equals_reduce_mask_then_conv(cuda_device, cin,
     assert torch.equal(a, b)
     if density == 0.0:
         assert bool((a == 3.0).all())
+
+
+DENSE_SINGLE = 512  # SBN_DEBUG_DENSE_SINGLE: the single-CTA kernel even where the CTA-pair one applies
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,stride", [
+    (3, 41, 37, 192, 256, 2),   # the config-4 stage-2 projection shape class (streamed halves)
+    (2, 27, 23, 256, 384, 2),   # stage 3: streamed halves, two N-slices of 192
+    (8, 60, 50, 192, 256, 2),   # many pair tiles per pair (ring wrap-around)
+    (1, 9, 15, 192, 256, 2)])   # an odd number of 8 x 16 tiles: the last pair has an empty rank-1 tile
+def test_dense_conv_pair_bit_identical_to_single_cta(cuda_device, n, h, w, cin, cout, stride):
+    """The CTA-pair (cta_group::2, M = 256, B split along N) projection issues the same k-steps
+    per accumulator row as the single-CTA kernel: bit-identical output."""
+    from paper_1801_02108_b200 import _lib
+    rng = np.random.default_rng(n + h + cin)
+    x = torch.from_numpy(rng.standard_normal((n, h, w, cin)).astype(np.float32)).bfloat16().cuda()
+    wt = (rng.standard_normal((3, 3, cin, cout)) / np.sqrt(9 * cin)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    f = P.FilterBank(torch.from_numpy(wt).bfloat16(), torch.from_numpy(b).bfloat16())
+    p = P.ConvParams((3, 3), (stride, stride), P.Padding.SAME, cout)
+    lib = _lib.load()
+    pair = projection_conv(x, f, p)
+    torch.cuda.synchronize()
+    prev = lib.sbn_debug_set_flags(DENSE_SINGLE)
+    try:
+        single = projection_conv(x, f, p)
+        torch.cuda.synchronize()
+    finally:
+        lib.sbn_debug_set_flags(prev)
+    assert torch.equal(pair, single), (pair.float() - single.float()).abs().max().item()
+    fb32 = P.FilterBank(torch.from_numpy(wt).bfloat16().float(), torch.from_numpy(b).bfloat16().float())
+    ref = P.conv2d_direct(P.Tensor4D(x.float()), fb32, p).data.cpu().numpy()
+    assert O.rel_err(pair.float().cpu().numpy(), ref) <= 1e-2
