@@ -41,7 +41,7 @@ residual_unit_into(x, x, u, spec, idx)
 torch.cuda.synchronize()
 lib.sbn_debug_set_trace(None)
 lib.sbn_debug_set_flags(prev)
-names = ["load", "landed", "bn", "g1", "e1", "g2", "e2a", "e2", "g1s", "g3", "e1s", "e3"]
+names = ["load", "landed", "bn", "g1", "e1", "g2", "e2a", "e2", "g1s", "g3", "e1s", "e3", "g2e"]
 t = buf.cpu().numpy()[:len(names) * 64].reshape(len(names), 64).astype(np.int64)
 nb = int((t[0] > 0).sum())
 t0 = t[t > 0].min()
