@@ -29,11 +29,6 @@ __device__ __forceinline__ uint64_t desc_kmajor_noswz(uint32_t saddr, uint32_t l
   return d;
 }
 
-// the same operand view `bytes` further on (a multiple of 16): only the 14-bit start-address
-// field changes, so the single-thread MMA issuers offset one base descriptor by an immediate
-// per MMA instead of rebuilding it (the start field of smem addresses < 256 KB cannot carry)
-__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
-
 // K-major swizzled operand (rows of 64 B (SWIZZLE_64B, layout 4) or 128 B (SWIZZLE_128B,
 // layout 2), 8-row atoms at SBO bytes), as TMA writes it with the matching swizzle mode.
 // A k-step inside the row is a +32 B start-address change (the swizzle is a function of
@@ -176,20 +171,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(a),
       "r"(parity)
-      : "memory");
-}
-
-// mbar_wait for warps off the critical issue path: between probes the thread sleeps
-// (NANOSLEEP.SYNCS, woken when the barrier changes) instead of spinning, so waiting warps do
-// not take issue slots from the single-thread MMA issuer on their scheduler
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra WAITS_%=;\n\t}\n" ::"r"(a),
-      "r"(parity), "r"(1000000)
       : "memory");
 }
 

@@ -741,7 +741,7 @@ constexpr int kFB = 16;                  // block size of the fused variant
 constexpr int kFBnThreads = 128;         // BN warps 0-3
 // CTA-0 event stamps per block k (diagnostics, tools/trace_fused.py)
 enum { kFevLoad = 0, kFevLanded = 1, kFevBn = 2, kFevG1 = 3, kFevE1 = 4, kFevG2 = 5, kFevE2a = 6, kFevE2 = 7,
-       kFevG1s = 8, kFevG3 = 9, kFevE1s = 10, kFevE3 = 11, kFevG2e = 12 };
+       kFevG1s = 8, kFevG3 = 9, kFevE1s = 10, kFevE3 = 11 };
 constexpr int kFR2 = 296;                // A2 rows: 256 + 2*16 + 2 = 290, rounded to 8
 constexpr int kFPA2 = kFR2 * 16;         // A2 plane stride
 constexpr int kFPA3 = 256 * 16;          // A3 plane stride (rows q = oy*16 + ox of both tiles)
@@ -1209,21 +1209,21 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         tc::fence_after();
         ftrace(a, kFevG2, k);
         const uint32_t acc = tmem + F::COL2 + b2 * 2 * M;
-        // one base descriptor per operand, immediate offsets per MMA (fully unrolled: the
-        // issuer shares its scheduler with busy warps, so instructions per MMA matter)
-        const uint64_t a2d = tc::desc_kmajor_noswz(tc::smem_u32(A2 + b2 * F::A2B), kFPA2, 128);
-        const uint64_t w2d = tc::desc_kmajor_noswz(tc::smem_u32(W2), F::PW2, 128);
-#pragma unroll
+        const uint32_t a2base = tc::smem_u32(A2 + b2 * F::A2B);
+#pragma unroll 1
         for (int kc = 0; kc < F::NKC2; ++kc)
-#pragma unroll
-          for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll 1
+          for (int tap = 0; tap < 9; ++tap) {  // (rolled: the unrolled tap loop made the issuer spill)
+            const uint32_t wbase = tc::smem_u32(W2 + (kc * 9 + tap) * F::WCH2);
             const int shift = (tap / 3) * kFB + (tap % 3);
 #pragma unroll
             for (int u = 0; u < 2; ++u)
 #pragma unroll
               for (int kk = 0; kk < F::KC2 / 16; ++kk)
-                tc::mma_bf16(acc + u * M, tc::desc_add(a2d, (kc * F::P2 + 2 * kk) * kFPA2 + (u * 128 + shift) * 16),
-                             tc::desc_add(w2d, (kc * 9 + tap) * F::WCH2 + 2 * kk * F::PW2), idesc, (kc | tap | kk) > 0);
+                tc::mma_bf16(acc + u * M,
+                             tc::desc_kmajor_noswz(a2base + (kc * F::P2 + 2 * kk) * kFPA2 + (u * 128 + shift) * 16,
+                                                   kFPA2, 128),
+                             tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW2, F::PW2, 128), idesc, (kc | tap | kk) > 0);
           }
         tc::mma_commit(&a2_empty[b2]);
         tc::mma_commit(&acc2_full[b2]);
@@ -1254,500 +1254,6 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
   __syncthreads();
   tc::fence_after();
   if (warp == 0) tc::tmem_free<F::TALLOC>(tmem);
-}
-
-// ---- CTA-pair one-launch unit for 16x16 blocks whose weights do not fit one CTA
-// (config-4 stage 1: c = 192, m = 96 -> 238 KB of weights).  A 2-CTA cluster runs each
-// block; rank r owns window rows 8r..8r+7 (GEMM1 M-tile r) and output rows q in
-// [128r, 128r + 128) (GEMM2 / GEMM3 M-tile r).  All three GEMMs are ONE M = 256 UMMA
-// (cta_group::2) issued by rank 0, B split along N: each rank keeps HALF of W1, W2 and W3
-// resident (119 KB).  GEMM2's row-shifted views of rank 0 reach 34 S1 rows of rank 1's
-// tile: rank 1's epilogue 1 writes those rows into rank 0's A2 as well (DSMEM).  Rims of the
-// in-place windows come from a snapshot as in the single-CTA unit.  MMA order per
-// accumulator and roundings = the three-launch path: bit-identical output.
-// Handshakes (rank 0 owns what its MMA issuer waits on; "both" = multicast commit):
-//   a_full[s], a2_full, a3_full     both ranks' operand writes done (remote release)   rank 0
-//   acc1/acc2/acc3_empty            both ranks drained the accumulator                 rank 0
-//   a_empty[s], a2_empty, a3_empty, acc*_full                                          both
-//   wpeer                           rank 1's weight halves landed                      rank 0
-constexpr int kPR2 = 162;              // A2 rows per rank: 128 + 2*16 + 2
-constexpr int kPPA2 = kPR2 * 16;
-constexpr int kPPA3 = 128 * 16;
-
-template <int C, int M>
-struct PUCfg {
-  using F = FCfg<C, M>;
-  using Q1 = WCfg<C, M, kIn>;
-  using Q2 = WCfg<M, M, kMid>;
-  using Q3 = WCfg<M, C, kOut>;
-  static constexpr int KC1 = Q1::KC, NKC1 = C / KC1, ROWB = KC1 * 2, ACH = 128 * ROWB;
-  static constexpr uint32_t SWZ = Q1::SWZ;
-  static constexpr int KC2 = Q2::KC, NKC2 = M / KC2, P2 = KC2 / 8;
-  static constexpr int PW1H = (M / 2) * 16, PW2H = (M / 2) * 16, PW3H = (C / 2) * 16;  // half-B plane strides
-  static constexpr int W1B = (C / 8) * PW1H, W2B = 9 * (M / 8) * PW2H, W3B = (M / 8) * PW3H;
-  static constexpr int A2B = (M / 8) * kPPA2, A3B = (M / 8) * kPPA3;
-  static constexpr int PAR1 = Q1::NPAR, PAR2 = Q2::NPAR, PAR3 = Q3::NPAR;
-  static constexpr int PARB = (PAR1 + PAR2 + PAR3) * 4 / 128 * 128 + 128;
-  static constexpr int SA = NKC1;  // one window tile per rank and block
-  static constexpr int NB2 = 2;
-  static constexpr int COL2 = M, COL3 = M + NB2 * M, TCOLS = COL3 + C;
-  static constexpr int TALLOC = TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
-  static constexpr int OFF_A2 = SA * ACH;
-  static constexpr int OFF_A3 = OFF_A2 + A2B;
-  static constexpr int OFF_W1 = OFF_A3 + A3B;
-  static constexpr int OFF_W2 = OFF_W1 + W1B;
-  static constexpr int OFF_W3 = OFF_W2 + W2B;
-  static constexpr int OFF_PAR = OFF_W3 + W3B;
-  static constexpr int SMEM = OFF_PAR + PARB;
-  static constexpr bool OK = !F::OK && M % 32 == 0 && C % 32 == 0 && C / 2 <= 256 && TCOLS <= 512 &&
-                             SMEM <= kFBudget && 60 * C <= 256 * M && C % KC1 == 0;
-};
-
-__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {  // acquire at cluster scope
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAITC_%=;\n\t}\n" ::"r"(tc::smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// arrive on the rank-0 instance of `bar`: publishes this thread's shared-memory operand
-// writes to rank 0's MMA issuer (release at CTA scope locally, at cluster scope remotely;
-// the cluster-scope release is a GPU-scope MEMBAR in SASS)
-__device__ __forceinline__ void arrive_r0(uint64_t* bar, uint32_t rank) {
-  if (rank == 0) tc::mbar_arrive(bar);
-  else tc::mbar_arrive_cluster(bar, 0);
-}
-// arrive on the rank-0 instance of `bar` without ordering any memory access: the
-// accumulator-drained signals (the tcgen05.ld's have completed in registers; the epilogue's
-// global stores must not be waited for)
-__device__ __forceinline__ void arrive_r0_relaxed(uint64_t* bar, uint32_t rank) {
-  uint32_t a = tc::smem_u32(bar);
-  if (rank == 0) {
-    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-  } else {
-    asm volatile("mapa.shared::cluster.u32 %0, %0, %1;" : "+r"(a) : "r"(0));
-    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
-  }
-}
-__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared::cluster.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-
-template <int C, int M>
-__global__ void __launch_bounds__(kWideThreads, 1) unit_wide_pair_kernel(const __grid_constant__ WArgs a) {
-  using U = PUCfg<C, M>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t a_load[U::SA], a_full[U::SA], a_empty[U::SA], wres, wpeer;
-  __shared__ uint64_t acc1_full, acc1_empty, a2_full, a2_empty, acc2_full[U::NB2], acc2_empty[U::NB2];
-  __shared__ uint64_t a3_full, a3_empty, acc3_full, acc3_empty;
-  __shared__ uint32_t tslot;
-  uint8_t* A1 = smem;
-  uint8_t* A2 = smem + U::OFF_A2;
-  uint8_t* A3 = smem + U::OFF_A3;
-  uint8_t* W1 = smem + U::OFF_W1;
-  uint8_t* W2 = smem + U::OFF_W2;
-  uint8_t* W3 = smem + U::OFF_W3;
-  float* par1 = reinterpret_cast<float*>(smem + U::OFF_PAR);
-  float* par2 = par1 + U::PAR1;
-  float* par3 = par2 + U::PAR2;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = tc::cluster_rank();
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const Geo& g = a.g;
-  constexpr int kLWarp = 16, kMWarp = 17, OB = kFB - 2;
-
-  if (tid == 0) {
-    for (int s = 0; s < U::SA; ++s) {
-      tc::mbar_init(&a_load[s], 1);
-      tc::mbar_init(&a_full[s], 2 * kFBnThreads);
-      tc::mbar_init(&a_empty[s], 1);
-    }
-    tc::mbar_init(&wres, 1);
-    tc::mbar_init(&wpeer, 1);
-    tc::mbar_init(&acc1_full, 1);
-    tc::mbar_init(&acc1_empty, 256);
-    tc::mbar_init(&a2_full, 256);
-    tc::mbar_init(&a2_empty, 1);
-    for (int b = 0; b < U::NB2; ++b) {
-      tc::mbar_init(&acc2_full[b], 1);
-      tc::mbar_init(&acc2_empty[b], 256);
-    }
-    tc::mbar_init(&a3_full, 256);
-    tc::mbar_init(&a3_empty, 1);
-    tc::mbar_init(&acc3_full, 1);
-    tc::mbar_init(&acc3_empty, 256);
-    tc::mbar_fence_init();
-  }
-  if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
-  for (int i = tid; i < U::PAR1; i += kWideThreads) par1[i] = a.par[i];
-  for (int i = tid; i < U::PAR2; i += kWideThreads) par2[i] = a.par2[i];
-  for (int i = tid; i < U::PAR3; i += kWideThreads) par3[i] = a.par3[i];
-  if (warp == 0) tc::tmem_alloc_cg2<U::TALLOC>(&tslot);
-  tc::fence_before();
-  __syncthreads();
-  tc::cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast commit
-  tc::fence_after();
-  const uint32_t tmem = tslot;
-  tc::pdl_trigger();
-  if (tid == kLWarp * 32) {
-    // my halves (output channels [rank * N/2, (rank+1) * N/2) of every plane) of the three
-    // packed weight images, one bulk copy per 16-B K-plane; they do not depend on the
-    // previous launch
-    tc::mbar_expect_tx(&wres, (uint32_t)(U::W1B + U::W2B + U::W3B));
-    for (int gp = 0; gp < C / 8; ++gp) {  // W1: chunk gp / (KC1/8), plane gp % (KC1/8)
-      const int c = gp / (U::KC1 / 8), p = gp % (U::KC1 / 8);
-      tc::bulk_g2s(W1 + gp * U::PW1H, a.wpk + (size_t)c * U::Q1::WCH + p * U::Q1::PW + rank * U::PW1H, U::PW1H, &wres);
-    }
-    for (int tap = 0; tap < 9; ++tap)
-      for (int gp = 0; gp < M / 8; ++gp) {  // W2: chunk (gp / P2, tap), plane gp % P2
-        const int kc = gp / U::P2, p = gp % U::P2;
-        tc::bulk_g2s(W2 + (tap * (M / 8) + gp) * U::PW2H,
-                     a.wpk2 + (size_t)(kc * 9 + tap) * U::Q2::WCH + p * U::Q2::PW + rank * U::PW2H, U::PW2H, &wres);
-      }
-    for (int gp = 0; gp < M / 8; ++gp) {  // W3
-      const int c = gp / (U::Q3::KC / 8), p = gp % (U::Q3::KC / 8);
-      tc::bulk_g2s(W3 + gp * U::PW3H, a.wpk3 + (size_t)c * U::Q3::WCH + p * U::Q3::PW + rank * U::PW3H, U::PW3H, &wres);
-    }
-  }
-  tc::pdl_wait();  // x, the rim snapshot and the index list of the previous launches are visible
-  const int B = ld_count(a.count, a.cap);
-  const int nb = B > pair ? (B - 1 - pair) / npairs + 1 : 0;
-
-  if (warp < 4) {
-    // ------------------------------------------------ BN1 + ReLU on my window tile
-    // 64-channel chunks (8 pieces per pixel row): thread gt owns pixel column wx = gt / 8
-    // and channel group gt % 8 of all 8 tile rows, so its rim pieces are known up front: all
-    // 8 when wx is a window edge column, else the one window edge row of this rank's tile.
-    // In place they come from the snapshot, loaded BEFORE the tile lands (their latency
-    // overlaps the TMA); the landed (possibly overwritten) rim values are never read.
-    static_assert(U::KC1 == 64 && kFBnThreads == 128, "pair BN mapping: 64-channel chunks, 128 threads");
-    const float* s1 = par1;
-    const int gt = tid, wx = gt >> 3, grp = gt & 7;
-    const bool edge = wx == 0 || wx == kFB - 1;
-    const int rim_jj = rank == 0 ? 0 : 7;  // tile row that is window row 0 (rank 0) / 15 (rank 1)
-    const Rim rim{kFB, kFB, 1};
-    int c = 0;
-    for (int k = 0; k < nb; ++k) {
-      const int j = pair + k * npairs;
-#pragma unroll 1
-      for (int kc = 0; kc < U::NKC1; ++kc, ++c) {
-        const int s = c % U::SA;
-        uint4 raw[8], rone = make_uint4(0, 0, 0, 0);
-        if (a.rim) {
-          const __nv_bfloat16* rj = a.rim + (size_t)j * rim.pixels() * C + kc * U::KC1 + grp * 8;
-          if (edge) {
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              raw[jj] = __ldcg(reinterpret_cast<const uint4*>(rj + (size_t)rim.index(8 * (int)rank + jj, wx) * C));
-          } else {
-            rone = __ldcg(reinterpret_cast<const uint4*>(rj + (size_t)rim.index(8 * (int)rank + rim_jj, wx) * C));
-          }
-        }
-        tc::mbar_wait_sleep(&a_load[s], (c / U::SA) & 1);
-        if (gt == 0 && kc == 0) ftrace(a, kFevLanded, k);
-        uint8_t* A = A1 + s * U::ACH;
-#ifdef SBN_PAIR_SKIP_BN
-        tc::fence_async_smem();
-        arrive_r0(&a_full[s], rank);
-        continue;
-#endif
-        const uint4 sg4 = *reinterpret_cast<const uint4*>(s1 + (kc * U::KC1 + grp * 8) / 2);
-        const uint4 vv4 = *reinterpret_cast<const uint4*>(s1 + C / 2 + (kc * U::KC1 + grp * 8) / 2);
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int r = jj * 16 + wx;  // tile row (pixel) of piece jj
-          if (a.rim && edge) continue;
-          if (a.rim && jj == rim_jj) {
-            raw[jj] = rone;
-            continue;
-          }
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(raw[jj].x), "=r"(raw[jj].y), "=r"(raw[jj].z), "=r"(raw[jj].w)
-                       : "r"(tc::smem_u32(A + r * U::ROWB + (grp ^ (r & 7)) * 16)));
-        }
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          const int r = jj * 16 + wx;
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw[jj]);
-          const __nv_bfloat162* hs = reinterpret_cast<const __nv_bfloat162*>(&sg4);
-          const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&vv4);
-          const __nv_bfloat162 z2 = __float2bfloat162_rn(0.f);
-          uint32_t o[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const __nv_bfloat162 y = __hmax2(__hfma2(h[e], hs[e], hv[e]), z2);
-            o[e] = *reinterpret_cast<const uint32_t*>(&y);
-          }
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(A + r * U::ROWB + (grp ^ (r & 7)) * 16)),
-                       "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
-                       : "memory");
-        }
-        tc::fence_async_smem();
-        arrive_r0(&a_full[s], rank);
-        if (gt == 0 && kc == U::NKC1 - 1) ftrace(a, kFevBn, k);
-      }
-    }
-  } else if (warp < 8) {
-    // ------------------------------------------------ epilogue 3: my output rows -> out
-    const int qd = warp & 3, r = qd * 32 + lane;
-    const uint32_t lanes = (uint32_t)(qd * 32) << 16;
-    const float* b3 = par3;
-    for (int k = 0; k < nb; ++k) {
-      const int j = pair + k * npairs;
-      const int n = __ldg(a.idx + 3 * j), by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-      const int q = (int)rank * 128 + r, oy = q >> 4, ox = q & 15;
-      const int Y = by * g.obh + oy, X = bx * g.obw + ox;
-      const bool store = oy < OB && ox < OB && Y < g.oh && X < g.ow;
-      uint4* dp = reinterpret_cast<uint4*>(a.dst + (((long)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * C);
-      if (r < 8) {  // pull my 8 output pixel rows of the residual into L2 while GEMM3 runs
-        const int Yr = by * g.obh + 8 * (int)rank + r, X0 = bx * g.obw;
-        const int w = min(OB, g.ow - X0);
-        if (8 * (int)rank + r < OB && Yr < g.oh && w > 0)
-          tc::prefetch_l2(a.dst + (((long)n * g.oh + Yr) * g.ow + X0) * C, (uint32_t)(w * C * 2));
-      }
-      tc::mbar_wait_sleep(&acc3_full, k & 1);
-      tc::fence_after();
-      const uint32_t acc = tmem + lanes + U::COL3;
-#ifdef SBN_PAIR_SKIP_E3
-      arrive_r0_relaxed(&acc3_empty, rank);
-      continue;
-#endif
-#pragma unroll 1
-      for (int c0 = 0; c0 < C; c0 += 32) {  // the residual of 32 channels in flight per step
-        uint4 xr[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) xr[e] = tc::ld_v4_pred(dp + c0 / 8 + e, store);
-        float v[32];
-        tc::tmem_ld32(acc + c0, v);
-        uint32_t o[16];
-#pragma unroll
-        for (int q2 = 0; q2 < 16; ++q2) {
-          const float2 bb = *reinterpret_cast<const float2*>(b3 + c0 + 2 * q2);
-          const __nv_bfloat162 st = __floats2bfloat162_rn(v[2 * q2] + bb.x, v[2 * q2 + 1] + bb.y);
-          const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr[q2 / 4]);
-          const float2 uf = __bfloat1622float2(st), xf = __bfloat1622float2(xh[q2 % 4]);
-          o[q2] = tc::pack_bf16(xf.x + uf.x, xf.y + uf.y);
-        }
-        if (store)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) dp[c0 / 8 + e] = make_uint4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
-      }
-      tc::fence_before();
-      arrive_r0_relaxed(&acc3_empty, rank);
-      if (r == 0) ftrace(a, kFevE3, k);
-    }
-  } else if (warp < 12) {
-    // ------------------------------------------------ epilogue 1: my S1 rows -> A2 (+ halo rows to rank 0)
-    const int qd = warp & 3, r = qd * 32 + lane;
-    const uint32_t lanes = (uint32_t)(qd * 32) << 16;
-    const float* sc = par1 + 2 * C + M;  // s2
-    const float* sh = sc + M;            // t2' (b1 folded)
-    // rank 1's S1 rows 128..161 are also rank 0's A2 rows 128..161 (its shifted views)
-    const bool halo = rank == 1 && r < kPR2 - 128;
-    uint32_t a2peer = 0;
-    if (rank == 1) {
-      const uint32_t mine = tc::smem_u32(A2 + (128 + r) * 16);
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a2peer) : "r"(mine), "r"(0));
-    }
-    for (int k = 0; k < nb; ++k) {
-      const int j = pair + k * npairs;
-      const int by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-      const int p = (int)rank * 128 + r, wy = p >> 4, wx = p & 15;
-      const int y = g.oy + by * g.sy + wy, x = g.ox + bx * g.sx + wx;
-      const bool valid = y >= 0 && y < g.h && x >= 0 && x < g.w;
-      tc::mbar_wait_sleep(&a2_empty, (k & 1) ^ 1);  // GEMM2 of the previous block read A2 (both ranks)
-      tc::mbar_wait_sleep(&acc1_full, k & 1);
-      tc::fence_after();
-      if (r == 0) ftrace(a, kFevE1s, k);
-#pragma unroll
-      for (int g0 = 0; g0 < M; g0 += 32) {
-        float v[32];
-        tc::tmem_ld32(tmem + lanes + g0, v);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 16 * hh;
-          const float* w = v + 16 * hh;
-          uint32_t o[8];
-#pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q);
-            const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q);
-            const float u0 = fmaxf(fmaf(w[2 * q], s4.x, t4.x), 0.f);
-            const float u1 = fmaxf(fmaf(w[2 * q + 1], s4.y, t4.y), 0.f);
-            const float u2 = fmaxf(fmaf(w[2 * q + 2], s4.z, t4.z), 0.f);
-            const float u3 = fmaxf(fmaf(w[2 * q + 3], s4.w, t4.w), 0.f);
-            o[q] = valid ? tc::pack_bf16(u0, u1) : 0u;
-            o[q + 1] = valid ? tc::pack_bf16(u2, u3) : 0u;
-          }
-          uint8_t* pl = A2 + (c0 / 8) * kPPA2 + r * 16;
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl)), "r"(o[0]), "r"(o[1]),
-                       "r"(o[2]), "r"(o[3])
-                       : "memory");
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl + kPPA2)), "r"(o[4]),
-                       "r"(o[5]), "r"(o[6]), "r"(o[7])
-                       : "memory");
-          if (halo) {
-            st_cluster_v4(a2peer + (c0 / 8) * kPPA2, o[0], o[1], o[2], o[3]);
-            st_cluster_v4(a2peer + (c0 / 8 + 1) * kPPA2, o[4], o[5], o[6], o[7]);
-          }
-        }
-      }
-      tc::fence_before();
-      arrive_r0_relaxed(&acc1_empty, rank);
-      asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
-      arrive_r0(&a2_full, rank);
-      if (r == 0) ftrace(a, kFevE1, k);
-    }
-  } else if (warp < 16) {
-    // ------------------------------------------------ epilogue 2: my output rows -> A3
-    const int qd = warp & 3, r = qd * 32 + lane;
-    const uint32_t lanes = (uint32_t)(qd * 32) << 16;
-    const float* sc = par2 + M;  // s3
-    const float* sh = sc + M;    // t3' (b2 folded)
-    for (int k = 0; k < nb; ++k) {
-      const int b2 = k & 1;
-      tc::mbar_wait_sleep(&acc2_full[b2], (k >> 1) & 1);
-      tc::mbar_wait_sleep(&a3_empty, (k & 1) ^ 1);
-      tc::fence_after();
-      if (r == 0) ftrace(a, kFevE2a, k);
-      const uint32_t acc = tmem + lanes + U::COL2 + b2 * M;
-#pragma unroll
-      for (int g0 = 0; g0 < M; g0 += 32) {
-        float v[32];
-        tc::tmem_ld32(acc + g0, v);
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int c0 = g0 + 16 * hh;
-          const float* w = v + 16 * hh;
-          uint32_t o[8];
-#pragma unroll
-          for (int q2 = 0; q2 < 8; q2 += 2) {
-            const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q2);
-            const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q2);
-            o[q2] = tc::pack_bf16(fmaxf(fmaf(w[2 * q2], s4.x, t4.x), 0.f), fmaxf(fmaf(w[2 * q2 + 1], s4.y, t4.y), 0.f));
-            o[q2 + 1] =
-                tc::pack_bf16(fmaxf(fmaf(w[2 * q2 + 2], s4.z, t4.z), 0.f), fmaxf(fmaf(w[2 * q2 + 3], s4.w, t4.w), 0.f));
-          }
-          uint8_t* pl = A3 + (c0 / 8) * kPPA3 + r * 16;
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl)), "r"(o[0]), "r"(o[1]),
-                       "r"(o[2]), "r"(o[3])
-                       : "memory");
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(tc::smem_u32(pl + kPPA3)), "r"(o[4]),
-                       "r"(o[5]), "r"(o[6]), "r"(o[7])
-                       : "memory");
-        }
-      }
-      tc::fence_before();
-      arrive_r0_relaxed(&acc2_empty[b2], rank);
-      tc::fence_async_smem();
-      arrive_r0(&a3_full, rank);
-      if (r == 0) ftrace(a, kFevE2, k);
-    }
-  } else if (warp == kLWarp) {
-    // ------------------------------------------------ loader: my window tile of each block
-    if (lane == 0) {
-      if (rank == 1) {  // tell rank 0's issuer that my weight halves have landed
-        tc::mbar_wait_sleep(&wres, 0);
-        tc::mbar_arrive_cluster(&wpeer, 0);
-      }
-      int c = 0;
-      for (int k = 0; k < nb; ++k) {
-        const int j = pair + k * npairs;
-        const int cn = __ldg(a.idx + 3 * j);
-        const int cy = g.oy + __ldg(a.idx + 3 * j + 1) * g.sy + 8 * (int)rank;
-        const int cx = g.ox + __ldg(a.idx + 3 * j + 2) * g.sx;
-        for (int kc = 0; kc < U::NKC1; ++kc, ++c) {
-          const int s = c % U::SA;
-          tc::mbar_wait_sleep(&a_empty[s], ((c / U::SA) & 1) ^ 1);
-          if (kc == 0) ftrace(a, kFevLoad, k);
-          tc::mbar_expect_tx(&a_load[s], (uint32_t)U::ACH);
-          tma_4d(A1 + s * U::ACH, &a.tmap, kc * U::KC1, cx, cy, cn, &a_load[s]);
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == kMWarp) {
-    // ------------------------------------------------ MMA issuer (rank 0): M = 256 over the pair
-    if (lane == 0 && rank == 0) {
-      tc::mbar_wait(&wres, 0);
-      mbar_wait_cl(&wpeer, 0);
-      int c = 0;
-      auto g1 = [&](int k) {
-        constexpr uint32_t idesc = tc::idesc_bf16_f32(256, M);
-        mbar_wait_cl(&acc1_empty, (k & 1) ^ 1);
-        tc::fence_after();
-        ftrace(a, kFevG1s, k);
-        for (int kc = 0; kc < U::NKC1; ++kc, ++c) {
-          const int s = c % U::SA;
-          mbar_wait_cl(&a_full[s], (c / U::SA) & 1);
-          tc::fence_after();
-          const uint32_t abase = tc::smem_u32(A1 + s * U::ACH);
-#pragma unroll
-          for (int kk = 0; kk < U::KC1 / 16; ++kk)
-            tc::mma_bf16_cg2(tmem, tc::desc_kmajor_swz(abase + kk * 32, 8 * U::ROWB, U::SWZ),
-                             tc::desc_kmajor_noswz(tc::smem_u32(W1) + (kc * (U::KC1 / 8) + 2 * kk) * U::PW1H, U::PW1H, 128),
-                             idesc, (kc | kk) > 0);
-          tc::mma_commit_mc(&a_empty[s], 3);
-        }
-        tc::mma_commit_mc(&acc1_full, 3);
-        ftrace(a, kFevG1, k);
-      };
-      auto g2 = [&](int k) {
-        constexpr uint32_t idesc = tc::idesc_bf16_f32(256, M);
-        const int b2 = k & 1;
-        mbar_wait_cl(&acc2_empty[b2], ((k >> 1) & 1) ^ 1);
-        mbar_wait_cl(&a2_full, k & 1);
-        tc::fence_after();
-        ftrace(a, kFevG2, k);
-        // one base descriptor per operand, immediate offsets per MMA (fully unrolled: the
-        // issuer shares its scheduler with busy warps, so instructions per MMA matter)
-        const uint64_t a2d = tc::desc_kmajor_noswz(tc::smem_u32(A2), kPPA2, 128);
-        const uint64_t w2d = tc::desc_kmajor_noswz(tc::smem_u32(W2), U::PW2H, 128);
-#pragma unroll
-        for (int kc = 0; kc < U::NKC2; ++kc)
-#pragma unroll
-          for (int tap = 0; tap < 9; ++tap)
-#pragma unroll
-            for (int kk = 0; kk < U::KC2 / 16; ++kk) {
-              const int shift = (tap / 3) * kFB + (tap % 3), pl = kc * U::P2 + 2 * kk;
-              tc::mma_bf16_cg2(tmem + U::COL2 + b2 * M, tc::desc_add(a2d, pl * kPPA2 + shift * 16),
-                               tc::desc_add(w2d, (tap * (M / 8) + pl) * U::PW2H), idesc, (kc | tap | kk) > 0);
-            }
-        tc::mma_commit_mc(&a2_empty, 3);
-        tc::mma_commit_mc(&acc2_full[b2], 3);
-        ftrace(a, kFevG2e, k);
-      };
-      auto g3 = [&](int k) {
-        constexpr uint32_t idesc = tc::idesc_bf16_f32(256, C);
-        mbar_wait_cl(&acc3_empty, (k & 1) ^ 1);
-        mbar_wait_cl(&a3_full, k & 1);
-        tc::fence_after();
-        ftrace(a, kFevG3, k);
-#pragma unroll
-        for (int kk = 0; kk < M / 16; ++kk)
-          tc::mma_bf16_cg2(tmem + U::COL3, tc::desc_kmajor_noswz(tc::smem_u32(A3) + 2 * kk * kPPA3, kPPA3, 128),
-                           tc::desc_kmajor_noswz(tc::smem_u32(W3) + 2 * kk * U::PW3H, U::PW3H, 128), idesc, kk > 0);
-        tc::mma_commit_mc(&a3_empty, 3);
-        tc::mma_commit_mc(&acc3_full, 3);
-      };
-      if (nb > 0) g1(0);
-      for (int k = 0; k < nb; ++k) {
-        g2(k);
-        if (k + 1 < nb) g1(k + 1);
-        if (k > 0) g3(k - 1);
-      }
-      if (nb > 0) g3(nb - 1);
-    }
-    __syncwarp();
-  }
-  if (tid == kLWarp * 32) tc::mbar_wait_sleep(&wres, 0);  // no copy in flight at exit
-  tc::fence_before();
-  __syncthreads();
-  tc::cluster_sync();  // the peer's MMAs / remote arrivals / DSMEM writes are done before TMEM is freed
-  tc::fence_after();
-  if (warp == 0) tc::tmem_free_cg2<U::TALLOC>(tmem);
 }
 
 // ---- packed image: [W1 chunks | W2 chunks | W3 chunks | params], regions 128-B aligned.
@@ -1898,49 +1404,6 @@ int launch_fused(const WArgs& a, long cap, cudaStream_t s) {
 }
 
 template <int C, int M>
-bool pair_ok(int b) {
-  if constexpr (PUCfg<C, M>::OK) {
-    return b == kFB && PUCfg<C, M>::SMEM <= max_smem_optin() && !(debug_flags() & kDebugWideUnfused);
-  } else {
-    (void)b;
-    return false;
-  }
-}
-
-template <int C, int M>
-int launch_pair_unit(const WArgs& a, long cap, cudaStream_t s) {
-  if constexpr (PUCfg<C, M>::OK) {
-    using U = PUCfg<C, M>;
-    auto kern = unit_wide_pair_kernel<C, M>;
-    static PerDeviceOnce once;
-    once([&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, U::SMEM); });
-    const long maxp = sm_count() / 2;
-    const long npairs = cap < maxp ? (cap < 1 ? 1 : cap) : maxp;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * npairs));
-    cfg.blockDim = dim3(kWideThreads);
-    cfg.dynamicSmemBytes = U::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, kern, a);
-    return launch_status("residual_unit_wide_pair");
-  } else {
-    (void)a;
-    (void)cap;
-    (void)s;
-    return SBN_ERR_UNSUPPORTED;
-  }
-}
-
-template <int C, int M>
 int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const int32_t* idx,
              const int32_t* count, int cap, uint8_t* s1, uint8_t* s2, cudaStream_t s) {
   constexpr WLayout L = wide_layout<C, M>();
@@ -1973,7 +1436,7 @@ int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const i
     if (st) return st;
   }
   int st = 0;
-  if (fused_ok<C, M>(b) || pair_ok<C, M>(b)) {
+  if (fused_ok<C, M>(b)) {
     // the whole unit in one launch; in place, the rims of the active windows are
     // snapshotted first (into the S1 stack, which this path does not use)
     if (x == out) {
@@ -1988,7 +1451,7 @@ int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const i
     a.par2 = (const float*)(img + L.p2);
     a.wpk3 = img + L.w3;
     a.par3 = (const float*)(img + L.p3);
-    return fused_ok<C, M>(b) ? launch_fused<C, M>(a, cap, s) : launch_pair_unit<C, M>(a, cap, s);
+    return launch_fused<C, M>(a, cap, s);
   }
   a.dst = (__nv_bfloat16*)s1;
   a.dst_rows = rows1;
@@ -2046,7 +1509,7 @@ bool unit_wide_supported(int dtype, int c, int m, const Geo& g, int halo, int pr
 
 bool unit_wide_one_launch(int c, int m, const Geo& g) {
   if (g.bh != g.bw) return false;
-#define X(C_, M_) if (c == C_ && m == M_) return fused_ok<C_, M_>(g.bh) || pair_ok<C_, M_>(g.bh);
+#define X(C_, M_) if (c == C_ && m == M_) return fused_ok<C_, M_>(g.bh);
   SBN_UNIT_WIDE_CONFIGS(X)
 #undef X
   return false;
