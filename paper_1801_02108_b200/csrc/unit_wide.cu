@@ -1209,21 +1209,23 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         tc::fence_after();
         ftrace(a, kFevG2, k);
         const uint32_t acc = tmem + F::COL2 + b2 * 2 * M;
-        const uint32_t a2base = tc::smem_u32(A2 + b2 * F::A2B);
+        // one base descriptor per operand, offset per (K-chunk, tap) and per MMA (the issuer
+        // shares its scheduler with busy warps: instructions per MMA matter)
+        const uint64_t a2d = tc::desc_kmajor_noswz(tc::smem_u32(A2 + b2 * F::A2B), kFPA2, 128);
+        const uint64_t w2d = tc::desc_kmajor_noswz(tc::smem_u32(W2), F::PW2, 128);
 #pragma unroll 1
         for (int kc = 0; kc < F::NKC2; ++kc)
 #pragma unroll 1
           for (int tap = 0; tap < 9; ++tap) {  // (rolled: the unrolled tap loop made the issuer spill)
-            const uint32_t wbase = tc::smem_u32(W2 + (kc * 9 + tap) * F::WCH2);
             const int shift = (tap / 3) * kFB + (tap % 3);
+            const uint64_t at = tc::desc_add(a2d, kc * F::P2 * kFPA2 + shift * 16);
+            const uint64_t wt = tc::desc_add(w2d, (kc * 9 + tap) * F::WCH2);
 #pragma unroll
             for (int u = 0; u < 2; ++u)
 #pragma unroll
               for (int kk = 0; kk < F::KC2 / 16; ++kk)
-                tc::mma_bf16(acc + u * M,
-                             tc::desc_kmajor_noswz(a2base + (kc * F::P2 + 2 * kk) * kFPA2 + (u * 128 + shift) * 16,
-                                                   kFPA2, 128),
-                             tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW2, F::PW2, 128), idesc, (kc | tap | kk) > 0);
+                tc::mma_bf16(acc + u * M, tc::desc_add(at, 2 * kk * kFPA2 + u * 128 * 16),
+                             tc::desc_add(wt, 2 * kk * F::PW2), idesc, (kc | tap | kk) > 0);
           }
         tc::mma_commit(&a2_empty[b2]);
         tc::mma_commit(&acc2_full[b2]);
