@@ -362,15 +362,15 @@ __global__ void __launch_bounds__(kCThreads, CCfg<CIN, COUT, KS>::CPS) conv_dens
             const int sw = Q::RES ? 0 : wit % SWB;
             if (!Q::RES) tc::mbar_wait(&w_full[sw], (wit / SWB) & 1);
             tc::fence_after();
-            const uint32_t abase = tc::smem_u32(Aring + s * Q::ACH);
-            const uint32_t wbase = tc::smem_u32(Wring + (Q::RES ? (kc * Q::TAPS + tap) * Q::WCH : sw * Q::WCH));
+            const uint64_t ad = tc::desc_kmajor_swz(tc::smem_u32(Aring + s * Q::ACH), 8 * Q::ROWB, Q::SWZ);
+            const uint64_t wd = tc::desc_kmajor_noswz(
+                tc::smem_u32(Wring + (Q::RES ? (kc * Q::TAPS + tap) * Q::WCH : sw * Q::WCH)), Q::PW, 128);
 #pragma unroll
             for (int kk = 0; kk < Q::KC / 16; ++kk)
 #pragma unroll
               for (int h = 0; h < Q::NSPLIT; ++h)
-                tc::mma_bf16(acc + h * Q::NS, tc::desc_kmajor_swz(abase + kk * 32, 8 * Q::ROWB, Q::SWZ),
-                             tc::desc_kmajor_noswz(wbase + 2 * kk * Q::PW + h * Q::NS * 16, Q::PW, 128), idesc,
-                             (kc | tap | kk) > 0);
+                tc::mma_bf16(acc + h * Q::NS, tc::desc_add(ad, kk * 32), tc::desc_add(wd, 2 * kk * Q::PW + h * Q::NS * 16),
+                             idesc, (kc | tap | kk) > 0);
             tc::mma_commit(&a_empty[s]);
             if (!Q::RES) {
               tc::mma_commit(&w_empty[sw]);
@@ -622,15 +622,15 @@ __global__ void __launch_bounds__(kCThreads, 1) conv_dense_pair_kernel(const __g
             const int sw = P::RES ? 0 : wit % SWB;
             if (!P::RES) tc::mbar_wait(&w_full[sw], (wit / SWB) & 1);
             tc::fence_after();
-            const uint32_t abase = tc::smem_u32(Aring + s * P::ACH);
-            const uint32_t wbase = tc::smem_u32(Wring + (P::RES ? (kc * P::TAPS + tap) * P::WCHR : sw * P::WCHR));
+            const uint64_t ad = tc::desc_kmajor_swz(tc::smem_u32(Aring + s * P::ACH), 8 * P::ROWB, P::SWZ);
+            const uint64_t wd = tc::desc_kmajor_noswz(
+                tc::smem_u32(Wring + (P::RES ? (kc * P::TAPS + tap) * P::WCHR : sw * P::WCHR)), P::PWR, 128);
 #pragma unroll
             for (int kk = 0; kk < P::KC / 16; ++kk)
 #pragma unroll
               for (int h = 0; h < P::NSPLIT; ++h)
-                tc::mma_bf16_cg2(acc + h * P::NS, tc::desc_kmajor_swz(abase + kk * 32, 8 * P::ROWB, P::SWZ),
-                                 tc::desc_kmajor_noswz(wbase + 2 * kk * P::PWR + h * P::NHS * 16, P::PWR, 128), idesc,
-                                 (kc | tap | kk) > 0);
+                tc::mma_bf16_cg2(acc + h * P::NS, tc::desc_add(ad, kk * 32), tc::desc_add(wd, 2 * kk * P::PWR + h * P::NHS * 16),
+                                 idesc, (kc | tap | kk) > 0);
             tc::mma_commit_mc(&a_empty[s], 3);
             if (!P::RES) {
               tc::mma_commit_mc(&w_empty[sw], 3);

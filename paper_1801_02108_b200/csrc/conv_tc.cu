@@ -253,15 +253,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs a) {
           tc::mbar_wait(&full[s], (it / K::STAGES) & 1);
           tc::fence_after();
           const int shift = (tap / 3) * BS + (tap % 3);
-          const uint32_t wbase = tc::smem_u32(Wst + s * K::TAP);
+          // one descriptor per operand and tap, immediate offsets per MMA (tc::desc_add)
+          const uint64_t ad = tc::desc_kmajor_noswz(tc::smem_u32(A) + shift * 16, K::PA, 128);
+          const uint64_t wd = tc::desc_kmajor_noswz(tc::smem_u32(Wst + s * K::TAP), K::PW, 128);
 #pragma unroll
           for (int t = 0; t < K::NT; ++t)
 #pragma unroll
             for (int k = 0; k < CIN / 16; ++k)
-              tc::mma_bf16(tmem + t * COUT,
-                           tc::desc_kmajor_noswz(tc::smem_u32(A + 2 * k * K::PA + (t * 128 + shift) * 16), K::PA, 128),
-                           tc::desc_kmajor_noswz(wbase + 2 * k * K::PW, K::PW, 128), idesc,
-                           (tap | k) > 0);
+              tc::mma_bf16(tmem + t * COUT, tc::desc_add(ad, 2 * k * K::PA + t * 128 * 16),
+                           tc::desc_add(wd, 2 * k * K::PW), idesc, (tap | k) > 0);
           tc::mma_commit(&empty[s]);  // frees the weight stage once these MMAs are done
         }
         tc::mma_commit(&accb);
@@ -463,16 +463,17 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
           t_w += clock64() - c3;
           tc::fence_after();
           const int shift = (tap / 3) * BS + (tap % 3);
-          const uint32_t wbase = tc::smem_u32(Wst + s * K::TAP);
+          // one descriptor per operand and tap, immediate offsets per MMA (tc::desc_add)
+          const uint64_t ad = tc::desc_kmajor_noswz(tc::smem_u32(A) + shift * 16, K::PA, 128);
+          const uint64_t wd = tc::desc_kmajor_noswz(tc::smem_u32(Wst + s * K::TAP), K::PW, 128);
           const int tm = job_tiles(job);
 #pragma unroll
           for (int t = 0; t < K::NT; ++t)
 #pragma unroll
             for (int kk = 0; kk < CIN / 16; ++kk)
               if (tm >> t & 1)
-              tc::mma_bf16(acc + t * COUT,
-                           tc::desc_kmajor_noswz(tc::smem_u32(A + 2 * kk * K::PA + (t * 128 + shift) * 16), K::PA, 128),
-                           tc::desc_kmajor_noswz(wbase + 2 * kk * K::PW, K::PW, 128), idesc, (tap | kk) > 0);
+              tc::mma_bf16(acc + t * COUT, tc::desc_add(ad, 2 * kk * K::PA + t * 128 * 16),
+                           tc::desc_add(wd, 2 * kk * K::PW), idesc, (tap | kk) > 0);
           tc::mma_commit(&empty[s]);
         }
         tc::mma_commit(&win_empty[b]);

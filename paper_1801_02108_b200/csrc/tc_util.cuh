@@ -32,7 +32,9 @@ __device__ __forceinline__ uint64_t desc_kmajor_noswz(uint32_t saddr, uint32_t l
 // the same operand view `bytes` further on (a multiple of 16): only the 14-bit start-address
 // field changes, so the single-thread MMA issuers offset one base descriptor instead of
 // rebuilding it (the start field of smem addresses < 256 KB cannot carry)
-__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) {
+  return (d & 0xFFFFFFFF00000000ull) | (uint32_t)((uint32_t)d + (bytes >> 4));  // one 32-bit add
+}
 
 // K-major swizzled operand (rows of 64 B (SWIZZLE_64B, layout 4) or 128 B (SWIZZLE_128B,
 // layout 2), 8-row atoms at SBO bytes), as TMA writes it with the matching swizzle mode.

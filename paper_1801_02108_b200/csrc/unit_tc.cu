@@ -571,8 +571,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 #pragma unroll
         for (int k = 0; k < C / 16; ++k)
           tc::mma_bf16(tmem + K::COL1 + t * MC,
-                       tc::desc_kmajor_noswz(tc::smem_u32(A1 + 2 * k * K::P1 + t * 128 * 16), K::P1, 128),
-                       tc::desc_kmajor_noswz(tc::smem_u32(B1 + 2 * k * K::PB1), K::PB1, 128), id1, k > 0);
+                       tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(A1), K::P1, 128), 2 * k * K::P1 + t * 128 * 16),
+                       tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(B1), K::PB1, 128), 2 * k * K::PB1), id1, k > 0);
       tc::mma_commit(&bar);
       trace(a.trace, 12);
     }
@@ -621,8 +621,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 #pragma unroll
           for (int k = 0; k < MC / 16; ++k)
             tc::mma_bf16(tmem + K::COL2 + t * MC,
-                         tc::desc_kmajor_noswz(tc::smem_u32(A2 + 2 * k * K::P2 + (t * 128 + shift) * 16), K::P2, 128),
-                         tc::desc_kmajor_noswz(tc::smem_u32(B2 + tap * K::TAPB + 2 * k * K::PB2), K::PB2, 128),
+                         tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(A2), K::P2, 128), 2 * k * K::P2 + (t * 128 + shift) * 16),
+                         tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(B2), K::PB2, 128), tap * K::TAPB + 2 * k * K::PB2),
                          id2, (tap | k) > 0);
         }
       tc::mma_commit(&bar);
@@ -680,8 +680,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
 #pragma unroll
         for (int k = 0; k < MC / 16; ++k)
           tc::mma_bf16(tmem + K::COL3 + t * C,
-                       tc::desc_kmajor_noswz(tc::smem_u32(A3 + 2 * k * K::P3 + t * 128 * 16), K::P3, 128),
-                       tc::desc_kmajor_noswz(tc::smem_u32(B3 + 2 * k * K::PB3), K::PB3, 128), id3, k > 0);
+                       tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(A3), K::P3, 128), 2 * k * K::P3 + t * 128 * 16),
+                       tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(B3), K::PB3, 128), 2 * k * K::PB3), id3, k > 0);
       tc::mma_commit(&bar);
       trace(a.trace, 14);
     }
@@ -1096,9 +1096,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
       constexpr uint32_t id1 = tc::idesc_bf16_f32(128, MC);
 #pragma unroll
       for (int k = 0; k < C / 16; ++k)
-        tc::mma_bf16(tmem + PK::COL1,
-                     tc::desc_kmajor_noswz(tc::smem_u32(A1 + 2 * k * PK::P1), PK::P1, 128),
-                     tc::desc_kmajor_noswz(tc::smem_u32(B1 + 2 * k * K::PB1), K::PB1, 128), id1, k > 0);
+        tc::mma_bf16(tmem + PK::COL1, tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(A1), PK::P1, 128), 2 * k * PK::P1),
+                     tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(B1), K::PB1, 128), 2 * k * K::PB1), id1, k > 0);
       tc::mma_commit(&bar);
     }
     tc::mbar_wait(&bar, phase);
@@ -1159,8 +1158,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
 #pragma unroll
         for (int k = 0; k < MC / 16; ++k)
           tc::mma_bf16(tmem + PK::COL2,
-                       tc::desc_kmajor_noswz(tc::smem_u32(A2 + 2 * k * PK::P2 + shift * 16), PK::P2, 128),
-                       tc::desc_kmajor_noswz(tc::smem_u32(B2 + tap * K::TAPB + 2 * k * K::PB2), K::PB2, 128),
+                       tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(A2), PK::P2, 128), 2 * k * PK::P2 + shift * 16),
+                       tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(B2), K::PB2, 128), tap * K::TAPB + 2 * k * K::PB2),
                        id2, (tap | k) > 0);
       }
       tc::mma_commit(&bar);
@@ -1205,9 +1204,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
       constexpr uint32_t id3 = tc::idesc_bf16_f32(128, C);
 #pragma unroll
       for (int k = 0; k < MC / 16; ++k)
-        tc::mma_bf16(tmem + PK::COL3,
-                     tc::desc_kmajor_noswz(tc::smem_u32(A3 + 2 * k * PK::P3), PK::P3, 128),
-                     tc::desc_kmajor_noswz(tc::smem_u32(B3 + 2 * k * K::PB3), K::PB3, 128), id3, k > 0);
+        tc::mma_bf16(tmem + PK::COL3, tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(A3), PK::P3, 128), 2 * k * PK::P3),
+                     tc::desc_add(tc::desc_kmajor_noswz(tc::smem_u32(B3), K::PB3, 128), 2 * k * K::PB3), id3, k > 0);
       tc::mma_commit(&bar);
     }
     tc::mbar_wait(&bar, phase);

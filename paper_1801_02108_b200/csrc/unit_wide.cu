@@ -171,11 +171,19 @@ struct __align__(64) WArgs {
 
 // CTA 0 event log (diagnostics): slot ev*64 + tile, tiles < 64
 enum { kEvPub = 0, kEvMma = 1, kEvAcc = 2, kEvEpi = 3, kEvIss = 4, kEvLoad = 5, kEvCIss = 7, kEvCData = 8, kEvCPub = 11 };
+// (diagnostics build only: the stamps' checks and live registers slow the single-thread
+// MMA issuers; tools/build_variant.sh trace -DSBN_TRACE_WIDE, then SBN_LIB_PATH=tools/bin/trace.so)
 __device__ __forceinline__ void wtrace(const WArgs& a, int ev, int t) {
+#ifdef SBN_TRACE_WIDE
   if (a.trace && blockIdx.x == 0 && t < 64) {
     a.trace[ev * 64 + t] = gtimer();
     a.trace[1024 + ev * 64 + t] = clock64();
   }
+#else
+  (void)a;
+  (void)ev;
+  (void)t;
+#endif
 }
 
 // tiles of the GEMM for B active blocks of size b
@@ -682,6 +690,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           if (MODE != kIn && kc == Q::NKC - 1) wtrace(a, kEvPub, k);
           if (MODE != kIn) wtrace(a, kEvCData, ait);
           const uint32_t abase = tc::smem_u32(Aring + sa * Q::ACH);
+#pragma unroll
           for (int tap = 0; tap < Q::TAPS; ++tap, ++wit) {
             const int sw = Q::RES ? 0 : wit % SWB;
             if (!Q::RES) {
@@ -690,15 +699,17 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             }
             const int shift = MODE == kMid ? (tap / 3) * b + (tap % 3) : 0;
             const uint32_t wbase = tc::smem_u32(Wring + (Q::RES ? (kc * Q::TAPS + tap) * Q::WCH : sw * Q::WCH));
+            // one descriptor per operand and tap, immediate offsets per MMA (the issuer shares
+            // its scheduler with the busy BN / epilogue warps)
+            const uint64_t ad = MODE == kIn ? tc::desc_kmajor_swz(abase, 8 * Q::ROWB, Q::SWZ)
+                                            : tc::desc_kmajor_noswz(abase + shift * 16, Q::PA, 128);
+            const uint64_t wd = tc::desc_kmajor_noswz(wbase, Q::PW, 128);
 #pragma unroll
             for (int kk = 0; kk < Q::KC / 16; ++kk)
 #pragma unroll
               for (int h = 0; h < Q::NSPLIT; ++h)
-                tc::mma_bf16(acc + h * Q::NS,
-                             MODE == kIn ? tc::desc_kmajor_swz(abase + kk * 32, 8 * Q::ROWB, Q::SWZ)
-                                         : tc::desc_kmajor_noswz(abase + 2 * kk * Q::PA + shift * 16, Q::PA, 128),
-                             tc::desc_kmajor_noswz(wbase + 2 * kk * Q::PW + h * Q::NS * 16, Q::PW, 128),
-                             idesc, (kc | tap | kk) > 0);
+                tc::mma_bf16(acc + h * Q::NS, tc::desc_add(ad, MODE == kIn ? kk * 32 : 2 * kk * Q::PA),
+                             tc::desc_add(wd, 2 * kk * Q::PW + h * Q::NS * 16), idesc, (kc | tap | kk) > 0);
             if (!Q::RES) tc::mma_commit(&w_empty[sw]);
           }
           tc::mma_commit(&a_empty[sa]);
@@ -793,18 +804,9 @@ struct FCfg {
   static constexpr int SMEM = OFF_PAR + PARB;
 };
 
-// per-block stamps (CTA 0) only in a diagnostics build: the stamps' live registers make the
-// single-thread MMA issuer spill at 96 registers per thread
-//   tools/build_variant.sh trace -DSBN_TRACE_FUSED; SBN_LIB_PATH=tools/bin/trace.so python tools/trace_fused.py
-__device__ __forceinline__ void ftrace(const WArgs& a, int ev, int k) {
-#ifdef SBN_TRACE_FUSED
-  wtrace(a, ev, k);
-#else
-  (void)a;
-  (void)ev;
-  (void)k;
-#endif
-}
+// per-block stamps (CTA 0), diagnostics build only (see wtrace)
+//   tools/build_variant.sh trace -DSBN_TRACE_WIDE; SBN_LIB_PATH=tools/bin/trace.so python tools/trace_fused.py
+__device__ __forceinline__ void ftrace(const WArgs& a, int ev, int k) { wtrace(a, ev, k); }
 
 // The issue order shared by the loader and the MMA issuer: GEMM1 tiles g1(k, t), GEMM2
 // blocks g2(k), GEMM3 blocks g3(k), k over this CTA's nb blocks.

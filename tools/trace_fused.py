@@ -4,7 +4,7 @@ window chunk (load), the first chunk landed (landed), BN1 finished the last chun
 GEMM1 of both tiles was issued (g1), epilogue 1 published A2 (e1), GEMM2 was issued (g2),
 epilogue 2 saw its accumulator (e2a) and released it (e2); microseconds from the first
 stamp; g1s / g3 / e1s / e3: GEMM1 issue start, GEMM3 issue, epilogue 1 start, epilogue 3 done.
-Needs the diagnostics build: tools/build_variant.sh trace -DSBN_TRACE_FUSED, then
+Needs the diagnostics build: tools/build_variant.sh trace -DSBN_TRACE_WIDE, then
 SBN_LIB_PATH=tools/bin/trace.so.
     python tools/trace_fused.py [stage 2|3] [frames]"""
 import os

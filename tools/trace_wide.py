@@ -3,7 +3,9 @@ per tile, when the A producers started issuing (iss), published the tile's last 
 (pub), the MMA thread started it (mma), the epilogue saw the accumulator (acc) and
 released it (epi); microseconds from the first stamp.  Only the LAST launch's stamps
 survive (each launch overwrites), so STAGE_KERNEL picks which of the three is traced.
-    python tools/trace_wide.py [stage 2..5] [in|mid|out]"""
+    python tools/trace_wide.py [stage 2..5] [in|mid|out]
+Needs the diagnostics build: tools/build_variant.sh trace -DSBN_TRACE_WIDE, then
+SBN_LIB_PATH=tools/bin/trace.so."""
 import os
 import sys
 
