@@ -147,28 +147,29 @@ __global__ void __launch_bounds__(kThreads)
 rim_kernel(const uint8_t* __restrict__ x, Geo g, Rim rim, int pix_bytes,
            const int32_t* __restrict__ idx, const int32_t* __restrict__ count, int cap,
            uint8_t* __restrict__ out) {
+  // CTA per active block (grid-strided over the device-side count), 32-bit index math:
+  // the rim of one block is P pixels x vpp vectors (config-4 stage 0: 60 x 12)
   using V = typename std::conditional<VS == 16, uint4, typename std::conditional<VS == 8, uint2, uint32_t>::type>::type;
   const int B = ld_count(count, cap);
   const int P = rim.pixels();
   const int vpp = pix_bytes / VS;
-  const long total = (long)B * P * vpp;
-  for (long i = blockIdx.x * (long)kThreads + threadIdx.x; i < total;
-       i += (long)gridDim.x * kThreads) {
-    const int k = (int)(i % vpp);
-    const long pr = i / vpp;
-    const int r = (int)(pr % P);
-    const int b = (int)(pr / P);
-    int wy, wx;
-    rim.coord(r, wy, wx);
+  const int per = P * vpp;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
     const int n = __ldg(idx + 3 * b);
-    const int y = g.oy + __ldg(idx + 3 * b + 1) * g.sy + wy;
-    const int xx = g.ox + __ldg(idx + 3 * b + 2) * g.sx + wx;
-    V v;
-    if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-      v = *(reinterpret_cast<const V*>(x + (((size_t)n * g.h + y) * g.w + xx) * pix_bytes) + k);
-    else
-      memset(&v, 0, sizeof(V));
-    reinterpret_cast<V*>(out)[i] = v;
+    const int y0 = g.oy + __ldg(idx + 3 * b + 1) * g.sy, x0 = g.ox + __ldg(idx + 3 * b + 2) * g.sx;
+    V* dst = reinterpret_cast<V*>(out) + (size_t)b * per;
+    for (int i = threadIdx.x; i < per; i += kThreads) {
+      const int r = i / vpp, k = i - r * vpp;
+      int wy, wx;
+      rim.coord(r, wy, wx);
+      const int y = y0 + wy, xx = x0 + wx;
+      V v;
+      if (y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+        v = *(reinterpret_cast<const V*>(x + (((size_t)n * g.h + y) * g.w + xx) * pix_bytes) + k);
+      else
+        memset(&v, 0, sizeof(V));
+      dst[i] = v;
+    }
   }
 }
 
@@ -224,9 +225,7 @@ int unit_rim_snapshot(const void* x, int es, int c, const Geo& g, int halo, cons
                       const int32_t* count, int cap, void* rim, cudaStream_t s) {
   Rim r{g.bh, g.bw, halo};
   const int pix = c * es;
-  const long work = (long)cap * r.pixels() * (pix / 4);
-  long grid = (work + kThreads - 1) / kThreads;
-  if (grid > (long)sm_count() * 8) grid = (long)sm_count() * 8;
+  long grid = cap < (long)sm_count() * 8 ? cap : (long)sm_count() * 8;  // CTAs stride over the blocks
   if (grid < 1) grid = 1;
   const uintptr_t al = (uintptr_t)x | (uintptr_t)rim;
   if (pix % 16 == 0 && al % 16 == 0)
