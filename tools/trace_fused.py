@@ -6,7 +6,7 @@ epilogue 2 saw its accumulator (e2a) and released it (e2); microseconds from the
 stamp; g1s / g3 / e1s / e3: GEMM1 issue start, GEMM3 issue, epilogue 1 start, epilogue 3 done.
 Needs the diagnostics build: tools/build_variant.sh trace -DSBN_TRACE_WIDE, then
 SBN_LIB_PATH=tools/bin/trace.so.
-    python tools/trace_fused.py [stage 2|3] [frames]"""
+    python tools/trace_fused.py [stage 2|3, or 0 for config-2 frames] [frames]"""
 import os
 import sys
 
@@ -18,17 +18,23 @@ import paper_1801_02108_b200 as P  # noqa: E402
 from paper_1801_02108_b200 import _lib, perf  # noqa: E402
 from paper_1801_02108_b200.layers import residual_unit_into  # noqa: E402
 
-stage = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+stage = int(sys.argv[1]) if len(sys.argv) > 1 else 2  # 2..3: config-4 stage; 0: config-2 frames (c=64)
 frames = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 dev = torch.device("cuda", 0)
-cfg = perf.detector_stage_configs()[stage - 2]
-c, m = cfg.channels[2], cfg.channels[1]
-hh, ww = 800 // cfg.mask_scale, 700 // cfg.mask_scale
+if stage == 0:
+    c, m, hh, ww = 64, 32, 400, 400
+    mask = P.synth_mask_blobs((frames, hh, ww), 0.8, 3).cuda()
+    blk = (16, 16)
+else:
+    cfg = perf.detector_stage_configs()[stage - 2]
+    c, m = cfg.channels[2], cfg.channels[1]
+    hh, ww = 800 // cfg.mask_scale, 700 // cfg.mask_scale
+    mk = np.concatenate([P.synth_mask_blobs((1, 800, 700), 0.8, s).numpy() for s in range(frames)])
+    mask = P.downsample_mask(P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False), cfg.mask_scale)
+    blk = cfg.block_size
 x = torch.randn(frames, hh, ww, c, device=dev).bfloat16()
-mk = np.concatenate([P.synth_mask_blobs((1, 800, 700), 0.8, s).numpy() for s in range(frames)])
-mask = P.downsample_mask(P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False), cfg.mask_scale)
 u = P.random_unit_params(np.random.default_rng(0), c, m)
-spec = P.unit_spec(tuple(x.shape), cfg.block_size)
+spec = P.unit_spec(tuple(x.shape), blk)
 idx = P.reduce_mask(mask, spec)
 for _ in range(3):
     residual_unit_into(x, x, u, spec, idx)
