@@ -792,7 +792,10 @@ struct FCfg {
                              60 * C <= 256 * M;
   static constexpr int COL2 = (NB1 > 0 ? NB1 : 1) * M;
   static constexpr int COL3 = COL2 + 4 * M;
-  static constexpr int TCOLS = COL3 + 2 * C;
+  // GEMM3 accumulators: two when TMEM allows (epilogue 3 — the residual loads and the
+  // block's stores — then overlaps the next block's GEMM3; it bounds the period otherwise)
+  static constexpr int NB3 = COL3 + 4 * C <= 512 ? 2 : 1;
+  static constexpr int TCOLS = COL3 + NB3 * 2 * C;
   static constexpr int TALLOC = TCOLS <= 32 ? 32 : TCOLS <= 64 ? 64 : TCOLS <= 128 ? 128 : TCOLS <= 256 ? 256 : 512;
   static constexpr bool BOTH_FIRST = NB1 >= 4;  // GEMM1 of both tiles of k+1 before GEMM2 of k
   static constexpr int OFF_A2 = (SA > 0 ? SA : 1) * TSB;
@@ -851,7 +854,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t a_load[F::SA], a_full[F::SA], a_empty[F::SA], wres;
   __shared__ uint64_t a2_full[2], a2_empty[2], acc1_full[F::NB1], acc1_empty[F::NB1];
-  __shared__ uint64_t acc2_full[2], acc2_empty[2], a3_full, a3_empty, acc3_full, acc3_empty;
+  __shared__ uint64_t acc2_full[2], acc2_empty[2], a3_full, a3_empty, acc3_full[F::NB3], acc3_empty[F::NB3];
   __shared__ uint32_t tslot;
   uint8_t* A1 = smem;
   uint8_t* A2 = smem + F::OFF_A2;
@@ -886,8 +889,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
     }
     tc::mbar_init(&a3_full, 128);
     tc::mbar_init(&a3_empty, 1);
-    tc::mbar_init(&acc3_full, 1);
-    tc::mbar_init(&acc3_empty, 128);
+    for (int b = 0; b < F::NB3; ++b) {
+      tc::mbar_init(&acc3_full[b], 1);
+      tc::mbar_init(&acc3_empty[b], 128);
+    }
     tc::mbar_fence_init();
   }
   if (tid == kLWarp * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tmap) : "memory");
@@ -1007,7 +1012,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
     for (int k = 0; k < nb; ++k) {
       const int j = (int)blockIdx.x + k * G;
       const int n = __ldg(a.idx + 3 * j), by = __ldg(a.idx + 3 * j + 1), bx = __ldg(a.idx + 3 * j + 2);
-      tc::mbar_wait(&acc3_full, k & 1);
+      const int b3i = k % F::NB3;
+      tc::mbar_wait(&acc3_full[b3i], (k / F::NB3) & 1);
       tc::fence_after();
 #pragma unroll 1
       for (int u = 0; u < 2; ++u) {
@@ -1018,7 +1024,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         uint4 xr[C / 8];
 #pragma unroll
         for (int e = 0; e < C / 8; ++e) xr[e] = tc::ld_v4_pred(dp + e, store);
-        const uint32_t acc = tmem + lanes + F::COL3 + u * C;
+        const uint32_t acc = tmem + lanes + F::COL3 + b3i * 2 * C + u * C;
 #pragma unroll
         for (int c0 = 0; c0 < C; c0 += 16) {
           float v[16];
@@ -1039,7 +1045,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         }
       }
       tc::fence_before();
-      tc::mbar_arrive(&acc3_empty);
+      tc::mbar_arrive(&acc3_empty[b3i]);
       if (r == 0) ftrace(a, kFevE3, k);
     }
   } else if (warp < 12) {
@@ -1234,7 +1240,8 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
       };
       auto g3 = [&](int k) {
         constexpr uint32_t idesc = tc::idesc_bf16_f32(128, C);
-        tc::mbar_wait(&acc3_empty, (k & 1) ^ 1);
+        const int b3i = k % F::NB3;
+        tc::mbar_wait(&acc3_empty[b3i], ((k / F::NB3) & 1) ^ 1);
         tc::mbar_wait(&a3_full, k & 1);
         tc::fence_after();
         ftrace(a, kFevG3, k);
@@ -1243,11 +1250,11 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
         for (int u = 0; u < 2; ++u)
 #pragma unroll
           for (int kk = 0; kk < M / 16; ++kk)
-            tc::mma_bf16(tmem + F::COL3 + u * C,
+            tc::mma_bf16(tmem + F::COL3 + b3i * 2 * C + u * C,
                          tc::desc_kmajor_noswz(a3base + 2 * kk * kFPA3 + u * 128 * 16, kFPA3, 128),
                          tc::desc_kmajor_noswz(wbase + 2 * kk * F::PW3, F::PW3, 128), idesc, kk > 0);
         tc::mma_commit(&a3_empty);
-        tc::mma_commit(&acc3_full);
+        tc::mma_commit(&acc3_full[b3i]);
       };
       fused_schedule<F::BOTH_FIRST>(nb, g1, g2, g3);
     }
