@@ -933,32 +933,41 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_fused_kernel(const 
     auto swz = [](int r) { return F::KC1 == 64 ? (r & 7) : ((r >> 1) & 3); };
     const int gt = tid;
     const Rim rim{kFB, kFB, 1};
+    // In place, the window's rim pixels (its neighbours' interiors, which other CTAs overwrite
+    // during this launch) are replaced by the snapshot with one 16-B cp.async per piece into
+    // the landed tile.  Tile tl+1's copies are issued (once it has landed) before tile tl is
+    // transformed, so their L2 round trip overlaps that work instead of preceding it.
+    auto land = [&](int tl2) {
+      tc::mbar_wait(&a_load[tl2 % F::SA], (tl2 / F::SA) & 1);
+      if (!a.rim) return;
+      const int k2 = tl2 >> 1, t2 = tl2 & 1, j2 = (int)blockIdx.x + k2 * G;
+#pragma unroll 1
+      for (int kc = 0; kc < F::NKC1; ++kc) {
+        uint8_t* A = A1 + (tl2 % F::SA) * F::TSB + kc * F::ACH;
+#pragma unroll 4
+        for (int jj = 0; jj < IT; ++jj) {
+          const int i = gt + jj * TG;
+          const int r = i / PR, grp = i % PR;
+          const int wy = 8 * t2 + (r >> 4), wx = r & 15;
+          if (wy == 0 || wy == kFB - 1 || wx == 0 || wx == kFB - 1)
+            tc::cp_async16(A + r * F::ROWB + (grp ^ swz(r)) * 16,
+                           a.rim + ((size_t)j2 * rim.pixels() + rim.index(wy, wx)) * C + kc * F::KC1 + grp * 8, true);
+        }
+      }
+      tc::cp_async_commit();
+    };
     int tl = 0;
+    if (nb > 0) land(0);
     for (int k = 0; k < nb; ++k) {
-      const int j = (int)blockIdx.x + k * G;
       for (int t = 0; t < 2; ++t, ++tl) {
         const int s = tl % F::SA;
-        tc::mbar_wait(&a_load[s], (tl / F::SA) & 1);
-        if (gt == 0 && t == 0) ftrace(a, kFevLanded, k);
-        if (a.rim) {
-          // in place: the rim pixels of the landed window may already hold a neighbour's
-          // output; overwrite them with the snapshot (16-B cp.async per piece, one wait)
-#pragma unroll 1
-          for (int kc = 0; kc < F::NKC1; ++kc) {
-            uint8_t* A = A1 + s * F::TSB + kc * F::ACH;
-#pragma unroll 4
-            for (int jj = 0; jj < IT; ++jj) {
-              const int i = gt + jj * TG;
-              const int r = i / PR, grp = i % PR;
-              const int wy = 8 * t + (r >> 4), wx = r & 15;
-              if (wy == 0 || wy == kFB - 1 || wx == 0 || wx == kFB - 1)
-                tc::cp_async16(A + r * F::ROWB + (grp ^ swz(r)) * 16,
-                               a.rim + ((size_t)j * rim.pixels() + rim.index(wy, wx)) * C + kc * F::KC1 + grp * 8, true);
-            }
-          }
-          tc::cp_async_commit();
+        if (tl + 1 < 2 * nb) {
+          land(tl + 1);
+          tc::cp_async_wait<1>();  // this tile's rim copies (the group before the one just issued)
+        } else {
           tc::cp_async_wait<0>();
         }
+        if (gt == 0 && t == 0) ftrace(a, kFevLanded, k);
 #pragma unroll 1
         for (int kc = 0; kc < F::NKC1; ++kc) {
           uint8_t* A = A1 + s * F::TSB + kc * F::ACH;
