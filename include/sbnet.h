@@ -283,6 +283,33 @@ int sbn_conv_grad_weight(const void* x, const void* g, int dtype, int n, int h, 
                          int ow, int cout, int kh, int kw, int sh, int sw, int ph, int pw, void* dw,
                          void* db, void* ws, size_t ws_bytes, sbn_stream_t stream);
 
+/* Training-path forward pieces (the unit backward's recomputation; F32 / F64):
+ *   sbn_conv_forward: y (n, oh, ow, cout) = direct NHWC convolution of x with W (kh, kw, cin,
+ *     cout) + bias (may be NULL), taps accumulated in order (reference `conv2d_nhwc`,
+ *     `ops.py:145-164`);
+ *   sbn_bn_relu: pre = x * scale + shift (per channel, rounded multiply then add; pre may be
+ *     NULL), post = relu(pre) * valid (valid: one value per pixel = count / c, or NULL)
+ *     (reference `ops.py:213-216`, `:233-234`);
+ *   sbn_bn_relu_grad: out = g * valid * (pre > 0) * scale (the adjoint of sbn_bn_relu);
+ *   sbn_add: out = a + b (elementwise). */
+int sbn_conv_forward(const void* x, int dtype, int n, int h, int w, int cin, int oh, int ow, int cout,
+                     const void* wt, int kh, int kw, int sh, int sw, int ph, int pw, const void* bias, void* y,
+                     sbn_stream_t stream);
+int sbn_bn_relu(const void* x, int dtype, long count, int c, const void* scale, const void* shift, const void* valid,
+                void* pre, void* post, sbn_stream_t stream);
+int sbn_bn_relu_grad(const void* g, const void* pre, int dtype, long count, int c, const void* scale,
+                     const void* valid, void* out, sbn_stream_t stream);
+int sbn_add(const void* a, const void* b, int dtype, long count, void* out, sbn_stream_t stream);
+
+/* Train-mode batch norm over gathered blocks (reference `sparse_batch_norm`, TRAIN_STATS,
+ * `layers.py:68-82`): x is (rows, c); per-channel mean and population variance (deterministic
+ * segmented sums, in the dtype's accumulation type) are written to mean / var (c values of the
+ * accumulation type: float for F32, double for F64) and
+ * out = (x - mean) * (gamma / sqrt(var + eps)) + beta.  F32 / F64. */
+size_t sbn_bn_train_workspace(int dtype, long rows, int c);
+int sbn_bn_train(const void* x, int dtype, long rows, int c, const void* gamma, const void* beta, double eps,
+                 void* out, void* mean, void* var, void* ws, size_t ws_bytes, sbn_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

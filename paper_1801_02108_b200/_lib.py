@@ -89,6 +89,12 @@ _PROTOS = {
     "sbn_conv_grad_weight_workspace": (C.c_size_t, [_I] * 8),
     "sbn_conv_grad_weight": (_I, [_P, _P, _I] + [_I] * 13 + [_P, _P, _P, C.c_size_t, _P]),
     "sbn_residual_unit_pack": (_I, [C.POINTER(UnitParams), _I, _I, _I, _G, _I, _I, _P, _P]),
+    "sbn_conv_forward": (_I, [_P, _I] + [_I] * 7 + [_P] + [_I] * 6 + [_P, _P, _P]),
+    "sbn_bn_relu": (_I, [_P, _I, C.c_long, _I, _P, _P, _P, _P, _P, _P]),
+    "sbn_bn_relu_grad": (_I, [_P, _P, _I, C.c_long, _I, _P, _P, _P, _P]),
+    "sbn_add": (_I, [_P, _P, _I, C.c_long, _P, _P]),
+    "sbn_bn_train_workspace": (C.c_size_t, [_I, C.c_long, _I]),
+    "sbn_bn_train": (_I, [_P, _I, C.c_long, _I, _P, _P, C.c_double, _P, _P, _P, _P, C.c_size_t, _P]),
 }
 
 _lib = None

@@ -20,8 +20,8 @@ import torch.nn.functional as F
 from . import _lib
 from .blocks import GatheredBlocks, gather, gather_grad, in_bounds_map, scatter_grad
 from .errors import EmptyBlockListError, GeometryError, ShapeMismatchError, UnsupportedConfigError
-from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, bn_inference,
-                  conv_grads_nhwc, dense_conv_nhwc, exact_fp32, projection_conv)
+from .ops import (BnMode, BnParams, ConvParams, FilterBank, Padding, PoolMode, add_nhwc, bn_inference, bn_relu_grad_nhwc,
+                  bn_relu_nhwc, conv_forward_nhwc, conv_grads_nhwc, dense_conv_nhwc, exact_fp32, projection_conv)
 from .tensor import Layout, Tensor4D, cuda, dtype_code
 from .tiling import (BinaryMask, BlockIndexList, BlockSpec, compute_block_spec, downsample_mask,
                      reduce_mask)
@@ -262,7 +262,9 @@ def sparse_residual_unit_grads(x: Tensor4D, mask: BinaryMask, u: "ResidualUnitPa
     """Input and conv-weight gradients of the pre-activation, inference-BN sparse unit
     (reference `layers.py:232-270`).  The branch is recomputed on the gathered stack with
     its intermediates, differentiated back through 1x1 / ReLU / BN scale / crop / 3x3 /
-    in-bounds map / 1x1 / ReLU / BN1 scale, and gather_grad'ed onto g_out.
+    in-bounds map / 1x1 / ReLU / BN1 scale, and gather_grad'ed onto g_out — every step on
+    the native kernels (direct convs `sbn_conv_forward`, `sbn_bn_relu` / `sbn_bn_relu_grad`,
+    `sbn_conv_grad_*`, `sbn_gather_grad`, `sbn_add`).
     Returns (dx, {"conv1": (dw, db), "conv2": ..., "conv3": ...}) on the device."""
     if not u.pre_activation:
         raise UnsupportedConfigError("gradients implemented for the pre-activation chain only")
@@ -291,30 +293,27 @@ def sparse_residual_unit_grads(x: Tensor4D, mask: BinaryMask, u: "ResidualUnitPa
     s3, t3 = u.bn3.folded(dt, dev)
 
     def conv(t, nm, pad=(0, 0)):
-        return dense_conv_nhwc(t, ws[nm][0], ws[nm][1], (1, 1), pad)
+        return conv_forward_nhwc(t, ws[nm][0], ws[nm][1], (1, 1), pad)
 
-    with exact_fp32():
-        b1 = a * s1 + t1
-        r1 = torch.relu(b1)
-        b2 = conv(r1, "conv1") * s2 + t2
-        r2 = torch.relu(b2) * valid
-        c2 = conv(r2, "conv2", conv2_pad)
-        c2c = c2[:, crop:c2.shape[1] - crop, crop:c2.shape[2] - crop] if crop else c2
-        b3 = c2c * s3 + t3
-        r3 = torch.relu(b3)
-        gb = cuda(scatter_grad(g_out, idx, spec).tensor.data)
-        d_r3, dw3, db3 = conv_grads_nhwc(r3, ws["conv3"][0], (1, 1), (0, 0), gb)
-        d_c2c = d_r3 * (b3 > 0).to(dt) * s3
-        if crop:
-            d_c2 = torch.zeros(c2.shape, dtype=dt, device=dev)
-            d_c2[:, crop:-crop, crop:-crop] = d_c2c
-            d_c2c = d_c2
-        d_r2, dw2, db2 = conv_grads_nhwc(r2, ws["conv2"][0], (1, 1), conv2_pad, d_c2c)
-        d_c1 = d_r2 * valid * (b2 > 0).to(dt) * s2
-        d_r1, dw1, db1 = conv_grads_nhwc(r1, ws["conv1"][0], (1, 1), (0, 0), d_c1)
-        d_a0 = d_r1 * (b1 > 0).to(dt) * s1
+    # every step native: direct convs, BN + ReLU (+ in-bounds map) and their adjoints
+    b1, r1 = bn_relu_nhwc(a, s1, t1)
+    b2, r2 = bn_relu_nhwc(conv(r1, "conv1"), s2, t2, valid)
+    c2 = conv(r2, "conv2", conv2_pad)
+    c2c = c2[:, crop:c2.shape[1] - crop, crop:c2.shape[2] - crop].contiguous() if crop else c2
+    b3, r3 = bn_relu_nhwc(c2c, s3, t3)
+    gb = cuda(scatter_grad(g_out, idx, spec).tensor.data)
+    d_r3, dw3, db3 = conv_grads_nhwc(r3, ws["conv3"][0], (1, 1), (0, 0), gb)
+    d_c2c = bn_relu_grad_nhwc(d_r3, b3, s3)
+    if crop:
+        d_c2 = torch.zeros(c2.shape, dtype=dt, device=dev)
+        d_c2[:, crop:-crop, crop:-crop] = d_c2c
+        d_c2c = d_c2
+    d_r2, dw2, db2 = conv_grads_nhwc(r2, ws["conv2"][0], (1, 1), conv2_pad, d_c2c)
+    d_c1 = bn_relu_grad_nhwc(d_r2, b2, s2, valid)
+    d_r1, dw1, db1 = conv_grads_nhwc(r1, ws["conv1"][0], (1, 1), (0, 0), d_c1)
+    d_a0 = bn_relu_grad_nhwc(d_r1, b1, s1)
     d_branch = gather_grad(GatheredBlocks(Tensor4D(d_a0.contiguous()), spec, idx), spec, x.dims)
-    dx = cuda(g_out.nhwc()) + d_branch.data
+    dx = add_nhwc(cuda(g_out.nhwc()), d_branch.data)
     return Tensor4D.from_nhwc(dx, x.layout), {"conv1": (dw1, db1), "conv2": (dw2, db2), "conv3": (dw3, db3)}
 
 
@@ -327,11 +326,23 @@ def sparse_batch_norm(blocks: GatheredBlocks, bn: BnParams, mode: BnMode = BnMod
         return blocks.with_tensor(Tensor4D.from_nhwc(bn_inference(t, bn), blocks.tensor.layout))
     if blocks.count == 0:
         raise EmptyBlockListError("train-mode statistics are undefined for an empty block list")
-    mean = t.mean(dim=(0, 1, 2))
-    var = t.var(dim=(0, 1, 2), unbiased=False)
+    if t.dtype not in (torch.float32, torch.float64):
+        raise UnsupportedConfigError("train-mode batch norm is float32 / float64 (as the reference)")
+    # native: deterministic per-channel mean / population variance + normalisation (sbn_bn_train)
+    lib = _lib.load()
+    t = t.contiguous()
+    c = t.shape[3]
+    rows = t.numel() // c
     g = torch.as_tensor(np.asarray(bn.gamma), device=t.device, dtype=t.dtype)
     be = torch.as_tensor(np.asarray(bn.beta), device=t.device, dtype=t.dtype)
-    out = (t - mean) * (g / torch.sqrt(var + bn.epsilon)) + be
+    out = torch.empty_like(t)
+    mean = torch.empty(c, dtype=t.dtype, device=t.device)
+    var = torch.empty(c, dtype=t.dtype, device=t.device)
+    dt = dtype_code(t.dtype)
+    ws = torch.empty(int(lib.sbn_bn_train_workspace(dt, rows, c)), dtype=torch.uint8, device=t.device)
+    _lib.check(lib.sbn_bn_train(t.data_ptr(), dt, rows, c, g.data_ptr(), be.data_ptr(), float(bn.epsilon),
+                                out.data_ptr(), mean.data_ptr(), var.data_ptr(), ws.data_ptr(), ws.numel(),
+                                _lib.stream_handle(t.device)), "bn_train")
     return blocks.with_tensor(Tensor4D.from_nhwc(out, blocks.tensor.layout)), (mean, var)
 
 

@@ -252,6 +252,68 @@ def relu(x: Tensor4D) -> Tensor4D:
 # The reference's dense helpers outside the sparse path (`ops.py:167-269`, `winograd.py`),
 # on cuDNN so a caller switching packages finds them; exact fp32 (no TF32).
 
+def conv_forward_nhwc(x: torch.Tensor, w_hwio: torch.Tensor, bias, stride, pad) -> torch.Tensor:
+    """Direct NHWC convolution + bias of a float32 / float64 CUDA tensor on the native kernel
+    (`sbn_conv_forward`; reference `ops.py:145-164`, taps accumulated in order) — the
+    training path's recomputation."""
+    from . import _lib
+    from .tensor import dtype_code
+    lib = _lib.load()
+    x = x.contiguous()
+    w = w_hwio.to(x.dtype).contiguous()
+    n, h, wd, cin = x.shape
+    kh, kw, _, cout = w.shape
+    (sh, sw), (ph, pw) = tuple(stride), tuple(pad)
+    oh, ow = (h + 2 * ph - kh) // sh + 1, (wd + 2 * pw - kw) // sw + 1
+    y = torch.empty((n, oh, ow, cout), dtype=x.dtype, device=x.device)
+    b = None if bias is None else bias.to(x.dtype).contiguous()
+    _lib.check(lib.sbn_conv_forward(x.data_ptr(), dtype_code(x.dtype), n, h, wd, cin, oh, ow, cout, w.data_ptr(), kh,
+                                    kw, sh, sw, ph, pw, None if b is None else b.data_ptr(), y.data_ptr(),
+                                    _lib.stream_handle(x.device)), "conv_forward")
+    return y
+
+
+def bn_relu_nhwc(x: torch.Tensor, scale: torch.Tensor, shift: torch.Tensor, valid=None):
+    """(pre, post) = (x * scale + shift, relu(pre) * valid) per channel on the native kernel
+    (`sbn_bn_relu`; reference `ops.py:213-216`, `:233-234`); valid: one 0/1 value per pixel."""
+    from . import _lib
+    from .tensor import dtype_code
+    lib = _lib.load()
+    x = x.contiguous()
+    pre, post = torch.empty_like(x), torch.empty_like(x)
+    v = None if valid is None else valid.to(x.dtype).contiguous()
+    _lib.check(lib.sbn_bn_relu(x.data_ptr(), dtype_code(x.dtype), x.numel(), x.shape[-1], scale.data_ptr(),
+                               shift.data_ptr(), None if v is None else v.data_ptr(), pre.data_ptr(), post.data_ptr(),
+                               _lib.stream_handle(x.device)), "bn_relu")
+    return pre, post
+
+
+def bn_relu_grad_nhwc(g: torch.Tensor, pre: torch.Tensor, scale: torch.Tensor, valid=None) -> torch.Tensor:
+    """Adjoint of bn_relu_nhwc: g * valid * (pre > 0) * scale (`sbn_bn_relu_grad`)."""
+    from . import _lib
+    from .tensor import dtype_code
+    lib = _lib.load()
+    g, pre = g.contiguous(), pre.contiguous()
+    out = torch.empty_like(g)
+    v = None if valid is None else valid.to(g.dtype).contiguous()
+    _lib.check(lib.sbn_bn_relu_grad(g.data_ptr(), pre.data_ptr(), dtype_code(g.dtype), g.numel(), g.shape[-1],
+                                    scale.data_ptr(), None if v is None else v.data_ptr(), out.data_ptr(),
+                                    _lib.stream_handle(g.device)), "bn_relu_grad")
+    return out
+
+
+def add_nhwc(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """a + b on the native kernel (`sbn_add`)."""
+    from . import _lib
+    from .tensor import dtype_code
+    lib = _lib.load()
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty_like(a)
+    _lib.check(lib.sbn_add(a.data_ptr(), b.data_ptr(), dtype_code(a.dtype), a.numel(), out.data_ptr(),
+                           _lib.stream_handle(a.device)), "add")
+    return out
+
+
 def conv_grads_nhwc(a: torch.Tensor, w_hwio: torch.Tensor, stride, pad, g: torch.Tensor):
     """(dx, dw, db) of a conv on an NHWC CUDA tensor for upstream gradient g (reference
     `ops.py:167-197`): the native gradient kernels (csrc/conv_grad.cu), deterministic."""

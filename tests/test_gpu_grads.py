@@ -169,3 +169,57 @@ def test_native_conv_grads_vs_autograd_and_deterministic(cuda_device, dt, tol):
         assert rel(db, br.grad) <= tol
         dx2, dw2, db2 = conv_grads_nhwc(x, wt, (s, s), (p, p), go)
         assert torch.equal(dx, dx2) and torch.equal(dw, dw2) and torch.equal(db, db2)
+
+
+@pytest.mark.parametrize("dt,tol", [(torch.float64, 1e-12), (torch.float32, 1e-5)])
+def test_native_conv_forward_and_bn_relu(cuda_device, dt, tol):
+    """The unit backward's recomputation kernels: sbn_conv_forward against F.conv2d (same
+    math, tap order differs), sbn_bn_relu / sbn_bn_relu_grad / sbn_add against the eager torch
+    expressions they replace — bit-exact (a rounded multiply, then a rounded add)."""
+    import torch.nn.functional as F
+
+    from paper_1801_02108_b200.ops import add_nhwc, bn_relu_grad_nhwc, bn_relu_nhwc, conv_forward_nhwc
+    g_ = torch.Generator(device="cuda").manual_seed(1)
+    for (n, h, w, c, co, k, s, p) in ((5, 16, 16, 32, 16, 1, 1, 0), (3, 16, 16, 16, 16, 3, 1, 0),
+                                      (2, 33, 29, 8, 20, 5, 2, 2)):
+        x = torch.randn(n, h, w, c, device="cuda", dtype=dt, generator=g_)
+        wt = torch.randn(k, k, c, co, device="cuda", dtype=dt, generator=g_)
+        b = torch.randn(co, device="cuda", dtype=dt, generator=g_)
+        y = conv_forward_nhwc(x, wt, b, (s, s), (p, p))
+        torch.backends.cudnn.allow_tf32 = False
+        ref = F.conv2d(x.permute(0, 3, 1, 2), wt.permute(3, 2, 0, 1), b, stride=s, padding=p).permute(0, 2, 3, 1)
+        assert float((y - ref).abs().max() / ref.abs().max()) <= tol
+    x = torch.randn(4, 16, 16, 24, device="cuda", dtype=dt, generator=g_)
+    sc = torch.randn(24, device="cuda", dtype=dt, generator=g_)
+    sh = torch.randn(24, device="cuda", dtype=dt, generator=g_)
+    valid = (torch.rand(4, 16, 16, 1, device="cuda", generator=g_) > 0.3).to(dt)
+    pre, post = bn_relu_nhwc(x, sc, sh, valid)
+    assert torch.equal(pre, x * sc + sh) and torch.equal(post, torch.relu(x * sc + sh) * valid)
+    g = torch.randn_like(x)
+    assert torch.equal(bn_relu_grad_nhwc(g, pre, sc, valid), g * valid * (pre > 0).to(dt) * sc)
+    assert torch.equal(bn_relu_grad_nhwc(g, pre, sc), g * (pre > 0).to(dt) * sc)
+    assert torch.equal(add_nhwc(x, g), x + g)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_native_train_stats_bn_vs_torch_and_deterministic(cuda_device, dt):
+    """sbn_bn_train (TRAIN_STATS sparse_batch_norm) against the torch expression, at a size
+    that splits the statistics into several row segments; repeated calls bit-identical."""
+    rng = np.random.default_rng(3)
+    t = torch.from_numpy(rng.standard_normal((40, 16, 16, 24)) * 3 + 1).to(dt).cuda()
+    idx = P.BlockIndexList(np.zeros((40, 3), np.int32))
+    bn = P.BnParams(rng.standard_normal(24), rng.standard_normal(24), np.zeros(24), np.ones(24))
+    from paper_1801_02108_b200.blocks import GatheredBlocks
+    spec = P.compute_block_spec((1, 64, 64, 24), P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 24), (16, 16))
+    blocks = GatheredBlocks(P.Tensor4D(t), spec, idx)
+    out, (mean, var) = P.sparse_batch_norm(blocks, bn, P.BnMode.TRAIN_STATS)
+    m_ref = t.mean(dim=(0, 1, 2))
+    v_ref = t.var(dim=(0, 1, 2), unbiased=False)
+    g = torch.as_tensor(np.asarray(bn.gamma), device=t.device, dtype=dt)
+    be = torch.as_tensor(np.asarray(bn.beta), device=t.device, dtype=dt)
+    ref = (t - m_ref) * (g / torch.sqrt(v_ref + bn.epsilon)) + be
+    tol = 1e-12 if dt == torch.float64 else 1e-5
+    rel = lambda a, b: float((a - b).abs().max() / b.abs().max())  # noqa: E731
+    assert rel(mean, m_ref) <= tol and rel(var, v_ref) <= tol and rel(out.tensor.data, ref) <= tol
+    out2, (mean2, var2) = P.sparse_batch_norm(blocks, bn, P.BnMode.TRAIN_STATS)
+    assert torch.equal(out.tensor.data, out2.tensor.data) and torch.equal(mean, mean2) and torch.equal(var, var2)
