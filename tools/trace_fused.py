@@ -28,7 +28,7 @@ if stage == 0:
 else:
     cfg = perf.detector_stage_configs()[stage - 2]
     c, m = cfg.channels[2], cfg.channels[1]
-    hh, ww = 800 // cfg.mask_scale, 700 // cfg.mask_scale
+    hh, ww = -(-800 // cfg.mask_scale), -(-700 // cfg.mask_scale)  # downsample_mask rounds up
     mk = np.concatenate([P.synth_mask_blobs((1, 800, 700), 0.8, s).numpy() for s in range(frames)])
     mask = P.downsample_mask(P.BinaryMask(torch.from_numpy(mk).to(dev), validate=False), cfg.mask_scale)
     blk = cfg.block_size

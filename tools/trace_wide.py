@@ -23,7 +23,7 @@ which = sys.argv[2] if len(sys.argv) > 2 else "in"
 dev = torch.device("cuda", 0)
 cfg = perf.detector_stage_configs()[stage - 2]
 c, m = cfg.channels[2], cfg.channels[1]
-hh, ww = 800 // cfg.mask_scale, 700 // cfg.mask_scale
+hh, ww = -(-800 // cfg.mask_scale), -(-700 // cfg.mask_scale)  # downsample_mask rounds up
 frames = 8
 x = torch.randn(frames, hh, ww, c, device=dev).bfloat16()
 mk = np.concatenate([P.synth_mask_blobs((1, 800, 700), 0.8, s).numpy() for s in range(frames)])
