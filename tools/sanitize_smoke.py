@@ -1,7 +1,8 @@
 """One small invocation of every hot kernel, for compute-sanitizer (memcheck / racecheck /
 synccheck): reduce_mask (ordered + cluster), gather / scatter / scatter_add / transpose,
 sparse conv (SIMT fp32, tcgen05 single-CTA, CTA-pair, strided TMA), residual unit (SIMT,
-fused mask + CTA pair in place, wide), dense conv, host-frame unit copies."""
+fused mask + CTA pair in place, wide: one launch and three launches), dense conv (single and
+CTA pair), host-frame unit copies, the training-path kernels."""
 import os
 import sys
 
@@ -89,5 +90,26 @@ P.sparse_conv2d(P.Tensor4D(xt3), P.synth_mask_topleft((1, 180, 200), 0.0).cuda()
 bb = P.build_backbone([P.StageConfig(1, (8, 12, 24), (16, 16), 1, 1), P.StageConfig(1, (24, 24, 48), (12, 12), 2, 2)],
                       np.random.default_rng(1))
 P.run_backbone(bb, P.Tensor4D(torch.randn(1, 60, 52, 8, device=dev)), P.synth_mask_blobs((1, 60, 52), 0.7, 2).cuda())
+# round 2, second half: the one-launch wide unit (functional and in place with the rim
+# snapshot; c = 64 and the config-4 stage-0 shape c = 96), the three-launch path it
+# replaces, the CTA-pair projection, and the native training-path kernels
+for c_, m_ in ((64, 32), (96, 48)):
+    xw = torch.randn(2, 72, 60, c_, device=dev).bfloat16()
+    uw = P.random_unit_params(rng, c_, m_)
+    for flags in (4, 4 | 256):
+        old = lib.sbn_debug_set_flags(flags)
+        P.sparse_residual_unit(P.Tensor4D(xw), mk, uw, (16, 16))
+        P.sparse_residual_unit(P.Tensor4D(xw.clone()), mk, uw, (16, 16), inplace=True)
+        lib.sbn_debug_set_flags(old)
+xq = torch.randn(2, 22, 19, 192, device=dev).bfloat16()
+fq = P.FilterBank((torch.randn(3, 3, 192, 256) / 41).bfloat16(), torch.randn(256).bfloat16())
+projection_conv(xq, fq, P.ConvParams((3, 3), (2, 2), P.Padding.SAME, 256))
+xf = P.Tensor4D(torch.randn(1, 40, 36, 16, device=dev))
+uf = P.random_unit_params(rng, 16, 8)
+mf = P.synth_mask_blobs((1, 40, 36), 0.5, 4)
+P.sparse_residual_unit_grads(xf, mf, uf, (10, 10), P.Tensor4D(torch.randn(1, 40, 36, 16, device=dev)))
+specb = P.compute_block_spec((1, 40, 36, 16), P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 16), (10, 10))
+gb_ = P.gather(xf, P.reduce_mask(mf, specb), specb)
+P.sparse_batch_norm(gb_, P.BnParams.identity(16), P.BnMode.TRAIN_STATS)
 torch.cuda.synchronize()
 print("sanitize smoke done", flush=True)
