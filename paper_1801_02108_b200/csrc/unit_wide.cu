@@ -138,6 +138,18 @@ struct WCfg {
   static constexpr int OFF_RES = OFF_STG + STGB;
   static constexpr int SMEM = OFF_RES + NRB * RESB;
   static constexpr int ITEMS = (128 * P + kAThreads / 2 - 1) / (kAThreads / 2);  // IN pieces per thread
+  // column slices (OUT): when a launch has too few tiles to fill the grid, each tile is done
+  // as two work items of N/2 output columns on different CTAs (same A, half the weights).
+  // The k-step order of every accumulator column is unchanged, so results are identical.
+  // (Measured on the config-4 stage-3 unit: OUT 13.4 -> 11.4 us; IN and MID got slower —
+  // the duplicated A / BN work and MID's streamed weights in plane pieces cost more than the
+  // shorter makespan saves — so only OUT slices.)
+  static constexpr bool SPL = MODE == kOut && !PF && N >= 128 && (N / 2) % 16 == 0;
+  static constexpr int N2 = N / 2;
+  static constexpr int NSPLIT2 = N2 > 256 ? 2 : 1;
+  static constexpr int NS2 = SPL ? N2 / NSPLIT2 : NS;
+  static constexpr int GSH = MODE != kOut || !SPL ? (GS > 0 ? GS : 16) : N2 <= GS ? N2 : N2 % GS == 0 ? GS : N2 / 2;
+  static_assert(!SPL || MODE != kOut || (N2 % GSH == 0 && GSH % 16 == 0 && GSH <= GS), "slice staging groups");
 };
 
 // Stacks S1 / S2 are stored PLANE-MAJOR: plane k (channels 8k..8k+7) of row r at
@@ -167,6 +179,7 @@ struct __align__(64) WArgs {
   long src_rows;             // MID / OUT: rows_alloc of the source stack (plane stride / 16)
   long dst_rows;             // IN / MID: rows_alloc of the destination stack
   unsigned long long* trace; // diagnostics: CTA 0 event stamps (sbn_debug_set_trace)
+  int split;                 // column slices allowed (WCfg::SPL launches with few tiles)
 };
 
 // CTA 0 event log (diagnostics): slot ev*64 + tile, tiles < 64
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int SWB = Q::SW > 0 ? Q::SW : 1;
   __shared__ uint64_t a_load[Q::SA], a_full[Q::SA], a_empty[Q::SA], w_full[SWB], w_empty[SWB];
-  __shared__ uint64_t acc_full[Q::NACC], acc_empty[Q::NACC];
+  __shared__ uint64_t acc_full[2], acc_empty[2];
   __shared__ uint32_t tslot;
   __shared__ long long rowdst[MODE == kOut ? 128 : 1];  // OUT: element offset of a row's pixel, -1 skip
   constexpr int NRBS = Q::NRB > 0 ? Q::NRB : 1;
@@ -268,7 +281,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       tc::mbar_init(&res_full[s], 2 * kAThreads);  // a st.shared release + a cp.async completion per A thread
       tc::mbar_init(&res_empty[s], kEThreads);
     }
-    for (int s = 0; s < Q::NACC; ++s) {
+    for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&acc_full[s], 1);
       tc::mbar_init(&acc_empty[s], kEThreads);
     }
@@ -292,6 +305,17 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
   tc::pdl_wait();  // the previous launch's S1 / S2 / x and the index list are visible
   const int B = ld_count(a.count, a.cap);
   const int ntiles = tile_count<MODE>(a, B, b);
+  // column slices (WCfg::SPL): ns = 2 work items per tile when that shortens the makespan
+  // (a half-width item costs ~0.6 of a tile: same A operand, half the MMA columns)
+  int ns = 1;
+  if constexpr (Q::SPL) {
+    const int G = gridDim.x, r1 = (ntiles + G - 1) / G, r2 = (2 * ntiles + G - 1) / G;
+    if (a.split && 3 * r2 < 5 * r1) ns = 2;
+  }
+  const int lg = ns - 1;                     // tile = w >> lg, slice = w & lg
+  const int nwork = ntiles << lg;
+  const int W = N >> lg;                     // output columns per work item
+  const int nacc = lg ? (2 * W <= Q::TALLOC ? 2 : 1) : Q::NACC;
 
   if (tid < kAThreads) {
     // ------------------------------------------------ IN: BN1 + ReLU on landed chunks
@@ -305,7 +329,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       constexpr int TG = kAThreads / 2;
       const int grp_id = tid / TG, gt = tid % TG;
       int c = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x)
         for (int kc = 0; kc < Q::NKC; ++kc, ++c) {
           if ((c & 1) != grp_id) continue;
           const int s = c % Q::SA;
@@ -392,8 +416,15 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
       constexpr int GS = Q::GS, CHR = GS * 2 / 16;
       constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
       const uint8_t* stg = smem + Q::OFF_STG;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int g0 = 0; g0 < N; g0 += GS) out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        if (Q::SPL && lg) {
+          constexpr int CHRH = Q::GSH * 2 / 16, IT2H = (128 * CHRH + kOutCopy - 1) / kOutCopy;
+          for (int g0 = 0; g0 < Q::N2; g0 += Q::GSH)
+            out_copy_phase<Q::SPITCH, CHRH, IT2H>(a.dst + (w & 1) * Q::N2, stg, rowdst, g0, tid);
+        } else {
+          for (int g0 = 0; g0 < N; g0 += GS) out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
+        }
+      }
     }
   } else if (tid < kAThreads + kEThreads) {
     // ------------------------------------------------ epilogue
@@ -407,7 +438,6 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
     const long TR = MODE == kOut ? (long)B * ob * ob : (long)B * bb;
     constexpr int NCH = N / 16;                 // 16-column chunks
     constexpr int MYCH = (NCH + 1) / 2;         // chunks of this half (upper bound)
-    constexpr int PG = 0;  // (OUT reads its residual in the staged copy phase)
     const float* sc = MODE == kIn ? par + 2 * K + N : par + N;  // IN: s2 | MID: s3
     const float* sh = sc + N;                                     // t2' | t3'
     // per-row metadata of a tile; the block-index loads (IN, OUT) are issued one tile
@@ -431,7 +461,6 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
     bool store = false, valid = true;
     __nv_bfloat16* dp = a.dst;   // OUT: the output pixel row
     long drow = 0;               // IN / MID: destination row of the plane-major stack
-    uint4 res[PG > 0 ? 2 * PG : 1];
     auto meta = [&](int tile) {
       const long gr = (long)tile * 128 + r;
       store = (MODE == kIn || gr < TR) && tile < ntiles;
@@ -459,24 +488,18 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
         const int Y = xby * g.obh + oy, X = xbx * g.obw + ox;
         store = Y < g.oh && X < g.ow;
         dp = a.dst + (((long)xn * g.oh + Y) * g.ow + X) * N;  // residual read from the same row
-#pragma unroll
-        for (int e = 0; e < PG; ++e) {
-          const int c0 = 16 * (2 * e + half);
-          if (store && c0 < N) {
-            res[2 * e] = reinterpret_cast<const uint4*>(dp + c0)[0];
-            res[2 * e + 1] = reinterpret_cast<const uint4*>(dp + c0)[1];
-          }
-        }
       }
     };
-    idx_next(blockIdx.x);
-    meta(blockIdx.x);
+    idx_next(blockIdx.x >> lg);
+    meta(blockIdx.x >> lg);
     int k = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-      const int buf = Q::NACC == 2 ? (k & 1) : 0;
-      const int use = Q::NACC == 2 ? (k >> 1) : k;
-      idx_next(tile + gridDim.x);
-      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * N;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++k) {
+      const int buf = nacc == 2 ? (k & 1) : 0;
+      const int use = nacc == 2 ? (k >> 1) : k;
+      const int nxt = (w + (int)gridDim.x) >> lg;  // the next work item's tile
+      const int choff = (w & lg) * W;              // first output column of this item
+      idx_next(nxt);
+      const uint32_t acc = tmem + ((uint32_t)(qd * 32) << 16) + buf * W;
       tc::mbar_wait(&acc_full[buf], use & 1);
       tc::fence_after();
       if (ew == 0 && lane == 0) wtrace(a, kEvAcc, k);
@@ -484,13 +507,14 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
         // staged OUT epilogue: phase 1 writes bf16(acc + b3) of GS columns of this row to
         // smem; phase 2 walks (row, 16-B chunk) items so consecutive lanes cover one pixel
         // row: residual loads and stores are coalesced 16-B vectors
-        constexpr int GS = Q::GS, CHR = GS * 2 / 16;
-        constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
-        static_assert(N % GS == 0, "staging groups");
+        static_assert(N % Q::GS == 0, "staging groups");
         uint8_t* stg = smem + Q::OFF_STG;
-        const float* b3 = par;
+        const float* b3 = par + choff;
         if (half == 0) rowdst[r] = store ? (long long)(dp - a.dst) : -1;
-        for (int g0 = 0; g0 < N; g0 += GS) {
+        auto drain = [&](auto gs_c) {
+        constexpr int GS = decltype(gs_c)::value, CHR = GS * 2 / 16;
+        constexpr int IT2 = (128 * CHR + kOutCopy - 1) / kOutCopy;
+        for (int g0 = 0; g0 < W; g0 += GS) {
 #pragma unroll
           for (int e = 0; e < (GS / 16 + 1) / 2; ++e) {
             const int cg = 16 * (2 * e + half);  // column inside the group
@@ -508,7 +532,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             sp[0] = make_uint4(o[0], o[1], o[2], o[3]);
             sp[1] = make_uint4(o[4], o[5], o[6], o[7]);
           }
-          if (g0 + GS >= N) {  // TMEM fully drained: release the accumulator early
+          if (g0 + GS >= W) {  // TMEM fully drained: release the accumulator early
             tc::fence_before();
             tc::mbar_arrive(&acc_empty[buf]);
           }
@@ -537,66 +561,47 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             tc::mbar_arrive(&res_empty[rb]);
             tc::named_bar<5, kEThreads>();  // staging buffer reuse
           } else {
-            out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst, stg, rowdst, g0, tid);
+            out_copy_phase<Q::SPITCH, CHR, IT2>(a.dst + choff, stg, rowdst, g0, tid);
           }
         }
+        };
+        if (Q::SPL && lg)
+          drain(std::integral_constant<int, Q::GSH>());
+        else
+          drain(std::integral_constant<int, Q::GS>());
         if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
-        meta(tile + gridDim.x);
+        meta(nxt);
         continue;
       }
 #pragma unroll
       for (int e = 0; e < MYCH; ++e) {
         const int c0 = 16 * (2 * e + half);
-        if (c0 >= N) break;  // warp-uniform
+        if (c0 >= W) break;  // warp-uniform
         float v[16];
         tc::tmem_ld16(acc + c0, v);
         if (!store) continue;
+        const int cc = choff + c0;  // output channel
         uint32_t o[8];
-        if (MODE == kOut) {
-          const float* b3 = par;
-          uint4 xr[2];
-          if (e < PG) {
-            xr[0] = res[2 * (e < PG ? e : 0)];
-            xr[1] = res[2 * (e < PG ? e : 0) + 1];
-          } else {
-            xr[0] = reinterpret_cast<const uint4*>(dp + c0)[0];
-            xr[1] = reinterpret_cast<const uint4*>(dp + c0)[1];
-          }
-          const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(xr);
 #pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            const float4 b4 = *reinterpret_cast<const float4*>(b3 + c0 + 2 * q);
-            const float2 x0 = __bfloat1622float2(xh[q]), x1 = __bfloat1622float2(xh[q + 1]);
-            o[q] = tc::pack_bf16(x0.x + (v[2 * q] + b4.x), x0.y + (v[2 * q + 1] + b4.y));
-            o[q + 1] = tc::pack_bf16(x1.x + (v[2 * q + 2] + b4.z), x1.y + (v[2 * q + 3] + b4.w));
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            const float4 s4 = *reinterpret_cast<const float4*>(sc + c0 + 2 * q);
-            const float4 t4 = *reinterpret_cast<const float4*>(sh + c0 + 2 * q);
-            const float u0 = fmaxf(fmaf(v[2 * q], s4.x, t4.x), 0.f);
-            const float u1 = fmaxf(fmaf(v[2 * q + 1], s4.y, t4.y), 0.f);
-            const float u2 = fmaxf(fmaf(v[2 * q + 2], s4.z, t4.z), 0.f);
-            const float u3 = fmaxf(fmaf(v[2 * q + 3], s4.w, t4.w), 0.f);
-            o[q] = valid ? tc::pack_bf16(u0, u1) : 0u;
-            o[q + 1] = valid ? tc::pack_bf16(u2, u3) : 0u;
-          }
+        for (int q = 0; q < 8; q += 2) {
+          const float4 s4 = *reinterpret_cast<const float4*>(sc + cc + 2 * q);
+          const float4 t4 = *reinterpret_cast<const float4*>(sh + cc + 2 * q);
+          const float u0 = fmaxf(fmaf(v[2 * q], s4.x, t4.x), 0.f);
+          const float u1 = fmaxf(fmaf(v[2 * q + 1], s4.y, t4.y), 0.f);
+          const float u2 = fmaxf(fmaf(v[2 * q + 2], s4.z, t4.z), 0.f);
+          const float u3 = fmaxf(fmaf(v[2 * q + 3], s4.w, t4.w), 0.f);
+          o[q] = valid ? tc::pack_bf16(u0, u1) : 0u;
+          o[q + 1] = valid ? tc::pack_bf16(u2, u3) : 0u;
         }
-        if (MODE == kOut) {
-          uint4* op = reinterpret_cast<uint4*>(dp + c0);
-          op[0] = make_uint4(o[0], o[1], o[2], o[3]);
-          op[1] = make_uint4(o[4], o[5], o[6], o[7]);
-        } else {  // plane-major stack: lanes hold consecutive rows -> coalesced 16-B stores
-          uint4* pl = reinterpret_cast<uint4*>(a.dst) + (long)(c0 / 8) * a.dst_rows + drow;
-          pl[0] = make_uint4(o[0], o[1], o[2], o[3]);
-          pl[a.dst_rows] = make_uint4(o[4], o[5], o[6], o[7]);
-        }
+        // plane-major stack: lanes hold consecutive rows -> coalesced 16-B stores
+        uint4* pl = reinterpret_cast<uint4*>(a.dst) + (long)(cc / 8) * a.dst_rows + drow;
+        pl[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        pl[a.dst_rows] = make_uint4(o[4], o[5], o[6], o[7]);
       }
       tc::fence_before();
       tc::mbar_arrive(&acc_empty[buf]);
       if (ew == 0 && lane == 0) wtrace(a, kEvEpi, k);
-      meta(tile + gridDim.x);
+      meta(nxt);
     }
   } else if (warp == kLWarp) {
     // ------------------------------------------------ loader: A boxes (+ streamed weights)
@@ -618,8 +623,9 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           }
         }
       };
-      if (MODE == kIn) idx_load(blockIdx.x);
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      if (MODE == kIn) idx_load(blockIdx.x >> lg);
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        const int tile = w >> lg;
         int cj[4], cn[4], cby[4], cbx[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -628,7 +634,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
           cby[i] = nby[i];
           cbx[i] = nbx[i];
         }
-        if (MODE == kIn) idx_load(tile + gridDim.x);
+        if (MODE == kIn) idx_load((w + (int)gridDim.x) >> lg);
         if (c % Q::NKC == 0) wtrace(a, kEvIss, c / Q::NKC);
         for (int kc = 0; kc < Q::NKC; ++kc, ++c) {
           const int s = c % Q::SA;
@@ -657,12 +663,20 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
                            a.stack + ((long)(kc * Q::P + k8) * a.src_rows + (long)tile * 128) * 16,
                            (uint32_t)(rows * 16), bar);
           }
-          if (!Q::RES) {  // streamed weights: this chunk's taps
+          if (!Q::RES) {  // streamed weights: this chunk's taps (a slice: its columns of every plane)
             for (int tap = 0; tap < Q::TAPS; ++tap, ++wit) {
               const int sw = wit % SWB;
               tc::mbar_wait(&w_empty[sw], ((wit / SWB) & 1) ^ 1);
-              tc::mbar_expect_tx(&w_full[sw], Q::WCH);
-              tc::bulk_g2s(Wring + sw * Q::WCH, a.wpk + (size_t)(kc * Q::TAPS + tap) * Q::WCH, Q::WCH, &w_full[sw]);
+              const uint8_t* wsrc = a.wpk + (size_t)(kc * Q::TAPS + tap) * Q::WCH;
+              if (Q::SPL && lg) {
+                const int co = (w & 1) * Q::N2 * 16;
+                tc::mbar_expect_tx(&w_full[sw], Q::P * Q::N2 * 16);
+                for (int p = 0; p < Q::P; ++p)
+                  tc::bulk_g2s(Wring + sw * Q::WCH + p * Q::PW + co, wsrc + p * Q::PW + co, Q::N2 * 16, &w_full[sw]);
+              } else {
+                tc::mbar_expect_tx(&w_full[sw], Q::WCH);
+                tc::bulk_g2s(Wring + sw * Q::WCH, wsrc, Q::WCH, &w_full[sw]);
+              }
             }
           }
         }
@@ -674,15 +688,17 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, Q::NS);
+      constexpr uint32_t idesc2 = tc::idesc_bf16_f32(128, Q::NS2);
       int ait = 0, wit = 0, k = 0;
       if (Q::RES) tc::mbar_wait(&w_full[0], 0);
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-        const int buf = Q::NACC == 2 ? (k & 1) : 0;
-        const int use = Q::NACC == 2 ? (k >> 1) : k;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++k) {
+        const int buf = nacc == 2 ? (k & 1) : 0;
+        const int use = nacc == 2 ? (k >> 1) : k;
+        const uint32_t wcol = (uint32_t)((w & lg) * W) * 16;  // this slice's B rows
         tc::mbar_wait(&acc_empty[buf], (use & 1) ^ 1);
         tc::fence_after();
         wtrace(a, kEvMma, k);
-        const uint32_t acc = tmem + buf * N;
+        const uint32_t acc = tmem + buf * W;
         for (int kc = 0; kc < Q::NKC; ++kc, ++ait) {
           const int sa = ait % Q::SA;
           tc::mbar_wait(&a_full[sa], (ait / Q::SA) & 1);
@@ -703,13 +719,22 @@ __global__ void __launch_bounds__(kWideThreads, 1) unit_wide_kernel(const __grid
             // its scheduler with the busy BN / epilogue warps)
             const uint64_t ad = MODE == kIn ? tc::desc_kmajor_swz(abase, 8 * Q::ROWB, Q::SWZ)
                                             : tc::desc_kmajor_noswz(abase + shift * 16, Q::PA, 128);
-            const uint64_t wd = tc::desc_kmajor_noswz(wbase, Q::PW, 128);
+            const uint64_t wd = tc::desc_kmajor_noswz(wbase + wcol, Q::PW, 128);
+            if (Q::SPL && lg) {
 #pragma unroll
-            for (int kk = 0; kk < Q::KC / 16; ++kk)
+              for (int kk = 0; kk < Q::KC / 16; ++kk)
 #pragma unroll
-              for (int h = 0; h < Q::NSPLIT; ++h)
-                tc::mma_bf16(acc + h * Q::NS, tc::desc_add(ad, MODE == kIn ? kk * 32 : 2 * kk * Q::PA),
-                             tc::desc_add(wd, 2 * kk * Q::PW + h * Q::NS * 16), idesc, (kc | tap | kk) > 0);
+                for (int h = 0; h < Q::NSPLIT2; ++h)
+                  tc::mma_bf16(acc + h * Q::NS2, tc::desc_add(ad, MODE == kIn ? kk * 32 : 2 * kk * Q::PA),
+                               tc::desc_add(wd, 2 * kk * Q::PW + h * Q::NS2 * 16), idesc2, (kc | tap | kk) > 0);
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < Q::KC / 16; ++kk)
+#pragma unroll
+                for (int h = 0; h < Q::NSPLIT; ++h)
+                  tc::mma_bf16(acc + h * Q::NS, tc::desc_add(ad, MODE == kIn ? kk * 32 : 2 * kk * Q::PA),
+                               tc::desc_add(wd, 2 * kk * Q::PW + h * Q::NS * 16), idesc, (kc | tap | kk) > 0);
+            }
             if (!Q::RES) tc::mma_commit(&w_empty[sw]);
           }
           tc::mma_commit(&a_empty[sa]);
@@ -1372,6 +1397,7 @@ int launch_wide(const WArgs& a, long max_tiles, cudaStream_t s, const char* what
   auto kern = unit_wide_kernel<K, N, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
+  if (Q::SPL) max_tiles *= 2;  // room for column slices
   cfg.gridDim = dim3((unsigned)(max_tiles < sm_count() ? (max_tiles < 1 ? 1 : max_tiles) : sm_count()));
   cfg.blockDim = dim3(kWideThreads);
   cfg.dynamicSmemBytes = Q::SMEM;
@@ -1440,6 +1466,7 @@ int run_wide(const void* x, void* out, const Geo& g, const uint8_t* img, const i
   a.slab_rows = (a.hb * b + 7) / 8 * 8;
   a.G = 128 / a.slab_rows < 4 ? 128 / a.slab_rows : 4;
   a.box_rows = (128 + 2 * b + 2 + 7) / 8 * 8;
+  a.split = !(debug_flags() & kDebugWideNoSplit);
   // diagnostics: stamps of ONE of the three launches, selected by debug flag bits 3-4
   const int tsel = (debug_flags() >> 3) & 3;
   unsigned long long* tb = trace_buffer();

@@ -24,6 +24,7 @@ pytestmark = pytest.mark.gpu
 
 FORCE_WIDE = 4      # SBN_DEBUG_FORCE_WIDE: the wide unit even where the single kernel applies
 WIDE_UNFUSED = 256  # SBN_DEBUG_WIDE_UNFUSED: IN and MID as two launches
+NO_SPLIT = 1024     # SBN_DEBUG_WIDE_NO_SPLIT: one work item per tile in the three-launch kernels
 
 
 def _case(seed, n, h, w, c, m, density):
@@ -37,25 +38,25 @@ def _case(seed, n, h, w, c, m, density):
     return x, u, P.BinaryMask(mk)
 
 
-def _run(x, mk, u, flags, inplace=False):
+def _run(x, mk, u, flags, inplace=False, block=16):
     lib = _lib.load()
     prev = lib.sbn_debug_set_flags(flags)
     try:
-        y = P.sparse_residual_unit(P.Tensor4D(x.clone().cuda()), mk, u, (16, 16), inplace=inplace)
+        y = P.sparse_residual_unit(P.Tensor4D(x.clone().cuda()), mk, u, (block, block), inplace=inplace)
         torch.cuda.synchronize()
     finally:
         lib.sbn_debug_set_flags(prev)
     return y.data.cpu()
 
 
-def _oracle(x_bf16, u, mk):
+def _oracle(x_bf16, u, mk, block=16):
     def r(a):
         return torch.from_numpy(np.asarray(a, np.float32)).bfloat16().float().numpy()
     ud = {"pre": u.pre_activation}
     for i, (fb, bn) in enumerate(((u.conv1, u.bn1), (u.conv2, u.bn2), (u.conv3, u.bn3)), 1):
         ud[f"w{i}"], ud[f"b{i}"] = r(fb.weights), r(fb.bias)
         ud[f"bn{i}"] = dict(gamma=bn.gamma, beta=bn.beta, mean=bn.running_mean, var=bn.running_var)
-    return O.sparse_residual_unit(x_bf16.float().numpy(), mk.numpy(), ud, (16, 16))
+    return O.sparse_residual_unit(x_bf16.float().numpy(), mk.numpy(), ud, (block, block))
 
 
 # (c, m, n, h, w, density)
@@ -120,3 +121,27 @@ def test_fused_unit_stage_chain(cuda_device):
         finally:
             lib.sbn_debug_set_flags(prev)
     assert torch.equal(outs[0], outs[1])
+
+
+# (c, m, block, n, h, w, density): few tiles per launch, so OUT (N >= 128) runs as two
+# half-width column slices per tile on different CTAs
+SPLIT_CASES = [
+    (384, 192, 6, 1, 60, 64, 0.3),    # config-4 stage-3 shape
+    (384, 192, 6, 2, 100, 90, 0.5),
+    (256, 128, 10, 1, 80, 84, 0.4),   # stage-2 shape
+    (192, 96, 16, 1, 64, 64, 0.3),    # stage-1 shape
+    (128, 64, 8, 1, 40, 48, 0.5),
+]
+
+
+@pytest.mark.parametrize("c,m,blk,n,h,w,density", SPLIT_CASES)
+def test_column_slices_bit_identical(cuda_device, c, m, blk, n, h, w, density):
+    """Column slices change which CTA computes which accumulator columns, not the k-step
+    order of any column: results are bit-identical to one work item per tile, in place and
+    functional, and within the bf16 tolerance of the oracle."""
+    x, u, mk = _case(c + blk, n, h, w, c, m, density)
+    split = _run(x, mk, u, FORCE_WIDE, block=blk)
+    whole = _run(x, mk, u, FORCE_WIDE | NO_SPLIT, block=blk)
+    assert torch.equal(split, whole), (c, m, blk, (split.float() - whole.float()).abs().max().item())
+    assert torch.equal(_run(x, mk, u, FORCE_WIDE, inplace=True, block=blk), split)
+    assert O.rel_err(split.float().numpy(), _oracle(x, u, mk, blk)) <= 2e-2
