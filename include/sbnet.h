@@ -255,9 +255,11 @@ int sbn_debug_set_trace(unsigned long long* buf);
  * SBN_DEBUG_CONV_TMA: run sparse convs on the strided-TMA tap-GEMM kernel even where the
  * single-window kernel applies.
  * SBN_DEBUG_CONV_PAIR: run 16x16-block 3x3 sparse convs on the CTA-pair (cta_group::2,
- * M = 256) kernel. */
+ * M = 256) kernel with streamed weights.
+ * SBN_DEBUG_CONV_NO_RESIDENT: do not use the resident-weight CTA-pair conv (16x16 blocks,
+ * 128 -> 128 channels); the single-CTA double-buffered kernel runs instead. */
 enum { SBN_DEBUG_NO_PAIR = 1, SBN_DEBUG_CONV_SINGLE_BUFFER = 2, SBN_DEBUG_FORCE_WIDE = 4, SBN_DEBUG_FORCE_FUSED = 8,
-       SBN_DEBUG_CONV_TMA = 16, SBN_DEBUG_CONV_PAIR = 32 };
+       SBN_DEBUG_CONV_TMA = 16, SBN_DEBUG_CONV_PAIR = 32, SBN_DEBUG_CONV_NO_RESIDENT = 2048 };
 int sbn_debug_set_flags(int flags);
 /* Diagnostics: occupancy the last tcgen05 unit launch computed (0: CTAs/SM of the
  * single-CTA kernel, 1: co-resident clusters of the CTA-pair kernel). */

@@ -870,6 +870,307 @@ int launch_conv_pair(const ConvArgs& c, int cap, cudaStream_t s) {
   return launch_status("sparse_conv_tcgen05_pair");
 }
 
+// ---------------------------------------------------------------------------------------
+// CTA pair with RESIDENT weights (16x16 blocks, CIN = COUT = 128: config 3).  The
+// single-CTA kernels stream all 9 weight taps (295 KB) through shared memory once per
+// block, and at M = 128, N = 128 the MMA's own operand reads (4 KB A + 4 KB B per 64-cycle
+// UMMA) already use the ~128 B/clk an SM's shared memory delivers, so the weight and window
+// writes slow every MMA (~86 cycles issuing; tools/conv_pair_trace.py) and the weight stream
+// costs ~25 B/clk per SM of L2 bandwidth on every SM at once.  Here, as in the streamed pair
+// kernel above, a block's two M-tiles are ONE M = 256 cta_group::2 UMMA issued by rank 0 and
+// each rank holds the output-channel half of B — but that half of ALL 9 taps (147 KB) stays
+// resident for the whole launch (9 TMA boxes at start), and the window streams through a
+// ring of KC-channel chunks (one 5-D TMA box per chunk and rank, 11 window rows) so the next
+// block's chunks land while this block's MMAs run.  Per SM an UMMA reads 4 KB of A plus its
+// 2 KB half of B (~96 B/clk) and the only other shared-memory writes are the window chunks.
+// MMA order per block: chunk-major (for chunk: for tap: for k16), fp32 accumulation — a
+// different rounding order from the single-CTA kernels (tap-major), so not bit-identical
+// to them; parity against the fp32 oracle (test_gpu_parity.py).
+// Block list: the reduce_mask list (list mode) or, mask-fused, the one-launch global list
+// (conv_mask_global: every CTA tests its candidates, publishes, and waits for all CTAs —
+// the grid is one CTA per SM, co-resident).
+//   wres         both ranks' weight halves landed (rank 1's TMA completes on it)   rank 0
+//   cfull[s]     both ranks' chunk boxes of stage s landed                       rank 0
+//   cempty[s]    MMAs reading stage s done (multicast commit)                    both
+//   acc_full[b]  accumulator b complete (multicast commit)                       both
+//   acc_empty[b] 2 x 256 worker arrivals (rank 1's arrive remotely)              rank 0
+template <int CIN, int COUT, int BS>
+struct PairResCfg {
+  static_assert(BS == 16 && COUT % 32 == 0 && CIN % 32 == 0, "resident pair conv");
+  static constexpr int WROWS = 11;                 // window rows per rank
+  static constexpr int PA = WROWS * BS * 16;       // plane stride (one 8-channel plane)
+  static constexpr int KC = 32;                    // channels per window chunk
+  static constexpr int KP = KC / 8;                // planes per chunk
+  static constexpr int NCH = CIN / KC;             // chunks per block
+  static constexpr int CHUNK = KP * PA;            // bytes of one chunk box (per rank)
+  static constexpr int SZ_C = (CHUNK + 1023) / 1024 * 1024;
+  static constexpr int NH = COUT / 2;
+  static constexpr int PWH = NH * 16;
+  static constexpr int TAPH = (CIN / 8) * PWH;      // one tap's half
+  static constexpr int WBOXR = TAPH / 128;
+  static constexpr int WCH = KP * PWH;             // one chunk's planes of one tap half
+  static constexpr int WCHR = WCH / 128;           // ... as 128-byte rows (weight box)
+  static constexpr int TAP = (CIN / 8) * COUT * 16;
+  static constexpr int OFF_C = 9 * TAPH;           // resident weights first
+  static constexpr int BUDGET = 220 * 1024;        // dynamic smem (static: mask-list arrays)
+  static constexpr int STAGES = (BUDGET - OFF_C - COUT * 4) / SZ_C > 8 ? 8 : (BUDGET - OFF_C - COUT * 4) / SZ_C;
+  static_assert(STAGES >= 2, "resident pair conv: ring does not fit");
+  static constexpr int OFF_BIAS = OFF_C + STAGES * SZ_C;
+  static constexpr int SMEM = OFF_BIAS + COUT * 4;
+  static constexpr int ACC = COUT;
+  static constexpr int TALLOC = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
+};
+
+template <int CIN, int COUT, int BS>
+__global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const __grid_constant__ PairConvArgs pa) {
+  using P = PairResCfg<CIN, COUT, BS>;
+  const ConvArgs& a = pa.c;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t cfull[P::STAGES], cempty[P::STAGES];
+  __shared__ uint64_t wres[P::NCH], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tslot;
+  __shared__ int32_t s_idx[3 * kMaxLocal];  // mask-fused: this CTA's candidates before publishing
+  uint8_t* W = smem;
+  float* bias = reinterpret_cast<float*>(smem + P::OFF_BIAS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const Geo& g = a.g;
+
+  if (tid == 0) {
+    for (int s = 0; s < P::STAGES; ++s) {
+      tc::mbar_init(&cfull[s], 1);
+      tc::mbar_init(&cempty[s], 1);
+    }
+    for (int c = 0; c < P::NCH; ++c) tc::mbar_init(&wres[c], 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], 2 * kWorkers);
+    }
+    tc::mbar_fence_init();
+  }
+  if (tid == 10 * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&pa.tmap) : "memory");
+  if (tid == 8 * 32) asm volatile("prefetch.tensormap [%0];" ::"l"(&pa.wmap) : "memory");
+  for (int i = tid; i < COUT; i += kPairThreads) bias[i] = a.bias ? __bfloat162float(a.bias[i]) : 0.f;
+  if (warp == 0) tc::tmem_alloc_cg2<P::TALLOC>(&tslot);
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast commit
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  tc::pdl_wait();
+  if (tid == 8 * 32) {
+    // weight loader: my half of all 9 taps, once, chunk-major (the issuer starts on chunk 0
+    // while the rest lands; in mask-fused mode the copies overlap the mask test below)
+    for (int c = 0; c < P::NCH; ++c) {
+      if (rank == 0) tc::mbar_expect_tx(&wres[c], 2 * 9 * P::WCH);
+      for (int tap = 0; tap < 9; ++tap) {
+        const int row = (2 * tap + (int)rank) * P::WBOXR + c * P::WCHR;
+        uint8_t* dst = W + tap * P::TAPH + c * P::WCH;
+        if (rank == 0) tma_2d(dst, &pa.wmap, 0, row, &wres[c]);
+        else tma_2d_cg2(dst, &pa.wmap, 0, row, &wres[c], 0);
+      }
+    }
+  }
+  const bool global = a.mask != nullptr;
+  const int B = global ? conv_mask_global<kPairThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
+  const int32_t* lidx = global ? a.gidx : a.idx;  // (n, by, bx) rows; written in this launch when global
+
+  if (warp == 8) {
+    // (the weight loader's copies were issued above)
+  } else if (warp == 10) {
+    // ---------------- window loader: my 11 rows of every block, KC channels per box
+    if (lane == 0) {
+      int it = 0;
+      for (int blk = pair; blk < B; blk += npairs) {
+        const int n = lidx[3 * blk], by = lidx[3 * blk + 1], bx = lidx[3 * blk + 2];
+        const int ys = g.oy + by * g.sy + (int)rank * (P::WROWS - 3), xs = g.ox + bx * g.sx;
+        for (int c = 0; c < P::NCH; ++c, ++it) {
+          const int s = it % P::STAGES;
+          tc::mbar_wait(&cempty[s], ((it / P::STAGES) & 1) ^ 1);
+          if (rank == 0) {
+            tc::mbar_expect_tx(&cfull[s], 2 * P::CHUNK);
+            tma_5d(smem + P::OFF_C + s * P::SZ_C, &pa.tmap, 0, xs, ys, c * P::KP, n, &cfull[s]);
+          } else {
+            tma_5d_cg2(smem + P::OFF_C + s * P::SZ_C, &pa.tmap, 0, xs, ys, c * P::KP, n, &cfull[s], 0);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (rank 0): M = 256 over the pair
+      int it = 0, k = 0;
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, COUT);
+      unsigned long long t_win = 0, t_acc = 0, t_w = 0, t0 = clock64();
+      const uint64_t wd0 = tc::desc_kmajor_noswz(tc::smem_u32(W), P::PWH, 128);
+      const uint64_t ad0 = tc::desc_kmajor_noswz(tc::smem_u32(smem + P::OFF_C), P::PA, 128);
+      for (int blk = pair; blk < B; blk += npairs, ++k) {
+        const int b = k & 1;
+        unsigned long long c1 = clock64();
+        tc::mbar_wait(&acc_empty[b], ((k >> 1) & 1) ^ 1);
+        t_acc += clock64() - c1;
+        tc::fence_after();
+        const uint32_t acc = tmem + b * P::ACC;
+        for (int c = 0; c < P::NCH; ++c, ++it) {
+          const int s = it % P::STAGES;
+          unsigned long long c3 = clock64();
+          if (k == 0) tc::mbar_wait(&wres[c], 0);
+          const unsigned long long c4 = clock64();
+          t_w += c4 - c3;
+          tc::mbar_wait(&cfull[s], (it / P::STAGES) & 1);
+          t_win += clock64() - c4;
+          tc::fence_after();
+          const uint64_t ad = tc::desc_add(ad0, s * P::SZ_C);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int shift = (tap / 3) * BS + (tap % 3);
+#pragma unroll
+            for (int kk = 0; kk < P::KP / 2; ++kk)
+              tc::mma_bf16_cg2(acc, tc::desc_add(ad, 2 * kk * P::PA + shift * 16),
+                               tc::desc_add(wd0, tap * P::TAPH + (c * P::KP + 2 * kk) * P::PWH), idesc,
+                               (c | tap | kk) > 0);
+          }
+          tc::mma_commit_mc(&cempty[s], 3);
+        }
+        tc::mma_commit_mc(&acc_full[b], 3);
+      }
+      if (k == 0)  // no blocks: the weight copies must land before the CTAs exit
+        for (int c = 0; c < P::NCH; ++c) tc::mbar_wait(&wres[c], 0);
+      if (pa.trace) {
+        unsigned long long* tb = pa.trace + blockIdx.x * 8;
+        tb[0] = clock64() - t0;
+        tb[1] = t_win;
+        tb[2] = t_acc;
+        tb[3] = t_w;
+        tb[4] = k;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- workers: drain my tile of each accumulator
+    const int q = warp & 3, tpar = warp >> 2;
+    int k = 0;
+    for (int blk = pair; blk < B; blk += npairs, ++k) {
+      const int n = lidx[3 * blk], by = lidx[3 * blk + 1], bx = lidx[3 * blk + 2];
+      const int b = k & 1;
+      const int r = (int)rank * 128 + q * 32 + lane;
+      const int oy = r / BS, ox = r % BS;
+      const int Y = by * g.obh + oy, X = bx * g.obw + ox;
+      const bool store = oy < g.obh && ox < g.obw && Y < g.oh && X < g.ow;
+      uint4* op = reinterpret_cast<uint4*>(a.out) +
+                  (((size_t)n * g.oh + (store ? Y : 0)) * g.ow + (store ? X : 0)) * (COUT / 8);
+      tc::mbar_wait(&acc_full[b], (k >> 1) & 1);
+      tc::fence_after();
+      const uint32_t acc = tmem + b * P::ACC;
+#pragma unroll
+      for (int c0 = tpar * (COUT / 2); c0 < (tpar + 1) * (COUT / 2); c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(acc + ((uint32_t)(q * 32) << 16) + c0, v);
+        if (c0 + 32 >= (tpar + 1) * (COUT / 2)) {  // accumulator drained: release it early
+          tc::fence_before();
+          if (rank == 0) tc::mbar_arrive(&acc_empty[b]);
+          else tc::mbar_arrive_cluster(&acc_empty[b], 0);
+        }
+        if (store) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              o[e] = tc::pack_bf16(v[16 * h + 2 * e] + bias[c0 + 16 * h + 2 * e],
+                                   v[16 * h + 2 * e + 1] + bias[c0 + 16 * h + 2 * e + 1]);
+            op[c0 / 8 + 2 * h] = make_uint4(o[0], o[1], o[2], o[3]);
+            op[c0 / 8 + 2 * h + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();  // the peer's MMAs / remote arrivals / TMA completions are done before exit
+  tc::fence_after();
+  if (warp == 0) tc::tmem_free_cg2<P::TALLOC>(tmem);
+}
+
+// pairs the resident kernel may launch (2-CTA clusters of its size co-resident on this
+// device; the mask-fused global list needs every CTA resident), cached per device
+template <int CIN, int COUT, int BS>
+int pair_res_max_pairs() {
+  using P = PairResCfg<CIN, COUT, BS>;
+  static int cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 0;
+  if (cache[dev]) return cache[dev] > 0 ? cache[dev] : 0;
+  auto kern = conv_tc_pair_res_kernel<CIN, COUT, BS>;
+  int v = -1;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(kPairThreads);
+    cfg.dynamicSmemBytes = P::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc > 0) v = nc < sm_count() / 2 ? nc : sm_count() / 2;
+  }
+  cudaGetLastError();
+  cache[dev] = v;
+  return v > 0 ? v : 0;
+}
+
+template <int CIN, int COUT, int BS>
+int launch_conv_pair_res(const ConvArgs& c, int cap, cudaStream_t s) {
+  using P = PairResCfg<CIN, COUT, BS>;
+  const int maxp = pair_res_max_pairs<CIN, COUT, BS>();
+  if (maxp <= 0) return SBN_ERR_UNSUPPORTED;
+  if (c.mask && (cap + 2 * maxp - 1) / (2 * maxp) > kMaxLocal) return SBN_ERR_UNSUPPORTED;
+  PairConvArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.c = c;
+  pa.trace = trace_buffer();
+  const Geo& g = c.g;
+  const uint64_t dims[5] = {8, (uint64_t)g.w, (uint64_t)g.h, (uint64_t)(CIN / 8), (uint64_t)g.n};
+  const uint64_t str[4] = {(uint64_t)CIN * 2, (uint64_t)g.w * CIN * 2, 16, (uint64_t)g.h * g.w * CIN * 2};
+  const uint32_t box[5] = {8, (uint32_t)BS, (uint32_t)P::WROWS, (uint32_t)P::KP, 1};
+  int st = encode_map(&pa.tmap, c.x, 5, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st) return st;
+  const uint64_t wdims[2] = {64, (uint64_t)18 * P::WBOXR};  // 18 tap halves of WBOXR 128-byte rows
+  const uint64_t wstr[1] = {128};
+  const uint32_t wbox[2] = {64, (uint32_t)P::WCHR};
+  st = encode_map(&pa.wmap, c.wpk + (size_t)9 * P::TAP, 2, wdims, wstr, wbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (st) return st;
+  auto kern = conv_tc_pair_res_kernel<CIN, COUT, BS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM);
+  // mask-fused: every CTA tests candidates, so the full co-resident grid; list mode: no more
+  // pairs than blocks
+  const int npairs = c.mask ? maxp : (cap < maxp ? (cap < 1 ? 1 : cap) : maxp);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * npairs));
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = P::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, pa);
+  return launch_status("sparse_conv_tcgen05_pair_res");
+}
+
 #define SBN_CONV_TC_CONFIGS(X) \
   X(128, 128, 16)              \
   X(128, 128, 8)               \
@@ -915,6 +1216,21 @@ int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout,
     return SBN_ERR_UNSUPPORTED;
   ConvArgs a;
   memset(&a, 0, sizeof(a));
+  if (!(debug_flags() & (kDebugConvNoRes | kDebugNoGlobalList)) && slotw && gidx && g.bh == 16 && cin == 128 && cout == 128) {
+    // resident-weight CTA pair with the one-launch global list
+    a.x = (const __nv_bfloat16*)x;
+    a.out = (__nv_bfloat16*)dst;
+    a.g = g;
+    a.wpk = (const uint8_t*)wpk;
+    a.bias = (const __nv_bfloat16*)bias;
+    a.cap = cap;
+    a.mask = mask;
+    a.sw = slotw;
+    a.gidx = gidx;
+    const int st = launch_conv_pair_res<128, 128, 16>(a, cap, s);
+    if (st != SBN_ERR_UNSUPPORTED) return st;
+    memset(&a, 0, sizeof(a));
+  }
   if (per_cta < kMinLocal) {
     a.sw = slotw;
     a.gidx = gidx;
@@ -954,6 +1270,10 @@ int sparse_conv_tc(const void* x, int cin, int cout, Geo g, const void* wpk, con
     if (cin == 128 && cout == 128) return launch_conv_pair<128, 128, 16>(a, cap, s);
     if (cin == 64 && cout == 64) return launch_conv_pair<64, 64, 16>(a, cap, s);
     if (cin == 32 && cout == 32) return launch_conv_pair<32, 32, 16>(a, cap, s);
+  }
+  if (!(debug_flags() & (kDebugConvSingleBuffer | kDebugConvNoRes)) && g.bh == 16 && cin == 128 && cout == 128) {
+    const int st = launch_conv_pair_res<128, 128, 16>(a, cap, s);  // resident-weight CTA pair
+    if (st != SBN_ERR_UNSUPPORTED) return st;
   }
   if (!(debug_flags() & kDebugConvSingleBuffer)) {
 #define X(CI, CO, BS_) if (cin == CI && cout == CO && g.bh == BS_ && DbCfg<CI, CO, BS_>::SMEM <= max_smem_optin()) return launch_conv_db<CI, CO, BS_>(a, cap, s);

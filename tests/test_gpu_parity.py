@@ -13,6 +13,8 @@ from paper_1801_02108_b200 import _lib
 from golden_cases import cases, conv_cfg, load, unit_dict
 from oracle import sbnet_oracle as O
 
+NO_RESIDENT = 2048  # SBN_DEBUG_CONV_NO_RESIDENT (include/sbnet.h)
+
 pytestmark = pytest.mark.gpu
 
 
@@ -477,7 +479,7 @@ def test_sparse_conv_double_buffered_bit_identical(cuda_device, cin, block, dens
     m = P.synth_mask_topleft((2, h, w), 1.0 - density)
     p = _conv((3, 3), (1, 1), True, cin)
     outs = []
-    for flags in (2, 0):
+    for flags in (2, NO_RESIDENT):  # (the resident-weight pair kernel accumulates in another order)
         old = lib.sbn_debug_set_flags(flags)
         try:
             outs.append(P.sparse_conv2d(P.Tensor4D(x), m, fb, p, (block, block)).data)
@@ -577,7 +579,7 @@ def test_sparse_conv_cta_pair_bit_identical(cuda_device, cin, density):
     mk = P.synth_mask_blobs((2, h, w), 1.0 - density, 4).cuda()
     idx = P.reduce_mask(mk, spec)
     outs = []
-    for flag in (lib.SBN_DEBUG_CONV_PAIR if hasattr(lib, "SBN_DEBUG_CONV_PAIR") else 32, 0):
+    for flag in (32, NO_RESIDENT):  # streamed-weight pair vs the single-CTA double-buffered kernel
         old = lib.sbn_debug_set_flags(flag)
         try:
             o = torch.zeros_like(x)
@@ -762,13 +764,24 @@ def test_backbone_hierarchical_stage_masks_equal_direct_downsample(cuda_device):
         assert torch.equal(r.mask.data, P.downsample_mask(base, c.mask_scale).data)
 
 
-@pytest.mark.parametrize("block,density", [(16, 0.1), (16, 0.3), (8, 0.1), (32, 0.1)])
-def test_sparse_conv_config3_size_vs_fp32_oracle(cuda_device, block, density):
+@pytest.mark.parametrize("block,density,flags", [(16, 0.1, 0), (16, 0.3, 0), (16, 0.3, 2048), (8, 0.1, 0),
+                                                  (32, 0.1, 0)])
+def test_sparse_conv_config3_size_vs_fp32_oracle(cuda_device, block, density, flags):
     """BASELINE config 3 at full size (1 x 800 x 700 x 128 bf16, 3x3 SAME, top-left mask) through
-    the public sparse_conv2d — the kernels the bench times: several blocks per CTA
-    (double-buffered windows), the half-block tail jobs (16x16 at 30 %: 896 blocks on 148 CTAs),
+    the public sparse_conv2d — the kernels the bench times: the resident-weight CTA pair with
+    the one-launch global list (16x16), the single-CTA double-buffered kernel with its
+    half-block tail jobs (16x16 at 30 % with the pair disabled: 896 blocks on 148 CTAs),
     mask-fused lists (8x8) and the TMA tap-GEMM (32x32) — against the fp32 oracle on
     bf16-rounded inputs (2e-2, north star); inactive pixels exactly zero."""
+    lib = _lib.load()
+    old = lib.sbn_debug_set_flags(flags)
+    try:
+        _config3_case(block, density)
+    finally:
+        lib.sbn_debug_set_flags(old)
+
+
+def _config3_case(block, density):
     rng = np.random.default_rng(block * 100 + int(density * 10))
     h, w, c = 800, 700, 128
     x = torch.from_numpy(rng.standard_normal((1, h, w, c), dtype=np.float32)).bfloat16()
@@ -804,3 +817,53 @@ def test_bf16_scatter_add_vs_oracle(cuda_device):
     ref = O.scatter(blk.float().numpy(), ri, geo, x.float().numpy(), add=True)
     ref_bf16 = torch.from_numpy(ref).bfloat16().float().numpy()
     assert np.array_equal(_np(out), ref_bf16)
+
+
+@pytest.mark.parametrize("n,density", [(3, 0.05), (2, 0.5), (1, 1.0), (2, 0.0)])
+def test_sparse_conv_resident_pair_modes(cuda_device, n, density):
+    """Resident-weight CTA-pair conv (16x16 blocks, 128 -> 128): list mode (reduce_mask list)
+    and the mask-fused global list give the same output bit for bit, call after call and
+    interleaved with the single-CTA kernel on the same sync workspace; against the
+    double-buffered kernel (another fp32 accumulation order, bf16 outputs) within 2^-7 of the
+    largest output; against
+    the fp32 oracle within 2e-2; untouched pixels stay zero."""
+    from paper_1801_02108_b200.layers import sparse_conv_into, sparse_conv_masked_into
+    lib = _lib.load()
+    rng = np.random.default_rng(40 + n)
+    h, w, c = 190, 230, 128
+    x = torch.from_numpy(rng.standard_normal((n, h, w, c)).astype(np.float32)).bfloat16()
+    wt = torch.from_numpy((rng.standard_normal((3, 3, c, c)) / np.sqrt(9 * c)).astype(np.float32)).bfloat16()
+    bias = torch.from_numpy(rng.standard_normal(c).astype(np.float32)).bfloat16()
+    fb = P.FilterBank(wt, bias)
+    p = _conv((3, 3), (1, 1), True, c)
+    spec = P.compute_block_spec((n, h, w, c), p, (16, 16))
+    m = (P.synth_mask_blobs((n, h, w), 1.0 - density, 6) if density < 1 else P.BinaryMask.full(n, h, w))
+    mk = m.cuda()
+    xd = x.cuda()
+    idx = P.reduce_mask(mk, spec)
+    res = []
+    for _ in range(2):
+        for flags in (0, NO_RESIDENT):
+            old = lib.sbn_debug_set_flags(flags)
+            try:
+                a = torch.zeros_like(xd)
+                sparse_conv_into(xd, a, fb, p, spec, idx)
+                b = torch.zeros_like(xd)
+                sparse_conv_masked_into(xd, b, mk.data, fb, p, spec)
+                torch.cuda.synchronize()
+            finally:
+                lib.sbn_debug_set_flags(old)
+            assert torch.equal(a, b)
+            res.append(a)
+    assert torch.equal(res[0], res[2]) and torch.equal(res[1], res[3])
+    y, y_db = _np(res[0]), _np(res[1])
+    if idx.count == 0:
+        assert not y.any()
+        return
+    assert O.rel_err(y, y_db) <= 2 ** -7  # bf16 outputs: the order may flip a last bit (2^-8 of a value)
+    ref = O.sparse_conv2d(x.float().numpy(), m.numpy(), wt.float().numpy(), bias.float().numpy(),
+                          (1, 1), True, (16, 16))
+    assert O.rel_err(y, ref) <= 2e-2
+    geo = O.geometry(h, w, (3, 3), (1, 1), True, (16, 16))
+    reg = O.active_region(geo, O.reduce_mask(m.numpy(), geo), n)
+    assert np.all(y[~reg] == 0)
