@@ -88,13 +88,13 @@ __device__ int conv_mask_local(const ConvArgs& a, int32_t* s_idx) {
     const int cand = (int)blockIdx.x + j * G;
     const int fr = cand / gyx, rr = cand - fr * gyx;
     const int y0 = g.oy + (rr / g.gx) * g.sy, x0 = g.ox + (rr % g.gx) * g.sx;
-    uint8_t v[PL];
+    uint32_t v[PL];  // predicated straight-line loads: all of the window's bytes in flight
 #pragma unroll
     for (int u = 0; u < PL; ++u) {
       const int p = lane + 32 * u;
       const int y = y0 + p / BS, xx = x0 + p % BS;
-      v[u] = (p < AREA && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-                 ? __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx) : (uint8_t)0;
+      const bool ok = p < AREA && y >= 0 && y < g.h && xx >= 0 && xx < g.w;
+      v[u] = tc::ld_u8_pred(a.mask + ((size_t)fr * g.h + (ok ? y : 0)) * g.w + (ok ? xx : 0), ok);
     }
     bool any = false;
 #pragma unroll
@@ -936,6 +936,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
   const uint32_t rank = tc::cluster_rank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const Geo& g = a.g;
+  // diagnostics (tools/conv_res_timeline.py): %globaltimer phase stamps per CTA
+  unsigned long long* tl = pa.trace ? pa.trace + 2048 * 8 + blockIdx.x * 8 : nullptr;
+  if (tl && tid == 0) tl[0] = gtimer();
 
   if (tid == 0) {
     for (int s = 0; s < P::STAGES; ++s) {
@@ -959,9 +962,11 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
   tc::fence_after();
   const uint32_t tmem = tslot;
   tc::pdl_wait();
-  if (tid == 8 * 32) {
-    // weight loader: my half of all 9 taps, once, chunk-major (the issuer starts on chunk 0
-    // while the rest lands; in mask-fused mode the copies overlap the mask test below)
+  if (tl && tid == 0) tl[1] = gtimer();
+  // weight loader: my half of all 9 taps, once, chunk-major (the issuer starts on chunk 0
+  // while the rest lands; mask-fused, the copies overlap the mask test and list exchange).
+  auto load_weights = [&]() {
+    if (tid != 8 * 32) return;
     for (int c = 0; c < P::NCH; ++c) {
       if (rank == 0) tc::mbar_expect_tx(&wres[c], 2 * 9 * P::WCH);
       for (int tap = 0; tap < 9; ++tap) {
@@ -971,10 +976,28 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
         else tma_2d_cg2(dst, &pa.wmap, 0, row, &wres[c], 0);
       }
     }
-  }
+  };
   const bool global = a.mask != nullptr;
+  load_weights();
   const int B = global ? conv_mask_global<kPairThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
-  const int32_t* lidx = global ? a.gidx : a.idx;  // (n, by, bx) rows; written in this launch when global
+  const int nmine = B > pair ? (B - pair + npairs - 1) / npairs : 0;  // my pair's blocks
+  // block k of my pair -> (frame, block row, block column)
+  auto block_of = [&](int k, int& n, int& by, int& bx) {
+    const int blk = pair + k * npairs;
+    if (global) {  // rows written in this launch: coherent loads
+      n = a.gidx[3 * blk];
+      by = a.gidx[3 * blk + 1];
+      bx = a.gidx[3 * blk + 2];
+    } else {
+      n = __ldg(a.idx + 3 * blk);
+      by = __ldg(a.idx + 3 * blk + 1);
+      bx = __ldg(a.idx + 3 * blk + 2);
+    }
+  };
+  if (tl && tid == 0) {
+    tl[2] = gtimer();
+    tl[7] = B;
+  }
 
   if (warp == 8) {
     // (the weight loader's copies were issued above)
@@ -982,8 +1005,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
     // ---------------- window loader: my 11 rows of every block, KC channels per box
     if (lane == 0) {
       int it = 0;
-      for (int blk = pair; blk < B; blk += npairs) {
-        const int n = lidx[3 * blk], by = lidx[3 * blk + 1], bx = lidx[3 * blk + 2];
+      for (int kb = 0; kb < nmine; ++kb) {
+        int n, by, bx;
+        block_of(kb, n, by, bx);
         const int ys = g.oy + by * g.sy + (int)rank * (P::WROWS - 3), xs = g.ox + bx * g.sx;
         for (int c = 0; c < P::NCH; ++c, ++it) {
           const int s = it % P::STAGES;
@@ -1006,7 +1030,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
       unsigned long long t_win = 0, t_acc = 0, t_w = 0, t0 = clock64();
       const uint64_t wd0 = tc::desc_kmajor_noswz(tc::smem_u32(W), P::PWH, 128);
       const uint64_t ad0 = tc::desc_kmajor_noswz(tc::smem_u32(smem + P::OFF_C), P::PA, 128);
-      for (int blk = pair; blk < B; blk += npairs, ++k) {
+      for (; k < nmine; ++k) {
         const int b = k & 1;
         unsigned long long c1 = clock64();
         tc::mbar_wait(&acc_empty[b], ((k >> 1) & 1) ^ 1);
@@ -1021,6 +1045,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
           t_w += c4 - c3;
           tc::mbar_wait(&cfull[s], (it / P::STAGES) & 1);
           t_win += clock64() - c4;
+          if (tl && it == 0) tl[3] = gtimer();
           tc::fence_after();
           const uint64_t ad = tc::desc_add(ad0, s * P::SZ_C);
 #pragma unroll
@@ -1036,6 +1061,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
         }
         tc::mma_commit_mc(&acc_full[b], 3);
       }
+      if (tl) tl[4] = gtimer();
       if (k == 0)  // no blocks: the weight copies must land before the CTAs exit
         for (int c = 0; c < P::NCH; ++c) tc::mbar_wait(&wres[c], 0);
       if (pa.trace) {
@@ -1052,8 +1078,9 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
     // ---------------- workers: drain my tile of each accumulator
     const int q = warp & 3, tpar = warp >> 2;
     int k = 0;
-    for (int blk = pair; blk < B; blk += npairs, ++k) {
-      const int n = lidx[3 * blk], by = lidx[3 * blk + 1], bx = lidx[3 * blk + 2];
+    for (; k < nmine; ++k) {
+      int n, by, bx;
+      block_of(k, n, by, bx);
       const int b = k & 1;
       const int r = (int)rank * 128 + q * 32 + lane;
       const int oy = r / BS, ox = r % BS;
@@ -1065,34 +1092,30 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
       tc::fence_after();
       const uint32_t acc = tmem + b * P::ACC;
 #pragma unroll
-      for (int c0 = tpar * (COUT / 2); c0 < (tpar + 1) * (COUT / 2); c0 += 32) {
-        float v[32];
-        tc::tmem_ld32(acc + ((uint32_t)(q * 32) << 16) + c0, v);
-        if (c0 + 32 >= (tpar + 1) * (COUT / 2)) {  // accumulator drained: release it early
-          tc::fence_before();
-          if (rank == 0) tc::mbar_arrive(&acc_empty[b]);
-          else tc::mbar_arrive_cluster(&acc_empty[b], 0);
-        }
+      for (int c0 = tpar * (COUT / 2); c0 < (tpar + 1) * (COUT / 2); c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(acc + ((uint32_t)(q * 32) << 16) + c0, v);
         if (store) {
+          uint32_t o[8];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t o[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              o[e] = tc::pack_bf16(v[16 * h + 2 * e] + bias[c0 + 16 * h + 2 * e],
-                                   v[16 * h + 2 * e + 1] + bias[c0 + 16 * h + 2 * e + 1]);
-            op[c0 / 8 + 2 * h] = make_uint4(o[0], o[1], o[2], o[3]);
-            op[c0 / 8 + 2 * h + 1] = make_uint4(o[4], o[5], o[6], o[7]);
-          }
+          for (int e = 0; e < 8; ++e)
+            o[e] = tc::pack_bf16(v[2 * e] + bias[c0 + 2 * e], v[2 * e + 1] + bias[c0 + 2 * e + 1]);
+          op[c0 / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+          op[c0 / 8 + 1] = make_uint4(o[4], o[5], o[6], o[7]);
         }
       }
+      tc::fence_before();
+      if (rank == 0) tc::mbar_arrive(&acc_empty[b]);
+      else tc::mbar_arrive_cluster(&acc_empty[b], 0);
     }
+    if (tl && tid == 0) tl[5] = gtimer();
   }
   tc::fence_before();
   __syncthreads();
   tc::cluster_sync();  // the peer's MMAs / remote arrivals / TMA completions are done before exit
   tc::fence_after();
   if (warp == 0) tc::tmem_free_cg2<P::TALLOC>(tmem);
+  if (tl && tid == 0) tl[6] = gtimer();
 }
 
 // pairs the resident kernel may launch (2-CTA clusters of its size co-resident on this

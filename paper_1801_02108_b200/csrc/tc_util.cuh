@@ -212,6 +212,18 @@ __device__ __forceinline__ uint4 ld_v4_pred(const void* p, bool pred) {
   return v;
 }
 
+// 1-byte global load (read-only path), zero when !pred: predicated, straight-line (see
+// ld_v4_pred) so a run of these stays in flight together
+__device__ __forceinline__ uint32_t ld_u8_pred(const void* p, bool pred) {
+  uint32_t v;
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b16 h;\n setp.ne.b32 q, %2, 0;\n mov.b16 h, 0;\n"
+      " @q ld.global.nc.u8 h, [%1];\n cvt.u32.u16 %0, h;\n}"
+      : "=r"(v)
+      : "l"(p), "r"((int)pred));
+  return v;
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool src_ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
                "r"(src_ok ? 16 : 0)
