@@ -15,12 +15,13 @@ import subprocess
 import sys
 
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1801_02108_b200/libsbnet.so"
-HOT = ("unit_tc_pair_kernel", "unit_tc_kernel", "conv_tc_db_kernel", "conv_dense_kernel", "conv_dense_pair_kernel",
+HOT = ("unit_tc_pair_kernel", "unit_tc_kernel", "conv_tc_db_kernel", "conv_tc_pair_res_kernel", "conv_dense_kernel", "conv_dense_pair_kernel",
        "unit_wide_kernel", "unit_wide_fused_kernel", "reduce_mask_cluster_kernel", "gather_kernel", "scatter_kernel")
 # instantiations whose tensor-core lines are printed (counts are printed for every hot kernel)
 HEADLINE = ("unit_tc_pair_kernel<64, 32, 16>", "conv_tc_db_kernel<128, 128, 16>", "conv_dense_kernel<128, 128, 3, false>",
             "unit_wide_kernel<192, 96, 1>", "unit_wide_kernel<96, 96, 2>", "unit_wide_kernel<96, 192, 3>",
-            "reduce_mask_cluster_kernel", "unit_wide_fused_kernel<96, 48>", "conv_dense_pair_kernel<192, 256, 3>")
+            "reduce_mask_cluster_kernel", "unit_wide_fused_kernel<96, 48>", "conv_dense_pair_kernel<192, 256, 3>",
+            "conv_tc_pair_res_kernel<128, 128, 16>")
 MAX_LINES = 40
 MNEM = ("UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "UTMASTG", "UBLKCP", "UTMAPF", "SYNCS")
 
