@@ -221,7 +221,11 @@ int sbn_residual_unit_pack(const sbn_unit_params* p, int dtype, int c, int m,
  * the caller and left zeroed by every call (barrier / look-back words at fixed offsets);
  * ws: sbn_sparse_residual_unit_workspace bytes, zeroed ONCE by the caller and kept between
  * calls (it carries the launch epoch and the tagged block-list entries; a new zeroed ws
- * simply restarts the epoch). */
+ * simply restarts the epoch).  Kernels are launched with programmatic dependent launch: the
+ * tcgen05 kernel reads the packed weights and tests its first round of mask candidates
+ * before griddepcontrol.wait, i.e. possibly while the previous kernel on the stream is
+ * still running — `mask` (like the packed image) must not be written by a kernel that
+ * triggers its dependents early (no kernel of this library that writes masks does). */
 size_t sbn_sparse_residual_unit_sync_bytes(const sbn_geometry* g);
 size_t sbn_sparse_residual_unit_workspace(int dtype, int c, int m, const sbn_geometry* g, int halo,
                                           int algo);
@@ -257,9 +261,12 @@ int sbn_debug_set_trace(unsigned long long* buf);
  * SBN_DEBUG_CONV_PAIR: run 16x16-block 3x3 sparse convs on the CTA-pair (cta_group::2,
  * M = 256) kernel with streamed weights.
  * SBN_DEBUG_CONV_NO_RESIDENT: do not use the resident-weight CTA-pair conv (16x16 blocks,
- * 128 -> 128 channels); the single-CTA double-buffered kernel runs instead. */
+ * 128 -> 128 channels); the single-CTA double-buffered kernel runs instead.
+ * SBN_DEBUG_NO_EARLY_MASK: the mask-fused tcgen05 unit tests its first round of candidates
+ * after griddepcontrol.wait instead of before it. */
 enum { SBN_DEBUG_NO_PAIR = 1, SBN_DEBUG_CONV_SINGLE_BUFFER = 2, SBN_DEBUG_FORCE_WIDE = 4, SBN_DEBUG_FORCE_FUSED = 8,
-       SBN_DEBUG_CONV_TMA = 16, SBN_DEBUG_CONV_PAIR = 32, SBN_DEBUG_CONV_NO_RESIDENT = 2048 };
+       SBN_DEBUG_CONV_TMA = 16, SBN_DEBUG_CONV_PAIR = 32, SBN_DEBUG_CONV_NO_RESIDENT = 2048,
+       SBN_DEBUG_NO_EARLY_MASK = 4096 };
 int sbn_debug_set_flags(int flags);
 /* Diagnostics: occupancy the last tcgen05 unit launch computed (0: CTAs/SM of the
  * single-CTA kernel, 1: co-resident clusters of the CTA-pair kernel). */

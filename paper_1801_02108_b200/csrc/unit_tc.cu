@@ -97,6 +97,7 @@ struct TcArgs {
   const int32_t* idx;
   const int32_t* count;
   int cap;
+  int early_mask;  // fused: test the first round of candidates before griddepcontrol.wait
 };
 
 __device__ __forceinline__ float bf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
@@ -158,63 +159,81 @@ __device__ __forceinline__ bool slot_match(unsigned long long e, unsigned tag) {
   return (unsigned)(e >> 32) == tag_hash(tag);
 }
 
-// Returns this launch's tag (epoch + 1); the epoch load overlaps the mask loads.  Thread 32
-// gets the old value of its `done` increment in `done_old`; it is only consumed by
-// slot_last_producer, after the CTA has polled for its entry (the round trip overlaps).
+// Flags of one round of this CTA's candidates (r0 + j*G, j < 32) in shared memory.
+struct SlotSmem {
+  int flag[32], fr[32], y0[32], x0[32];
+  int base;
+  unsigned tag;
+};
+
 template <int C, int BS>
-__device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done_old) {
+__device__ __forceinline__ void slot_test(const TcArgs& a, SlotSmem& ss, int r0) {
   const Geo& g = a.g;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  __shared__ int s_flag[32], s_fr[32], s_y0[32], s_x0[32];
-  __shared__ int s_base;
-  __shared__ unsigned s_tag;
-  unsigned ep = 0;
-  if (tid == 0) ep = ld_relaxed_u32(a.sw);
+  const int tid = threadIdx.x;
   const int T = g.n * g.gy * g.gx;
   constexpr int area = BS * BS;  // the unit's window (bh == bw == BS)
   const int G = gridDim.x;
+  const int nj = min(32, (T - r0 + G - 1) / G);
+  if (tid < 32) {
+    ss.flag[tid] = 0;
+    const int cand = r0 + tid * G;
+    const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
+    const int cy = rr / g.gx, cx = rr - cy * g.gx;
+    ss.fr[tid] = fr;
+    ss.y0[tid] = g.oy + cy * g.sy;
+    ss.x0[tid] = g.ox + cx * g.sx;
+  }
+  __syncthreads();
+  constexpr int U = 4;  // loads in flight per thread before any is tested
+  for (int e0 = tid; e0 < nj * area; e0 += U * kThreads) {
+    uint8_t v[U];
+    int jj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * kThreads;
+      const int j = min(e / area, 31), p = e % area;
+      const int fr = ss.fr[j];
+      const int y = ss.y0[j] + p / BS, xx = ss.x0[j] + p % BS;
+      jj[u] = j;
+      v[u] = (e < nj * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
+                 ? __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx) : (uint8_t)0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v[u]) ss.flag[jj[u]] = 1;
+  }
+  __syncthreads();
+}
+
+// Returns this launch's tag (epoch + 1).  Thread 32 gets the old value of its `done`
+// increment in `done_old`; it is only consumed by slot_last_producer, after the CTA has
+// polled for its entry (the round trip overlaps).  `pretested`: the first round's flags are
+// already in `ss` — the kernels test their first round of candidates BEFORE
+// griddepcontrol.wait, overlapping the previous kernel's tail (the mask, like the packed
+// weights, is never written by a kernel that triggers its dependents early).
+template <int C, int BS>
+__device__ __forceinline__ unsigned slot_produce(const TcArgs& a, SlotSmem& ss, bool pretested, unsigned& done_old) {
+  const Geo& g = a.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned ep = 0;
+  if (tid == 0) ep = ld_relaxed_u32(a.sw);
+  const int T = g.n * g.gy * g.gx;
+  const int G = gridDim.x;
   for (int r0 = blockIdx.x; r0 < T; r0 += 32 * G) {
     const int nj = min(32, (T - r0 + G - 1) / G);
-    if (tid < 32) {
-      s_flag[tid] = 0;
-      const int cand = r0 + tid * G;
-      const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
-      const int cy = rr / g.gx, cx = rr - cy * g.gx;
-      s_fr[tid] = fr;
-      s_y0[tid] = g.oy + cy * g.sy;
-      s_x0[tid] = g.ox + cx * g.sx;
-    }
-    __syncthreads();
-    constexpr int U = 4;  // loads in flight per thread before any is tested
-    for (int e0 = tid; e0 < nj * area; e0 += U * kThreads) {
-      uint8_t v[U];
-      int jj[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * kThreads;
-        const int j = min(e / area, 31), p = e % area;
-        const int fr = s_fr[j];
-        const int y = s_y0[j] + p / BS, xx = s_x0[j] + p % BS;
-        jj[u] = j;
-        v[u] = (e < nj * area && y >= 0 && y < g.h && xx >= 0 && xx < g.w)
-                   ? __ldg(a.mask + ((size_t)fr * g.h + y) * g.w + xx) : (uint8_t)0;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (v[u]) s_flag[jj[u]] = 1;
-    }
-    if (tid == 0) s_tag = ep + 1u;
+    if (!(pretested && r0 == (int)blockIdx.x)) slot_test<C, BS>(a, ss, r0);
+    if (tid == 0) ss.tag = ep + 1u;
     __syncthreads();
     trace(a.trace, 12);
-    const unsigned tag = s_tag;
+    const unsigned tag = ss.tag;
     if (warp == 0) {
-      const bool on = lane < nj && s_flag[lane];
+      const bool on = lane < nj && ss.flag[lane];
       const unsigned bal = __ballot_sync(0xffffffffu, on);
-      if (lane == 0) s_base = bal ? (int)atomicAdd(slot_ring(a, tag), (unsigned)__popc(bal)) : 0;
+      if (lane == 0) ss.base = bal ? (int)atomicAdd(slot_ring(a, tag), (unsigned)__popc(bal)) : 0;
       __syncwarp();
       if (bal) trace(a.trace, 19);
       if (on) {
-        const int pos = s_base + __popc(bal & ((1u << lane) - 1u));
+        const int pos = ss.base + __popc(bal & ((1u << lane) - 1u));
         const int cand = r0 + lane * G;
         const int fr = cand / (g.gy * g.gx), rr = cand - fr * (g.gy * g.gx);
         const int by = rr / g.gx, bx = rr % g.gx;
@@ -224,13 +243,23 @@ __device__ __forceinline__ unsigned slot_produce(const TcArgs& a, unsigned& done
         a.idx_out[3 * pos + 2] = bx;
       }
     }
+    __syncthreads();  // warp 0's reads of this round's flags before the next round's test
   }
-  if (T <= (int)blockIdx.x && tid == 0) s_tag = ep + 1u;  // no candidate for this CTA
+  if (T <= (int)blockIdx.x && tid == 0) ss.tag = ep + 1u;  // no candidate for this CTA
   __syncthreads();
-  const unsigned tag = s_tag;
+  const unsigned tag = ss.tag;
   if (tid == 32) done_old = atom_add_release(slot_ring(a, tag) + 1, 1u);
   trace(a.trace, 14);
   return tag;
+}
+
+// the kernels' early half of slot_produce: the first round of mask tests, before
+// griddepcontrol.wait
+template <int C, int BS>
+__device__ __forceinline__ bool slot_pretest(const TcArgs& a, SlotSmem& ss) {
+  if (a.mask == nullptr || (int)blockIdx.x >= a.g.n * a.g.gy * a.g.gx || !a.early_mask) return false;
+  slot_test<C, BS>(a, ss, blockIdx.x);
+  return true;
 }
 
 // The last producer (done_old == G - 1: every CTA has read the epoch) publishes the block
@@ -425,6 +454,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
     tc::mbar_expect_tx(&wbar, bytes);
     tc::bulk_g2s(B1, a.packed, bytes, &wbar);
   }
+  __shared__ SlotSmem ss;
+  const bool pretested = slot_pretest<C, BS>(a, ss);  // under the previous kernel's tail
   if (warp == 0) tc::tmem_alloc<K::TALLOC>(&tslot);
   tc::fence_before();
   __syncthreads();
@@ -448,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<C, MC, BS>::OCC) unit_tc_kernel(
   bool have;
   if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
     unsigned done_old = 0;
-    tag = slot_produce<C, BS>(a, done_old);
+    tag = slot_produce<C, BS>(a, ss, pretested, done_old);
     idx = a.idx_out;
     have = slot_entry(a, tag, blockIdx.x, n0, by0, bx0);
     slot_last_producer(a, tag, done_old);
@@ -955,6 +986,8 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
     tc::mbar_expect_tx(&wbar, PK::IMG);
     tc::bulk_g2s(B1, a.packed, PK::IMG, &wbar);
   }
+  __shared__ SlotSmem ss;
+  const bool pretested = slot_pretest<C, BS>(a, ss);  // under the previous kernel's tail
   if (warp == 0) tc::tmem_alloc<PK::TALLOC>(&tslot);
   tc::fence_before();
   __syncthreads();
@@ -975,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads, 2) unit_tc_pair_kernel(TcArgs a) {
   bool have;
   if (fused) {  // mask -> blocks in this kernel (slot compaction), see slot_produce
     unsigned done_old = 0;
-    tag = slot_produce<C, BS>(a, done_old);
+    tag = slot_produce<C, BS>(a, ss, pretested, done_old);
     idx = a.idx_out;
     have = slot_entry(a, tag, pair, n1, by1, bx1);
     slot_last_producer(a, tag, done_old);
@@ -1364,6 +1397,7 @@ static TcArgs make_args(const void* x, void* out, const void* rim, const Geo& g,
   a.cst = nullptr;
   a.etag = nullptr;
   a.sw = nullptr;
+  a.early_mask = 0;
   a.idx = idx; a.count = count; a.cap = cap;
   return a;
 }
@@ -1384,6 +1418,7 @@ int unit_tc_launch(const void* x, void* out, void* rim_buf, unsigned int* gbar, 
                    unsigned long long* etag, unsigned int* slotw) {
   TcArgs a = make_args(x, out, nullptr, g, p, idx, count, cap);
   a.mask = mask;
+  a.early_mask = !(debug_flags() & kDebugNoEarlyMask);
   a.idx_out = idx_out;
   a.count_out = count_out;
   a.cst = cst;
