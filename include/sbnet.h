@@ -263,10 +263,12 @@ int sbn_debug_set_trace(unsigned long long* buf);
  * SBN_DEBUG_CONV_NO_RESIDENT: do not use the resident-weight CTA-pair conv (16x16 blocks,
  * 128 -> 128 channels); the single-CTA double-buffered kernel runs instead.
  * SBN_DEBUG_NO_EARLY_MASK: the mask-fused tcgen05 unit tests its first round of candidates
- * after griddepcontrol.wait instead of before it. */
+ * after griddepcontrol.wait instead of before it.
+ * SBN_DEBUG_ROW_REDUCE_MASK: reduce_mask on the one-block-row-per-CTA kernel even where the
+ * ranges kernel (several block rows per CTA) applies. */
 enum { SBN_DEBUG_NO_PAIR = 1, SBN_DEBUG_CONV_SINGLE_BUFFER = 2, SBN_DEBUG_FORCE_WIDE = 4, SBN_DEBUG_FORCE_FUSED = 8,
        SBN_DEBUG_CONV_TMA = 16, SBN_DEBUG_CONV_PAIR = 32, SBN_DEBUG_CONV_NO_RESIDENT = 2048,
-       SBN_DEBUG_NO_EARLY_MASK = 4096 };
+       SBN_DEBUG_NO_EARLY_MASK = 4096, SBN_DEBUG_ROW_REDUCE_MASK = 8192 };
 int sbn_debug_set_flags(int flags);
 /* Diagnostics: occupancy the last tcgen05 unit launch computed (0: CTAs/SM of the
  * single-CTA kernel, 1: co-resident clusters of the CTA-pair kernel). */

@@ -123,7 +123,8 @@ int debug_flags();                   // host side: sbn_debug_set_flags()
 enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4, kDebugForceFused = 8, kDebugConvTma = 16,
        kDebugConvPair = 32, kDebugCooperative = 64, kDebugNoGlobalList = 128,
        kDebugWideUnfused = 256, kDebugDenseSingle = 512, kDebugWideNoSplit = 1024, kDebugConvNoRes = 2048,
-       kDebugNoEarlyMask = 4096 };
+       kDebugNoEarlyMask = 4096,
+       kDebugRowReduceMask = 8192 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

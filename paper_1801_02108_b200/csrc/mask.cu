@@ -338,6 +338,192 @@ reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, do
   }
 }
 
+// Large problems (many block rows, e.g. 64 frames): CTA r (in ticket order) owns `per`
+// consecutive block rows — the cluster kernel's column-reduce / window-reduce / in-CTA scan
+// over all of its rows with every row load of a (row, 4-column word) item in flight — and
+// its count joins the ordered list through the decoupled look-back of reduce_mask_kernel
+// over the earlier ranges (ws->status[range]).  A few hundred CTAs with several block rows
+// each instead of one CTA (ticket, look-back step, done atomic) per block row.
+constexpr int kRangeThreads = 256;
+
+__global__ void __launch_bounds__(kRangeThreads)
+reduce_mask_ranges_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int per,
+                          int32_t* __restrict__ idx, int32_t* __restrict__ count, MaskWs* ws, int ranges,
+                          int vec, unsigned long long* tr) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ int wsum[kRangeThreads / 32];
+  __shared__ unsigned int s_range;
+  __shared__ int s_prefix, s_total, s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long tt0 = tr ? gtimer() : 0;
+  if (tid == 0) s_range = atomicAdd(&ws->ticket, 1u);
+  __syncthreads();
+  const int range = (int)s_range;
+  unsigned long long* trc = tr && tid == 0 ? tr + (size_t)range * 8 : nullptr;
+  if (trc) { trc[0] = tt0; trc[1] = gtimer(); }
+  const int tiles = g.n * g.gy;
+  const int t0 = range * per, t1 = min(t0 + per, tiles);
+  const int mt = max(t1 - t0, 0);
+  int* colsum = reinterpret_cast<int*>(sm);   // [per][w]
+  uint8_t* flag = sm + (size_t)per * g.w * 4;  // [per * gx]
+  const double area = (double)g.bh * (double)g.bw;
+
+  if (vec) {
+    const int wpr = g.w >> 2;
+    for (int i = tid; i < mt * wpr; i += kRangeThreads) {
+      const int tl = i / wpr, wi = i - tl * wpr;
+      const int t = t0 + tl;
+      const int n = t / g.gy, by = t - n * g.gy;
+      const int wy0 = g.oy + by * g.sy;
+      const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
+      const uint32_t* base = reinterpret_cast<const uint32_t*>(mask + (size_t)n * g.h * g.w) + wi;
+      uint32_t acc = 0;
+      for (int y = y0; y < y1; y += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = (y + r < y1) ? __ldg(base + (size_t)(y + r) * wpr) : 0u;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) acc += v[r];
+      }
+      int* cs = colsum + (size_t)tl * g.w + 4 * wi;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cs[e] = (acc >> (8 * e)) & 0xffu;
+    }
+  } else {
+    for (int i = tid; i < mt * g.w; i += kRangeThreads) {
+      const int tl = i / g.w, x = i - tl * g.w;
+      const int t = t0 + tl;
+      const int n = t / g.gy, by = t - n * g.gy;
+      const int wy0 = g.oy + by * g.sy;
+      const int y0 = max(wy0, 0), y1 = min(wy0 + g.bh, g.h);
+      int acc = 0;
+      for (int y = y0; y < y1; ++y) acc += __ldg(mask + ((size_t)n * g.h + y) * g.w + x);
+      colsum[i] = acc;
+    }
+  }
+  __syncthreads();
+  if (trc) trc[2] = gtimer();
+  const int T = mt * g.gx;
+  for (int c = tid; c < T; c += kRangeThreads) {
+    const int tl = c / g.gx, bx = c - tl * g.gx;
+    const int by = (t0 + tl) % g.gy;
+    const int wy0 = g.oy + by * g.sy;
+    const bool rows = max(wy0, 0) < min(wy0 + g.bh, g.h);
+    const int wx0 = g.ox + bx * g.sx;
+    const int xa = max(wx0, 0), xb = min(wx0 + g.bw, g.w);
+    int cnt = 0;
+    if (rows)
+      for (int x = xa; x < xb; ++x) cnt += colsum[(size_t)tl * g.w + x];
+    flag[c] = pool == SBN_POOL_MAX ? (cnt > 0) : (((double)cnt / area) >= thr - 1e-12);
+  }
+  __syncthreads();
+  // per-thread contiguous run of candidates -> in-CTA exclusive scan
+  const int pc = (T + kRangeThreads - 1) / kRangeThreads;
+  const int c0 = min(tid * pc, T), c1 = min(c0 + pc, T);
+  int mine = 0;
+  for (int c = c0; c < c1; ++c) mine += flag[c];
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (trc) trc[3] = gtimer();
+  if (warp == 0) {
+    const int w_s = lane < kRangeThreads / 32 ? wsum[lane] : 0;
+    int wi = w_s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    if (lane < kRangeThreads / 32) wsum[lane] = wi - w_s;
+    if (lane == 31) s_total = wi;
+  }
+  __syncthreads();
+  // decoupled look-back over the earlier ranges with the WHOLE CTA: thread i inspects range
+  // j - i, so each round covers 256 predecessors (the one-warp look-back of
+  // reduce_mask_kernel advances 32 per memory round trip, which over hundreds of ranges
+  // published at about the same time becomes a chain of round trips)
+  __shared__ int s_incl[kRangeThreads / 32], s_none[kRangeThreads / 32], s_val[kRangeThreads / 32];
+  const int total = s_total;
+  if (tid == 0) atomicExch(&ws->status[range], ((range == 0 ? 2ull : 1ull) << 32) | (unsigned)total);
+  int prefix = 0;
+  for (int j = range - 1; j >= 0;) {
+    const int k = j - tid;
+    const unsigned long long st = k >= 0 ? ld_volatile(&ws->status[k]) : (2ull << 32);
+    const unsigned fl = (unsigned)(st >> 32);
+    const unsigned inc_b = __ballot_sync(0xffffffffu, fl == 2);
+    const unsigned non_b = __ballot_sync(0xffffffffu, fl == 0);
+    if (lane == 0) {
+      s_incl[warp] = inc_b ? 32 * warp + __ffs(inc_b) - 1 : 1 << 30;  // nearest inclusive in this warp
+      s_none[warp] = non_b ? 32 * warp + __ffs(non_b) - 1 : 1 << 30;  // nearest missing
+    }
+    __syncthreads();
+    int first = 1 << 30, miss = 1 << 30;
+#pragma unroll
+    for (int w = 0; w < kRangeThreads / 32; ++w) {
+      first = min(first, s_incl[w]);
+      miss = min(miss, s_none[w]);
+    }
+    const int upto = first < kRangeThreads ? first : kRangeThreads - 1;
+    __syncthreads();
+    if (miss <= upto) {  // a needed predecessor has not published yet: retry the window
+      __nanosleep(64);
+      continue;
+    }
+    int v = tid <= upto ? (int)(unsigned)(st & 0xffffffffull) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) s_val[warp] = v;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kRangeThreads / 32; ++w) prefix += s_val[w];
+    __syncthreads();
+    if (first < kRangeThreads) break;
+    j -= kRangeThreads;
+  }
+  if (tid == 0) {
+    if (range > 0) {
+      __threadfence();
+      atomicExch(&ws->status[range], (2ull << 32) | (unsigned)(prefix + total));
+    }
+    s_prefix = prefix;
+    if (range == ranges - 1) *count = prefix + total;
+  }
+  __syncthreads();
+  if (trc) trc[4] = gtimer();
+  int pos = s_prefix + wsum[warp] + incl - mine;
+  for (int c = c0; c < c1; ++c) {
+    if (flag[c]) {
+      const int tl = c / g.gx, bx = c - tl * g.gx;
+      const int t = t0 + tl;
+      const int n = t / g.gy, by = t - n * g.gy;
+      idx[3 * pos] = n;
+      idx[3 * pos + 1] = by;
+      idx[3 * pos + 2] = bx;
+      ++pos;
+    }
+  }
+  // self-cleaning workspace: the last CTA out resets ticket / done / status
+  if (tid == 0) {
+    __threadfence();
+    s_last = (atomicAdd(&ws->done, 1u) == (unsigned)(ranges - 1));
+  }
+  __syncthreads();
+  if (trc) trc[5] = gtimer();
+  if (s_last) {
+    for (int t = tid; t < ranges; t += kRangeThreads) ws->status[t] = 0ull;
+    if (tid == 0) {
+      ws->ticket = 0u;
+      ws->done = 0u;
+    }
+    __threadfence();
+  }
+}
+
 __global__ void downsample_kernel(const uint8_t* __restrict__ in, int n, int h, int w, int f,
                                   int oh, int ow, uint8_t* __restrict__ out, int vec4) {
   const long total = (long)n * oh * ow;
@@ -447,6 +633,21 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
                              count, vec) == cudaSuccess)
         return launch_status("reduce_mask(cluster)");
       cudaGetLastError();  // cluster launch refused: fall through to the look-back kernel
+    }
+  }
+  {
+    // several block rows per CTA (about four CTAs per SM), ordered by the look-back
+    long per = (tiles + 4L * sm_count() - 1) / (4L * sm_count());
+    if (per < 1) per = 1;
+    const size_t smem = (size_t)per * g.w * 4 + (size_t)per * g.gx;
+    // (at one row per CTA the row kernel below is as fast or faster: tools/reduce_mask_ab.py)
+    if (per >= 2 && smem <= 48 * 1024 && !(debug_flags() & kDebugRowReduceMask)) {
+      const int vec = ((g.w & 3) == 0) && (((uintptr_t)mask & 3) == 0) && g.bh < 256;
+      const int ranges = (int)((tiles + per - 1) / per);
+      reduce_mask_ranges_kernel<<<(unsigned)ranges, kRangeThreads, smem, s>>>(
+          mask, g, pool, threshold, (int)per, idx, count, reinterpret_cast<MaskWs*>(ws), ranges, vec,
+          trace_buffer());
+      return launch_status("reduce_mask(ranges)");
     }
   }
   // chunk of block columns whose column range fits the column-sum buffer

@@ -867,3 +867,28 @@ def test_sparse_conv_resident_pair_modes(cuda_device, n, density):
     geo = O.geometry(h, w, (3, 3), (1, 1), True, (16, 16))
     reg = O.active_region(geo, O.reduce_mask(m.numpy(), geo), n)
     assert np.all(y[~reg] == 0)
+
+
+@pytest.mark.parametrize("pool,thr", [("max", None), ("avg", 0.3)])
+def test_reduce_mask_ranges_kernel_vs_oracle(cuda_device, pool, thr):
+    """Large batches (64 frames of 400x400, 16x16 unit windows: 1856 block rows) run the
+    ranges kernel (several block rows per CTA, whole-CTA look-back); MAX and AVG pooling,
+    vectorised column sums: bit-exact against the oracle and against the one-row-per-CTA
+    kernel (SBN_DEBUG_ROW_REDUCE_MASK), call after call."""
+    lib = _lib.load()
+    m = P.synth_mask_blobs((64, 400, 400), 0.8, 3)
+    spec = P.unit_spec((64, 400, 400, 8), (16, 16))
+    pm = P.PoolMode.MAX if pool == "max" else P.PoolMode.AVG
+    mk = m.cuda()
+    got = [P.reduce_mask(mk, spec, pm, thr).entries for _ in range(3)]
+    old = lib.sbn_debug_set_flags(8192)
+    try:
+        row = P.reduce_mask(mk, spec, pm, thr).entries
+    finally:
+        lib.sbn_debug_set_flags(old)
+    geo = O.geometry(400, 400, (3, 3), (1, 1), True, (16, 16))
+    ref = O.reduce_mask(m.numpy(), geo, pool, thr)
+    assert len(ref) > 0
+    for g in got:
+        assert np.array_equal(g, ref)
+    assert np.array_equal(row, ref)

@@ -28,6 +28,10 @@ idx = P.reduce_mask(mk, spec)
 P.gather(P.Tensor4D(x32), idx, spec)
 spec1 = P.compute_block_spec((n, h, w, 16), P.ConvParams((1, 1), (1, 1), P.Padding.VALID, 16), (8, 8))
 idx1 = P.reduce_mask(mk, spec1)
+# many block rows: the ranges kernel (several rows per CTA, whole-CTA look-back), vec and not
+for (nb, hb, wb) in ((96, 64, 64), (64, 40, 30)):
+    mkb = P.synth_mask_blobs((nb, hb, wb), 0.7, 2).cuda()
+    P.reduce_mask(mkb, P.compute_block_spec((nb, hb, wb, 8), P.ConvParams((1, 1), (1, 1), P.Padding.VALID, 8), (4, 4)))
 g1 = P.gather(P.Tensor4D(x32), idx1, spec1)
 P.scatter(g1, spec1, P.Tensor4D(torch.zeros_like(x32)))
 P.scatter_add(g1, spec1, P.Tensor4D(torch.zeros_like(x32)))
