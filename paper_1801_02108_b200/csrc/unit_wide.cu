@@ -783,6 +783,9 @@ constexpr int kFPA2 = kFR2 * 16;         // A2 plane stride
 constexpr int kFPA3 = 256 * 16;          // A3 plane stride (rows q = oy*16 + ox of both tiles)
 constexpr int kFBudget = 232448 - 1024;  // opt-in dynamic smem minus the static barriers
 
+#ifndef SBN_FUSED_SA_MAX
+#define SBN_FUSED_SA_MAX 4
+#endif
 template <int C, int M>
 struct FCfg {
   using Q1 = WCfg<C, M, kIn>;
@@ -807,7 +810,7 @@ struct FCfg {
   static constexpr int TSB = NKC1 * ACH;
   static constexpr long FIX = 2L * A2B + A3B + W1B + W2B + W3B + PARB;
   static constexpr int SAF = (int)((kFBudget - FIX) / TSB);
-  static constexpr int SA = SAF > 4 ? 4 : SAF;  // <= two blocks of tiles
+  static constexpr int SA = SAF > SBN_FUSED_SA_MAX ? SBN_FUSED_SA_MAX : SAF;  // window ring depth (tiles)
   // TMEM: NB1 GEMM1 tile accumulators (M columns each), two GEMM2 block accumulators (2M),
   // one GEMM3 block accumulator (2C)
   static constexpr int NB1R = (512 - 4 * M - 2 * C) / M;
