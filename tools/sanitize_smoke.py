@@ -40,7 +40,7 @@ P.scatter_transpose(gt, spec1, P.Tensor4D(torch.zeros_like(x32)))
 # sparse convs
 f32 = P.FilterBank(torch.randn(3, 3, 16, 16) * 0.1, torch.randn(16))
 P.sparse_conv2d(P.Tensor4D(x32), mk, f32, p3, (16, 16))
-for c, blk_, flags in ((128, 16, 0), (128, 16, 32), (64, 8, 0)):
+for c, blk_, flags in ((128, 16, 0), (128, 16, 2048), (128, 16, 32), (64, 8, 0)):  # 0: resident pair, 2048: single-CTA
     x = torch.randn(n, h, w, c, device=dev).bfloat16()
     fb = P.FilterBank((torch.randn(3, 3, c, c) / (3 * c ** 0.5)).bfloat16(), torch.randn(c).bfloat16())
     pc = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, c)
@@ -89,8 +89,11 @@ xs1 = torch.randn(1, 64, 64, 16, device=dev)
 P.sparse_conv2d(P.Tensor4D(xs1), P.synth_mask_blobs((1, 64, 64), 0.5, 3).cuda(), f32, p3, (16, 16))
 xt3 = torch.randn(1, 180, 200, 128, device=dev).bfloat16()  # 195 blocks on 148 CTAs: 47 split
 ft3 = P.FilterBank((torch.randn(3, 3, 128, 128) / 34).bfloat16(), torch.randn(128).bfloat16())
-P.sparse_conv2d(P.Tensor4D(xt3), P.synth_mask_topleft((1, 180, 200), 0.0).cuda(), ft3,
-                P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 128), (16, 16), pool=P.PoolMode.MAX, threshold=1 / 256)
+for flags in (0, 2048):  # list mode: resident pair (5 pair rounds) / single-CTA with split tail jobs
+    old = lib.sbn_debug_set_flags(flags)
+    P.sparse_conv2d(P.Tensor4D(xt3), P.synth_mask_topleft((1, 180, 200), 0.0).cuda(), ft3,
+                    P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 128), (16, 16), pool=P.PoolMode.MAX, threshold=1 / 256)
+    lib.sbn_debug_set_flags(old)
 bb = P.build_backbone([P.StageConfig(1, (8, 12, 24), (16, 16), 1, 1), P.StageConfig(1, (24, 24, 48), (12, 12), 2, 2)],
                       np.random.default_rng(1))
 P.run_backbone(bb, P.Tensor4D(torch.randn(1, 60, 52, 8, device=dev)), P.synth_mask_blobs((1, 60, 52), 0.7, 2).cuda())
