@@ -961,10 +961,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
   tc::cluster_sync();  // both CTAs' barriers exist before any remote arrive / multicast commit
   tc::fence_after();
   const uint32_t tmem = tslot;
-  tc::pdl_wait();
-  if (tl && tid == 0) tl[1] = gtimer();
   // weight loader: my half of all 9 taps, once, chunk-major (the issuer starts on chunk 0
-  // while the rest lands; mask-fused, the copies overlap the mask test and list exchange).
+  // while the rest lands).  Issued before griddepcontrol.wait: the packed image does not
+  // depend on the previous kernel (a reduce_mask launch triggers its dependents at entry, so
+  // these copies overlap it), and mask-fused they also overlap the mask test.
   auto load_weights = [&]() {
     if (tid != 8 * 32) return;
     for (int c = 0; c < P::NCH; ++c) {
@@ -977,8 +977,10 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
       }
     }
   };
-  const bool global = a.mask != nullptr;
   load_weights();
+  tc::pdl_wait();
+  if (tl && tid == 0) tl[1] = gtimer();
+  const bool global = a.mask != nullptr;
   const int B = global ? conv_mask_global<kPairThreads, BS>(a, s_idx) : ld_count(a.count, a.cap);
   const int nmine = B > pair ? (B - pair + npairs - 1) / npairs : 0;  // my pair's blocks
   // block k of my pair -> (frame, block row, block column)
@@ -1240,7 +1242,13 @@ int sparse_conv_tc_masked(const void* x, const uint8_t* mask, int cin, int cout,
   ConvArgs a;
   memset(&a, 0, sizeof(a));
   if (!(debug_flags() & (kDebugConvNoRes | kDebugNoGlobalList)) && slotw && gidx && g.bh == 16 && cin == 128 && cout == 128) {
-    // resident-weight CTA pair with the one-launch global list
+    // Resident-weight CTA pair.  Default: reduce_mask (which triggers its PDL dependents at
+    // entry) + the pair's list mode, whose prologue and 147 KB weight copies then overlap
+    // the mask reduction — measured faster than the one-launch global list at every density
+    // (config 3: 30.7 vs 31.5 us at 10 %, 200 vs 206 us at 100 %; tools/conv_res_ab.py).
+    if (!(debug_flags() & kDebugConvResOneLaunch) && pair_res_max_pairs<128, 128, 16>() > 0)
+      return SBN_ERR_UNSUPPORTED;
+    // one launch: the mask test and the global list inside the pair kernel
     a.x = (const __nv_bfloat16*)x;
     a.out = (__nv_bfloat16*)dst;
     a.g = g;

@@ -51,6 +51,9 @@ __device__ __forceinline__ int block_sum(int v, int* red) {
 __global__ void __launch_bounds__(kMaskThreads)
 reduce_mask_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int chunk,
                    int32_t* __restrict__ idx, int32_t* __restrict__ count, MaskWs* ws, int tiles) {
+  // dependents launched with PDL (the conv / unit kernels) may start their prologues and
+  // weight copies now; they read the list only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ int colsum[kColBuf];
   __shared__ int red[kMaskThreads / 32];
   __shared__ int woff[kMaskThreads / 32];
@@ -216,6 +219,7 @@ constexpr int kClusterThreads = 256;
 __global__ void __launch_bounds__(kClusterThreads, 1)
 reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int per,
                            int32_t* __restrict__ idx, int32_t* __restrict__ count, int vec) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (see reduce_mask_kernel)
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int s_cnt[kClusterMax];
   __shared__ int wsum[kClusterThreads / 32];
@@ -350,6 +354,7 @@ __global__ void __launch_bounds__(kRangeThreads)
 reduce_mask_ranges_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int per,
                           int32_t* __restrict__ idx, int32_t* __restrict__ count, MaskWs* ws, int ranges,
                           int vec, unsigned long long* tr) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (see reduce_mask_kernel)
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int wsum[kRangeThreads / 32];
   __shared__ unsigned int s_range;

@@ -821,8 +821,9 @@ def test_bf16_scatter_add_vs_oracle(cuda_device):
 
 @pytest.mark.parametrize("n,density", [(3, 0.05), (2, 0.5), (1, 1.0), (2, 0.0)])
 def test_sparse_conv_resident_pair_modes(cuda_device, n, density):
-    """Resident-weight CTA-pair conv (16x16 blocks, 128 -> 128): list mode (reduce_mask list)
-    and the mask-fused global list give the same output bit for bit, call after call and
+    """Resident-weight CTA-pair conv (16x16 blocks, 128 -> 128): list mode (reduce_mask list,
+    the default from the mask) and the one-launch mask-fused global list give the same output
+    bit for bit, call after call and
     interleaved with the single-CTA kernel on the same sync workspace; against the
     double-buffered kernel (another fp32 accumulation order, bf16 outputs) within 2^-7 of the
     largest output; against
@@ -843,7 +844,9 @@ def test_sparse_conv_resident_pair_modes(cuda_device, n, density):
     idx = P.reduce_mask(mk, spec)
     res = []
     for _ in range(2):
-        for flags in (0, NO_RESIDENT):
+        # 0: reduce_mask + the pair's list mode; 16384: one launch (mask test + global list in
+        # the pair kernel); NO_RESIDENT: the single-CTA double-buffered kernel
+        for flags in (0, 16384, NO_RESIDENT):
             old = lib.sbn_debug_set_flags(flags)
             try:
                 a = torch.zeros_like(xd)
@@ -855,8 +858,8 @@ def test_sparse_conv_resident_pair_modes(cuda_device, n, density):
                 lib.sbn_debug_set_flags(old)
             assert torch.equal(a, b)
             res.append(a)
-    assert torch.equal(res[0], res[2]) and torch.equal(res[1], res[3])
-    y, y_db = _np(res[0]), _np(res[1])
+    assert torch.equal(res[0], res[1]) and torch.equal(res[0], res[3]) and torch.equal(res[2], res[5])
+    y, y_db = _np(res[0]), _np(res[2])
     if idx.count == 0:
         assert not y.any()
         return

@@ -23,7 +23,7 @@ for d in (0.3, 1.0, 0.0):
     mk = (P.synth_mask_blobs((n, h, w), 1.0 - d, 4) if d < 1 else P.BinaryMask.full(n, h, w)).cuda()
     idx = P.reduce_mask(mk, spec)
     outs = []
-    for fl in (2048, 0):
+    for fl in (2048, 16384):  # single-CTA / resident pair with the one-launch global list
         old = lib.sbn_debug_set_flags(fl)
         o = torch.zeros_like(x)
         sparse_conv_into(x, o, fb, p, spec, idx)

@@ -40,7 +40,7 @@ P.scatter_transpose(gt, spec1, P.Tensor4D(torch.zeros_like(x32)))
 # sparse convs
 f32 = P.FilterBank(torch.randn(3, 3, 16, 16) * 0.1, torch.randn(16))
 P.sparse_conv2d(P.Tensor4D(x32), mk, f32, p3, (16, 16))
-for c, blk_, flags in ((128, 16, 0), (128, 16, 2048), (128, 16, 32), (64, 8, 0)):  # 0: resident pair, 2048: single-CTA
+for c, blk_, flags in ((128, 16, 0), (128, 16, 16384), (128, 16, 2048), (128, 16, 32), (64, 8, 0)):  # resident pair (two launches / one), single-CTA, streamed pair
     x = torch.randn(n, h, w, c, device=dev).bfloat16()
     fb = P.FilterBank((torch.randn(3, 3, c, c) / (3 * c ** 0.5)).bfloat16(), torch.randn(c).bfloat16())
     pc = P.ConvParams((3, 3), (1, 1), P.Padding.SAME, c)
