@@ -125,7 +125,8 @@ enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4, kDebug
        kDebugWideUnfused = 256, kDebugDenseSingle = 512, kDebugWideNoSplit = 1024, kDebugConvNoRes = 2048,
        kDebugNoEarlyMask = 4096,
        kDebugRowReduceMask = 8192,
-       kDebugConvResOneLaunch = 16384 };
+       kDebugConvResOneLaunch = 16384,
+       kDebugNoMaskPdl = 32768 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

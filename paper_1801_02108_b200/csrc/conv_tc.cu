@@ -664,6 +664,7 @@ struct __align__(64) PairConvArgs {
   CUtensorMap wmap;  // pair copy of the packed weights as 128-byte rows, box = one tap half
   ConvArgs c;
   unsigned long long* trace;  // diagnostics: per-CTA issuer wait totals (sbn_debug_set_trace)
+  int early_trigger;          // resident pair kernel: griddepcontrol.launch_dependents after the prologue
 };
 
 template <int CIN, int COUT, int BS>
@@ -978,6 +979,7 @@ __global__ void __launch_bounds__(kPairThreads, 1) conv_tc_pair_res_kernel(const
     }
   };
   load_weights();
+  if (pa.early_trigger) tc::pdl_trigger();  // the next launch (e.g. reduce_mask) may start
   tc::pdl_wait();
   if (tl && tid == 0) tl[1] = gtimer();
   const bool global = a.mask != nullptr;
@@ -1162,6 +1164,7 @@ int launch_conv_pair_res(const ConvArgs& c, int cap, cudaStream_t s) {
   memset(&pa, 0, sizeof(pa));
   pa.c = c;
   pa.trace = trace_buffer();
+  pa.early_trigger = !(debug_flags() & kDebugNoMaskPdl);
   const Geo& g = c.g;
   const uint64_t dims[5] = {8, (uint64_t)g.w, (uint64_t)g.h, (uint64_t)(CIN / 8), (uint64_t)g.n};
   const uint64_t str[4] = {(uint64_t)CIN * 2, (uint64_t)g.w * CIN * 2, 16, (uint64_t)g.h * g.w * CIN * 2};

@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
 reduce_mask_cluster_kernel(const uint8_t* __restrict__ mask, Geo g, int pool, double thr, int per,
                            int32_t* __restrict__ idx, int32_t* __restrict__ count, int vec) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (see reduce_mask_kernel)
+  // launched with PDL itself (under the previous kernel's tail): the mask may be that
+  // kernel's output
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int s_cnt[kClusterMax];
   __shared__ int wsum[kClusterThreads / 32];
@@ -627,13 +630,15 @@ extern "C" int sbn_reduce_mask(const uint8_t* mask, const sbn_geometry* gp, int 
       cfg.blockDim = dim3(kClusterThreads);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = cl;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
-      cfg.numAttrs = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = (debug_flags() & kDebugNoMaskPdl) ? 0 : 1;
+      cfg.numAttrs = 2;
       if (cudaLaunchKernelEx(&cfg, reduce_mask_cluster_kernel, mask, g, pool, threshold, per, idx,
                              count, vec) == cudaSuccess)
         return launch_status("reduce_mask(cluster)");
