@@ -66,6 +66,7 @@ struct ConvArgs {
   const uint8_t* mask;
   unsigned* sw;    // global list: [0] launch epoch, [4 + 4 * (tag & 1) + {0 claimed, 1 done}]
   int32_t* gidx;   // global list rows (cap x 3)
+  int early_trigger;  // double-buffered kernel: griddepcontrol.launch_dependents after the prologue
 };
 
 // Mask reduction fused in front of the conv (reference `tiling.py:138-160`, MAX pool),
@@ -401,6 +402,7 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tslot;
+  if (a.early_trigger) tc::pdl_trigger();  // the next launch may start its prologue
   tc::pdl_wait();
   __shared__ int32_t s_idx[3 * kMaxLocal];  // mask-fused mode: this CTA's own block list
   const bool global = a.mask != nullptr && a.gidx != nullptr;  // mask-fused, one global list
@@ -596,8 +598,10 @@ __global__ void __launch_bounds__(kDbThreads, 1) conv_tc_db_kernel(ConvArgs a) {
 }
 
 template <int CIN, int COUT, int BS>
-int launch_conv_db(const ConvArgs& a, int cap, cudaStream_t s) {
+int launch_conv_db(const ConvArgs& a_in, int cap, cudaStream_t s) {
   using D = DbCfg<CIN, COUT, BS>;
+  ConvArgs a = a_in;
+  a.early_trigger = !(debug_flags() & kDebugNoMaskPdl);
   auto kern = conv_tc_db_kernel<CIN, COUT, BS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, D::SMEM);
   cudaLaunchConfig_t cfg = {};
