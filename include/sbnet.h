@@ -270,11 +270,14 @@ int sbn_debug_set_trace(unsigned long long* buf);
  * as ONE launch (mask test + global list inside the conv) instead of reduce_mask + the
  * pair's list mode.
  * SBN_DEBUG_NO_MASK_PDL: launch the cluster reduce_mask without programmatic dependent
- * launch and keep the resident pair conv from triggering its dependents early. */
+ * launch and keep the resident pair conv from triggering its dependents early.
+ * SBN_DEBUG_TMA_GLOBAL_LIST: sparse_conv2d from the mask on the tap-GEMM conv as one launch
+ * with a global block list for any window size (default: windows of 128..512 pixels). */
 enum { SBN_DEBUG_NO_PAIR = 1, SBN_DEBUG_CONV_SINGLE_BUFFER = 2, SBN_DEBUG_FORCE_WIDE = 4, SBN_DEBUG_FORCE_FUSED = 8,
        SBN_DEBUG_CONV_TMA = 16, SBN_DEBUG_CONV_PAIR = 32, SBN_DEBUG_CONV_NO_RESIDENT = 2048,
        SBN_DEBUG_NO_EARLY_MASK = 4096, SBN_DEBUG_ROW_REDUCE_MASK = 8192,
-       SBN_DEBUG_CONV_RES_ONE_LAUNCH = 16384, SBN_DEBUG_NO_MASK_PDL = 32768 };
+       SBN_DEBUG_CONV_RES_ONE_LAUNCH = 16384, SBN_DEBUG_NO_MASK_PDL = 32768,
+       SBN_DEBUG_TMA_GLOBAL_LIST = 65536 };
 int sbn_debug_set_flags(int flags);
 /* Diagnostics: occupancy the last tcgen05 unit launch computed (0: CTAs/SM of the
  * single-CTA kernel, 1: co-resident clusters of the CTA-pair kernel). */

@@ -126,7 +126,8 @@ enum { kDebugNoPair = 1, kDebugConvSingleBuffer = 2, kDebugForceWide = 4, kDebug
        kDebugNoEarlyMask = 4096,
        kDebugRowReduceMask = 8192,
        kDebugConvResOneLaunch = 16384,
-       kDebugNoMaskPdl = 32768 };
+       kDebugNoMaskPdl = 32768,
+       kDebugTmaGlobalList = 65536 };
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

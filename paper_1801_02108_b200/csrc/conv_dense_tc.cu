@@ -131,9 +131,16 @@ struct __align__(64) CArgs {
   const uint8_t* mask;
   int gy, gx, wbh, wbw;   // candidate grid and window (= block) size
   int n_h, n_w;           // input (= mask) height / width
+  // mask-fused GLOBAL-list mode (mask and gidx set, list-mode kernel): every CTA tests its
+  // candidates (c, c + G, ...), publishes the active ones into gidx, and after all G CTAs have
+  // published the CTAs stride through the list as in list mode — one launch for grids too
+  // big for the local lists.  sw: [0] launch epoch, [4 + 4 * (tag & 1) + {0 claimed, 1 done}]
+  unsigned* sw;
+  int32_t* gidx;
 };
 
 constexpr int kMaxLocalTma = 4;
+constexpr int kMaxGlobTma = 64;  // candidates per CTA in the global-list mode
 #ifndef SBN_FUSED_UNITS_PER_CTA
 #define SBN_FUSED_UNITS_PER_CTA 4  // mask-fused mode only while every CTA owns <= this many units (2 vs 4: conv-3 block 16 12.3 vs 8.7 us)
 #endif
@@ -146,7 +153,7 @@ __device__ __forceinline__ void conv_tile(const CArgs& a, const int32_t* lidx, i
                                           int& iy0, int& ix0, int& ly, int& lx) {
   ly = a.th;
   lx = a.tw;
-  if (LOCAL || a.idx) {
+  if (LOCAL || a.idx || a.gidx) {
     int by, bx, sub;
     if constexpr (LOCAL) {  // this CTA's local list in shared memory: (n, by, bx, sub) per unit
       n = lidx[4 * tile];
@@ -157,9 +164,15 @@ __device__ __forceinline__ void conv_tile(const CArgs& a, const int32_t* lidx, i
       const int subs = a.subs_y * a.subs_x;
       const int j = tile / subs;
       sub = tile - j * subs;
-      n = __ldg(a.idx + 3 * j);
-      by = __ldg(a.idx + 3 * j + 1);
-      bx = __ldg(a.idx + 3 * j + 2);
+      if (a.gidx) {  // written in this launch: coherent loads
+        n = a.gidx[3 * j];
+        by = a.gidx[3 * j + 1];
+        bx = a.gidx[3 * j + 2];
+      } else {
+        n = __ldg(a.idx + 3 * j);
+        by = __ldg(a.idx + 3 * j + 1);
+        bx = __ldg(a.idx + 3 * j + 2);
+      }
     }
     const int ty = sub / a.subs_x, tx = sub - ty * a.subs_x;
     oy0 = by * a.obh + ty * a.th;
@@ -254,8 +267,79 @@ __global__ void __launch_bounds__(kCThreads, CCfg<CIN, COUT, KS>::CPS) conv_dens
     }
     __syncthreads();
   }
+  if constexpr (!LOCAL) {
+    if (a.gidx) {  // mask-fused global list (reference tiling.py:138-160, MAX pool)
+      __shared__ uint8_t s_flag[kMaxGlobTma];
+      __shared__ int s_base;
+      __shared__ unsigned s_tag;
+      const int T = a.n * a.gy * a.gx, G = gridDim.x, gyx = a.gy * a.gx, area = a.wbh * a.wbw;
+      const int nc = T > (int)blockIdx.x ? min((T - (int)blockIdx.x + G - 1) / G, kMaxGlobTma) : 0;
+      if (tid == 0) s_tag = *reinterpret_cast<volatile unsigned*>(a.sw) + 1u;
+      constexpr int NW = kCThreads / 32;
+      for (int j = warp; j < nc; j += NW) {  // one warp per candidate, all its loads in flight
+        const int cand = (int)blockIdx.x + j * G;
+        const int fr = cand / gyx, rr = cand - fr * gyx, by = rr / a.gx, bx = rr - by * a.gx;
+        const int y0 = a.goy + by * a.gsy, x0 = a.gox + bx * a.gsx;
+        uint32_t v = 0;
+#pragma unroll 8
+        for (int p = lane; p < area; p += 32) {
+          const int y = y0 + p / a.wbw, xx = x0 + p % a.wbw;
+          const bool ok = y >= 0 && y < a.n_h && xx >= 0 && xx < a.n_w;
+          v |= tc::ld_u8_pred(a.mask + ((size_t)fr * a.n_h + (ok ? y : 0)) * a.n_w + (ok ? xx : 0), ok);
+        }
+        const bool any = __any_sync(0xffffffffu, v != 0);
+        if (lane == 0) s_flag[j] = any;
+      }
+      __syncthreads();
+      const unsigned tag = s_tag;
+      unsigned* ring = a.sw + 4 + 4 * (tag & 1u);
+      if (warp == 0) {  // compact this CTA's active candidates, claim slots, publish rows
+        int nl = 0;
+        for (int c0 = 0; c0 < nc; c0 += 32) nl += __popc(__ballot_sync(0xffffffffu, c0 + lane < nc && s_flag[c0 + lane]));
+        int base = 0;
+        if (lane == 0 && nl) base = (int)atomicAdd(ring, (unsigned)nl);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int c0 = 0; c0 < nc; c0 += 32) {
+          const bool on = c0 + lane < nc && s_flag[c0 + lane];
+          const unsigned bal = __ballot_sync(0xffffffffu, on);
+          if (on) {
+            const int q = base + __popc(bal & ((1u << lane) - 1u));
+            const int cand = (int)blockIdx.x + (c0 + lane) * G;
+            const int fr = cand / gyx, rr = cand - fr * gyx;
+            a.gidx[3 * q] = fr;
+            a.gidx[3 * q + 1] = rr / a.gx;
+            a.gidx[3 * q + 2] = rr % a.gx;
+          }
+          base += __popc(bal);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        unsigned old;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(ring + 1) : "memory");
+        if (old == gridDim.x - 1) {  // last to publish: recycle the other slot, advance the epoch
+          unsigned* other = a.sw + 4 + 4 * ((tag + 1u) & 1u);
+          other[0] = 0u;
+          other[1] = 0u;
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.sw), "r"(tag) : "memory");
+        }
+        SpinGuard sg;
+        unsigned d;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(ring + 1) : "memory");
+          if (d == gridDim.x) break;
+          __nanosleep(32);
+          sg.tick(kSpinSlotDone);
+        }
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(d) : "l"(ring) : "memory");
+        s_nloc = (int)d;
+      }
+      __syncthreads();
+    }
+  }
   const int32_t* lidx = s_idx;  // read only in LOCAL mode
   const int ntiles = LOCAL ? s_nloc
+                           : a.gidx ? s_nloc * a.subs_y * a.subs_x
                            : a.idx ? ld_count(a.count, a.cap) * a.subs_y * a.subs_x : a.n * a.tiles_y * a.tiles_x;
 
   if (warp < kLWarp) {
@@ -737,7 +821,8 @@ template <int CIN, int COUT, int KS>
 int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int px, int oh, int ow,
                  const void* wpk, const float* bias, void* out, cudaStream_t s,
                  const Geo* sparse = nullptr, const int32_t* idx = nullptr, const int32_t* count = nullptr,
-                 int cap = 0, const __nv_bfloat16* bias_bf16 = nullptr, const uint8_t* mask = nullptr) {
+                 int cap = 0, const __nv_bfloat16* bias_bf16 = nullptr, const uint8_t* mask = nullptr,
+                 unsigned* slotw = nullptr, int32_t* gidx = nullptr) {
   using Q = CCfg<CIN, COUT, KS>;
   CArgs a;
   memset(&a, 0, sizeof(a));
@@ -789,14 +874,24 @@ int launch_dense(const void* x, int n, int h, int w, int sy, int sx, int py, int
       a.n_h = h;
       a.n_w = w;
       tiles = (long)sparse->n * sparse->gy * sparse->gx * subs_y * subs_x;  // (candidate, sub-tile) units
-      if (tiles > (long)kMaxLocalTma * Q::CPS * sm_count()) {
+      if (gidx) {  // global-list mode: every co-resident CTA tests candidates and strides the list
+        const long slots = (long)Q::CPS * sm_count();
+        const long cands = (long)sparse->n * sparse->gy * sparse->gx;
+        if ((cands + slots - 1) / slots > kMaxGlobTma) {
+          set_error("mask-fused tap-GEMM conv: %ld candidates exceed %d per CTA", cands, kMaxGlobTma);
+          return SBN_ERR_UNSUPPORTED;
+        }
+        a.gidx = gidx;
+        a.sw = slotw;
+        tiles = slots;
+      } else if (tiles > (long)kMaxLocalTma * Q::CPS * sm_count()) {
         set_error("mask-fused tap-GEMM conv: %ld units exceed %d per CTA", tiles, kMaxLocalTma);
         return SBN_ERR_UNSUPPORTED;
       }
     }
   }
   if (!sparse && PCfg<CIN, COUT, KS>::USE && !(debug_flags() & kDebugDenseSingle)) return launch_dense_pair<CIN, COUT, KS>(a, s);
-  auto kern = mask ? conv_dense_kernel<CIN, COUT, KS, true> : conv_dense_kernel<CIN, COUT, KS, false>;
+  auto kern = mask && !gidx ? conv_dense_kernel<CIN, COUT, KS, true> : conv_dense_kernel<CIN, COUT, KS, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
   cudaLaunchConfig_t cfg = {};
   const long slots = (long)Q::CPS * sm_count();
@@ -881,16 +976,27 @@ int sparse_conv_tma(const void* x, int cin, int cout, int k, int sh, int sw, con
 // are then as balanced as a striped global list); SBN_ERR_UNSUPPORTED above that, and the
 // caller reduces the mask separately.
 int sparse_conv_tma_masked(const void* x, const uint8_t* mask, int cin, int cout, int k, int sh, int sw,
-                           const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s) {
+                           const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s,
+                           unsigned* slotw, int32_t* gidx) {
   int th = 0, tw = 0, subs_y = 1, subs_x = 1;
   if (!sparse_tile_shape(g.obh, g.obw, sh, sw, th, tw, subs_y, subs_x)) return SBN_ERR_UNSUPPORTED;
   const long units = (long)g.n * g.gy * g.gx * subs_y * subs_x;
+  // local lists while every CTA slot owns few units; otherwise the global list (when the
+  // caller passed its sync words and list buffer); otherwise the caller reduces the mask
+  // (default for windows of 128..512 pixels, where one warp's test of a candidate is one
+  // round of loads and the conv is short: Table-1 conv-2 with 16x16 blocks 13.1 -> 12.1 us;
+  // 8x8 and 32x32 windows measured as fast or faster with reduce_mask + the list launch;
+  // SBN_DEBUG_TMA_GLOBAL_LIST forces it for any window)
+  const int area = g.bh * g.bw;
+  const bool glob_ok = slotw && gidx && ((debug_flags() & kDebugTmaGlobalList) || (area >= 128 && area <= 512));
 #define X(CI, CO, KS)                                                                                            \
-  if (cin == CI && cout == CO && k == KS)                                                                        \
-    return units > (long)SBN_FUSED_UNITS_PER_CTA * CCfg<CI, CO, KS>::CPS * sm_count()                          \
-               ? SBN_ERR_UNSUPPORTED                                                                             \
-               : launch_dense<CI, CO, KS>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, nullptr, \
-                                    nullptr, g.n * g.gy * g.gx, (const __nv_bfloat16*)bias, mask);
+  if (cin == CI && cout == CO && k == KS) {                                                                      \
+    const bool local = units <= (long)SBN_FUSED_UNITS_PER_CTA * CCfg<CI, CO, KS>::CPS * sm_count();           \
+    if (!local && !glob_ok) return SBN_ERR_UNSUPPORTED;                                                        \
+    return launch_dense<CI, CO, KS>(x, g.n, g.h, g.w, sh, sw, 0, 0, g.oh, g.ow, wpk, nullptr, dst, s, &g, nullptr, \
+                                    nullptr, g.n * g.gy * g.gx, (const __nv_bfloat16*)bias, mask,              \
+                                    local ? nullptr : slotw, local ? nullptr : gidx);                          \
+  }
   SBN_DENSE_CONV_CONFIGS(X)
 #undef X
   return SBN_ERR_UNSUPPORTED;

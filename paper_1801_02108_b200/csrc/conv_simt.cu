@@ -161,7 +161,8 @@ int sparse_conv_tma(const void* x, int cin, int cout, int k, int sh, int sw, con
 bool sparse_conv_tc_supported(int dtype, int cin, int cout, int kh, int kw, int sh, int sw,
                               const Geo& g);
 int sparse_conv_tma_masked(const void* x, const uint8_t* mask, int cin, int cout, int k, int sh, int sw,
-                           const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s);
+                           const Geo& g, const void* wpk, const void* bias, void* dst, cudaStream_t s,
+                           unsigned* slotw, int32_t* gidx);
 
 }  // namespace sbn
 
@@ -307,14 +308,14 @@ extern "C" int sbn_sparse_conv_masked(const void* x, const uint8_t* mask, int dt
   }
   // (a global list in this launch, as for the kernel above, measured slower here than
   // reduce_mask + conv: config 3, 32x32 blocks, 26.1 vs 23.4 us at 5 %, 90 vs 82 at 30 %)
-  if (kind == 2 && algo != SBN_ALGO_SIMT && (long)cap <= 8L * sm_count()) {  // small grids: one launch
+  if (kind == 2 && algo != SBN_ALGO_SIMT && (long)cap <= 64L * sm_count()) {  // one launch (local or global list)
     const void* wpk = w_packed;
     if (!wpk) {
       st = sparse_conv_tma_pack(w, cin, cout, kh, pk, s);
       if (st) return st;
       wpk = pk;
     }
-    st = sparse_conv_tma_masked(x, mask, cin, cout, kh, sh, sw, g, wpk, bias, dst, s);
+    st = sparse_conv_tma_masked(x, mask, cin, cout, kh, sh, sw, g, wpk, bias, dst, s, (unsigned*)sync_ws, idx);
     if (st != SBN_ERR_UNSUPPORTED) return st;
   }
   st = sbn_reduce_mask(mask, gp, SBN_POOL_MAX, 1.0 / ((double)gp->bh * gp->bw), idx, count, rmws, rmb, stream);

@@ -895,3 +895,31 @@ def test_reduce_mask_ranges_kernel_vs_oracle(cuda_device, pool, thr):
     for g in got:
         assert np.array_equal(g, ref)
     assert np.array_equal(row, ref)
+
+
+@pytest.mark.parametrize("h,w,c,block,density", [(400, 704, 24, 32, 0.1), (200, 352, 48, 8, 0.2), (130, 150, 64, 17, 0.5)])
+def test_tap_gemm_global_list_mode_bit_identical(cuda_device, h, w, c, block, density):
+    """The tap-GEMM conv's one-launch global-list mode (every CTA tests its candidates,
+    publishes them, then all stride the list; SBN_DEBUG 65536) computes exactly what
+    reduce_mask + the list-mode launch computes (per-tile math identical), call after call."""
+    from paper_1801_02108_b200.layers import sparse_conv_algo, sparse_conv_into, sparse_conv_masked_into
+    lib = _lib.load()
+    rng = np.random.default_rng(h + c)
+    x = torch.from_numpy(rng.standard_normal((1, h, w, c)).astype(np.float32)).bfloat16().cuda()
+    fb = P.FilterBank(torch.from_numpy((rng.standard_normal((3, 3, c, c)) / np.sqrt(9 * c)).astype(np.float32)).bfloat16(),
+                      torch.from_numpy(rng.standard_normal(c).astype(np.float32)).bfloat16())
+    p = _conv((3, 3), (1, 1), True, c)
+    spec = P.compute_block_spec((1, h, w, c), p, (block, block))
+    mk = P.synth_mask_topleft((1, h, w), 1.0 - density).cuda()
+    idx = P.reduce_mask(mk, spec)
+    ref = torch.zeros_like(x)
+    sparse_conv_into(x, ref, fb, p, spec, idx)
+    old = lib.sbn_debug_set_flags(65536)
+    try:
+        for _ in range(3):
+            o = torch.zeros_like(x)
+            sparse_conv_masked_into(x, o, mk.data, fb, p, spec)
+            torch.cuda.synchronize()
+            assert torch.equal(o, ref)
+    finally:
+        lib.sbn_debug_set_flags(old)

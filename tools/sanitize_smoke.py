@@ -94,6 +94,14 @@ for flags in (0, 2048):  # list mode: resident pair (5 pair rounds) / single-CTA
     P.sparse_conv2d(P.Tensor4D(xt3), P.synth_mask_topleft((1, 180, 200), 0.0).cuda(), ft3,
                     P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 128), (16, 16), pool=P.PoolMode.MAX, threshold=1 / 256)
     lib.sbn_debug_set_flags(old)
+# tap-GEMM conv, one launch with the global block list (16x16 windows by default; forced for 32x32)
+xg2 = torch.randn(1, 120, 150, 24, device=dev).bfloat16()
+fg2 = P.FilterBank((torch.randn(3, 3, 24, 24) / 14).bfloat16(), torch.randn(24).bfloat16())
+for blk_, flags in ((16, 0), (32, 65536)):
+    old = lib.sbn_debug_set_flags(flags)
+    P.sparse_conv2d(P.Tensor4D(xg2), P.synth_mask_topleft((1, 120, 150), 0.8).cuda(), fg2,
+                    P.ConvParams((3, 3), (1, 1), P.Padding.SAME, 24), (blk_, blk_))
+    lib.sbn_debug_set_flags(old)
 bb = P.build_backbone([P.StageConfig(1, (8, 12, 24), (16, 16), 1, 1), P.StageConfig(1, (24, 24, 48), (12, 12), 2, 2)],
                       np.random.default_rng(1))
 P.run_backbone(bb, P.Tensor4D(torch.randn(1, 60, 52, 8, device=dev)), P.synth_mask_blobs((1, 60, 52), 0.7, 2).cuda())

@@ -13,6 +13,8 @@ import paper_1801_02108_b200 as P  # noqa: E402
 from paper_1801_02108_b200.layers import sparse_conv_into, sparse_conv_masked_into  # noqa: E402
 
 dev = torch.device("cuda", 0)
+from paper_1801_02108_b200 import _lib  # noqa: E402
+_lib.load().sbn_debug_set_flags(int(os.environ.get("SBN_FLAGS", 0)))  # kernel-variant A/B
 
 
 def timed(fn, reps=200):
