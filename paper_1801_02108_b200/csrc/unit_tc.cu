@@ -342,6 +342,9 @@ __device__ __forceinline__ bool slot_before_store(const TcArgs& a, unsigned tag,
   return true;
 }
 
+#ifndef SBN_ENTRY_POLL_NS
+#define SBN_ENTRY_POLL_NS 64  // back-off per entry poll: config 2 at 10 % 11.75 -> 11.56 us (tools/poll_ab.sh)
+#endif
 // Entry `blk` of this launch: returns false when the list is complete and shorter.
 __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int blk, int& n, int& by,
                                            int& bx) {
@@ -355,6 +358,9 @@ __device__ __forceinline__ bool slot_entry(const TcArgs& a, unsigned tag, int bl
     SpinGuard sg;
     while (true) {  // both words in flight per iteration: one round trip per poll
       sg.tick(kSpinSlotEntry);
+#if SBN_ENTRY_POLL_NS > 0
+      __nanosleep(SBN_ENTRY_POLL_NS);  // back off the L2 line the producers' `done` atomics hit
+#endif
       e = ld_relaxed_u64(&a.etag[blk]);
       const unsigned d = ld_relaxed_u32(ring + 1);
       if (slot_match(e, tag)) {
